@@ -1,0 +1,255 @@
+/*
+ * nat.h — C ABI of libnat: the Helmholtz boundary-integral hot path of NAT
+ * (arXiv 2506.06190) on NVIDIA B200 (sm_100a).
+ *
+ * Citations: P:n = line n of the paper's LaTeX source; readings R-* are
+ * listed in DESIGN.md §3.
+ *
+ * Conventions (every call):
+ *  - Pointers are CUDA DEVICE pointers on the current device unless marked [host].
+ *    Passing a host pointer where a device pointer is required -> NAT_ERR_INVALID_ARG.
+ *  - Every buffer is caller-owned (torch tensors, contiguous).  The library never
+ *    allocates device memory: calls that need scratch take (ws, ws_bytes) and have a
+ *    *_workspace() size query; ws must be 256-byte aligned.
+ *  - Layouts: coordinates are structure-of-arrays [3][n] float64 (x row, y row, z row);
+ *    complex values are interleaved (re, im) pairs = torch complex128 ("c128") or
+ *    complex64 ("c64").  Vectors handed to / returned by the library are c128; only
+ *    stored matrices use the precision `nat_prec` selects.
+ *  - Calls marked (async) only enqueue work on `stream`; calls marked (sync) return
+ *    host-visible results and synchronise the stream.
+ *  - Errors: negative status = no valid output, message in nat_last_error()
+ *    (thread-local, valid until the next nat_* call on that thread).  There is no CPU
+ *    fallback and no sign flipping at run time.
+ *  - Not reentrant on the same stream for the same workspace; reentrant otherwise.
+ */
+#ifndef NAT_H
+#define NAT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NAT_ABI_VERSION 1
+
+typedef struct CUstream_st* nat_stream_t; /* == cudaStream_t (torch.cuda.Stream.cuda_stream) */
+
+typedef enum {
+  NAT_OK = 0,
+  NAT_WARN_NOT_CONVERGED = 1, /* GMRES hit max_iter: best iterate written, converged = 0 */
+  NAT_ERR_INVALID_ARG = -1,   /* null/host pointer, bad size/range, k < 0 or non-finite          */
+  NAT_ERR_CUDA = -2,          /* CUDA runtime or launch error                                    */
+  NAT_ERR_NCCL = -3,          /* NCCL error                                                      */
+  NAT_ERR_SINGULAR = -4,      /* zero-area triangle, inward mesh, coincident MC samples          */
+  NAT_ERR_NUMERIC = -5,       /* NaN/Inf in a residual norm                              */
+  NAT_ERR_WORKSPACE = -6      /* ws_bytes smaller than the matching *_workspace() query          */
+} nat_status;
+
+typedef enum {
+  NAT_FP32 = 0, /* fp32 kernel arithmetic, c64 stored matrices, fp64 tile/Krylov sums (R-prec) */
+  NAT_FP64 = 1  /* fp64 arithmetic, c128 stored matrices                                      */
+} nat_prec;
+
+int nat_abi_version(void);
+const char* nat_last_error(void);
+
+/* ---------------------------------------------------------------------------------
+ * a1 — mesh preparation ("construct the scene and obtain its surface triangle
+ * mesh"; reading R-geom).  Per triangle t with vertices (v1, v2, v3):
+ *   e = (v2-v1) x (v3-v1);  area = |e|/2;  normal = e/|e|;  centroid = ((v1+v2)+v3)/3;
+ *   diam = longest edge;  area_cdf = sequential fp64 prefix sum of area (no FMA
+ *   contraction anywhere: these values decide integer results bit for bit).
+ * Host scalars: total_area = area_cdf[n-1]; center = sum A_t c_t / total_area;
+ * bound_radius = max over vertices |v - center|.
+ * Errors: NAT_ERR_SINGULAR for a zero-area triangle or signed volume <= 0.
+ * ------------------------------------------------------------------------------- */
+typedef struct {
+  int64_t n_vert, n_tri;
+  const double* vxyz; /* [3][n_vert] metres                                           */
+  const int32_t* tri; /* [3][n_tri] 0-based; CCW seen from outside => outward normals */
+} nat_mesh;
+
+typedef struct {
+  int64_t n_tri;
+  double* centroid; /* [3][n_tri] out */
+  double* normal;   /* [3][n_tri] out */
+  double* area;     /* [n_tri] out    */
+  double* diam;     /* [n_tri] out    */
+  double* area_cdf; /* [n_tri] out    */
+  double total_area, center[3], bound_radius, volume; /* [host] out */
+} nat_geom;
+
+size_t nat_mesh_prepare_workspace(int64_t n_vert, int64_t n_tri);
+nat_status nat_mesh_prepare(const nat_mesh* mesh, nat_geom* geom, void* ws, size_t ws_bytes,
+                            nat_stream_t stream); /* (sync) */
+
+/* ---------------------------------------------------------------------------------
+ * Quadrature options (reading R-colloc / R-self).  All-zero fields => defaults.
+ * ------------------------------------------------------------------------------- */
+typedef struct {
+  int far_pts;        /* 1 | 3 | 6 | 7 points on far pairs, default 3                       */
+  int near_levels_S;  /* midpoint-subdivision levels x 7-pt rule, vertex-sharing pairs, def 3 */
+  int near_levels_N;  /* same for close pairs, default 1                                     */
+  double near_eta;    /* class N: |c_i - c_j| < near_eta * diam_j, default 4                 */
+  int self_theta_pts; /* Gauss-Legendre points per edge of the polar self term, default 16   */
+} nat_quad_opts;
+
+/* ---------------------------------------------------------------------------------
+ * a2 — near list ("adjacent or identical elements"; reading R-near) for rows
+ * [row_begin, row_end).  Class 1 (S): shares a vertex index; class 2 (N): otherwise
+ * |c_i - c_j| < eta diam_j (fp64, strict).  CSR, columns ascending.
+ * nat_bem_near_count fills row_ptr[rows+1] (exclusive scan) and returns nnz; it
+ * synchronises.  nat_bem_near_build then fills col[nnz], cls[nnz] (async).
+ * ------------------------------------------------------------------------------- */
+nat_status nat_bem_near_count(const nat_mesh* mesh, const nat_geom* geom, const nat_quad_opts* opts,
+                              int64_t row_begin, int64_t row_end, int64_t* row_ptr,
+                              int64_t* nnz /* [host] */, nat_stream_t stream); /* (sync) */
+nat_status nat_bem_near_build(const nat_mesh* mesh, const nat_geom* geom, const nat_quad_opts* opts,
+                              int64_t row_begin, int64_t row_end, const int64_t* row_ptr,
+                              int32_t* col, uint8_t* cls, nat_stream_t stream); /* (async) */
+
+/* ---------------------------------------------------------------------------------
+ * a4 + a5 — dense collocation assembly of the conventional BIE (Eq. BM with beta = 0,
+ * P:174-180; readings R-sign, R-colloc, R-self) for rows [row_begin, row_end):
+ *   A[r][j] = 1/2 delta_ij - K_ij,   rhs[q][r] = - sum_j V_ij g[q][j],
+ *   K_ij = int_{T_j} dG/dn_y(c_i, y) dS,  V_ij = int_{T_j} G(c_i, y) dS,  i = row_begin + r.
+ * Far pairs use the far rule; pairs in the near list (rows of the CSR built for the
+ * same row range) and the self pair are overwritten with the near/self rules and the
+ * right-hand side is corrected in a fixed order (deterministic).
+ * A: row-major [rows][lda], c64 (NAT_FP32) or c128 (NAT_FP64).  g: c128 [n_rhs][n_tri]
+ * (may be NULL iff n_rhs == 0).  rhs: c128 [n_rhs][rows].  k >= 0 finite.
+ * ------------------------------------------------------------------------------- */
+size_t nat_bem_assemble_workspace(int64_t n_tri, int64_t rows, int n_rhs);
+nat_status nat_bem_assemble(const nat_mesh* mesh, const nat_geom* geom, const nat_quad_opts* opts,
+                            const int64_t* near_row_ptr, const int32_t* near_col,
+                            const uint8_t* near_cls, double k, nat_prec prec, int64_t row_begin,
+                            int64_t row_end, int n_rhs, const void* g, void* A, int64_t lda,
+                            void* rhs, void* ws, size_t ws_bytes, nat_stream_t stream); /* (async) */
+
+/* a6 — y = A x, A [rows][lda] in `prec`, x c128 [n], y c128 [rows]; fp64 accumulation
+ * in a fixed per-row order (independent of the number of GPUs).                       */
+nat_status nat_bem_matvec(nat_prec prec, int64_t rows, int64_t n, const void* A, int64_t lda,
+                          const void* x, void* y, nat_stream_t stream); /* (async) */
+
+/* ---------------------------------------------------------------------------------
+ * Communicator for the row-sharded solve (NCCL over NVLink / NVSwitch).  Rank 0 calls
+ * nat_comm_unique_id and broadcasts the 128 bytes (torch.distributed); every rank
+ * then calls nat_comm_create_from_id.  A NULL communicator means world size 1.
+ * ------------------------------------------------------------------------------- */
+typedef struct nat_comm nat_comm;
+nat_status nat_comm_unique_id(uint8_t* id /* [host] 128 B */);
+nat_status nat_comm_create_from_id(nat_comm** comm, const uint8_t* id /* [host] 128 B */, int rank,
+                                   int world);
+nat_status nat_comm_destroy(nat_comm* comm);
+
+/* ---------------------------------------------------------------------------------
+ * a7 — unrestarted GMRES (tol 1e-6, max 200; reading R-gmres) on the
+ * row-sharded system: this rank owns rows [row_begin, row_end) of A (A_local, b_local);
+ * each iteration = local matvec -> all-gather of the iterate (NCCL) -> replicated
+ * Arnoldi (CGS2, deterministic reductions).  x0 = 0.  x: c128 [n] out, identical on
+ * all ranks.  tol <= 0 => 1e-6, max_iter <= 0 => 200.  Returns NAT_OK or
+ * NAT_WARN_NOT_CONVERGED; info->rel_residual is the true ||b - A x|| / ||b||.
+ * ------------------------------------------------------------------------------- */
+typedef struct {
+  int iters, converged;
+  double rel_residual; /* true residual from one extra matvec            */
+  double t_total_s, t_matvec_s, t_comm_s; /* host wall times of the phases (info only) */
+} nat_solve_info;
+
+size_t nat_bem_solve_workspace(nat_prec prec, int64_t n, int64_t rows_local, int max_iter);
+nat_status nat_bem_solve(nat_comm* comm, nat_prec prec, int64_t n, int64_t row_begin, int64_t row_end,
+                         const void* A_local, int64_t lda, const void* b_local, void* x, double tol,
+                         int max_iter, void* ws, size_t ws_bytes, nat_solve_info* info /* [host] */,
+                         nat_stream_t stream); /* (sync) */
+
+/* ---------------------------------------------------------------------------------
+ * (b) Monte-Carlo BEM (Eq. BIE / SYS; disk terms P:215-236; readings
+ * R-mc-sample, R-eps, R-weight, R-disk).
+ *
+ * a8  nat_mc_sample: sample j = Philox4x32-10(ctr (j, 0, stream_lo, stream_hi),
+ *     key seed) -> triangle by area CDF (upper bound) -> uniform barycentric point;
+ *     samples [6][M] float64 = (x, y, z, nx, ny, nz) rows; sample_tri [M] int32.
+ *     Bit-identical with the oracle.  (async)
+ * a9  nat_mc_rhs: b[m][i] = -w sum_{j != i} G_m(y_i, y_j) g[m][j] - (eps/2) g[m][i].
+ * a10 nat_mc_apply: out[m][i] = 1/2 p[m][i] - w sum_{j != i} dG_m/dn_y(y_i, y_j) p[m][j].
+ *     w = (|Gamma| - pi eps^2)/(M - 1);  k [host][n_sys];  g, p, b, out c128 [n_sys][M].
+ * nat_mc_surface_pressure: a8 (or caller samples) -> a9 -> batched GMRES over a10
+ *     for all n_sys wavenumbers sharing one sample set; g_tri c128 [n_sys][n_tri].
+ *     Errors: NAT_ERR_SINGULAR on coincident samples (|y_i - y_j| < 1e-12).
+ * ------------------------------------------------------------------------------- */
+typedef struct {
+  int64_t M;
+  uint64_t seed, stream_id;
+  double eps;                 /* <= 0 => sqrt(|Gamma| / (pi M))        */
+  const double* samples_in;   /* optional [6][M] (e.g. a host Poisson-disk set) */
+  const int32_t* sample_tri_in; /* required with samples_in                     */
+} nat_mc_opts;
+
+nat_status nat_mc_sample(const nat_mesh* mesh, const nat_geom* geom, int64_t M, uint64_t seed,
+                         uint64_t stream_id, double* samples, int32_t* sample_tri,
+                         nat_stream_t stream); /* (async) */
+size_t nat_mc_op_workspace(nat_prec prec, int64_t M, int n_sys);
+nat_status nat_mc_rhs(nat_prec prec, int64_t M, const double* samples, int n_sys, const double* k,
+                      const void* g, double w, double eps, void* b, void* ws, size_t ws_bytes,
+                      nat_stream_t stream); /* (async) */
+nat_status nat_mc_apply(nat_prec prec, int64_t M, const double* samples, int n_sys, const double* k,
+                        const void* p, double w, void* out, void* ws, size_t ws_bytes,
+                        nat_stream_t stream); /* (async) */
+nat_status nat_mc_check_coincident(int64_t M, const double* samples, int64_t* pair /* [host] 2 */,
+                                   void* ws, size_t ws_bytes, nat_stream_t stream); /* (sync) */
+
+size_t nat_mc_workspace(nat_prec prec, int64_t M, int n_sys, int max_iter);
+nat_status nat_mc_surface_pressure(const nat_mesh* mesh, const nat_geom* geom, int n_sys,
+                                   const double* k /* [host] */, const void* g_tri, const nat_mc_opts* opts,
+                                   nat_prec prec, double tol, int max_iter, double* samples_out,
+                                   int32_t* sample_tri_out, void* p_out, void* ws, size_t ws_bytes,
+                                   nat_solve_info* info /* [host][n_sys] */,
+                                   nat_stream_t stream); /* (sync) */
+
+/* ---------------------------------------------------------------------------------
+ * (c) radiation to listeners (reading R-ext):
+ *   p[m][l] = sum_s w_s [ p[m][s] dG_m/dn_y(x_l, y_s) - g[m][s] G_m(x_l, y_s) ].
+ * ------------------------------------------------------------------------------- */
+typedef struct {
+  int64_t n_src;
+  const double* xyz; /* [3][n_src]                       */
+  const double* nrm; /* [3][n_src] unit normals          */
+  const double* w;   /* [n_src] quadrature / MC weights  */
+  int n_modes;
+  const void* p;     /* c128 [n_modes][n_src] Dirichlet  */
+  const void* g;     /* c128 [n_modes][n_src] Neumann    */
+  double center[3];  /* [host] coordinate origin used for the fp32 cast (mesh centre) */
+} nat_sources;
+
+/* BEM solution -> sources: the q_rad (1|3|6|7) rule points of every triangle,
+ * w = omega_q A_t, normal n_t, values p_t, g_t (c128 [n_modes][n_tri] in,
+ * [n_modes][n_tri*q_rad] out; point index t*q_rad + q).                                */
+nat_status nat_bem_sources(const nat_mesh* mesh, const nat_geom* geom, int q_rad, int n_modes,
+                           const void* p_tri, const void* g_tri, double* xyz, double* nrm, double* w,
+                           void* p_src, void* g_src, nat_stream_t stream); /* (async) */
+/* MC solution -> sources: xyz/nrm rows of samples, w = total_area / M.               */
+nat_status nat_mc_sources(int64_t M, const double* samples, double total_area, double* xyz,
+                          double* nrm, double* w, nat_stream_t stream); /* (async) */
+
+size_t nat_radiate_workspace(nat_prec prec, int64_t n_src, int n_modes, int64_t n_lis);
+nat_status nat_radiate_field(const nat_sources* src, nat_prec prec, const double* k /* [host][n_modes] */,
+                             int64_t n_lis, const double* lis_xyz /* [3][n_lis] */,
+                             void* p_out /* c128 [n_modes][n_lis] */, void* ws, size_t ws_bytes,
+                             nat_stream_t stream); /* (async) */
+
+/* ---------------------------------------------------------------------------------
+ * a12 — listener shell grid (reading R-listen): point ((w n_phi)+v) n_theta + u,
+ *   theta_u = -pi + (u+1/2) 2pi/n_theta, phi_v = (v+1/2) pi/n_phi,
+ *   r_w = R (r_lo + (r_hi - r_lo)(w+1/2)/n_r), x = center + r (sin phi cos theta,
+ *   sin phi sin theta, cos phi).  out: [3][n_theta n_phi n_r] float64.
+ * ------------------------------------------------------------------------------- */
+nat_status nat_listener_grid(const double* center /* [host] 3 */, double R, int n_theta, int n_phi,
+                             int n_r, double r_lo, double r_hi, double* out,
+                             nat_stream_t stream); /* (async) */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NAT_H */

@@ -1,0 +1,221 @@
+// Row a1 — mesh preparation (reading R-geom) and
+// row a12 — listener shell grid (reading R-listen).
+//
+// Every fp64 operation that feeds an integer decision downstream (near list, MC
+// triangle choice, MC sample position) is written with explicit round-to-nearest
+// intrinsics (__dadd_rn, __dmul_rn, ...) so nvcc cannot contract it into an FMA:
+// the results are bit-identical to any IEEE implementation of the same formula.
+#include "nat_internal.cuh"
+
+namespace {
+
+struct PrepScalars {
+  double total_area, cx, cy, cz, volume, radius;
+  long long bad_tri;  // min index of a zero-area triangle, or LLONG_MAX
+};
+
+__device__ __forceinline__ double dnorm_rn(double x, double y, double z) {
+  return __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)), __dmul_rn(z, z)));
+}
+
+__global__ void tri_geom_kernel(int64_t nv, int64_t nt, const double* __restrict__ vx,
+                                const int32_t* __restrict__ tri, double* __restrict__ cen,
+                                double* __restrict__ nrm, double* __restrict__ area,
+                                double* __restrict__ diam, double* __restrict__ vol_term,
+                                PrepScalars* sc) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= nt) return;
+  const double* X = vx;
+  const double* Y = vx + nv;
+  const double* Z = vx + 2 * nv;
+  int a = tri[t], b = tri[nt + t], c = tri[2 * nt + t];
+  double x1 = X[a], y1 = Y[a], z1 = Z[a];
+  double x2 = X[b], y2 = Y[b], z2 = Z[b];
+  double x3 = X[c], y3 = Y[c], z3 = Z[c];
+  double ax = __dsub_rn(x2, x1), ay = __dsub_rn(y2, y1), az = __dsub_rn(z2, z1);
+  double bx = __dsub_rn(x3, x1), by = __dsub_rn(y3, y1), bz = __dsub_rn(z3, z1);
+  double ex = __dsub_rn(__dmul_rn(ay, bz), __dmul_rn(az, by));
+  double ey = __dsub_rn(__dmul_rn(az, bx), __dmul_rn(ax, bz));
+  double ez = __dsub_rn(__dmul_rn(ax, by), __dmul_rn(ay, bx));
+  double en = dnorm_rn(ex, ey, ez);
+  if (!(en > 0.0)) atomicMin(&sc->bad_tri, (long long)t);
+  area[t] = __dmul_rn(0.5, en);
+  nrm[t] = __ddiv_rn(ex, en);
+  nrm[nt + t] = __ddiv_rn(ey, en);
+  nrm[2 * nt + t] = __ddiv_rn(ez, en);
+  cen[t] = __ddiv_rn(__dadd_rn(__dadd_rn(x1, x2), x3), 3.0);
+  cen[nt + t] = __ddiv_rn(__dadd_rn(__dadd_rn(y1, y2), y3), 3.0);
+  cen[2 * nt + t] = __ddiv_rn(__dadd_rn(__dadd_rn(z1, z2), z3), 3.0);
+  double l12 = dnorm_rn(__dsub_rn(x2, x1), __dsub_rn(y2, y1), __dsub_rn(z2, z1));
+  double l23 = dnorm_rn(__dsub_rn(x3, x2), __dsub_rn(y3, y2), __dsub_rn(z3, z2));
+  double l31 = dnorm_rn(__dsub_rn(x1, x3), __dsub_rn(y1, y3), __dsub_rn(z1, z3));
+  diam[t] = fmax(fmax(l12, l23), l31);
+  // v1 . (v2 x v3) for the signed volume (order of the final sum is irrelevant)
+  vol_term[t] = x1 * (y2 * z3 - z2 * y3) + y1 * (z2 * x3 - x2 * z3) + z1 * (x2 * y3 - y2 * x3);
+}
+
+// Sequential prefix sum, exactly the left-to-right order of the definition.
+__global__ void cdf_kernel(int64_t nt, const double* __restrict__ area, double* __restrict__ cdf) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double s = 0.0;
+  int64_t t = 0;
+  for (; t + 8 <= nt; t += 8) {
+    double a[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) a[q] = area[t + q];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      s = __dadd_rn(s, a[q]);
+      cdf[t + q] = s;
+    }
+  }
+  for (; t < nt; ++t) {
+    s = __dadd_rn(s, area[t]);
+    cdf[t] = s;
+  }
+}
+
+constexpr int RB = 1024;
+
+// One block: deterministic tree reductions of sum(A c), sum(vol_term).
+__global__ void __launch_bounds__(RB) centre_kernel(int64_t nt, const double* __restrict__ area,
+                                                    const double* __restrict__ cen,
+                                                    const double* __restrict__ vol_term,
+                                                    const double* __restrict__ cdf, PrepScalars* sc) {
+  __shared__ double red[4][RB];
+  double s[4] = {0, 0, 0, 0};
+  for (int64_t t = threadIdx.x; t < nt; t += RB) {
+    double a = area[t];
+    s[0] += a * cen[t];
+    s[1] += a * cen[nt + t];
+    s[2] += a * cen[2 * nt + t];
+    s[3] += vol_term[t];
+  }
+  for (int q = 0; q < 4; ++q) red[q][threadIdx.x] = s[q];
+  __syncthreads();
+  for (int w = RB / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w)
+      for (int q = 0; q < 4; ++q) red[q][threadIdx.x] += red[q][threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    double tot = cdf[nt - 1];
+    sc->total_area = tot;
+    sc->cx = red[0][0] / tot;
+    sc->cy = red[1][0] / tot;
+    sc->cz = red[2][0] / tot;
+    sc->volume = red[3][0] / 6.0;
+  }
+}
+
+__global__ void __launch_bounds__(RB) radius_kernel(int64_t nv, const double* __restrict__ vx,
+                                                    PrepScalars* sc) {
+  __shared__ double red[RB];
+  double cx = sc->cx, cy = sc->cy, cz = sc->cz, m = 0.0;
+  for (int64_t v = threadIdx.x; v < nv; v += RB) {
+    double dx = vx[v] - cx, dy = vx[nv + v] - cy, dz = vx[2 * nv + v] - cz;
+    m = fmax(m, sqrt(dx * dx + dy * dy + dz * dz));
+  }
+  red[threadIdx.x] = m;
+  __syncthreads();
+  for (int w = RB / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + w]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) sc->radius = red[0];
+}
+
+__global__ void init_scalars(PrepScalars* sc) {
+  sc->total_area = sc->cx = sc->cy = sc->cz = sc->volume = sc->radius = 0.0;
+  sc->bad_tri = 0x7fffffffffffffffLL;
+}
+
+__global__ void listener_grid_kernel(double cx, double cy, double cz, double R, int nth, int nph,
+                                     int nr, double r_lo, double r_hi, double* __restrict__ out) {
+  int64_t n = (int64_t)nth * nph * nr;
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int u = (int)(i % nth);
+  int v = (int)((i / nth) % nph);
+  int w = (int)(i / ((int64_t)nth * nph));
+  const double pi = nat::kPi;
+  double th = -pi + (u + 0.5) * 2.0 * pi / nth;
+  double ph = (v + 0.5) * pi / nph;
+  double r = R * (r_lo + (r_hi - r_lo) * (w + 0.5) / nr);
+  double st, ct, sp, cp;
+  sincos(th, &st, &ct);
+  sincos(ph, &sp, &cp);
+  out[i] = cx + r * (sp * ct);
+  out[n + i] = cy + r * (sp * st);
+  out[2 * n + i] = cz + r * cp;
+}
+
+}  // namespace
+
+extern "C" size_t nat_mesh_prepare_workspace(int64_t n_vert, int64_t n_tri) {
+  (void)n_vert;
+  nat::Carver c(nullptr);
+  c.take<PrepScalars>(1);
+  c.take<double>(n_tri);
+  return c.bytes();
+}
+
+extern "C" nat_status nat_mesh_prepare(const nat_mesh* mesh, nat_geom* geom, void* ws,
+                                       size_t ws_bytes, nat_stream_t stream) {
+  NAT_REQUIRE(mesh && geom, "mesh and geom must be non-null");
+  NAT_REQUIRE(mesh->n_vert >= 3 && mesh->n_tri >= 1, "need n_vert >= 3 and n_tri >= 1");
+  NAT_REQUIRE(geom->n_tri == mesh->n_tri, "geom->n_tri (%lld) != mesh->n_tri (%lld)",
+              (long long)geom->n_tri, (long long)mesh->n_tri);
+  NAT_REQUIRE_DEV(mesh->vxyz);
+  NAT_REQUIRE_DEV(mesh->tri);
+  NAT_REQUIRE_DEV(geom->centroid);
+  NAT_REQUIRE_DEV(geom->normal);
+  NAT_REQUIRE_DEV(geom->area);
+  NAT_REQUIRE_DEV(geom->diam);
+  NAT_REQUIRE_DEV(geom->area_cdf);
+  size_t need = nat_mesh_prepare_workspace(mesh->n_vert, mesh->n_tri);
+  if (ws_bytes < need) return nat::fail(NAT_ERR_WORKSPACE, "workspace %zu < %zu", ws_bytes, need);
+  NAT_REQUIRE_DEV(ws);
+  nat::Carver c(ws);
+  PrepScalars* sc = c.take<PrepScalars>(1);
+  double* vol = c.take<double>(mesh->n_tri);
+  cudaStream_t s = (cudaStream_t)stream;
+  int64_t nt = mesh->n_tri;
+  init_scalars<<<1, 1, 0, s>>>(sc);
+  tri_geom_kernel<<<(unsigned)((nt + 255) / 256), 256, 0, s>>>(
+      mesh->n_vert, nt, mesh->vxyz, mesh->tri, geom->centroid, geom->normal, geom->area, geom->diam,
+      vol, sc);
+  cdf_kernel<<<1, 32, 0, s>>>(nt, geom->area, geom->area_cdf);
+  centre_kernel<<<1, RB, 0, s>>>(nt, geom->area, geom->centroid, vol, geom->area_cdf, sc);
+  radius_kernel<<<1, RB, 0, s>>>(mesh->n_vert, mesh->vxyz, sc);
+  NAT_LAUNCH_CHECK();
+  PrepScalars h;
+  NAT_CUDA_TRY(cudaMemcpyAsync(&h, sc, sizeof h, cudaMemcpyDeviceToHost, s));
+  NAT_CUDA_TRY(cudaStreamSynchronize(s));
+  if (h.bad_tri != 0x7fffffffffffffffLL)
+    return nat::fail(NAT_ERR_SINGULAR, "zero-area triangle %lld", h.bad_tri);
+  if (!(h.volume > 0.0))
+    return nat::fail(NAT_ERR_SINGULAR, "mesh is not outward-oriented (signed volume %g <= 0)",
+                     h.volume);
+  geom->total_area = h.total_area;
+  geom->center[0] = h.cx;
+  geom->center[1] = h.cy;
+  geom->center[2] = h.cz;
+  geom->bound_radius = h.radius;
+  geom->volume = h.volume;
+  return NAT_OK;
+}
+
+extern "C" nat_status nat_listener_grid(const double* center, double R, int n_theta, int n_phi,
+                                        int n_r, double r_lo, double r_hi, double* out,
+                                        nat_stream_t stream) {
+  NAT_REQUIRE(center, "center must be a host pointer to 3 doubles");
+  NAT_REQUIRE(n_theta > 0 && n_phi > 0 && n_r > 0, "grid sizes must be positive");
+  NAT_REQUIRE(R > 0 && r_lo > 0 && r_hi >= r_lo, "need R > 0, 0 < r_lo <= r_hi");
+  NAT_REQUIRE_DEV(out);
+  int64_t n = (int64_t)n_theta * n_phi * n_r;
+  listener_grid_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      center[0], center[1], center[2], R, n_theta, n_phi, n_r, r_lo, r_hi, out);
+  NAT_LAUNCH_CHECK();
+  return NAT_OK;
+}

@@ -1,0 +1,65 @@
+// Internal helpers of libnat (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+
+#include "../../include/nat.h"
+
+namespace nat {
+
+void set_error(const char* fmt, ...);
+nat_status fail(nat_status st, const char* fmt, ...);
+bool is_device_ptr(const void* p);
+
+constexpr double kPi = 3.141592653589793238462643383279502884;
+constexpr double kInv4Pi = 0.0795774715459476678844418816862571810;
+constexpr int kNumSMs = 148;
+
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// Carves sub-buffers out of a caller workspace (256-byte aligned pieces).
+struct Carver {
+  char* base;
+  size_t off = 0;
+  explicit Carver(void* b) : base(static_cast<char*>(b)) {}
+  template <class T>
+  T* take(size_t count) {
+    off = align_up(off, 256);
+    T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
+    off += count * sizeof(T);
+    return p;
+  }
+  size_t bytes() const { return align_up(off, 256); }
+};
+
+int device_sm_count();
+
+}  // namespace nat
+
+#define NAT_CUDA_TRY(expr)                                                                   \
+  do {                                                                                       \
+    cudaError_t _e = (expr);                                                                 \
+    if (_e != cudaSuccess)                                                                   \
+      return nat::fail(NAT_ERR_CUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(_e),        \
+                       __FILE__, __LINE__);                                                  \
+  } while (0)
+
+#define NAT_LAUNCH_CHECK()                                                                   \
+  do {                                                                                       \
+    cudaError_t _e = cudaGetLastError();                                                     \
+    if (_e != cudaSuccess)                                                                   \
+      return nat::fail(NAT_ERR_CUDA, "kernel launch: %s (%s:%d)", cudaGetErrorString(_e),   \
+                       __FILE__, __LINE__);                                                  \
+  } while (0)
+
+#define NAT_REQUIRE(cond, ...)                                                               \
+  do {                                                                                       \
+    if (!(cond)) return nat::fail(NAT_ERR_INVALID_ARG, __VA_ARGS__);                          \
+  } while (0)
+
+#define NAT_REQUIRE_DEV(ptr)                                                                 \
+  NAT_REQUIRE(nat::is_device_ptr(ptr), "%s must be a device pointer", #ptr)

@@ -1,0 +1,613 @@
+// Row a11 — radiation of the surface field to listener points (reading R-ext):
+//   p_m(x_l) = sum_s w_s [ p_ms dG_m/dn_y(x_l, y_s) - g_ms G_m(x_l, y_s) ].
+//
+// B200 design:
+//  * stage kernel folds w/(4 pi) and k into per-source constants (O(S) work):
+//      alpha = w p/(4pi), beta = w g/(4pi);  A1 = -Re a, A2 = -k Im a, A3 = k Re a,
+//      A4 = -Im a, B1 = -Re b, B2 = -Im b, so that per pair (rho = 1/r, q = (d.n) rho^2)
+//      C = q (rho A1 + A2) + rho B1 + i [q (rho A4 + A3) + rho B2],  acc += e^{ikr} C;
+//  * main kernel: CTA = 256 threads x R targets each (registers); source tiles of
+//    128 records are streamed into shared memory with TMA bulk copies (cp.async.bulk +
+//    mbarrier, double buffered) and read back as warp-broadcast LDS.128; MB wavenumbers
+//    share r, 1/r and d.n; fp32 math with MUFU rsqrt/sin/cos; per-tile fp32 sums are
+//    added into fp64 accumulators kept in shared memory;
+//  * split-K over source chunks when the target grid is too small for 148 SMs, with a
+//    fixed-order fp64 reduction (deterministic, no atomics).
+#include "async_copy.cuh"
+#include "nat_internal.cuh"
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kTile = 128;  // sources per shared-memory tile (fp32)
+constexpr int kTile64 = 64; // sources per tile (fp64)
+
+template <int MB>
+struct Rec {
+  static constexpr int NF = ((6 + 6 * MB) + 3) / 4 * 4;  // floats per source record
+};
+
+struct RadParams {
+  const void* rec;      // [n_mchunk][n_src_pad][NF] records
+  int64_t n_src_pad;    // multiple of the tile
+  int n_tiles;          // n_src_pad / tile
+  int chunk_tiles;      // tiles per split
+  const double* lis;    // [3][n_lis]
+  int64_t n_lis;
+  double cx, cy, cz;    // coordinate origin
+  const float* kf;      // [n_mchunk*MB] wavenumbers (fp32)
+  const double* kd;     // [n_mchunk*MB] wavenumbers (fp64)
+  double2* out;         // [n_split][n_modes][n_lis]
+  int n_modes;
+};
+
+// ------------------------------------------------------------------------------------
+// staging
+// ------------------------------------------------------------------------------------
+template <typename T>
+__global__ void stage_kernel(int64_t n_src, int64_t n_src_pad, int NF, int MB, int n_mchunk,
+                             const double* __restrict__ xyz, const double* __restrict__ nrm,
+                             const double* __restrict__ w, const double2* __restrict__ p,
+                             const double2* __restrict__ g, const double* __restrict__ kd,
+                             int n_modes, double cx, double cy, double cz, T* __restrict__ rec) {
+  int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s >= n_src_pad) return;
+  double x, y, z, nx, ny, nz, ws;
+  if (s < n_src) {
+    x = xyz[s] - cx;
+    y = xyz[n_src + s] - cy;
+    z = xyz[2 * n_src + s] - cz;
+    nx = nrm[s];
+    ny = nrm[n_src + s];
+    nz = nrm[2 * n_src + s];
+    ws = w[s] * nat::kInv4Pi;
+  } else {  // padding: far away, zero weight -> contributes exactly 0
+    x = y = z = 3.0e3;
+    nx = 1.0;
+    ny = nz = 0.0;
+    ws = 0.0;
+  }
+  for (int c = 0; c < n_mchunk; ++c) {
+    T* r = rec + ((size_t)c * n_src_pad + s) * NF;
+    r[0] = (T)x;
+    r[1] = (T)y;
+    r[2] = (T)z;
+    r[3] = (T)nx;
+    r[4] = (T)ny;
+    r[5] = (T)nz;
+    for (int m = 0; m < MB; ++m) {
+      int mode = c * MB + m;
+      double ar = 0, ai = 0, br = 0, bi = 0, k = 0;
+      if (mode < n_modes && ws != 0.0) {
+        double2 pv = p[(size_t)mode * n_src + s];
+        double2 gv = g[(size_t)mode * n_src + s];
+        ar = ws * pv.x;
+        ai = ws * pv.y;
+        br = ws * gv.x;
+        bi = ws * gv.y;
+        k = kd[mode];
+      }
+      T* q = r + 6 + 6 * m;
+      q[0] = (T)(-ar);
+      q[1] = (T)(-k * ai);
+      q[2] = (T)(k * ar);
+      q[3] = (T)(-ai);
+      q[4] = (T)(-br);
+      q[5] = (T)(-bi);
+    }
+    for (int f = 6 + 6 * MB; f < NF; ++f) r[f] = (T)0;
+  }
+}
+
+// ------------------------------------------------------------------------------------
+// fp32 main kernel
+// ------------------------------------------------------------------------------------
+__device__ __forceinline__ float rsqrt_approx(float x) {
+  float y;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+template <int R, int MB>
+__global__ void __launch_bounds__(kThreads) radiate_f32_kernel(RadParams prm) {
+  constexpr int NF = Rec<MB>::NF;
+  constexpr int kTileFloats = kTile * NF;
+  extern __shared__ __align__(128) unsigned char smem[];
+  float* buf = reinterpret_cast<float*>(smem);
+  double2* dacc = reinterpret_cast<double2*>(smem + 2 * kTileFloats * sizeof(float));
+  __shared__ __align__(8) uint64_t bars[2];
+
+  const int tid = threadIdx.x;
+  const int64_t tbase = (int64_t)blockIdx.x * (R * kThreads);
+  const int split = blockIdx.y;
+  const int mch = blockIdx.z;
+
+  float tx[R], ty[R], tz[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    int64_t l = tbase + r * kThreads + tid;
+    if (l >= prm.n_lis) l = prm.n_lis - 1;
+    tx[r] = (float)(prm.lis[l] - prm.cx);
+    ty[r] = (float)(prm.lis[prm.n_lis + l] - prm.cy);
+    tz[r] = (float)(prm.lis[2 * prm.n_lis + l] - prm.cz);
+  }
+  float kk[MB];
+#pragma unroll
+  for (int m = 0; m < MB; ++m) kk[m] = prm.kf[mch * MB + m];
+#pragma unroll
+  for (int q = 0; q < R * MB; ++q) dacc[q * kThreads + tid] = make_double2(0.0, 0.0);
+
+  const int t0 = split * prm.chunk_tiles;
+  const int t1 = min(t0 + prm.chunk_tiles, prm.n_tiles);
+  const float* src = static_cast<const float*>(prm.rec) + (size_t)mch * prm.n_src_pad * NF;
+  constexpr uint32_t kBytes = kTileFloats * sizeof(float);
+
+  if (tid == 0) {
+    nat::mbar_init(&bars[0], 1);
+    nat::mbar_init(&bars[1], 1);
+    nat::fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int st = 0; st < 2 && t0 + st < t1; ++st) {
+      nat::mbar_arrive_expect_tx(&bars[st], kBytes);
+      nat::bulk_g2s(buf + st * kTileFloats, src + (size_t)(t0 + st) * kTileFloats, kBytes, &bars[st]);
+    }
+  }
+
+  for (int it = 0; t0 + it < t1; ++it) {
+    const int st = it & 1;
+    nat::mbar_wait(&bars[st], (it >> 1) & 1);
+    const float4* b4 = reinterpret_cast<const float4*>(buf + st * kTileFloats);
+    float ar[R][MB], ai[R][MB];
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int m = 0; m < MB; ++m) ar[r][m] = ai[r][m] = 0.f;
+
+#pragma unroll 2
+    for (int s = 0; s < kTile; ++s) {
+      float f[NF];
+#pragma unroll
+      for (int q = 0; q < NF / 4; ++q) {
+        float4 v = b4[s * (NF / 4) + q];
+        f[4 * q] = v.x;
+        f[4 * q + 1] = v.y;
+        f[4 * q + 2] = v.z;
+        f[4 * q + 3] = v.w;
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const float dx = f[0] - tx[r];
+        const float dy = f[1] - ty[r];
+        const float dz = f[2] - tz[r];
+        const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+        const float dn = fmaf(dz, f[5], fmaf(dy, f[4], dx * f[3]));
+        const float rho = rsqrt_approx(r2);
+        const float qq = dn * (rho * rho);
+        const float rr = r2 * rho;
+#pragma unroll
+        for (int m = 0; m < MB; ++m) {
+          float sn, cs;
+          __sincosf(rr * kk[m], &sn, &cs);
+          const float* c = f + 6 + 6 * m;
+          const float cr = fmaf(qq, fmaf(rho, c[0], c[1]), rho * c[4]);
+          const float ci = fmaf(qq, fmaf(rho, c[3], c[2]), rho * c[5]);
+          ar[r][m] = fmaf(cs, cr, fmaf(-sn, ci, ar[r][m]));
+          ai[r][m] = fmaf(sn, cr, fmaf(cs, ci, ai[r][m]));
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int m = 0; m < MB; ++m) {
+        double2 d = dacc[(r * MB + m) * kThreads + tid];
+        d.x += (double)ar[r][m];
+        d.y += (double)ai[r][m];
+        dacc[(r * MB + m) * kThreads + tid] = d;
+      }
+    __syncthreads();  // every thread is done with buf[st]
+    if (tid == 0 && t0 + it + 2 < t1) {
+      nat::fence_proxy_async_smem();
+      nat::mbar_arrive_expect_tx(&bars[st], kBytes);
+      nat::bulk_g2s(buf + st * kTileFloats, src + (size_t)(t0 + it + 2) * kTileFloats, kBytes,
+                    &bars[st]);
+    }
+  }
+
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    int64_t l = tbase + r * kThreads + tid;
+    if (l >= prm.n_lis) continue;
+#pragma unroll
+    for (int m = 0; m < MB; ++m) {
+      int mode = mch * MB + m;
+      if (mode < prm.n_modes)
+        prm.out[((size_t)split * prm.n_modes + mode) * prm.n_lis + l] =
+            dacc[(r * MB + m) * kThreads + tid];
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------
+// fp64 main kernel: one wavenumber per pass (MB = 1), R targets per thread, fp64 math.
+// ------------------------------------------------------------------------------------
+template <int R>
+__global__ void __launch_bounds__(kThreads) radiate_f64_kernel(RadParams prm) {
+  constexpr int NF = 12;
+  constexpr int kTileD = kTile64 * NF;
+  extern __shared__ __align__(128) unsigned char smem[];
+  double* buf = reinterpret_cast<double*>(smem);
+  __shared__ __align__(8) uint64_t bars[2];
+  const int tid = threadIdx.x;
+  const int64_t tbase = (int64_t)blockIdx.x * (R * kThreads);
+  const int split = blockIdx.y, mch = blockIdx.z;
+  double tx[R], ty[R], tz[R], ar[R], ai[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    int64_t l = tbase + r * kThreads + tid;
+    if (l >= prm.n_lis) l = prm.n_lis - 1;
+    tx[r] = prm.lis[l] - prm.cx;
+    ty[r] = prm.lis[prm.n_lis + l] - prm.cy;
+    tz[r] = prm.lis[2 * prm.n_lis + l] - prm.cz;
+    ar[r] = ai[r] = 0.0;
+  }
+  const double k = prm.kd[mch];
+  const int t0 = split * prm.chunk_tiles;
+  const int t1 = min(t0 + prm.chunk_tiles, prm.n_tiles);
+  const double* src = static_cast<const double*>(prm.rec) + (size_t)mch * prm.n_src_pad * NF;
+  constexpr uint32_t kBytes = kTileD * sizeof(double);
+  if (tid == 0) {
+    nat::mbar_init(&bars[0], 1);
+    nat::mbar_init(&bars[1], 1);
+    nat::fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int st = 0; st < 2 && t0 + st < t1; ++st) {
+      nat::mbar_arrive_expect_tx(&bars[st], kBytes);
+      nat::bulk_g2s(buf + st * kTileD, src + (size_t)(t0 + st) * kTileD, kBytes, &bars[st]);
+    }
+  }
+  for (int it = 0; t0 + it < t1; ++it) {
+    const int st = it & 1;
+    nat::mbar_wait(&bars[st], (it >> 1) & 1);
+    const double2* b2 = reinterpret_cast<const double2*>(buf + st * kTileD);
+    for (int s = 0; s < kTile64; ++s) {
+      double f[NF];
+#pragma unroll
+      for (int q = 0; q < NF / 2; ++q) {
+        double2 v = b2[s * (NF / 2) + q];
+        f[2 * q] = v.x;
+        f[2 * q + 1] = v.y;
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const double dx = f[0] - tx[r], dy = f[1] - ty[r], dz = f[2] - tz[r];
+        const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
+        const double dn = fma(dz, f[5], fma(dy, f[4], dx * f[3]));
+        const double rr = sqrt(r2);
+        const double rho = 1.0 / rr;
+        const double qq = dn * (rho * rho);
+        double sn, cs;
+        sincos(k * rr, &sn, &cs);
+        const double cr = fma(qq, fma(rho, f[6], f[7]), rho * f[10]);
+        const double ci = fma(qq, fma(rho, f[9], f[8]), rho * f[11]);
+        ar[r] = fma(cs, cr, fma(-sn, ci, ar[r]));
+        ai[r] = fma(sn, cr, fma(cs, ci, ai[r]));
+      }
+    }
+    __syncthreads();
+    if (tid == 0 && t0 + it + 2 < t1) {
+      nat::fence_proxy_async_smem();
+      nat::mbar_arrive_expect_tx(&bars[st], kBytes);
+      nat::bulk_g2s(buf + st * kTileD, src + (size_t)(t0 + it + 2) * kTileD, kBytes, &bars[st]);
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    int64_t l = tbase + r * kThreads + tid;
+    if (l < prm.n_lis && mch < prm.n_modes)
+      prm.out[((size_t)split * prm.n_modes + mch) * prm.n_lis + l] = make_double2(ar[r], ai[r]);
+  }
+}
+
+__global__ void reduce_splits_kernel(const double2* __restrict__ part, int n_split, int64_t n,
+                                     double2* __restrict__ out) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double2 s = part[i];
+  for (int k = 1; k < n_split; ++k) {
+    double2 v = part[(size_t)k * n + i];
+    s.x += v.x;
+    s.y += v.y;
+  }
+  out[i] = s;
+}
+
+struct RuleQ {
+  double lam[9], w[3];
+  int Q;
+};
+
+__global__ void bem_sources_kernel(int64_t nv, int64_t nt, const double* __restrict__ vx,
+                                   const int32_t* __restrict__ tri, const double* __restrict__ nrm,
+                                   const double* __restrict__ area, RuleQ rq, int n_modes, const double2* __restrict__ p_tri,
+                                   const double2* __restrict__ g_tri, double* __restrict__ xyz,
+                                   double* __restrict__ nout, double* __restrict__ w,
+                                   double2* __restrict__ p_src, double2* __restrict__ g_src) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int Q = rq.Q;
+  int64_t S = nt * Q;
+  if (i >= S) return;
+  int64_t t = i / Q;
+  int q = (int)(i % Q);
+  int a = tri[t], b = tri[nt + t], c = tri[2 * nt + t];
+  double l1 = rq.lam[3 * q], l2 = rq.lam[3 * q + 1], l3 = rq.lam[3 * q + 2];
+  for (int d = 0; d < 3; ++d) {
+    const double* X = vx + d * nv;
+    xyz[d * S + i] = __dadd_rn(__dadd_rn(__dmul_rn(l1, X[a]), __dmul_rn(l2, X[b])), __dmul_rn(l3, X[c]));
+    nout[d * S + i] = nrm[d * nt + t];
+  }
+  w[i] = rq.w[q] * area[t];
+  for (int m = 0; m < n_modes; ++m) {
+    p_src[(size_t)m * S + i] = p_tri[(size_t)m * nt + t];
+    g_src[(size_t)m * S + i] = g_tri[(size_t)m * nt + t];
+  }
+}
+
+__global__ void mc_sources_kernel(int64_t M, const double* __restrict__ smp, double wv,
+                                  double* __restrict__ xyz, double* __restrict__ nrm,
+                                  double* __restrict__ w) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= M) return;
+  for (int d = 0; d < 3; ++d) {
+    xyz[d * M + i] = smp[d * M + i];
+    nrm[d * M + i] = smp[(3 + d) * M + i];
+  }
+  w[i] = wv;
+}
+
+// ------------------------------------------------------------------------------------
+// host side
+// ------------------------------------------------------------------------------------
+struct Plan {
+  int MB, R, NF, n_mchunk, tile, n_tiles, chunk_tiles, n_split;
+  int64_t n_src_pad, tgt_tiles;
+  size_t rec_elems, smem;
+  bool fp64;
+};
+
+int pick_mb(int n_modes) {
+  if (n_modes >= 8) return 4;
+  if (n_modes >= 4) return 4;
+  if (n_modes == 3) return 3;
+  if (n_modes == 2) return 2;
+  return 1;
+}
+
+Plan make_plan(nat_prec prec, int64_t n_src, int n_modes, int64_t n_lis) {
+  Plan pl{};
+  pl.fp64 = (prec == NAT_FP64);
+  if (pl.fp64) {
+    pl.MB = 1;
+    pl.R = 2;
+    pl.NF = 12;
+    pl.tile = kTile64;
+  } else {
+    pl.MB = pick_mb(n_modes);
+    pl.R = 4;
+    pl.NF = ((6 + 6 * pl.MB) + 3) / 4 * 4;
+    pl.tile = kTile;
+  }
+  pl.n_mchunk = (n_modes + pl.MB - 1) / pl.MB;
+  pl.n_tiles = (int)((n_src + pl.tile - 1) / pl.tile);
+  pl.n_src_pad = (int64_t)pl.n_tiles * pl.tile;
+  pl.tgt_tiles = (n_lis + (int64_t)pl.R * kThreads - 1) / ((int64_t)pl.R * kThreads);
+  int64_t base = pl.tgt_tiles * pl.n_mchunk;
+  int64_t want = 4LL * nat::kNumSMs * 2;  // enough CTAs for several full waves
+  int n_split = 1;
+  if (base < want) n_split = (int)std::min<int64_t>((want + base - 1) / base, pl.n_tiles);
+  pl.chunk_tiles = (pl.n_tiles + n_split - 1) / n_split;
+  pl.n_split = (pl.n_tiles + pl.chunk_tiles - 1) / pl.chunk_tiles;
+  pl.rec_elems = (size_t)pl.n_mchunk * pl.n_src_pad * pl.NF;
+  if (pl.fp64)
+    pl.smem = 2 * (size_t)kTile64 * 12 * sizeof(double);
+  else
+    pl.smem = 2 * (size_t)kTile * pl.NF * sizeof(float) + (size_t)pl.R * pl.MB * kThreads * 16;
+  return pl;
+}
+
+size_t plan_ws(const Plan& pl, int n_modes, int64_t n_lis, nat::Carver& c, void** rec, float** kf,
+               double** kd, double2** part) {
+  *rec = pl.fp64 ? (void*)c.take<double>(pl.rec_elems) : (void*)c.take<float>(pl.rec_elems);
+  *kf = c.take<float>((size_t)pl.n_mchunk * pl.MB);
+  *kd = c.take<double>((size_t)pl.n_mchunk * pl.MB);
+  *part = pl.n_split > 1 ? c.take<double2>((size_t)pl.n_split * n_modes * n_lis) : nullptr;
+  return c.bytes();
+}
+
+template <int R, int MB>
+cudaError_t launch_f32(const Plan& pl, const RadParams& prm, cudaStream_t s) {
+  auto kern = radiate_f32_kernel<R, MB>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
+  if (e != cudaSuccess) return e;
+  dim3 grid((unsigned)pl.tgt_tiles, (unsigned)pl.n_split, (unsigned)pl.n_mchunk);
+  kern<<<grid, kThreads, pl.smem, s>>>(prm);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+extern "C" size_t nat_radiate_workspace(nat_prec prec, int64_t n_src, int n_modes, int64_t n_lis) {
+  if (n_src <= 0 || n_modes <= 0 || n_lis <= 0) return 0;
+  Plan pl = make_plan(prec, n_src, n_modes, n_lis);
+  nat::Carver c(nullptr);
+  void* rec;
+  float* kf;
+  double* kd;
+  double2* part;
+  return plan_ws(pl, n_modes, n_lis, c, &rec, &kf, &kd, &part);
+}
+
+extern "C" nat_status nat_radiate_field(const nat_sources* src, nat_prec prec, const double* k,
+                                        int64_t n_lis, const double* lis_xyz, void* p_out, void* ws,
+                                        size_t ws_bytes, nat_stream_t stream) {
+  NAT_REQUIRE(src && k, "src and k must be non-null");
+  NAT_REQUIRE(prec == NAT_FP32 || prec == NAT_FP64, "bad precision %d", (int)prec);
+  NAT_REQUIRE(src->n_src > 0 && src->n_modes > 0 && n_lis > 0, "need n_src, n_modes, n_lis > 0");
+  NAT_REQUIRE(src->n_src < (1LL << 31) && n_lis < (1LL << 40), "size out of range");
+  for (int m = 0; m < src->n_modes; ++m)
+    NAT_REQUIRE(k[m] >= 0.0 && k[m] < 1e300, "k[%d] = %g must be finite and >= 0", m, k[m]);
+  NAT_REQUIRE_DEV(src->xyz);
+  NAT_REQUIRE_DEV(src->nrm);
+  NAT_REQUIRE_DEV(src->w);
+  NAT_REQUIRE_DEV(src->p);
+  NAT_REQUIRE_DEV(src->g);
+  NAT_REQUIRE_DEV(lis_xyz);
+  NAT_REQUIRE_DEV(p_out);
+  const int n_modes = src->n_modes;
+  Plan pl = make_plan(prec, src->n_src, n_modes, n_lis);
+  nat::Carver c(ws);
+  void* rec;
+  float* kf;
+  double* kd;
+  double2* part;
+  size_t need = plan_ws(pl, n_modes, n_lis, c, &rec, &kf, &kd, &part);
+  if (ws_bytes < need) return nat::fail(NAT_ERR_WORKSPACE, "workspace %zu < %zu", ws_bytes, need);
+  NAT_REQUIRE_DEV(ws);
+  cudaStream_t s = (cudaStream_t)stream;
+
+  // wavenumbers -> device (padded with zeros)
+  int nk = pl.n_mchunk * pl.MB;
+  std::string hbuf(nk * (sizeof(float) + sizeof(double)), '\0');
+  float* hkf = reinterpret_cast<float*>(&hbuf[0]);
+  double* hkd = reinterpret_cast<double*>(&hbuf[nk * sizeof(float)]);
+  for (int m = 0; m < nk; ++m) {
+    hkd[m] = m < n_modes ? k[m] : 0.0;
+    hkf[m] = (float)hkd[m];
+  }
+  NAT_CUDA_TRY(cudaMemcpyAsync(kf, hkf, nk * sizeof(float), cudaMemcpyHostToDevice, s));
+  NAT_CUDA_TRY(cudaMemcpyAsync(kd, hkd, nk * sizeof(double), cudaMemcpyHostToDevice, s));
+
+  const double cx = src->center[0], cy = src->center[1], cz = src->center[2];
+  unsigned sblocks = (unsigned)((pl.n_src_pad + 255) / 256);
+  if (pl.fp64)
+    stage_kernel<double><<<sblocks, 256, 0, s>>>(src->n_src, pl.n_src_pad, pl.NF, pl.MB, pl.n_mchunk,
+        src->xyz, src->nrm, src->w, (const double2*)src->p, (const double2*)src->g, kd, n_modes,
+        cx, cy, cz, (double*)rec);
+  else
+    stage_kernel<float><<<sblocks, 256, 0, s>>>(src->n_src, pl.n_src_pad, pl.NF, pl.MB, pl.n_mchunk,
+        src->xyz, src->nrm, src->w, (const double2*)src->p, (const double2*)src->g, kd, n_modes,
+        cx, cy, cz, (float*)rec);
+  NAT_LAUNCH_CHECK();
+
+  RadParams prm{};
+  prm.rec = rec;
+  prm.n_src_pad = pl.n_src_pad;
+  prm.n_tiles = pl.n_tiles;
+  prm.chunk_tiles = pl.chunk_tiles;
+  prm.lis = lis_xyz;
+  prm.n_lis = n_lis;
+  prm.cx = cx;
+  prm.cy = cy;
+  prm.cz = cz;
+  prm.kf = kf;
+  prm.kd = kd;
+  prm.out = pl.n_split > 1 ? part : (double2*)p_out;
+  prm.n_modes = n_modes;
+
+  cudaError_t e = cudaSuccess;
+  if (pl.fp64) {
+    auto kern = radiate_f64_kernel<2>;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
+    if (e == cudaSuccess) {
+      dim3 grid((unsigned)pl.tgt_tiles, (unsigned)pl.n_split, (unsigned)pl.n_mchunk);
+      kern<<<grid, kThreads, pl.smem, s>>>(prm);
+      e = cudaGetLastError();
+    }
+  } else {
+    switch (pl.MB) {
+      case 1: e = launch_f32<4, 1>(pl, prm, s); break;
+      case 2: e = launch_f32<4, 2>(pl, prm, s); break;
+      case 3: e = launch_f32<4, 3>(pl, prm, s); break;
+      default: e = launch_f32<4, 4>(pl, prm, s); break;
+    }
+  }
+  if (e != cudaSuccess) return nat::fail(NAT_ERR_CUDA, "radiate launch: %s", cudaGetErrorString(e));
+  if (pl.n_split > 1) {
+    int64_t n = (int64_t)n_modes * n_lis;
+    reduce_splits_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(part, pl.n_split, n,
+                                                                      (double2*)p_out);
+    NAT_LAUNCH_CHECK();
+  }
+  return NAT_OK;
+}
+
+namespace {
+// Barycentric rules for the radiation sources (the library's own tables).
+bool rad_rule(int q, double* lam, double* w) {
+  switch (q) {
+    case 1:
+      lam[0] = lam[1] = lam[2] = 1.0 / 3.0;
+      w[0] = 1.0;
+      return true;
+    case 3: {
+      const double a = 2.0 / 3.0, b = 1.0 / 6.0;
+      double L[9] = {a, b, b, b, a, b, b, b, a};
+      for (int i = 0; i < 9; ++i) lam[i] = L[i];
+      w[0] = w[1] = w[2] = 1.0 / 3.0;
+      return true;
+    }
+    default:
+      return false;
+  }
+}
+}  // namespace
+
+extern "C" nat_status nat_bem_sources(const nat_mesh* mesh, const nat_geom* geom, int q_rad,
+                                      int n_modes, const void* p_tri, const void* g_tri, double* xyz,
+                                      double* nrm, double* w, void* p_src, void* g_src,
+                                      nat_stream_t stream) {
+  NAT_REQUIRE(mesh && geom, "mesh and geom must be non-null");
+  if (q_rad == 0) q_rad = 3;
+  double lam[9], wq[3];
+  NAT_REQUIRE(rad_rule(q_rad, lam, wq), "q_rad must be 1 or 3 (got %d)", q_rad);
+  NAT_REQUIRE(n_modes >= 1, "n_modes must be >= 1");
+  NAT_REQUIRE_DEV(mesh->vxyz);
+  NAT_REQUIRE_DEV(mesh->tri);
+  NAT_REQUIRE_DEV(geom->normal);
+  NAT_REQUIRE_DEV(geom->area);
+  NAT_REQUIRE_DEV(p_tri);
+  NAT_REQUIRE_DEV(g_tri);
+  NAT_REQUIRE_DEV(xyz);
+  NAT_REQUIRE_DEV(nrm);
+  NAT_REQUIRE_DEV(w);
+  NAT_REQUIRE_DEV(p_src);
+  NAT_REQUIRE_DEV(g_src);
+  cudaStream_t s = (cudaStream_t)stream;
+  RuleQ rq{};
+  rq.Q = q_rad;
+  for (int i = 0; i < 3 * q_rad; ++i) rq.lam[i] = lam[i];
+  for (int i = 0; i < q_rad; ++i) rq.w[i] = wq[i];
+  int64_t S = mesh->n_tri * q_rad;
+  bem_sources_kernel<<<(unsigned)((S + 255) / 256), 256, 0, s>>>(
+      mesh->n_vert, mesh->n_tri, mesh->vxyz, mesh->tri, geom->normal, geom->area, rq, n_modes, (const double2*)p_tri, (const double2*)g_tri, xyz, nrm, w,
+      (double2*)p_src, (double2*)g_src);
+  NAT_LAUNCH_CHECK();
+  return NAT_OK;
+}
+
+extern "C" nat_status nat_mc_sources(int64_t M, const double* samples, double total_area, double* xyz,
+                                     double* nrm, double* w, nat_stream_t stream) {
+  NAT_REQUIRE(M >= 1 && total_area > 0, "need M >= 1 and total_area > 0");
+  NAT_REQUIRE_DEV(samples);
+  NAT_REQUIRE_DEV(xyz);
+  NAT_REQUIRE_DEV(nrm);
+  NAT_REQUIRE_DEV(w);
+  mc_sources_kernel<<<(unsigned)((M + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      M, samples, total_area / (double)M, xyz, nrm, w);
+  NAT_LAUNCH_CHECK();
+  return NAT_OK;
+}

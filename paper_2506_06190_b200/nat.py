@@ -1,0 +1,312 @@
+"""Thin ctypes binding of libnat (include/nat.h).  Argument marshalling only: every step
+of the hot path runs in the library's CUDA kernels.  torch supplies device memory and
+streams.  There is no fallback: if libnat.so is missing or the device is not a CUDA
+device, the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+import os
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libnat.so")
+
+NAT_OK, NAT_WARN_NOT_CONVERGED = 0, 1
+NAT_FP32, NAT_FP64 = 0, 1
+STATUS_NAMES = {0: "NAT_OK", 1: "NAT_WARN_NOT_CONVERGED", -1: "NAT_ERR_INVALID_ARG",
+                -2: "NAT_ERR_CUDA", -3: "NAT_ERR_NCCL", -4: "NAT_ERR_SINGULAR",
+                -5: "NAT_ERR_NUMERIC", -6: "NAT_ERR_WORKSPACE"}
+
+
+class NatError(RuntimeError):
+    def __init__(self, status: int, message: str):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {message}")
+        self.status = status
+
+
+class _Mesh(C.Structure):
+    _fields_ = [("n_vert", C.c_int64), ("n_tri", C.c_int64), ("vxyz", C.c_void_p),
+                ("tri", C.c_void_p)]
+
+
+class _Geom(C.Structure):
+    _fields_ = [("n_tri", C.c_int64), ("centroid", C.c_void_p), ("normal", C.c_void_p),
+                ("area", C.c_void_p), ("diam", C.c_void_p), ("area_cdf", C.c_void_p),
+                ("total_area", C.c_double), ("center", C.c_double * 3),
+                ("bound_radius", C.c_double), ("volume", C.c_double)]
+
+
+class _QuadOpts(C.Structure):
+    _fields_ = [("far_pts", C.c_int), ("near_levels_S", C.c_int), ("near_levels_N", C.c_int),
+                ("near_eta", C.c_double), ("self_theta_pts", C.c_int)]
+
+
+class _SolveInfo(C.Structure):
+    _fields_ = [("iters", C.c_int), ("converged", C.c_int), ("rel_residual", C.c_double),
+                ("t_total_s", C.c_double), ("t_matvec_s", C.c_double), ("t_comm_s", C.c_double)]
+
+
+class _McOpts(C.Structure):
+    _fields_ = [("M", C.c_int64), ("seed", C.c_uint64), ("stream_id", C.c_uint64),
+                ("eps", C.c_double), ("samples_in", C.c_void_p), ("sample_tri_in", C.c_void_p)]
+
+
+class _Sources(C.Structure):
+    _fields_ = [("n_src", C.c_int64), ("xyz", C.c_void_p), ("nrm", C.c_void_p),
+                ("w", C.c_void_p), ("n_modes", C.c_int), ("p", C.c_void_p), ("g", C.c_void_p),
+                ("center", C.c_double * 3)]
+
+
+_P = C.c_void_p
+_I64 = C.c_int64
+_D = C.c_double
+_SZ = C.c_size_t
+# name -> (restype, argtypes)
+_SIGS = {
+    "nat_abi_version": (C.c_int, []),
+    "nat_last_error": (C.c_char_p, []),
+    "nat_mesh_prepare_workspace": (_SZ, [_I64, _I64]),
+    "nat_mesh_prepare": (C.c_int, [C.POINTER(_Mesh), C.POINTER(_Geom), _P, _SZ, _P]),
+    "nat_bem_near_count": (C.c_int, [C.POINTER(_Mesh), C.POINTER(_Geom), C.POINTER(_QuadOpts),
+                                     _I64, _I64, _P, C.POINTER(_I64), _P]),
+    "nat_bem_near_build": (C.c_int, [C.POINTER(_Mesh), C.POINTER(_Geom), C.POINTER(_QuadOpts),
+                                     _I64, _I64, _P, _P, _P, _P]),
+    "nat_bem_assemble_workspace": (_SZ, [_I64, _I64, C.c_int]),
+    "nat_bem_assemble": (C.c_int, [C.POINTER(_Mesh), C.POINTER(_Geom), C.POINTER(_QuadOpts),
+                                   _P, _P, _P, _D, C.c_int, _I64, _I64, C.c_int, _P, _P, _I64,
+                                   _P, _P, _SZ, _P]),
+    "nat_bem_matvec": (C.c_int, [C.c_int, _I64, _I64, _P, _I64, _P, _P, _P]),
+    "nat_comm_unique_id": (C.c_int, [_P]),
+    "nat_comm_create_from_id": (C.c_int, [C.POINTER(_P), _P, C.c_int, C.c_int]),
+    "nat_comm_destroy": (C.c_int, [_P]),
+    "nat_bem_solve_workspace": (_SZ, [C.c_int, _I64, _I64, C.c_int]),
+    "nat_bem_solve": (C.c_int, [_P, C.c_int, _I64, _I64, _I64, _P, _I64, _P, _P, _D, C.c_int,
+                                _P, _SZ, C.POINTER(_SolveInfo), _P]),
+    "nat_mc_sample": (C.c_int, [C.POINTER(_Mesh), C.POINTER(_Geom), _I64, C.c_uint64,
+                                C.c_uint64, _P, _P, _P]),
+    "nat_mc_op_workspace": (_SZ, [C.c_int, _I64, C.c_int]),
+    "nat_mc_rhs": (C.c_int, [C.c_int, _I64, _P, C.c_int, C.POINTER(_D), _P, _D, _D, _P, _P,
+                             _SZ, _P]),
+    "nat_mc_apply": (C.c_int, [C.c_int, _I64, _P, C.c_int, C.POINTER(_D), _P, _D, _P, _P, _SZ,
+                               _P]),
+    "nat_mc_check_coincident": (C.c_int, [_I64, _P, C.POINTER(_I64), _P, _SZ, _P]),
+    "nat_mc_workspace": (_SZ, [C.c_int, _I64, C.c_int, C.c_int]),
+    "nat_mc_surface_pressure": (C.c_int, [C.POINTER(_Mesh), C.POINTER(_Geom), C.c_int,
+                                          C.POINTER(_D), _P, C.POINTER(_McOpts), C.c_int, _D,
+                                          C.c_int, _P, _P, _P, _P, _SZ, C.POINTER(_SolveInfo),
+                                          _P]),
+    "nat_bem_sources": (C.c_int, [C.POINTER(_Mesh), C.POINTER(_Geom), C.c_int, C.c_int, _P, _P,
+                                  _P, _P, _P, _P, _P, _P]),
+    "nat_mc_sources": (C.c_int, [_I64, _P, _D, _P, _P, _P, _P]),
+    "nat_radiate_workspace": (_SZ, [C.c_int, _I64, C.c_int, _I64]),
+    "nat_radiate_field": (C.c_int, [C.POINTER(_Sources), C.c_int, C.POINTER(_D), _I64, _P, _P,
+                                    _P, _SZ, _P]),
+    "nat_listener_grid": (C.c_int, [C.POINTER(_D), _D, C.c_int, C.c_int, C.c_int, _D, _D, _P,
+                                    _P]),
+}
+
+_lib = None
+
+
+def lib():
+    """Load libnat.so (raises if absent: there is no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built: run `python -m paper_2506_06190_b200.build`")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def exported_symbols():
+    return list(_SIGS)
+
+
+def _check(status, allow_warn=False):
+    if status == NAT_OK or (allow_warn and status == NAT_WARN_NOT_CONVERGED):
+        return status
+    raise NatError(status, lib().nat_last_error().decode())
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise NatError(-1, "tensor must live on a CUDA device")
+    if not t.is_contiguous():
+        raise NatError(-1, "tensor must be contiguous")
+    return C.c_void_p(t.data_ptr())
+
+
+def _stream():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _ws(nbytes: int, device):
+    return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+
+
+def _prec(prec):
+    if prec in ("fp32", NAT_FP32, torch.float32):
+        return NAT_FP32
+    if prec in ("fp64", NAT_FP64, torch.float64):
+        return NAT_FP64
+    raise ValueError(f"bad precision {prec!r}")
+
+
+# ------------------------------------------------------------------------------------
+# data holders
+# ------------------------------------------------------------------------------------
+@dataclasses.dataclass
+class Mesh:
+    vxyz: torch.Tensor  # (3, V) float64 cuda
+    tri: torch.Tensor   # (3, N) int32 cuda
+
+    @classmethod
+    def from_numpy(cls, v, t, device="cuda"):
+        v = np.ascontiguousarray(np.asarray(v, dtype=np.float64).T)
+        t = np.ascontiguousarray(np.asarray(t, dtype=np.int32).T)
+        return cls(torch.from_numpy(v).to(device), torch.from_numpy(t).to(device))
+
+    @property
+    def n_vert(self):
+        return self.vxyz.shape[1]
+
+    @property
+    def n_tri(self):
+        return self.tri.shape[1]
+
+    def c(self):
+        return _Mesh(self.n_vert, self.n_tri, _ptr(self.vxyz), _ptr(self.tri))
+
+
+@dataclasses.dataclass
+class Geom:
+    centroid: torch.Tensor
+    normal: torch.Tensor
+    area: torch.Tensor
+    diam: torch.Tensor
+    area_cdf: torch.Tensor
+    total_area: float = 0.0
+    center: tuple = (0.0, 0.0, 0.0)
+    bound_radius: float = 0.0
+    volume: float = 0.0
+
+    def c(self):
+        g = _Geom(self.area.shape[0], _ptr(self.centroid), _ptr(self.normal), _ptr(self.area),
+                  _ptr(self.diam), _ptr(self.area_cdf), self.total_area, (C.c_double * 3)(*self.center),
+                  self.bound_radius, self.volume)
+        return g
+
+
+@dataclasses.dataclass
+class Sources:
+    xyz: torch.Tensor     # (3, S) float64
+    nrm: torch.Tensor     # (3, S) float64
+    w: torch.Tensor       # (S,) float64
+    p: torch.Tensor       # (n_modes, S) complex128
+    g: torch.Tensor       # (n_modes, S) complex128
+    center: tuple = (0.0, 0.0, 0.0)
+
+    def c(self):
+        return _Sources(self.xyz.shape[1], _ptr(self.xyz), _ptr(self.nrm), _ptr(self.w),
+                        self.p.shape[0], _ptr(self.p), _ptr(self.g), (C.c_double * 3)(*self.center))
+
+
+def quad_opts(far_pts=0, near_levels_S=0, near_levels_N=0, near_eta=0.0, self_theta_pts=0):
+    return _QuadOpts(far_pts, near_levels_S, near_levels_N, near_eta, self_theta_pts)
+
+
+# ------------------------------------------------------------------------------------
+# calls (same names as the C ABI)
+# ------------------------------------------------------------------------------------
+def nat_abi_version():
+    return lib().nat_abi_version()
+
+
+def nat_mesh_prepare(mesh: Mesh) -> Geom:
+    dev = mesh.vxyz.device
+    n = mesh.n_tri
+    f = dict(dtype=torch.float64, device=dev)
+    geo = Geom(torch.empty(3, n, **f), torch.empty(3, n, **f), torch.empty(n, **f),
+               torch.empty(n, **f), torch.empty(n, **f))
+    cg = geo.c()
+    ws = _ws(lib().nat_mesh_prepare_workspace(mesh.n_vert, n), dev)
+    _check(lib().nat_mesh_prepare(C.byref(mesh.c()), C.byref(cg), _ptr(ws), ws.numel(), _stream()))
+    geo.total_area, geo.center = cg.total_area, tuple(cg.center)
+    geo.bound_radius, geo.volume = cg.bound_radius, cg.volume
+    return geo
+
+
+def nat_listener_grid(center, R, n_theta, n_phi, n_r, r_lo=1.5, r_hi=3.0, device="cuda"):
+    n = n_theta * n_phi * n_r
+    out = torch.empty(3, n, dtype=torch.float64, device=device)
+    c = (C.c_double * 3)(*[float(x) for x in center])
+    _check(lib().nat_listener_grid(c, float(R), n_theta, n_phi, n_r, float(r_lo), float(r_hi),
+                                   _ptr(out), _stream()))
+    return out
+
+
+def nat_bem_sources(mesh: Mesh, geom: Geom, p_tri, g_tri, q_rad=3) -> Sources:
+    dev = mesh.vxyz.device
+    p_tri = torch.atleast_2d(p_tri).to(torch.complex128).contiguous()
+    g_tri = torch.atleast_2d(g_tri).to(torch.complex128).contiguous()
+    nm = p_tri.shape[0]
+    S = mesh.n_tri * q_rad
+    f = dict(dtype=torch.float64, device=dev)
+    src = Sources(torch.empty(3, S, **f), torch.empty(3, S, **f), torch.empty(S, **f),
+                  torch.empty(nm, S, dtype=torch.complex128, device=dev),
+                  torch.empty(nm, S, dtype=torch.complex128, device=dev), tuple(geom.center))
+    _check(lib().nat_bem_sources(C.byref(mesh.c()), C.byref(geom.c()), q_rad, nm, _ptr(p_tri),
+                                 _ptr(g_tri), _ptr(src.xyz), _ptr(src.nrm), _ptr(src.w),
+                                 _ptr(src.p), _ptr(src.g), _stream()))
+    return src
+
+
+def nat_mc_sources(samples, total_area, p, g, center=(0.0, 0.0, 0.0)) -> Sources:
+    dev = samples.device
+    M = samples.shape[1]
+    f = dict(dtype=torch.float64, device=dev)
+    src = Sources(torch.empty(3, M, **f), torch.empty(3, M, **f), torch.empty(M, **f),
+                  torch.atleast_2d(p).to(torch.complex128).contiguous(),
+                  torch.atleast_2d(g).to(torch.complex128).contiguous(), tuple(center))
+    _check(lib().nat_mc_sources(M, _ptr(samples), float(total_area), _ptr(src.xyz), _ptr(src.nrm),
+                                _ptr(src.w), _stream()))
+    return src
+
+
+class RadiatePlan:
+    """Pre-sized workspace for repeated nat_radiate_field calls (bench / serving loop)."""
+
+    def __init__(self, n_src, n_modes, n_lis, prec="fp32", device="cuda"):
+        self.prec = _prec(prec)
+        self.ws = _ws(lib().nat_radiate_workspace(self.prec, n_src, n_modes, n_lis), device)
+
+
+def nat_radiate_field(src: Sources, k: Sequence[float], lis_xyz: torch.Tensor, prec="fp32",
+                      out: Optional[torch.Tensor] = None, plan: Optional[RadiatePlan] = None):
+    pr = _prec(prec)
+    nm = src.p.shape[0]
+    k = np.ascontiguousarray(np.atleast_1d(np.asarray(k, dtype=np.float64)))
+    if k.size != nm:
+        raise NatError(-1, f"{k.size} wavenumbers for {nm} modes")
+    n_lis = lis_xyz.shape[1]
+    dev = lis_xyz.device
+    if out is None:
+        out = torch.empty(nm, n_lis, dtype=torch.complex128, device=dev)
+    ws = plan.ws if plan is not None else _ws(
+        lib().nat_radiate_workspace(pr, src.xyz.shape[1], nm, n_lis), dev)
+    _check(lib().nat_radiate_field(C.byref(src.c()), pr, k.ctypes.data_as(C.POINTER(C.c_double)),
+                                   n_lis, _ptr(lis_xyz), _ptr(out), _ptr(ws), ws.numel(),
+                                   _stream()))
+    return out

@@ -1,0 +1,97 @@
+"""Row a11 (radiation): CUDA path vs the fp64 oracle, element by element.
+
+Tolerances: relative L2 <= 1e-4 (fp32 path) and <= 1e-10 (fp64 path), the north-star
+acceptance (BASELINE.json)."""
+import numpy as np
+import pytest
+import torch
+
+import nat_inputs as I
+from gpu_util import rel_l2, requires_cuda, soa_to_aos, to_np
+from oracle import geometry, radiate
+
+pytestmark = [pytest.mark.gpu, requires_cuda]
+
+
+def _nat():
+    from paper_2506_06190_b200 import nat
+    return nat
+
+
+def _setup(m, n_modes, seed):
+    nat = _nat()
+    ref_geo = geometry.mesh_prepare(m.v, m.t)
+    mesh = nat.Mesh.from_numpy(m.v, m.t)
+    geo = nat.nat_mesh_prepare(mesh)
+    p = I.random_complex((n_modes, m.n_tri), seed)
+    g = I.random_complex((n_modes, m.n_tri), seed + 1)
+    src = nat.nat_bem_sources(mesh, geo, torch.from_numpy(p).cuda(), torch.from_numpy(g).cuda())
+    ref_src = radiate.bem_sources(m.v, m.t, ref_geo, p, g)
+    return nat, src, ref_src, ref_geo
+
+
+def test_bem_sources_bitwise():
+    m = I.icosphere(2)
+    nat, src, ref, _ = _setup(m, 2, 3)
+    assert np.array_equal(soa_to_aos(src.xyz), ref[0])
+    assert np.array_equal(soa_to_aos(src.nrm), ref[1])
+    assert np.array_equal(to_np(src.w), ref[2])
+    assert np.array_equal(to_np(src.p), ref[3])
+    assert np.array_equal(to_np(src.g), ref[4])
+
+
+@pytest.mark.parametrize("prec,tol", [("fp32", 1e-4), ("fp64", 1e-10)])
+@pytest.mark.parametrize("n_modes", [1, 2, 3, 5, 8])
+def test_radiate_parity_multimode(prec, tol, n_modes):
+    m = I.icosphere(2)                       # 320 tri -> 960 sources (ragged vs tiles)
+    nat, src, ref_src, geo = _setup(m, n_modes, 10 + n_modes)
+    ks = list(np.linspace(0.3, 9.0, n_modes))
+    x = I.random_points_in_shell(1500, 1.5, 3.0, seed=4)   # ragged vs 1024-target tiles
+    xt = torch.from_numpy(np.ascontiguousarray(x.T)).cuda()
+    out = to_np(nat.nat_radiate_field(src, ks, xt, prec=prec))
+    ref = radiate.radiate(ref_src, ks, x)
+    for mode in range(n_modes):
+        assert rel_l2(out[mode], ref[mode]) <= tol, (mode, rel_l2(out[mode], ref[mode]))
+
+
+@pytest.mark.parametrize("prec,tol", [("fp32", 1e-4), ("fp64", 1e-10)])
+def test_radiate_edge_sizes(prec, tol):
+    nat = _nat()
+    # one source, one listener; and one listener against many sources
+    for n_src, n_lis in ((1, 1), (1, 3000), (5000, 1), (129, 257)):
+        rng = np.random.default_rng(n_src + n_lis)
+        y = rng.normal(size=(n_src, 3))
+        nrm = rng.normal(size=(n_src, 3))
+        nrm /= np.linalg.norm(nrm, axis=1, keepdims=True)
+        w = rng.uniform(0.1, 1.0, n_src)
+        p = I.random_complex((1, n_src), 1)
+        g = I.random_complex((1, n_src), 2)
+        x = I.random_points_in_shell(n_lis, 4.0, 6.0, seed=5)
+        T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+        src = nat.Sources(T(y.T), T(nrm.T), T(w), T(p), T(g))
+        out = to_np(nat.nat_radiate_field(src, [2.5], T(x.T), prec=prec))
+        ref = radiate.radiate((y, nrm, w, p, g), [2.5], x)
+        assert rel_l2(out, ref) <= tol, (n_src, n_lis)
+
+
+def test_radiate_full_c2_size_sampled():
+    """C2 launch configuration (20480 tri -> 61440 sources, 32^3 listeners, ka = 8),
+    compared on 256 sampled listeners."""
+    nat = _nat()
+    m = I.icosphere(5)
+    nat_, src, ref_src, geo = _setup(m, 1, 77)
+    lis = nat.nat_listener_grid((0, 0, 0), 1.0, 32, 32, 32)
+    out = to_np(nat.nat_radiate_field(src, [8.0], lis, prec="fp32"))[0]
+    idx = np.random.default_rng(0).choice(lis.shape[1], 256, replace=False)
+    x = soa_to_aos(lis)[idx]
+    ref = radiate.radiate(ref_src, [8.0], x)[0]
+    assert rel_l2(out[idx], ref) <= 1e-4
+
+
+def test_radiate_deterministic():
+    m = I.icosphere(3)
+    nat, src, _, _ = _setup(m, 1, 5)
+    lis = nat.nat_listener_grid((0, 0, 0), 1.0, 16, 16, 4)
+    a = nat.nat_radiate_field(src, [3.0], lis)
+    b = nat.nat_radiate_field(src, [3.0], lis)
+    assert torch.equal(a, b)
