@@ -121,7 +121,7 @@ nat_status nat_bem_near_build(const nat_mesh* mesh, const nat_geom* geom, const 
  * A: row-major [rows][lda], c64 (NAT_FP32) or c128 (NAT_FP64).  g: c128 [n_rhs][n_tri]
  * (may be NULL iff n_rhs == 0).  rhs: c128 [n_rhs][rows].  k >= 0 finite.
  * ------------------------------------------------------------------------------- */
-size_t nat_bem_assemble_workspace(int64_t n_tri, int64_t rows, int n_rhs);
+size_t nat_bem_assemble_workspace(int64_t n_tri, int64_t rows, int64_t nnz, int n_rhs); /* nnz from near_count */
 nat_status nat_bem_assemble(const nat_mesh* mesh, const nat_geom* geom, const nat_quad_opts* opts,
                             const int64_t* near_row_ptr, const int32_t* near_col,
                             const uint8_t* near_cls, double k, nat_prec prec, int64_t row_begin,
@@ -148,7 +148,9 @@ nat_status nat_comm_destroy(nat_comm* comm);
  * a7 — unrestarted GMRES (tol 1e-6, max 200; reading R-gmres) on the
  * row-sharded system: this rank owns rows [row_begin, row_end) of A (A_local, b_local);
  * each iteration = local matvec -> all-gather of the iterate (NCCL) -> replicated
- * Arnoldi (CGS2, deterministic reductions).  x0 = 0.  x: c128 [n] out, identical on
+ * Arnoldi (CGS2, deterministic reductions).  x0 = 0.  Row ownership is fixed:
+ * rows_per_rank = ceil(n / world), row_begin = rank * rows_per_rank,
+ * row_end = min(n, row_begin + rows_per_rank); comm == NULL means world = 1.  x: c128 [n] out, identical on
  * all ranks.  tol <= 0 => 1e-6, max_iter <= 0 => 200.  Returns NAT_OK or
  * NAT_WARN_NOT_CONVERGED; info->rel_residual is the true ||b - A x|| / ||b||.
  * ------------------------------------------------------------------------------- */

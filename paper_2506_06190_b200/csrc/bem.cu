@@ -1,0 +1,856 @@
+// Rows a4 + a5 — dense collocation assembly of the conventional BIE and a6 — the
+// stored-matrix matvec.
+//
+// Equation: Eq. BM with beta = 0 ("i.e., beta = 0" P:191), outward normals
+// (reading R-sign): 1/2 p(x) - int p dG/dn_y = - int g G.  P0 collocation at centroids
+// (reading R-colloc): A = 1/2 I - K, b = -V g,
+//   K_ij = int_{T_j} dG/dn_y(c_i, y) dS,  V_ij = int_{T_j} G(c_i, y) dS.
+// Quadrature by pair class ("adjacent or identical elements"): far rule on every
+// pair (a4, fused with the row reduction of b so V is never stored), then the near and
+// self kernels (a5) overwrite the near entries of A and correct b in a fixed order.
+//
+// B200 mapping: far kernel CTA = 16 rows x 1024 columns, one column per
+// thread per pass (its 3 quadrature points, weights and normal in registers), the
+// 16 collocation points broadcast from shared memory; every warp stores 32 consecutive
+// entries of a row (coalesced 256 B / 512 B); the RHS partial sums stay in registers
+// and are reduced once per CTA (warp shuffles, then a fixed-order shared-memory sum).
+// Near pairs: one 32-lane group per vertex-sharing pair (448 points), one 8-lane group
+// per close pair (28 points), fp64 point positions and differences, kernel math in the
+// path's precision.  Self term: one thread per row, polar Gauss-Legendre in fp64.
+#include <cmath>
+#include <vector>
+
+#include "nat_internal.cuh"
+#include "pair.cuh"
+
+namespace {
+
+using nat::C2;
+
+constexpr int kThreads = 256;
+constexpr int kTI = 16;       // rows per far CTA
+constexpr int kCC = 4;        // column passes per far CTA (columns = 256 * kCC)
+constexpr int kMaxFarQ = 7;
+constexpr int kNRmax = 2;
+
+// ------------------------------------------------------------------------------------
+// quadrature tables (the library's own host code; DESIGN.md §3 R-colloc / R-self)
+// ------------------------------------------------------------------------------------
+struct Pt {
+  double l1, l2, l3, w;
+};
+
+bool base_rule(int npts, std::vector<Pt>& out) {
+  out.clear();
+  if (npts == 1) {
+    out.push_back({1.0 / 3, 1.0 / 3, 1.0 / 3, 1.0});
+  } else if (npts == 3) {
+    const double a = 2.0 / 3, b = 1.0 / 6;
+    out = {{a, b, b, 1.0 / 3}, {b, a, b, 1.0 / 3}, {b, b, a, 1.0 / 3}};
+  } else if (npts == 6) {  // Dunavant degree 4
+    const double a1 = 0.10810301816807023, b1 = 0.44594849091596489, w1 = 0.22338158967801147;
+    const double a2 = 0.81684757298045851, b2 = 0.091576213509770743, w2 = 0.10995174365532187;
+    out = {{a1, b1, b1, w1}, {b1, a1, b1, w1}, {b1, b1, a1, w1},
+           {a2, b2, b2, w2}, {b2, a2, b2, w2}, {b2, b2, a2, w2}};
+  } else if (npts == 7) {  // Radon degree 5
+    const double s15 = std::sqrt(15.0);
+    const double ap = (6 + s15) / 21, am = (6 - s15) / 21;
+    const double wp = (155 + s15) / 1200, wm = (155 - s15) / 1200;
+    out.push_back({1.0 / 3, 1.0 / 3, 1.0 / 3, 9.0 / 40});
+    for (int s = 0; s < 2; ++s) {
+      double a = s == 0 ? ap : am, w = s == 0 ? wp : wm, b = 1 - 2 * a;
+      out.push_back({b, a, a, w});
+      out.push_back({a, b, a, w});
+      out.push_back({a, a, b, w});
+    }
+  } else {
+    return false;
+  }
+  return true;
+}
+
+struct Bary {
+  double p[3][3];
+};
+
+void subdivide(const Bary& t, int level, std::vector<Bary>& out) {
+  if (level == 0) {
+    out.push_back(t);
+    return;
+  }
+  Bary c[4];
+  double m12[3], m13[3], m23[3];
+  for (int a = 0; a < 3; ++a) {
+    m12[a] = (t.p[0][a] + t.p[1][a]) / 2;
+    m13[a] = (t.p[0][a] + t.p[2][a]) / 2;
+    m23[a] = (t.p[1][a] + t.p[2][a]) / 2;
+  }
+  for (int a = 0; a < 3; ++a) {
+    c[0].p[0][a] = t.p[0][a]; c[0].p[1][a] = m12[a];    c[0].p[2][a] = m13[a];
+    c[1].p[0][a] = m12[a];    c[1].p[1][a] = t.p[1][a]; c[1].p[2][a] = m23[a];
+    c[2].p[0][a] = m13[a];    c[2].p[1][a] = m23[a];    c[2].p[2][a] = t.p[2][a];
+    c[3].p[0][a] = m12[a];    c[3].p[1][a] = m23[a];    c[3].p[2][a] = m13[a];
+  }
+  for (auto& ch : c) subdivide(ch, level - 1, out);
+}
+
+void composite_rule(int level, std::vector<Pt>& out) {
+  std::vector<Pt> base;
+  base_rule(7, base);
+  std::vector<Bary> subs;
+  Bary root{{{1, 0, 0}, {0, 1, 0}, {0, 0, 1}}};
+  subdivide(root, level, subs);
+  out.clear();
+  const double scale = 1.0 / (double)subs.size();
+  for (auto& s : subs)
+    for (auto& q : base) {
+      Pt p;
+      double l[3];
+      for (int a = 0; a < 3; ++a) l[a] = q.l1 * s.p[0][a] + q.l2 * s.p[1][a] + q.l3 * s.p[2][a];
+      p.l1 = l[0];
+      p.l2 = l[1];
+      p.l3 = l[2];
+      p.w = q.w * scale;
+      out.push_back(p);
+    }
+}
+
+// Gauss-Legendre nodes/weights on [-1, 1] by Newton iteration on P_n.
+void gauss_legendre(int n, std::vector<double>& x, std::vector<double>& w) {
+  x.assign(n, 0.0);
+  w.assign(n, 0.0);
+  for (int i = 0; i < (n + 1) / 2; ++i) {
+    double z = std::cos(nat::kPi * (i + 0.75) / (n + 0.5)), pp = 0;
+    for (int it = 0; it < 100; ++it) {
+      double p1 = 1, p2 = 0;
+      for (int j = 1; j <= n; ++j) {
+        double p3 = p2;
+        p2 = p1;
+        p1 = ((2.0 * j - 1) * z * p2 - (j - 1.0) * p3) / j;
+      }
+      pp = n * (z * p1 - p2) / (z * z - 1);
+      double dz = p1 / pp;
+      z -= dz;
+      if (std::fabs(dz) < 1e-17) break;
+    }
+    x[i] = -z;
+    x[n - 1 - i] = z;
+    w[i] = w[n - 1 - i] = 2.0 / ((1 - z * z) * pp * pp);
+  }
+}
+
+struct Opts {
+  int far_pts, lev_S, lev_N, gl;
+  double eta;
+};
+
+Opts opts_of(const nat_quad_opts* o) {
+  Opts r{3, 3, 1, 16, 4.0};
+  if (o) {
+    if (o->far_pts) r.far_pts = o->far_pts;
+    if (o->near_levels_S) r.lev_S = o->near_levels_S;
+    if (o->near_levels_N) r.lev_N = o->near_levels_N;
+    if (o->self_theta_pts) r.gl = o->self_theta_pts;
+    if (o->near_eta > 0) r.eta = o->near_eta;
+  }
+  return r;
+}
+
+// ------------------------------------------------------------------------------------
+// kernels
+// ------------------------------------------------------------------------------------
+template <typename R>
+struct FarCols {        // per column j: NQ points (relative to centre), weights, normal
+  const R* qxyz;        // [NQ][3][n]
+  const R* qw;          // [NQ][n]  (omega_q A_j / 4pi)
+  const R* nrm;         // [3][n]
+};
+
+template <typename R>
+__global__ void far_prep_kernel(int64_t nv, int64_t n, const double* __restrict__ vx,
+                                const int32_t* __restrict__ tri, const double* __restrict__ nrm,
+                                const double* __restrict__ area, const double4* __restrict__ rule,
+                                int NQ, double cx, double cy, double cz, R* __restrict__ qxyz,
+                                R* __restrict__ qw, R* __restrict__ nout) {
+  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  int a = tri[j], b = tri[n + j], c = tri[2 * n + j];
+  const double cen[3] = {cx, cy, cz};
+  for (int q = 0; q < NQ; ++q) {
+    double4 L = rule[q];
+    for (int d = 0; d < 3; ++d) {
+      const double* X = vx + d * nv;
+      double y = (L.x * X[a] + L.y * X[b]) + L.z * X[c];
+      qxyz[((size_t)q * 3 + d) * n + j] = (R)(y - cen[d]);
+    }
+    qw[(size_t)q * n + j] = (R)(L.w * area[j] * nat::kInv4Pi);
+  }
+  for (int d = 0; d < 3; ++d) nout[(size_t)d * n + j] = (R)nrm[(size_t)d * n + j];
+}
+
+template <typename R, int NQ>
+__device__ __forceinline__ void far_entry(const R (&y)[NQ][3], const R (&w)[NQ], R nx, R ny, R nz,
+                                          R cx, R cy, R cz, R k, R& Vr, R& Vi, R& Kr, R& Ki) {
+  Vr = Vi = Kr = Ki = R(0);
+#pragma unroll
+  for (int q = 0; q < NQ; ++q)
+    nat::pair_accumulate<R>(y[q][0] - cx, y[q][1] - cy, y[q][2] - cz, nx, ny, nz, w[q], k, Vr, Vi,
+                            Kr, Ki);
+}
+
+template <typename R>
+__device__ __forceinline__ void store_entry(void* A, size_t idx, R re, R im) {
+  if constexpr (sizeof(R) == 4)
+    reinterpret_cast<float2*>(A)[idx] = make_float2(re, im);
+  else
+    reinterpret_cast<double2*>(A)[idx] = make_double2(re, im);
+}
+
+template <typename R>
+struct FarArgs {
+  int64_t n, row_begin, rows, lda;
+  FarCols<R> cols;
+  const double* cen;     // geom centroid [3][n]
+  double cx, cy, cz;
+  R k;
+  int n_rhs, rhs0;       // this pass covers rhs [rhs0, rhs0 + NR)
+  const double2* g;      // [n_rhs][n]
+  void* A;
+  bool store_A;
+  double2* bpart;        // [n_colblk][n_rhs][rows]
+};
+
+template <typename R, int NQ, int NR>
+__global__ void __launch_bounds__(kThreads) far_kernel(FarArgs<R> a) {
+  __shared__ R s_c[3][kTI];
+  __shared__ double2 s_red[kThreads / 32][kTI][NR > 0 ? NR : 1];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t i0 = (int64_t)blockIdx.y * kTI;
+  const int64_t n = a.n;
+  if (tid < kTI) {
+    int64_t r = i0 + tid;
+    int64_t i = a.row_begin + (r < a.rows ? r : 0);
+    s_c[0][tid] = (R)(a.cen[i] - a.cx);
+    s_c[1][tid] = (R)(a.cen[n + i] - a.cy);
+    s_c[2][tid] = (R)(a.cen[2 * n + i] - a.cz);
+  }
+  __syncthreads();
+  const int nrows = (int)nat::min64(kTI, a.rows - i0);
+  C2<R> bacc[kTI][NR > 0 ? NR : 1];
+#pragma unroll
+  for (int t = 0; t < kTI; ++t)
+#pragma unroll
+    for (int q = 0; q < (NR > 0 ? NR : 1); ++q) bacc[t][q] = {R(0), R(0)};
+
+  for (int cc = 0; cc < kCC; ++cc) {
+    const int64_t j = (int64_t)blockIdx.x * (kThreads * kCC) + cc * kThreads + tid;
+    const bool valid = j < n;
+    const int64_t jj = valid ? j : 0;
+    R y[NQ][3], w[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      y[q][0] = a.cols.qxyz[((size_t)q * 3 + 0) * n + jj];
+      y[q][1] = a.cols.qxyz[((size_t)q * 3 + 1) * n + jj];
+      y[q][2] = a.cols.qxyz[((size_t)q * 3 + 2) * n + jj];
+      w[q] = valid ? a.cols.qw[(size_t)q * n + jj] : R(0);
+    }
+    const R nx = a.cols.nrm[jj], ny = a.cols.nrm[n + jj], nz = a.cols.nrm[2 * n + jj];
+    C2<R> gj[NR > 0 ? NR : 1];
+#pragma unroll
+    for (int q = 0; q < NR; ++q) {
+      double2 gv = valid ? a.g[(size_t)(a.rhs0 + q) * n + jj] : make_double2(0.0, 0.0);
+      gj[q] = {(R)gv.x, (R)gv.y};
+    }
+#pragma unroll
+    for (int t = 0; t < kTI; ++t) {
+      if (t < nrows) {
+        R Vr, Vi, Kr, Ki;
+        far_entry<R, NQ>(y, w, nx, ny, nz, s_c[0][t], s_c[1][t], s_c[2][t], a.k, Vr, Vi, Kr, Ki);
+        if (a.store_A && valid) store_entry<R>(a.A, (size_t)(i0 + t) * a.lda + j, -Kr, -Ki);
+#pragma unroll
+        for (int q = 0; q < NR; ++q) {
+          bacc[t][q].x += Vr * gj[q].x - Vi * gj[q].y;
+          bacc[t][q].y += Vr * gj[q].y + Vi * gj[q].x;
+        }
+      }
+    }
+  }
+  if constexpr (NR > 0) {
+#pragma unroll
+    for (int t = 0; t < kTI; ++t)
+#pragma unroll
+      for (int q = 0; q < NR; ++q) {
+        double vx = (double)bacc[t][q].x, vy = (double)bacc[t][q].y;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          vx += __shfl_xor_sync(0xffffffffu, vx, o);
+          vy += __shfl_xor_sync(0xffffffffu, vy, o);
+        }
+        if (lane == 0) s_red[warp][t][q] = make_double2(vx, vy);
+      }
+    __syncthreads();
+    if (tid < kTI * NR) {
+      const int t = tid / NR, q = tid % NR;
+      if (t < nrows) {
+        double2 s = s_red[0][t][q];
+        for (int wv = 1; wv < kThreads / 32; ++wv) {
+          s.x += s_red[wv][t][q].x;
+          s.y += s_red[wv][t][q].y;
+        }
+        // b = -V g
+        a.bpart[((size_t)blockIdx.x * a.n_rhs + a.rhs0 + q) * a.rows + i0 + t] = make_double2(-s.x, -s.y);
+      }
+    }
+  }
+}
+
+template <typename R>
+struct NearArgs {
+  int64_t n, nv, row_begin, rows, lda, nnz;
+  const int64_t* row_ptr;
+  const int32_t* col;
+  const uint8_t* cls;
+  const int32_t* rowidx;   // [nnz] row of each entry
+  const double* vx;
+  const int32_t* tri;
+  const double* cen;
+  const double* nrm;
+  const double* area;
+  const double4* rule;     // near rule points (parent barycentrics, weight)
+  int npts;
+  FarCols<R> cols;         // far rule (to subtract the far contribution from b)
+  double cx, cy, cz;
+  R k;
+  int n_rhs;
+  const double2* g;
+  void* A;
+  double2* corr;           // [nnz][n_rhs]
+};
+
+template <typename R, int NQ, int G, int CLS>
+__global__ void __launch_bounds__(kThreads) near_kernel(NearArgs<R> a) {
+  const int64_t gid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
+  const int lig = threadIdx.x % G;
+  if (gid >= a.nnz) return;
+  const int64_t e = gid;
+  if (a.cls[e] != CLS) return;  // uniform within the group
+  const int64_t r = a.rowidx[e];
+  const int64_t i = a.row_begin + r;
+  const int64_t j = a.col[e];
+  const int64_t n = a.n;
+  const double ci[3] = {a.cen[i], a.cen[n + i], a.cen[2 * n + i]};
+  const int vid[3] = {a.tri[j], a.tri[n + j], a.tri[2 * n + j]};
+  double v[3][3];
+#pragma unroll
+  for (int p = 0; p < 3; ++p)
+#pragma unroll
+    for (int d = 0; d < 3; ++d) v[p][d] = a.vx[d * a.nv + vid[p]];
+  const R nx = (R)a.nrm[j], ny = (R)a.nrm[n + j], nz = (R)a.nrm[2 * n + j];
+  const double wA = a.area[j] * nat::kInv4Pi;
+  R Vr = 0, Vi = 0, Kr = 0, Ki = 0;
+  for (int q = lig; q < a.npts; q += G) {
+    const double4 L = a.rule[q];
+    R d[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) d[c] = (R)(((L.x * v[0][c] + L.y * v[1][c]) + L.z * v[2][c]) - ci[c]);
+    nat::pair_accumulate<R>(d[0], d[1], d[2], nx, ny, nz, (R)(L.w * wA), a.k, Vr, Vi, Kr, Ki);
+  }
+  const unsigned mask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << ((threadIdx.x & 31) / G * G));
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) {
+    Vr += __shfl_xor_sync(mask, Vr, o, G);
+    Vi += __shfl_xor_sync(mask, Vi, o, G);
+    Kr += __shfl_xor_sync(mask, Kr, o, G);
+    Ki += __shfl_xor_sync(mask, Ki, o, G);
+  }
+  if (lig != 0) return;
+  store_entry<R>(a.A, (size_t)r * a.lda + j, -Kr, -Ki);
+  if (a.n_rhs > 0) {
+    R y[NQ][3], w[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      y[q][0] = a.cols.qxyz[((size_t)q * 3 + 0) * n + j];
+      y[q][1] = a.cols.qxyz[((size_t)q * 3 + 1) * n + j];
+      y[q][2] = a.cols.qxyz[((size_t)q * 3 + 2) * n + j];
+      w[q] = a.cols.qw[(size_t)q * n + j];
+    }
+    R fVr, fVi, fKr, fKi;
+    far_entry<R, NQ>(y, w, a.cols.nrm[j], a.cols.nrm[n + j], a.cols.nrm[2 * n + j],
+                     (R)(ci[0] - a.cx), (R)(ci[1] - a.cy), (R)(ci[2] - a.cz), a.k, fVr, fVi, fKr, fKi);
+    const double dVr = (double)Vr - (double)fVr, dVi = (double)Vi - (double)fVi;
+    for (int q = 0; q < a.n_rhs; ++q) {
+      double2 gv = a.g[(size_t)q * n + j];
+      a.corr[(size_t)e * a.n_rhs + q] = make_double2(-(dVr * gv.x - dVi * gv.y), -(dVr * gv.y + dVi * gv.x));
+    }
+  }
+}
+
+// Polar self term (reading R-self): V_ii = 1/(4 pi) sum_e h_e int E(k h_e cosh u) du.
+__device__ void self_single_layer(const double (&v)[3][3], const double (&c)[3], double k,
+                                  const double* glx, const double* glw, int ngl, double& Vr,
+                                  double& Vi) {
+  Vr = Vi = 0.0;
+  for (int e = 0; e < 3; ++e) {
+    const double* A = v[e];
+    const double* B = v[(e + 1) % 3];
+    double ab[3] = {B[0] - A[0], B[1] - A[1], B[2] - A[2]};
+    double L = sqrt(ab[0] * ab[0] + ab[1] * ab[1] + ab[2] * ab[2]);
+    double u[3] = {ab[0] / L, ab[1] / L, ab[2] / L};
+    double ca[3] = {c[0] - A[0], c[1] - A[1], c[2] - A[2]};
+    double tproj = ca[0] * u[0] + ca[1] * u[1] + ca[2] * u[2];
+    double foot[3] = {A[0] + tproj * u[0], A[1] + tproj * u[1], A[2] + tproj * u[2]};
+    double hv[3] = {c[0] - foot[0], c[1] - foot[1], c[2] - foot[2]};
+    double h = sqrt(hv[0] * hv[0] + hv[1] * hv[1] + hv[2] * hv[2]);
+    double s0 = (A[0] - foot[0]) * u[0] + (A[1] - foot[1]) * u[1] + (A[2] - foot[2]) * u[2];
+    double s1 = (B[0] - foot[0]) * u[0] + (B[1] - foot[1]) * u[1] + (B[2] - foot[2]) * u[2];
+    double u0 = asinh(s0 / h), u1 = asinh(s1 / h);
+    double half = 0.5 * (u1 - u0), mid = 0.5 * (u1 + u0);
+    double er = 0, ei = 0;
+    for (int g = 0; g < ngl; ++g) {
+      double R = h * cosh(mid + half * glx[g]);
+      double x = k * R, re = 1.0, im = 0.0;
+      if (x != 0.0) {
+        double sx, cx, sh, ch;
+        sincos(x, &sx, &cx);
+        sincos(0.5 * x, &sh, &ch);
+        re = sx / x;
+        im = 2.0 * sh * sh / x;
+      }
+      er += glw[g] * re;
+      ei += glw[g] * im;
+    }
+    Vr += h * half * er;
+    Vi += h * half * ei;
+  }
+  Vr *= nat::kInv4Pi;
+  Vi *= nat::kInv4Pi;
+}
+
+template <typename R, int NQ>
+__global__ void self_kernel(int64_t n, int64_t nv, int64_t row_begin, int64_t rows, int64_t lda,
+                            const double* __restrict__ vx, const int32_t* __restrict__ tri,
+                            const double* __restrict__ cen, FarCols<R> cols, double cx, double cy,
+                            double cz, double k, const double* glx, const double* glw, int ngl,
+                            int n_rhs, const double2* __restrict__ g, void* A,
+                            double2* __restrict__ corr_self) {
+  int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  int64_t i = row_begin + r;
+  store_entry<R>(A, (size_t)r * lda + i, R(0.5), R(0));  // K_ii = 0 on a flat triangle
+  if (n_rhs == 0) return;
+  double v[3][3], c[3] = {cen[i], cen[n + i], cen[2 * n + i]};
+  for (int p = 0; p < 3; ++p) {
+    int vi = tri[p * n + i];
+    for (int d = 0; d < 3; ++d) v[p][d] = vx[d * nv + vi];
+  }
+  double Vr, Vi;
+  self_single_layer(v, c, k, glx, glw, ngl, Vr, Vi);
+  R y[NQ][3], w[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    y[q][0] = cols.qxyz[((size_t)q * 3 + 0) * n + i];
+    y[q][1] = cols.qxyz[((size_t)q * 3 + 1) * n + i];
+    y[q][2] = cols.qxyz[((size_t)q * 3 + 2) * n + i];
+    w[q] = cols.qw[(size_t)q * n + i];
+  }
+  R fVr, fVi, fKr, fKi;
+  far_entry<R, NQ>(y, w, cols.nrm[i], cols.nrm[n + i], cols.nrm[2 * n + i], (R)(c[0] - cx),
+                   (R)(c[1] - cy), (R)(c[2] - cz), (R)k, fVr, fVi, fKr, fKi);
+  double dVr = Vr - (double)fVr, dVi = Vi - (double)fVi;
+  for (int q = 0; q < n_rhs; ++q) {
+    double2 gv = g[(size_t)q * n + i];
+    corr_self[(size_t)r * n_rhs + q] = make_double2(-(dVr * gv.x - dVi * gv.y), -(dVr * gv.y + dVi * gv.x));
+  }
+}
+
+__global__ void rowidx_kernel(int64_t rows, const int64_t* __restrict__ rp, int32_t* __restrict__ ri) {
+  int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  for (int64_t e = rp[r]; e < rp[r + 1]; ++e) ri[e] = (int32_t)r;
+}
+
+__global__ void rhs_final_kernel(int64_t rows, int n_rhs, int n_colblk, const double2* __restrict__ bpart,
+                                 const int64_t* __restrict__ rp, const double2* __restrict__ corr,
+                                 const double2* __restrict__ corr_self, double2* __restrict__ b) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= rows * n_rhs) return;
+  int q = (int)(t / rows);
+  int64_t r = t % rows;
+  double2 s = make_double2(0.0, 0.0);
+  for (int cb = 0; cb < n_colblk; ++cb) {
+    double2 v = bpart[((size_t)cb * n_rhs + q) * rows + r];
+    s.x += v.x;
+    s.y += v.y;
+  }
+  for (int64_t e = rp[r]; e < rp[r + 1]; ++e) {
+    double2 v = corr[(size_t)e * n_rhs + q];
+    s.x += v.x;
+    s.y += v.y;
+  }
+  double2 v = corr_self[(size_t)r * n_rhs + q];
+  s.x += v.x;
+  s.y += v.y;
+  b[(size_t)q * rows + r] = s;
+}
+
+// ------------------------------------------------------------------------------------
+// a6: y = A x, fp64 accumulation; CTA = 8 rows x 256 threads, x reused across rows.
+// ------------------------------------------------------------------------------------
+constexpr int kGemvRows = 8;
+
+__global__ void __launch_bounds__(kThreads) gemv_c64_kernel(int64_t rows, int64_t n, const float2* __restrict__ A,
+                                                           int64_t lda, const double2* __restrict__ x,
+                                                           double2* __restrict__ y) {
+  __shared__ double2 red[kThreads / 32][kGemvRows];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t r0 = (int64_t)blockIdx.x * kGemvRows;
+  const int nr = (int)nat::min64(kGemvRows, rows - r0);
+  double ar[kGemvRows], ai[kGemvRows];
+#pragma unroll
+  for (int r = 0; r < kGemvRows; ++r) ar[r] = ai[r] = 0.0;
+  const int64_t n2 = n / 2;
+  const float4* A4 = reinterpret_cast<const float4*>(A);
+  const int64_t lda2 = lda / 2;
+#pragma unroll 2
+  for (int64_t c = tid; c < n2; c += kThreads) {
+    const double2 x0 = __ldg(&x[2 * c]), x1 = __ldg(&x[2 * c + 1]);
+    float4 av[kGemvRows];
+#pragma unroll
+    for (int r = 0; r < kGemvRows; ++r)
+      av[r] = r < nr ? __ldcs(&A4[(r0 + r) * lda2 + c]) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int r = 0; r < kGemvRows; ++r) {
+      const double a0r = av[r].x, a0i = av[r].y, a1r = av[r].z, a1i = av[r].w;
+      ar[r] = fma(a0r, x0.x, fma(-a0i, x0.y, fma(a1r, x1.x, fma(-a1i, x1.y, ar[r]))));
+      ai[r] = fma(a0r, x0.y, fma(a0i, x0.x, fma(a1r, x1.y, fma(a1i, x1.x, ai[r]))));
+    }
+  }
+  if ((n & 1) && tid == 0) {
+    const double2 xl = x[n - 1];
+    for (int r = 0; r < nr; ++r) {
+      float2 a = A[(r0 + r) * lda + n - 1];
+      ar[r] += (double)a.x * xl.x - (double)a.y * xl.y;
+      ai[r] += (double)a.x * xl.y + (double)a.y * xl.x;
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < kGemvRows; ++r) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      ar[r] += __shfl_xor_sync(0xffffffffu, ar[r], o);
+      ai[r] += __shfl_xor_sync(0xffffffffu, ai[r], o);
+    }
+    if (lane == 0) red[warp][r] = make_double2(ar[r], ai[r]);
+  }
+  __syncthreads();
+  if (tid < nr) {
+    double2 s = red[0][tid];
+    for (int w = 1; w < kThreads / 32; ++w) {
+      s.x += red[w][tid].x;
+      s.y += red[w][tid].y;
+    }
+    y[r0 + tid] = s;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) gemv_c128_kernel(int64_t rows, int64_t n, const double2* __restrict__ A,
+                                                            int64_t lda, const double2* __restrict__ x,
+                                                            double2* __restrict__ y) {
+  __shared__ double2 red[kThreads / 32][kGemvRows];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t r0 = (int64_t)blockIdx.x * kGemvRows;
+  const int nr = (int)nat::min64(kGemvRows, rows - r0);
+  double ar[kGemvRows], ai[kGemvRows];
+#pragma unroll
+  for (int r = 0; r < kGemvRows; ++r) ar[r] = ai[r] = 0.0;
+#pragma unroll 2
+  for (int64_t c = tid; c < n; c += kThreads) {
+    const double2 xv = __ldg(&x[c]);
+    double2 av[kGemvRows];
+#pragma unroll
+    for (int r = 0; r < kGemvRows; ++r)
+      av[r] = r < nr ? __ldcs(&A[(r0 + r) * lda + c]) : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int r = 0; r < kGemvRows; ++r) {
+      ar[r] = fma(av[r].x, xv.x, fma(-av[r].y, xv.y, ar[r]));
+      ai[r] = fma(av[r].x, xv.y, fma(av[r].y, xv.x, ai[r]));
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < kGemvRows; ++r) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      ar[r] += __shfl_xor_sync(0xffffffffu, ar[r], o);
+      ai[r] += __shfl_xor_sync(0xffffffffu, ai[r], o);
+    }
+    if (lane == 0) red[warp][r] = make_double2(ar[r], ai[r]);
+  }
+  __syncthreads();
+  if (tid < nr) {
+    double2 s = red[0][tid];
+    for (int w = 1; w < kThreads / 32; ++w) {
+      s.x += red[w][tid].x;
+      s.y += red[w][tid].y;
+    }
+    y[r0 + tid] = s;
+  }
+}
+
+// ------------------------------------------------------------------------------------
+// host orchestration
+// ------------------------------------------------------------------------------------
+struct AsmWs {
+  double4* rule_far;
+  double4* rule_S;
+  double4* rule_N;
+  double* gl;     // [2][ngl]
+  void* qxyz;
+  void* qw;
+  void* qn;
+  int32_t* rowidx;
+  double2* bpart;
+  double2* corr;
+  double2* corr_self;
+};
+
+size_t carve(nat::Carver& c, AsmWs& w, int64_t n, int64_t rows, int64_t nnz, int n_rhs, int nfar,
+             int nS, int nN, int ngl, size_t rsz) {
+  int64_t n_colblk = (n + kThreads * kCC - 1) / (kThreads * kCC);
+  w.rule_far = c.take<double4>(kMaxFarQ);
+  w.rule_S = c.take<double4>(nS);
+  w.rule_N = c.take<double4>(nN);
+  w.gl = c.take<double>(2 * (size_t)ngl);
+  w.qxyz = c.take<char>(rsz * kMaxFarQ * 3 * n);
+  w.qw = c.take<char>(rsz * kMaxFarQ * n);
+  w.qn = c.take<char>(rsz * 3 * n);
+  w.rowidx = c.take<int32_t>(nnz > 0 ? nnz : 1);
+  w.bpart = c.take<double2>((size_t)n_colblk * (n_rhs > 0 ? n_rhs : 1) * rows);
+  w.corr = c.take<double2>((size_t)(nnz > 0 ? nnz : 1) * (n_rhs > 0 ? n_rhs : 1));
+  w.corr_self = c.take<double2>((size_t)rows * (n_rhs > 0 ? n_rhs : 1));
+  return c.bytes();
+}
+
+constexpr int kMaxLevel = 4;
+constexpr int kMaxGL = 64;
+
+template <typename R, int NQ>
+nat_status assemble_impl(const nat_mesh* mesh, const nat_geom* geom, const Opts& o,
+                         const int64_t* rp, const int32_t* col, const uint8_t* cls, int64_t nnz, double k,
+                         int64_t row_begin, int64_t rows, int n_rhs, const double2* g, void* A,
+                         int64_t lda, double2* rhs, AsmWs& w, const std::vector<Pt>& pS,
+                         const std::vector<Pt>& pN, cudaStream_t s) {
+  const int64_t n = mesh->n_tri;
+  const double cx = geom->center[0], cy = geom->center[1], cz = geom->center[2];
+  FarCols<R> cols{(const R*)w.qxyz, (const R*)w.qw, (const R*)w.qn};
+  far_prep_kernel<R><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(
+      mesh->n_vert, n, mesh->vxyz, mesh->tri, geom->normal, geom->area, w.rule_far, NQ, cx, cy, cz,
+      (R*)w.qxyz, (R*)w.qw, (R*)w.qn);
+  NAT_LAUNCH_CHECK();
+  // a4: far rule on every pair, RHS partial sums
+  FarArgs<R> fa{};
+  fa.n = n;
+  fa.row_begin = row_begin;
+  fa.rows = rows;
+  fa.lda = lda;
+  fa.cols = cols;
+  fa.cen = geom->centroid;
+  fa.cx = cx;
+  fa.cy = cy;
+  fa.cz = cz;
+  fa.k = (R)k;
+  fa.n_rhs = n_rhs;
+  fa.g = g;
+  fa.A = A;
+  fa.bpart = w.bpart;
+  const int64_t n_colblk = (n + kThreads * kCC - 1) / (kThreads * kCC);
+  dim3 grid((unsigned)n_colblk, (unsigned)((rows + kTI - 1) / kTI));
+  if (n_rhs == 0) {
+    fa.store_A = true;
+    far_kernel<R, NQ, 0><<<grid, kThreads, 0, s>>>(fa);
+  } else {
+    for (int q0 = 0; q0 < n_rhs; q0 += kNRmax) {
+      fa.rhs0 = q0;
+      fa.store_A = (q0 == 0);
+      if (n_rhs - q0 >= 2)
+        far_kernel<R, NQ, 2><<<grid, kThreads, 0, s>>>(fa);
+      else
+        far_kernel<R, NQ, 1><<<grid, kThreads, 0, s>>>(fa);
+    }
+  }
+  NAT_LAUNCH_CHECK();
+  // a5: near pairs overwrite A and correct b; self term
+  if (nnz > 0) {
+    rowidx_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, s>>>(rows, rp, w.rowidx);
+    NearArgs<R> na{};
+    na.n = n;
+    na.nv = mesh->n_vert;
+    na.row_begin = row_begin;
+    na.rows = rows;
+    na.lda = lda;
+    na.nnz = nnz;
+    na.row_ptr = rp;
+    na.col = col;
+    na.cls = cls;
+    na.rowidx = w.rowidx;
+    na.vx = mesh->vxyz;
+    na.tri = mesh->tri;
+    na.cen = geom->centroid;
+    na.nrm = geom->normal;
+    na.area = geom->area;
+    na.cols = cols;
+    na.cx = cx;
+    na.cy = cy;
+    na.cz = cz;
+    na.k = (R)k;
+    na.n_rhs = n_rhs;
+    na.g = g;
+    na.A = A;
+    na.corr = w.corr;
+    na.rule = w.rule_S;
+    na.npts = (int)pS.size();
+    near_kernel<R, NQ, 32, 1><<<(unsigned)((nnz * 32 + kThreads - 1) / kThreads), kThreads, 0, s>>>(na);
+    na.rule = w.rule_N;
+    na.npts = (int)pN.size();
+    near_kernel<R, NQ, 8, 2><<<(unsigned)((nnz * 8 + kThreads - 1) / kThreads), kThreads, 0, s>>>(na);
+    NAT_LAUNCH_CHECK();
+  }
+  self_kernel<R, NQ><<<(unsigned)((rows + 127) / 128), 128, 0, s>>>(
+      n, mesh->n_vert, row_begin, rows, lda, mesh->vxyz, mesh->tri, geom->centroid, cols, cx, cy, cz,
+      k, w.gl, w.gl + o.gl, o.gl, n_rhs, g, A, w.corr_self);
+  NAT_LAUNCH_CHECK();
+  if (n_rhs > 0) {
+    int64_t t = rows * n_rhs;
+    rhs_final_kernel<<<(unsigned)((t + 255) / 256), 256, 0, s>>>(rows, n_rhs, (int)n_colblk, w.bpart,
+                                                                 rp, w.corr, w.corr_self, rhs);
+    NAT_LAUNCH_CHECK();
+  }
+  return NAT_OK;
+}
+
+}  // namespace
+
+extern "C" size_t nat_bem_assemble_workspace(int64_t n_tri, int64_t rows, int64_t nnz, int n_rhs) {
+  nat::Carver c(nullptr);
+  AsmWs w;
+  int64_t nS = 7 * (1LL << (2 * kMaxLevel)), nN = nS;
+  return carve(c, w, n_tri, rows, nnz, n_rhs, kMaxFarQ, (int)nS, (int)nN, kMaxGL, sizeof(double));
+}
+
+extern "C" nat_status nat_bem_assemble(const nat_mesh* mesh, const nat_geom* geom,
+                                       const nat_quad_opts* opts, const int64_t* near_row_ptr,
+                                       const int32_t* near_col, const uint8_t* near_cls, double k,
+                                       nat_prec prec, int64_t row_begin, int64_t row_end, int n_rhs,
+                                       const void* g, void* A, int64_t lda, void* rhs, void* ws,
+                                       size_t ws_bytes, nat_stream_t stream) {
+  NAT_REQUIRE(mesh && geom, "mesh and geom must be non-null");
+  NAT_REQUIRE(prec == NAT_FP32 || prec == NAT_FP64, "bad precision %d", (int)prec);
+  const int64_t n = mesh->n_tri;
+  NAT_REQUIRE(geom->n_tri == n && n >= 1 && n < (1LL << 31), "inconsistent n_tri");
+  NAT_REQUIRE(0 <= row_begin && row_begin < row_end && row_end <= n, "bad row range");
+  NAT_REQUIRE(lda >= n, "lda (%lld) < n_tri (%lld)", (long long)lda, (long long)n);
+  NAT_REQUIRE(k >= 0.0 && k < 1e300, "k = %g must be finite and >= 0", k);
+  NAT_REQUIRE(n_rhs >= 0 && (n_rhs == 0) == (g == nullptr), "g must be NULL iff n_rhs == 0");
+  Opts o = opts_of(opts);
+  NAT_REQUIRE(o.far_pts == 1 || o.far_pts == 3 || o.far_pts == 6 || o.far_pts == 7,
+              "far_pts must be 1, 3, 6 or 7");
+  NAT_REQUIRE(o.lev_S >= 0 && o.lev_S <= kMaxLevel && o.lev_N >= 0 && o.lev_N <= kMaxLevel,
+              "near levels must be in [0, %d]", kMaxLevel);
+  NAT_REQUIRE(o.gl >= 2 && o.gl <= kMaxGL, "self_theta_pts must be in [2, %d]", kMaxGL);
+  NAT_REQUIRE_DEV(near_row_ptr);
+  NAT_REQUIRE_DEV(A);
+  NAT_REQUIRE_DEV(mesh->vxyz);
+  NAT_REQUIRE_DEV(mesh->tri);
+  NAT_REQUIRE_DEV(geom->centroid);
+  NAT_REQUIRE_DEV(geom->normal);
+  NAT_REQUIRE_DEV(geom->area);
+  if (n_rhs > 0) {
+    NAT_REQUIRE_DEV(g);
+    NAT_REQUIRE_DEV(rhs);
+  }
+  const int64_t rows = row_end - row_begin;
+  cudaStream_t s = (cudaStream_t)stream;
+  int64_t nnz = 0;
+  NAT_CUDA_TRY(cudaMemcpyAsync(&nnz, near_row_ptr + rows, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  NAT_CUDA_TRY(cudaStreamSynchronize(s));
+  NAT_REQUIRE(nnz >= 0 && nnz < (1LL << 31), "near list has %lld entries", (long long)nnz);
+  if (nnz > 0) {
+    NAT_REQUIRE_DEV(near_col);
+    NAT_REQUIRE_DEV(near_cls);
+  }
+  std::vector<Pt> pF, pS, pN;
+  base_rule(o.far_pts, pF);
+  composite_rule(o.lev_S, pS);
+  composite_rule(o.lev_N, pN);
+  std::vector<double> glx, glw;
+  gauss_legendre(o.gl, glx, glw);
+
+  nat::Carver c(ws);
+  AsmWs w;
+  size_t rsz = prec == NAT_FP32 ? sizeof(float) : sizeof(double);
+  size_t need = carve(c, w, n, rows, nnz, n_rhs, kMaxFarQ, (int)pS.size(), (int)pN.size(), o.gl, rsz);
+  if (ws_bytes < need) return nat::fail(NAT_ERR_WORKSPACE, "workspace %zu < %zu", ws_bytes, need);
+  NAT_REQUIRE_DEV(ws);
+  // rule tables -> workspace (pageable copies: staged before the call returns)
+  NAT_CUDA_TRY(cudaMemcpyAsync(w.rule_far, pF.data(), pF.size() * sizeof(Pt), cudaMemcpyHostToDevice, s));
+  NAT_CUDA_TRY(cudaMemcpyAsync(w.rule_S, pS.data(), pS.size() * sizeof(Pt), cudaMemcpyHostToDevice, s));
+  NAT_CUDA_TRY(cudaMemcpyAsync(w.rule_N, pN.data(), pN.size() * sizeof(Pt), cudaMemcpyHostToDevice, s));
+  std::vector<double> gl(glx);
+  gl.insert(gl.end(), glw.begin(), glw.end());
+  NAT_CUDA_TRY(cudaMemcpyAsync(w.gl, gl.data(), gl.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+
+  const double2* gg = (const double2*)g;
+  double2* bb = (double2*)rhs;
+#define NAT_ASM(R, NQ)                                                                         \
+  assemble_impl<R, NQ>(mesh, geom, o, near_row_ptr, near_col, near_cls, nnz, k, row_begin, rows, \
+                       n_rhs, gg, A, lda, bb, w, pS, pN, s)
+  if (prec == NAT_FP32) {
+    switch (o.far_pts) {
+      case 1: return NAT_ASM(float, 1);
+      case 3: return NAT_ASM(float, 3);
+      case 6: return NAT_ASM(float, 6);
+      default: return NAT_ASM(float, 7);
+    }
+  } else {
+    switch (o.far_pts) {
+      case 1: return NAT_ASM(double, 1);
+      case 3: return NAT_ASM(double, 3);
+      case 6: return NAT_ASM(double, 6);
+      default: return NAT_ASM(double, 7);
+    }
+  }
+#undef NAT_ASM
+}
+
+extern "C" nat_status nat_bem_matvec(nat_prec prec, int64_t rows, int64_t n, const void* A, int64_t lda,
+                                     const void* x, void* y, nat_stream_t stream) {
+  NAT_REQUIRE(prec == NAT_FP32 || prec == NAT_FP64, "bad precision %d", (int)prec);
+  NAT_REQUIRE(rows >= 1 && n >= 1 && lda >= n, "need rows, n >= 1 and lda >= n");
+  NAT_REQUIRE(prec == NAT_FP64 || (lda % 2 == 0 && ((uintptr_t)A % 16) == 0),
+              "NAT_FP32 matvec needs an even lda and a 16-byte aligned A");
+  NAT_REQUIRE_DEV(A);
+  NAT_REQUIRE_DEV(x);
+  NAT_REQUIRE_DEV(y);
+  unsigned grid = (unsigned)((rows + kGemvRows - 1) / kGemvRows);
+  if (prec == NAT_FP32)
+    gemv_c64_kernel<<<grid, kThreads, 0, (cudaStream_t)stream>>>(rows, n, (const float2*)A, lda,
+                                                                 (const double2*)x, (double2*)y);
+  else
+    gemv_c128_kernel<<<grid, kThreads, 0, (cudaStream_t)stream>>>(rows, n, (const double2*)A, lda,
+                                                                  (const double2*)x, (double2*)y);
+  NAT_LAUNCH_CHECK();
+  return NAT_OK;
+}
+
+namespace nat {
+// Used by the GMRES driver (gmres.cu).
+nat_status matvec_internal(nat_prec prec, int64_t rows, int64_t n, const void* A, int64_t lda,
+                           const void* x, void* y, cudaStream_t s) {
+  unsigned grid = (unsigned)((rows + kGemvRows - 1) / kGemvRows);
+  if (prec == NAT_FP32)
+    gemv_c64_kernel<<<grid, kThreads, 0, s>>>(rows, n, (const float2*)A, lda, (const double2*)x, (double2*)y);
+  else
+    gemv_c128_kernel<<<grid, kThreads, 0, s>>>(rows, n, (const double2*)A, lda, (const double2*)x, (double2*)y);
+  NAT_LAUNCH_CHECK();
+  return NAT_OK;
+}
+}  // namespace nat

@@ -63,3 +63,7 @@ int device_sm_count();
 
 #define NAT_REQUIRE_DEV(ptr)                                                                 \
   NAT_REQUIRE(nat::is_device_ptr(ptr), "%s must be a device pointer", #ptr)
+
+namespace nat {
+__host__ __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
+}  // namespace nat

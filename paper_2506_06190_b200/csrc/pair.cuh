@@ -1,0 +1,44 @@
+// Device-side Helmholtz pair evaluation helpers, fp32 and fp64.
+#pragma once
+#include <cuda_runtime.h>
+
+namespace nat {
+
+template <typename T>
+struct C2 {
+  T x, y;
+};
+
+__device__ __forceinline__ float pair_rsqrt(float x) {
+  float y;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ double pair_rsqrt(double x) { return rsqrt(x); }
+
+__device__ __forceinline__ void pair_sincos(float x, float* s, float* c) { __sincosf(x, s, c); }
+__device__ __forceinline__ void pair_sincos(double x, double* s, double* c) { sincos(x, s, c); }
+
+// Accumulates, for target x and source point y (d = y - x) with weight w (already
+// divided by 4 pi) and source normal n:
+//   V += w G-part = w rho e^{ikr}                         (single layer, 4 pi G = e^{ikr}/r)
+//   K += w dn rho^3 (ikr - 1) e^{ikr}                     (double layer, 4 pi dG/dn_y)
+template <typename R>
+__device__ __forceinline__ void pair_accumulate(R dx, R dy, R dz, R nx, R ny, R nz, R w, R k,
+                                                R& Vr, R& Vi, R& Kr, R& Ki) {
+  const R r2 = dx * dx + dy * dy + dz * dz;
+  const R dn = dx * nx + dy * ny + dz * nz;
+  const R rho = pair_rsqrt(r2);
+  const R rr = r2 * rho;
+  const R kr = k * rr;
+  R s, c;
+  pair_sincos(kr, &s, &c);
+  const R t = w * rho;
+  Vr += t * c;
+  Vi += t * s;
+  const R u = t * dn * (rho * rho);
+  Kr += u * (-c - kr * s);
+  Ki += u * (kr * c - s);
+}
+
+}  // namespace nat

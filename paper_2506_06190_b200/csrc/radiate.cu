@@ -408,7 +408,7 @@ Plan make_plan(nat_prec prec, int64_t n_src, int n_modes, int64_t n_lis) {
   int64_t base = pl.tgt_tiles * pl.n_mchunk;
   int64_t want = 4LL * nat::kNumSMs * 2;  // enough CTAs for several full waves
   int n_split = 1;
-  if (base < want) n_split = (int)std::min<int64_t>((want + base - 1) / base, pl.n_tiles);
+  if (base < want) n_split = (int)nat::min64((want + base - 1) / base, pl.n_tiles);
   pl.chunk_tiles = (pl.n_tiles + n_split - 1) / n_split;
   pl.n_split = (pl.n_tiles + pl.chunk_tiles - 1) / pl.chunk_tiles;
   pl.rec_elems = (size_t)pl.n_mchunk * pl.n_src_pad * pl.NF;

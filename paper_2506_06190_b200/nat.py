@@ -76,7 +76,7 @@ _SIGS = {
                                      _I64, _I64, _P, C.POINTER(_I64), _P]),
     "nat_bem_near_build": (C.c_int, [C.POINTER(_Mesh), C.POINTER(_Geom), C.POINTER(_QuadOpts),
                                      _I64, _I64, _P, _P, _P, _P]),
-    "nat_bem_assemble_workspace": (_SZ, [_I64, _I64, C.c_int]),
+    "nat_bem_assemble_workspace": (_SZ, [_I64, _I64, _I64, C.c_int]),
     "nat_bem_assemble": (C.c_int, [C.POINTER(_Mesh), C.POINTER(_Geom), C.POINTER(_QuadOpts),
                                    _P, _P, _P, _D, C.c_int, _I64, _I64, C.c_int, _P, _P, _I64,
                                    _P, _P, _SZ, _P]),
@@ -310,3 +310,129 @@ def nat_radiate_field(src: Sources, k: Sequence[float], lis_xyz: torch.Tensor, p
                                    n_lis, _ptr(lis_xyz), _ptr(out), _ptr(ws), ws.numel(),
                                    _stream()))
     return out
+
+
+# ------------------------------------------------------------------------------------
+# dense BEM (rows a2, a4-a7)
+# ------------------------------------------------------------------------------------
+@dataclasses.dataclass
+class NearList:
+    row_begin: int
+    row_end: int
+    row_ptr: torch.Tensor  # (rows+1,) int64
+    col: torch.Tensor      # (nnz,) int32
+    cls: torch.Tensor      # (nnz,) uint8
+
+    @property
+    def nnz(self):
+        return self.col.numel()
+
+
+def nat_bem_near_list(mesh: Mesh, geom: Geom, row_begin=0, row_end=None, opts=None) -> NearList:
+    """nat_bem_near_count + nat_bem_near_build."""
+    row_end = mesh.n_tri if row_end is None else row_end
+    dev = mesh.vxyz.device
+    o = opts or quad_opts()
+    rp = torch.empty(row_end - row_begin + 1, dtype=torch.int64, device=dev)
+    nnz = C.c_int64(0)
+    _check(lib().nat_bem_near_count(C.byref(mesh.c()), C.byref(geom.c()), C.byref(o), row_begin,
+                                    row_end, _ptr(rp), C.byref(nnz), _stream()))
+    col = torch.empty(max(nnz.value, 1), dtype=torch.int32, device=dev)[: nnz.value]
+    cls = torch.empty(max(nnz.value, 1), dtype=torch.uint8, device=dev)[: nnz.value]
+    _check(lib().nat_bem_near_build(C.byref(mesh.c()), C.byref(geom.c()), C.byref(o), row_begin,
+                                    row_end, _ptr(rp), C.c_void_p(col.data_ptr()),
+                                    C.c_void_p(cls.data_ptr()), _stream()))
+    return NearList(row_begin, row_end, rp, col, cls)
+
+
+def nat_bem_assemble(mesh: Mesh, geom: Geom, near: NearList, k: float, g=None, prec="fp32",
+                     opts=None, A: Optional[torch.Tensor] = None, lda: Optional[int] = None):
+    """Rows [near.row_begin, near.row_end) of A (c64 for fp32, c128 for fp64) and
+    rhs = -V g (c128 [n_rhs][rows]).  Returns (A, rhs)."""
+    pr = _prec(prec)
+    dev = mesh.vxyz.device
+    n = mesh.n_tri
+    rows = near.row_end - near.row_begin
+    lda = lda or (n + (n & 1))
+    cdt = torch.complex64 if pr == NAT_FP32 else torch.complex128
+    if A is None:
+        A = torch.empty(rows, lda, dtype=cdt, device=dev)
+    n_rhs = 0
+    rhs = None
+    if g is not None:
+        g = torch.atleast_2d(g).to(torch.complex128).contiguous()
+        n_rhs = g.shape[0]
+        rhs = torch.empty(n_rhs, rows, dtype=torch.complex128, device=dev)
+    o = opts or quad_opts()
+    ws = _ws(lib().nat_bem_assemble_workspace(n, rows, near.nnz, n_rhs), dev)
+    _check(lib().nat_bem_assemble(C.byref(mesh.c()), C.byref(geom.c()), C.byref(o), _ptr(near.row_ptr),
+                                  C.c_void_p(near.col.data_ptr()), C.c_void_p(near.cls.data_ptr()),
+                                  float(k), pr, near.row_begin, near.row_end, n_rhs, _ptr(g), _ptr(A),
+                                  lda, _ptr(rhs), _ptr(ws), ws.numel(), _stream()))
+    return A, rhs
+
+
+def nat_bem_matvec(A: torch.Tensor, x: torch.Tensor, n: Optional[int] = None, out=None):
+    pr = NAT_FP32 if A.dtype == torch.complex64 else NAT_FP64
+    rows, lda = A.shape
+    n = n or x.numel()
+    out = torch.empty(rows, dtype=torch.complex128, device=A.device) if out is None else out
+    _check(lib().nat_bem_matvec(pr, rows, n, _ptr(A), lda, _ptr(x.to(torch.complex128).contiguous()),
+                                _ptr(out), _stream()))
+    return out
+
+
+class Comm:
+    """NCCL communicator built from a torch.distributed-broadcast unique id."""
+
+    def __init__(self, rank: int, world: int, uid: bytes):
+        self.rank, self.world = rank, world
+        self.handle = C.c_void_p()
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        _check(lib().nat_comm_create_from_id(C.byref(self.handle), buf, rank, world))
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (C.c_uint8 * 128)()
+        _check(lib().nat_comm_unique_id(buf))
+        return bytes(buf)
+
+    @classmethod
+    def from_torch_distributed(cls):
+        import torch.distributed as dist
+        rank, world = dist.get_rank(), dist.get_world_size()
+        t = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            t.copy_(torch.frombuffer(bytearray(cls.unique_id()), dtype=torch.uint8))
+        dist.broadcast(t, 0)
+        return cls(rank, world, bytes(t.cpu().numpy().tobytes()))
+
+    def close(self):
+        if self.handle:
+            _check(lib().nat_comm_destroy(self.handle))
+            self.handle = C.c_void_p()
+
+
+def row_range(n: int, rank: int, world: int):
+    """Row ownership of the row-sharded solve: ceil(n/world) rows per rank."""
+    rpr = -(-n // world)
+    return min(n, rank * rpr), min(n, (rank + 1) * rpr)
+
+
+def nat_bem_solve(A_local: torch.Tensor, b_local: torch.Tensor, n: int, row_begin=0, comm: Optional[Comm] = None,
+                  tol=1e-6, max_iter=200, ws=None):
+    """Returns (x c128 [n], info dict).  Raises on errors; non-convergence is reported
+    in info['converged'] (status NAT_WARN_NOT_CONVERGED)."""
+    pr = NAT_FP32 if A_local.dtype == torch.complex64 else NAT_FP64
+    rows, lda = A_local.shape
+    dev = A_local.device
+    x = torch.empty(n, dtype=torch.complex128, device=dev)
+    if ws is None:
+        ws = _ws(lib().nat_bem_solve_workspace(pr, n, rows, max_iter), dev)
+    info = _SolveInfo()
+    st = lib().nat_bem_solve(comm.handle if comm else None, pr, n, row_begin, row_begin + rows, _ptr(A_local),
+                             lda, _ptr(b_local.contiguous()), _ptr(x), float(tol), int(max_iter), _ptr(ws),
+                             ws.numel(), C.byref(info), _stream())
+    _check(st, allow_warn=True)
+    return x, dict(iters=info.iters, converged=info.converged, rel_residual=info.rel_residual,
+                   t_total_s=info.t_total_s, t_matvec_s=info.t_matvec_s, t_comm_s=info.t_comm_s)
