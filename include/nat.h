@@ -177,6 +177,8 @@ nat_status nat_bem_solve(nat_comm* comm, nat_prec prec, int64_t n, int64_t row_b
  * a9  nat_mc_rhs: b[m][i] = -w sum_{j != i} G_m(y_i, y_j) g[m][j] - (eps/2) g[m][i].
  * a10 nat_mc_apply: out[m][i] = 1/2 p[m][i] - w sum_{j != i} dG_m/dn_y(y_i, y_j) p[m][j].
  *     w = (|Gamma| - pi eps^2)/(M - 1);  k [host][n_sys];  g, p, b, out c128 [n_sys][M].
+ *     NAT_FP32: sample pairs closer than 2 eps (the disk diameter) are evaluated in fp64
+ *     (their fp32 coordinates cannot resolve d.n); all other pairs in fp32.
  * nat_mc_surface_pressure: a8 (or caller samples) -> a9 -> batched GMRES over a10
  *     for all n_sys wavenumbers sharing one sample set; g_tri c128 [n_sys][n_tri].
  *     Errors: NAT_ERR_SINGULAR on coincident samples (|y_i - y_j| < 1e-12).
@@ -197,7 +199,7 @@ nat_status nat_mc_rhs(nat_prec prec, int64_t M, const double* samples, int n_sys
                       const void* g, double w, double eps, void* b, void* ws, size_t ws_bytes,
                       nat_stream_t stream); /* (async) */
 nat_status nat_mc_apply(nat_prec prec, int64_t M, const double* samples, int n_sys, const double* k,
-                        const void* p, double w, void* out, void* ws, size_t ws_bytes,
+                        const void* p, double w, double eps, void* out, void* ws, size_t ws_bytes,
                         nat_stream_t stream); /* (async) */
 nat_status nat_mc_check_coincident(int64_t M, const double* samples, int64_t* pair /* [host] 2 */,
                                    void* ws, size_t ws_bytes, nat_stream_t stream); /* (sync) */

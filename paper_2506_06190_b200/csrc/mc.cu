@@ -1,0 +1,589 @@
+// Rows a8-a10 — the Monte-Carlo BEM estimator BEM-MC (§4.1.1-4.2: Eq. BIE
+// l.194-198, Eq. SYS l.200-204, the disk split and disk terms l.215-236), with the
+// readings R-sign, R-mc-sample, R-eps, R-weight, R-disk of DESIGN.md §3:
+//   a8  uniform-by-area samples from a Philox4x32-10 counter stream (bit-identical with
+//       the oracle: every fp64 step uses round-to-nearest intrinsics, no FMA);
+//   a9  b_i = -w sum_{j != i} G(y_i, y_j) g_j - (eps/2) g_i;
+//   a10 (A p)_i = 1/2 p_i - w sum_{j != i} dG/dn_y(y_i, y_j) p_j   (matrix-free);
+// batched over every wavenumber sharing the sample set and solved with the batched
+// GMRES engine (krylov.cuh).  a9/a10 reuse the radiation kernel with targets = sources
+// (TMA-staged source tiles, self pair excluded exactly).
+#include <chrono>
+#include <cmath>
+#include <vector>
+
+#include "krylov.cuh"
+#include "nat_internal.cuh"
+#include "pair.cuh"
+#include "radiate.cuh"
+
+namespace {
+
+__device__ __forceinline__ void philox4x32_10(uint32_t& c0, uint32_t& c1, uint32_t& c2, uint32_t& c3,
+                                              uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r > 0) {
+      k0 += 0x9E3779B9u;
+      k1 += 0xBB67AE85u;
+    }
+    const uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
+    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
+    const uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+    c0 = n0;
+    c1 = lo1;
+    c2 = n2;
+    c3 = lo0;
+  }
+}
+
+__global__ void mc_sample_kernel(int64_t M, uint64_t seed, uint64_t stream_id, int64_t nv, int64_t nt,
+                                 const double* __restrict__ vx, const int32_t* __restrict__ tri,
+                                 const double* __restrict__ nrm, const double* __restrict__ cdf,
+                                 double* __restrict__ smp, int32_t* __restrict__ stri) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= M) return;
+  uint32_t c0 = (uint32_t)j, c1 = 0u, c2 = (uint32_t)stream_id, c3 = (uint32_t)(stream_id >> 32);
+  philox4x32_10(c0, c1, c2, c3, (uint32_t)seed, (uint32_t)(seed >> 32));
+  const double two32 = 2.3283064365386963e-10;  // 2^-32
+  const double u0 = __dmul_rn(__dadd_rn((double)c0, 0.5), two32);
+  const double u1 = __dmul_rn(__dadd_rn((double)c1, 0.5), two32);
+  const double u2 = __dmul_rn(__dadd_rn((double)c2, 0.5), two32);
+  // upper_bound: first t with cdf[t] > u0 * cdf[N-1]
+  const double v = __dmul_rn(u0, cdf[nt - 1]);
+  int64_t lo = 0, hi = nt;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (cdf[mid] > v)
+      hi = mid;
+    else
+      lo = mid + 1;
+  }
+  const int64_t t = lo < nt ? lo : nt - 1;
+  const double s = __dsqrt_rn(u1);
+  const double b1 = __dsub_rn(1.0, s);
+  const double b2 = __dmul_rn(s, __dsub_rn(1.0, u2));
+  const double b3 = __dmul_rn(s, u2);
+  const int a = tri[t], b = tri[nt + t], c = tri[2 * nt + t];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    const double* X = vx + d * nv;
+    smp[d * M + j] = __dadd_rn(__dadd_rn(__dmul_rn(b1, X[a]), __dmul_rn(b2, X[b])), __dmul_rn(b3, X[c]));
+    smp[(3 + d) * M + j] = nrm[d * nt + t];
+  }
+  stri[j] = (int32_t)t;
+}
+
+constexpr int kCT = 256;
+
+// Smallest (i, j), i != j, with |y_i - y_j| < 1e-12 (packed i << 32 | j), brute force.
+__global__ void __launch_bounds__(kCT) coincident_kernel(int64_t M, const double* __restrict__ smp,
+                                                       unsigned long long* best) {
+  __shared__ double sx[kCT], sy[kCT], sz[kCT];
+  const int64_t i = blockIdx.x * (int64_t)kCT + threadIdx.x;
+  double xi = 0, yi = 0, zi = 0;
+  if (i < M) {
+    xi = smp[i];
+    yi = smp[M + i];
+    zi = smp[2 * M + i];
+  }
+  unsigned long long mine = ~0ull;
+  for (int64_t j0 = 0; j0 < M; j0 += kCT) {
+    __syncthreads();
+    const int64_t jl = j0 + threadIdx.x;
+    if (jl < M) {
+      sx[threadIdx.x] = smp[jl];
+      sy[threadIdx.x] = smp[M + jl];
+      sz[threadIdx.x] = smp[2 * M + jl];
+    }
+    __syncthreads();
+    const int jn = (int)nat::min64(kCT, M - j0);
+    if (i < M && mine == ~0ull) {
+      for (int t = 0; t < jn; ++t) {
+        const double dx = xi - sx[t], dy = yi - sy[t], dz = zi - sz[t];
+        if (dx * dx + dy * dy + dz * dz < 1e-24 && j0 + t != i) {
+          mine = ((unsigned long long)i << 32) | (unsigned long long)(j0 + t);
+          break;
+        }
+      }
+    }
+  }
+  if (mine != ~0ull) atomicMin(best, mine);
+}
+
+__global__ void init_best_kernel(unsigned long long* best) { *best = ~0ull; }
+
+__global__ void gather_g_kernel(int nsys, int64_t M, int64_t nt, const double2* __restrict__ g_tri,
+                                const int32_t* __restrict__ stri, double2* __restrict__ gs) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int s = blockIdx.y;
+  if (j >= M || s >= nsys) return;
+  gs[(size_t)s * M + j] = g_tri[(size_t)s * nt + stri[j]];
+}
+
+// b = R - (eps/2) g   (disk single-layer term, with the sign of Eq. BM)
+__global__ void rhs_combine_kernel(int nsys, int64_t M, double eps, const double2* __restrict__ g,
+                                   double2* __restrict__ b) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int s = blockIdx.y;
+  if (j >= M) return;
+  const size_t q = (size_t)s * M + j;
+  const double2 gv = g[q], r = b[q];
+  b[q] = make_double2(r.x - 0.5 * eps * gv.x, r.y - 0.5 * eps * gv.y);
+}
+
+// out = 1/2 p - R   (the disk double-layer term is 0)
+__global__ void apply_combine_kernel(int nsys, int64_t M, const double2* __restrict__ p,
+                                     double2* __restrict__ out) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int s = blockIdx.y;
+  if (j >= M) return;
+  const size_t q = (size_t)s * M + j;
+  const double2 pv = p[q], r = out[q];
+  out[q] = make_double2(0.5 * pv.x - r.x, 0.5 * pv.y - r.y);
+}
+
+// ---- close sample pairs (fp32 r^2 <= (2 eps)^2): evaluated in fp64 -------------------
+// With random samples some pairs are far closer than the sample spacing; their fp32
+// coordinates (rounded to ~6e-8 |y|) would give O(1e-3) errors in d.n and 1/r.  The fp32
+// kernel skips exactly these pairs (same pair_r2_f32 on the same staged coordinates) and
+// this fp64 pass adds them, so the fp32 path keeps the 1e-4 parity bar.
+constexpr int kNT = 256;
+
+template <bool kFill>
+__global__ void __launch_bounds__(kNT) mc_near_kernel(int64_t M, const double* __restrict__ smp, double cx,
+                                                      double cy, double cz, float thr,
+                                                      int32_t* __restrict__ rp, int32_t* __restrict__ col,
+                                                      int64_t cap, int* overflow) {
+  __shared__ float sx[kNT], sy[kNT], sz[kNT];
+  const int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x;
+  float xi = 0.f, yi = 0.f, zi = 0.f;
+  if (i < M) {
+    xi = (float)(smp[i] - cx);
+    yi = (float)(smp[M + i] - cy);
+    zi = (float)(smp[2 * M + i] - cz);
+  }
+  int cnt = 0;
+  int64_t pos = (kFill && i < M) ? rp[i] : 0;
+  for (int64_t j0 = 0; j0 < M; j0 += kNT) {
+    __syncthreads();
+    const int64_t jl = j0 + threadIdx.x;
+    if (jl < M) {
+      sx[threadIdx.x] = (float)(smp[jl] - cx);
+      sy[threadIdx.x] = (float)(smp[M + jl] - cy);
+      sz[threadIdx.x] = (float)(smp[2 * M + jl] - cz);
+    }
+    __syncthreads();
+    const int jn = (int)nat::min64(kNT, M - j0);
+    if (i < M) {
+      for (int t = 0; t < jn; ++t) {
+        const float r2 = nat::pair_r2_f32(__fsub_rn(sx[t], xi), __fsub_rn(sy[t], yi), __fsub_rn(sz[t], zi));
+        if (r2 <= thr && j0 + t != i) {
+          if (kFill) {
+            if (pos < cap) col[pos] = (int32_t)(j0 + t);
+            ++pos;
+          } else {
+            ++cnt;
+          }
+        }
+      }
+    }
+  }
+  if (!kFill && i < M) rp[i + 1] = cnt;
+}
+
+__global__ void __launch_bounds__(1024) scan32_kernel(int32_t* rp, int64_t M, int64_t cap, int* overflow) {
+  __shared__ int64_t part[1024];
+  const int t = threadIdx.x;
+  const int64_t per = (M + 1023) / 1024;
+  const int64_t b = 1 + t * per, e = nat::min64(M + 1, b + per);
+  int64_t s = 0;
+  for (int64_t i = b; i < e; ++i) s += rp[i];
+  part[t] = s;
+  __syncthreads();
+  if (t == 0) {
+    int64_t acc = 0;
+    for (int q = 0; q < 1024; ++q) {
+      int64_t v = part[q];
+      part[q] = acc;
+      acc += v;
+    }
+    if (acc > cap) *overflow = 1;
+  }
+  __syncthreads();
+  int64_t acc = part[t];
+  for (int64_t i = b; i < e; ++i) {
+    acc += rp[i];
+    rp[i] = (int32_t)(acc < cap ? acc : cap);
+  }
+  if (t == 0) rp[0] = 0;
+}
+
+// R[s][i] += w [p_s(y_j) dG_s/dn_y(y_i, y_j) - g_s(y_j) G_s(y_i, y_j)] over the close pairs
+// of row i, in CSR order, fp64.
+struct KArr {
+  double k[64];
+};
+
+__global__ void mc_near_apply_kernel(int nsys, int64_t M, const double* __restrict__ smp,
+                                     const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
+                                     KArr ka, double w, const double2* __restrict__ p,
+                                     const double2* __restrict__ g, double2* __restrict__ R) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int s = blockIdx.y;
+  if (i >= M) return;
+  const double k = ka.k[s];
+  const double xi = smp[i], yi = smp[M + i], zi = smp[2 * M + i];
+  double ar = 0.0, ai = 0.0;
+  for (int e = rp[i]; e < rp[i + 1]; ++e) {
+    const int64_t j = col[e];
+    const double dx = smp[j] - xi, dy = smp[M + j] - yi, dz = smp[2 * M + j] - zi;
+    const double r = sqrt(dx * dx + dy * dy + dz * dz);
+    const double dn = dx * smp[3 * M + j] + dy * smp[4 * M + j] + dz * smp[5 * M + j];
+    double sn, cs;
+    sincos(k * r, &sn, &cs);
+    const double t = w * nat::kInv4Pi / r;  // w G = t e^{ikr}
+    if (p) {  // w p dG/dn_y = t dn/r^2 (ikr - 1) e^{ikr} p
+      const double2 pv = p[(size_t)s * M + j];
+      const double u = t * dn / (r * r);
+      const double er = -cs - k * r * sn, ei = k * r * cs - sn;  // (ikr - 1) e^{ikr}
+      ar += u * (er * pv.x - ei * pv.y);
+      ai += u * (er * pv.y + ei * pv.x);
+    }
+    if (g) {  // - w g G
+      const double2 gv = g[(size_t)s * M + j];
+      ar -= t * (cs * gv.x - sn * gv.y);
+      ai -= t * (cs * gv.y + sn * gv.x);
+    }
+  }
+  const size_t q = (size_t)s * M + i;
+  double2 o = R[q];
+  R[q] = make_double2(o.x + ar, o.y + ai);
+}
+
+struct NearPairs {
+  int32_t* rp = nullptr;   // [M+1]
+  int32_t* col = nullptr;  // [cap]
+  int* overflow = nullptr;
+  int64_t cap = 0;
+  float thr = 0.f;
+  bool on = false;
+};
+
+int64_t near_cap(int64_t M) { return 64 * M + 1024; }
+
+void carve_near(nat::Carver& c, NearPairs* np, int64_t M) {
+  NearPairs t;
+  t.cap = near_cap(M);
+  t.rp = c.take<int32_t>(M + 1);
+  t.col = c.take<int32_t>(t.cap);
+  t.overflow = c.take<int>(1);
+  if (np) *np = t;
+}
+
+nat_status build_near(NearPairs& np, int64_t M, const double* smp, const double* center, double eps,
+                      cudaStream_t s) {
+  np.on = true;
+  np.thr = (float)(4.0 * eps * eps);
+  const double cx = center ? center[0] : 0.0, cy = center ? center[1] : 0.0, cz = center ? center[2] : 0.0;
+  const unsigned grid = (unsigned)((M + kNT - 1) / kNT);
+  NAT_CUDA_TRY(cudaMemsetAsync(np.overflow, 0, sizeof(int), s));
+  mc_near_kernel<false><<<grid, kNT, 0, s>>>(M, smp, cx, cy, cz, np.thr, np.rp, np.col, np.cap, np.overflow);
+  scan32_kernel<<<1, 1024, 0, s>>>(np.rp, M, np.cap, np.overflow);
+  mc_near_kernel<true><<<grid, kNT, 0, s>>>(M, smp, cx, cy, cz, np.thr, np.rp, np.col, np.cap, np.overflow);
+  NAT_LAUNCH_CHECK();
+  int ov = 0;
+  NAT_CUDA_TRY(cudaMemcpyAsync(&ov, np.overflow, sizeof(int), cudaMemcpyDeviceToHost, s));
+  NAT_CUDA_TRY(cudaStreamSynchronize(s));
+  if (ov) return nat::fail(NAT_ERR_WORKSPACE, "more than %lld close sample pairs", (long long)np.cap);
+  return NAT_OK;
+}
+
+nat_status near_apply(const NearPairs& np, int nsys, int64_t M, const double* smp, const double* k, double w,
+                      const double2* p, const double2* g, double2* R, cudaStream_t s) {
+  if (!np.on) return NAT_OK;
+  for (int s0 = 0; s0 < nsys; s0 += 64) {
+    const int nb = (nsys - s0) < 64 ? (nsys - s0) : 64;
+    KArr ka{};
+    for (int q = 0; q < nb; ++q) ka.k[q] = k[s0 + q];
+    mc_near_apply_kernel<<<dim3((unsigned)((M + 255) / 256), nb), 256, 0, s>>>(
+        nb, M, smp, np.rp, np.col, ka, w, p ? p + (size_t)s0 * M : nullptr, g ? g + (size_t)s0 * M : nullptr,
+        R + (size_t)s0 * M);
+  }
+  NAT_LAUNCH_CHECK();
+  return NAT_OK;
+}
+
+nat::RadInput self_input(int64_t M, const double* smp, int nsys, double w) {
+  nat::RadInput in{};
+  in.n_src = M;
+  in.xyz = smp;
+  in.nrm = smp + 3 * M;
+  in.w = nullptr;
+  in.w_const = w;
+  in.n_modes = nsys;
+  in.ldpg = M;
+  in.center[0] = in.center[1] = in.center[2] = 0.0;
+  return in;
+}
+
+nat_status mc_rhs_impl(nat_prec prec, int64_t M, const double* smp, int nsys, const double* k,
+                       const double2* g, double w, double eps, double2* b, void* ws, size_t ws_bytes,
+                       const double* center, const NearPairs& np, cudaStream_t s) {
+  nat::RadInput in = self_input(M, smp, nsys, w);
+  if (center)
+    for (int d = 0; d < 3; ++d) in.center[d] = center[d];
+  in.g = g;
+  in.self_r2 = np.on ? np.thr : 0.f;
+  nat_status st = nat::radiate_internal(in, prec, k, M, smp, b, ws, ws_bytes, true, s);
+  if (st != NAT_OK) return st;
+  st = near_apply(np, nsys, M, smp, k, w, nullptr, g, b, s);
+  if (st != NAT_OK) return st;
+  rhs_combine_kernel<<<dim3((unsigned)((M + 255) / 256), nsys), 256, 0, s>>>(nsys, M, eps, g, b);
+  NAT_LAUNCH_CHECK();
+  return NAT_OK;
+}
+
+nat_status mc_apply_impl(nat_prec prec, int64_t M, const double* smp, int nsys, const double* k,
+                         const double2* p, double w, double2* out, void* ws, size_t ws_bytes,
+                         const double* center, const NearPairs& np, cudaStream_t s) {
+  nat::RadInput in = self_input(M, smp, nsys, w);
+  if (center)
+    for (int d = 0; d < 3; ++d) in.center[d] = center[d];
+  in.p = p;
+  in.self_r2 = np.on ? np.thr : 0.f;
+  nat_status st = nat::radiate_internal(in, prec, k, M, smp, out, ws, ws_bytes, true, s);
+  if (st != NAT_OK) return st;
+  st = near_apply(np, nsys, M, smp, k, w, p, nullptr, out, s);
+  if (st != NAT_OK) return st;
+  apply_combine_kernel<<<dim3((unsigned)((M + 255) / 256), nsys), 256, 0, s>>>(nsys, M, p, out);
+  NAT_LAUNCH_CHECK();
+  return NAT_OK;
+}
+
+nat_status check_k(int n, const double* k) {
+  NAT_REQUIRE(k, "k must be a host array");
+  for (int m = 0; m < n; ++m)
+    NAT_REQUIRE(k[m] >= 0.0 && k[m] < 1e300, "k[%d] = %g must be finite and >= 0", m, k[m]);
+  return NAT_OK;
+}
+
+}  // namespace
+
+extern "C" nat_status nat_mc_sample(const nat_mesh* mesh, const nat_geom* geom, int64_t M, uint64_t seed,
+                                    uint64_t stream_id, double* samples, int32_t* sample_tri,
+                                    nat_stream_t stream) {
+  NAT_REQUIRE(mesh && geom, "mesh and geom must be non-null");
+  NAT_REQUIRE(M >= 1 && M < (1LL << 32), "M must be in [1, 2^32)");
+  NAT_REQUIRE(geom->n_tri == mesh->n_tri && mesh->n_tri >= 1, "inconsistent n_tri");
+  NAT_REQUIRE_DEV(mesh->vxyz);
+  NAT_REQUIRE_DEV(mesh->tri);
+  NAT_REQUIRE_DEV(geom->normal);
+  NAT_REQUIRE_DEV(geom->area_cdf);
+  NAT_REQUIRE_DEV(samples);
+  NAT_REQUIRE_DEV(sample_tri);
+  mc_sample_kernel<<<(unsigned)((M + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      M, seed, stream_id, mesh->n_vert, mesh->n_tri, mesh->vxyz, mesh->tri, geom->normal, geom->area_cdf,
+      samples, sample_tri);
+  NAT_LAUNCH_CHECK();
+  return NAT_OK;
+}
+
+extern "C" nat_status nat_mc_check_coincident(int64_t M, const double* samples, int64_t* pair, void* ws,
+                                              size_t ws_bytes, nat_stream_t stream) {
+  NAT_REQUIRE(M >= 1 && pair, "need M >= 1 and a host pair[2]");
+  NAT_REQUIRE(ws_bytes >= 8, "workspace must hold 8 bytes");
+  NAT_REQUIRE_DEV(samples);
+  NAT_REQUIRE_DEV(ws);
+  cudaStream_t s = (cudaStream_t)stream;
+  unsigned long long* best = (unsigned long long*)ws;
+  init_best_kernel<<<1, 1, 0, s>>>(best);
+  coincident_kernel<<<(unsigned)((M + kCT - 1) / kCT), kCT, 0, s>>>(M, samples, best);
+  NAT_LAUNCH_CHECK();
+  unsigned long long h = 0;
+  NAT_CUDA_TRY(cudaMemcpyAsync(&h, best, 8, cudaMemcpyDeviceToHost, s));
+  NAT_CUDA_TRY(cudaStreamSynchronize(s));
+  if (h == ~0ull) {
+    pair[0] = pair[1] = -1;
+    return NAT_OK;
+  }
+  pair[0] = (int64_t)(h >> 32);
+  pair[1] = (int64_t)(h & 0xffffffffull);
+  return nat::fail(NAT_ERR_SINGULAR, "coincident samples (%lld, %lld)", (long long)pair[0], (long long)pair[1]);
+}
+
+extern "C" size_t nat_mc_op_workspace(nat_prec prec, int64_t M, int n_sys) {
+  nat::Carver c(nullptr);
+  carve_near(c, nullptr, M);
+  c.take<char>(nat::radiate_ws_bytes(prec, M, n_sys, M));
+  return c.bytes();
+}
+
+namespace {
+// Standalone a9 / a10 calls: near-pair list (fp32 path) + radiation scratch in ws.
+nat_status op_setup(nat_prec prec, int64_t M, int n_sys, const double* smp, double eps, void* ws, size_t ws_bytes,
+                    NearPairs& np, void** rad, size_t* rad_bytes, cudaStream_t s) {
+  nat::Carver c(ws);
+  carve_near(c, &np, M);
+  *rad_bytes = nat::radiate_ws_bytes(prec, M, n_sys, M);
+  *rad = c.take<char>(*rad_bytes);
+  if (ws_bytes < c.bytes()) return nat::fail(NAT_ERR_WORKSPACE, "workspace %zu < %zu", ws_bytes, c.bytes());
+  if (prec == NAT_FP32 && eps > 0) return build_near(np, M, smp, nullptr, eps, s);
+  return NAT_OK;
+}
+}  // namespace
+
+extern "C" nat_status nat_mc_rhs(nat_prec prec, int64_t M, const double* samples, int n_sys, const double* k,
+                                 const void* g, double w, double eps, void* b, void* ws, size_t ws_bytes,
+                                 nat_stream_t stream) {
+  NAT_REQUIRE(prec == NAT_FP32 || prec == NAT_FP64, "bad precision %d", (int)prec);
+  NAT_REQUIRE(M >= 1 && n_sys >= 1, "need M >= 1 and n_sys >= 1");
+  nat_status st = check_k(n_sys, k);
+  if (st != NAT_OK) return st;
+  NAT_REQUIRE_DEV(samples);
+  NAT_REQUIRE_DEV(g);
+  NAT_REQUIRE_DEV(b);
+  NAT_REQUIRE_DEV(ws);
+  NearPairs np;
+  void* rad;
+  size_t rad_bytes;
+  st = op_setup(prec, M, n_sys, samples, eps, ws, ws_bytes, np, &rad, &rad_bytes, (cudaStream_t)stream);
+  if (st != NAT_OK) return st;
+  return mc_rhs_impl(prec, M, samples, n_sys, k, (const double2*)g, w, eps, (double2*)b, rad, rad_bytes,
+                     nullptr, np, (cudaStream_t)stream);
+}
+
+extern "C" nat_status nat_mc_apply(nat_prec prec, int64_t M, const double* samples, int n_sys, const double* k,
+                                   const void* p, double w, double eps, void* out, void* ws, size_t ws_bytes,
+                                   nat_stream_t stream) {
+  NAT_REQUIRE(prec == NAT_FP32 || prec == NAT_FP64, "bad precision %d", (int)prec);
+  NAT_REQUIRE(M >= 1 && n_sys >= 1, "need M >= 1 and n_sys >= 1");
+  nat_status st = check_k(n_sys, k);
+  if (st != NAT_OK) return st;
+  NAT_REQUIRE_DEV(samples);
+  NAT_REQUIRE_DEV(p);
+  NAT_REQUIRE_DEV(out);
+  NAT_REQUIRE_DEV(ws);
+  NearPairs np;
+  void* rad;
+  size_t rad_bytes;
+  st = op_setup(prec, M, n_sys, samples, eps, ws, ws_bytes, np, &rad, &rad_bytes, (cudaStream_t)stream);
+  if (st != NAT_OK) return st;
+  return mc_apply_impl(prec, M, samples, n_sys, k, (const double2*)p, w, (double2*)out, rad, rad_bytes, nullptr,
+                       np, (cudaStream_t)stream);
+}
+
+namespace {
+struct McWs {
+  unsigned long long* best;
+  double2* gs;
+  double2* b;
+  nat::KrylovWs kw;
+  void* rad;
+  size_t rad_bytes;
+  NearPairs np;
+};
+
+size_t mc_carve(nat::Carver& c, McWs* w, nat_prec prec, int64_t M, int n_sys, int max_iter) {
+  const int nb = n_sys < 64 ? n_sys : 64;
+  McWs t;
+  t.best = c.take<unsigned long long>(1);
+  t.gs = c.take<double2>((size_t)nb * M);
+  t.b = c.take<double2>((size_t)nb * M);
+  nat::krylov_workspace(nb, M, M, max_iter, c, &t.kw);
+  t.rad_bytes = nat::radiate_ws_bytes(prec, M, nb, M);
+  t.rad = c.take<char>(t.rad_bytes);
+  carve_near(c, &t.np, M);
+  if (w) *w = t;
+  return c.bytes();
+}
+}  // namespace
+
+extern "C" size_t nat_mc_workspace(nat_prec prec, int64_t M, int n_sys, int max_iter) {
+  if (max_iter <= 0) max_iter = 200;
+  nat::Carver c(nullptr);
+  return mc_carve(c, nullptr, prec, M, n_sys, max_iter);
+}
+
+extern "C" nat_status nat_mc_surface_pressure(const nat_mesh* mesh, const nat_geom* geom, int n_sys,
+                                              const double* k, const void* g_tri, const nat_mc_opts* opts,
+                                              nat_prec prec, double tol, int max_iter, double* samples_out,
+                                              int32_t* sample_tri_out, void* p_out, void* ws, size_t ws_bytes,
+                                              nat_solve_info* info, nat_stream_t stream) {
+  auto t_start = std::chrono::steady_clock::now();
+  NAT_REQUIRE(mesh && geom && opts, "mesh, geom and opts must be non-null");
+  NAT_REQUIRE(prec == NAT_FP32 || prec == NAT_FP64, "bad precision %d", (int)prec);
+  NAT_REQUIRE(n_sys >= 1, "n_sys must be >= 1");
+  const int64_t M = opts->M;
+  NAT_REQUIRE(M >= 1 && M < (1LL << 31), "M must be in [1, 2^31) (S:170)");
+  NAT_REQUIRE(geom->total_area > 0, "geom->total_area must come from nat_mesh_prepare");
+  nat_status st = check_k(n_sys, k);
+  if (st != NAT_OK) return st;
+  if (tol <= 0) tol = 1e-6;
+  if (max_iter <= 0) max_iter = 200;
+  NAT_REQUIRE_DEV(g_tri);
+  NAT_REQUIRE_DEV(samples_out);
+  NAT_REQUIRE_DEV(sample_tri_out);
+  NAT_REQUIRE_DEV(p_out);
+  NAT_REQUIRE_DEV(ws);
+  nat::Carver c(ws);
+  McWs w;
+  size_t need = mc_carve(c, &w, prec, M, n_sys, max_iter);
+  if (ws_bytes < need) return nat::fail(NAT_ERR_WORKSPACE, "workspace %zu < %zu", ws_bytes, need);
+  cudaStream_t s = (cudaStream_t)stream;
+  // a8: samples (or the caller's set, e.g. a host Poisson-disk set, enters unchanged)
+  if (opts->samples_in) {
+    NAT_REQUIRE_DEV(opts->samples_in);
+    NAT_REQUIRE_DEV(opts->sample_tri_in);
+    NAT_CUDA_TRY(cudaMemcpyAsync(samples_out, opts->samples_in, sizeof(double) * 6 * M, cudaMemcpyDeviceToDevice, s));
+    NAT_CUDA_TRY(cudaMemcpyAsync(sample_tri_out, opts->sample_tri_in, sizeof(int32_t) * M, cudaMemcpyDeviceToDevice, s));
+  } else {
+    st = nat_mc_sample(mesh, geom, M, opts->seed, opts->stream_id, samples_out, sample_tri_out, stream);
+    if (st != NAT_OK) return st;
+  }
+  int64_t pair[2];
+  st = nat_mc_check_coincident(M, samples_out, pair, w.best, 8, stream);
+  if (st != NAT_OK) return st;
+  // disk radius and off-disk weight (readings R-eps, R-weight)
+  const double area = geom->total_area;
+  const double eps = opts->eps > 0 ? opts->eps : std::sqrt(area / (nat::kPi * (double)M));
+  const double wgt = M > 1 ? (area - nat::kPi * eps * eps) / (double)(M - 1) : 0.0;
+  const double* cen = geom->center;
+  if (prec == NAT_FP32 && M > 1) {
+    st = build_near(w.np, M, samples_out, cen, eps, s);
+    if (st != NAT_OK) return st;
+  }
+  bool all_conv = true;
+  for (int s0 = 0; s0 < n_sys; s0 += 64) {
+    const int nb = (n_sys - s0) < 64 ? (n_sys - s0) : 64;
+    gather_g_kernel<<<dim3((unsigned)((M + 255) / 256), nb), 256, 0, s>>>(
+        nb, M, mesh->n_tri, (const double2*)g_tri + (size_t)s0 * mesh->n_tri, sample_tri_out, w.gs);
+    NAT_LAUNCH_CHECK();
+    st = mc_rhs_impl(prec, M, samples_out, nb, k + s0, w.gs, wgt, eps, w.b, w.rad, w.rad_bytes, cen, w.np, s);
+    if (st != NAT_OK) return st;
+    auto op = [&](const double2* in, double2* out, uint64_t, cudaStream_t ss) -> nat_status {
+      return mc_apply_impl(prec, M, samples_out, nb, k + s0, in, wgt, out, w.rad, w.rad_bytes, cen, w.np, ss);
+    };
+    std::vector<nat::KrylovResult> res;
+    double t_op = 0;
+    st = nat::gmres_batched(nb, M, M, w.b, (double2*)p_out + (size_t)s0 * M, op, tol, max_iter, w.kw, res, s,
+                            info ? &t_op : nullptr);
+    if (st != NAT_OK) return st;
+    for (int q = 0; q < nb; ++q) all_conv = all_conv && res[q].converged;
+    if (info)
+      for (int q = 0; q < nb; ++q) {
+        info[s0 + q].iters = res[q].iters;
+        info[s0 + q].converged = res[q].converged;
+        info[s0 + q].rel_residual = res[q].rel_residual;
+        info[s0 + q].t_matvec_s = t_op;
+        info[s0 + q].t_comm_s = 0;
+      }
+  }
+  NAT_CUDA_TRY(cudaStreamSynchronize(s));
+  double tt = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+  if (info)
+    for (int q = 0; q < n_sys; ++q) {
+      info[q].t_total_s = tt;
+    }
+  return all_conv ? NAT_OK : NAT_WARN_NOT_CONVERGED;
+}

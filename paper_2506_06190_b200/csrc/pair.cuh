@@ -42,3 +42,12 @@ __device__ __forceinline__ void pair_accumulate(R dx, R dy, R dz, R nx, R ny, R 
 }
 
 }  // namespace nat
+
+namespace nat {
+// Squared distance in fp32 exactly as the radiation / MC kernels form it.  The MC
+// near-pair list uses the same function so that the pairs the fp32 kernel skips are
+// exactly the pairs evaluated in fp64.
+__device__ __forceinline__ float pair_r2_f32(float dx, float dy, float dz) {
+  return __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
+}
+}  // namespace nat

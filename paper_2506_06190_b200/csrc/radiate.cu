@@ -15,6 +15,8 @@
 //    fixed-order fp64 reduction (deterministic, no atomics).
 #include "async_copy.cuh"
 #include "nat_internal.cuh"
+#include "pair.cuh"
+#include "radiate.cuh"
 
 namespace {
 
@@ -27,6 +29,12 @@ struct Rec {
   static constexpr int NF = ((6 + 6 * MB) + 3) / 4 * 4;  // floats per source record
 };
 
+constexpr int kMaxModes = 64;  // wavenumbers per launch (passed by value)
+struct KVals {
+  float f[kMaxModes];
+  double d[kMaxModes];
+};
+
 struct RadParams {
   const void* rec;      // [n_mchunk][n_src_pad][NF] records
   int64_t n_src_pad;    // multiple of the tile
@@ -35,10 +43,10 @@ struct RadParams {
   const double* lis;    // [3][n_lis]
   int64_t n_lis;
   double cx, cy, cz;    // coordinate origin
-  const float* kf;      // [n_mchunk*MB] wavenumbers (fp32)
-  const double* kd;     // [n_mchunk*MB] wavenumbers (fp64)
+  KVals k;              // wavenumbers of this launch (<= kMaxModes)
   double2* out;         // [n_split][n_modes][n_lis]
   int n_modes;
+  float self_r2;        // SELF mode threshold (see radiate.cuh)
 };
 
 // ------------------------------------------------------------------------------------
@@ -47,9 +55,10 @@ struct RadParams {
 template <typename T>
 __global__ void stage_kernel(int64_t n_src, int64_t n_src_pad, int NF, int MB, int n_mchunk,
                              const double* __restrict__ xyz, const double* __restrict__ nrm,
-                             const double* __restrict__ w, const double2* __restrict__ p,
-                             const double2* __restrict__ g, const double* __restrict__ kd,
-                             int n_modes, double cx, double cy, double cz, T* __restrict__ rec) {
+                             const double* __restrict__ w, double w_const,
+                             const double2* __restrict__ p, const double2* __restrict__ g,
+                             int64_t ldpg, const KVals kv, int n_modes, double cx,
+                             double cy, double cz, T* __restrict__ rec) {
   int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (s >= n_src_pad) return;
   double x, y, z, nx, ny, nz, ws;
@@ -60,7 +69,7 @@ __global__ void stage_kernel(int64_t n_src, int64_t n_src_pad, int NF, int MB, i
     nx = nrm[s];
     ny = nrm[n_src + s];
     nz = nrm[2 * n_src + s];
-    ws = w[s] * nat::kInv4Pi;
+    ws = (w ? w[s] : w_const) * nat::kInv4Pi;
   } else {  // padding: far away, zero weight -> contributes exactly 0
     x = y = z = 3.0e3;
     nx = 1.0;
@@ -79,13 +88,13 @@ __global__ void stage_kernel(int64_t n_src, int64_t n_src_pad, int NF, int MB, i
       int mode = c * MB + m;
       double ar = 0, ai = 0, br = 0, bi = 0, k = 0;
       if (mode < n_modes && ws != 0.0) {
-        double2 pv = p[(size_t)mode * n_src + s];
-        double2 gv = g[(size_t)mode * n_src + s];
+        double2 pv = p ? p[(size_t)mode * ldpg + s] : make_double2(0.0, 0.0);
+        double2 gv = g ? g[(size_t)mode * ldpg + s] : make_double2(0.0, 0.0);
         ar = ws * pv.x;
         ai = ws * pv.y;
         br = ws * gv.x;
         bi = ws * gv.y;
-        k = kd[mode];
+        k = kv.d[mode];
       }
       T* q = r + 6 + 6 * m;
       q[0] = (T)(-ar);
@@ -108,7 +117,10 @@ __device__ __forceinline__ float rsqrt_approx(float x) {
   return y;
 }
 
-template <int R, int MB>
+// SELF = 1: targets coincide with the sources (MC operators): the self pair has d = 0
+// exactly (same fp64 value, same cast) and is excluded by setting 1/r = 0, which makes
+// its contribution exactly 0 (the disk terms are added by the caller).
+template <int R, int MB, int SELF>
 __global__ void __launch_bounds__(kThreads) radiate_f32_kernel(RadParams prm) {
   constexpr int NF = Rec<MB>::NF;
   constexpr int kTileFloats = kTile * NF;
@@ -133,7 +145,7 @@ __global__ void __launch_bounds__(kThreads) radiate_f32_kernel(RadParams prm) {
   }
   float kk[MB];
 #pragma unroll
-  for (int m = 0; m < MB; ++m) kk[m] = prm.kf[mch * MB + m];
+  for (int m = 0; m < MB; ++m) kk[m] = prm.k.f[mch * MB + m];
 #pragma unroll
   for (int q = 0; q < R * MB; ++q) dacc[q * kThreads + tid] = make_double2(0.0, 0.0);
 
@@ -181,9 +193,9 @@ __global__ void __launch_bounds__(kThreads) radiate_f32_kernel(RadParams prm) {
         const float dx = f[0] - tx[r];
         const float dy = f[1] - ty[r];
         const float dz = f[2] - tz[r];
-        const float r2 = fmaf(dz, dz, fmaf(dy, dy, dx * dx));
+        const float r2 = nat::pair_r2_f32(dx, dy, dz);
         const float dn = fmaf(dz, f[5], fmaf(dy, f[4], dx * f[3]));
-        const float rho = rsqrt_approx(r2);
+        const float rho = SELF ? (r2 > prm.self_r2 ? rsqrt_approx(r2) : 0.f) : rsqrt_approx(r2);
         const float qq = dn * (rho * rho);
         const float rr = r2 * rho;
 #pragma unroll
@@ -253,7 +265,7 @@ __global__ void __launch_bounds__(kThreads) radiate_f64_kernel(RadParams prm) {
     tz[r] = prm.lis[2 * prm.n_lis + l] - prm.cz;
     ar[r] = ai[r] = 0.0;
   }
-  const double k = prm.kd[mch];
+  const double k = prm.k.d[mch];
   const int t0 = split * prm.chunk_tiles;
   const int t1 = min(t0 + prm.chunk_tiles, prm.n_tiles);
   const double* src = static_cast<const double*>(prm.rec) + (size_t)mch * prm.n_src_pad * NF;
@@ -288,7 +300,7 @@ __global__ void __launch_bounds__(kThreads) radiate_f64_kernel(RadParams prm) {
         const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
         const double dn = fma(dz, f[5], fma(dy, f[4], dx * f[3]));
         const double rr = sqrt(r2);
-        const double rho = 1.0 / rr;
+        const double rho = r2 > 0.0 ? 1.0 / rr : 0.0;  // self pair (MC operators) -> 0
         const double qq = dn * (rho * rho);
         double sn, cs;
         sincos(k * rr, &sn, &cs);
@@ -419,18 +431,15 @@ Plan make_plan(nat_prec prec, int64_t n_src, int n_modes, int64_t n_lis) {
   return pl;
 }
 
-size_t plan_ws(const Plan& pl, int n_modes, int64_t n_lis, nat::Carver& c, void** rec, float** kf,
-               double** kd, double2** part) {
+size_t plan_ws(const Plan& pl, int n_modes, int64_t n_lis, nat::Carver& c, void** rec, double2** part) {
   *rec = pl.fp64 ? (void*)c.take<double>(pl.rec_elems) : (void*)c.take<float>(pl.rec_elems);
-  *kf = c.take<float>((size_t)pl.n_mchunk * pl.MB);
-  *kd = c.take<double>((size_t)pl.n_mchunk * pl.MB);
   *part = pl.n_split > 1 ? c.take<double2>((size_t)pl.n_split * n_modes * n_lis) : nullptr;
   return c.bytes();
 }
 
-template <int R, int MB>
+template <int R, int MB, int SELF>
 cudaError_t launch_f32(const Plan& pl, const RadParams& prm, cudaStream_t s) {
-  auto kern = radiate_f32_kernel<R, MB>;
+  auto kern = radiate_f32_kernel<R, MB, SELF>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
   if (e != cudaSuccess) return e;
   dim3 grid((unsigned)pl.tgt_tiles, (unsigned)pl.n_split, (unsigned)pl.n_mchunk);
@@ -438,17 +447,99 @@ cudaError_t launch_f32(const Plan& pl, const RadParams& prm, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+template <int SELF>
+cudaError_t launch_f32_mb(const Plan& pl, const RadParams& prm, cudaStream_t s) {
+  switch (pl.MB) {
+    case 1: return launch_f32<4, 1, SELF>(pl, prm, s);
+    case 2: return launch_f32<4, 2, SELF>(pl, prm, s);
+    case 3: return launch_f32<4, 3, SELF>(pl, prm, s);
+    default: return launch_f32<4, 4, SELF>(pl, prm, s);
+  }
+}
+
 }  // namespace
 
-extern "C" size_t nat_radiate_workspace(nat_prec prec, int64_t n_src, int n_modes, int64_t n_lis) {
+namespace nat {
+
+size_t radiate_ws_bytes(nat_prec prec, int64_t n_src, int n_modes, int64_t n_lis) {
   if (n_src <= 0 || n_modes <= 0 || n_lis <= 0) return 0;
-  Plan pl = make_plan(prec, n_src, n_modes, n_lis);
-  nat::Carver c(nullptr);
+  const int nm = n_modes < kMaxModes ? n_modes : kMaxModes;
+  Plan pl = make_plan(prec, n_src, nm, n_lis);
+  Carver c(nullptr);
   void* rec;
-  float* kf;
-  double* kd;
   double2* part;
-  return plan_ws(pl, n_modes, n_lis, c, &rec, &kf, &kd, &part);
+  return plan_ws(pl, nm, n_lis, c, &rec, &part);
+}
+
+nat_status radiate_internal(const RadInput& in, nat_prec prec, const double* k, int64_t n_lis,
+                            const double* lis, double2* out, void* ws, size_t ws_bytes, bool self,
+                            cudaStream_t s) {
+  for (int m0 = 0; m0 < in.n_modes; m0 += kMaxModes) {
+    const int nm = (in.n_modes - m0) < kMaxModes ? (in.n_modes - m0) : kMaxModes;
+    Plan pl = make_plan(prec, in.n_src, nm, n_lis);
+    Carver c(ws);
+    void* rec;
+    double2* part;
+    size_t need = plan_ws(pl, nm, n_lis, c, &rec, &part);
+    if (ws_bytes < need) return fail(NAT_ERR_WORKSPACE, "workspace %zu < %zu", ws_bytes, need);
+    KVals kv{};
+    for (int m = 0; m < nm; ++m) {
+      kv.d[m] = k[m0 + m];
+      kv.f[m] = (float)kv.d[m];
+    }
+    const double2* p = in.p ? in.p + (size_t)m0 * in.ldpg : nullptr;
+    const double2* g = in.g ? in.g + (size_t)m0 * in.ldpg : nullptr;
+    unsigned sblocks = (unsigned)((pl.n_src_pad + 255) / 256);
+    if (pl.fp64)
+      stage_kernel<double><<<sblocks, 256, 0, s>>>(in.n_src, pl.n_src_pad, pl.NF, pl.MB, pl.n_mchunk,
+          in.xyz, in.nrm, in.w, in.w_const, p, g, in.ldpg, kv, nm, in.center[0], in.center[1],
+          in.center[2], (double*)rec);
+    else
+      stage_kernel<float><<<sblocks, 256, 0, s>>>(in.n_src, pl.n_src_pad, pl.NF, pl.MB, pl.n_mchunk,
+          in.xyz, in.nrm, in.w, in.w_const, p, g, in.ldpg, kv, nm, in.center[0], in.center[1],
+          in.center[2], (float*)rec);
+    NAT_LAUNCH_CHECK();
+    RadParams prm{};
+    prm.rec = rec;
+    prm.n_src_pad = pl.n_src_pad;
+    prm.n_tiles = pl.n_tiles;
+    prm.chunk_tiles = pl.chunk_tiles;
+    prm.lis = lis;
+    prm.n_lis = n_lis;
+    prm.cx = in.center[0];
+    prm.cy = in.center[1];
+    prm.cz = in.center[2];
+    prm.k = kv;
+    double2* dst = out + (size_t)m0 * n_lis;
+    prm.out = pl.n_split > 1 ? part : dst;
+    prm.n_modes = nm;
+    prm.self_r2 = in.self_r2;
+    cudaError_t e = cudaSuccess;
+    if (pl.fp64) {
+      auto kern = radiate_f64_kernel<2>;
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
+      if (e == cudaSuccess) {
+        dim3 grid((unsigned)pl.tgt_tiles, (unsigned)pl.n_split, (unsigned)pl.n_mchunk);
+        kern<<<grid, kThreads, pl.smem, s>>>(prm);
+        e = cudaGetLastError();
+      }
+    } else {
+      e = self ? launch_f32_mb<1>(pl, prm, s) : launch_f32_mb<0>(pl, prm, s);
+    }
+    if (e != cudaSuccess) return fail(NAT_ERR_CUDA, "radiate launch: %s", cudaGetErrorString(e));
+    if (pl.n_split > 1) {
+      int64_t n = (int64_t)nm * n_lis;
+      reduce_splits_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(part, pl.n_split, n, dst);
+      NAT_LAUNCH_CHECK();
+    }
+  }
+  return NAT_OK;
+}
+
+}  // namespace nat
+
+extern "C" size_t nat_radiate_workspace(nat_prec prec, int64_t n_src, int n_modes, int64_t n_lis) {
+  return nat::radiate_ws_bytes(prec, n_src, n_modes, n_lis);
 }
 
 extern "C" nat_status nat_radiate_field(const nat_sources* src, nat_prec prec, const double* k,
@@ -467,82 +558,19 @@ extern "C" nat_status nat_radiate_field(const nat_sources* src, nat_prec prec, c
   NAT_REQUIRE_DEV(src->g);
   NAT_REQUIRE_DEV(lis_xyz);
   NAT_REQUIRE_DEV(p_out);
-  const int n_modes = src->n_modes;
-  Plan pl = make_plan(prec, src->n_src, n_modes, n_lis);
-  nat::Carver c(ws);
-  void* rec;
-  float* kf;
-  double* kd;
-  double2* part;
-  size_t need = plan_ws(pl, n_modes, n_lis, c, &rec, &kf, &kd, &part);
-  if (ws_bytes < need) return nat::fail(NAT_ERR_WORKSPACE, "workspace %zu < %zu", ws_bytes, need);
   NAT_REQUIRE_DEV(ws);
-  cudaStream_t s = (cudaStream_t)stream;
-
-  // wavenumbers -> device (padded with zeros)
-  int nk = pl.n_mchunk * pl.MB;
-  std::string hbuf(nk * (sizeof(float) + sizeof(double)), '\0');
-  float* hkf = reinterpret_cast<float*>(&hbuf[0]);
-  double* hkd = reinterpret_cast<double*>(&hbuf[nk * sizeof(float)]);
-  for (int m = 0; m < nk; ++m) {
-    hkd[m] = m < n_modes ? k[m] : 0.0;
-    hkf[m] = (float)hkd[m];
-  }
-  NAT_CUDA_TRY(cudaMemcpyAsync(kf, hkf, nk * sizeof(float), cudaMemcpyHostToDevice, s));
-  NAT_CUDA_TRY(cudaMemcpyAsync(kd, hkd, nk * sizeof(double), cudaMemcpyHostToDevice, s));
-
-  const double cx = src->center[0], cy = src->center[1], cz = src->center[2];
-  unsigned sblocks = (unsigned)((pl.n_src_pad + 255) / 256);
-  if (pl.fp64)
-    stage_kernel<double><<<sblocks, 256, 0, s>>>(src->n_src, pl.n_src_pad, pl.NF, pl.MB, pl.n_mchunk,
-        src->xyz, src->nrm, src->w, (const double2*)src->p, (const double2*)src->g, kd, n_modes,
-        cx, cy, cz, (double*)rec);
-  else
-    stage_kernel<float><<<sblocks, 256, 0, s>>>(src->n_src, pl.n_src_pad, pl.NF, pl.MB, pl.n_mchunk,
-        src->xyz, src->nrm, src->w, (const double2*)src->p, (const double2*)src->g, kd, n_modes,
-        cx, cy, cz, (float*)rec);
-  NAT_LAUNCH_CHECK();
-
-  RadParams prm{};
-  prm.rec = rec;
-  prm.n_src_pad = pl.n_src_pad;
-  prm.n_tiles = pl.n_tiles;
-  prm.chunk_tiles = pl.chunk_tiles;
-  prm.lis = lis_xyz;
-  prm.n_lis = n_lis;
-  prm.cx = cx;
-  prm.cy = cy;
-  prm.cz = cz;
-  prm.kf = kf;
-  prm.kd = kd;
-  prm.out = pl.n_split > 1 ? part : (double2*)p_out;
-  prm.n_modes = n_modes;
-
-  cudaError_t e = cudaSuccess;
-  if (pl.fp64) {
-    auto kern = radiate_f64_kernel<2>;
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
-    if (e == cudaSuccess) {
-      dim3 grid((unsigned)pl.tgt_tiles, (unsigned)pl.n_split, (unsigned)pl.n_mchunk);
-      kern<<<grid, kThreads, pl.smem, s>>>(prm);
-      e = cudaGetLastError();
-    }
-  } else {
-    switch (pl.MB) {
-      case 1: e = launch_f32<4, 1>(pl, prm, s); break;
-      case 2: e = launch_f32<4, 2>(pl, prm, s); break;
-      case 3: e = launch_f32<4, 3>(pl, prm, s); break;
-      default: e = launch_f32<4, 4>(pl, prm, s); break;
-    }
-  }
-  if (e != cudaSuccess) return nat::fail(NAT_ERR_CUDA, "radiate launch: %s", cudaGetErrorString(e));
-  if (pl.n_split > 1) {
-    int64_t n = (int64_t)n_modes * n_lis;
-    reduce_splits_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(part, pl.n_split, n,
-                                                                      (double2*)p_out);
-    NAT_LAUNCH_CHECK();
-  }
-  return NAT_OK;
+  nat::RadInput in{};
+  in.n_src = src->n_src;
+  in.xyz = src->xyz;
+  in.nrm = src->nrm;
+  in.w = src->w;
+  in.n_modes = src->n_modes;
+  in.p = (const double2*)src->p;
+  in.g = (const double2*)src->g;
+  in.ldpg = src->n_src;
+  for (int d = 0; d < 3; ++d) in.center[d] = src->center[d];
+  return nat::radiate_internal(in, prec, k, n_lis, lis_xyz, (double2*)p_out, ws, ws_bytes, false,
+                               (cudaStream_t)stream);
 }
 
 namespace {

@@ -1,0 +1,28 @@
+// Internal radiation entry shared by nat_radiate_field and the MC operators.
+#pragma once
+#include "nat_internal.cuh"
+
+namespace nat {
+
+struct RadInput {
+  int64_t n_src;
+  const double* xyz;  // [3][n_src]
+  const double* nrm;  // [3][n_src]
+  const double* w;    // [n_src] or nullptr => w_const
+  double w_const;
+  int n_modes;
+  const double2* p;   // [n_modes][ldpg] or nullptr (=> 0)
+  const double2* g;   // [n_modes][ldpg] or nullptr (=> 0)
+  int64_t ldpg;
+  double center[3];
+  float self_r2;      // self mode: pairs with fp32 r^2 <= self_r2 are skipped (0 => self pair only)
+};
+
+size_t radiate_ws_bytes(nat_prec prec, int64_t n_src, int n_modes, int64_t n_lis);
+// out[m][l] (c128 [n_modes][n_lis]) = sum_s w_s [p_ms dG_m/dn_y - g_ms G_m](x_l, y_s);
+// self = true excludes the pair with identical coordinates (targets == sources).
+nat_status radiate_internal(const RadInput& in, nat_prec prec, const double* k, int64_t n_lis,
+                            const double* lis, double2* out, void* ws, size_t ws_bytes, bool self,
+                            cudaStream_t s);
+
+}  // namespace nat

@@ -92,7 +92,7 @@ _SIGS = {
     "nat_mc_op_workspace": (_SZ, [C.c_int, _I64, C.c_int]),
     "nat_mc_rhs": (C.c_int, [C.c_int, _I64, _P, C.c_int, C.POINTER(_D), _P, _D, _D, _P, _P,
                              _SZ, _P]),
-    "nat_mc_apply": (C.c_int, [C.c_int, _I64, _P, C.c_int, C.POINTER(_D), _P, _D, _P, _P, _SZ,
+    "nat_mc_apply": (C.c_int, [C.c_int, _I64, _P, C.c_int, C.POINTER(_D), _P, _D, _D, _P, _P, _SZ,
                                _P]),
     "nat_mc_check_coincident": (C.c_int, [_I64, _P, C.POINTER(_I64), _P, _SZ, _P]),
     "nat_mc_workspace": (_SZ, [C.c_int, _I64, C.c_int, C.c_int]),
@@ -411,6 +411,101 @@ class Comm:
         if self.handle:
             _check(lib().nat_comm_destroy(self.handle))
             self.handle = C.c_void_p()
+
+
+# ------------------------------------------------------------------------------------
+# Monte-Carlo BEM (rows a8-a10)
+# ------------------------------------------------------------------------------------
+def _karr(k):
+    k = np.ascontiguousarray(np.atleast_1d(np.asarray(k, dtype=np.float64)))
+    return k, k.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def nat_mc_sample(mesh: Mesh, geom: Geom, M: int, seed: int, stream_id: int = 0):
+    """Returns (samples (6, M) float64 [xyz; normal], sample_tri (M,) int32)."""
+    dev = mesh.vxyz.device
+    smp = torch.empty(6, M, dtype=torch.float64, device=dev)
+    tri = torch.empty(M, dtype=torch.int32, device=dev)
+    _check(lib().nat_mc_sample(C.byref(mesh.c()), C.byref(geom.c()), M, seed, stream_id, _ptr(smp),
+                               _ptr(tri), _stream()))
+    return smp, tri
+
+
+def nat_mc_check_coincident(samples: torch.Tensor):
+    M = samples.shape[1]
+    pair = (C.c_int64 * 2)()
+    ws = _ws(256, samples.device)
+    _check(lib().nat_mc_check_coincident(M, _ptr(samples), pair, _ptr(ws), ws.numel(), _stream()))
+    return None
+
+
+def mc_weights(total_area: float, M: int, eps: float = 0.0):
+    """(eps, w) of readings R-eps / R-weight: eps = sqrt(|Gamma|/(pi M)),
+    w = (|Gamma| - pi eps^2)/(M - 1)."""
+    import math
+    eps = eps if eps > 0 else math.sqrt(total_area / (math.pi * M))
+    w = (total_area - math.pi * eps * eps) / (M - 1) if M > 1 else 0.0
+    return eps, w
+
+
+def nat_mc_rhs(samples, k, g, w, eps, prec="fp32"):
+    pr = _prec(prec)
+    M = samples.shape[1]
+    g = torch.atleast_2d(g).to(torch.complex128).contiguous()
+    ks, kp = _karr(k)
+    b = torch.empty_like(g)
+    ws = _ws(lib().nat_mc_op_workspace(pr, M, g.shape[0]), samples.device)
+    _check(lib().nat_mc_rhs(pr, M, _ptr(samples), g.shape[0], kp, _ptr(g), float(w), float(eps), _ptr(b),
+                            _ptr(ws), ws.numel(), _stream()))
+    return b
+
+
+def nat_mc_apply(samples, k, p, w, eps, prec="fp32"):
+    pr = _prec(prec)
+    M = samples.shape[1]
+    p = torch.atleast_2d(p).to(torch.complex128).contiguous()
+    ks, kp = _karr(k)
+    out = torch.empty_like(p)
+    ws = _ws(lib().nat_mc_op_workspace(pr, M, p.shape[0]), samples.device)
+    _check(lib().nat_mc_apply(pr, M, _ptr(samples), p.shape[0], kp, _ptr(p), float(w), float(eps), _ptr(out), _ptr(ws),
+                              ws.numel(), _stream()))
+    return out
+
+
+class McPlan:
+    """Pre-sized workspace for repeated nat_mc_surface_pressure calls."""
+
+    def __init__(self, M, n_sys, prec="fp32", max_iter=200, device="cuda"):
+        self.prec = _prec(prec)
+        self.ws = _ws(lib().nat_mc_workspace(self.prec, M, n_sys, max_iter), device)
+
+
+def nat_mc_surface_pressure(mesh: Mesh, geom: Geom, k, g_tri, M: int, seed: int = 0, stream_id: int = 0,
+                            eps: float = 0.0, prec="fp32", tol=1e-6, max_iter=200, samples_in=None,
+                            sample_tri_in=None, plan: Optional[McPlan] = None, out=None):
+    """Returns (samples (6, M), sample_tri (M,), p (n_sys, M) c128, infos list)."""
+    pr = _prec(prec)
+    dev = mesh.vxyz.device
+    g_tri = torch.atleast_2d(g_tri).to(torch.complex128).contiguous()
+    ks, kp = _karr(k)
+    n_sys = ks.size
+    if g_tri.shape[0] != n_sys:
+        raise NatError(-1, f"{g_tri.shape[0]} Neumann fields for {n_sys} wavenumbers")
+    if out is None:
+        smp = torch.empty(6, M, dtype=torch.float64, device=dev)
+        tri = torch.empty(M, dtype=torch.int32, device=dev)
+        p = torch.empty(n_sys, M, dtype=torch.complex128, device=dev)
+    else:
+        smp, tri, p = out
+    opts = _McOpts(M, seed, stream_id, float(eps), _ptr(samples_in), _ptr(sample_tri_in))
+    ws = plan.ws if plan is not None else _ws(lib().nat_mc_workspace(pr, M, n_sys, max_iter), dev)
+    infos = (_SolveInfo * n_sys)()
+    st = lib().nat_mc_surface_pressure(C.byref(mesh.c()), C.byref(geom.c()), n_sys, kp, _ptr(g_tri),
+                                       C.byref(opts), pr, float(tol), int(max_iter), _ptr(smp), _ptr(tri),
+                                       _ptr(p), _ptr(ws), ws.numel(), infos, _stream())
+    _check(st, allow_warn=True)
+    return smp, tri, p, [dict(iters=i.iters, converged=i.converged, rel_residual=i.rel_residual,
+                              t_total_s=i.t_total_s) for i in infos]
 
 
 def row_range(n: int, rank: int, world: int):

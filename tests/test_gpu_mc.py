@@ -1,0 +1,146 @@
+"""Rows a8 (sampling), a9 (MC right-hand side), a10 (MC operator) and the full MC
+solve: CUDA path vs oracle.  Samples are compared bit for bit (same Philox stream)."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import nat_inputs as I
+from gpu_util import rel_l2, requires_cuda, soa_to_aos, to_np
+from oracle import geometry, kernel, mc, radiate
+
+pytestmark = [pytest.mark.gpu, requires_cuda]
+
+TOL = {"fp32": 1e-4, "fp64": 1e-10}
+
+
+def _nat():
+    from paper_2506_06190_b200 import nat
+    return nat
+
+
+def _case(m):
+    nat = _nat()
+    mesh = nat.Mesh.from_numpy(m.v, m.t)
+    return geometry.mesh_prepare(m.v, m.t), mesh, nat.nat_mesh_prepare(mesh)
+
+
+@pytest.mark.parametrize("name,M,seed,sid", [("bowl", 4096, 20250606, 0), ("bowl", 1001, 7, 3),
+                                              ("c4", 2048, 20250606, 9), ("ico3", 1, 1, 2**40 + 5)])
+def test_sampling_bitwise(name, M, seed, sid):
+    nat = _nat()
+    m = {"bowl": lambda: I.bowl(64, 12, 2), "c4": lambda: I.c4_geometry(9)[0],
+         "ico3": lambda: I.icosphere(3)}[name]()
+    geo, mesh, gg = _case(m)
+    y, n, tri = mc.sample_uniform(m.v, m.t, geo, M, seed, sid)
+    smp, stri = nat.nat_mc_sample(mesh, gg, M, seed, sid)
+    s = to_np(smp)
+    assert np.array_equal(to_np(stri), tri)
+    assert np.array_equal(s[:3].T, y)
+    assert np.array_equal(s[3:].T, n)
+
+
+def _system_case(M, seed=5):
+    m = I.icosphere(3)
+    geo, mesh, gg = _case(m)
+    y, n, tri = mc.sample_uniform(m.v, m.t, geo, M, seed)
+    return m, geo, mesh, gg, y, n, tri
+
+
+@pytest.mark.parametrize("prec", ["fp32", "fp64"])
+@pytest.mark.parametrize("n_sys", [1, 3, 6])
+def test_mc_operator_and_rhs_parity(prec, n_sys):
+    nat = _nat()
+    M = 2333     # dense enough that random samples form close pairs (fp64 path)
+    m, geo, mesh, gg, y, n, tri = _system_case(M)
+    ks = list(np.linspace(0.5, 6.0, n_sys))
+    eps, w = nat.mc_weights(geo["total_area"], M)
+    g = I.random_complex((n_sys, M), 11)
+    p = I.random_complex((n_sys, M), 12)
+    smp = torch.from_numpy(np.ascontiguousarray(np.concatenate([y.T, n.T]))).cuda()
+    b = to_np(nat.nat_mc_rhs(smp, ks, torch.from_numpy(g).cuda(), w, eps, prec))
+    Ap = to_np(nat.nat_mc_apply(smp, ks, torch.from_numpy(p).cuda(), w, eps, prec))
+    for s, k in enumerate(ks):
+        A_ref, b_ref = mc.system(y, n, g[s], k, geo["total_area"])
+        assert rel_l2(b[s], b_ref) <= TOL[prec]
+        assert rel_l2(Ap[s], A_ref @ p[s]) <= TOL[prec]
+
+
+@pytest.mark.parametrize("prec", ["fp32", "fp64"])
+def test_surface_pressure_parity(prec):
+    nat = _nat()
+    m = I.bowl(32, 8, 2)
+    geo, mesh, gg = _case(m)
+    M, seed = 700, 3
+    ks = [0.5, 2.0, 4.5]
+    g_tri = I.neumann_harmonics(m, 3)
+    y, n, tri, p_ref, infos = mc.surface_pressure(m.v, m.t, geo, ks, g_tri, M, seed, tol=1e-13)
+    tol = 1e-6 if prec == "fp32" else 1e-12
+    smp, stri, p, ginfo = nat.nat_mc_surface_pressure(mesh, gg, ks, torch.from_numpy(g_tri).cuda(), M, seed,
+                                                      prec=prec, tol=tol)
+    assert np.array_equal(to_np(stri), tri)
+    for s in range(3):
+        # the true residual of the fp32 path is floored by the fp32 operator (~1e-7)
+        assert ginfo[s]["converged"] == 1 and ginfo[s]["rel_residual"] <= (1e-5 if prec == "fp32" else 2 * tol)
+        assert rel_l2(to_np(p)[s], p_ref[s]) <= TOL[prec]
+    # radiated field of the MC solution (MC sources, w = |Gamma|/M)
+    src = nat.nat_mc_sources(smp, gg.total_area, p, torch.from_numpy(g_tri[:, tri]).cuda(), center=gg.center)
+    x = I.random_points_in_shell(300, 1.6, 3.0, seed=2) + np.asarray(geo["center"])
+    out = to_np(nat.nat_radiate_field(src, ks, torch.from_numpy(np.ascontiguousarray(x.T)).cuda(), prec=prec))
+    ref = radiate.radiate(radiate.mc_sources(y, n, geo["total_area"], p_ref, g_tri[:, tri]), ks, x)
+    for s in range(3):
+        assert rel_l2(out[s], ref[s]) <= TOL[prec]
+
+
+def test_degenerate_cases():
+    nat = _nat()
+    m = I.icosphere(2)
+    geo, mesh, gg = _case(m)
+    g = torch.from_numpy(np.full((1, m.n_tri), 2.0 + 1.0j)).cuda()
+    # M = 1: 1/2 p = -(eps/2) g  ->  p = -eps g  (reading R-sign)
+    smp, stri, p, info = nat.nat_mc_surface_pressure(mesh, gg, [1.0], g, 1, seed=4)
+    eps = math.sqrt(gg.total_area / math.pi)
+    assert abs(to_np(p)[0, 0] - (-eps * (2.0 + 1.0j))) < 1e-12
+    # g = 0 -> p = 0 after 0 iterations
+    _, _, p0, i0 = nat.nat_mc_surface_pressure(mesh, gg, [1.0, 3.0], torch.zeros(2, m.n_tri, dtype=torch.complex128,
+                                                                                 device="cuda"), 256, seed=4)
+    assert torch.count_nonzero(p0) == 0 and i0[0]["iters"] == 0
+    # coincident samples -> NAT_ERR_SINGULAR naming the pair
+    smp, stri = nat.nat_mc_sample(mesh, gg, 50, 1)
+    smp[:, 17] = smp[:, 4]
+    stri[17] = stri[4]
+    with pytest.raises(nat.NatError, match=r"coincident samples \(4, 17\)"):
+        nat.nat_mc_surface_pressure(mesh, gg, [1.0], g, 50, samples_in=smp, sample_tri_in=stri)
+
+
+def test_c3_launch_configuration():
+    """Config C3: bowl 49,664 tri, M = 4096 uniform samples, 32 modes k_m a = 0.5 +
+    7.5 m / 31, fp32, tol 1e-6: the GPU solution satisfies sampled rows of the oracle's
+    system (property that holds at any size) and samples are bitwise identical."""
+    nat = _nat()
+    m = I.bowl()
+    geo, mesh, gg = _case(m)
+    M = 4096
+    ks = I.c3_wavenumbers()
+    g_tri = I.neumann_harmonics(m, 32)
+    smp, stri, p, infos = nat.nat_mc_surface_pressure(mesh, gg, ks, torch.from_numpy(g_tri).cuda(), M,
+                                                      seed=I.SEED, stream_id=0)
+    assert all(i["converged"] == 1 for i in infos)
+    y, n, tri = mc.sample_uniform(m.v, m.t, geo, M, I.SEED, 0)
+    assert np.array_equal(to_np(stri), tri)
+    P = to_np(p)
+    eps, w = mc.default_eps(geo["total_area"], M), None
+    w = mc.weight(geo["total_area"], M, eps)
+    rows = np.random.default_rng(1).choice(M, 16, replace=False)
+    for s in (0, 13, 31):
+        k = ks[s]
+        g = g_tri[s][tri]
+        res, nb = [], []
+        for i in rows:
+            j = np.arange(M) != i
+            Ai = -w * kernel.green_dn_y(y[i], y[j], n[j], k)
+            bi = -w * np.sum(kernel.green(y[i], y[j], k) * g[j]) - 0.5 * eps * g[i]
+            res.append(0.5 * P[s, i] + Ai @ P[s, j] - bi)
+            nb.append(bi)
+        assert np.linalg.norm(res) / np.linalg.norm(nb) <= 1e-4
