@@ -157,7 +157,10 @@ nat_status nat_comm_destroy(nat_comm* comm);
 typedef struct {
   int iters, converged;
   double rel_residual; /* true residual from one extra matvec            */
-  double t_total_s, t_matvec_s, t_comm_s; /* host wall times of the phases (info only) */
+  double t_total_s;  /* host wall time of the call                                         */
+  double t_matvec_s; /* device time (CUDA events) of the operator applications: matvec and,
+                        on > 1 rank, the all-gather (bem_solve) / MC operator (mc)          */
+  double t_comm_s;   /* host-side time spent enqueueing the all-gathers (info only)        */
 } nat_solve_info;
 
 size_t nat_bem_solve_workspace(nat_prec prec, int64_t n, int64_t rows_local, int max_iter);
@@ -201,6 +204,10 @@ nat_status nat_mc_rhs(nat_prec prec, int64_t M, const double* samples, int n_sys
 nat_status nat_mc_apply(nat_prec prec, int64_t M, const double* samples, int n_sys, const double* k,
                         const void* p, double w, double eps, void* out, void* ws, size_t ws_bytes,
                         nat_stream_t stream); /* (async) */
+/* g_out[m][j] = g_tri[m][sample_tri[j]] (piecewise-constant Neumann data at the samples,
+ * P:164; c128 [n_sys][n_tri] -> c128 [n_sys][M]).  (async)                              */
+nat_status nat_mc_gather_neumann(int n_sys, int64_t M, int64_t n_tri, const void* g_tri,
+                                 const int32_t* sample_tri, void* g_out, nat_stream_t stream);
 nat_status nat_mc_check_coincident(int64_t M, const double* samples, int64_t* pair /* [host] 2 */,
                                    void* ws, size_t ws_bytes, nat_stream_t stream); /* (sync) */
 

@@ -172,8 +172,19 @@ nat_status gmres_batched(int nsys, int64_t n, int64_t ldv, const double2* b, dou
   const size_t vstride = (size_t)nsys * ldv;
   const unsigned gx = (unsigned)((n + kT - 1) / kT);
   const uint64_t all = nsys == 64 ? ~0ull : ((1ull << nsys) - 1);
-  double t_op = 0;
-  auto clk = [] { return std::chrono::steady_clock::now(); };
+  double t_op = 0;  // device time of the operator (CUDA events), if requested
+  struct Events {
+    cudaEvent_t e[2] = {nullptr, nullptr};
+    ~Events() {
+      for (auto x : e)
+        if (x) cudaEventDestroy(x);
+    }
+  } evs;
+  cudaEvent_t* ev = evs.e;
+  if (t_op_s) {
+    NAT_CUDA_TRY(cudaEventCreate(&ev[0]));
+    NAT_CUDA_TRY(cudaEventCreate(&ev[1]));
+  }
   res.assign(nsys, KrylovResult{0, 1, 0.0});
   std::vector<SysState> st(nsys);
   std::vector<double2> hbuf((size_t)nsys * mp2);
@@ -205,13 +216,10 @@ nat_status gmres_batched(int nsys, int64_t n, int64_t ldv, const double2* b, dou
 
   for (int j = 0; j < m && active; ++j) {
     double2* Vj = ws.V + (size_t)j * vstride;
-    auto t0 = clk();
+    if (t_op_s) NAT_CUDA_TRY(cudaEventRecord(ev[0], s));
     nat_status stt = op(Vj, ws.w, active, s);
     if (stt != NAT_OK) return stt;
-    if (t_op_s) {
-      NAT_CUDA_TRY(cudaStreamSynchronize(s));
-      t_op += std::chrono::duration<double>(clk() - t0).count();
-    }
+    if (t_op_s) NAT_CUDA_TRY(cudaEventRecord(ev[1], s));
     for (int pass = 0; pass < 2; ++pass) {  // CGS2
       dots_kernel<<<dim3(nchunk, j + 1, nsys), kT, 0, s>>>(ws.V, vstride, ldv, ws.w, n, j + 1, nchunk, mp1,
                                                           active, ws.part);
@@ -226,6 +234,11 @@ nat_status gmres_batched(int nsys, int64_t n, int64_t ldv, const double2* b, dou
     NAT_CUDA_TRY(cudaMemcpy2DAsync(hbuf.data(), sizeof(double2) * mp2, ws.h, sizeof(double2) * mp2,
                                    sizeof(double2) * (j + 2), nsys, cudaMemcpyDeviceToHost, s));
     NAT_CUDA_TRY(cudaStreamSynchronize(s));
+    if (t_op_s) {
+      float ms = 0.f;
+      NAT_CUDA_TRY(cudaEventElapsedTime(&ms, ev[0], ev[1]));
+      t_op += 1e-3 * ms;
+    }
     for (int q = 0; q < nsys; ++q) {
       if (!((active >> q) & 1ull)) continue;
       SysState& S = st[q];

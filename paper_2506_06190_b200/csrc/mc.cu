@@ -412,6 +412,21 @@ extern "C" nat_status nat_mc_check_coincident(int64_t M, const double* samples, 
   return nat::fail(NAT_ERR_SINGULAR, "coincident samples (%lld, %lld)", (long long)pair[0], (long long)pair[1]);
 }
 
+extern "C" nat_status nat_mc_gather_neumann(int n_sys, int64_t M, int64_t n_tri, const void* g_tri,
+                                            const int32_t* sample_tri, void* g_out, nat_stream_t stream) {
+  NAT_REQUIRE(n_sys >= 1 && M >= 1 && n_tri >= 1, "need n_sys, M, n_tri >= 1");
+  NAT_REQUIRE_DEV(g_tri);
+  NAT_REQUIRE_DEV(sample_tri);
+  NAT_REQUIRE_DEV(g_out);
+  for (int s0 = 0; s0 < n_sys; s0 += 65535) {
+    const int nb = (n_sys - s0) < 65535 ? (n_sys - s0) : 65535;
+    gather_g_kernel<<<dim3((unsigned)((M + 255) / 256), nb), 256, 0, (cudaStream_t)stream>>>(
+        nb, M, n_tri, (const double2*)g_tri + (size_t)s0 * n_tri, sample_tri, (double2*)g_out + (size_t)s0 * M);
+  }
+  NAT_LAUNCH_CHECK();
+  return NAT_OK;
+}
+
 extern "C" size_t nat_mc_op_workspace(nat_prec prec, int64_t M, int n_sys) {
   nat::Carver c(nullptr);
   carve_near(c, nullptr, M);

@@ -95,6 +95,7 @@ _SIGS = {
     "nat_mc_apply": (C.c_int, [C.c_int, _I64, _P, C.c_int, C.POINTER(_D), _P, _D, _D, _P, _P, _SZ,
                                _P]),
     "nat_mc_check_coincident": (C.c_int, [_I64, _P, C.POINTER(_I64), _P, _SZ, _P]),
+    "nat_mc_gather_neumann": (C.c_int, [C.c_int, _I64, _I64, _P, _P, _P, _P]),
     "nat_mc_workspace": (_SZ, [C.c_int, _I64, C.c_int, C.c_int]),
     "nat_mc_surface_pressure": (C.c_int, [C.POINTER(_Mesh), C.POINTER(_Geom), C.c_int,
                                           C.POINTER(_D), _P, C.POINTER(_McOpts), C.c_int, _D,
@@ -437,6 +438,15 @@ def nat_mc_check_coincident(samples: torch.Tensor):
     ws = _ws(256, samples.device)
     _check(lib().nat_mc_check_coincident(M, _ptr(samples), pair, _ptr(ws), ws.numel(), _stream()))
     return None
+
+
+def nat_mc_gather_neumann(g_tri: torch.Tensor, sample_tri: torch.Tensor, out=None):
+    g_tri = torch.atleast_2d(g_tri).to(torch.complex128).contiguous()
+    n_sys, n_tri = g_tri.shape
+    M = sample_tri.numel()
+    out = torch.empty(n_sys, M, dtype=torch.complex128, device=g_tri.device) if out is None else out
+    _check(lib().nat_mc_gather_neumann(n_sys, M, n_tri, _ptr(g_tri), _ptr(sample_tri), _ptr(out), _stream()))
+    return out
 
 
 def mc_weights(total_area: float, M: int, eps: float = 0.0):
