@@ -103,16 +103,14 @@ class ClockSampler:
         while not self._stop.is_set():
             try:
                 mhz = self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM)
-                util = self.nv.nvmlDeviceGetUtilizationRates(self.h).gpu
                 r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                if util > 0:
-                    self.samples.append(mhz)
-                    for bit, name in self.REASONS.items():
-                        if r & bit and name != "gpu_idle":
-                            self.reasons.add(name)
-            except Exception:
-                pass
-            time.sleep(0.05)
+                self.samples.append(mhz)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception as ex:
+                self.err = str(ex)
+            time.sleep(0.02)
 
     def __enter__(self):
         if self.ok:
@@ -159,8 +157,10 @@ class Step:
         self.solve_ws = nat._ws(nat.lib().nat_bem_solve_workspace(nat.NAT_FP32, self.n, rows, 200), dev)
         self.S_bem = 3 * self.n
         self.n_lis = self.l1 - self.l0
-        self.rad_plan_bem = nat.RadiatePlan(self.S_bem, 1, self.n_lis, "fp32", dev)
+        self.rad_plan_bem = nat.RadiatePlan(self.S_bem, len(KAS), self.n_lis, "fp32", dev)
         self.out_bem = torch.empty(len(KAS), self.n_lis, dtype=torch.complex128, device=dev)
+        self.x_bem = torch.empty(len(KAS), self.n, dtype=torch.complex128, device=dev)
+        self.g3 = self.g.expand(len(KAS), -1).contiguous()
         if self.mc_idx:
             self.mc_plan = nat.McPlan(M_MC, len(self.mc_idx), "fp32", 200, dev)
             self.rad_plan_mc = nat.RadiatePlan(M_MC, len(self.mc_idx), self.n_lis, "fp32", dev)
@@ -183,6 +183,7 @@ class Step:
             mesh.vxyz.copy_(hv, non_blocking=True)
             mesh.tri.copy_(ht, non_blocking=True)
             g.copy_(hg, non_blocking=True)
+            self.g3.copy_(g.expand(len(KAS), -1))
             if self.g_mc is not None:
                 self.g_mc.copy_(g.expand(len(self.mc_idx), -1))
         self._ev("geom0")
@@ -202,13 +203,9 @@ class Step:
             self._ev("asm0")
             A, b = nat.nat_bem_assemble(mesh, geo, near, ka, g, prec="fp32", A=self.A, lda=self.lda)  # a4+a5
             self._ev("asm1")
-            x, info = nat.nat_bem_solve(A, b[0], self.n, self.r0, self.comm, tol=1e-6, max_iter=200,
-                                        ws=self.solve_ws)                                          # a6+a7
+            _, info = nat.nat_bem_solve(A, b[0], self.n, self.r0, self.comm, tol=1e-6, max_iter=200,
+                                        ws=self.solve_ws, out=self.x_bem[q])                       # a6+a7
             self._ev("solve1")
-            src = nat.nat_bem_sources(mesh, geo, x[None], g)
-            self._ev("rad0")
-            nat.nat_radiate_field(src, [ka], lis, "fp32", out=self.out_bem[q:q + 1], plan=self.rad_plan_bem)  # a11
-            self._ev("rad1")
             counts["far"] += rows * self.n * 3
             counts["near"] += nS * 448 + nN * 28
             counts["self"] += rows * 48
@@ -216,6 +213,11 @@ class Step:
             counts["gemv_bytes"] += info["iters"] * rows * self.lda * 8
             counts["gemv_s"] += info["t_matvec_s"]
             counts["iters"].append(info["iters"])
+        # a11: the three solutions radiate in one launch (shared r, 1/r, d.n per pair)
+        src = nat.nat_bem_sources(mesh, geo, self.x_bem, self.g3)
+        self._ev("rad0")
+        nat.nat_radiate_field(src, list(KAS), lis, "fp32", out=self.out_bem, plan=self.rad_plan_bem)
+        self._ev("rad1")
         if self.mc_idx:
             ks = [KAS[i] for i in self.mc_idx]
             self._ev("mc0")

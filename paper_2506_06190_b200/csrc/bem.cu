@@ -496,45 +496,103 @@ __global__ void rhs_final_kernel(int64_t rows, int n_rhs, int n_colblk, const do
 // ------------------------------------------------------------------------------------
 // a6: y = A x, fp64 accumulation; CTA = 8 rows x 256 threads, x reused across rows.
 // ------------------------------------------------------------------------------------
-constexpr int kGemvRows = 8;
+constexpr int kGemvRows = 8;   // c128 kernel
+constexpr int kGemvRows32 = 4; // c64 kernel
 
-__global__ void __launch_bounds__(kThreads) gemv_c64_kernel(int64_t rows, int64_t n, const float2* __restrict__ A,
-                                                           int64_t lda, const double2* __restrict__ x,
-                                                           double2* __restrict__ y) {
-  __shared__ double2 red[kThreads / 32][kGemvRows];
+// c64 (NAT_FP32) matvec, HBM-bound: CTA = 4 rows x 256 threads, each thread streams two
+// float4 (= 4 complex) per row per iteration with streaming loads (8 LDG.128 in flight),
+// x (c128) is converted to fp32 once per column pair and reused by the 4 rows; products
+// are accumulated in fp32 over 8 columns and flushed into fp64 accumulators (the matrix
+// itself carries fp32 rounding, so this keeps the matvec error at the c64 level while the
+// register budget allows 4 CTAs/SM); fixed-order reduction -> deterministic.
+__global__ void __launch_bounds__(kThreads, 3) gemv_c64_kernel(int64_t rows, int64_t n, const float2* __restrict__ A,
+                                                              int64_t lda, const double2* __restrict__ x,
+                                                              double2* __restrict__ y) {
+  constexpr int RB = kGemvRows32;
+  __shared__ double2 red[kThreads / 32][RB];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t r0 = (int64_t)blockIdx.x * kGemvRows;
-  const int nr = (int)nat::min64(kGemvRows, rows - r0);
-  double ar[kGemvRows], ai[kGemvRows];
+  const int64_t r0 = (int64_t)blockIdx.x * RB;
+  const int nr = (int)nat::min64(RB, rows - r0);
+  double ar[RB], ai[RB];
 #pragma unroll
-  for (int r = 0; r < kGemvRows; ++r) ar[r] = ai[r] = 0.0;
+  for (int r = 0; r < RB; ++r) ar[r] = ai[r] = 0.0;
   const int64_t n2 = n / 2;
   const float4* A4 = reinterpret_cast<const float4*>(A);
   const int64_t lda2 = lda / 2;
-#pragma unroll 2
-  for (int64_t c = tid; c < n2; c += kThreads) {
+  // rows past the end re-read the last valid row (results discarded)
+  const float4* const A0 = A4 + (r0 + 0) * lda2;
+  const float4* const A1 = A4 + (r0 + (1 < nr ? 1 : 0)) * lda2;
+  const float4* const A2 = A4 + (r0 + (2 < nr ? 2 : 0)) * lda2;
+  const float4* const A3 = A4 + (r0 + (3 < nr ? 3 : 0)) * lda2;
+  static_assert(RB == 4, "row pointers below assume 4 rows");
+#define NAT_AROW(r) ((r) == 0 ? A0 : (r) == 1 ? A1 : (r) == 2 ? A2 : A3)
+  int64_t c = tid;
+  float sr[RB], si[RB];
+#pragma unroll
+  for (int r = 0; r < RB; ++r) sr[r] = si[r] = 0.f;
+  int nacc = 0;
+  for (; c + kThreads < n2; c += 2 * kThreads) {
+    float4 av[2][RB];
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+      for (int r = 0; r < RB; ++r) av[u][r] = __ldcs(&NAT_AROW(r)[c + u * kThreads]);
+    float xr[2][4];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const double2 x0 = __ldg(&x[2 * (c + u * kThreads)]), x1 = __ldg(&x[2 * (c + u * kThreads) + 1]);
+      xr[u][0] = (float)x0.x;
+      xr[u][1] = (float)x0.y;
+      xr[u][2] = (float)x1.x;
+      xr[u][3] = (float)x1.y;
+    }
+#pragma unroll
+    for (int r = 0; r < RB; ++r) {
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const float4 a = av[u][r];
+        sr[r] = fmaf(a.x, xr[u][0], fmaf(-a.y, xr[u][1], fmaf(a.z, xr[u][2], fmaf(-a.w, xr[u][3], sr[r]))));
+        si[r] = fmaf(a.x, xr[u][1], fmaf(a.y, xr[u][0], fmaf(a.z, xr[u][3], fmaf(a.w, xr[u][2], si[r]))));
+      }
+    }
+    if (++nacc == 4) {  // flush 16 complex products per row into fp64
+#pragma unroll
+      for (int r = 0; r < RB; ++r) {
+        ar[r] += (double)sr[r];
+        ai[r] += (double)si[r];
+        sr[r] = si[r] = 0.f;
+      }
+      nacc = 0;
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < RB; ++r) {
+    ar[r] += (double)sr[r];
+    ai[r] += (double)si[r];
+  }
+  for (; c < n2; c += kThreads) {
     const double2 x0 = __ldg(&x[2 * c]), x1 = __ldg(&x[2 * c + 1]);
-    float4 av[kGemvRows];
 #pragma unroll
-    for (int r = 0; r < kGemvRows; ++r)
-      av[r] = r < nr ? __ldcs(&A4[(r0 + r) * lda2 + c]) : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-    for (int r = 0; r < kGemvRows; ++r) {
-      const double a0r = av[r].x, a0i = av[r].y, a1r = av[r].z, a1i = av[r].w;
-      ar[r] = fma(a0r, x0.x, fma(-a0i, x0.y, fma(a1r, x1.x, fma(-a1i, x1.y, ar[r]))));
-      ai[r] = fma(a0r, x0.y, fma(a0i, x0.x, fma(a1r, x1.y, fma(a1i, x1.x, ai[r]))));
+    for (int r = 0; r < RB; ++r) {
+      const float4 a = __ldcs(&NAT_AROW(r)[c]);
+      ar[r] += (double)a.x * x0.x - (double)a.y * x0.y + (double)a.z * x1.x - (double)a.w * x1.y;
+      ai[r] += (double)a.x * x0.y + (double)a.y * x0.x + (double)a.z * x1.y + (double)a.w * x1.x;
     }
   }
   if ((n & 1) && tid == 0) {
     const double2 xl = x[n - 1];
-    for (int r = 0; r < nr; ++r) {
-      float2 a = A[(r0 + r) * lda + n - 1];
-      ar[r] += (double)a.x * xl.x - (double)a.y * xl.y;
-      ai[r] += (double)a.x * xl.y + (double)a.y * xl.x;
+#pragma unroll
+    for (int r = 0; r < RB; ++r) {
+      if (r < nr) {
+        float2 a = A[(r0 + r) * lda + n - 1];
+        ar[r] += (double)a.x * xl.x - (double)a.y * xl.y;
+        ai[r] += (double)a.x * xl.y + (double)a.y * xl.x;
+      }
     }
   }
+#undef NAT_AROW
 #pragma unroll
-  for (int r = 0; r < kGemvRows; ++r) {
+  for (int r = 0; r < RB; ++r) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       ar[r] += __shfl_xor_sync(0xffffffffu, ar[r], o);
@@ -830,7 +888,8 @@ extern "C" nat_status nat_bem_matvec(nat_prec prec, int64_t rows, int64_t n, con
   NAT_REQUIRE_DEV(A);
   NAT_REQUIRE_DEV(x);
   NAT_REQUIRE_DEV(y);
-  unsigned grid = (unsigned)((rows + kGemvRows - 1) / kGemvRows);
+  const int rb = prec == NAT_FP32 ? kGemvRows32 : kGemvRows;
+  unsigned grid = (unsigned)((rows + rb - 1) / rb);
   if (prec == NAT_FP32)
     gemv_c64_kernel<<<grid, kThreads, 0, (cudaStream_t)stream>>>(rows, n, (const float2*)A, lda,
                                                                  (const double2*)x, (double2*)y);
@@ -845,7 +904,8 @@ namespace nat {
 // Used by the GMRES driver (gmres.cu).
 nat_status matvec_internal(nat_prec prec, int64_t rows, int64_t n, const void* A, int64_t lda,
                            const void* x, void* y, cudaStream_t s) {
-  unsigned grid = (unsigned)((rows + kGemvRows - 1) / kGemvRows);
+  const int rb = prec == NAT_FP32 ? kGemvRows32 : kGemvRows;
+  unsigned grid = (unsigned)((rows + rb - 1) / rb);
   if (prec == NAT_FP32)
     gemv_c64_kernel<<<grid, kThreads, 0, s>>>(rows, n, (const float2*)A, lda, (const double2*)x, (double2*)y);
   else

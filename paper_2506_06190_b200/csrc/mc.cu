@@ -497,7 +497,40 @@ struct McWs {
   void* rad;
   size_t rad_bytes;
   NearPairs np;
+  double2* tin;   // compacted operator input / output of the systems still iterating
+  double2* tout;
 };
+
+struct RowIdx {
+  int idx[64];
+};
+
+// gather (dst[q] = src[idx[q]]) or scatter (dst[idx[q]] = src[q]) of [M]-rows
+__global__ void copy_rows_kernel(RowIdx ix, int64_t M, const double2* __restrict__ src, double2* __restrict__ dst,
+                                 bool gather) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int q = blockIdx.y;
+  if (j >= M) return;
+  if (gather)
+    dst[(size_t)q * M + j] = src[(size_t)ix.idx[q] * M + j];
+  else
+    dst[(size_t)ix.idx[q] * M + j] = src[(size_t)q * M + j];
+}
+
+// smallest (i, j) with fp64 |y_i - y_j| < 1e-12 among the close pairs.
+__global__ void coincident_near_kernel(int64_t M, const double* __restrict__ smp, const int32_t* __restrict__ rp,
+                                       const int32_t* __restrict__ col, unsigned long long* best) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= M) return;
+  for (int e = rp[i]; e < rp[i + 1]; ++e) {
+    const int64_t j = col[e];
+    const double dx = smp[j] - smp[i], dy = smp[M + j] - smp[M + i], dz = smp[2 * M + j] - smp[2 * M + i];
+    if (sqrt(dx * dx + dy * dy + dz * dz) < 1e-12) {
+      atomicMin(best, ((unsigned long long)i << 32) | (unsigned long long)j);
+      return;
+    }
+  }
+}
 
 size_t mc_carve(nat::Carver& c, McWs* w, nat_prec prec, int64_t M, int n_sys, int max_iter) {
   const int nb = n_sys < 64 ? n_sys : 64;
@@ -509,6 +542,8 @@ size_t mc_carve(nat::Carver& c, McWs* w, nat_prec prec, int64_t M, int n_sys, in
   t.rad_bytes = nat::radiate_ws_bytes(prec, M, nb, M);
   t.rad = c.take<char>(t.rad_bytes);
   carve_near(c, &t.np, M);
+  t.tin = c.take<double2>((size_t)nb * M);
+  t.tout = c.take<double2>((size_t)nb * M);
   if (w) *w = t;
   return c.bytes();
 }
@@ -556,17 +591,25 @@ extern "C" nat_status nat_mc_surface_pressure(const nat_mesh* mesh, const nat_ge
     st = nat_mc_sample(mesh, geom, M, opts->seed, opts->stream_id, samples_out, sample_tri_out, stream);
     if (st != NAT_OK) return st;
   }
-  int64_t pair[2];
-  st = nat_mc_check_coincident(M, samples_out, pair, w.best, 8, stream);
-  if (st != NAT_OK) return st;
   // disk radius and off-disk weight (readings R-eps, R-weight)
   const double area = geom->total_area;
   const double eps = opts->eps > 0 ? opts->eps : std::sqrt(area / (nat::kPi * (double)M));
   const double wgt = M > 1 ? (area - nat::kPi * eps * eps) / (double)(M - 1) : 0.0;
   const double* cen = geom->center;
-  if (prec == NAT_FP32 && M > 1) {
+  if (M > 1) {
+    // close pairs (fp32 r <= 2 eps); every coincident pair (fp64 r < 1e-12) is among them,
+    // so the singularity check only scans this list
     st = build_near(w.np, M, samples_out, cen, eps, s);
     if (st != NAT_OK) return st;
+    init_best_kernel<<<1, 1, 0, s>>>(w.best);
+    coincident_near_kernel<<<(unsigned)((M + 255) / 256), 256, 0, s>>>(M, samples_out, w.np.rp, w.np.col, w.best);
+    NAT_LAUNCH_CHECK();
+    unsigned long long hb = 0;
+    NAT_CUDA_TRY(cudaMemcpyAsync(&hb, w.best, 8, cudaMemcpyDeviceToHost, s));
+    NAT_CUDA_TRY(cudaStreamSynchronize(s));
+    if (hb != ~0ull)
+      return nat::fail(NAT_ERR_SINGULAR, "coincident samples (%llu, %llu)", hb >> 32, hb & 0xffffffffull);
+    w.np.on = (prec == NAT_FP32);  // the fp64 kernel resolves close pairs itself
   }
   bool all_conv = true;
   for (int s0 = 0; s0 < n_sys; s0 += 64) {
@@ -576,8 +619,28 @@ extern "C" nat_status nat_mc_surface_pressure(const nat_mesh* mesh, const nat_ge
     NAT_LAUNCH_CHECK();
     st = mc_rhs_impl(prec, M, samples_out, nb, k + s0, w.gs, wgt, eps, w.b, w.rad, w.rad_bytes, cen, w.np, s);
     if (st != NAT_OK) return st;
-    auto op = [&](const double2* in, double2* out, uint64_t, cudaStream_t ss) -> nat_status {
-      return mc_apply_impl(prec, M, samples_out, nb, k + s0, in, wgt, out, w.rad, w.rad_bytes, cen, w.np, ss);
+    const uint64_t all = nb == 64 ? ~0ull : ((1ull << nb) - 1);
+    auto op = [&](const double2* in, double2* out, uint64_t active, cudaStream_t ss) -> nat_status {
+      if ((active & all) == all)
+        return mc_apply_impl(prec, M, samples_out, nb, k + s0, in, wgt, out, w.rad, w.rad_bytes, cen, w.np, ss);
+      // only the systems still iterating: gather them, apply, scatter back
+      RowIdx ix{};
+      double kc[64];
+      int na = 0;
+      for (int q = 0; q < nb; ++q)
+        if ((active >> q) & 1ull) {
+          ix.idx[na] = q;
+          kc[na++] = k[s0 + q];
+        }
+      if (na == 0) return NAT_OK;
+      const dim3 g2((unsigned)((M + 255) / 256), na);
+      copy_rows_kernel<<<g2, 256, 0, ss>>>(ix, M, in, w.tin, true);
+      nat_status r = mc_apply_impl(prec, M, samples_out, na, kc, w.tin, wgt, w.tout, w.rad, w.rad_bytes, cen,
+                                   w.np, ss);
+      if (r != NAT_OK) return r;
+      copy_rows_kernel<<<g2, 256, 0, ss>>>(ix, M, w.tout, out, false);
+      NAT_LAUNCH_CHECK();
+      return NAT_OK;
     };
     std::vector<nat::KrylovResult> res;
     double t_op = 0;

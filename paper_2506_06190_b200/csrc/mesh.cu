@@ -55,23 +55,27 @@ __global__ void tri_geom_kernel(int64_t nv, int64_t nt, const double* __restrict
 }
 
 // Sequential prefix sum, exactly the left-to-right order of the definition.
-__global__ void cdf_kernel(int64_t nt, const double* __restrict__ area, double* __restrict__ cdf) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+// The block stages chunks of the areas in shared memory (coalesced), thread 0 runs the
+// dependent fp64 chain out of shared memory, the block writes the chunk back.
+constexpr int kCdfChunk = 4096;
+__global__ void __launch_bounds__(1024) cdf_kernel(int64_t nt, const double* __restrict__ area,
+                                                   double* __restrict__ cdf) {
+  __shared__ double buf[kCdfChunk];
   double s = 0.0;
-  int64_t t = 0;
-  for (; t + 8 <= nt; t += 8) {
-    double a[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) a[q] = area[t + q];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      s = __dadd_rn(s, a[q]);
-      cdf[t + q] = s;
+  for (int64_t c0 = 0; c0 < nt; c0 += kCdfChunk) {
+    const int len = (int)nat::min64(kCdfChunk, nt - c0);
+    for (int t = threadIdx.x; t < len; t += blockDim.x) buf[t] = area[c0 + t];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+#pragma unroll 8
+      for (int t = 0; t < len; ++t) {
+        s = __dadd_rn(s, buf[t]);
+        buf[t] = s;
+      }
     }
-  }
-  for (; t < nt; ++t) {
-    s = __dadd_rn(s, area[t]);
-    cdf[t] = s;
+    __syncthreads();
+    for (int t = threadIdx.x; t < len; t += blockDim.x) cdf[c0 + t] = buf[t];
+    __syncthreads();
   }
 }
 
@@ -185,7 +189,7 @@ extern "C" nat_status nat_mesh_prepare(const nat_mesh* mesh, nat_geom* geom, voi
   tri_geom_kernel<<<(unsigned)((nt + 255) / 256), 256, 0, s>>>(
       mesh->n_vert, nt, mesh->vxyz, mesh->tri, geom->centroid, geom->normal, geom->area, geom->diam,
       vol, sc);
-  cdf_kernel<<<1, 32, 0, s>>>(nt, geom->area, geom->area_cdf);
+  cdf_kernel<<<1, 1024, 0, s>>>(nt, geom->area, geom->area_cdf);
   centre_kernel<<<1, RB, 0, s>>>(nt, geom->area, geom->centroid, vol, geom->area_cdf, sc);
   radius_kernel<<<1, RB, 0, s>>>(mesh->n_vert, mesh->vxyz, sc);
   NAT_LAUNCH_CHECK();

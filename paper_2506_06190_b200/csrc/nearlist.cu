@@ -34,6 +34,7 @@ struct NearArgs {
 template <bool kBuild>
 __global__ void __launch_bounds__(kWarps * 32) near_kernel(NearArgs a) {
   __shared__ double s_cx[kJTile], s_cy[kJTile], s_cz[kJTile], s_thr[kJTile];
+  __shared__ float s_f[5][kJTile];  // fp32 centroid, eta*diam, diam: conservative prefilter
   __shared__ int32_t s_v[3][kJTile];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t r0 = (int64_t)blockIdx.x * kRowsPerCta + warp * kRowsPerWarp;
@@ -41,6 +42,7 @@ __global__ void __launch_bounds__(kWarps * 32) near_kernel(NearArgs a) {
 
   int64_t gi[kRowsPerWarp];
   double cx[kRowsPerWarp], cy[kRowsPerWarp], cz[kRowsPerWarp];
+  float fx[kRowsPerWarp], fy[kRowsPerWarp], fz[kRowsPerWarp], fd[kRowsPerWarp];
   int32_t va[kRowsPerWarp], vb[kRowsPerWarp], vc[kRowsPerWarp];
   int64_t pos[kRowsPerWarp];
   bool live[kRowsPerWarp];
@@ -53,6 +55,10 @@ __global__ void __launch_bounds__(kWarps * 32) near_kernel(NearArgs a) {
     cx[q] = a.cen[i];
     cy[q] = a.cen[nt + i];
     cz[q] = a.cen[2 * nt + i];
+    fx[q] = (float)cx[q];
+    fy[q] = (float)cy[q];
+    fz[q] = (float)cz[q];
+    fd[q] = (float)a.diam[i];
     va[q] = a.tri[i];
     vb[q] = a.tri[nt + i];
     vc[q] = a.tri[2 * nt + i];
@@ -68,6 +74,11 @@ __global__ void __launch_bounds__(kWarps * 32) near_kernel(NearArgs a) {
         s_cy[t] = a.cen[nt + j];
         s_cz[t] = a.cen[2 * nt + j];
         s_thr[t] = __dmul_rn(a.eta, a.diam[j]);
+        s_f[0][t] = (float)s_cx[t];
+        s_f[1][t] = (float)s_cy[t];
+        s_f[2][t] = (float)s_cz[t];
+        s_f[3][t] = (float)s_thr[t];
+        s_f[4][t] = (float)a.diam[j];
         s_v[0][t] = a.tri[j];
         s_v[1][t] = a.tri[nt + j];
         s_v[2][t] = a.tri[2 * nt + j];
@@ -79,26 +90,33 @@ __global__ void __launch_bounds__(kWarps * 32) near_kernel(NearArgs a) {
       const int t = jj + lane;
       const bool in = t < jn;
       const int64_t j = j0 + t;
-      double ox = 0, oy = 0, oz = 0, thr = 0;
-      int32_t u0 = -1, u1 = -1, u2 = -1;
+      float ofx = 3e30f, ofy = 3e30f, ofz = 3e30f, ofth = 0.f, ofd = 0.f;
       if (in) {
-        ox = s_cx[t];
-        oy = s_cy[t];
-        oz = s_cz[t];
-        thr = s_thr[t];
-        u0 = s_v[0][t];
-        u1 = s_v[1][t];
-        u2 = s_v[2][t];
+        ofx = s_f[0][t];
+        ofy = s_f[1][t];
+        ofz = s_f[2][t];
+        ofth = s_f[3][t];
+        ofd = s_f[4][t];
       }
 #pragma unroll
       for (int q = 0; q < kRowsPerWarp; ++q) {
         if (!live[q]) continue;  // warp-uniform
-        bool shares = (u0 == va[q] || u0 == vb[q] || u0 == vc[q] || u1 == va[q] || u1 == vb[q] ||
-                       u1 == vc[q] || u2 == va[q] || u2 == vb[q] || u2 == vc[q]);
-        double dx = __dsub_rn(cx[q], ox), dy = __dsub_rn(cy[q], oy), dz = __dsub_rn(cz[q], oz);
-        double dist = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)),
-                                           __dmul_rn(dz, dz)));
-        bool hit = in && j != gi[q] && (shares || dist < thr);
+        // Conservative fp32 reject: a listed pair has |c_i - c_j| < eta diam_j (class N) or
+        // shares a vertex, which implies |c_i - c_j| <= 2/3 (diam_i + diam_j) (class S).
+        const float ex = fx[q] - ofx, ey = fy[q] - ofy, ez = fz[q] - ofz;
+        const float d2 = ex * ex + ey * ey + ez * ez;
+        const float reach = fmaxf(ofth, fd[q] + ofd) * 1.001f + 1e-30f;
+        bool hit = false, shares = false;
+        if (in && d2 <= reach * reach && j != gi[q]) {
+          const int32_t u0 = s_v[0][t], u1 = s_v[1][t], u2 = s_v[2][t];
+          shares = (u0 == va[q] || u0 == vb[q] || u0 == vc[q] || u1 == va[q] || u1 == vb[q] ||
+                    u1 == vc[q] || u2 == va[q] || u2 == vb[q] || u2 == vc[q]);
+          // the exact predicate (reading R-near): fp64, round-to-nearest, no contraction
+          double dx = __dsub_rn(cx[q], s_cx[t]), dy = __dsub_rn(cy[q], s_cy[t]), dz = __dsub_rn(cz[q], s_cz[t]);
+          double dist = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)),
+                                             __dmul_rn(dz, dz)));
+          hit = shares || dist < s_thr[t];
+        }
         unsigned m = __ballot_sync(0xffffffffu, hit);
         if (kBuild) {
           if (hit) {

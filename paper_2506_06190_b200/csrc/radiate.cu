@@ -52,7 +52,21 @@ struct RadParams {
 // ------------------------------------------------------------------------------------
 // staging
 // ------------------------------------------------------------------------------------
-template <typename T>
+// DUP: every value is written twice (x x y y ...), the layout of the FP32x2 kernel.
+template <typename T, bool DUP>
+struct RecWriter {
+  T* r;
+  __device__ __forceinline__ void put(int f, double v) const {
+    if (DUP) {
+      r[2 * f] = (T)v;
+      r[2 * f + 1] = (T)v;
+    } else {
+      r[f] = (T)v;
+    }
+  }
+};
+
+template <typename T, bool DUP = false>
 __global__ void stage_kernel(int64_t n_src, int64_t n_src_pad, int NF, int MB, int n_mchunk,
                              const double* __restrict__ xyz, const double* __restrict__ nrm,
                              const double* __restrict__ w, double w_const,
@@ -78,12 +92,13 @@ __global__ void stage_kernel(int64_t n_src, int64_t n_src_pad, int NF, int MB, i
   }
   for (int c = 0; c < n_mchunk; ++c) {
     T* r = rec + ((size_t)c * n_src_pad + s) * NF;
-    r[0] = (T)x;
-    r[1] = (T)y;
-    r[2] = (T)z;
-    r[3] = (T)nx;
-    r[4] = (T)ny;
-    r[5] = (T)nz;
+    const RecWriter<T, DUP> wr{r};
+    wr.put(0, x);
+    wr.put(1, y);
+    wr.put(2, z);
+    wr.put(3, nx);
+    wr.put(4, ny);
+    wr.put(5, nz);
     for (int m = 0; m < MB; ++m) {
       int mode = c * MB + m;
       double ar = 0, ai = 0, br = 0, bi = 0, k = 0;
@@ -96,15 +111,15 @@ __global__ void stage_kernel(int64_t n_src, int64_t n_src_pad, int NF, int MB, i
         bi = ws * gv.y;
         k = kv.d[mode];
       }
-      T* q = r + 6 + 6 * m;
-      q[0] = (T)(-ar);
-      q[1] = (T)(-k * ai);
-      q[2] = (T)(k * ar);
-      q[3] = (T)(-ai);
-      q[4] = (T)(-br);
-      q[5] = (T)(-bi);
+      const int q = 6 + 6 * m;
+      wr.put(q + 0, -ar);
+      wr.put(q + 1, -k * ai);
+      wr.put(q + 2, k * ar);
+      wr.put(q + 3, -ai);
+      wr.put(q + 4, -br);
+      wr.put(q + 5, -bi);
     }
-    for (int f = 6 + 6 * MB; f < NF; ++f) r[f] = (T)0;
+    for (int f = (DUP ? 2 : 1) * (6 + 6 * MB); f < NF; ++f) r[f] = (T)0;
   }
 }
 
@@ -115,6 +130,196 @@ __device__ __forceinline__ float rsqrt_approx(float x) {
   float y;
   asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
+}
+
+// ------------------------------------------------------------------------------------
+// fp32 main kernel on the packed FP32x2 pipe (FADD2 / FMUL2 / FFMA2, sm_100a).
+// Two targets share every instruction; each source record is stored duplicated
+// (x x y y z z nx nx ...) so a packed operand is one half of an LDS.128 broadcast.
+// Per pair: 12.5 FP32-pipe instructions + 3 MUFU (rsqrt, sin, cos) instead of 24 + 3.
+// ------------------------------------------------------------------------------------
+typedef unsigned long long f2r;  // a float2 in a 64-bit register pair
+__device__ __forceinline__ f2r f2pack(float lo, float hi) {
+  f2r r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ float f2lo(f2r a) {
+  float lo, hi;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(a));
+  return lo;
+}
+__device__ __forceinline__ float f2hi(f2r a) {
+  float lo, hi;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(a));
+  return hi;
+}
+__device__ __forceinline__ f2r f2add(f2r a, f2r b) {
+  f2r r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f2r f2sub(f2r a, f2r b) {
+  f2r r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f2r f2mul(f2r a, f2r b) {
+  f2r r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f2r f2fma(f2r a, f2r b, f2r c) {
+  f2r r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+
+template <int MB>
+struct Rec2 {
+  static constexpr int NF = 12 + 12 * MB;  // duplicated floats per source record
+};
+
+template <int R, int MB, int SELF>
+__global__ void __launch_bounds__(kThreads) radiate_f32x2_kernel(RadParams prm) {
+  static_assert(R % 2 == 0, "targets are processed in pairs");
+  constexpr int RP = R / 2;
+  constexpr int NF = Rec2<MB>::NF;
+  constexpr int kTileFloats = kTile * NF;
+  extern __shared__ __align__(128) unsigned char smem[];
+  float* buf = reinterpret_cast<float*>(smem);
+  double2* dacc = reinterpret_cast<double2*>(smem + 2 * kTileFloats * sizeof(float));
+  __shared__ __align__(8) uint64_t bars[2];
+
+  const int tid = threadIdx.x;
+  const int64_t tbase = (int64_t)blockIdx.x * (R * kThreads);
+  const int split = blockIdx.y;
+  const int mch = blockIdx.z;
+
+  f2r tx[RP], ty[RP], tz[RP];
+#pragma unroll
+  for (int p = 0; p < RP; ++p) {
+    float c[2][3];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      int64_t l = tbase + (2 * p + h) * kThreads + tid;
+      if (l >= prm.n_lis) l = prm.n_lis - 1;
+      c[h][0] = (float)(prm.lis[l] - prm.cx);
+      c[h][1] = (float)(prm.lis[prm.n_lis + l] - prm.cy);
+      c[h][2] = (float)(prm.lis[2 * prm.n_lis + l] - prm.cz);
+    }
+    tx[p] = f2pack(c[0][0], c[1][0]);
+    ty[p] = f2pack(c[0][1], c[1][1]);
+    tz[p] = f2pack(c[0][2], c[1][2]);
+  }
+  f2r kk[MB];
+#pragma unroll
+  for (int m = 0; m < MB; ++m) {
+    const float k = prm.k.f[mch * MB + m];
+    kk[m] = f2pack(k, k);
+  }
+  const f2r minus1 = f2pack(-1.f, -1.f);
+#pragma unroll
+  for (int q = 0; q < R * MB; ++q) dacc[q * kThreads + tid] = make_double2(0.0, 0.0);
+
+  const int t0 = split * prm.chunk_tiles;
+  const int t1 = min(t0 + prm.chunk_tiles, prm.n_tiles);
+  const float* src = static_cast<const float*>(prm.rec) + (size_t)mch * prm.n_src_pad * NF;
+  constexpr uint32_t kBytes = kTileFloats * sizeof(float);
+
+  if (tid == 0) {
+    nat::mbar_init(&bars[0], 1);
+    nat::mbar_init(&bars[1], 1);
+    nat::fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int st = 0; st < 2 && t0 + st < t1; ++st) {
+      nat::mbar_arrive_expect_tx(&bars[st], kBytes);
+      nat::bulk_g2s(buf + st * kTileFloats, src + (size_t)(t0 + st) * kTileFloats, kBytes, &bars[st]);
+    }
+  }
+
+  for (int it = 0; t0 + it < t1; ++it) {
+    const int st = it & 1;
+    nat::mbar_wait(&bars[st], (it >> 1) & 1);
+    const ulonglong2* b4 = reinterpret_cast<const ulonglong2*>(buf + st * kTileFloats);
+    f2r ar[RP][MB], ai[RP][MB];
+#pragma unroll
+    for (int p = 0; p < RP; ++p)
+#pragma unroll
+      for (int m = 0; m < MB; ++m) ar[p][m] = ai[p][m] = 0ull;
+
+#pragma unroll 2
+    for (int s = 0; s < kTile; ++s) {
+      f2r f[NF / 2];
+#pragma unroll
+      for (int q = 0; q < NF / 4; ++q) {
+        const ulonglong2 v = b4[s * (NF / 4) + q];
+        f[2 * q] = v.x;
+        f[2 * q + 1] = v.y;
+      }
+#pragma unroll
+      for (int p = 0; p < RP; ++p) {
+        const f2r dx = f2sub(f[0], tx[p]);
+        const f2r dy = f2sub(f[1], ty[p]);
+        const f2r dz = f2sub(f[2], tz[p]);
+        const f2r r2 = f2fma(dz, dz, f2fma(dy, dy, f2mul(dx, dx)));
+        const f2r dn = f2fma(dz, f[5], f2fma(dy, f[4], f2mul(dx, f[3])));
+        const float r2a = f2lo(r2), r2b = f2hi(r2);
+        const float ra = SELF ? (r2a > prm.self_r2 ? rsqrt_approx(r2a) : 0.f) : rsqrt_approx(r2a);
+        const float rb = SELF ? (r2b > prm.self_r2 ? rsqrt_approx(r2b) : 0.f) : rsqrt_approx(r2b);
+        const f2r rho = f2pack(ra, rb);
+        const f2r qq = f2mul(dn, f2mul(rho, rho));
+        const f2r rr = f2mul(r2, rho);
+#pragma unroll
+        for (int m = 0; m < MB; ++m) {
+          const f2r kr = f2mul(rr, kk[m]);
+          float sa, ca, sb, cb;
+          __sincosf(f2lo(kr), &sa, &ca);
+          __sincosf(f2hi(kr), &sb, &cb);
+          const f2r sn = f2pack(sa, sb), cs = f2pack(ca, cb);
+          const f2r* c = f + 6 + 6 * m;  // A1 A2 A3 A4 B1 B2 (pairs)
+          const f2r cr = f2fma(qq, f2fma(rho, c[0], c[1]), f2mul(rho, c[4]));
+          const f2r ci = f2fma(qq, f2fma(rho, c[3], c[2]), f2mul(rho, c[5]));
+          const f2r nci = f2mul(ci, minus1);
+          ar[p][m] = f2fma(cs, cr, f2fma(sn, nci, ar[p][m]));
+          ai[p][m] = f2fma(sn, cr, f2fma(cs, ci, ai[p][m]));
+        }
+      }
+    }
+#pragma unroll
+    for (int p = 0; p < RP; ++p)
+#pragma unroll
+      for (int m = 0; m < MB; ++m) {
+        const int q0 = (2 * p) * MB + m, q1 = (2 * p + 1) * MB + m;
+        double2 d0 = dacc[q0 * kThreads + tid], d1 = dacc[q1 * kThreads + tid];
+        d0.x += (double)f2lo(ar[p][m]);
+        d0.y += (double)f2lo(ai[p][m]);
+        d1.x += (double)f2hi(ar[p][m]);
+        d1.y += (double)f2hi(ai[p][m]);
+        dacc[q0 * kThreads + tid] = d0;
+        dacc[q1 * kThreads + tid] = d1;
+      }
+    __syncthreads();  // every thread is done with buf[st]
+    if (tid == 0 && t0 + it + 2 < t1) {
+      nat::fence_proxy_async_smem();
+      nat::mbar_arrive_expect_tx(&bars[st], kBytes);
+      nat::bulk_g2s(buf + st * kTileFloats, src + (size_t)(t0 + it + 2) * kTileFloats, kBytes, &bars[st]);
+    }
+  }
+
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    int64_t l = tbase + r * kThreads + tid;
+    if (l >= prm.n_lis) continue;
+#pragma unroll
+    for (int m = 0; m < MB; ++m) {
+      int mode = mch * MB + m;
+      if (mode < prm.n_modes)
+        prm.out[((size_t)split * prm.n_modes + mode) * prm.n_lis + l] = dacc[(r * MB + m) * kThreads + tid];
+    }
+  }
 }
 
 // SELF = 1: targets coincide with the sources (MC operators): the self pair has d = 0
@@ -410,7 +615,7 @@ Plan make_plan(nat_prec prec, int64_t n_src, int n_modes, int64_t n_lis) {
   } else {
     pl.MB = pick_mb(n_modes);
     pl.R = 4;
-    pl.NF = ((6 + 6 * pl.MB) + 3) / 4 * 4;
+    pl.NF = 12 + 12 * pl.MB;  // duplicated records of the FP32x2 kernel
     pl.tile = kTile;
   }
   pl.n_mchunk = (n_modes + pl.MB - 1) / pl.MB;
@@ -418,7 +623,8 @@ Plan make_plan(nat_prec prec, int64_t n_src, int n_modes, int64_t n_lis) {
   pl.n_src_pad = (int64_t)pl.n_tiles * pl.tile;
   pl.tgt_tiles = (n_lis + (int64_t)pl.R * kThreads - 1) / ((int64_t)pl.R * kThreads);
   int64_t base = pl.tgt_tiles * pl.n_mchunk;
-  int64_t want = 4LL * nat::kNumSMs * 2;  // enough CTAs for several full waves
+  // enough CTAs for ~2 waves at 2-4 resident CTAs/SM, without inflating the partials
+  int64_t want = 2LL * nat::kNumSMs * (pl.MB == 1 ? 4 : 2);
   int n_split = 1;
   if (base < want) n_split = (int)nat::min64((want + base - 1) / base, pl.n_tiles);
   pl.chunk_tiles = (pl.n_tiles + n_split - 1) / n_split;
@@ -439,7 +645,7 @@ size_t plan_ws(const Plan& pl, int n_modes, int64_t n_lis, nat::Carver& c, void*
 
 template <int R, int MB, int SELF>
 cudaError_t launch_f32(const Plan& pl, const RadParams& prm, cudaStream_t s) {
-  auto kern = radiate_f32_kernel<R, MB, SELF>;
+  auto kern = radiate_f32x2_kernel<R, MB, SELF>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
   if (e != cudaSuccess) return e;
   dim3 grid((unsigned)pl.tgt_tiles, (unsigned)pl.n_split, (unsigned)pl.n_mchunk);
@@ -495,7 +701,7 @@ nat_status radiate_internal(const RadInput& in, nat_prec prec, const double* k, 
           in.xyz, in.nrm, in.w, in.w_const, p, g, in.ldpg, kv, nm, in.center[0], in.center[1],
           in.center[2], (double*)rec);
     else
-      stage_kernel<float><<<sblocks, 256, 0, s>>>(in.n_src, pl.n_src_pad, pl.NF, pl.MB, pl.n_mchunk,
+      stage_kernel<float, true><<<sblocks, 256, 0, s>>>(in.n_src, pl.n_src_pad, pl.NF, pl.MB, pl.n_mchunk,
           in.xyz, in.nrm, in.w, in.w_const, p, g, in.ldpg, kv, nm, in.center[0], in.center[1],
           in.center[2], (float*)rec);
     NAT_LAUNCH_CHECK();

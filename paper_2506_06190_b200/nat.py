@@ -525,13 +525,13 @@ def row_range(n: int, rank: int, world: int):
 
 
 def nat_bem_solve(A_local: torch.Tensor, b_local: torch.Tensor, n: int, row_begin=0, comm: Optional[Comm] = None,
-                  tol=1e-6, max_iter=200, ws=None):
+                  tol=1e-6, max_iter=200, ws=None, out=None):
     """Returns (x c128 [n], info dict).  Raises on errors; non-convergence is reported
     in info['converged'] (status NAT_WARN_NOT_CONVERGED)."""
     pr = NAT_FP32 if A_local.dtype == torch.complex64 else NAT_FP64
     rows, lda = A_local.shape
     dev = A_local.device
-    x = torch.empty(n, dtype=torch.complex128, device=dev)
+    x = torch.empty(n, dtype=torch.complex128, device=dev) if out is None else out
     if ws is None:
         ws = _ws(lib().nat_bem_solve_workspace(pr, n, rows, max_iter), dev)
     info = _SolveInfo()

@@ -1,0 +1,9 @@
+python -m paper_2506_06190_b200.build > /dev/null || exit 1
+timeout 1500 python -m pytest -x -q -m gpu tests/ 2>&1 | tail -5
+timeout 600 python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bench2.json 2> gpurun_out/bench2.err; echo "bench rc=$?"
+python - <<'P'
+import json; d=json.load(open('gpurun_out/bench2.json'))
+print(d['value'], d['ms_per_step'], d['phase_ms_per_step'], d['gmres_iters'], d['mc_gmres_iters'])
+for k,v in d['rooflines'].items(): print(k, round(v['achieved'],1), round(v['frac'],3))
+print(d['e2e'], d['gpu_launches'], d['clocks'])
+P

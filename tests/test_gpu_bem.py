@@ -106,7 +106,8 @@ def test_matvec_parity(prec):
         At = torch.from_numpy(A).to(dt).cuda()
         y = to_np(nat.nat_bem_matvec(At, torch.from_numpy(x).cuda(), n=n))
         Aq = to_np(At).astype(np.complex128)[:, :n]      # the stored (rounded) matrix
-        assert rel_l2(y, Aq @ x) <= 1e-13
+        # fp64: fp64 products; fp32 (c64 matrix): fp32 products flushed to fp64 every 16
+        assert rel_l2(y, Aq @ x) <= (1e-13 if prec == "fp64" else 1e-6)
 
 
 @pytest.mark.parametrize("prec", ["fp32", "fp64"])
