@@ -20,6 +20,7 @@
 #include <cmath>
 #include <vector>
 
+#include "f32x2.cuh"
 #include "nat_internal.cuh"
 #include "pair.cuh"
 
@@ -29,7 +30,7 @@ using nat::C2;
 
 constexpr int kThreads = 256;
 constexpr int kTI = 16;       // rows per far CTA
-constexpr int kCC = 4;        // column passes per far CTA (columns = 256 * kCC)
+constexpr int kCC = 8;        // column passes per far CTA (columns = 256 * kCC)
 constexpr int kMaxFarQ = 7;
 constexpr int kNRmax = 2;
 
@@ -304,6 +305,142 @@ __global__ void __launch_bounds__(kThreads) far_kernel(FarArgs<R> a) {
   }
 }
 
+// NAT_FP32 far assembly on the packed FP32x2 pipe: two rows (collocation points) share
+// each instruction, the column's quadrature data is broadcast into both halves.  Per
+// quadrature point and row: 11 packed-pipe instructions + 1 FMUL.RZ + 3 MUFU.  The kernel
+// accumulates -K directly (A_ij = -K_ij off the diagonal) and V g for the RHS.
+template <int NQ, int NR>
+__global__ void __launch_bounds__(kThreads, 3) far_kernel_x2(FarArgs<float> a) {
+  static_assert(kTI % 2 == 0, "row pairs");
+  constexpr int TP = kTI / 2;
+  constexpr int NRr = NR > 0 ? NR : 1;
+  __shared__ __align__(16) f2r s_c[3][TP];
+  __shared__ double2 s_red[kThreads / 32][kTI][NRr];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t i0 = (int64_t)blockIdx.y * kTI;
+  const int64_t n = a.n;
+  if (tid < TP) {
+    float c[2][3];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t r = i0 + 2 * tid + h;
+      const int64_t i = a.row_begin + (r < a.rows ? r : 0);
+      c[h][0] = (float)(a.cen[i] - a.cx);
+      c[h][1] = (float)(a.cen[n + i] - a.cy);
+      c[h][2] = (float)(a.cen[2 * n + i] - a.cz);
+    }
+#pragma unroll
+    for (int d = 0; d < 3; ++d) s_c[d][tid] = f2pack(c[0][d], c[1][d]);
+  }
+  __syncthreads();
+  const int nrows = (int)nat::min64(kTI, a.rows - i0);
+  const f2r kk = f2pack(a.k, a.k), nkk = f2pack(-a.k, -a.k);
+  f2r br[TP][NRr], bi[TP][NRr];  // sum_j V_ij g_j for the row pair (real / imaginary)
+#pragma unroll
+  for (int t = 0; t < TP; ++t)
+#pragma unroll
+    for (int q = 0; q < NRr; ++q) br[t][q] = bi[t][q] = 0ull;
+
+  for (int cc = 0; cc < kCC; ++cc) {
+    const int64_t j = (int64_t)blockIdx.x * (kThreads * kCC) + cc * kThreads + tid;
+    const bool valid = j < n;
+    const int64_t jj = valid ? j : 0;
+    f2r y[NQ][3], w[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        const float v = a.cols.qxyz[((size_t)q * 3 + d) * n + jj];
+        y[q][d] = f2pack(v, v);
+      }
+      const float wv = valid ? a.cols.qw[(size_t)q * n + jj] : 0.f;
+      w[q] = f2pack(wv, wv);
+    }
+    const float nxs = a.cols.nrm[jj], nys = a.cols.nrm[n + jj], nzs = a.cols.nrm[2 * n + jj];
+    const f2r nx = f2pack(nxs, nxs), ny = f2pack(nys, nys), nz = f2pack(nzs, nzs);
+    f2r gr[NRr], gi[NRr], ngi[NRr];
+#pragma unroll
+    for (int q = 0; q < NR; ++q) {
+      const double2 gv = valid ? a.g[(size_t)(a.rhs0 + q) * n + jj] : make_double2(0.0, 0.0);
+      gr[q] = f2pack((float)gv.x, (float)gv.x);
+      gi[q] = f2pack((float)gv.y, (float)gv.y);
+      ngi[q] = f2pack(-(float)gv.y, -(float)gv.y);
+    }
+#pragma unroll
+    for (int t = 0; t < TP; ++t) {
+      if (2 * t < nrows) {
+        const f2r cx = s_c[0][t], cy = s_c[1][t], cz = s_c[2][t];
+        f2r Vr = 0ull, Vi = 0ull, Kr = 0ull, Ki = 0ull;  // K here is -K
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+          const f2r dx = f2sub(y[q][0], cx), dy = f2sub(y[q][1], cy), dz = f2sub(y[q][2], cz);
+          const f2r r2 = f2fma(dz, dz, f2fma(dy, dy, f2mul(dx, dx)));
+          const f2r dn = f2fma(dz, nz, f2fma(dy, ny, f2mul(dx, nx)));
+          const f2r rho = f2pack(nat::pair_rsqrt(f2lo(r2)), nat::pair_rsqrt(f2hi(r2)));
+          const f2r rr = f2mul(r2, rho);
+          const f2r kr = f2mul(rr, kk), nkr = f2mul(rr, nkk);
+          float s0, c0, s1, c1;
+          __sincosf(f2lo(kr), &s0, &c0);
+          __sincosf(f2hi(kr), &s1, &c1);
+          const f2r sn = f2pack(s0, s1), cs = f2pack(c0, c1);
+          const f2r tq = f2mul(w[q], rho);               // w G-part: tq e^{ikr}
+          Vr = f2fma(tq, cs, Vr);
+          Vi = f2fma(tq, sn, Vi);
+          const f2r u = f2mul(tq, f2mul(dn, f2mul(rho, rho)));
+          // -K += u (c + kr s) + i u (s - kr c)   [K = u (ikr - 1) e^{ikr}]
+          Kr = f2fma(u, f2fma(kr, sn, cs), Kr);
+          Ki = f2fma(u, f2fma(nkr, cs, sn), Ki);
+        }
+        if (a.store_A && valid) {
+          float2* A2 = reinterpret_cast<float2*>(a.A);
+          A2[(size_t)(i0 + 2 * t) * a.lda + j] = make_float2(f2lo(Kr), f2lo(Ki));
+          if (2 * t + 1 < nrows) A2[(size_t)(i0 + 2 * t + 1) * a.lda + j] = make_float2(f2hi(Kr), f2hi(Ki));
+        }
+#pragma unroll
+        for (int q = 0; q < NR; ++q) {
+          br[t][q] = f2fma(Vr, gr[q], f2fma(Vi, ngi[q], br[t][q]));
+          bi[t][q] = f2fma(Vr, gi[q], f2fma(Vi, gr[q], bi[t][q]));
+        }
+      }
+    }
+  }
+  if constexpr (NR > 0) {
+#pragma unroll
+    for (int t = 0; t < kTI; ++t)
+#pragma unroll
+      for (int q = 0; q < NR; ++q) {
+        const f2r pr = br[t / 2][q], pi = bi[t / 2][q];
+        double vx = (double)((t & 1) ? f2hi(pr) : f2lo(pr)), vy = (double)((t & 1) ? f2hi(pi) : f2lo(pi));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          vx += __shfl_xor_sync(0xffffffffu, vx, o);
+          vy += __shfl_xor_sync(0xffffffffu, vy, o);
+        }
+        if (lane == 0) s_red[warp][t][q] = make_double2(vx, vy);
+      }
+    __syncthreads();
+    if (tid < kTI * NR) {
+      const int t = tid / NR, q = tid % NR;
+      if (t < nrows) {
+        double2 s = s_red[0][t][q];
+        for (int wv = 1; wv < kThreads / 32; ++wv) {
+          s.x += s_red[wv][t][q].x;
+          s.y += s_red[wv][t][q].y;
+        }
+        a.bpart[((size_t)blockIdx.x * a.n_rhs + a.rhs0 + q) * a.rows + i0 + t] = make_double2(-s.x, -s.y);
+      }
+    }
+  }
+}
+
+template <typename R, int NQ, int NR>
+void launch_far(dim3 grid, const FarArgs<R>& fa, cudaStream_t s) {
+  if constexpr (sizeof(R) == 4)
+    far_kernel_x2<NQ, NR><<<grid, kThreads, 0, s>>>(fa);
+  else
+    far_kernel<R, NQ, NR><<<grid, kThreads, 0, s>>>(fa);
+}
+
 template <typename R>
 struct NearArgs {
   int64_t n, nv, row_begin, rows, lda, nnz;
@@ -317,6 +454,7 @@ struct NearArgs {
   const double* nrm;
   const double* area;
   const double4* rule;     // near rule points (parent barycentrics, weight)
+  const float4* rule_f;    // the same rule in fp32 (fp32 path)
   int npts;
   FarCols<R> cols;         // far rule (to subtract the far contribution from b)
   double cx, cy, cz;
@@ -348,12 +486,31 @@ __global__ void __launch_bounds__(kThreads) near_kernel(NearArgs<R> a) {
   const R nx = (R)a.nrm[j], ny = (R)a.nrm[n + j], nz = (R)a.nrm[2 * n + j];
   const double wA = a.area[j] * nat::kInv4Pi;
   R Vr = 0, Vi = 0, Kr = 0, Ki = 0;
-  for (int q = lig; q < a.npts; q += G) {
-    const double4 L = a.rule[q];
-    R d[3];
+  if constexpr (sizeof(R) == 4) {
+    // fp32 path: vertex offsets from the collocation point are formed in fp64 once per
+    // pair and rounded (|v - c_i| ~ element size, so the rounding is relative to r);
+    // each quadrature point is then d = l1 e1 + l2 e2 + l3 e3 in fp32
+    float e[3][3];
 #pragma unroll
-    for (int c = 0; c < 3; ++c) d[c] = (R)(((L.x * v[0][c] + L.y * v[1][c]) + L.z * v[2][c]) - ci[c]);
-    nat::pair_accumulate<R>(d[0], d[1], d[2], nx, ny, nz, (R)(L.w * wA), a.k, Vr, Vi, Kr, Ki);
+    for (int p = 0; p < 3; ++p)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) e[p][c] = (float)(v[p][c] - ci[c]);
+    const float wAf = (float)wA;
+    for (int q = lig; q < a.npts; q += G) {
+      const float4 L = a.rule_f[q];
+      float d[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) d[c] = fmaf(L.z, e[2][c], fmaf(L.y, e[1][c], L.x * e[0][c]));
+      nat::pair_accumulate<float>(d[0], d[1], d[2], nx, ny, nz, L.w * wAf, a.k, Vr, Vi, Kr, Ki);
+    }
+  } else {
+    for (int q = lig; q < a.npts; q += G) {
+      const double4 L = a.rule[q];
+      R d[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) d[c] = (R)(((L.x * v[0][c] + L.y * v[1][c]) + L.z * v[2][c]) - ci[c]);
+      nat::pair_accumulate<R>(d[0], d[1], d[2], nx, ny, nz, (R)(L.w * wA), a.k, Vr, Vi, Kr, Ki);
+    }
   }
   const unsigned mask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << ((threadIdx.x & 31) / G * G));
 #pragma unroll
@@ -661,6 +818,8 @@ struct AsmWs {
   double4* rule_far;
   double4* rule_S;
   double4* rule_N;
+  float4* rule_Sf;
+  float4* rule_Nf;
   double* gl;     // [2][ngl]
   void* qxyz;
   void* qw;
@@ -678,6 +837,8 @@ size_t carve(nat::Carver& c, AsmWs& w, int64_t n, int64_t rows, int64_t nnz, int
   w.rule_S = c.take<double4>(nS);
   w.rule_N = c.take<double4>(nN);
   w.gl = c.take<double>(2 * (size_t)ngl);
+  w.rule_Sf = c.take<float4>(nS);
+  w.rule_Nf = c.take<float4>(nN);
   w.qxyz = c.take<char>(rsz * kMaxFarQ * 3 * n);
   w.qw = c.take<char>(rsz * kMaxFarQ * n);
   w.qn = c.take<char>(rsz * 3 * n);
@@ -724,15 +885,15 @@ nat_status assemble_impl(const nat_mesh* mesh, const nat_geom* geom, const Opts&
   dim3 grid((unsigned)n_colblk, (unsigned)((rows + kTI - 1) / kTI));
   if (n_rhs == 0) {
     fa.store_A = true;
-    far_kernel<R, NQ, 0><<<grid, kThreads, 0, s>>>(fa);
+    launch_far<R, NQ, 0>(grid, fa, s);
   } else {
     for (int q0 = 0; q0 < n_rhs; q0 += kNRmax) {
       fa.rhs0 = q0;
       fa.store_A = (q0 == 0);
       if (n_rhs - q0 >= 2)
-        far_kernel<R, NQ, 2><<<grid, kThreads, 0, s>>>(fa);
+        launch_far<R, NQ, 2>(grid, fa, s);
       else
-        far_kernel<R, NQ, 1><<<grid, kThreads, 0, s>>>(fa);
+        launch_far<R, NQ, 1>(grid, fa, s);
     }
   }
   NAT_LAUNCH_CHECK();
@@ -765,9 +926,11 @@ nat_status assemble_impl(const nat_mesh* mesh, const nat_geom* geom, const Opts&
     na.A = A;
     na.corr = w.corr;
     na.rule = w.rule_S;
+    na.rule_f = w.rule_Sf;
     na.npts = (int)pS.size();
     near_kernel<R, NQ, 32, 1><<<(unsigned)((nnz * 32 + kThreads - 1) / kThreads), kThreads, 0, s>>>(na);
     na.rule = w.rule_N;
+    na.rule_f = w.rule_Nf;
     na.npts = (int)pN.size();
     near_kernel<R, NQ, 8, 2><<<(unsigned)((nnz * 8 + kThreads - 1) / kThreads), kThreads, 0, s>>>(na);
     NAT_LAUNCH_CHECK();
@@ -852,6 +1015,11 @@ extern "C" nat_status nat_bem_assemble(const nat_mesh* mesh, const nat_geom* geo
   NAT_CUDA_TRY(cudaMemcpyAsync(w.rule_far, pF.data(), pF.size() * sizeof(Pt), cudaMemcpyHostToDevice, s));
   NAT_CUDA_TRY(cudaMemcpyAsync(w.rule_S, pS.data(), pS.size() * sizeof(Pt), cudaMemcpyHostToDevice, s));
   NAT_CUDA_TRY(cudaMemcpyAsync(w.rule_N, pN.data(), pN.size() * sizeof(Pt), cudaMemcpyHostToDevice, s));
+  std::vector<float4> fS(pS.size()), fN(pN.size());
+  for (size_t q = 0; q < pS.size(); ++q) fS[q] = make_float4((float)pS[q].l1, (float)pS[q].l2, (float)pS[q].l3, (float)pS[q].w);
+  for (size_t q = 0; q < pN.size(); ++q) fN[q] = make_float4((float)pN[q].l1, (float)pN[q].l2, (float)pN[q].l3, (float)pN[q].w);
+  NAT_CUDA_TRY(cudaMemcpyAsync(w.rule_Sf, fS.data(), fS.size() * sizeof(float4), cudaMemcpyHostToDevice, s));
+  NAT_CUDA_TRY(cudaMemcpyAsync(w.rule_Nf, fN.data(), fN.size() * sizeof(float4), cudaMemcpyHostToDevice, s));
   std::vector<double> gl(glx);
   gl.insert(gl.end(), glw.begin(), glw.end());
   NAT_CUDA_TRY(cudaMemcpyAsync(w.gl, gl.data(), gl.size() * sizeof(double), cudaMemcpyHostToDevice, s));

@@ -539,7 +539,7 @@ size_t mc_carve(nat::Carver& c, McWs* w, nat_prec prec, int64_t M, int n_sys, in
   t.gs = c.take<double2>((size_t)nb * M);
   t.b = c.take<double2>((size_t)nb * M);
   nat::krylov_workspace(nb, M, M, max_iter, c, &t.kw);
-  t.rad_bytes = nat::radiate_ws_bytes(prec, M, nb, M);
+  t.rad_bytes = nat::radiate_ws_bytes_upto(prec, M, nb, M);  // the operator shrinks to the active systems
   t.rad = c.take<char>(t.rad_bytes);
   carve_near(c, &t.np, M);
   t.tin = c.take<double2>((size_t)nb * M);

@@ -40,8 +40,13 @@ __global__ void __launch_bounds__(kWarps * 32) near_kernel(NearArgs a) {
   const int64_t r0 = (int64_t)blockIdx.x * kRowsPerCta + warp * kRowsPerWarp;
   const int64_t nt = a.nt;
 
+  // the rows' fp64 centroids live in shared memory (used only by the exact test, rarely)
+  __shared__ double s_rc[kWarps][kRowsPerWarp][3];
+  __shared__ float s_rd[kWarps][kRowsPerWarp];
+  __shared__ float s_rb[8];            // rows: min xyz, -max xyz, max diam, fp32 margin
+  __shared__ float s_tb[kWarps][7];    // tile reduction scratch
+  __shared__ int s_skip;
   int64_t gi[kRowsPerWarp];
-  double cx[kRowsPerWarp], cy[kRowsPerWarp], cz[kRowsPerWarp];
   float fx[kRowsPerWarp], fy[kRowsPerWarp], fz[kRowsPerWarp], fd[kRowsPerWarp];
   int32_t va[kRowsPerWarp], vb[kRowsPerWarp], vc[kRowsPerWarp];
   int64_t pos[kRowsPerWarp];
@@ -52,17 +57,39 @@ __global__ void __launch_bounds__(kWarps * 32) near_kernel(NearArgs a) {
     live[q] = r < a.rows;
     int64_t i = a.row_begin + (live[q] ? r : 0);
     gi[q] = i;
-    cx[q] = a.cen[i];
-    cy[q] = a.cen[nt + i];
-    cz[q] = a.cen[2 * nt + i];
-    fx[q] = (float)cx[q];
-    fy[q] = (float)cy[q];
-    fz[q] = (float)cz[q];
+    const double cxd = a.cen[i], cyd = a.cen[nt + i], czd = a.cen[2 * nt + i];
+    if (lane == 0) {
+      s_rc[warp][q][0] = cxd;
+      s_rc[warp][q][1] = cyd;
+      s_rc[warp][q][2] = czd;
+      s_rd[warp][q] = live[q] ? (float)a.diam[i] : -1.f;
+    }
+    fx[q] = (float)cxd;
+    fy[q] = (float)cyd;
+    fz[q] = (float)czd;
     fd[q] = (float)a.diam[i];
     va[q] = a.tri[i];
     vb[q] = a.tri[nt + i];
     vc[q] = a.tri[2 * nt + i];
     pos[q] = (kBuild && live[q]) ? a.row_ptr[r] : 0;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {  // bounding box of this CTA's live rows (fp32, for tile skipping)
+    float b[7] = {3e30f, 3e30f, 3e30f, 3e30f, 3e30f, 3e30f, 0.f};
+    float mabs = 0.f;
+    for (int w = 0; w < kWarps; ++w)
+      for (int q = 0; q < kRowsPerWarp; ++q) {
+        if (s_rd[w][q] < 0.f) continue;
+        for (int d = 0; d < 3; ++d) {
+          const float c = (float)s_rc[w][q][d];
+          b[d] = fminf(b[d], c);
+          b[3 + d] = fminf(b[3 + d], -c);
+          mabs = fmaxf(mabs, fabsf(c));
+        }
+        b[6] = fmaxf(b[6], s_rd[w][q]);
+      }
+    for (int c = 0; c < 7; ++c) s_rb[c] = b[c];
+    s_rb[7] = 1e-5f * (1.f + mabs);
   }
 
   for (int64_t j0 = 0; j0 < nt; j0 += kJTile) {
@@ -84,7 +111,41 @@ __global__ void __launch_bounds__(kWarps * 32) near_kernel(NearArgs a) {
         s_v[2][t] = a.tri[2 * nt + j];
       }
     }
-    __syncthreads();
+    // tile bounding box + reach (fp32, conservative): skip the whole tile when it cannot
+    // hold a listed column of any of this CTA's rows (uniform branch)
+    {
+      const int t = threadIdx.x;
+      const bool ok = j0 + t < nt;
+      float v[7] = {ok ? s_f[0][t] : 3e30f, ok ? s_f[1][t] : 3e30f, ok ? s_f[2][t] : 3e30f,
+                    ok ? -s_f[0][t] : 3e30f, ok ? -s_f[1][t] : 3e30f, ok ? -s_f[2][t] : 3e30f,
+                    ok ? -fmaxf(s_f[3][t], s_f[4][t]) : 0.f};
+      // v[6] holds -max(eta diam, diam); min-reductions throughout
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int c = 0; c < 7; ++c) v[c] = fminf(v[c], __shfl_xor_sync(0xffffffffu, v[c], o));
+      if (lane == 0)
+#pragma unroll
+        for (int c = 0; c < 7; ++c) s_tb[warp][c] = v[c];
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        float b[7];
+        for (int c = 0; c < 7; ++c) {
+          b[c] = s_tb[0][c];
+          for (int w = 1; w < kWarps; ++w) b[c] = fminf(b[c], s_tb[w][c]);
+        }
+        float g2 = 0.f;
+        for (int d = 0; d < 3; ++d) {
+          // rows: [s_rb[d], -s_rb[3+d]], tile: [b[d], -b[3+d]]
+          const float gap = fmaxf(0.f, fmaxf(s_rb[d] + b[3 + d], b[d] + s_rb[3 + d]));
+          g2 += gap * gap;
+        }
+        const float reach = fmaxf(-b[6], s_rb[6] + (-b[6])) * 1.01f + s_rb[7];
+        s_skip = g2 > reach * reach;
+      }
+      __syncthreads();
+      if (s_skip) continue;
+    }
     const int jn = (int)nat::min64(kJTile, nt - j0);
     for (int jj = 0; jj < jn; jj += 32) {
       const int t = jj + lane;
@@ -112,7 +173,8 @@ __global__ void __launch_bounds__(kWarps * 32) near_kernel(NearArgs a) {
           shares = (u0 == va[q] || u0 == vb[q] || u0 == vc[q] || u1 == va[q] || u1 == vb[q] ||
                     u1 == vc[q] || u2 == va[q] || u2 == vb[q] || u2 == vc[q]);
           // the exact predicate (reading R-near): fp64, round-to-nearest, no contraction
-          double dx = __dsub_rn(cx[q], s_cx[t]), dy = __dsub_rn(cy[q], s_cy[t]), dz = __dsub_rn(cz[q], s_cz[t]);
+          double dx = __dsub_rn(s_rc[warp][q][0], s_cx[t]), dy = __dsub_rn(s_rc[warp][q][1], s_cy[t]),
+                 dz = __dsub_rn(s_rc[warp][q][2], s_cz[t]);
           double dist = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)),
                                              __dmul_rn(dz, dz)));
           hit = shares || dist < s_thr[t];

@@ -15,6 +15,7 @@
 //    fixed-order fp64 reduction (deterministic, no atomics).
 #include "async_copy.cuh"
 #include "nat_internal.cuh"
+#include "f32x2.cuh"
 #include "pair.cuh"
 #include "radiate.cuh"
 
@@ -138,43 +139,6 @@ __device__ __forceinline__ float rsqrt_approx(float x) {
 // (x x y y z z nx nx ...) so a packed operand is one half of an LDS.128 broadcast.
 // Per pair: 12.5 FP32-pipe instructions + 3 MUFU (rsqrt, sin, cos) instead of 24 + 3.
 // ------------------------------------------------------------------------------------
-typedef unsigned long long f2r;  // a float2 in a 64-bit register pair
-__device__ __forceinline__ f2r f2pack(float lo, float hi) {
-  f2r r;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
-  return r;
-}
-__device__ __forceinline__ float f2lo(f2r a) {
-  float lo, hi;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(a));
-  return lo;
-}
-__device__ __forceinline__ float f2hi(f2r a) {
-  float lo, hi;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(a));
-  return hi;
-}
-__device__ __forceinline__ f2r f2add(f2r a, f2r b) {
-  f2r r;
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-  return r;
-}
-__device__ __forceinline__ f2r f2sub(f2r a, f2r b) {
-  f2r r;
-  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-  return r;
-}
-__device__ __forceinline__ f2r f2mul(f2r a, f2r b) {
-  f2r r;
-  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-  return r;
-}
-__device__ __forceinline__ f2r f2fma(f2r a, f2r b, f2r c) {
-  f2r r;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
-  return r;
-}
-
 template <int MB>
 struct Rec2 {
   static constexpr int NF = 12 + 12 * MB;  // duplicated floats per source record
@@ -604,6 +568,40 @@ int pick_mb(int n_modes) {
   return 1;
 }
 
+template <int R, int MB>
+int occ_of(size_t smem) {
+  int occ = 0;
+  auto k = radiate_f32x2_kernel<R, MB, 0>;
+  if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kThreads, smem) != cudaSuccess) {
+    cudaGetLastError();
+    return 2;
+  }
+  return occ > 0 ? occ : 1;
+}
+
+// Resident CTAs per SM of the radiation kernel instance (cached per configuration).
+int occupancy(bool fp64, int R, int MB, size_t smem) {
+  static int cache[2][5][5];  // [fp64][R][MB], 0 = unknown
+  int& c = cache[fp64 ? 1 : 0][R][MB];
+  if (c) return c;
+  if (fp64) {
+    int occ = 0;
+    auto k = radiate_f64_kernel<2>;
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kThreads, smem) != cudaSuccess) {
+      cudaGetLastError();
+      occ = 2;
+    }
+    c = occ > 0 ? occ : 1;
+  } else if (R == 2) {
+    c = MB == 1 ? occ_of<2, 1>(smem) : MB == 2 ? occ_of<2, 2>(smem) : MB == 3 ? occ_of<2, 3>(smem) : occ_of<2, 4>(smem);
+  } else {
+    c = MB == 1 ? occ_of<4, 1>(smem) : MB == 2 ? occ_of<4, 2>(smem) : MB == 3 ? occ_of<4, 3>(smem) : occ_of<4, 4>(smem);
+  }
+  return c;
+}
+
 Plan make_plan(nat_prec prec, int64_t n_src, int n_modes, int64_t n_lis) {
   Plan pl{};
   pl.fp64 = (prec == NAT_FP64);
@@ -621,19 +619,42 @@ Plan make_plan(nat_prec prec, int64_t n_src, int n_modes, int64_t n_lis) {
   pl.n_mchunk = (n_modes + pl.MB - 1) / pl.MB;
   pl.n_tiles = (int)((n_src + pl.tile - 1) / pl.tile);
   pl.n_src_pad = (int64_t)pl.n_tiles * pl.tile;
-  pl.tgt_tiles = (n_lis + (int64_t)pl.R * kThreads - 1) / ((int64_t)pl.R * kThreads);
-  int64_t base = pl.tgt_tiles * pl.n_mchunk;
-  // enough CTAs for ~2 waves at 2-4 resident CTAs/SM, without inflating the partials
-  int64_t want = 2LL * nat::kNumSMs * (pl.MB == 1 ? 4 : 2);
-  int n_split = 1;
-  if (base < want) n_split = (int)nat::min64((want + base - 1) / base, pl.n_tiles);
-  pl.chunk_tiles = (pl.n_tiles + n_split - 1) / n_split;
+  // Choose targets/thread R and the source chunk (tiles per CTA, split-K) to minimise
+  // waves x per-CTA work on the resident-CTA slots of 148 SMs (all CTAs do equal work).
+  const int n_sm = nat::device_sm_count();
+  double best = 1e300;
+  const int r_opts[2] = {4, 2};
+  for (int ri = 0; ri < (pl.fp64 ? 1 : 2); ++ri) {
+    const int R = pl.fp64 ? 2 : r_opts[ri];
+    const size_t smem = pl.fp64 ? 2 * (size_t)kTile64 * 12 * sizeof(double)
+                                : 2 * (size_t)kTile * pl.NF * sizeof(float) + (size_t)R * pl.MB * kThreads * 16;
+    const int occ = occupancy(pl.fp64, R, pl.MB, smem);
+    const int64_t tgt = (n_lis + (int64_t)R * kThreads - 1) / ((int64_t)R * kThreads);
+    const int64_t base = tgt * pl.n_mchunk;
+    const int tile = pl.fp64 ? kTile64 : kTile;
+    // per-SM pair throughput at the MUFU roofline (~1.0e10 pairs/s per SM, fp32)
+    const double sm_rate = pl.fp64 ? 1.2e9 : 1.0e10;
+    for (int c = 1; c <= pl.n_tiles; ++c) {
+      const int64_t ns = (pl.n_tiles + c - 1) / c;
+      if (c > 1 && (pl.n_tiles + c - 2) / (c - 1) == ns) continue;  // same split count, more work
+      // all CTAs do equal work: time ~ work on the busiest SM; an SM needs >= ~24 resident
+      // warps (3 CTAs of 8) to saturate its pipes
+      const int64_t cpsm = (base * ns + n_sm - 1) / n_sm;
+      const double eff = std::min(1.0, (double)std::min<int64_t>(cpsm, occ) * (kThreads / 32) / 24.0);
+      const double t_comp = (double)cpsm * c * tile * R * kThreads * pl.MB / sm_rate / eff * (R == 2 ? 1.1 : 1.0);
+      const double t_part = ns > 1 ? (double)ns * n_modes * n_lis * 32.0 / 6.0e12 : 0.0;
+      const double cost = t_comp + t_part + 2e-6 * (ns > 1);
+      if (cost < best) {
+        best = cost;
+        pl.R = R;
+        pl.tgt_tiles = tgt;
+        pl.chunk_tiles = c;
+        pl.smem = smem;
+      }
+    }
+  }
   pl.n_split = (pl.n_tiles + pl.chunk_tiles - 1) / pl.chunk_tiles;
   pl.rec_elems = (size_t)pl.n_mchunk * pl.n_src_pad * pl.NF;
-  if (pl.fp64)
-    pl.smem = 2 * (size_t)kTile64 * 12 * sizeof(double);
-  else
-    pl.smem = 2 * (size_t)kTile * pl.NF * sizeof(float) + (size_t)pl.R * pl.MB * kThreads * 16;
   return pl;
 }
 
@@ -653,14 +674,19 @@ cudaError_t launch_f32(const Plan& pl, const RadParams& prm, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+template <int R, int SELF>
+cudaError_t launch_f32_r(const Plan& pl, const RadParams& prm, cudaStream_t s) {
+  switch (pl.MB) {
+    case 1: return launch_f32<R, 1, SELF>(pl, prm, s);
+    case 2: return launch_f32<R, 2, SELF>(pl, prm, s);
+    case 3: return launch_f32<R, 3, SELF>(pl, prm, s);
+    default: return launch_f32<R, 4, SELF>(pl, prm, s);
+  }
+}
+
 template <int SELF>
 cudaError_t launch_f32_mb(const Plan& pl, const RadParams& prm, cudaStream_t s) {
-  switch (pl.MB) {
-    case 1: return launch_f32<4, 1, SELF>(pl, prm, s);
-    case 2: return launch_f32<4, 2, SELF>(pl, prm, s);
-    case 3: return launch_f32<4, 3, SELF>(pl, prm, s);
-    default: return launch_f32<4, 4, SELF>(pl, prm, s);
-  }
+  return pl.R == 2 ? launch_f32_r<2, SELF>(pl, prm, s) : launch_f32_r<4, SELF>(pl, prm, s);
 }
 
 }  // namespace
@@ -675,6 +701,13 @@ size_t radiate_ws_bytes(nat_prec prec, int64_t n_src, int n_modes, int64_t n_lis
   void* rec;
   double2* part;
   return plan_ws(pl, nm, n_lis, c, &rec, &part);
+}
+
+size_t radiate_ws_bytes_upto(nat_prec prec, int64_t n_src, int max_modes, int64_t n_lis) {
+  size_t b = 0;
+  for (int m = 1; m <= (max_modes < kMaxModes ? max_modes : kMaxModes); ++m)
+    b = std::max(b, radiate_ws_bytes(prec, n_src, m, n_lis));
+  return b;
 }
 
 nat_status radiate_internal(const RadInput& in, nat_prec prec, const double* k, int64_t n_lis,

@@ -19,6 +19,8 @@ struct RadInput {
 };
 
 size_t radiate_ws_bytes(nat_prec prec, int64_t n_src, int n_modes, int64_t n_lis);
+// Largest workspace over 1..max_modes wavenumbers (callers that shrink the mode set).
+size_t radiate_ws_bytes_upto(nat_prec prec, int64_t n_src, int max_modes, int64_t n_lis);
 // out[m][l] (c128 [n_modes][n_lis]) = sum_s w_s [p_ms dG_m/dn_y - g_ms G_m](x_l, y_s);
 // self = true excludes the pair with identical coordinates (targets == sources).
 nat_status radiate_internal(const RadInput& in, nat_prec prec, const double* k, int64_t n_lis,
