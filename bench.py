@@ -258,41 +258,40 @@ def pairs_of(c):
 # ----------------------------------------------------------------------------------
 # oracle timing (cpu_baseline and --impl reference)
 # ----------------------------------------------------------------------------------
-def oracle_sample(host, seconds_hint=None):
-    """Times the fp64 oracle, as it stands, on a bounded sample of the same workload:
-    4 full rows of the C2 dense assembly at ka = 8 (far + near + self rules), radiation of
-    the BEM sources to 64 listeners, and 8 rows of the BEM-MC operator + RHS
-    (M = 10,000).  Returns (pair-evals, seconds, description)."""
-    from oracle import bem, geometry, mc, radiate
+def oracle_sample(host, scale=1):
+    """Times the fp64 oracle, as it stands, on a bounded sample of the same workload
+    (scale 1: 4 full rows of the C2 dense assembly at ka = 8 with far + near + self rules,
+    radiation of the 61,440 BEM sources to 64 listeners, 8 rows of the BEM-MC operator and
+    RHS at M = 10,000; every count is multiplied by ``scale``).
+    Returns (pair-evals, seconds, description)."""
+    from oracle import bem, geometry, kernel, listeners, mc, nearlist, radiate
     m = host["mesh"]
     t0 = time.perf_counter()
     geo = geometry.mesh_prepare(m.v, m.t)
-    rows = np.array([0, 5000, 10000, 15000])
+    rows = np.linspace(0, m.n_tri - 1, 4 * scale).astype(int)
     A, b = bem.assemble(m.v, m.t, geo, 8.0, host["g"], rows=rows)
-    from oracle import nearlist
     rp, col, cls = nearlist.near_list(m.t, geo["centroid"], geo["diam"], rows=rows)
     n_pairs = len(rows) * m.n_tri * 3 + int((cls == 1).sum()) * 448 + int((cls == 2).sum()) * 28 + len(rows) * 48
     x = np.ones(m.n_tri, dtype=complex)
     src = radiate.bem_sources(m.v, m.t, geo, x[None], host["g"])
-    from oracle import listeners
-    L = listeners.shell_grid(np.zeros(3), 1.0, *GRID)[:: (GRID[0] * GRID[1] * GRID[2]) // 64][:64]
+    nl = 64 * scale
+    L = listeners.shell_grid(np.zeros(3), 1.0, *GRID)[:: (GRID[0] * GRID[1] * GRID[2]) // nl][:nl]
     radiate.radiate(src, [8.0], L)
-    n_pairs += 64 * src[0].shape[0]
+    n_pairs += nl * src[0].shape[0]
     y, n, tri = mc.sample_uniform(m.v, m.t, geo, M_MC, 20250606, 0)
     eps = mc.default_eps(geo["total_area"], M_MC)
     w = mc.weight(geo["total_area"], M_MC, eps)
-    from oracle import kernel
     g = host["g"][0][tri]
     p = np.ones(M_MC, dtype=complex)
-    for i in range(8):
+    for i in range(8 * scale):
         j = np.arange(M_MC) != i
         _ = 0.5 * p[i] - w * np.sum(kernel.green_dn_y(y[i], y[j], n[j], 8.0) * p[j])
         _ = -w * np.sum(kernel.green(y[i], y[j], 8.0) * g[j]) - 0.5 * eps * g[i]
         n_pairs += 2 * (M_MC - 1)
     dt = time.perf_counter() - t0
-    desc = ("fp64 NumPy oracle on a bounded sample of the C2 step: 4 full rows of the dense "
-            "assembly at ka=8 (far+near+self rules), radiation of 61,440 BEM sources to 64 "
-            "listeners, 8 rows of the BEM-MC operator and RHS (M=10,000); pair-evals/s")
+    desc = (f"fp64 NumPy oracle on a bounded sample of the C2 step: {len(rows)} full rows of the dense "
+            f"assembly at ka=8 (far+near+self rules), radiation of 61,440 BEM sources to {nl} "
+            f"listeners, {8 * scale} rows of the BEM-MC operator and RHS (M=10,000); pair-evals/s")
     return n_pairs, dt, desc
 
 
@@ -495,7 +494,7 @@ def main():
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        p, t, desc = oracle_sample(host)
+        p, t, desc = oracle_sample(host, scale=8)   # ~10-20 s of host work
         cpu = {"value": p / t / 1e9, "unit": UNIT, "cores": oracle_cores(), "kind": "oracle", "sample": desc,
                "seconds": t}
     K = args.steps

@@ -398,15 +398,23 @@ class Comm:
         _check(lib().nat_comm_unique_id(buf))
         return bytes(buf)
 
+    @staticmethod
+    def broadcast_unique_id(make_id=None) -> bytes:
+        """Rank 0's 128-byte NCCL unique id, broadcast with torch.distributed (works on
+        nccl and gloo process groups)."""
+        import torch.distributed as dist
+        dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+        t = torch.zeros(128, dtype=torch.uint8, device=dev)
+        if dist.get_rank() == 0:
+            uid = (make_id or Comm.unique_id)()
+            t.copy_(torch.frombuffer(bytearray(uid), dtype=torch.uint8))
+        dist.broadcast(t, 0)
+        return bytes(t.cpu().numpy().tobytes())
+
     @classmethod
     def from_torch_distributed(cls):
         import torch.distributed as dist
-        rank, world = dist.get_rank(), dist.get_world_size()
-        t = torch.zeros(128, dtype=torch.uint8, device="cuda")
-        if rank == 0:
-            t.copy_(torch.frombuffer(bytearray(cls.unique_id()), dtype=torch.uint8))
-        dist.broadcast(t, 0)
-        return cls(rank, world, bytes(t.cpu().numpy().tobytes()))
+        return cls(dist.get_rank(), dist.get_world_size(), cls.broadcast_unique_id())
 
     def close(self):
         if self.handle:
