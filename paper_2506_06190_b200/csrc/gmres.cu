@@ -36,12 +36,55 @@ __device__ __forceinline__ double2 block_reduce(double2 v, double2* sm) {
   return s;
 }
 
-// part[s][k][c] = sum_{i in chunk c} conj(V_k[s][i]) w[s][i]
+// Fixed-order sum of the nvec x nchunk partials of system s into h / h2:
+// mode 0: h = h2 = sum;  mode 1: h2 = sum, h += sum;  mode 2: h[s][slot] = (sqrt(Re sum), 0)
+__device__ void finish_sums(const double2* __restrict__ part, int s, int nvec, int nchunk, int mp1, int mp2,
+                            int mode, int slot, double2* __restrict__ h, double2* __restrict__ h2) {
+  for (int k = threadIdx.x; k < nvec; k += blockDim.x) {
+    double2 t = make_double2(0.0, 0.0);
+    for (int c = 0; c < nchunk; ++c) {
+      const double2 v = __ldcg(&part[((size_t)s * mp1 + k) * nchunk + c]);
+      t.x += v.x;
+      t.y += v.y;
+    }
+    if (mode == 0) {
+      h[(size_t)s * mp2 + k] = t;
+      h2[(size_t)s * mp2 + k] = t;
+    } else if (mode == 1) {
+      h2[(size_t)s * mp2 + k] = t;
+      const double2 o = h[(size_t)s * mp2 + k];
+      h[(size_t)s * mp2 + k] = make_double2(o.x + t.x, o.y + t.y);
+    } else {
+      h[(size_t)s * mp2 + slot] = make_double2(sqrt(t.x), 0.0);
+    }
+  }
+}
+
+// True for exactly one block of system s: the last one to finish (its partials are then
+// all visible).  The counter is reset for the next launch.
+__device__ bool last_block(unsigned* cnt, unsigned total, bool* flag) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned prev = atomicAdd(cnt, 1u);
+    *flag = (prev == total - 1);
+    if (*flag) *cnt = 0u;
+  }
+  __syncthreads();
+  if (*flag) __threadfence();
+  return *flag;
+}
+
+// part[s][k][c] = sum_{i in chunk c} conj(V_k[s][i]) w[s][i]; the last block of each
+// system reduces the partials (fixed order) into h / h2 (finish_sums).
 __global__ void __launch_bounds__(kT) dots_kernel(const double2* __restrict__ V, size_t vstride_k,
                                                  int64_t ldv, const double2* __restrict__ w, int64_t n,
                                                  int nvec, int nchunk, int mp1, uint64_t active,
-                                                 double2* __restrict__ part) {
+                                                 double2* __restrict__ part, int mp2, int mode, int slot,
+                                                 double2* __restrict__ h, double2* __restrict__ h2,
+                                                 unsigned* __restrict__ cnt) {
   __shared__ double2 sm[kT / 32];
+  __shared__ bool flag;
   const int c = blockIdx.x, k = blockIdx.y, s = blockIdx.z;
   if (!((active >> s) & 1ull)) return;
   const double2* v = V + k * vstride_k + (size_t)s * ldv;
@@ -55,51 +98,43 @@ __global__ void __launch_bounds__(kT) dots_kernel(const double2* __restrict__ V,
   }
   double2 r = block_reduce(acc, sm);
   if (threadIdx.x == 0) part[((size_t)s * mp1 + k) * nchunk + c] = r;
+  if (last_block(&cnt[s], (unsigned)(nchunk * nvec), &flag))
+    finish_sums(part, s, nvec, nchunk, mp1, mp2, mode, slot, h, h2);
 }
 
-// mode 0: h = h2 = sum;  mode 1: h2 = sum, h += sum;  mode 2: h[s][slot] = (sqrt(Re sum), 0)
-__global__ void sum_parts_kernel(const double2* __restrict__ part, int nvec, int nchunk, int mp1, int mp2,
-                                 int mode, int slot, uint64_t active, double2* __restrict__ h,
-                                 double2* __restrict__ h2) {
-  const int s = blockIdx.x;
-  if (!((active >> s) & 1ull)) return;
-  for (int k = threadIdx.x; k < nvec; k += blockDim.x) {
-    double2 t = make_double2(0.0, 0.0);
-    for (int c = 0; c < nchunk; ++c) {
-      double2 v = part[((size_t)s * mp1 + k) * nchunk + c];
-      t.x += v.x;
-      t.y += v.y;
-    }
-    if (mode == 0) {
-      h[(size_t)s * mp2 + k] = t;
-      h2[(size_t)s * mp2 + k] = t;
-    } else if (mode == 1) {
-      h2[(size_t)s * mp2 + k] = t;
-      double2 o = h[(size_t)s * mp2 + k];
-      h[(size_t)s * mp2 + k] = make_double2(o.x + t.x, o.y + t.y);
-    } else {
-      h[(size_t)s * mp2 + slot] = make_double2(sqrt(t.x), 0.0);
-    }
-  }
-}
-
-// w[s][i] -= sum_{k < nvec} h2[s][k] V_k[s][i]
-__global__ void update_kernel(const double2* __restrict__ V, size_t vstride_k, int64_t ldv, int64_t n,
-                              int nvec, int mp2, uint64_t active, const double2* __restrict__ h2,
-                              double2* __restrict__ w) {
+// w[s][i] -= sum_{k < nvec} h2[s][k] V_k[s][i]; with norm_slot >= 0 also
+// h[s][norm_slot] = ||w[s]|| (block partials, last block sums them in fixed order).
+__global__ void __launch_bounds__(kT) update_kernel(const double2* __restrict__ V, size_t vstride_k, int64_t ldv,
+                                                   int64_t n, int nvec, int mp2, uint64_t active,
+                                                   const double2* __restrict__ h2, double2* __restrict__ w,
+                                                   int norm_slot, double2* __restrict__ h,
+                                                   double2* __restrict__ npart, unsigned* __restrict__ cnt) {
+  __shared__ double2 sm[kT / 32];
+  __shared__ bool flag;
   const int s = blockIdx.y;
   if (!((active >> s) & 1ull)) return;
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  double2 acc = make_double2(0.0, 0.0);
-  for (int k = 0; k < nvec; ++k) {
-    double2 c = h2[(size_t)s * mp2 + k];
-    double2 v = V[k * vstride_k + (size_t)s * ldv + i];
-    acc.x += c.x * v.x - c.y * v.y;
-    acc.y += c.x * v.y + c.y * v.x;
+  double2 o = make_double2(0.0, 0.0);
+  if (i < n) {
+    double2 acc = make_double2(0.0, 0.0);
+    for (int k = 0; k < nvec; ++k) {
+      double2 c = h2[(size_t)s * mp2 + k];
+      double2 v = V[k * vstride_k + (size_t)s * ldv + i];
+      acc.x += c.x * v.x - c.y * v.y;
+      acc.y += c.x * v.y + c.y * v.x;
+    }
+    o = w[(size_t)s * ldv + i];
+    o = make_double2(o.x - acc.x, o.y - acc.y);
+    w[(size_t)s * ldv + i] = o;
   }
-  double2 o = w[(size_t)s * ldv + i];
-  w[(size_t)s * ldv + i] = make_double2(o.x - acc.x, o.y - acc.y);
+  if (norm_slot < 0) return;
+  const double2 r = block_reduce(make_double2(o.x * o.x + o.y * o.y, 0.0), sm);
+  if (threadIdx.x == 0) npart[(size_t)s * gridDim.x + blockIdx.x] = r;
+  if (last_block(&cnt[s], gridDim.x, &flag) && threadIdx.x == 0) {
+    double t = 0.0;
+    for (unsigned b = 0; b < gridDim.x; ++b) t += __ldcg(&npart[(size_t)s * gridDim.x + b]).x;
+    h[(size_t)s * mp2 + norm_slot] = make_double2(sqrt(t), 0.0);
+  }
 }
 
 // dst[s][i] = src[s][i] / h[s][slot]   (slot = norm); zero if the norm is 0
@@ -159,6 +194,8 @@ size_t krylov_workspace(int nsys, int64_t n, int64_t ldv, int max_iter, Carver& 
   t.h = c.take<double2>((size_t)nsys * (m + 2));
   t.h2 = c.take<double2>((size_t)nsys * (m + 2));
   t.y = c.take<double2>((size_t)nsys * m);
+  t.npart = c.take<double2>((size_t)nsys * ((n + kT - 1) / kT));
+  t.cnt = c.take<unsigned>(2 * 64);
   if (w) *w = t;
   return c.bytes();
 }
@@ -189,9 +226,14 @@ nat_status gmres_batched(int nsys, int64_t n, int64_t ldv, const double2* b, dou
   std::vector<SysState> st(nsys);
   std::vector<double2> hbuf((size_t)nsys * mp2);
 
+  NAT_CUDA_TRY(cudaMemsetAsync(ws.cnt, 0, sizeof(unsigned) * 2 * 64, s));
+  // dots of nvec basis vectors (or of w with itself) with w, reduced into h / h2
+  auto dots = [&](const double2* Vb, size_t vs, const double2* w, int nvec, uint64_t act, int mode, int slot) {
+    dots_kernel<<<dim3(nchunk, nvec, nsys), kT, 0, s>>>(Vb, vs, ldv, w, n, nvec, nchunk, mp1, act, ws.part, mp2,
+                                                       mode, slot, ws.h, ws.h2, ws.cnt);
+  };
   // beta = ||b||, V0 = b / beta
-  dots_kernel<<<dim3(nchunk, 1, nsys), kT, 0, s>>>(b, 0, ldv, b, n, 1, nchunk, mp1, all, ws.part);
-  sum_parts_kernel<<<nsys, 32, 0, s>>>(ws.part, 1, nchunk, mp1, mp2, 2, 0, all, ws.h, ws.h2);
+  dots(b, 0, b, 1, all, 2, 0);
   NAT_LAUNCH_CHECK();
   NAT_CUDA_TRY(cudaMemcpyAsync(hbuf.data(), ws.h, sizeof(double2) * nsys * mp2, cudaMemcpyDeviceToHost, s));
   NAT_CUDA_TRY(cudaStreamSynchronize(s));
@@ -220,14 +262,11 @@ nat_status gmres_batched(int nsys, int64_t n, int64_t ldv, const double2* b, dou
     nat_status stt = op(Vj, ws.w, active, s);
     if (stt != NAT_OK) return stt;
     if (t_op_s) NAT_CUDA_TRY(cudaEventRecord(ev[1], s));
-    for (int pass = 0; pass < 2; ++pass) {  // CGS2
-      dots_kernel<<<dim3(nchunk, j + 1, nsys), kT, 0, s>>>(ws.V, vstride, ldv, ws.w, n, j + 1, nchunk, mp1,
-                                                          active, ws.part);
-      sum_parts_kernel<<<nsys, 256, 0, s>>>(ws.part, j + 1, nchunk, mp1, mp2, pass, 0, active, ws.h, ws.h2);
-      update_kernel<<<dim3(gx, nsys), kT, 0, s>>>(ws.V, vstride, ldv, n, j + 1, mp2, active, ws.h2, ws.w);
+    for (int pass = 0; pass < 2; ++pass) {  // CGS2; the second update also forms ||w||
+      dots(ws.V, vstride, ws.w, j + 1, active, pass, 0);
+      update_kernel<<<dim3(gx, nsys), kT, 0, s>>>(ws.V, vstride, ldv, n, j + 1, mp2, active, ws.h2, ws.w,
+                                                  pass == 1 ? j + 1 : -1, ws.h, ws.npart, ws.cnt + 64);
     }
-    dots_kernel<<<dim3(nchunk, 1, nsys), kT, 0, s>>>(ws.w, 0, ldv, ws.w, n, 1, nchunk, mp1, active, ws.part);
-    sum_parts_kernel<<<nsys, 32, 0, s>>>(ws.part, 1, nchunk, mp1, mp2, 2, j + 1, active, ws.h, ws.h2);
     scale_kernel<<<dim3(gx, nsys), kT, 0, s>>>(ws.w, ldv, n, mp2, j + 1, active, ws.h,
                                                ws.V + (size_t)(j + 1) * vstride);
     NAT_LAUNCH_CHECK();
@@ -298,8 +337,7 @@ nat_status gmres_batched(int nsys, int64_t n, int64_t ldv, const double2* b, dou
   nat_status stt = op(x, ws.w, all, s);
   if (stt != NAT_OK) return stt;
   sub_kernel<<<dim3(gx, nsys), kT, 0, s>>>(b, ldv, n, ws.w);
-  dots_kernel<<<dim3(nchunk, 1, nsys), kT, 0, s>>>(ws.w, 0, ldv, ws.w, n, 1, nchunk, mp1, all, ws.part);
-  sum_parts_kernel<<<nsys, 32, 0, s>>>(ws.part, 1, nchunk, mp1, mp2, 2, 0, all, ws.h, ws.h2);
+  dots(ws.w, 0, ws.w, 1, all, 2, 0);
   NAT_LAUNCH_CHECK();
   NAT_CUDA_TRY(cudaMemcpyAsync(hbuf.data(), ws.h, sizeof(double2) * nsys * mp2, cudaMemcpyDeviceToHost, s));
   NAT_CUDA_TRY(cudaStreamSynchronize(s));

@@ -17,6 +17,8 @@ struct KrylovWs {
   double2* h;     // [nsys][m+2]
   double2* h2;    // [nsys][m+2]
   double2* y;     // [nsys][m]
+  double2* npart; // [nsys][ceil(n/256)] norm partials
+  unsigned* cnt;  // [2][64] last-block counters (zeroed at the start of every solve)
 };
 
 constexpr int kKrylovChunk = 4096;

@@ -637,10 +637,10 @@ Plan make_plan(nat_prec prec, int64_t n_src, int n_modes, int64_t n_lis) {
     for (int c = 1; c <= pl.n_tiles; ++c) {
       const int64_t ns = (pl.n_tiles + c - 1) / c;
       if (c > 1 && (pl.n_tiles + c - 2) / (c - 1) == ns) continue;  // same split count, more work
-      // all CTAs do equal work: time ~ work on the busiest SM; an SM needs >= ~24 resident
-      // warps (3 CTAs of 8) to saturate its pipes
+      // all CTAs do equal work: time ~ work on the busiest SM; measured (ncu, r01): the
+      // MUFU/FMA pipes need ~40 resident warps per SM (5 CTAs of 8) to saturate
       const int64_t cpsm = (base * ns + n_sm - 1) / n_sm;
-      const double eff = std::min(1.0, (double)std::min<int64_t>(cpsm, occ) * (kThreads / 32) / 24.0);
+      const double eff = std::min(1.0, (double)std::min<int64_t>(cpsm, occ) * (kThreads / 32) / 40.0);
       const double t_comp = (double)cpsm * c * tile * R * kThreads * pl.MB / sm_rate / eff * (R == 2 ? 1.1 : 1.0);
       const double t_part = ns > 1 ? (double)ns * n_modes * n_lis * 32.0 / 6.0e12 : 0.0;
       const double cost = t_comp + t_part + 2e-6 * (ns > 1);
