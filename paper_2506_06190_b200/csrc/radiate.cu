@@ -13,6 +13,9 @@
 //    added into fp64 accumulators kept in shared memory;
 //  * split-K over source chunks when the target grid is too small for 148 SMs, with a
 //    fixed-order fp64 reduction (deterministic, no atomics).
+#include <cstdio>
+#include <cstdlib>
+
 #include "async_copy.cuh"
 #include "nat_internal.cuh"
 #include "f32x2.cuh"
@@ -144,8 +147,11 @@ struct Rec2 {
   static constexpr int NF = 12 + 12 * MB;  // duplicated floats per source record
 };
 
-template <int R, int MB, int SELF>
-__global__ void __launch_bounds__(kThreads) radiate_f32x2_kernel(RadParams prm) {
+// SELF = 1: targets coincide with the sources (MC operators): pairs with fp32 r^2 <= self_r2
+// (the self pair, d = 0 exactly, and the close pairs evaluated in fp64 by the caller) get
+// 1/r = 0, i.e. contribute exactly 0.  NT = threads per CTA (256, or 128 for fine grids).
+template <int R, int MB, int SELF, int NT>
+__global__ void __launch_bounds__(NT) radiate_f32x2_kernel(RadParams prm) {
   static_assert(R % 2 == 0, "targets are processed in pairs");
   constexpr int RP = R / 2;
   constexpr int NF = Rec2<MB>::NF;
@@ -156,7 +162,7 @@ __global__ void __launch_bounds__(kThreads) radiate_f32x2_kernel(RadParams prm) 
   __shared__ __align__(8) uint64_t bars[2];
 
   const int tid = threadIdx.x;
-  const int64_t tbase = (int64_t)blockIdx.x * (R * kThreads);
+  const int64_t tbase = (int64_t)blockIdx.x * (R * NT);
   const int split = blockIdx.y;
   const int mch = blockIdx.z;
 
@@ -166,7 +172,7 @@ __global__ void __launch_bounds__(kThreads) radiate_f32x2_kernel(RadParams prm) 
     float c[2][3];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      int64_t l = tbase + (2 * p + h) * kThreads + tid;
+      int64_t l = tbase + (2 * p + h) * NT + tid;
       if (l >= prm.n_lis) l = prm.n_lis - 1;
       c[h][0] = (float)(prm.lis[l] - prm.cx);
       c[h][1] = (float)(prm.lis[prm.n_lis + l] - prm.cy);
@@ -184,7 +190,7 @@ __global__ void __launch_bounds__(kThreads) radiate_f32x2_kernel(RadParams prm) 
   }
   const f2r minus1 = f2pack(-1.f, -1.f);
 #pragma unroll
-  for (int q = 0; q < R * MB; ++q) dacc[q * kThreads + tid] = make_double2(0.0, 0.0);
+  for (int q = 0; q < R * MB; ++q) dacc[q * NT + tid] = make_double2(0.0, 0.0);
 
   const int t0 = split * prm.chunk_tiles;
   const int t1 = min(t0 + prm.chunk_tiles, prm.n_tiles);
@@ -214,7 +220,10 @@ __global__ void __launch_bounds__(kThreads) radiate_f32x2_kernel(RadParams prm) 
 #pragma unroll
       for (int m = 0; m < MB; ++m) ar[p][m] = ai[p][m] = 0ull;
 
-#pragma unroll 2
+    // short bodies (one target pair, one wavenumber) need a deeper unroll so the
+    // shared-memory loads of later sources overlap the arithmetic (ncu r01: LDS-wait)
+    constexpr int kUnroll = (RP * MB <= 1) ? 4 : 2;
+#pragma unroll kUnroll
     for (int s = 0; s < kTile; ++s) {
       f2r f[NF / 2];
 #pragma unroll
@@ -257,13 +266,13 @@ __global__ void __launch_bounds__(kThreads) radiate_f32x2_kernel(RadParams prm) 
 #pragma unroll
       for (int m = 0; m < MB; ++m) {
         const int q0 = (2 * p) * MB + m, q1 = (2 * p + 1) * MB + m;
-        double2 d0 = dacc[q0 * kThreads + tid], d1 = dacc[q1 * kThreads + tid];
+        double2 d0 = dacc[q0 * NT + tid], d1 = dacc[q1 * NT + tid];
         d0.x += (double)f2lo(ar[p][m]);
         d0.y += (double)f2lo(ai[p][m]);
         d1.x += (double)f2hi(ar[p][m]);
         d1.y += (double)f2hi(ai[p][m]);
-        dacc[q0 * kThreads + tid] = d0;
-        dacc[q1 * kThreads + tid] = d1;
+        dacc[q0 * NT + tid] = d0;
+        dacc[q1 * NT + tid] = d1;
       }
     __syncthreads();  // every thread is done with buf[st]
     if (tid == 0 && t0 + it + 2 < t1) {
@@ -275,138 +284,13 @@ __global__ void __launch_bounds__(kThreads) radiate_f32x2_kernel(RadParams prm) 
 
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    int64_t l = tbase + r * kThreads + tid;
+    int64_t l = tbase + r * NT + tid;
     if (l >= prm.n_lis) continue;
 #pragma unroll
     for (int m = 0; m < MB; ++m) {
       int mode = mch * MB + m;
       if (mode < prm.n_modes)
-        prm.out[((size_t)split * prm.n_modes + mode) * prm.n_lis + l] = dacc[(r * MB + m) * kThreads + tid];
-    }
-  }
-}
-
-// SELF = 1: targets coincide with the sources (MC operators): the self pair has d = 0
-// exactly (same fp64 value, same cast) and is excluded by setting 1/r = 0, which makes
-// its contribution exactly 0 (the disk terms are added by the caller).
-template <int R, int MB, int SELF>
-__global__ void __launch_bounds__(kThreads) radiate_f32_kernel(RadParams prm) {
-  constexpr int NF = Rec<MB>::NF;
-  constexpr int kTileFloats = kTile * NF;
-  extern __shared__ __align__(128) unsigned char smem[];
-  float* buf = reinterpret_cast<float*>(smem);
-  double2* dacc = reinterpret_cast<double2*>(smem + 2 * kTileFloats * sizeof(float));
-  __shared__ __align__(8) uint64_t bars[2];
-
-  const int tid = threadIdx.x;
-  const int64_t tbase = (int64_t)blockIdx.x * (R * kThreads);
-  const int split = blockIdx.y;
-  const int mch = blockIdx.z;
-
-  float tx[R], ty[R], tz[R];
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    int64_t l = tbase + r * kThreads + tid;
-    if (l >= prm.n_lis) l = prm.n_lis - 1;
-    tx[r] = (float)(prm.lis[l] - prm.cx);
-    ty[r] = (float)(prm.lis[prm.n_lis + l] - prm.cy);
-    tz[r] = (float)(prm.lis[2 * prm.n_lis + l] - prm.cz);
-  }
-  float kk[MB];
-#pragma unroll
-  for (int m = 0; m < MB; ++m) kk[m] = prm.k.f[mch * MB + m];
-#pragma unroll
-  for (int q = 0; q < R * MB; ++q) dacc[q * kThreads + tid] = make_double2(0.0, 0.0);
-
-  const int t0 = split * prm.chunk_tiles;
-  const int t1 = min(t0 + prm.chunk_tiles, prm.n_tiles);
-  const float* src = static_cast<const float*>(prm.rec) + (size_t)mch * prm.n_src_pad * NF;
-  constexpr uint32_t kBytes = kTileFloats * sizeof(float);
-
-  if (tid == 0) {
-    nat::mbar_init(&bars[0], 1);
-    nat::mbar_init(&bars[1], 1);
-    nat::fence_mbar_init();
-  }
-  __syncthreads();
-  if (tid == 0) {
-    for (int st = 0; st < 2 && t0 + st < t1; ++st) {
-      nat::mbar_arrive_expect_tx(&bars[st], kBytes);
-      nat::bulk_g2s(buf + st * kTileFloats, src + (size_t)(t0 + st) * kTileFloats, kBytes, &bars[st]);
-    }
-  }
-
-  for (int it = 0; t0 + it < t1; ++it) {
-    const int st = it & 1;
-    nat::mbar_wait(&bars[st], (it >> 1) & 1);
-    const float4* b4 = reinterpret_cast<const float4*>(buf + st * kTileFloats);
-    float ar[R][MB], ai[R][MB];
-#pragma unroll
-    for (int r = 0; r < R; ++r)
-#pragma unroll
-      for (int m = 0; m < MB; ++m) ar[r][m] = ai[r][m] = 0.f;
-
-#pragma unroll 2
-    for (int s = 0; s < kTile; ++s) {
-      float f[NF];
-#pragma unroll
-      for (int q = 0; q < NF / 4; ++q) {
-        float4 v = b4[s * (NF / 4) + q];
-        f[4 * q] = v.x;
-        f[4 * q + 1] = v.y;
-        f[4 * q + 2] = v.z;
-        f[4 * q + 3] = v.w;
-      }
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const float dx = f[0] - tx[r];
-        const float dy = f[1] - ty[r];
-        const float dz = f[2] - tz[r];
-        const float r2 = nat::pair_r2_f32(dx, dy, dz);
-        const float dn = fmaf(dz, f[5], fmaf(dy, f[4], dx * f[3]));
-        const float rho = SELF ? (r2 > prm.self_r2 ? rsqrt_approx(r2) : 0.f) : rsqrt_approx(r2);
-        const float qq = dn * (rho * rho);
-        const float rr = r2 * rho;
-#pragma unroll
-        for (int m = 0; m < MB; ++m) {
-          float sn, cs;
-          __sincosf(rr * kk[m], &sn, &cs);
-          const float* c = f + 6 + 6 * m;
-          const float cr = fmaf(qq, fmaf(rho, c[0], c[1]), rho * c[4]);
-          const float ci = fmaf(qq, fmaf(rho, c[3], c[2]), rho * c[5]);
-          ar[r][m] = fmaf(cs, cr, fmaf(-sn, ci, ar[r][m]));
-          ai[r][m] = fmaf(sn, cr, fmaf(cs, ci, ai[r][m]));
-        }
-      }
-    }
-#pragma unroll
-    for (int r = 0; r < R; ++r)
-#pragma unroll
-      for (int m = 0; m < MB; ++m) {
-        double2 d = dacc[(r * MB + m) * kThreads + tid];
-        d.x += (double)ar[r][m];
-        d.y += (double)ai[r][m];
-        dacc[(r * MB + m) * kThreads + tid] = d;
-      }
-    __syncthreads();  // every thread is done with buf[st]
-    if (tid == 0 && t0 + it + 2 < t1) {
-      nat::fence_proxy_async_smem();
-      nat::mbar_arrive_expect_tx(&bars[st], kBytes);
-      nat::bulk_g2s(buf + st * kTileFloats, src + (size_t)(t0 + it + 2) * kTileFloats, kBytes,
-                    &bars[st]);
-    }
-  }
-
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    int64_t l = tbase + r * kThreads + tid;
-    if (l >= prm.n_lis) continue;
-#pragma unroll
-    for (int m = 0; m < MB; ++m) {
-      int mode = mch * MB + m;
-      if (mode < prm.n_modes)
-        prm.out[((size_t)split * prm.n_modes + mode) * prm.n_lis + l] =
-            dacc[(r * MB + m) * kThreads + tid];
+        prm.out[((size_t)split * prm.n_modes + mode) * prm.n_lis + l] = dacc[(r * MB + m) * NT + tid];
     }
   }
 }
@@ -558,6 +442,7 @@ struct Plan {
   int64_t n_src_pad, tgt_tiles;
   size_t rec_elems, smem;
   bool fp64;
+  int NT;  // threads per CTA of the fp32 kernel
 };
 
 int pick_mb(int n_modes) {
@@ -568,22 +453,28 @@ int pick_mb(int n_modes) {
   return 1;
 }
 
-template <int R, int MB>
+template <int R, int MB, int NT>
 int occ_of(size_t smem) {
   int occ = 0;
-  auto k = radiate_f32x2_kernel<R, MB, 0>;
+  auto k = radiate_f32x2_kernel<R, MB, 0, NT>;
   if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kThreads, smem) != cudaSuccess) {
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, NT, smem) != cudaSuccess) {
     cudaGetLastError();
     return 2;
   }
   return occ > 0 ? occ : 1;
 }
 
+template <int R, int NT>
+int occ_mb(int MB, size_t smem) {
+  return MB == 1 ? occ_of<R, 1, NT>(smem) : MB == 2 ? occ_of<R, 2, NT>(smem)
+       : MB == 3 ? occ_of<R, 3, NT>(smem) : occ_of<R, 4, NT>(smem);
+}
+
 // Resident CTAs per SM of the radiation kernel instance (cached per configuration).
-int occupancy(bool fp64, int R, int MB, size_t smem) {
-  static int cache[2][5][5];  // [fp64][R][MB], 0 = unknown
-  int& c = cache[fp64 ? 1 : 0][R][MB];
+int occupancy(bool fp64, int R, int MB, int NT, size_t smem) {
+  static int cache[2][5][5][2];  // [fp64][R][MB][NT == 128], 0 = unknown
+  int& c = cache[fp64 ? 1 : 0][R][MB][NT == 128 ? 1 : 0];
   if (c) return c;
   if (fp64) {
     int occ = 0;
@@ -594,10 +485,10 @@ int occupancy(bool fp64, int R, int MB, size_t smem) {
       occ = 2;
     }
     c = occ > 0 ? occ : 1;
-  } else if (R == 2) {
-    c = MB == 1 ? occ_of<2, 1>(smem) : MB == 2 ? occ_of<2, 2>(smem) : MB == 3 ? occ_of<2, 3>(smem) : occ_of<2, 4>(smem);
+  } else if (NT == 128) {
+    c = R == 2 ? occ_mb<2, 128>(MB, smem) : occ_mb<4, 128>(MB, smem);
   } else {
-    c = MB == 1 ? occ_of<4, 1>(smem) : MB == 2 ? occ_of<4, 2>(smem) : MB == 3 ? occ_of<4, 3>(smem) : occ_of<4, 4>(smem);
+    c = R == 2 ? occ_mb<2, 256>(MB, smem) : occ_mb<4, 256>(MB, smem);
   }
   return c;
 }
@@ -616,41 +507,63 @@ Plan make_plan(nat_prec prec, int64_t n_src, int n_modes, int64_t n_lis) {
     pl.NF = 12 + 12 * pl.MB;  // duplicated records of the FP32x2 kernel
     pl.tile = kTile;
   }
+  pl.NT = kThreads;
   pl.n_mchunk = (n_modes + pl.MB - 1) / pl.MB;
   pl.n_tiles = (int)((n_src + pl.tile - 1) / pl.tile);
   pl.n_src_pad = (int64_t)pl.n_tiles * pl.tile;
-  // Choose targets/thread R and the source chunk (tiles per CTA, split-K) to minimise
-  // waves x per-CTA work on the resident-CTA slots of 148 SMs (all CTAs do equal work).
+  // Choose the CTA width NT, targets/thread R and the source chunk (tiles per CTA,
+  // split-K) minimising the modelled time of the busiest SM (all CTAs do equal work).
   const int n_sm = nat::device_sm_count();
   double best = 1e300;
-  const int r_opts[2] = {4, 2};
-  for (int ri = 0; ri < (pl.fp64 ? 1 : 2); ++ri) {
-    const int R = pl.fp64 ? 2 : r_opts[ri];
-    const size_t smem = pl.fp64 ? 2 * (size_t)kTile64 * 12 * sizeof(double)
-                                : 2 * (size_t)kTile * pl.NF * sizeof(float) + (size_t)R * pl.MB * kThreads * 16;
-    const int occ = occupancy(pl.fp64, R, pl.MB, smem);
-    const int64_t tgt = (n_lis + (int64_t)R * kThreads - 1) / ((int64_t)R * kThreads);
-    const int64_t base = tgt * pl.n_mchunk;
-    const int tile = pl.fp64 ? kTile64 : kTile;
-    // per-SM pair throughput at the MUFU roofline (~1.0e10 pairs/s per SM, fp32)
-    const double sm_rate = pl.fp64 ? 1.2e9 : 1.0e10;
-    for (int c = 1; c <= pl.n_tiles; ++c) {
-      const int64_t ns = (pl.n_tiles + c - 1) / c;
-      if (c > 1 && (pl.n_tiles + c - 2) / (c - 1) == ns) continue;  // same split count, more work
-      // all CTAs do equal work: time ~ work on the busiest SM; measured (ncu, r01): the
-      // MUFU/FMA pipes need ~40 resident warps per SM (5 CTAs of 8) to saturate
-      const int64_t cpsm = (base * ns + n_sm - 1) / n_sm;
-      const double eff = std::min(1.0, (double)std::min<int64_t>(cpsm, occ) * (kThreads / 32) / 40.0);
-      const double t_comp = (double)cpsm * c * tile * R * kThreads * pl.MB / sm_rate / eff * (R == 2 ? 1.1 : 1.0);
-      const double t_part = ns > 1 ? (double)ns * n_modes * n_lis * 32.0 / 6.0e12 : 0.0;
-      const double cost = t_comp + t_part + 2e-6 * (ns > 1);
-      if (cost < best) {
-        best = cost;
-        pl.R = R;
-        pl.tgt_tiles = tgt;
-        pl.chunk_tiles = c;
-        pl.smem = smem;
+  const int r_opts[2] = {4, 2}, nt_opts[2] = {256, 128};
+  for (int ni = 0; ni < (pl.fp64 ? 1 : 2); ++ni)
+    for (int ri = 0; ri < (pl.fp64 ? 1 : 2); ++ri) {
+      const int R = pl.fp64 ? 2 : r_opts[ri];
+      const int NT = pl.fp64 ? kThreads : nt_opts[ni];
+      const size_t smem = pl.fp64 ? 2 * (size_t)kTile64 * 12 * sizeof(double)
+                                  : 2 * (size_t)kTile * pl.NF * sizeof(float) + (size_t)R * pl.MB * NT * 16;
+      const int occ = occupancy(pl.fp64, R, pl.MB, NT, smem);
+      const int64_t tgt = (n_lis + (int64_t)R * NT - 1) / ((int64_t)R * NT);
+      const int64_t base = tgt * pl.n_mchunk;
+      const int tile = pl.fp64 ? kTile64 : kTile;
+      // per-SM pair throughput at the MUFU roofline (~1.0e10 pairs/s per SM, fp32)
+      const double sm_rate = pl.fp64 ? 1.2e9 : 1.0e10;
+      for (int c = 1; c <= pl.n_tiles; ++c) {
+        const int64_t ns = (pl.n_tiles + c - 1) / c;
+        if (c > 1 && (pl.n_tiles + c - 2) / (c - 1) == ns) continue;  // same split count, more work
+        // the busiest SM runs cpsm CTAs of work W in rounds of `occ` resident CTAs; a round
+        // of r CTAs proceeds at sm_rate * eff(r) (measured, ncu r01: the MUFU/FMA pipes need
+        // ~40 resident warps per SM to saturate)
+        const int64_t cpsm = (base * ns + n_sm - 1) / n_sm;
+        auto eff = [&](int64_t r) { return std::min(1.0, (double)r * (NT / 32) / 40.0); };
+        const double W = (double)c * tile * R * NT * pl.MB;
+        const int64_t full = cpsm / occ, rest = cpsm % occ;
+        double t_comp = (double)full * occ * W / (sm_rate * eff(occ));
+        if (rest) t_comp += (double)rest * W / (sm_rate * eff(rest));
+        // R = 2 doubles the shared-memory loads per pair; a CTA has a fixed prologue/epilogue
+        t_comp *= (R == 2 ? 1.1 : 1.0);
+        const double t_fix = (double)(full + (rest > 0)) * 0.5e-6;  // sweep r01: finest splits win on MC shapes
+        const double t_part = ns > 1 ? (double)ns * n_modes * n_lis * 32.0 / 6.0e12 : 0.0;
+        const double cost = t_comp + t_fix + t_part + 2e-6 * (ns > 1);
+        if (cost < best) {
+          best = cost;
+          pl.R = R;
+          pl.NT = NT;
+          pl.tgt_tiles = tgt;
+          pl.chunk_tiles = c;
+          pl.smem = smem;
+        }
       }
+    }
+  if (const char* ov = std::getenv("NAT_RAD_PLAN")) {  // tuning sweeps only: "R,NT,c"
+    int R = 0, NT = 0, c = 0;
+    if (!pl.fp64 && std::sscanf(ov, "%d,%d,%d", &R, &NT, &c) == 3 && (R == 2 || R == 4) &&
+        (NT == 128 || NT == 256) && c >= 1) {
+      pl.R = R;
+      pl.NT = NT;
+      pl.chunk_tiles = std::min(c, pl.n_tiles);
+      pl.tgt_tiles = (n_lis + (int64_t)R * NT - 1) / ((int64_t)R * NT);
+      pl.smem = 2 * (size_t)kTile * pl.NF * sizeof(float) + (size_t)R * pl.MB * NT * 16;
     }
   }
   pl.n_split = (pl.n_tiles + pl.chunk_tiles - 1) / pl.chunk_tiles;
@@ -664,29 +577,31 @@ size_t plan_ws(const Plan& pl, int n_modes, int64_t n_lis, nat::Carver& c, void*
   return c.bytes();
 }
 
-template <int R, int MB, int SELF>
+template <int R, int MB, int SELF, int NT>
 cudaError_t launch_f32(const Plan& pl, const RadParams& prm, cudaStream_t s) {
-  auto kern = radiate_f32x2_kernel<R, MB, SELF>;
+  auto kern = radiate_f32x2_kernel<R, MB, SELF, NT>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
   if (e != cudaSuccess) return e;
   dim3 grid((unsigned)pl.tgt_tiles, (unsigned)pl.n_split, (unsigned)pl.n_mchunk);
-  kern<<<grid, kThreads, pl.smem, s>>>(prm);
+  kern<<<grid, NT, pl.smem, s>>>(prm);
   return cudaGetLastError();
 }
 
-template <int R, int SELF>
+template <int R, int SELF, int NT>
 cudaError_t launch_f32_r(const Plan& pl, const RadParams& prm, cudaStream_t s) {
   switch (pl.MB) {
-    case 1: return launch_f32<R, 1, SELF>(pl, prm, s);
-    case 2: return launch_f32<R, 2, SELF>(pl, prm, s);
-    case 3: return launch_f32<R, 3, SELF>(pl, prm, s);
-    default: return launch_f32<R, 4, SELF>(pl, prm, s);
+    case 1: return launch_f32<R, 1, SELF, NT>(pl, prm, s);
+    case 2: return launch_f32<R, 2, SELF, NT>(pl, prm, s);
+    case 3: return launch_f32<R, 3, SELF, NT>(pl, prm, s);
+    default: return launch_f32<R, 4, SELF, NT>(pl, prm, s);
   }
 }
 
 template <int SELF>
 cudaError_t launch_f32_mb(const Plan& pl, const RadParams& prm, cudaStream_t s) {
-  return pl.R == 2 ? launch_f32_r<2, SELF>(pl, prm, s) : launch_f32_r<4, SELF>(pl, prm, s);
+  if (pl.NT == 128)
+    return pl.R == 2 ? launch_f32_r<2, SELF, 128>(pl, prm, s) : launch_f32_r<4, SELF, 128>(pl, prm, s);
+  return pl.R == 2 ? launch_f32_r<2, SELF, 256>(pl, prm, s) : launch_f32_r<4, SELF, 256>(pl, prm, s);
 }
 
 }  // namespace
