@@ -1,0 +1,92 @@
+"""C4 and C5 in their launch configurations (BASELINE.json configs[3], configs[4]):
+sampled rows / listeners against the oracle, since the full-size oracle is out of reach."""
+import numpy as np
+import pytest
+import torch
+
+import nat_inputs as I
+from gpu_util import rel_l2, requires_cuda, soa_to_aos, to_np
+from oracle import bem, geometry, kernel, mc, radiate
+
+pytestmark = [pytest.mark.gpu, requires_cuda]
+
+
+def _nat():
+    from paper_2506_06190_b200 import nat
+    return nat
+
+
+@pytest.mark.parametrize("gi", [0, 63])
+def test_c4_scene_mc_and_64_wavenumber_radiation(gi):
+    """One C4 geometry (bowl over slab, ~19.6k tri): BEM-MC with M = 2048 and its 64
+    wavenumbers batched in one solve, then radiation of all 64 fused to the 64^3 grid."""
+    nat = _nat()
+    m, g8, D = I.c4_geometry(gi)
+    ks = I.c4_wavenumbers(D)
+    g_tri = np.tile(g8, (8, 1))                      # index 8*material + mode
+    geo = geometry.mesh_prepare(m.v, m.t)
+    mesh = nat.Mesh.from_numpy(m.v, m.t)
+    gg = nat.nat_mesh_prepare(mesh)
+    M = 2048
+    smp, stri, p, infos = nat.nat_mc_surface_pressure(mesh, gg, ks, torch.from_numpy(g_tri).cuda(), M,
+                                                      seed=I.SEED, stream_id=gi)
+    assert all(i["converged"] == 1 for i in infos)
+    y, n, tri = mc.sample_uniform(m.v, m.t, geo, M, I.SEED, gi)
+    assert np.array_equal(to_np(stri), tri)
+    P = to_np(p)
+    eps = mc.default_eps(geo["total_area"], M)
+    w = mc.weight(geo["total_area"], M, eps)
+    rows = np.random.default_rng(gi).choice(M, 12, replace=False)
+    for s in (0, 27, 63):
+        g = g_tri[s][tri]
+        res, nb = [], []
+        for i in rows:
+            j = np.arange(M) != i
+            Ai = -w * kernel.green_dn_y(y[i], y[j], n[j], ks[s])
+            bi = -w * np.sum(kernel.green(y[i], y[j], ks[s]) * g[j]) - 0.5 * eps * g[i]
+            res.append(0.5 * P[s, i] + Ai @ P[s, j] - bi)
+            nb.append(bi)
+        assert np.linalg.norm(res) / np.linalg.norm(nb) <= 1e-4
+    # radiation: 64 wavenumbers fused, 64^3 listeners around the scene centre
+    gs = nat.nat_mc_gather_neumann(torch.from_numpy(g_tri).cuda(), stri)
+    src = nat.nat_mc_sources(smp, gg.total_area, p, gs, center=gg.center)
+    lis = nat.nat_listener_grid(gg.center, gg.bound_radius, 64, 64, 64)
+    out = to_np(nat.nat_radiate_field(src, list(ks), lis, "fp32"))
+    idx = np.random.default_rng(1).choice(lis.shape[1], 48, replace=False)
+    x = soa_to_aos(lis)[idx]
+    ref = radiate.radiate(radiate.mc_sources(y, n, geo["total_area"], P, g_tri[:, tri]), ks, x)
+    for s in (0, 9, 40, 63):
+        assert rel_l2(out[s][idx], ref[s]) <= 1e-4
+
+
+def test_c5_rank_row_block_fp64():
+    """C5 mesh (equiangular cubed sphere, 199,692 tri), fp64: the row block one rank of a
+    multi-GPU solve owns (first 1024 rows), assembled at ka = 8 with the dipole data;
+    sampled rows of A and b against the oracle (1e-10), the block's GEMV against numpy,
+    and fp64 radiation of all 599,076 sources on sampled listeners."""
+    nat = _nat()
+    m = I.cubed_sphere(129)
+    g = I.neumann_rigid_z(m)
+    mesh = nat.Mesh.from_numpy(m.v, m.t)
+    gg = nat.nat_mesh_prepare(mesh)
+    r0, r1 = 0, 1024
+    nl = nat.nat_bem_near_list(mesh, gg, r0, r1)
+    gt = torch.from_numpy(g[None]).cuda()
+    A, b = nat.nat_bem_assemble(mesh, gg, nl, 8.0, gt, prec="fp64")
+    geo = geometry.mesh_prepare(m.v, m.t)
+    rows = np.array([0, 311, 777, 1023])
+    A_ref, b_ref = bem.assemble(m.v, m.t, geo, 8.0, g[None], rows=rows)
+    A_rows = to_np(A[torch.from_numpy(rows).cuda()])[:, : m.n_tri]
+    assert rel_l2(A_rows, A_ref) <= 1e-10
+    assert rel_l2(to_np(b[0])[rows], b_ref[0]) <= 1e-10
+    x = I.random_complex(m.n_tri, 5)
+    y = to_np(nat.nat_bem_matvec(A, torch.from_numpy(x).cuda(), n=m.n_tri))
+    assert rel_l2(y[rows], A_ref @ x) <= 1e-10
+    # fp64 radiation of the full source set (3 points per triangle)
+    pv = I.random_complex(m.n_tri, 6)
+    src = nat.nat_bem_sources(mesh, gg, torch.from_numpy(pv[None]).cuda(), gt)
+    lis = nat.nat_listener_grid((0, 0, 0), 1.0, 8, 8, 4)
+    out = to_np(nat.nat_radiate_field(src, [8.0], lis, "fp64"))[0]
+    idx = np.array([0, 77, 200, 255])
+    ref = radiate.radiate(radiate.bem_sources(m.v, m.t, geo, pv[None], g[None]), [8.0], soa_to_aos(lis)[idx])[0]
+    assert rel_l2(out[idx], ref) <= 1e-10
