@@ -470,15 +470,15 @@ def main():
 
     def alu(name, pairs, t):
         a = pairs / t / 1e9 if t > 0 else 0.0
-        return {"kernel": name, "bound": "alu", "achieved": a, "peak": R_PIPE / 1e9, "unit": "Gpair-evals/s",
+        return {"kernel": name, "traffic_note": "dram read+write bytes per launch, ncu --set full (profiles/traffic.json)", "bound": "alu", "achieved": a, "peak": R_PIPE / 1e9, "unit": "Gpair-evals/s",
                 "frac": a / (R_PIPE / 1e9), "traffic": traffic.get(name),
                 "peak_note": "FP32-pipe roofline: 148 SM x 128 lanes x 1965 MHz / 24 instr per combined "
                              "G+dG pair (= 16 MUFU/SM/clk / 3); derived, DESIGN.md §5",
                 "frac_at_measured_clock": (a / (R_PIPE / 1e9) * MAX_MHZ / clk["sm_mhz"]) if clk["sm_mhz"] else None}
 
     roof = {
-        "radiate": alu("radiate_f32_kernel", totals["rad"], t_rad),
-        "bem_assembly": alu("far_kernel+near_kernel+self_kernel", totals["far"] + totals["near"] + totals["self"], t_asm),
+        "radiate": alu("radiate_f32x2_kernel", totals["rad"], t_rad),
+        "bem_assembly": alu("far_kernel_x2", totals["far"] + totals["near"] + totals["self"], t_asm),
         "mc_solve": alu("radiate_f32_kernel<SELF> (MC operator/RHS)", totals["mc_op"] + totals["mc_rhs"], t_mc),
         "gemv": {"kernel": "gemv_c64_kernel", "bound": "hbm",
                  "achieved": totals["gemv_bytes"] / t_gemv / 1e9 if t_gemv > 0 else 0.0,
