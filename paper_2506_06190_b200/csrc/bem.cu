@@ -447,7 +447,6 @@ struct NearArgs {
   const int64_t* row_ptr;
   const int32_t* col;
   const uint8_t* cls;
-  const int32_t* rowidx;   // [nnz] row of each entry
   const double* vx;
   const int32_t* tri;
   const double* cen;
@@ -456,6 +455,8 @@ struct NearArgs {
   const double4* rule;     // near rule points (parent barycentrics, weight)
   const float4* rule_f;    // the same rule in fp32 (fp32 path)
   int npts;
+  const int2* items;       // compacted (entry, row) list of this launch's class
+  int64_t nitems;
   FarCols<R> cols;         // far rule (to subtract the far contribution from b)
   double cx, cy, cz;
   R k;
@@ -465,14 +466,29 @@ struct NearArgs {
   double2* corr;           // [nnz][n_rhs]
 };
 
-template <typename R, int NQ, int G, int CLS>
+// One G-lane group per near pair of one class (compacted list `items` = (entry, row)):
+// G = 1 for class N (28 points per thread), G = 4 for class S (448 points over 4 lanes).
+// The rule table is staged in shared memory (all groups walk it in the same order).
+constexpr int kMaxNearPts = 7 << 8;  // up to 4 subdivision levels x 7 points (S: 448 at 3)
+
+template <typename R, int NQ, int G>
 __global__ void __launch_bounds__(kThreads) near_kernel(NearArgs<R> a) {
+  extern __shared__ __align__(16) unsigned char near_smem[];
+  float4* s_rf = reinterpret_cast<float4*>(near_smem);
+  double4* s_rd = reinterpret_cast<double4*>(near_smem);
+  for (int q = threadIdx.x; q < a.npts; q += blockDim.x) {
+    if constexpr (sizeof(R) == 4)
+      s_rf[q] = a.rule_f[q];
+    else
+      s_rd[q] = a.rule[q];
+  }
+  __syncthreads();
   const int64_t gid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
   const int lig = threadIdx.x % G;
-  if (gid >= a.nnz) return;
-  const int64_t e = gid;
-  if (a.cls[e] != CLS) return;  // uniform within the group
-  const int64_t r = a.rowidx[e];
+  if (gid >= a.nitems) return;  // whole groups
+  const int2 item = a.items[gid];
+  const int64_t e = item.x;
+  const int64_t r = item.y;
   const int64_t i = a.row_begin + r;
   const int64_t j = a.col[e];
   const int64_t n = a.n;
@@ -497,7 +513,7 @@ __global__ void __launch_bounds__(kThreads) near_kernel(NearArgs<R> a) {
       for (int c = 0; c < 3; ++c) e[p][c] = (float)(v[p][c] - ci[c]);
     const float wAf = (float)wA;
     for (int q = lig; q < a.npts; q += G) {
-      const float4 L = a.rule_f[q];
+      const float4 L = s_rf[q];
       float d[3];
 #pragma unroll
       for (int c = 0; c < 3; ++c) d[c] = fmaf(L.z, e[2][c], fmaf(L.y, e[1][c], L.x * e[0][c]));
@@ -505,22 +521,24 @@ __global__ void __launch_bounds__(kThreads) near_kernel(NearArgs<R> a) {
     }
   } else {
     for (int q = lig; q < a.npts; q += G) {
-      const double4 L = a.rule[q];
+      const double4 L = s_rd[q];
       R d[3];
 #pragma unroll
       for (int c = 0; c < 3; ++c) d[c] = (R)(((L.x * v[0][c] + L.y * v[1][c]) + L.z * v[2][c]) - ci[c]);
       nat::pair_accumulate<R>(d[0], d[1], d[2], nx, ny, nz, (R)(L.w * wA), a.k, Vr, Vi, Kr, Ki);
     }
   }
-  const unsigned mask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << ((threadIdx.x & 31) / G * G));
+  if constexpr (G > 1) {
+    const unsigned mask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << ((threadIdx.x & 31) / G * G));
 #pragma unroll
-  for (int o = G / 2; o > 0; o >>= 1) {
-    Vr += __shfl_xor_sync(mask, Vr, o, G);
-    Vi += __shfl_xor_sync(mask, Vi, o, G);
-    Kr += __shfl_xor_sync(mask, Kr, o, G);
-    Ki += __shfl_xor_sync(mask, Ki, o, G);
+    for (int o = G / 2; o > 0; o >>= 1) {
+      Vr += __shfl_xor_sync(mask, Vr, o, G);
+      Vi += __shfl_xor_sync(mask, Vi, o, G);
+      Kr += __shfl_xor_sync(mask, Kr, o, G);
+      Ki += __shfl_xor_sync(mask, Ki, o, G);
+    }
+    if (lig != 0) return;
   }
-  if (lig != 0) return;
   store_entry<R>(a.A, (size_t)r * a.lda + j, -Kr, -Ki);
   if (a.n_rhs > 0) {
     R y[NQ][3], w[NQ];
@@ -620,10 +638,60 @@ __global__ void self_kernel(int64_t n, int64_t nv, int64_t row_begin, int64_t ro
   }
 }
 
-__global__ void rowidx_kernel(int64_t rows, const int64_t* __restrict__ rp, int32_t* __restrict__ ri) {
+// Per-class compaction of the near list (CSR order kept): cnt[c][r+1] = entries of class
+// c+1 in row r; after the scan, fill writes (entry, row) pairs into the class lists.
+__global__ void class_count_kernel(int64_t rows, const int64_t* __restrict__ rp, const uint8_t* __restrict__ cls,
+                                   int32_t* __restrict__ cntS, int32_t* __restrict__ cntN) {
   int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (r >= rows) return;
-  for (int64_t e = rp[r]; e < rp[r + 1]; ++e) ri[e] = (int32_t)r;
+  int s = 0, nn = 0;
+  for (int64_t e = rp[r]; e < rp[r + 1]; ++e) {
+    if (cls[e] == 1) ++s;
+    else ++nn;
+  }
+  cntS[r + 1] = s;
+  cntN[r + 1] = nn;
+  if (r == 0) cntS[0] = cntN[0] = 0;
+}
+
+// In-place inclusive scan of cnt[1..rows] (cnt[0] = 0), one CTA, fixed segmentation.
+__global__ void __launch_bounds__(1024) scan_i32_kernel(int32_t* cnt, int64_t rows) {
+  __shared__ int64_t part[1024];
+  const int t = threadIdx.x;
+  const int64_t per = (rows + 1023) / 1024;
+  const int64_t b = 1 + t * per, e = nat::min64(rows + 1, b + per);
+  int64_t s = 0;
+  for (int64_t i = b; i < e; ++i) s += cnt[i];
+  part[t] = s;
+  __syncthreads();
+  if (t == 0) {
+    int64_t acc = 0;
+    for (int q = 0; q < 1024; ++q) {
+      const int64_t v = part[q];
+      part[q] = acc;
+      acc += v;
+    }
+  }
+  __syncthreads();
+  int64_t acc = part[t];
+  for (int64_t i = b; i < e; ++i) {
+    acc += cnt[i];
+    cnt[i] = (int32_t)acc;
+  }
+}
+
+__global__ void class_fill_kernel(int64_t rows, const int64_t* __restrict__ rp, const uint8_t* __restrict__ cls,
+                                  const int32_t* __restrict__ offS, const int32_t* __restrict__ offN,
+                                  int2* __restrict__ listS, int2* __restrict__ listN) {
+  int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  int s = offS[r], nn = offN[r];
+  for (int64_t e = rp[r]; e < rp[r + 1]; ++e) {
+    if (cls[e] == 1)
+      listS[s++] = make_int2((int)e, (int)r);
+    else
+      listN[nn++] = make_int2((int)e, (int)r);
+  }
 }
 
 __global__ void rhs_final_kernel(int64_t rows, int n_rhs, int n_colblk, const double2* __restrict__ bpart,
@@ -824,7 +892,10 @@ struct AsmWs {
   void* qxyz;
   void* qw;
   void* qn;
-  int32_t* rowidx;
+  int32_t* cntS;   // [rows+1] per-class counts -> offsets
+  int32_t* cntN;
+  int2* listS;     // compacted (entry, row) lists
+  int2* listN;
   double2* bpart;
   double2* corr;
   double2* corr_self;
@@ -842,7 +913,10 @@ size_t carve(nat::Carver& c, AsmWs& w, int64_t n, int64_t rows, int64_t nnz, int
   w.qxyz = c.take<char>(rsz * kMaxFarQ * 3 * n);
   w.qw = c.take<char>(rsz * kMaxFarQ * n);
   w.qn = c.take<char>(rsz * 3 * n);
-  w.rowidx = c.take<int32_t>(nnz > 0 ? nnz : 1);
+  w.cntS = c.take<int32_t>(rows + 1);
+  w.cntN = c.take<int32_t>(rows + 1);
+  w.listS = c.take<int2>(nnz > 0 ? nnz : 1);
+  w.listN = c.take<int2>(nnz > 0 ? nnz : 1);
   w.bpart = c.take<double2>((size_t)n_colblk * (n_rhs > 0 ? n_rhs : 1) * rows);
   w.corr = c.take<double2>((size_t)(nnz > 0 ? nnz : 1) * (n_rhs > 0 ? n_rhs : 1));
   w.corr_self = c.take<double2>((size_t)rows * (n_rhs > 0 ? n_rhs : 1));
@@ -899,7 +973,16 @@ nat_status assemble_impl(const nat_mesh* mesh, const nat_geom* geom, const Opts&
   NAT_LAUNCH_CHECK();
   // a5: near pairs overwrite A and correct b; self term
   if (nnz > 0) {
-    rowidx_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, s>>>(rows, rp, w.rowidx);
+    const unsigned rb = (unsigned)((rows + 255) / 256);
+    class_count_kernel<<<rb, 256, 0, s>>>(rows, rp, cls, w.cntS, w.cntN);
+    scan_i32_kernel<<<1, 1024, 0, s>>>(w.cntS, rows);
+    scan_i32_kernel<<<1, 1024, 0, s>>>(w.cntN, rows);
+    class_fill_kernel<<<rb, 256, 0, s>>>(rows, rp, cls, w.cntS, w.cntN, w.listS, w.listN);
+    NAT_LAUNCH_CHECK();
+    int32_t counts[2] = {0, 0};
+    NAT_CUDA_TRY(cudaMemcpyAsync(&counts[0], w.cntS + rows, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    NAT_CUDA_TRY(cudaMemcpyAsync(&counts[1], w.cntN + rows, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    NAT_CUDA_TRY(cudaStreamSynchronize(s));
     NearArgs<R> na{};
     na.n = n;
     na.nv = mesh->n_vert;
@@ -910,7 +993,6 @@ nat_status assemble_impl(const nat_mesh* mesh, const nat_geom* geom, const Opts&
     na.row_ptr = rp;
     na.col = col;
     na.cls = cls;
-    na.rowidx = w.rowidx;
     na.vx = mesh->vxyz;
     na.tri = mesh->tri;
     na.cen = geom->centroid;
@@ -925,14 +1007,24 @@ nat_status assemble_impl(const nat_mesh* mesh, const nat_geom* geom, const Opts&
     na.g = g;
     na.A = A;
     na.corr = w.corr;
-    na.rule = w.rule_S;
-    na.rule_f = w.rule_Sf;
-    na.npts = (int)pS.size();
-    near_kernel<R, NQ, 32, 1><<<(unsigned)((nnz * 32 + kThreads - 1) / kThreads), kThreads, 0, s>>>(na);
-    na.rule = w.rule_N;
-    na.rule_f = w.rule_Nf;
-    na.npts = (int)pN.size();
-    near_kernel<R, NQ, 8, 2><<<(unsigned)((nnz * 8 + kThreads - 1) / kThreads), kThreads, 0, s>>>(na);
+    const size_t rsz = sizeof(R) == 4 ? sizeof(float4) : sizeof(double4);
+    if (counts[0] > 0) {  // class S: 4 lanes per pair
+      na.rule = w.rule_S;
+      na.rule_f = w.rule_Sf;
+      na.npts = (int)pS.size();
+      na.items = w.listS;
+      na.nitems = counts[0];
+      near_kernel<R, NQ, 4><<<(unsigned)((counts[0] * 4LL + kThreads - 1) / kThreads), kThreads,
+                              na.npts * rsz, s>>>(na);
+    }
+    if (counts[1] > 0) {  // class N: one thread per pair
+      na.rule = w.rule_N;
+      na.rule_f = w.rule_Nf;
+      na.npts = (int)pN.size();
+      na.items = w.listN;
+      na.nitems = counts[1];
+      near_kernel<R, NQ, 1><<<(unsigned)((counts[1] + kThreads - 1) / kThreads), kThreads, na.npts * rsz, s>>>(na);
+    }
     NAT_LAUNCH_CHECK();
   }
   self_kernel<R, NQ><<<(unsigned)((rows + 127) / 128), 128, 0, s>>>(

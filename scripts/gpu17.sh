@@ -1,0 +1,5 @@
+python -m paper_2506_06190_b200.build > /dev/null || exit 1
+python scripts/prof_kernels.py > gpurun_out/prof_plain.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:"near_kernel" -s 2 -c 4 \
+    -o gpurun_out/prof_near python scripts/prof_kernels.py > gpurun_out/ncu_full.log 2>&1
+echo "full rc=$?"
