@@ -150,21 +150,30 @@ __global__ void apply_combine_kernel(int nsys, int64_t M, const double2* __restr
 // this fp64 pass adds them, so the fp32 path keeps the 1e-4 parity bar.
 constexpr int kNT = 256;
 
+// One warp per 4 rows (32 rows per CTA), candidates staged 256 at a time in shared
+// memory, hits compacted with __ballot_sync (columns ascending, deterministic).
+constexpr int kNW = 8, kNRows = 4;
 template <bool kFill>
 __global__ void __launch_bounds__(kNT) mc_near_kernel(int64_t M, const double* __restrict__ smp, double cx,
                                                       double cy, double cz, float thr,
                                                       int32_t* __restrict__ rp, int32_t* __restrict__ col,
                                                       int64_t cap, int* overflow) {
   __shared__ float sx[kNT], sy[kNT], sz[kNT];
-  const int64_t i = blockIdx.x * (int64_t)kNT + threadIdx.x;
-  float xi = 0.f, yi = 0.f, zi = 0.f;
-  if (i < M) {
-    xi = (float)(smp[i] - cx);
-    yi = (float)(smp[M + i] - cy);
-    zi = (float)(smp[2 * M + i] - cz);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t r0 = (int64_t)blockIdx.x * (kNW * kNRows) + warp * kNRows;
+  float xi[kNRows], yi[kNRows], zi[kNRows];
+  int64_t pos[kNRows];
+  bool live[kNRows];
+#pragma unroll
+  for (int q = 0; q < kNRows; ++q) {
+    const int64_t i = r0 + q;
+    live[q] = i < M;
+    const int64_t ii = live[q] ? i : 0;
+    xi[q] = (float)(smp[ii] - cx);
+    yi[q] = (float)(smp[M + ii] - cy);
+    zi[q] = (float)(smp[2 * M + ii] - cz);
+    pos[q] = (kFill && live[q]) ? rp[i] : 0;
   }
-  int cnt = 0;
-  int64_t pos = (kFill && i < M) ? rp[i] : 0;
   for (int64_t j0 = 0; j0 < M; j0 += kNT) {
     __syncthreads();
     const int64_t jl = j0 + threadIdx.x;
@@ -175,21 +184,29 @@ __global__ void __launch_bounds__(kNT) mc_near_kernel(int64_t M, const double* _
     }
     __syncthreads();
     const int jn = (int)nat::min64(kNT, M - j0);
-    if (i < M) {
-      for (int t = 0; t < jn; ++t) {
-        const float r2 = nat::pair_r2_f32(__fsub_rn(sx[t], xi), __fsub_rn(sy[t], yi), __fsub_rn(sz[t], zi));
-        if (r2 <= thr && j0 + t != i) {
-          if (kFill) {
-            if (pos < cap) col[pos] = (int32_t)(j0 + t);
-            ++pos;
-          } else {
-            ++cnt;
-          }
+    for (int jj = 0; jj < jn; jj += 32) {
+      const int t = jj + lane;
+      const bool in = t < jn;
+      const float ox = in ? sx[t] : 3e30f, oy = in ? sy[t] : 3e30f, oz = in ? sz[t] : 3e30f;
+#pragma unroll
+      for (int q = 0; q < kNRows; ++q) {
+        if (!live[q]) continue;  // warp-uniform
+        const float r2 = nat::pair_r2_f32(__fsub_rn(ox, xi[q]), __fsub_rn(oy, yi[q]), __fsub_rn(oz, zi[q]));
+        const bool hit = in && r2 <= thr && j0 + t != r0 + q;
+        const unsigned m = __ballot_sync(0xffffffffu, hit);
+        if (kFill && hit) {
+          const int64_t o = pos[q] + __popc(m & ((1u << lane) - 1u));
+          if (o < cap) col[o] = (int32_t)(j0 + t);
         }
+        pos[q] += __popc(m);
       }
     }
   }
-  if (!kFill && i < M) rp[i + 1] = cnt;
+  if (!kFill && lane == 0) {
+#pragma unroll
+    for (int q = 0; q < kNRows; ++q)
+      if (live[q]) rp[r0 + q + 1] = (int32_t)pos[q];
+  }
 }
 
 __global__ void __launch_bounds__(1024) scan32_kernel(int32_t* rp, int64_t M, int64_t cap, int* overflow) {
@@ -240,8 +257,9 @@ __global__ void mc_near_apply_kernel(int nsys, int64_t M, const double* __restri
     const double dx = smp[j] - xi, dy = smp[M + j] - yi, dz = smp[2 * M + j] - zi;
     const double r = sqrt(dx * dx + dy * dy + dz * dz);
     const double dn = dx * smp[3 * M + j] + dy * smp[4 * M + j] + dz * smp[5 * M + j];
-    double sn, cs;
-    sincos(k * r, &sn, &cs);
+    float snf, csf;  // |kr| < 2 k eps: the fp32 phase is accurate to ~1e-7 absolute
+    __sincosf((float)(k * r), &snf, &csf);
+    const double sn = snf, cs = csf;
     const double t = w * nat::kInv4Pi / r;  // w G = t e^{ikr}
     if (p) {  // w p dG/dn_y = t dn/r^2 (ikr - 1) e^{ikr} p
       const double2 pv = p[(size_t)s * M + j];
@@ -286,7 +304,7 @@ nat_status build_near(NearPairs& np, int64_t M, const double* smp, const double*
   np.on = true;
   np.thr = (float)(4.0 * eps * eps);
   const double cx = center ? center[0] : 0.0, cy = center ? center[1] : 0.0, cz = center ? center[2] : 0.0;
-  const unsigned grid = (unsigned)((M + kNT - 1) / kNT);
+  const unsigned grid = (unsigned)((M + kNW * kNRows - 1) / (kNW * kNRows));
   NAT_CUDA_TRY(cudaMemsetAsync(np.overflow, 0, sizeof(int), s));
   mc_near_kernel<false><<<grid, kNT, 0, s>>>(M, smp, cx, cy, cz, np.thr, np.rp, np.col, np.cap, np.overflow);
   scan32_kernel<<<1, 1024, 0, s>>>(np.rp, M, np.cap, np.overflow);
