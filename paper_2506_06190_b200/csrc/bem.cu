@@ -366,8 +366,12 @@ __global__ void __launch_bounds__(kThreads, 3) far_kernel_x2(FarArgs<float> a) {
       gi[q] = f2pack((float)gv.y, (float)gv.y);
       ngi[q] = f2pack(-(float)gv.y, -(float)gv.y);
     }
+    // running pointer to A[i0 + 2t][j] (one 64-bit add per row pair instead of a
+    // 64-bit multiply per store)
+    float2* arow = reinterpret_cast<float2*>(a.A) + (size_t)i0 * a.lda + jj;
+    const int64_t ld = a.lda;
 #pragma unroll
-    for (int t = 0; t < TP; ++t) {
+    for (int t = 0; t < TP; ++t, arow += 2 * ld) {
       if (2 * t < nrows) {
         const f2r cx = s_c[0][t], cy = s_c[1][t], cz = s_c[2][t];
         f2r Vr = 0ull, Vi = 0ull, Kr = 0ull, Ki = 0ull;  // K here is -K
@@ -392,9 +396,8 @@ __global__ void __launch_bounds__(kThreads, 3) far_kernel_x2(FarArgs<float> a) {
           Ki = f2fma(u, f2fma(nkr, cs, sn), Ki);
         }
         if (a.store_A && valid) {
-          float2* A2 = reinterpret_cast<float2*>(a.A);
-          A2[(size_t)(i0 + 2 * t) * a.lda + j] = make_float2(f2lo(Kr), f2lo(Ki));
-          if (2 * t + 1 < nrows) A2[(size_t)(i0 + 2 * t + 1) * a.lda + j] = make_float2(f2hi(Kr), f2hi(Ki));
+          arow[0] = make_float2(f2lo(Kr), f2lo(Ki));
+          if (2 * t + 1 < nrows) arow[ld] = make_float2(f2hi(Kr), f2hi(Ki));
         }
 #pragma unroll
         for (int q = 0; q < NR; ++q) {

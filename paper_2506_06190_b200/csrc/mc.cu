@@ -279,6 +279,60 @@ __global__ void mc_near_apply_kernel(int nsys, int64_t M, const double* __restri
   R[q] = make_double2(o.x + ar, o.y + ai);
 }
 
+// Fused epilogue of the MC operators: sum of the split-K partials (fixed order), the
+// fp64 close-pair contributions (same formula as mc_near_apply_kernel) and the disk /
+// diagonal terms:  apply: out = 1/2 p - R;  rhs: b = R - (eps/2) g.
+__global__ void mc_finish_kernel(int nsys, int64_t M, const double* __restrict__ smp,
+                                 const int32_t* __restrict__ rp, const int32_t* __restrict__ col, KArr ka,
+                                 double w, const double2* __restrict__ part, int n_split,
+                                 const double2* __restrict__ p, const double2* __restrict__ g, double eps,
+                                 double2* __restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int s = blockIdx.y;
+  if (i >= M) return;
+  const size_t q = (size_t)s * M + i;
+  const size_t stride = (size_t)nsys * M;
+  double ar = 0.0, ai = 0.0;
+  for (int sp = 0; sp < n_split; ++sp) {
+    const double2 v = part[sp * stride + q];
+    ar += v.x;
+    ai += v.y;
+  }
+  if (rp) {
+    const double k = ka.k[s];
+    const double xi = smp[i], yi = smp[M + i], zi = smp[2 * M + i];
+    for (int e = rp[i]; e < rp[i + 1]; ++e) {
+      const int64_t j = col[e];
+      const double dx = smp[j] - xi, dy = smp[M + j] - yi, dz = smp[2 * M + j] - zi;
+      const double r = sqrt(dx * dx + dy * dy + dz * dz);
+      float snf, csf;
+      __sincosf((float)(k * r), &snf, &csf);
+      const double sn = snf, cs = csf;
+      const double t = w * nat::kInv4Pi / r;
+      if (p) {
+        const double dn = dx * smp[3 * M + j] + dy * smp[4 * M + j] + dz * smp[5 * M + j];
+        const double2 pv = p[(size_t)s * M + j];
+        const double u = t * dn / (r * r);
+        const double er = -cs - k * r * sn, ei = k * r * cs - sn;
+        ar += u * (er * pv.x - ei * pv.y);
+        ai += u * (er * pv.y + ei * pv.x);
+      }
+      if (g) {
+        const double2 gv = g[(size_t)s * M + j];
+        ar -= t * (cs * gv.x - sn * gv.y);
+        ai -= t * (cs * gv.y + sn * gv.x);
+      }
+    }
+  }
+  if (p) {
+    const double2 pv = p[q];
+    out[q] = make_double2(0.5 * pv.x - ar, 0.5 * pv.y - ai);
+  } else {
+    const double2 gv = g[q];
+    out[q] = make_double2(ar - 0.5 * eps * gv.x, ai - 0.5 * eps * gv.y);
+  }
+}
+
 struct NearPairs {
   int32_t* rp = nullptr;   // [M+1]
   int32_t* col = nullptr;  // [cap]
@@ -345,6 +399,21 @@ nat::RadInput self_input(int64_t M, const double* smp, int nsys, double w) {
   return in;
 }
 
+// radiation kernel (partials kept) + one fused epilogue launch per 64 systems
+nat_status finish_op(const nat::RadInput& in, nat_prec prec, int64_t M, const double* smp, int nsys,
+                     const double* k, double w, double eps, const double2* p, const double2* g, double2* out,
+                     void* ws, size_t ws_bytes, const NearPairs& np, cudaStream_t s) {
+  nat::RadPartials keep;
+  nat_status st = nat::radiate_internal(in, prec, k, M, smp, out, ws, ws_bytes, true, s, &keep);
+  if (st != NAT_OK) return st;
+  KArr ka{};
+  for (int q = 0; q < nsys && q < 64; ++q) ka.k[q] = k[q];
+  mc_finish_kernel<<<dim3((unsigned)((M + 255) / 256), nsys), 256, 0, s>>>(
+      nsys, M, smp, np.on ? np.rp : nullptr, np.on ? np.col : nullptr, ka, w, keep.part, keep.n_split, p, g, eps, out);
+  NAT_LAUNCH_CHECK();
+  return NAT_OK;
+}
+
 nat_status mc_rhs_impl(nat_prec prec, int64_t M, const double* smp, int nsys, const double* k,
                        const double2* g, double w, double eps, double2* b, void* ws, size_t ws_bytes,
                        const double* center, const NearPairs& np, cudaStream_t s) {
@@ -353,13 +422,7 @@ nat_status mc_rhs_impl(nat_prec prec, int64_t M, const double* smp, int nsys, co
     for (int d = 0; d < 3; ++d) in.center[d] = center[d];
   in.g = g;
   in.self_r2 = np.on ? np.thr : 0.f;
-  nat_status st = nat::radiate_internal(in, prec, k, M, smp, b, ws, ws_bytes, true, s);
-  if (st != NAT_OK) return st;
-  st = near_apply(np, nsys, M, smp, k, w, nullptr, g, b, s);
-  if (st != NAT_OK) return st;
-  rhs_combine_kernel<<<dim3((unsigned)((M + 255) / 256), nsys), 256, 0, s>>>(nsys, M, eps, g, b);
-  NAT_LAUNCH_CHECK();
-  return NAT_OK;
+  return finish_op(in, prec, M, smp, nsys, k, w, eps, nullptr, g, b, ws, ws_bytes, np, s);
 }
 
 nat_status mc_apply_impl(nat_prec prec, int64_t M, const double* smp, int nsys, const double* k,
@@ -370,13 +433,7 @@ nat_status mc_apply_impl(nat_prec prec, int64_t M, const double* smp, int nsys, 
     for (int d = 0; d < 3; ++d) in.center[d] = center[d];
   in.p = p;
   in.self_r2 = np.on ? np.thr : 0.f;
-  nat_status st = nat::radiate_internal(in, prec, k, M, smp, out, ws, ws_bytes, true, s);
-  if (st != NAT_OK) return st;
-  st = near_apply(np, nsys, M, smp, k, w, p, nullptr, out, s);
-  if (st != NAT_OK) return st;
-  apply_combine_kernel<<<dim3((unsigned)((M + 255) / 256), nsys), 256, 0, s>>>(nsys, M, p, out);
-  NAT_LAUNCH_CHECK();
-  return NAT_OK;
+  return finish_op(in, prec, M, smp, nsys, k, w, 0.0, p, nullptr, out, ws, ws_bytes, np, s);
 }
 
 nat_status check_k(int n, const double* k) {

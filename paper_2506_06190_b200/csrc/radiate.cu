@@ -627,7 +627,8 @@ size_t radiate_ws_bytes_upto(nat_prec prec, int64_t n_src, int max_modes, int64_
 
 nat_status radiate_internal(const RadInput& in, nat_prec prec, const double* k, int64_t n_lis,
                             const double* lis, double2* out, void* ws, size_t ws_bytes, bool self,
-                            cudaStream_t s) {
+                            cudaStream_t s, RadPartials* keep) {
+  if (keep && in.n_modes > kMaxModes) return fail(NAT_ERR_INVALID_ARG, "unreduced partials need <= 64 modes");
   for (int m0 = 0; m0 < in.n_modes; m0 += kMaxModes) {
     const int nm = (in.n_modes - m0) < kMaxModes ? (in.n_modes - m0) : kMaxModes;
     Plan pl = make_plan(prec, in.n_src, nm, n_lis);
@@ -681,7 +682,10 @@ nat_status radiate_internal(const RadInput& in, nat_prec prec, const double* k, 
       e = self ? launch_f32_mb<1>(pl, prm, s) : launch_f32_mb<0>(pl, prm, s);
     }
     if (e != cudaSuccess) return fail(NAT_ERR_CUDA, "radiate launch: %s", cudaGetErrorString(e));
-    if (pl.n_split > 1) {
+    if (keep) {  // the caller reduces the partials in its own epilogue
+      keep->part = pl.n_split > 1 ? part : dst;
+      keep->n_split = pl.n_split;
+    } else if (pl.n_split > 1) {
       int64_t n = (int64_t)nm * n_lis;
       reduce_splits_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(part, pl.n_split, n, dst);
       NAT_LAUNCH_CHECK();

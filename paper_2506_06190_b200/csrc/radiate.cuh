@@ -23,8 +23,13 @@ size_t radiate_ws_bytes(nat_prec prec, int64_t n_src, int n_modes, int64_t n_lis
 size_t radiate_ws_bytes_upto(nat_prec prec, int64_t n_src, int max_modes, int64_t n_lis);
 // out[m][l] (c128 [n_modes][n_lis]) = sum_s w_s [p_ms dG_m/dn_y - g_ms G_m](x_l, y_s);
 // self = true excludes the pair with identical coordinates (targets == sources).
+// Split-K partials left unreduced for a fused caller epilogue: part[split][mode][lis].
+struct RadPartials {
+  const double2* part = nullptr;
+  int n_split = 0;
+};
 nat_status radiate_internal(const RadInput& in, nat_prec prec, const double* k, int64_t n_lis,
                             const double* lis, double2* out, void* ws, size_t ws_bytes, bool self,
-                            cudaStream_t s);
+                            cudaStream_t s, RadPartials* keep = nullptr);
 
 }  // namespace nat
