@@ -17,7 +17,9 @@
 // Near pairs: one 32-lane group per vertex-sharing pair (448 points), one 8-lane group
 // per close pair (28 points), fp64 point positions and differences, kernel math in the
 // path's precision.  Self term: one thread per row, polar Gauss-Legendre in fp64.
+#include <algorithm>
 #include <cmath>
+#include <cstring>
 #include <vector>
 
 #include "f32x2.cuh"
@@ -459,7 +461,7 @@ struct NearArgs {
   const float4* rule_f;    // the same rule in fp32 (fp32 path)
   int npts;
   const int2* items;       // compacted (entry, row) list of this launch's class
-  int64_t nitems;
+  const int32_t* nitems;   // [device] its length
   FarCols<R> cols;         // far rule (to subtract the far contribution from b)
   double cx, cy, cz;
   R k;
@@ -475,10 +477,16 @@ struct NearArgs {
 constexpr int kMaxNearPts = 7 << 8;  // up to 4 subdivision levels x 7 points (S: 448 at 3)
 
 template <typename R, int NQ, int G>
+__device__ __forceinline__ void near_item(const NearArgs<R>& a, int64_t gid, int lig, const float4* s_rf,
+                                          const double4* s_rd);
+
+template <typename R, int NQ, int G>
 __global__ void __launch_bounds__(kThreads) near_kernel(NearArgs<R> a) {
   extern __shared__ __align__(16) unsigned char near_smem[];
   float4* s_rf = reinterpret_cast<float4*>(near_smem);
   double4* s_rd = reinterpret_cast<double4*>(near_smem);
+  const int64_t nitems = *a.nitems;
+  if ((int64_t)blockIdx.x * (blockDim.x / G) >= nitems) return;  // grid sized for the worst case
   for (int q = threadIdx.x; q < a.npts; q += blockDim.x) {
     if constexpr (sizeof(R) == 4)
       s_rf[q] = a.rule_f[q];
@@ -486,9 +494,16 @@ __global__ void __launch_bounds__(kThreads) near_kernel(NearArgs<R> a) {
       s_rd[q] = a.rule[q];
   }
   __syncthreads();
-  const int64_t gid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
+  // grid-stride over the pair groups; the item count is read on the device (no host sync)
   const int lig = threadIdx.x % G;
-  if (gid >= a.nitems) return;  // whole groups
+  const int64_t stride = (int64_t)gridDim.x * (blockDim.x / G);
+  for (int64_t gid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G; gid < nitems; gid += stride)
+    near_item<R, NQ, G>(a, gid, lig, s_rf, s_rd);
+}
+
+template <typename R, int NQ, int G>
+__device__ __forceinline__ void near_item(const NearArgs<R>& a, int64_t gid, int lig, const float4* s_rf,
+                                          const double4* s_rd) {
   const int2 item = a.items[gid];
   const int64_t e = item.x;
   const int64_t r = item.y;
@@ -735,7 +750,9 @@ constexpr int kGemvRows32 = 4; // c64 kernel
 // register budget allows 4 CTAs/SM); fixed-order reduction -> deterministic.
 __global__ void __launch_bounds__(kThreads, 3) gemv_c64_kernel(int64_t rows, int64_t n, const float2* __restrict__ A,
                                                               int64_t lda, const double2* __restrict__ x,
-                                                              double2* __restrict__ y) {
+                                                              double2* __restrict__ y,
+                                                              const unsigned long long* __restrict__ skip) {
+  if (skip && *skip == 0ull) return;  // Krylov driver: every system already converged
   constexpr int RB = kGemvRows32;
   __shared__ double2 red[kThreads / 32][RB];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -841,7 +858,9 @@ __global__ void __launch_bounds__(kThreads, 3) gemv_c64_kernel(int64_t rows, int
 
 __global__ void __launch_bounds__(kThreads) gemv_c128_kernel(int64_t rows, int64_t n, const double2* __restrict__ A,
                                                             int64_t lda, const double2* __restrict__ x,
-                                                            double2* __restrict__ y) {
+                                                            double2* __restrict__ y,
+                                                            const unsigned long long* __restrict__ skip) {
+  if (skip && *skip == 0ull) return;
   __shared__ double2 red[kThreads / 32][kGemvRows];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t r0 = (int64_t)blockIdx.x * kGemvRows;
@@ -982,10 +1001,6 @@ nat_status assemble_impl(const nat_mesh* mesh, const nat_geom* geom, const Opts&
     scan_i32_kernel<<<1, 1024, 0, s>>>(w.cntN, rows);
     class_fill_kernel<<<rb, 256, 0, s>>>(rows, rp, cls, w.cntS, w.cntN, w.listS, w.listN);
     NAT_LAUNCH_CHECK();
-    int32_t counts[2] = {0, 0};
-    NAT_CUDA_TRY(cudaMemcpyAsync(&counts[0], w.cntS + rows, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-    NAT_CUDA_TRY(cudaMemcpyAsync(&counts[1], w.cntN + rows, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-    NAT_CUDA_TRY(cudaStreamSynchronize(s));
     NearArgs<R> na{};
     na.n = n;
     na.nv = mesh->n_vert;
@@ -1011,23 +1026,22 @@ nat_status assemble_impl(const nat_mesh* mesh, const nat_geom* geom, const Opts&
     na.A = A;
     na.corr = w.corr;
     const size_t rsz = sizeof(R) == 4 ? sizeof(float4) : sizeof(double4);
-    if (counts[0] > 0) {  // class S: 4 lanes per pair
-      na.rule = w.rule_S;
-      na.rule_f = w.rule_Sf;
-      na.npts = (int)pS.size();
-      na.items = w.listS;
-      na.nitems = counts[0];
-      near_kernel<R, NQ, 4><<<(unsigned)((counts[0] * 4LL + kThreads - 1) / kThreads), kThreads,
-                              na.npts * rsz, s>>>(na);
-    }
-    if (counts[1] > 0) {  // class N: one thread per pair
-      na.rule = w.rule_N;
-      na.rule_f = w.rule_Nf;
-      na.npts = (int)pN.size();
-      na.items = w.listN;
-      na.nitems = counts[1];
-      near_kernel<R, NQ, 1><<<(unsigned)((counts[1] + kThreads - 1) / kThreads), kThreads, na.npts * rsz, s>>>(na);
-    }
+    // persistent grids (the class counts stay on the device): at most one group per item
+    const int64_t cap = (int64_t)nat::device_sm_count() * 64;
+    na.rule = w.rule_S;  // class S: 4 lanes per pair
+    na.rule_f = w.rule_Sf;
+    na.npts = (int)pS.size();
+    na.items = w.listS;
+    na.nitems = w.cntS + rows;
+    near_kernel<R, NQ, 4><<<(unsigned)std::min(cap, (nnz * 4 + kThreads - 1) / kThreads), kThreads,
+                            na.npts * rsz, s>>>(na);
+    na.rule = w.rule_N;  // class N: one thread per pair
+    na.rule_f = w.rule_Nf;
+    na.npts = (int)pN.size();
+    na.items = w.listN;
+    na.nitems = w.cntN + rows;
+    near_kernel<R, NQ, 1><<<(unsigned)std::min(cap, (nnz + kThreads - 1) / kThreads), kThreads, na.npts * rsz,
+                            s>>>(na);
     NAT_LAUNCH_CHECK();
   }
   self_kernel<R, NQ><<<(unsigned)((rows + 127) / 128), 128, 0, s>>>(
@@ -1106,18 +1120,30 @@ extern "C" nat_status nat_bem_assemble(const nat_mesh* mesh, const nat_geom* geo
   size_t need = carve(c, w, n, rows, nnz, n_rhs, kMaxFarQ, (int)pS.size(), (int)pN.size(), o.gl, rsz);
   if (ws_bytes < need) return nat::fail(NAT_ERR_WORKSPACE, "workspace %zu < %zu", ws_bytes, need);
   NAT_REQUIRE_DEV(ws);
-  // rule tables -> workspace (pageable copies: staged before the call returns)
-  NAT_CUDA_TRY(cudaMemcpyAsync(w.rule_far, pF.data(), pF.size() * sizeof(Pt), cudaMemcpyHostToDevice, s));
-  NAT_CUDA_TRY(cudaMemcpyAsync(w.rule_S, pS.data(), pS.size() * sizeof(Pt), cudaMemcpyHostToDevice, s));
-  NAT_CUDA_TRY(cudaMemcpyAsync(w.rule_N, pN.data(), pN.size() * sizeof(Pt), cudaMemcpyHostToDevice, s));
-  std::vector<float4> fS(pS.size()), fN(pN.size());
-  for (size_t q = 0; q < pS.size(); ++q) fS[q] = make_float4((float)pS[q].l1, (float)pS[q].l2, (float)pS[q].l3, (float)pS[q].w);
-  for (size_t q = 0; q < pN.size(); ++q) fN[q] = make_float4((float)pN[q].l1, (float)pN[q].l2, (float)pN[q].l3, (float)pN[q].w);
-  NAT_CUDA_TRY(cudaMemcpyAsync(w.rule_Sf, fS.data(), fS.size() * sizeof(float4), cudaMemcpyHostToDevice, s));
-  NAT_CUDA_TRY(cudaMemcpyAsync(w.rule_Nf, fN.data(), fN.size() * sizeof(float4), cudaMemcpyHostToDevice, s));
-  std::vector<double> gl(glx);
-  gl.insert(gl.end(), glw.begin(), glw.end());
-  NAT_CUDA_TRY(cudaMemcpyAsync(w.gl, gl.data(), gl.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+  // rule tables -> workspace in one copy (they are carved contiguously; pageable source:
+  // staged before the call returns)
+  {
+    std::vector<float4> fS(pS.size()), fN(pN.size());
+    for (size_t q = 0; q < pS.size(); ++q)
+      fS[q] = make_float4((float)pS[q].l1, (float)pS[q].l2, (float)pS[q].l3, (float)pS[q].w);
+    for (size_t q = 0; q < pN.size(); ++q)
+      fN[q] = make_float4((float)pN[q].l1, (float)pN[q].l2, (float)pN[q].l3, (float)pN[q].w);
+    std::vector<double> gl(glx);
+    gl.insert(gl.end(), glw.begin(), glw.end());
+    char* base = reinterpret_cast<char*>(w.rule_far);
+    const size_t total = (size_t)(reinterpret_cast<char*>(w.rule_Nf + fN.size()) - base);
+    std::vector<char> blob(total, 0);
+    auto put = [&](const void* dst, const void* src, size_t bytes) {
+      std::memcpy(blob.data() + (reinterpret_cast<const char*>(dst) - base), src, bytes);
+    };
+    put(w.rule_far, pF.data(), pF.size() * sizeof(Pt));
+    put(w.rule_S, pS.data(), pS.size() * sizeof(Pt));
+    put(w.rule_N, pN.data(), pN.size() * sizeof(Pt));
+    put(w.gl, gl.data(), gl.size() * sizeof(double));
+    put(w.rule_Sf, fS.data(), fS.size() * sizeof(float4));
+    put(w.rule_Nf, fN.data(), fN.size() * sizeof(float4));
+    NAT_CUDA_TRY(cudaMemcpyAsync(base, blob.data(), total, cudaMemcpyHostToDevice, s));
+  }
 
   const double2* gg = (const double2*)g;
   double2* bb = (double2*)rhs;
@@ -1155,10 +1181,10 @@ extern "C" nat_status nat_bem_matvec(nat_prec prec, int64_t rows, int64_t n, con
   unsigned grid = (unsigned)((rows + rb - 1) / rb);
   if (prec == NAT_FP32)
     gemv_c64_kernel<<<grid, kThreads, 0, (cudaStream_t)stream>>>(rows, n, (const float2*)A, lda,
-                                                                 (const double2*)x, (double2*)y);
+                                                                 (const double2*)x, (double2*)y, nullptr);
   else
     gemv_c128_kernel<<<grid, kThreads, 0, (cudaStream_t)stream>>>(rows, n, (const double2*)A, lda,
-                                                                  (const double2*)x, (double2*)y);
+                                                                  (const double2*)x, (double2*)y, nullptr);
   NAT_LAUNCH_CHECK();
   return NAT_OK;
 }
@@ -1166,13 +1192,14 @@ extern "C" nat_status nat_bem_matvec(nat_prec prec, int64_t rows, int64_t n, con
 namespace nat {
 // Used by the GMRES driver (gmres.cu).
 nat_status matvec_internal(nat_prec prec, int64_t rows, int64_t n, const void* A, int64_t lda,
-                           const void* x, void* y, cudaStream_t s) {
+                           const void* x, void* y, cudaStream_t s, const unsigned long long* skip) {
   const int rb = prec == NAT_FP32 ? kGemvRows32 : kGemvRows;
   unsigned grid = (unsigned)((rows + rb - 1) / rb);
   if (prec == NAT_FP32)
-    gemv_c64_kernel<<<grid, kThreads, 0, s>>>(rows, n, (const float2*)A, lda, (const double2*)x, (double2*)y);
+    gemv_c64_kernel<<<grid, kThreads, 0, s>>>(rows, n, (const float2*)A, lda, (const double2*)x, (double2*)y, skip);
   else
-    gemv_c128_kernel<<<grid, kThreads, 0, s>>>(rows, n, (const double2*)A, lda, (const double2*)x, (double2*)y);
+    gemv_c128_kernel<<<grid, kThreads, 0, s>>>(rows, n, (const double2*)A, lda, (const double2*)x, (double2*)y,
+                                               skip);
   NAT_LAUNCH_CHECK();
   return NAT_OK;
 }

@@ -4,11 +4,16 @@
 // Arnoldi).  Arnoldi uses classical Gram-Schmidt applied twice (CGS2): two batched
 // dot-product launches instead of j+1 dependent ones per iteration.  All reductions
 // use fixed chunking (kKrylovChunk) and fixed in-block trees: deterministic, and
-// identical on every rank and for every GPU count.
+// identical on every rank and for every GPU count.  The Givens update, the convergence
+// test and the back-substitution run on the device (one thread per system), so the host
+// never stalls the GPU between iterations (krylov.cuh).
 #include <chrono>
 #include <cmath>
-#include <complex>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <algorithm>
+#include <map>
 
 #include "krylov.cuh"
 #include "nat_comm.cuh"
@@ -17,6 +22,13 @@ namespace nat {
 namespace {
 
 constexpr int kT = 256;
+constexpr int kRing = 4;  // pinned mask slots / events in flight
+
+__device__ __forceinline__ bool sys_on(uint64_t active, const unsigned long long* dmask, int s) {
+  uint64_t a = active;
+  if (dmask) a &= *dmask;
+  return (a >> s) & 1ull;
+}
 
 __device__ __forceinline__ double2 block_reduce(double2 v, double2* sm) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -80,21 +92,30 @@ __device__ bool last_block(unsigned* cnt, unsigned total, bool* flag) {
 __global__ void __launch_bounds__(kT) dots_kernel(const double2* __restrict__ V, size_t vstride_k,
                                                  int64_t ldv, const double2* __restrict__ w, int64_t n,
                                                  int nvec, int nchunk, int mp1, uint64_t active,
+                                                 const unsigned long long* __restrict__ dmask,
                                                  double2* __restrict__ part, int mp2, int mode, int slot,
                                                  double2* __restrict__ h, double2* __restrict__ h2,
                                                  unsigned* __restrict__ cnt) {
   __shared__ double2 sm[kT / 32];
   __shared__ bool flag;
   const int c = blockIdx.x, k = blockIdx.y, s = blockIdx.z;
-  if (!((active >> s) & 1ull)) return;
+  if (!sys_on(active, dmask, s)) return;
   const double2* v = V + k * vstride_k + (size_t)s * ldv;
   const double2* ww = w + (size_t)s * ldv;
-  const int64_t i0 = (int64_t)c * kKrylovChunk, i1 = nat::min64(n, i0 + kKrylovChunk);
+  const int64_t i0 = (int64_t)c * kKrylovChunk;
   double2 acc = make_double2(0.0, 0.0);
-  for (int64_t i = i0 + threadIdx.x; i < i1; i += kT) {
-    double2 a = v[i], b = ww[i];
-    acc.x += a.x * b.x + a.y * b.y;
-    acc.y += a.x * b.y - a.y * b.x;
+  constexpr int U = kKrylovChunk / kT;
+  double2 a[U], b[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int64_t i = i0 + u * kT + threadIdx.x;
+    a[u] = i < n ? v[i] : make_double2(0.0, 0.0);
+    b[u] = i < n ? ww[i] : make_double2(0.0, 0.0);
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    acc.x += a[u].x * b[u].x + a[u].y * b[u].y;
+    acc.y += a[u].x * b[u].y - a[u].y * b[u].x;
   }
   double2 r = block_reduce(acc, sm);
   if (threadIdx.x == 0) part[((size_t)s * mp1 + k) * nchunk + c] = r;
@@ -102,17 +123,149 @@ __global__ void __launch_bounds__(kT) dots_kernel(const double2* __restrict__ V,
     finish_sums(part, s, nvec, nchunk, mp1, mp2, mode, slot, h, h2);
 }
 
+// dst[s][i] = src[s][i] / h[s][slot]   (slot = norm); zero if the norm is 0
+// With `publish` (host-mapped pinned word), block (0, 0) first copies the live mask there.
+__global__ void scale_kernel(const double2* __restrict__ src, int64_t ldv, int64_t n, int mp2, int slot,
+                             uint64_t active, const unsigned long long* __restrict__ dmask,
+                             const double2* __restrict__ h, double2* __restrict__ dst,
+                             volatile unsigned long long* publish) {
+  const int s = blockIdx.y;
+  if (publish && blockIdx.x == 0 && s == 0 && threadIdx.x == 0) {
+    *publish = *dmask;
+    __threadfence_system();
+  }
+  if (!sys_on(active, dmask, s)) return;
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double nv = h[(size_t)s * mp2 + slot].x;
+  double2 v = src[(size_t)s * ldv + i];
+  dst[(size_t)s * ldv + i] = nv > 0 ? make_double2(v.x / nv, v.y / nv) : make_double2(0.0, 0.0);
+}
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ double2 cjmul(double2 a, double2 b) {  // conj(a) * b
+  return make_double2(a.x * b.x + a.y * b.y, a.x * b.y - a.y * b.x);
+}
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 cdiv(double2 a, double2 b) {
+  const double d = b.x * b.x + b.y * b.y;
+  return make_double2((a.x * b.x + a.y * b.y) / d, (a.y * b.x - a.x * b.y) / d);
+}
+
+// beta = ||b|| (h[s][0]), gamma_0 = beta, k = 0; systems with b = 0 are done (x = 0,
+// S:281), a non-finite norm is flagged.
+__global__ void gm_init_kernel(int nsys, int mp1, int mp2, const double2* __restrict__ h, double2* __restrict__ gam,
+                               DevSys* __restrict__ sys, unsigned long long* __restrict__ mask) {
+  __shared__ unsigned long long bits;
+  const int q = threadIdx.x;
+  if (q == 0) bits = 0ull;
+  __syncthreads();
+  if (q < nsys) {
+    const double beta = h[(size_t)q * mp2].x;
+    DevSys S{beta, 0, 0};
+    gam[(size_t)q * mp1] = make_double2(beta, 0.0);
+    if (!isfinite(beta))
+      S.flags = kSysNonFinite;
+    else if (beta == 0.0)
+      S.flags = kSysConverged;
+    else
+      atomicOr(&bits, 1ull << q);
+    sys[q] = S;
+  }
+  __syncthreads();
+  if (q == 0) *mask = bits;
+}
+
+// Givens state of the batched solve (device pointers) for the fused update kernel.
+struct GivensArgs {
+  int j, m, mp1, mp2;
+  double tol;
+  const double2* h;
+  double2 *H, *cs, *sn, *gam;
+  DevSys* sys;
+  unsigned long long* mask;
+};
+
+// Arnoldi column j of system q, run by one whole block: apply the previous rotations,
+// form the new one, update gamma and decide convergence (|gamma_{j+1}| <= tol beta, or
+// breakdown) or the iteration cap; the mask bit is cleared when the system stops.  The
+// column and the rotations are staged in shared memory (gsm: mp1 + 2m entries); one
+// thread runs the sequential rotation chain.
+__device__ void givens_block(const GivensArgs& g, int q, double2* gsm) {
+  const int j = g.j, m = g.m, mp1 = g.mp1, tid = threadIdx.x, nt = blockDim.x;
+  double2* col = gsm;
+  double2* sc = gsm + mp1;
+  double2* ss = sc + m;
+  const double2* hq = g.h + (size_t)q * g.mp2;
+  double2* c = g.cs + (size_t)q * m;
+  double2* s = g.sn + (size_t)q * m;
+  for (int i = tid; i <= j + 1; i += nt) col[i] = __ldcg(&hq[i]);
+  for (int i = tid; i < j; i += nt) {
+    sc[i] = c[i];
+    ss[i] = s[i];
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double2* gm = g.gam + (size_t)q * mp1;
+    DevSys S = g.sys[q];
+    S.k = j + 1;
+    const double nrm = col[j + 1].x;
+    if (!isfinite(nrm)) {
+      S.flags |= kSysNonFinite;
+      g.sys[q] = S;
+      atomicAnd(g.mask, ~(1ull << q));
+    } else {
+      const bool breakdown = nrm == 0.0;
+      for (int i = 0; i < j; ++i) {
+        const double2 hi = col[i], hi1 = col[i + 1];
+        col[i] = cadd(cjmul(sc[i], hi), cjmul(ss[i], hi1));
+        const double2 t = cmul(ss[i], hi);
+        col[i + 1] = cadd(make_double2(-t.x, -t.y), cmul(sc[i], hi1));
+      }
+      const double2 a = col[j], bb = col[j + 1];
+      const double den = sqrt((a.x * a.x + a.y * a.y) + (bb.x * bb.x + bb.y * bb.y));
+      double2 cj = make_double2(1.0, 0.0), sj = make_double2(0.0, 0.0);
+      if (den != 0.0) {
+        cj = make_double2(a.x / den, a.y / den);
+        sj = make_double2(bb.x / den, bb.y / den);
+      }
+      c[j] = cj;
+      s[j] = sj;
+      col[j] = cadd(cjmul(cj, a), cjmul(sj, bb));
+      col[j + 1] = make_double2(0.0, 0.0);
+      const double2 gj = gm[j];
+      const double2 t = cmul(sj, gj);
+      const double2 g1 = make_double2(-t.x, -t.y);
+      gm[j + 1] = g1;
+      gm[j] = cjmul(cj, gj);
+      const bool stop_conv = hypot(g1.x, g1.y) <= g.tol * S.beta || breakdown;
+      if (stop_conv) S.flags |= kSysConverged;
+      g.sys[q] = S;
+      if (stop_conv || j + 1 == m) atomicAnd(g.mask, ~(1ull << q));
+    }
+  }
+  __syncthreads();
+  double2* Hc = g.H + ((size_t)q * m + j) * mp1;
+  for (int i = tid; i <= j + 1; i += nt) Hc[i] = col[i];
+}
+
 // w[s][i] -= sum_{k < nvec} h2[s][k] V_k[s][i]; with norm_slot >= 0 also
-// h[s][norm_slot] = ||w[s]|| (block partials, last block sums them in fixed order).
+// h[s][norm_slot] = ||w[s]|| (block partials, last block sums them in fixed order), and
+// with `giv` that last block then runs the Givens step of system s (dynamic smem).
 __global__ void __launch_bounds__(kT) update_kernel(const double2* __restrict__ V, size_t vstride_k, int64_t ldv,
                                                    int64_t n, int nvec, int mp2, uint64_t active,
+                                                   const unsigned long long* __restrict__ dmask,
                                                    const double2* __restrict__ h2, double2* __restrict__ w,
                                                    int norm_slot, double2* __restrict__ h,
-                                                   double2* __restrict__ npart, unsigned* __restrict__ cnt) {
+                                                   double2* __restrict__ npart, unsigned* __restrict__ cnt,
+                                                   bool giv, GivensArgs ga) {
+  extern __shared__ double2 gsm[];
   __shared__ double2 sm[kT / 32];
   __shared__ bool flag;
   const int s = blockIdx.y;
-  if (!((active >> s) & 1ull)) return;
+  if (!sys_on(active, dmask, s)) return;
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   double2 o = make_double2(0.0, 0.0);
   if (i < n) {
@@ -130,31 +283,63 @@ __global__ void __launch_bounds__(kT) update_kernel(const double2* __restrict__ 
   if (norm_slot < 0) return;
   const double2 r = block_reduce(make_double2(o.x * o.x + o.y * o.y, 0.0), sm);
   if (threadIdx.x == 0) npart[(size_t)s * gridDim.x + blockIdx.x] = r;
-  if (last_block(&cnt[s], gridDim.x, &flag) && threadIdx.x == 0) {
-    double t = 0.0;
-    for (unsigned b = 0; b < gridDim.x; ++b) t += __ldcg(&npart[(size_t)s * gridDim.x + b]).x;
-    h[(size_t)s * mp2 + norm_slot] = make_double2(sqrt(t), 0.0);
+  if (last_block(&cnt[s], gridDim.x, &flag)) {
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (unsigned b = 0; b < gridDim.x; ++b) t += __ldcg(&npart[(size_t)s * gridDim.x + b]).x;
+      h[(size_t)s * mp2 + norm_slot] = make_double2(sqrt(t), 0.0);
+    }
+    if (giv) {
+      __syncthreads();
+      givens_block(ga, s, gsm);
+    }
   }
 }
 
-// dst[s][i] = src[s][i] / h[s][slot]   (slot = norm); zero if the norm is 0
-__global__ void scale_kernel(const double2* __restrict__ src, int64_t ldv, int64_t n, int mp2, int slot,
-                             uint64_t active, const double2* __restrict__ h, double2* __restrict__ dst) {
-  const int s = blockIdx.y;
-  if (!((active >> s) & 1ull)) return;
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  double nv = h[(size_t)s * mp2 + slot].x;
-  double2 v = src[(size_t)s * ldv + i];
-  dst[(size_t)s * ldv + i] = nv > 0 ? make_double2(v.x / nv, v.y / nv) : make_double2(0.0, 0.0);
+// y = R^{-1} gamma (k x k upper triangle of the rotated Hessenberg matrix), one block
+// per system, column-oriented: y_i = r_i / R_ii, then r_t -= R_ti y_i for t < i in
+// parallel.  The triangle is staged in shared memory (packed by columns) when it fits.
+constexpr int kBackT = 256;
+constexpr int kBackSmemMax = 200 * 1024;
+__global__ void __launch_bounds__(kBackT) backsolve_kernel(int m, int mp1, const double2* __restrict__ H,
+                                                           const double2* __restrict__ gam,
+                                                           const DevSys* __restrict__ sys,
+                                                           double2* __restrict__ y, int smem_bytes) {
+  extern __shared__ double2 bsm[];  // r[m], y[m], packed triangle (staged)
+  const int q = blockIdx.x, tid = threadIdx.x;
+  const int k = (sys[q].flags & kSysNonFinite) ? 0 : sys[q].k;
+  const double2* Hq = H + (size_t)q * m * mp1;
+  double2* r = bsm;
+  double2* yy = bsm + m;
+  double2* tri = bsm + 2 * m;
+  const bool staged = sizeof(double2) * (2 * (size_t)m + (size_t)k * (k + 1) / 2) <= (size_t)smem_bytes;
+  for (int i = tid; i < k; i += kBackT) r[i] = gam[(size_t)q * mp1 + i];
+  if (staged)
+    for (int i = 0; i < k; ++i)
+      for (int t = tid; t <= i; t += kBackT) tri[i * (i + 1) / 2 + t] = Hq[(size_t)i * mp1 + t];
+  __syncthreads();
+  for (int i = k - 1; i >= 0; --i) {
+    if (tid == 0) yy[i] = cdiv(r[i], staged ? tri[i * (i + 1) / 2 + i] : Hq[(size_t)i * mp1 + i]);
+    __syncthreads();
+    const double2 yi = yy[i];
+    for (int t = tid; t < i; t += kBackT) {
+      const double2 hv = staged ? tri[i * (i + 1) / 2 + t] : Hq[(size_t)i * mp1 + t];
+      const double2 p = cmul(hv, yi);
+      r[t] = make_double2(r[t].x - p.x, r[t].y - p.y);
+    }
+    __syncthreads();
+  }
+  for (int i = tid; i < k; i += kBackT) y[(size_t)q * m + i] = yy[i];
 }
 
-// x[s][i] = sum_{k < kmax} y[s][k] V_k[s][i]
-__global__ void combine_kernel(const double2* __restrict__ V, size_t vstride_k, int64_t ldv, int64_t n,
-                               int kmax, int m, const double2* __restrict__ y, double2* __restrict__ x) {
+// x[s][i] = sum_{k < k_s} y[s][k] V_k[s][i]
+__global__ void combine_kernel(const double2* __restrict__ V, size_t vstride_k, int64_t ldv, int64_t n, int m,
+                               const double2* __restrict__ y, const DevSys* __restrict__ sys,
+                               double2* __restrict__ x) {
   const int s = blockIdx.y;
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
+  const int kmax = (sys[s].flags & kSysNonFinite) ? 0 : sys[s].k;
   double2 acc = make_double2(0.0, 0.0);
   for (int k = 0; k < kmax; ++k) {
     double2 c = y[(size_t)s * m + k];
@@ -173,16 +358,45 @@ __global__ void sub_kernel(const double2* __restrict__ b, int64_t ldv, int64_t n
   w[(size_t)s * ldv + i] = make_double2(a.x - c.x, a.y - c.y);
 }
 
-using cplx = std::complex<double>;
-
-struct SysState {
-  std::vector<cplx> H, cs, sn, gam;  // H column-major (m+1) x m
-  double beta = 0;
-  int k = 0;
-  bool done = false, converged = false;
+// Per-thread, per-device host resources: a pinned ring for the convergence mask and
+// its events, plus reusable timing events.
+struct HostSync {
+  unsigned long long* ring = nullptr;      // pinned, host-mapped
+  unsigned long long* ring_dev = nullptr;  // its device alias
+  cudaEvent_t ev[kRing] = {};
+  std::vector<cudaEvent_t> timing[2];
 };
 
+HostSync* host_sync() {
+  thread_local std::map<int, HostSync> per_dev;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  HostSync& h = per_dev[dev];
+  if (!h.ring) {
+    if (cudaHostAlloc(&h.ring, sizeof(unsigned long long) * kRing, cudaHostAllocMapped) != cudaSuccess ||
+        cudaHostGetDevicePointer(&h.ring_dev, h.ring, 0) != cudaSuccess) {
+      h.ring = nullptr;
+      return nullptr;
+    }
+    for (auto& e : h.ev)
+      if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+  }
+  return &h;
+}
+
 }  // namespace
+
+cudaEvent_t timing_event(int slot, size_t i) {
+  HostSync* h = host_sync();
+  if (!h) return nullptr;
+  auto& v = h->timing[slot];
+  while (v.size() <= i) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+    v.push_back(e);
+  }
+  return v[i];
+}
 
 size_t krylov_workspace(int nsys, int64_t n, int64_t ldv, int max_iter, Carver& c, KrylovWs* w) {
   const int m = max_iter;
@@ -195,6 +409,12 @@ size_t krylov_workspace(int nsys, int64_t n, int64_t ldv, int max_iter, Carver& 
   t.h2 = c.take<double2>((size_t)nsys * (m + 2));
   t.y = c.take<double2>((size_t)nsys * m);
   t.npart = c.take<double2>((size_t)nsys * ((n + kT - 1) / kT));
+  t.H = c.take<double2>((size_t)nsys * m * (m + 1));
+  t.cs = c.take<double2>((size_t)nsys * m);
+  t.sn = c.take<double2>((size_t)nsys * m);
+  t.gam = c.take<double2>((size_t)nsys * (m + 1));
+  t.sys = c.take<DevSys>(nsys);
+  t.mask = c.take<unsigned long long>(1);
   t.cnt = c.take<unsigned>(2 * 64);
   if (w) *w = t;
   return c.bytes();
@@ -209,146 +429,123 @@ nat_status gmres_batched(int nsys, int64_t n, int64_t ldv, const double2* b, dou
   const size_t vstride = (size_t)nsys * ldv;
   const unsigned gx = (unsigned)((n + kT - 1) / kT);
   const uint64_t all = nsys == 64 ? ~0ull : ((1ull << nsys) - 1);
-  double t_op = 0;  // device time of the operator (CUDA events), if requested
-  struct Events {
-    cudaEvent_t e[2] = {nullptr, nullptr};
-    ~Events() {
-      for (auto x : e)
-        if (x) cudaEventDestroy(x);
-    }
-  } evs;
-  cudaEvent_t* ev = evs.e;
-  if (t_op_s) {
-    NAT_CUDA_TRY(cudaEventCreate(&ev[0]));
-    NAT_CUDA_TRY(cudaEventCreate(&ev[1]));
-  }
+  const size_t gsmem = sizeof(double2) * (mp1 + 2 * (size_t)m);
+  if (gsmem > (size_t)kBackSmemMax) return fail(NAT_ERR_INVALID_ARG, "max_iter %d too large", m);
+  if (gsmem > 48 * 1024)
+    NAT_CUDA_TRY(cudaFuncSetAttribute(update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsmem));
+  HostSync* hs = host_sync();
+  if (!hs) return fail(NAT_ERR_CUDA, "pinned host ring / events: %s", cudaGetErrorString(cudaGetLastError()));
   res.assign(nsys, KrylovResult{0, 1, 0.0});
-  std::vector<SysState> st(nsys);
-  std::vector<double2> hbuf((size_t)nsys * mp2);
 
   NAT_CUDA_TRY(cudaMemsetAsync(ws.cnt, 0, sizeof(unsigned) * 2 * 64, s));
   // dots of nvec basis vectors (or of w with itself) with w, reduced into h / h2
-  auto dots = [&](const double2* Vb, size_t vs, const double2* w, int nvec, uint64_t act, int mode, int slot) {
-    dots_kernel<<<dim3(nchunk, nvec, nsys), kT, 0, s>>>(Vb, vs, ldv, w, n, nvec, nchunk, mp1, act, ws.part, mp2,
+  auto dots = [&](const double2* Vb, size_t vs, const double2* w, int nvec, const unsigned long long* dm, int mode,
+                  int slot) {
+    dots_kernel<<<dim3(nchunk, nvec, nsys), kT, 0, s>>>(Vb, vs, ldv, w, n, nvec, nchunk, mp1, all, dm, ws.part, mp2,
                                                        mode, slot, ws.h, ws.h2, ws.cnt);
   };
   // beta = ||b||, V0 = b / beta
-  dots(b, 0, b, 1, all, 2, 0);
-  NAT_LAUNCH_CHECK();
-  NAT_CUDA_TRY(cudaMemcpyAsync(hbuf.data(), ws.h, sizeof(double2) * nsys * mp2, cudaMemcpyDeviceToHost, s));
-  NAT_CUDA_TRY(cudaStreamSynchronize(s));
-  uint64_t active = 0;
-  for (int q = 0; q < nsys; ++q) {
-    double beta = hbuf[(size_t)q * mp2].x;
-    if (!std::isfinite(beta)) return fail(NAT_ERR_NUMERIC, "non-finite right-hand side (system %d)", q);
-    st[q].beta = beta;
-    st[q].H.assign((size_t)mp1 * m, 0.0);
-    st[q].cs.assign(m, 0.0);
-    st[q].sn.assign(m, 0.0);
-    st[q].gam.assign(mp1, 0.0);
-    st[q].gam[0] = beta;
-    if (beta == 0.0) {
-      st[q].done = st[q].converged = true;
-    } else {
-      active |= 1ull << q;
-    }
-  }
-  scale_kernel<<<dim3(gx, nsys), kT, 0, s>>>(b, ldv, n, mp2, 0, active, ws.h, ws.V);
+  dots(b, 0, b, 1, nullptr, 2, 0);
+  gm_init_kernel<<<1, 64, 0, s>>>(nsys, mp1, mp2, ws.h, ws.gam, ws.sys, ws.mask);
+  scale_kernel<<<dim3(gx, nsys), kT, 0, s>>>(b, ldv, n, mp2, 0, all, ws.mask, ws.h, ws.V, nullptr);
   NAT_LAUNCH_CHECK();
 
-  for (int j = 0; j < m && active; ++j) {
+  GivensArgs ga{0, m, mp1, mp2, tol, ws.h, ws.H, ws.cs, ws.sn, ws.gam, ws.sys, ws.mask};
+  int n_timed = 0;
+  auto enqueue = [&](int j, uint64_t host_active) -> nat_status {
     double2* Vj = ws.V + (size_t)j * vstride;
-    if (t_op_s) NAT_CUDA_TRY(cudaEventRecord(ev[0], s));
-    nat_status stt = op(Vj, ws.w, active, s);
-    if (stt != NAT_OK) return stt;
-    if (t_op_s) NAT_CUDA_TRY(cudaEventRecord(ev[1], s));
-    for (int pass = 0; pass < 2; ++pass) {  // CGS2; the second update also forms ||w||
-      dots(ws.V, vstride, ws.w, j + 1, active, pass, 0);
-      update_kernel<<<dim3(gx, nsys), kT, 0, s>>>(ws.V, vstride, ldv, n, j + 1, mp2, active, ws.h2, ws.w,
-                                                  pass == 1 ? j + 1 : -1, ws.h, ws.npart, ws.cnt + 64);
-    }
-    scale_kernel<<<dim3(gx, nsys), kT, 0, s>>>(ws.w, ldv, n, mp2, j + 1, active, ws.h,
-                                               ws.V + (size_t)(j + 1) * vstride);
-    NAT_LAUNCH_CHECK();
-    NAT_CUDA_TRY(cudaMemcpy2DAsync(hbuf.data(), sizeof(double2) * mp2, ws.h, sizeof(double2) * mp2,
-                                   sizeof(double2) * (j + 2), nsys, cudaMemcpyDeviceToHost, s));
-    NAT_CUDA_TRY(cudaStreamSynchronize(s));
     if (t_op_s) {
-      float ms = 0.f;
-      NAT_CUDA_TRY(cudaEventElapsedTime(&ms, ev[0], ev[1]));
-      t_op += 1e-3 * ms;
+      cudaEvent_t e0 = timing_event(0, 2 * j), e1 = timing_event(0, 2 * j + 1);
+      if (!e0 || !e1) return fail(NAT_ERR_CUDA, "timing events");
+      NAT_CUDA_TRY(cudaEventRecord(e0, s));
+      nat_status stt = op(Vj, ws.w, host_active, ws.mask, s);
+      if (stt != NAT_OK) return stt;
+      NAT_CUDA_TRY(cudaEventRecord(e1, s));
+      n_timed = j + 1;
+    } else {
+      nat_status stt = op(Vj, ws.w, host_active, ws.mask, s);
+      if (stt != NAT_OK) return stt;
     }
-    for (int q = 0; q < nsys; ++q) {
-      if (!((active >> q) & 1ull)) continue;
-      SysState& S = st[q];
-      cplx* col = &S.H[(size_t)j * mp1];
-      for (int i = 0; i <= j + 1; ++i) col[i] = cplx(hbuf[(size_t)q * mp2 + i].x, hbuf[(size_t)q * mp2 + i].y);
-      if (!std::isfinite(col[j + 1].real()))
-        return fail(NAT_ERR_NUMERIC, "non-finite Arnoldi norm (system %d, iteration %d)", q, j);
-      const bool breakdown = col[j + 1] == 0.0;
-      for (int i = 0; i < j; ++i) {
-        cplx hi = col[i], hi1 = col[i + 1];
-        col[i] = std::conj(S.cs[i]) * hi + std::conj(S.sn[i]) * hi1;
-        col[i + 1] = -S.sn[i] * hi + S.cs[i] * hi1;
-      }
-      cplx a = col[j], bb = col[j + 1];
-      double den = std::sqrt(std::norm(a) + std::norm(bb));
-      if (den != 0) {
-        S.cs[j] = a / den;
-        S.sn[j] = bb / den;
-      } else {
-        S.cs[j] = 1.0;
-        S.sn[j] = 0.0;
-      }
-      col[j] = std::conj(S.cs[j]) * a + std::conj(S.sn[j]) * bb;
-      col[j + 1] = 0.0;
-      S.gam[j + 1] = -S.sn[j] * S.gam[j];
-      S.gam[j] = std::conj(S.cs[j]) * S.gam[j];
-      S.k = j + 1;
-      if (std::abs(S.gam[j + 1]) <= tol * S.beta || breakdown) {
-        S.done = S.converged = true;
-        active &= ~(1ull << q);
-      } else if (j + 1 == m) {
-        S.done = true;
-        active &= ~(1ull << q);
-      }
+    for (int pass = 0; pass < 2; ++pass) {  // CGS2; the second update also forms ||w||
+      dots(ws.V, vstride, ws.w, j + 1, ws.mask, pass, 0);
+      ga.j = j;
+      update_kernel<<<dim3(gx, nsys), kT, pass == 1 ? gsmem : 0, s>>>(
+          ws.V, vstride, ldv, n, j + 1, mp2, all, ws.mask, ws.h2, ws.w, pass == 1 ? j + 1 : -1, ws.h, ws.npart,
+          ws.cnt + 64, pass == 1, ga);
     }
+    scale_kernel<<<dim3(gx, nsys), kT, 0, s>>>(ws.w, ldv, n, mp2, j + 1, all, ws.mask, ws.h,
+                                               ws.V + (size_t)(j + 1) * vstride, hs->ring_dev + j % kRing);
+    NAT_LAUNCH_CHECK();
+    NAT_CUDA_TRY(cudaEventRecord(hs->ev[j % kRing], s));
+    return NAT_OK;
+  };
+  // Iteration j is enqueued with the mask read back after iteration j-2; the host then
+  // waits for iteration j-1 while the GPU runs iteration j.
+  if (m > 0) {
+    nat_status stt = enqueue(0, all);
+    if (stt != NAT_OK) return stt;
+    uint64_t known = all;
+    static const bool dbg = std::getenv("NAT_DEBUG_GMRES") != nullptr;
+    double t_enq = 0, t_wait = 0;
+    int j = 1;
+    for (; j < m; ++j) {
+      auto c0 = std::chrono::steady_clock::now();
+      stt = enqueue(j, known);
+      if (stt != NAT_OK) return stt;
+      auto c1 = std::chrono::steady_clock::now();
+      NAT_CUDA_TRY(cudaEventSynchronize(hs->ev[(j - 1) % kRing]));
+      auto c2 = std::chrono::steady_clock::now();
+      t_enq += std::chrono::duration<double>(c1 - c0).count();
+      t_wait += std::chrono::duration<double>(c2 - c1).count();
+      known = *(volatile unsigned long long*)&hs->ring[(j - 1) % kRing];
+      if (!known) break;
+    }
+    if (dbg)
+      std::fprintf(stderr, "[gmres] nsys=%d n=%lld iters<=%d host enqueue %.1f us/it, wait %.1f us/it\n", nsys,
+                   (long long)n, j, 1e6 * t_enq / j, 1e6 * t_wait / j);
   }
-  // back-substitution on the host, x = V y on the device
-  std::vector<double2> yh((size_t)nsys * m, make_double2(0.0, 0.0));
-  int kmax = 0;
-  for (int q = 0; q < nsys; ++q) {
-    SysState& S = st[q];
-    int k = S.k;
-    kmax = std::max(kmax, k);
-    std::vector<cplx> yy(k);
-    for (int i = k - 1; i >= 0; --i) {
-      cplx acc = S.gam[i];
-      for (int l = i + 1; l < k; ++l) acc -= S.H[(size_t)l * mp1 + i] * yy[l];
-      yy[i] = acc / S.H[(size_t)i * mp1 + i];
-    }
-    for (int i = 0; i < k; ++i) yh[(size_t)q * m + i] = make_double2(yy[i].real(), yy[i].imag());
+  {
+    // the kernel stages the triangle when k(k+1)/2 entries fit next to r and y
+    const size_t base = sizeof(double2) * 2 * (size_t)m;
+    if (base > (size_t)kBackSmemMax) return fail(NAT_ERR_INVALID_ARG, "max_iter %d too large", m);
+    const size_t smem = std::min(base + sizeof(double2) * (size_t)m * (m + 1) / 2, (size_t)kBackSmemMax);
+    if (smem > 48 * 1024)
+      NAT_CUDA_TRY(cudaFuncSetAttribute(backsolve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    backsolve_kernel<<<nsys, kBackT, smem, s>>>(m, mp1, ws.H, ws.gam, ws.sys, ws.y, (int)smem);
   }
-  if (m > 0)
-    NAT_CUDA_TRY(cudaMemcpyAsync(ws.y, yh.data(), sizeof(double2) * nsys * m, cudaMemcpyHostToDevice, s));
-  combine_kernel<<<dim3(gx, nsys), kT, 0, s>>>(ws.V, vstride, ldv, n, kmax, m, ws.y, x);
+  combine_kernel<<<dim3(gx, nsys), kT, 0, s>>>(ws.V, vstride, ldv, n, m, ws.y, ws.sys, x);
   NAT_LAUNCH_CHECK();
   // true residual ||b - A x|| / beta
-  nat_status stt = op(x, ws.w, all, s);
+  nat_status stt = op(x, ws.w, all, nullptr, s);
   if (stt != NAT_OK) return stt;
   sub_kernel<<<dim3(gx, nsys), kT, 0, s>>>(b, ldv, n, ws.w);
-  dots(ws.w, 0, ws.w, 1, all, 2, 0);
+  dots(ws.w, 0, ws.w, 1, nullptr, 2, 0);
   NAT_LAUNCH_CHECK();
+  std::vector<double2> hbuf((size_t)nsys * mp2);
+  std::vector<DevSys> sys(nsys);
   NAT_CUDA_TRY(cudaMemcpyAsync(hbuf.data(), ws.h, sizeof(double2) * nsys * mp2, cudaMemcpyDeviceToHost, s));
+  NAT_CUDA_TRY(cudaMemcpyAsync(sys.data(), ws.sys, sizeof(DevSys) * nsys, cudaMemcpyDeviceToHost, s));
   NAT_CUDA_TRY(cudaStreamSynchronize(s));
   for (int q = 0; q < nsys; ++q) {
-    double rn = hbuf[(size_t)q * mp2].x;
+    if (sys[q].flags & kSysNonFinite) {
+      if (sys[q].k == 0) return fail(NAT_ERR_NUMERIC, "non-finite right-hand side (system %d)", q);
+      return fail(NAT_ERR_NUMERIC, "non-finite Arnoldi norm (system %d, iteration %d)", q, sys[q].k - 1);
+    }
+    const double rn = hbuf[(size_t)q * mp2].x;
     if (!std::isfinite(rn)) return fail(NAT_ERR_NUMERIC, "non-finite residual (system %d)", q);
-    res[q].iters = st[q].k;
-    res[q].converged = st[q].converged ? 1 : 0;
-    res[q].rel_residual = st[q].beta > 0 ? rn / st[q].beta : 0.0;
+    res[q].iters = sys[q].k;
+    res[q].converged = (sys[q].flags & kSysConverged) ? 1 : 0;
+    res[q].rel_residual = sys[q].beta > 0 ? rn / sys[q].beta : 0.0;
   }
-  if (t_op_s) *t_op_s = t_op;
+  if (t_op_s) {
+    double t = 0;
+    for (int j = 0; j < n_timed; ++j) {
+      float ms = 0.f;
+      NAT_CUDA_TRY(cudaEventElapsedTime(&ms, timing_event(0, 2 * j), timing_event(0, 2 * j + 1)));
+      t += 1e-3 * ms;
+    }
+    *t_op_s = t;
+  }
   return NAT_OK;
 }
 
@@ -427,7 +624,7 @@ extern "C" nat_status nat_bem_solve(nat_comm* comm, nat_prec prec, int64_t n, in
   if (ws_bytes < need) return nat::fail(NAT_ERR_WORKSPACE, "workspace %zu < %zu", ws_bytes, need);
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t rows = row_end - row_begin;
-  double t_comm = 0;
+  int n_comm = 0;
   // gather b
   NAT_CUDA_TRY(cudaMemsetAsync(bfull, 0, sizeof(double2) * L.ldv, s));
   NAT_CUDA_TRY(cudaMemcpyAsync(bfull + rb, b_local, sizeof(double2) * rows, cudaMemcpyDeviceToDevice, s));
@@ -435,13 +632,19 @@ extern "C" nat_status nat_bem_solve(nat_comm* comm, nat_prec prec, int64_t n, in
     nat_status st = nat::allgather_inplace(comm, (double*)bfull, (size_t)L.rpr * 2, s);
     if (st != NAT_OK) return st;
   }
-  auto op = [&](const double2* in, double2* out, uint64_t, cudaStream_t ss) -> nat_status {
-    nat_status st = nat::matvec_internal(prec, rows, n, A_local, lda, in, out + rb, ss);
+  auto op = [&](const double2* in, double2* out, uint64_t, const unsigned long long* dmask,
+                cudaStream_t ss) -> nat_status {
+    nat_status st = nat::matvec_internal(prec, rows, n, A_local, lda, in, out + rb, ss, dmask);
     if (st != NAT_OK) return st;
-    if (L.world > 1) {
-      auto t0 = std::chrono::steady_clock::now();
+    if (L.world > 1) {  // every rank enqueues the same iterations (replicated, deterministic mask)
+      cudaEvent_t e0 = info ? nat::timing_event(1, 2 * n_comm) : nullptr;
+      cudaEvent_t e1 = info ? nat::timing_event(1, 2 * n_comm + 1) : nullptr;
+      if (e0 && e1) NAT_CUDA_TRY(cudaEventRecord(e0, ss));
       st = nat::allgather_inplace(comm, (double*)out, (size_t)L.rpr * 2, ss);
-      t_comm += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      if (e0 && e1) {
+        NAT_CUDA_TRY(cudaEventRecord(e1, ss));
+        ++n_comm;
+      }
     }
     return st;
   };
@@ -452,6 +655,12 @@ extern "C" nat_status nat_bem_solve(nat_comm* comm, nat_prec prec, int64_t n, in
   if (st != NAT_OK) return st;
   NAT_CUDA_TRY(cudaMemcpyAsync(x, xfull, sizeof(double2) * n, cudaMemcpyDeviceToDevice, s));
   NAT_CUDA_TRY(cudaStreamSynchronize(s));
+  double t_comm = 0;
+  for (int c = 0; c < n_comm; ++c) {
+    float ms = 0.f;
+    NAT_CUDA_TRY(cudaEventElapsedTime(&ms, nat::timing_event(1, 2 * c), nat::timing_event(1, 2 * c + 1)));
+    t_comm += 1e-3 * ms;
+  }
   if (info) {
     info->iters = res[0].iters;
     info->converged = res[0].converged;

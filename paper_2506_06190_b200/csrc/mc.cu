@@ -9,6 +9,7 @@
 // GMRES engine (krylov.cuh).  a9/a10 reuse the radiation kernel with targets = sources
 // (TMA-staged source tiles, self pair excluded exactly).
 #include <chrono>
+#include <algorithm>
 #include <cmath>
 #include <vector>
 
@@ -286,17 +287,24 @@ __global__ void mc_finish_kernel(int nsys, int64_t M, const double* __restrict__
                                  const int32_t* __restrict__ rp, const int32_t* __restrict__ col, KArr ka,
                                  double w, const double2* __restrict__ part, int n_split,
                                  const double2* __restrict__ p, const double2* __restrict__ g, double eps,
-                                 double2* __restrict__ out) {
+                                 double2* __restrict__ out, const unsigned long long* __restrict__ skip) {
+  if (skip && *skip == 0ull) return;
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int s = blockIdx.y;
   if (i >= M) return;
   const size_t q = (size_t)s * M + i;
   const size_t stride = (size_t)nsys * M;
   double ar = 0.0, ai = 0.0;
-  for (int sp = 0; sp < n_split; ++sp) {
-    const double2 v = part[sp * stride + q];
-    ar += v.x;
-    ai += v.y;
+  // split order is fixed; loads issued 8 at a time (latency, not bandwidth, bound)
+  for (int sp0 = 0; sp0 < n_split; sp0 += 8) {
+    double2 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = sp0 + u < n_split ? part[(sp0 + u) * stride + q] : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      ar += v[u].x;
+      ai += v[u].y;
+    }
   }
   if (rp) {
     const double k = ka.k[s];
@@ -409,7 +417,8 @@ nat_status finish_op(const nat::RadInput& in, nat_prec prec, int64_t M, const do
   KArr ka{};
   for (int q = 0; q < nsys && q < 64; ++q) ka.k[q] = k[q];
   mc_finish_kernel<<<dim3((unsigned)((M + 255) / 256), nsys), 256, 0, s>>>(
-      nsys, M, smp, np.on ? np.rp : nullptr, np.on ? np.col : nullptr, ka, w, keep.part, keep.n_split, p, g, eps, out);
+      nsys, M, smp, np.on ? np.rp : nullptr, np.on ? np.col : nullptr, ka, w, keep.part, keep.n_split, p, g, eps, out,
+      in.skip);
   NAT_LAUNCH_CHECK();
   return NAT_OK;
 }
@@ -427,11 +436,13 @@ nat_status mc_rhs_impl(nat_prec prec, int64_t M, const double* smp, int nsys, co
 
 nat_status mc_apply_impl(nat_prec prec, int64_t M, const double* smp, int nsys, const double* k,
                          const double2* p, double w, double2* out, void* ws, size_t ws_bytes,
-                         const double* center, const NearPairs& np, cudaStream_t s) {
+                         const double* center, const NearPairs& np, cudaStream_t s,
+                         const unsigned long long* skip = nullptr) {
   nat::RadInput in = self_input(M, smp, nsys, w);
   if (center)
     for (int d = 0; d < 3; ++d) in.center[d] = center[d];
   in.p = p;
+  in.skip = skip;
   in.self_r2 = np.on ? np.thr : 0.f;
   return finish_op(in, prec, M, smp, nsys, k, w, 0.0, p, nullptr, out, ws, ws_bytes, np, s);
 }
@@ -505,7 +516,7 @@ extern "C" nat_status nat_mc_gather_neumann(int n_sys, int64_t M, int64_t n_tri,
 extern "C" size_t nat_mc_op_workspace(nat_prec prec, int64_t M, int n_sys) {
   nat::Carver c(nullptr);
   carve_near(c, nullptr, M);
-  c.take<char>(nat::radiate_ws_bytes(prec, M, n_sys, M));
+  c.take<char>(std::max(nat::radiate_ws_bytes(prec, M, n_sys, M, 1), nat::radiate_ws_bytes(prec, M, n_sys, M, 2)));
   return c.bytes();
 }
 
@@ -515,7 +526,7 @@ nat_status op_setup(nat_prec prec, int64_t M, int n_sys, const double* smp, doub
                     NearPairs& np, void** rad, size_t* rad_bytes, cudaStream_t s) {
   nat::Carver c(ws);
   carve_near(c, &np, M);
-  *rad_bytes = nat::radiate_ws_bytes(prec, M, n_sys, M);
+  *rad_bytes = std::max(nat::radiate_ws_bytes(prec, M, n_sys, M, 1), nat::radiate_ws_bytes(prec, M, n_sys, M, 2));
   *rad = c.take<char>(*rad_bytes);
   if (ws_bytes < c.bytes()) return nat::fail(NAT_ERR_WORKSPACE, "workspace %zu < %zu", ws_bytes, c.bytes());
   if (prec == NAT_FP32 && eps > 0) return build_near(np, M, smp, nullptr, eps, s);
@@ -695,9 +706,11 @@ extern "C" nat_status nat_mc_surface_pressure(const nat_mesh* mesh, const nat_ge
     st = mc_rhs_impl(prec, M, samples_out, nb, k + s0, w.gs, wgt, eps, w.b, w.rad, w.rad_bytes, cen, w.np, s);
     if (st != NAT_OK) return st;
     const uint64_t all = nb == 64 ? ~0ull : ((1ull << nb) - 1);
-    auto op = [&](const double2* in, double2* out, uint64_t active, cudaStream_t ss) -> nat_status {
+    auto op = [&](const double2* in, double2* out, uint64_t active, const unsigned long long* dmask,
+                  cudaStream_t ss) -> nat_status {
       if ((active & all) == all)
-        return mc_apply_impl(prec, M, samples_out, nb, k + s0, in, wgt, out, w.rad, w.rad_bytes, cen, w.np, ss);
+        return mc_apply_impl(prec, M, samples_out, nb, k + s0, in, wgt, out, w.rad, w.rad_bytes, cen, w.np, ss,
+                             dmask);
       // only the systems still iterating: gather them, apply, scatter back
       RowIdx ix{};
       double kc[64];
@@ -711,7 +724,7 @@ extern "C" nat_status nat_mc_surface_pressure(const nat_mesh* mesh, const nat_ge
       const dim3 g2((unsigned)((M + 255) / 256), na);
       copy_rows_kernel<<<g2, 256, 0, ss>>>(ix, M, in, w.tin, true);
       nat_status r = mc_apply_impl(prec, M, samples_out, na, kc, w.tin, wgt, w.tout, w.rad, w.rad_bytes, cen,
-                                   w.np, ss);
+                                   w.np, ss, dmask);
       if (r != NAT_OK) return r;
       copy_rows_kernel<<<g2, 256, 0, ss>>>(ix, M, w.tout, out, false);
       NAT_LAUNCH_CHECK();

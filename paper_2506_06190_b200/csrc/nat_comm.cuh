@@ -12,5 +12,5 @@ struct nat_comm {
 namespace nat {
 nat_status allgather_inplace(nat_comm* comm, double* buf, size_t count, cudaStream_t s);
 nat_status matvec_internal(nat_prec prec, int64_t rows, int64_t n, const void* A, int64_t lda,
-                           const void* x, void* y, cudaStream_t s);
+                           const void* x, void* y, cudaStream_t s, const unsigned long long* skip = nullptr);
 }  // namespace nat

@@ -39,6 +39,17 @@ struct KVals {
   double d[kMaxModes];
 };
 
+// Kernel kinds: 0 = radiation (G and dG/dn_y, no self exclusion), 1 = MC operator
+// (double layer only, self/close pairs excluded), 2 = MC right-hand side (single layer
+// only, self/close pairs excluded).  Record per source (each float duplicated for the
+// FP32x2 pipe): kind 0: x y z nx ny nz | A1 A2 A3 A4 B1 B2 per mode;  kind 1: x y z nx ny nz |
+// A1 A2 A3 A4;  kind 2: x y z | B1 B2.  Padded to a multiple of 4 floats (16-byte loads).
+__host__ __device__ constexpr int rec_geo(int kind) { return kind == 2 ? 3 : 6; }
+__host__ __device__ constexpr int rec_per_mode(int kind) { return kind == 0 ? 6 : kind == 1 ? 4 : 2; }
+__host__ __device__ constexpr int rec_nf(int kind, int MB) {  // duplicated floats
+  return (2 * (rec_geo(kind) + rec_per_mode(kind) * MB) + 3) / 4 * 4;
+}
+
 struct RadParams {
   const void* rec;      // [n_mchunk][n_src_pad][NF] records
   int64_t n_src_pad;    // multiple of the tile
@@ -51,6 +62,7 @@ struct RadParams {
   double2* out;         // [n_split][n_modes][n_lis]
   int n_modes;
   float self_r2;        // SELF mode threshold (see radiate.cuh)
+  const unsigned long long* skip;  // see RadInput::skip
 };
 
 // ------------------------------------------------------------------------------------
@@ -70,15 +82,26 @@ struct RecWriter {
   }
 };
 
+// One CTA stages kStageSrc consecutive sources: each thread builds its record in shared
+// memory, then the CTA writes the contiguous block with coalesced 16-byte stores.
+constexpr int kStageSrc = 128;
+constexpr int kStageMaxBytes = 64 * 4;  // per source: <= 64 floats (fp32) or 32 doubles
+
 template <typename T, bool DUP = false>
-__global__ void stage_kernel(int64_t n_src, int64_t n_src_pad, int NF, int MB, int n_mchunk,
+__global__ void __launch_bounds__(kStageSrc) stage_kernel(int64_t n_src, int64_t n_src_pad, int NF, int MB,
+                                                         int n_mchunk, int kind,
                              const double* __restrict__ xyz, const double* __restrict__ nrm,
                              const double* __restrict__ w, double w_const,
                              const double2* __restrict__ p, const double2* __restrict__ g,
                              int64_t ldpg, const KVals kv, int n_modes, double cx,
-                             double cy, double cz, T* __restrict__ rec) {
-  int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (s >= n_src_pad) return;
+                             double cy, double cz, T* __restrict__ rec,
+                             const unsigned long long* __restrict__ skip) {
+  if (skip && *skip == 0ull) return;
+  __shared__ __align__(16) unsigned char sbuf[kStageSrc * kStageMaxBytes];
+  T* sm = reinterpret_cast<T*>(sbuf);
+  const int64_t s0 = (int64_t)blockIdx.x * kStageSrc;
+  const int64_t s = s0 + threadIdx.x;
+  const int nblk = (int)nat::min64(kStageSrc, n_src_pad - s0);
   double x, y, z, nx, ny, nz, ws;
   if (s < n_src) {
     x = xyz[s] - cx;
@@ -95,35 +118,54 @@ __global__ void stage_kernel(int64_t n_src, int64_t n_src_pad, int NF, int MB, i
     ws = 0.0;
   }
   for (int c = 0; c < n_mchunk; ++c) {
-    T* r = rec + ((size_t)c * n_src_pad + s) * NF;
-    const RecWriter<T, DUP> wr{r};
-    wr.put(0, x);
-    wr.put(1, y);
-    wr.put(2, z);
-    wr.put(3, nx);
-    wr.put(4, ny);
-    wr.put(5, nz);
-    for (int m = 0; m < MB; ++m) {
-      int mode = c * MB + m;
-      double ar = 0, ai = 0, br = 0, bi = 0, k = 0;
-      if (mode < n_modes && ws != 0.0) {
-        double2 pv = p ? p[(size_t)mode * ldpg + s] : make_double2(0.0, 0.0);
-        double2 gv = g ? g[(size_t)mode * ldpg + s] : make_double2(0.0, 0.0);
-        ar = ws * pv.x;
-        ai = ws * pv.y;
-        br = ws * gv.x;
-        bi = ws * gv.y;
-        k = kv.d[mode];
+    if (threadIdx.x < nblk) {
+      T* r = sm + (size_t)threadIdx.x * NF;
+      const RecWriter<T, DUP> wr{r};
+      wr.put(0, x);
+      wr.put(1, y);
+      wr.put(2, z);
+      if (kind != 2) {
+        wr.put(3, nx);
+        wr.put(4, ny);
+        wr.put(5, nz);
       }
-      const int q = 6 + 6 * m;
-      wr.put(q + 0, -ar);
-      wr.put(q + 1, -k * ai);
-      wr.put(q + 2, k * ar);
-      wr.put(q + 3, -ai);
-      wr.put(q + 4, -br);
-      wr.put(q + 5, -bi);
+      const int G = rec_geo(kind), F = rec_per_mode(kind);
+      for (int m = 0; m < MB; ++m) {
+        int mode = c * MB + m;
+        double ar = 0, ai = 0, br = 0, bi = 0, k = 0;
+        if (mode < n_modes && ws != 0.0) {
+          double2 pv = p ? p[(size_t)mode * ldpg + s] : make_double2(0.0, 0.0);
+          double2 gv = g ? g[(size_t)mode * ldpg + s] : make_double2(0.0, 0.0);
+          ar = ws * pv.x;
+          ai = ws * pv.y;
+          br = ws * gv.x;
+          bi = ws * gv.y;
+          k = kv.d[mode];
+        }
+        const int q = G + F * m;
+        if (kind != 2) {
+          wr.put(q + 0, -ar);
+          wr.put(q + 1, -k * ai);
+          wr.put(q + 2, k * ar);
+          wr.put(q + 3, -ai);
+        }
+        if (kind == 0) {
+          wr.put(q + 4, -br);
+          wr.put(q + 5, -bi);
+        } else if (kind == 2) {
+          wr.put(q + 0, -br);
+          wr.put(q + 1, -bi);
+        }
+      }
+      for (int f = (DUP ? 2 : 1) * (G + F * MB); f < NF; ++f) r[f] = (T)0;
     }
-    for (int f = (DUP ? 2 : 1) * (6 + 6 * MB); f < NF; ++f) r[f] = (T)0;
+    __syncthreads();
+    // NF * sizeof(T) is a multiple of 16 bytes (rec_nf pads to 4 floats; fp64 NF = 12)
+    const float4* src4 = reinterpret_cast<const float4*>(sm);
+    float4* dst4 = reinterpret_cast<float4*>(rec + ((size_t)c * n_src_pad + s0) * NF);
+    const int nvec = (int)((size_t)nblk * NF * sizeof(T) / 16);
+    for (int v = threadIdx.x; v < nvec; v += kStageSrc) dst4[v] = src4[v];
+    __syncthreads();
   }
 }
 
@@ -142,24 +184,30 @@ __device__ __forceinline__ float rsqrt_approx(float x) {
 // (x x y y z z nx nx ...) so a packed operand is one half of an LDS.128 broadcast.
 // Per pair: 12.5 FP32-pipe instructions + 3 MUFU (rsqrt, sin, cos) instead of 24 + 3.
 // ------------------------------------------------------------------------------------
-template <int MB>
+template <int MB, int KIND>
 struct Rec2 {
-  static constexpr int NF = 12 + 12 * MB;  // duplicated floats per source record
+  static constexpr int NF = rec_nf(KIND, MB);
 };
 
-// SELF = 1: targets coincide with the sources (MC operators): pairs with fp32 r^2 <= self_r2
-// (the self pair, d = 0 exactly, and the close pairs evaluated in fp64 by the caller) get
-// 1/r = 0, i.e. contribute exactly 0.  NT = threads per CTA (256, or 128 for fine grids).
-template <int R, int MB, int SELF, int NT>
+// KIND 1, 2 (SELF): targets coincide with the sources (MC operators): pairs with fp32
+// r^2 <= self_r2 (the self pair, d = 0 exactly, and the close pairs evaluated in fp64 by
+// the caller) get 1/r = 0, i.e. contribute exactly 0.  NT = threads per CTA (256, or 128
+// for fine grids).
+template <int R, int MB, int KIND, int NT>
 __global__ void __launch_bounds__(NT) radiate_f32x2_kernel(RadParams prm) {
   static_assert(R % 2 == 0, "targets are processed in pairs");
   constexpr int RP = R / 2;
-  constexpr int NF = Rec2<MB>::NF;
+  constexpr bool SELF = KIND != 0;
+  constexpr int NF = Rec2<MB, KIND>::NF;
+  constexpr int G = rec_geo(KIND), F = rec_per_mode(KIND);
+  // short bodies keep cos/sin products in four accumulators (no negation per pair)
+  constexpr bool ACC4 = RP * MB <= 2;
   constexpr int kTileFloats = kTile * NF;
   extern __shared__ __align__(128) unsigned char smem[];
   float* buf = reinterpret_cast<float*>(smem);
   double2* dacc = reinterpret_cast<double2*>(smem + 2 * kTileFloats * sizeof(float));
   __shared__ __align__(8) uint64_t bars[2];
+  if (prm.skip && *prm.skip == 0ull) return;
 
   const int tid = threadIdx.x;
   const int64_t tbase = (int64_t)blockIdx.x * (R * NT);
@@ -214,11 +262,11 @@ __global__ void __launch_bounds__(NT) radiate_f32x2_kernel(RadParams prm) {
     const int st = it & 1;
     nat::mbar_wait(&bars[st], (it >> 1) & 1);
     const ulonglong2* b4 = reinterpret_cast<const ulonglong2*>(buf + st * kTileFloats);
-    f2r ar[RP][MB], ai[RP][MB];
+    f2r ar[RP][MB], ai[RP][MB], br[RP][MB], bi[RP][MB];  // br / bi: ACC4 only
 #pragma unroll
     for (int p = 0; p < RP; ++p)
 #pragma unroll
-      for (int m = 0; m < MB; ++m) ar[p][m] = ai[p][m] = 0ull;
+      for (int m = 0; m < MB; ++m) ar[p][m] = ai[p][m] = br[p][m] = bi[p][m] = 0ull;
 
     // short bodies (one target pair, one wavenumber) need a deeper unroll so the
     // shared-memory loads of later sources overlap the arithmetic (ncu r01: LDS-wait)
@@ -238,12 +286,15 @@ __global__ void __launch_bounds__(NT) radiate_f32x2_kernel(RadParams prm) {
         const f2r dy = f2sub(f[1], ty[p]);
         const f2r dz = f2sub(f[2], tz[p]);
         const f2r r2 = f2fma(dz, dz, f2fma(dy, dy, f2mul(dx, dx)));
-        const f2r dn = f2fma(dz, f[5], f2fma(dy, f[4], f2mul(dx, f[3])));
         const float r2a = f2lo(r2), r2b = f2hi(r2);
         const float ra = SELF ? (r2a > prm.self_r2 ? rsqrt_approx(r2a) : 0.f) : rsqrt_approx(r2a);
         const float rb = SELF ? (r2b > prm.self_r2 ? rsqrt_approx(r2b) : 0.f) : rsqrt_approx(r2b);
         const f2r rho = f2pack(ra, rb);
-        const f2r qq = f2mul(dn, f2mul(rho, rho));
+        f2r qq = 0ull;
+        if constexpr (KIND != 2) {
+          const f2r dn = f2fma(dz, f[5], f2fma(dy, f[4], f2mul(dx, f[3])));
+          qq = f2mul(dn, f2mul(rho, rho));
+        }
         const f2r rr = f2mul(r2, rho);
 #pragma unroll
         for (int m = 0; m < MB; ++m) {
@@ -252,12 +303,28 @@ __global__ void __launch_bounds__(NT) radiate_f32x2_kernel(RadParams prm) {
           __sincosf(f2lo(kr), &sa, &ca);
           __sincosf(f2hi(kr), &sb, &cb);
           const f2r sn = f2pack(sa, sb), cs = f2pack(ca, cb);
-          const f2r* c = f + 6 + 6 * m;  // A1 A2 A3 A4 B1 B2 (pairs)
-          const f2r cr = f2fma(qq, f2fma(rho, c[0], c[1]), f2mul(rho, c[4]));
-          const f2r ci = f2fma(qq, f2fma(rho, c[3], c[2]), f2mul(rho, c[5]));
-          const f2r nci = f2mul(ci, minus1);
-          ar[p][m] = f2fma(cs, cr, f2fma(sn, nci, ar[p][m]));
-          ai[p][m] = f2fma(sn, cr, f2fma(cs, ci, ai[p][m]));
+          const f2r* c = f + G + F * m;  // kind 0: A1 A2 A3 A4 B1 B2; 1: A1..A4; 2: B1 B2
+          f2r cr, ci;
+          if constexpr (KIND == 0) {
+            cr = f2fma(qq, f2fma(rho, c[0], c[1]), f2mul(rho, c[4]));
+            ci = f2fma(qq, f2fma(rho, c[3], c[2]), f2mul(rho, c[5]));
+          } else if constexpr (KIND == 1) {
+            cr = f2mul(qq, f2fma(rho, c[0], c[1]));
+            ci = f2mul(qq, f2fma(rho, c[3], c[2]));
+          } else {
+            cr = f2mul(rho, c[0]);
+            ci = f2mul(rho, c[1]);
+          }
+          if constexpr (ACC4) {  // (ar - br) + i (ai + bi)
+            ar[p][m] = f2fma(cs, cr, ar[p][m]);
+            br[p][m] = f2fma(sn, ci, br[p][m]);
+            ai[p][m] = f2fma(sn, cr, ai[p][m]);
+            bi[p][m] = f2fma(cs, ci, bi[p][m]);
+          } else {
+            const f2r nci = f2mul(ci, minus1);
+            ar[p][m] = f2fma(cs, cr, f2fma(sn, nci, ar[p][m]));
+            ai[p][m] = f2fma(sn, cr, f2fma(cs, ci, ai[p][m]));
+          }
         }
       }
     }
@@ -267,10 +334,17 @@ __global__ void __launch_bounds__(NT) radiate_f32x2_kernel(RadParams prm) {
       for (int m = 0; m < MB; ++m) {
         const int q0 = (2 * p) * MB + m, q1 = (2 * p + 1) * MB + m;
         double2 d0 = dacc[q0 * NT + tid], d1 = dacc[q1 * NT + tid];
-        d0.x += (double)f2lo(ar[p][m]);
-        d0.y += (double)f2lo(ai[p][m]);
-        d1.x += (double)f2hi(ar[p][m]);
-        d1.y += (double)f2hi(ai[p][m]);
+        if constexpr (ACC4) {
+          d0.x += (double)f2lo(ar[p][m]) - (double)f2lo(br[p][m]);
+          d0.y += (double)f2lo(ai[p][m]) + (double)f2lo(bi[p][m]);
+          d1.x += (double)f2hi(ar[p][m]) - (double)f2hi(br[p][m]);
+          d1.y += (double)f2hi(ai[p][m]) + (double)f2hi(bi[p][m]);
+        } else {
+          d0.x += (double)f2lo(ar[p][m]);
+          d0.y += (double)f2lo(ai[p][m]);
+          d1.x += (double)f2hi(ar[p][m]);
+          d1.y += (double)f2hi(ai[p][m]);
+        }
         dacc[q0 * NT + tid] = d0;
         dacc[q1 * NT + tid] = d1;
       }
@@ -305,6 +379,7 @@ __global__ void __launch_bounds__(kThreads) radiate_f64_kernel(RadParams prm) {
   extern __shared__ __align__(128) unsigned char smem[];
   double* buf = reinterpret_cast<double*>(smem);
   __shared__ __align__(8) uint64_t bars[2];
+  if (prm.skip && *prm.skip == 0ull) return;
   const int tid = threadIdx.x;
   const int64_t tbase = (int64_t)blockIdx.x * (R * kThreads);
   const int split = blockIdx.y, mch = blockIdx.z;
@@ -438,6 +513,7 @@ __global__ void mc_sources_kernel(int64_t M, const double* __restrict__ smp, dou
 // host side
 // ------------------------------------------------------------------------------------
 struct Plan {
+  int kind;  // record / kernel kind (fp32 only; see rec_geo)
   int MB, R, NF, n_mchunk, tile, n_tiles, chunk_tiles, n_split;
   int64_t n_src_pad, tgt_tiles;
   size_t rec_elems, smem;
@@ -453,10 +529,10 @@ int pick_mb(int n_modes) {
   return 1;
 }
 
-template <int R, int MB, int NT>
+template <int R, int MB, int KIND, int NT>
 int occ_of(size_t smem) {
   int occ = 0;
-  auto k = radiate_f32x2_kernel<R, MB, 0, NT>;
+  auto k = radiate_f32x2_kernel<R, MB, KIND, NT>;
   if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, NT, smem) != cudaSuccess) {
     cudaGetLastError();
@@ -465,16 +541,20 @@ int occ_of(size_t smem) {
   return occ > 0 ? occ : 1;
 }
 
-template <int R, int NT>
+template <int R, int KIND, int NT>
 int occ_mb(int MB, size_t smem) {
-  return MB == 1 ? occ_of<R, 1, NT>(smem) : MB == 2 ? occ_of<R, 2, NT>(smem)
-       : MB == 3 ? occ_of<R, 3, NT>(smem) : occ_of<R, 4, NT>(smem);
+  return MB == 1 ? occ_of<R, 1, KIND, NT>(smem) : MB == 2 ? occ_of<R, 2, KIND, NT>(smem)
+       : MB == 3 ? occ_of<R, 3, KIND, NT>(smem) : occ_of<R, 4, KIND, NT>(smem);
+}
+template <int R, int NT>
+int occ_kind(int kind, int MB, size_t smem) {
+  return kind == 0 ? occ_mb<R, 0, NT>(MB, smem) : kind == 1 ? occ_mb<R, 1, NT>(MB, smem) : occ_mb<R, 2, NT>(MB, smem);
 }
 
 // Resident CTAs per SM of the radiation kernel instance (cached per configuration).
-int occupancy(bool fp64, int R, int MB, int NT, size_t smem) {
-  static int cache[2][5][5][2];  // [fp64][R][MB][NT == 128], 0 = unknown
-  int& c = cache[fp64 ? 1 : 0][R][MB][NT == 128 ? 1 : 0];
+int occupancy(bool fp64, int kind, int R, int MB, int NT, size_t smem) {
+  static int cache[2][3][5][5][2];  // [fp64][kind][R][MB][NT == 128], 0 = unknown
+  int& c = cache[fp64 ? 1 : 0][fp64 ? 0 : kind][R][MB][NT == 128 ? 1 : 0];
   if (c) return c;
   if (fp64) {
     int occ = 0;
@@ -486,16 +566,17 @@ int occupancy(bool fp64, int R, int MB, int NT, size_t smem) {
     }
     c = occ > 0 ? occ : 1;
   } else if (NT == 128) {
-    c = R == 2 ? occ_mb<2, 128>(MB, smem) : occ_mb<4, 128>(MB, smem);
+    c = R == 2 ? occ_kind<2, 128>(kind, MB, smem) : occ_kind<4, 128>(kind, MB, smem);
   } else {
-    c = R == 2 ? occ_mb<2, 256>(MB, smem) : occ_mb<4, 256>(MB, smem);
+    c = R == 2 ? occ_kind<2, 256>(kind, MB, smem) : occ_kind<4, 256>(kind, MB, smem);
   }
   return c;
 }
 
-Plan make_plan(nat_prec prec, int64_t n_src, int n_modes, int64_t n_lis) {
+Plan make_plan(nat_prec prec, int64_t n_src, int n_modes, int64_t n_lis, int kind) {
   Plan pl{};
   pl.fp64 = (prec == NAT_FP64);
+  pl.kind = pl.fp64 ? 0 : kind;
   if (pl.fp64) {
     pl.MB = 1;
     pl.R = 2;
@@ -504,7 +585,7 @@ Plan make_plan(nat_prec prec, int64_t n_src, int n_modes, int64_t n_lis) {
   } else {
     pl.MB = pick_mb(n_modes);
     pl.R = 4;
-    pl.NF = 12 + 12 * pl.MB;  // duplicated records of the FP32x2 kernel
+    pl.NF = rec_nf(pl.kind, pl.MB);  // duplicated records of the FP32x2 kernel
     pl.tile = kTile;
   }
   pl.NT = kThreads;
@@ -522,7 +603,7 @@ Plan make_plan(nat_prec prec, int64_t n_src, int n_modes, int64_t n_lis) {
       const int NT = pl.fp64 ? kThreads : nt_opts[ni];
       const size_t smem = pl.fp64 ? 2 * (size_t)kTile64 * 12 * sizeof(double)
                                   : 2 * (size_t)kTile * pl.NF * sizeof(float) + (size_t)R * pl.MB * NT * 16;
-      const int occ = occupancy(pl.fp64, R, pl.MB, NT, smem);
+      const int occ = occupancy(pl.fp64, pl.kind, R, pl.MB, NT, smem);
       const int64_t tgt = (n_lis + (int64_t)R * NT - 1) / ((int64_t)R * NT);
       const int64_t base = tgt * pl.n_mchunk;
       const int tile = pl.fp64 ? kTile64 : kTile;
@@ -577,9 +658,9 @@ size_t plan_ws(const Plan& pl, int n_modes, int64_t n_lis, nat::Carver& c, void*
   return c.bytes();
 }
 
-template <int R, int MB, int SELF, int NT>
+template <int R, int MB, int KIND, int NT>
 cudaError_t launch_f32(const Plan& pl, const RadParams& prm, cudaStream_t s) {
-  auto kern = radiate_f32x2_kernel<R, MB, SELF, NT>;
+  auto kern = radiate_f32x2_kernel<R, MB, KIND, NT>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
   if (e != cudaSuccess) return e;
   dim3 grid((unsigned)pl.tgt_tiles, (unsigned)pl.n_split, (unsigned)pl.n_mchunk);
@@ -587,31 +668,31 @@ cudaError_t launch_f32(const Plan& pl, const RadParams& prm, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-template <int R, int SELF, int NT>
+template <int R, int KIND, int NT>
 cudaError_t launch_f32_r(const Plan& pl, const RadParams& prm, cudaStream_t s) {
   switch (pl.MB) {
-    case 1: return launch_f32<R, 1, SELF, NT>(pl, prm, s);
-    case 2: return launch_f32<R, 2, SELF, NT>(pl, prm, s);
-    case 3: return launch_f32<R, 3, SELF, NT>(pl, prm, s);
-    default: return launch_f32<R, 4, SELF, NT>(pl, prm, s);
+    case 1: return launch_f32<R, 1, KIND, NT>(pl, prm, s);
+    case 2: return launch_f32<R, 2, KIND, NT>(pl, prm, s);
+    case 3: return launch_f32<R, 3, KIND, NT>(pl, prm, s);
+    default: return launch_f32<R, 4, KIND, NT>(pl, prm, s);
   }
 }
 
-template <int SELF>
+template <int KIND>
 cudaError_t launch_f32_mb(const Plan& pl, const RadParams& prm, cudaStream_t s) {
   if (pl.NT == 128)
-    return pl.R == 2 ? launch_f32_r<2, SELF, 128>(pl, prm, s) : launch_f32_r<4, SELF, 128>(pl, prm, s);
-  return pl.R == 2 ? launch_f32_r<2, SELF, 256>(pl, prm, s) : launch_f32_r<4, SELF, 256>(pl, prm, s);
+    return pl.R == 2 ? launch_f32_r<2, KIND, 128>(pl, prm, s) : launch_f32_r<4, KIND, 128>(pl, prm, s);
+  return pl.R == 2 ? launch_f32_r<2, KIND, 256>(pl, prm, s) : launch_f32_r<4, KIND, 256>(pl, prm, s);
 }
 
 }  // namespace
 
 namespace nat {
 
-size_t radiate_ws_bytes(nat_prec prec, int64_t n_src, int n_modes, int64_t n_lis) {
+size_t radiate_ws_bytes(nat_prec prec, int64_t n_src, int n_modes, int64_t n_lis, int kind) {
   if (n_src <= 0 || n_modes <= 0 || n_lis <= 0) return 0;
   const int nm = n_modes < kMaxModes ? n_modes : kMaxModes;
-  Plan pl = make_plan(prec, n_src, nm, n_lis);
+  Plan pl = make_plan(prec, n_src, nm, n_lis, kind);
   Carver c(nullptr);
   void* rec;
   double2* part;
@@ -621,7 +702,7 @@ size_t radiate_ws_bytes(nat_prec prec, int64_t n_src, int n_modes, int64_t n_lis
 size_t radiate_ws_bytes_upto(nat_prec prec, int64_t n_src, int max_modes, int64_t n_lis) {
   size_t b = 0;
   for (int m = 1; m <= (max_modes < kMaxModes ? max_modes : kMaxModes); ++m)
-    b = std::max(b, radiate_ws_bytes(prec, n_src, m, n_lis));
+    for (int kind = 0; kind < 3; ++kind) b = std::max(b, radiate_ws_bytes(prec, n_src, m, n_lis, kind));
   return b;
 }
 
@@ -629,9 +710,12 @@ nat_status radiate_internal(const RadInput& in, nat_prec prec, const double* k, 
                             const double* lis, double2* out, void* ws, size_t ws_bytes, bool self,
                             cudaStream_t s, RadPartials* keep) {
   if (keep && in.n_modes > kMaxModes) return fail(NAT_ERR_INVALID_ARG, "unreduced partials need <= 64 modes");
+  // self-excluding launches are the MC operators: double layer (g absent) or single layer (p absent)
+  if (self && in.p && in.g) return fail(NAT_ERR_INVALID_ARG, "self-excluding radiation needs p or g absent");
+  const int kind = !self ? 0 : (in.p ? 1 : 2);
   for (int m0 = 0; m0 < in.n_modes; m0 += kMaxModes) {
     const int nm = (in.n_modes - m0) < kMaxModes ? (in.n_modes - m0) : kMaxModes;
-    Plan pl = make_plan(prec, in.n_src, nm, n_lis);
+    Plan pl = make_plan(prec, in.n_src, nm, n_lis, kind);
     Carver c(ws);
     void* rec;
     double2* part;
@@ -644,15 +728,15 @@ nat_status radiate_internal(const RadInput& in, nat_prec prec, const double* k, 
     }
     const double2* p = in.p ? in.p + (size_t)m0 * in.ldpg : nullptr;
     const double2* g = in.g ? in.g + (size_t)m0 * in.ldpg : nullptr;
-    unsigned sblocks = (unsigned)((pl.n_src_pad + 255) / 256);
+    unsigned sblocks = (unsigned)((pl.n_src_pad + kStageSrc - 1) / kStageSrc);
     if (pl.fp64)
-      stage_kernel<double><<<sblocks, 256, 0, s>>>(in.n_src, pl.n_src_pad, pl.NF, pl.MB, pl.n_mchunk,
+      stage_kernel<double><<<sblocks, kStageSrc, 0, s>>>(in.n_src, pl.n_src_pad, pl.NF, pl.MB, pl.n_mchunk, 0,
           in.xyz, in.nrm, in.w, in.w_const, p, g, in.ldpg, kv, nm, in.center[0], in.center[1],
-          in.center[2], (double*)rec);
+          in.center[2], (double*)rec, in.skip);
     else
-      stage_kernel<float, true><<<sblocks, 256, 0, s>>>(in.n_src, pl.n_src_pad, pl.NF, pl.MB, pl.n_mchunk,
+      stage_kernel<float, true><<<sblocks, kStageSrc, 0, s>>>(in.n_src, pl.n_src_pad, pl.NF, pl.MB, pl.n_mchunk, pl.kind,
           in.xyz, in.nrm, in.w, in.w_const, p, g, in.ldpg, kv, nm, in.center[0], in.center[1],
-          in.center[2], (float*)rec);
+          in.center[2], (float*)rec, in.skip);
     NAT_LAUNCH_CHECK();
     RadParams prm{};
     prm.rec = rec;
@@ -669,6 +753,7 @@ nat_status radiate_internal(const RadInput& in, nat_prec prec, const double* k, 
     prm.out = pl.n_split > 1 ? part : dst;
     prm.n_modes = nm;
     prm.self_r2 = in.self_r2;
+    prm.skip = in.skip;
     cudaError_t e = cudaSuccess;
     if (pl.fp64) {
       auto kern = radiate_f64_kernel<2>;
@@ -679,7 +764,8 @@ nat_status radiate_internal(const RadInput& in, nat_prec prec, const double* k, 
         e = cudaGetLastError();
       }
     } else {
-      e = self ? launch_f32_mb<1>(pl, prm, s) : launch_f32_mb<0>(pl, prm, s);
+      e = kind == 0 ? launch_f32_mb<0>(pl, prm, s) : kind == 1 ? launch_f32_mb<1>(pl, prm, s)
+                                                   : launch_f32_mb<2>(pl, prm, s);
     }
     if (e != cudaSuccess) return fail(NAT_ERR_CUDA, "radiate launch: %s", cudaGetErrorString(e));
     if (keep) {  // the caller reduces the partials in its own epilogue

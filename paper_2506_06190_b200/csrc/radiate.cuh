@@ -16,9 +16,11 @@ struct RadInput {
   int64_t ldpg;
   double center[3];
   float self_r2;      // self mode: pairs with fp32 r^2 <= self_r2 are skipped (0 => self pair only)
+  const unsigned long long* skip = nullptr;  // device word; when it reads 0 the launches return at once
+                                             // (Krylov driver: every system has converged)
 };
 
-size_t radiate_ws_bytes(nat_prec prec, int64_t n_src, int n_modes, int64_t n_lis);
+size_t radiate_ws_bytes(nat_prec prec, int64_t n_src, int n_modes, int64_t n_lis, int kind = 0);
 // Largest workspace over 1..max_modes wavenumbers (callers that shrink the mode set).
 size_t radiate_ws_bytes_upto(nat_prec prec, int64_t n_src, int max_modes, int64_t n_lis);
 // out[m][l] (c128 [n_modes][n_lis]) = sum_s w_s [p_ms dG_m/dn_y - g_ms G_m](x_l, y_s);

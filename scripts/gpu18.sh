@@ -1,0 +1,14 @@
+python -m paper_2506_06190_b200.build > /dev/null || exit 1
+timeout 1500 python -m pytest -x -q -m gpu tests/ 2>&1 | tail -3
+timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench5.json 2> gpurun_out/bench5.err; echo "bench rc=$?"
+python - <<'P'
+import json; d=json.load(open('gpurun_out/bench5.json'))
+print(d['value'], d['ms_per_step'], d['phase_ms_per_step'], d['gmres_iters'], d['mc_gmres_iters'])
+for k,v in d['rooflines'].items(): print(k, round(v['achieved'],1), round(v['frac'],3))
+P
+NAT_DEBUG_GMRES=1 timeout 600 python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e --no-profile-count 2>&1 >/dev/null | grep gmres | tail -8
+python scripts/timeline.py > gpurun_out/timeline.txt 2>&1
+python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-profile-count > gpurun_out/plain.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches4.csv \
+    python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-profile-count > gpurun_out/ncu_launch.log 2>&1
+echo "launch list rc=$?"
