@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-profile-count", action="store_true")
+    ap.add_argument("--no-overlap", dest="overlap", action="store_false",
+                    help="run the dense-BEM and BEM-MC chains one after the other")
     return ap.parse_args()
 
 
@@ -147,14 +149,19 @@ class Step:
         self.P = P
         self.l0, self.l1 = shard(P, rank, world)
         self.mc_idx = mc_share(len(KAS), rank, world)
+        self.lock = threading.Lock()
         # device-resident inputs and buffers (allocated once, outside the timed region)
         self.mesh = nat.Mesh.from_numpy(m.v, m.t, device=dev)
         self.g = torch.from_numpy(host["g"]).to(dev)            # (1, n) dipole Neumann
         self.g_mc = self.g.expand(len(self.mc_idx), -1).contiguous() if self.mc_idx else None
         rows = self.r1 - self.r0
         self.lda = self.n + (self.n & 1)
-        self.A = torch.empty(rows, self.lda, dtype=torch.complex64, device=dev)
-        self.solve_ws = nat._ws(nat.lib().nat_bem_solve_workspace(nat.NAT_FP32, self.n, rows, 200), dev)
+        # the three ka run one after the other in the dense-BEM chain (one NCCL communicator,
+        # collectives issued in the same order on every rank): one matrix, one workspace
+        A = torch.empty(rows, self.lda, dtype=torch.complex64, device=dev)
+        ws = nat._ws(nat.lib().nat_bem_solve_workspace(nat.NAT_FP32, self.n, rows, 200), dev)
+        self.A = [A] * len(KAS)
+        self.solve_ws = [ws] * len(KAS)
         self.S_bem = 3 * self.n
         self.n_lis = self.l1 - self.l0
         self.rad_plan_bem = nat.RadiatePlan(self.S_bem, len(KAS), self.n_lis, "fp32", dev)
@@ -166,17 +173,30 @@ class Step:
             self.rad_plan_mc = nat.RadiatePlan(M_MC, len(self.mc_idx), self.n_lis, "fp32", dev)
             self.out_mc = torch.empty(len(self.mc_idx), self.n_lis, dtype=torch.complex128, device=dev)
         self.ev = {}
+        self.overlap = True
+        # the MC chain gets the high-priority stream: its FP32/MUFU-bound launches run at full
+        # rate while the dense-BEM chains (HBM-bound GEMV) fill the remaining issue slots
+        prio = os.environ.get("NAT_BENCH_PRIO", "mc")
+        self.s_bem = torch.cuda.Stream(priority=-1 if prio == "bem" else 0)
+        self.s_mc = torch.cuda.Stream(priority=-1 if prio == "mc" else 0)
 
-    def _ev(self, name):
+    def _ev(self, name, tag=""):
+        """Event on the current stream; `tag` keeps the start/end events of concurrent
+        chains apart (phase spans pair events with the same tag)."""
         e = self.torch.cuda.Event(enable_timing=True)
         e.record()
-        self.ev.setdefault(name, []).append(e)
+        with self.lock:
+            self.ev.setdefault(name, {}).setdefault(tag, []).append(e)
 
-    def run(self, host_inputs=False):
+    def run(self, host_inputs=False, overlap=None):
         """One step.  host_inputs=True: the step's inputs (mesh, Neumann data) are copied
-        from pinned host memory and the results read back (the e2e measurement)."""
+        from pinned host memory and the results read back (the e2e measurement).
+        overlap=True: the dense-BEM chain (assembly, HBM-bound GEMV solve, radiation) and
+        the BEM-MC chain (FP32/MUFU-bound operators, radiation) run concurrently on two
+        streams from two host threads (the C calls release the GIL), so the compute-bound MC
+        kernels fill the SMs the GEMV leaves idle."""
         nat, torch = self.nat, self.torch
-        t = {}
+        overlap = self.overlap if overlap is None else overlap
         mesh, g = self.mesh, self.g
         if host_inputs:
             hv, ht, hg = self.host["pinned"]
@@ -197,44 +217,42 @@ class Step:
                       mc_op_s=0.0, iters=[], mc_iters=[])
         if not hasattr(self, "nS"):   # class counts for the pair accounting (first step only)
             self.nS = int((near.cls == 1).sum().item())
-        nS, nN = self.nS, near.nnz - self.nS
-        rows = self.r1 - self.r0
-        for q, ka in enumerate(KAS):
-            self._ev("asm0")
-            A, b = nat.nat_bem_assemble(mesh, geo, near, ka, g, prec="fp32", A=self.A, lda=self.lda)  # a4+a5
-            self._ev("asm1")
-            _, info = nat.nat_bem_solve(A, b[0], self.n, self.r0, self.comm, tol=1e-6, max_iter=200,
-                                        ws=self.solve_ws, out=self.x_bem[q])                       # a6+a7
-            self._ev("solve1")
-            counts["far"] += rows * self.n * 3
-            counts["near"] += nS * 448 + nN * 28
-            counts["self"] += rows * 48
-            counts["rad"] += self.S_bem * self.n_lis
-            counts["gemv_bytes"] += info["iters"] * rows * self.lda * 8
-            counts["gemv_s"] += info["t_matvec_s"]
-            counts["iters"].append(info["iters"])
-        # a11: the three solutions radiate in one launch (shared r, 1/r, d.n per pair)
-        src = nat.nat_bem_sources(mesh, geo, self.x_bem, self.g3)
-        self._ev("rad0")
-        nat.nat_radiate_field(src, list(KAS), lis, "fp32", out=self.out_bem, plan=self.rad_plan_bem)
-        self._ev("rad1")
-        if self.mc_idx:
-            ks = [KAS[i] for i in self.mc_idx]
-            self._ev("mc0")
-            smp, stri, p, infos = nat.nat_mc_surface_pressure(mesh, geo, ks, self.g_mc, M_MC, seed=20250606,
-                                                              stream_id=0, prec="fp32", tol=1e-6,
-                                                              plan=self.mc_plan)                    # a8-a10
-            self._ev("mc1")
-            gs = nat.nat_mc_gather_neumann(self.g_mc, stri)
-            src = nat.nat_mc_sources(smp, geo.total_area, p, gs)
-            self._ev("radmc0")
-            nat.nat_radiate_field(src, ks, lis, "fp32", out=self.out_mc, plan=self.rad_plan_mc)          # a11
-            self._ev("radmc1")
-            for inf in infos:
-                counts["mc_rhs"] += M_MC * (M_MC - 1)
-                counts["mc_op"] += inf["iters"] * M_MC * (M_MC - 1)
-                counts["mc_iters"].append(inf["iters"])
-            counts["rad"] += M_MC * self.n_lis * len(ks)
+        if not overlap:
+            for q in range(len(KAS)):
+                self._bem_one(q, geo, near, counts)
+            self._bem_radiate(geo, lis)
+            if self.mc_idx:
+                self._mc_chain(geo, lis, counts)
+        else:
+            cur = torch.cuda.current_stream()
+            ready = torch.cuda.Event()
+            ready.record(cur)
+            err = []
+
+            def worker(stream, fn, *a):
+                try:
+                    with torch.cuda.stream(stream):
+                        stream.wait_event(ready)
+                        fn(*a)
+                except BaseException as ex:  # re-raised on the main thread
+                    err.append(ex)
+
+            def bem_all():
+                for q in range(len(KAS)):
+                    self._bem_one(q, geo, near, counts)
+
+            ths = [threading.Thread(target=worker, args=(self.s_bem, bem_all))]
+            if self.mc_idx:
+                ths.append(threading.Thread(target=worker, args=(self.s_mc, self._mc_chain, geo, lis, counts)))
+            for t in ths:
+                t.start()
+            for t in ths:
+                t.join()
+            if err:
+                raise err[0]
+            cur.wait_stream(self.s_bem)
+            self._bem_radiate(geo, lis)
+            cur.wait_stream(self.s_mc)
         if host_inputs:
             hb, hm = self.host["out_pinned"]
             hb.copy_(self.out_bem, non_blocking=True)
@@ -242,10 +260,62 @@ class Step:
                 hm[: self.out_mc.shape[0]].copy_(self.out_mc, non_blocking=True)
         return counts
 
+    def _bem_one(self, q, geo, near, counts):
+        """a4-a7 for KAS[q] (row-sharded across ranks)."""
+        nat = self.nat
+        mesh, g = self.mesh, self.g
+        nS, nN = self.nS, near.nnz - self.nS
+        rows = self.r1 - self.r0
+        tag = str(q)
+        self._ev("asm0", tag)
+        A, b = nat.nat_bem_assemble(mesh, geo, near, KAS[q], g, prec="fp32", A=self.A[q], lda=self.lda)  # a4+a5
+        self._ev("asm1", tag)
+        _, info = nat.nat_bem_solve(A, b[0], self.n, self.r0, self.comm, tol=1e-6, max_iter=200,
+                                    ws=self.solve_ws[q], out=self.x_bem[q])                       # a6+a7
+        self._ev("solve1", tag)
+        with self.lock:
+            counts["far"] += rows * self.n * 3
+            counts["near"] += nS * 448 + nN * 28
+            counts["self"] += rows * 48
+            counts["rad"] += self.S_bem * self.n_lis
+            counts["gemv_bytes"] += info["iters"] * rows * self.lda * 8
+            counts["gemv_s"] += info["t_matvec_s"]
+            counts["iters"].append((q, info["iters"]))
+
+    def _bem_radiate(self, geo, lis):
+        """a11: the three solutions radiate in one launch (shared r, 1/r, d.n per pair)."""
+        nat = self.nat
+        src = nat.nat_bem_sources(self.mesh, geo, self.x_bem, self.g3)
+        self._ev("rad0")
+        nat.nat_radiate_field(src, list(KAS), lis, "fp32", out=self.out_bem, plan=self.rad_plan_bem)
+        self._ev("rad1")
+
+    def _mc_chain(self, geo, lis, counts):
+        """a8-a10 (batched over the rank's wavenumbers), then a11 of the MC solution."""
+        nat = self.nat
+        ks = [KAS[i] for i in self.mc_idx]
+        self._ev("mc0")
+        smp, stri, p, infos = nat.nat_mc_surface_pressure(self.mesh, geo, ks, self.g_mc, M_MC, seed=20250606,
+                                                          stream_id=0, prec="fp32", tol=1e-6,
+                                                          plan=self.mc_plan)                    # a8-a10
+        self._ev("mc1")
+        gs = nat.nat_mc_gather_neumann(self.g_mc, stri)
+        src = nat.nat_mc_sources(smp, geo.total_area, p, gs)
+        self._ev("radmc0")
+        nat.nat_radiate_field(src, ks, lis, "fp32", out=self.out_mc, plan=self.rad_plan_mc)          # a11
+        self._ev("radmc1")
+        with self.lock:
+            for inf in infos:
+                counts["mc_rhs"] += M_MC * (M_MC - 1)
+                counts["mc_op"] += inf["iters"] * M_MC * (M_MC - 1)
+                counts["mc_iters"].append(inf["iters"])
+            counts["rad"] += M_MC * self.n_lis * len(ks)
+
     def phase_ms(self):
         """Device time per phase, summed over the recorded steps (call after sync)."""
         def span(a, b):
-            return sum(x.elapsed_time(y) for x, y in zip(self.ev.get(a, []), self.ev.get(b, [])))
+            ea, eb = self.ev.get(a, {}), self.ev.get(b, {})
+            return sum(x.elapsed_time(y) for t in ea for x, y in zip(ea[t], eb.get(t, [])))
         return {"geometry+near": span("geom0", "geom1"), "assembly": span("asm0", "asm1"),
                 "bem_solve": span("asm1", "solve1"), "radiate_bem": span("rad0", "rad1"),
                 "mc_solve": span("mc0", "mc1"), "radiate_mc": span("radmc0", "radmc1")}
@@ -373,6 +443,7 @@ def main():
         comm = nat.Comm.from_torch_distributed()
     host = load_host()
     step = Step(nat, torch, rank, world, comm, host)
+    step.overlap = args.overlap
     # pinned host copies for the e2e measurement
     m = host["mesh"]
     hv = torch.from_numpy(np.ascontiguousarray(m.v.T)).pin_memory()
@@ -390,18 +461,21 @@ def main():
 
     for _ in range(max(3, args.warmup)):
         step.run()
+    if args.overlap:
+        step.run(overlap=False)   # the serialised steps below allocate on the default stream
     barrier()
-    step.ev = {}
-    cs = ClockSampler(local)
-    totals, ms_steps = None, []
-    with cs:
+
+    def timed(overlap):
+        """K steps bracketed by barrier + synchronize; returns (ms, totals, phases)."""
+        step.ev = {}
+        totals, ms_steps = None, []
         barrier()
         for _ in range(args.steps):
             flush.fill_(1)   # L2 flush between timed iterations (outside the step events)
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record()
-            c = step.run()
+            c = step.run(overlap=overlap)
             e1.record()
             ms_steps.append((e0, e1))
             if totals is None:
@@ -410,8 +484,14 @@ def main():
                 for k, v in c.items():
                     totals[k] = totals[k] + v
         barrier()
-    ms = sum(a.elapsed_time(b) for a, b in ms_steps)
-    phases = step.phase_ms()
+        return sum(a.elapsed_time(b) for a, b in ms_steps), totals, step.phase_ms()
+
+    cs = ClockSampler(local)
+    with cs:
+        ms, totals, _ = timed(args.overlap)
+    # per-kernel rooflines and phase times come from the same steps with the two chains
+    # serialised (overlapped kernels share the SMs, so their spans would not be per-kernel)
+    ms_seq, totals_seq, phases = timed(False) if args.overlap else (ms, totals, step.phase_ms())
     ms_t = torch.tensor([ms], dtype=torch.float64, device="cuda")
     pairs_t = torch.tensor([float(pairs_of(totals)), float(totals["rad"])], dtype=torch.float64, device="cuda")
     if world > 1:
@@ -459,7 +539,7 @@ def main():
     t_rad = (phases["radiate_bem"] + phases["radiate_mc"]) * 1e-3
     t_asm = phases["assembly"] * 1e-3
     t_mc = phases["mc_solve"] * 1e-3
-    t_gemv = totals["gemv_s"]
+    t_gemv = totals_seq["gemv_s"]
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
     hbm = peaks.get("hbm_gbs", 6650.0)
@@ -477,20 +557,21 @@ def main():
                 "frac_at_measured_clock": (a / (R_PIPE / 1e9) * MAX_MHZ / clk["sm_mhz"]) if clk["sm_mhz"] else None}
 
     roof = {
-        "radiate": alu("radiate_f32x2_kernel", totals["rad"], t_rad),
-        "bem_assembly": alu("far_kernel_x2", totals["far"] + totals["near"] + totals["self"], t_asm),
-        "mc_solve": alu("radiate_f32_kernel<SELF> (MC operator/RHS)", totals["mc_op"] + totals["mc_rhs"], t_mc),
+        "radiate": alu("radiate_f32x2_kernel", totals_seq["rad"], t_rad),
+        "bem_assembly": alu("far_kernel_x2", totals_seq["far"] + totals_seq["near"] + totals_seq["self"], t_asm),
+        "mc_solve": alu("radiate_f32_kernel<SELF> (MC operator/RHS)", totals_seq["mc_op"] + totals_seq["mc_rhs"],
+                        t_mc),
         "gemv": {"kernel": "gemv_c64_kernel", "bound": "hbm",
-                 "achieved": totals["gemv_bytes"] / t_gemv / 1e9 if t_gemv > 0 else 0.0,
+                 "achieved": totals_seq["gemv_bytes"] / t_gemv / 1e9 if t_gemv > 0 else 0.0,
                  "peak": hbm, "unit": "GB/s",
-                 "frac": (totals["gemv_bytes"] / t_gemv / 1e9 / hbm) if t_gemv > 0 else 0.0,
+                 "frac": (totals_seq["gemv_bytes"] / t_gemv / 1e9 / hbm) if t_gemv > 0 else 0.0,
                  "traffic": traffic.get("gemv_c64_kernel"),
                  "peak_note": "measured HBM copy bandwidth, MEASURED_PEAKS.json"},
     }
     share = {"radiate": t_rad, "bem_assembly": t_asm, "mc_solve": t_mc, "gemv": t_gemv}
     dom = max(share, key=share.get)
     roofline = dict(roof[dom])
-    roofline["share_of_step"] = share[dom] / (ms * 1e-3)
+    roofline["share_of_step"] = share[dom] / (ms_seq * 1e-3)
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
@@ -509,7 +590,11 @@ def main():
         "radiate_listener_pts_per_s": (step.n_lis * (len(KAS) + len(step.mc_idx)) * K) / t_rad if t_rad > 0 else None,
         "pairs_per_step": pairs_all / K,
         "phase_ms_per_step": {k: v / K for k, v in phases.items()},
-        "gmres_iters": totals["iters"][: len(KAS)], "mc_gmres_iters": totals["mc_iters"][: len(step.mc_idx)],
+        "phase_note": ("phases and rooflines from K more steps with the two chains serialised "
+                       f"({ms_seq / K:.3f} ms/step); value/ms_per_step from the overlapped steps")
+        if args.overlap else "chains serialised (--no-overlap)",
+        "overlap": bool(args.overlap),
+        "gmres_iters": [it for _, it in sorted(totals["iters"][: len(KAS)])], "mc_gmres_iters": totals["mc_iters"][: len(step.mc_idx)],
         "roofline": roofline, "rooflines": roof,
         "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": (per_step_launch * K) if per_step_launch is not None else None,

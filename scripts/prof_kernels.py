@@ -26,6 +26,8 @@ def main():
         eps, w = nat.mc_weights(geo.total_area, 10000)
         p = torch.ones(3, 10000, dtype=torch.complex128, device="cuda")
         nat.nat_mc_apply(smp, [0.5, 2.0, 8.0], p, w, eps, "fp32")
+        nat.nat_mc_apply(smp, [8.0], p[:1], w, eps, "fp32")
+        nat.nat_mc_rhs(smp, [0.5, 2.0, 8.0], p, w, eps, "fp32")
         torch.cuda.synchronize()
     print("ok")
 
