@@ -211,15 +211,24 @@ class Step:
         lis = nat.nat_listener_grid((0.0, 0.0, 0.0), 1.0, *GRID, device=self.dev)    # a12
         if self.world > 1:
             lis = lis[:, self.l0:self.l1].contiguous()
-        near = nat.nat_bem_near_list(mesh, geo, self.r0, self.r1)                   # a2
         self._ev("geom1")
+        # a2 before the fork: only the dense-BEM chain (the critical path) needs it, and it
+        # runs fastest with the GPU to itself
+        self._ev("near0")
+        near = nat.nat_bem_near_list(mesh, geo, self.r0, self.r1)                   # a2
+        self._ev("near1")
         counts = dict(far=0, near=0, self=0, rad=0, mc_rhs=0, mc_op=0, gemv_bytes=0, gemv_s=0.0,
                       mc_op_s=0.0, iters=[], mc_iters=[])
+
         if not hasattr(self, "nS"):   # class counts for the pair accounting (first step only)
             self.nS = int((near.cls == 1).sum().item())
-        if not overlap:
+
+        def bem_all():
             for q in range(len(KAS)):
                 self._bem_one(q, geo, near, counts)
+
+        if not overlap:
+            bem_all()
             self._bem_radiate(geo, lis)
             if self.mc_idx:
                 self._mc_chain(geo, lis, counts)
@@ -236,10 +245,6 @@ class Step:
                         fn(*a)
                 except BaseException as ex:  # re-raised on the main thread
                     err.append(ex)
-
-            def bem_all():
-                for q in range(len(KAS)):
-                    self._bem_one(q, geo, near, counts)
 
             ths = [threading.Thread(target=worker, args=(self.s_bem, bem_all))]
             if self.mc_idx:
@@ -316,7 +321,8 @@ class Step:
         def span(a, b):
             ea, eb = self.ev.get(a, {}), self.ev.get(b, {})
             return sum(x.elapsed_time(y) for t in ea for x, y in zip(ea[t], eb.get(t, [])))
-        return {"geometry+near": span("geom0", "geom1"), "assembly": span("asm0", "asm1"),
+        return {"geometry": span("geom0", "geom1"), "near_list": span("near0", "near1"),
+                "assembly": span("asm0", "asm1"),
                 "bem_solve": span("asm1", "solve1"), "radiate_bem": span("rad0", "rad1"),
                 "mc_solve": span("mc0", "mc1"), "radiate_mc": span("radmc0", "radmc1")}
 

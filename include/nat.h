@@ -101,14 +101,19 @@ typedef struct {
  * [row_begin, row_end).  Class 1 (S): shares a vertex index; class 2 (N): otherwise
  * |c_i - c_j| < eta diam_j (fp64, strict).  CSR, columns ascending.
  * nat_bem_near_count fills row_ptr[rows+1] (exclusive scan) and returns nnz; it
- * synchronises.  nat_bem_near_build then fills col[nnz], cls[nnz] (async).
+ * synchronises.  nat_bem_near_build then fills col[nnz], cls[nnz] (async).  Both take a
+ * caller-owned device workspace of nat_bem_near_workspace(n_tri) bytes (tile bounding
+ * boxes used to skip far source tiles); NAT_ERR_WORKSPACE when ws_bytes is smaller.
  * ------------------------------------------------------------------------------- */
+size_t nat_bem_near_workspace(int64_t n_tri); /* bytes of ws for count / build (per-tile boxes) */
 nat_status nat_bem_near_count(const nat_mesh* mesh, const nat_geom* geom, const nat_quad_opts* opts,
                               int64_t row_begin, int64_t row_end, int64_t* row_ptr,
-                              int64_t* nnz /* [host] */, nat_stream_t stream); /* (sync) */
+                              int64_t* nnz /* [host] */, void* ws, size_t ws_bytes,
+                              nat_stream_t stream); /* (sync) */
 nat_status nat_bem_near_build(const nat_mesh* mesh, const nat_geom* geom, const nat_quad_opts* opts,
                               int64_t row_begin, int64_t row_end, const int64_t* row_ptr,
-                              int32_t* col, uint8_t* cls, nat_stream_t stream); /* (async) */
+                              int32_t* col, uint8_t* cls, void* ws, size_t ws_bytes,
+                              nat_stream_t stream); /* (async) */
 
 /* ---------------------------------------------------------------------------------
  * a4 + a5 — dense collocation assembly of the conventional BIE (Eq. BM with beta = 0,

@@ -672,26 +672,17 @@ __global__ void class_count_kernel(int64_t rows, const int64_t* __restrict__ rp,
   if (r == 0) cntS[0] = cntN[0] = 0;
 }
 
-// In-place inclusive scan of cnt[1..rows] (cnt[0] = 0), one CTA, fixed segmentation.
-__global__ void __launch_bounds__(1024) scan_i32_kernel(int32_t* cnt, int64_t rows) {
-  __shared__ int64_t part[1024];
+// In-place inclusive scan of cnt[1..rows] (cnt[0] = 0); blockIdx.x selects the array
+// (class S / class N counts, one launch).
+__global__ void __launch_bounds__(1024) scan_i32_kernel(int32_t* cntS, int32_t* cntN, int64_t rows) {
+  __shared__ int64_t sh[33];
+  int32_t* cnt = blockIdx.x == 0 ? cntS : cntN;
   const int t = threadIdx.x;
   const int64_t per = (rows + 1023) / 1024;
   const int64_t b = 1 + t * per, e = nat::min64(rows + 1, b + per);
   int64_t s = 0;
   for (int64_t i = b; i < e; ++i) s += cnt[i];
-  part[t] = s;
-  __syncthreads();
-  if (t == 0) {
-    int64_t acc = 0;
-    for (int q = 0; q < 1024; ++q) {
-      const int64_t v = part[q];
-      part[q] = acc;
-      acc += v;
-    }
-  }
-  __syncthreads();
-  int64_t acc = part[t];
+  int64_t acc = nat::block_exscan_1024(s, sh, nullptr);
   for (int64_t i = b; i < e; ++i) {
     acc += cnt[i];
     cnt[i] = (int32_t)acc;
@@ -997,8 +988,7 @@ nat_status assemble_impl(const nat_mesh* mesh, const nat_geom* geom, const Opts&
   if (nnz > 0) {
     const unsigned rb = (unsigned)((rows + 255) / 256);
     class_count_kernel<<<rb, 256, 0, s>>>(rows, rp, cls, w.cntS, w.cntN);
-    scan_i32_kernel<<<1, 1024, 0, s>>>(w.cntS, rows);
-    scan_i32_kernel<<<1, 1024, 0, s>>>(w.cntN, rows);
+    scan_i32_kernel<<<2, 1024, 0, s>>>(w.cntS, w.cntN, rows);
     class_fill_kernel<<<rb, 256, 0, s>>>(rows, rp, cls, w.cntS, w.cntN, w.listS, w.listN);
     NAT_LAUNCH_CHECK();
     NearArgs<R> na{};

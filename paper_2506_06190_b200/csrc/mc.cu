@@ -122,28 +122,6 @@ __global__ void gather_g_kernel(int nsys, int64_t M, int64_t nt, const double2* 
   gs[(size_t)s * M + j] = g_tri[(size_t)s * nt + stri[j]];
 }
 
-// b = R - (eps/2) g   (disk single-layer term, with the sign of Eq. BM)
-__global__ void rhs_combine_kernel(int nsys, int64_t M, double eps, const double2* __restrict__ g,
-                                   double2* __restrict__ b) {
-  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int s = blockIdx.y;
-  if (j >= M) return;
-  const size_t q = (size_t)s * M + j;
-  const double2 gv = g[q], r = b[q];
-  b[q] = make_double2(r.x - 0.5 * eps * gv.x, r.y - 0.5 * eps * gv.y);
-}
-
-// out = 1/2 p - R   (the disk double-layer term is 0)
-__global__ void apply_combine_kernel(int nsys, int64_t M, const double2* __restrict__ p,
-                                     double2* __restrict__ out) {
-  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int s = blockIdx.y;
-  if (j >= M) return;
-  const size_t q = (size_t)s * M + j;
-  const double2 pv = p[q], r = out[q];
-  out[q] = make_double2(0.5 * pv.x - r.x, 0.5 * pv.y - r.y);
-}
-
 // ---- close sample pairs (fp32 r^2 <= (2 eps)^2): evaluated in fp64 -------------------
 // With random samples some pairs are far closer than the sample spacing; their fp32
 // coordinates (rounded to ~6e-8 |y|) would give O(1e-3) errors in d.n and 1/r.  The fp32
@@ -211,25 +189,15 @@ __global__ void __launch_bounds__(kNT) mc_near_kernel(int64_t M, const double* _
 }
 
 __global__ void __launch_bounds__(1024) scan32_kernel(int32_t* rp, int64_t M, int64_t cap, int* overflow) {
-  __shared__ int64_t part[1024];
+  __shared__ int64_t sh[33];
   const int t = threadIdx.x;
   const int64_t per = (M + 1023) / 1024;
   const int64_t b = 1 + t * per, e = nat::min64(M + 1, b + per);
   int64_t s = 0;
   for (int64_t i = b; i < e; ++i) s += rp[i];
-  part[t] = s;
-  __syncthreads();
-  if (t == 0) {
-    int64_t acc = 0;
-    for (int q = 0; q < 1024; ++q) {
-      int64_t v = part[q];
-      part[q] = acc;
-      acc += v;
-    }
-    if (acc > cap) *overflow = 1;
-  }
-  __syncthreads();
-  int64_t acc = part[t];
+  int64_t total = 0;
+  int64_t acc = nat::block_exscan_1024(s, sh, &total);
+  if (t == 0 && total > cap) *overflow = 1;
   for (int64_t i = b; i < e; ++i) {
     acc += rp[i];
     rp[i] = (int32_t)(acc < cap ? acc : cap);
@@ -243,95 +211,74 @@ struct KArr {
   double k[64];
 };
 
-__global__ void mc_near_apply_kernel(int nsys, int64_t M, const double* __restrict__ smp,
-                                     const int32_t* __restrict__ rp, const int32_t* __restrict__ col,
-                                     KArr ka, double w, const double2* __restrict__ p,
-                                     const double2* __restrict__ g, double2* __restrict__ R) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int s = blockIdx.y;
-  if (i >= M) return;
-  const double k = ka.k[s];
-  const double xi = smp[i], yi = smp[M + i], zi = smp[2 * M + i];
-  double ar = 0.0, ai = 0.0;
-  for (int e = rp[i]; e < rp[i + 1]; ++e) {
-    const int64_t j = col[e];
-    const double dx = smp[j] - xi, dy = smp[M + j] - yi, dz = smp[2 * M + j] - zi;
-    const double r = sqrt(dx * dx + dy * dy + dz * dz);
-    const double dn = dx * smp[3 * M + j] + dy * smp[4 * M + j] + dz * smp[5 * M + j];
-    float snf, csf;  // |kr| < 2 k eps: the fp32 phase is accurate to ~1e-7 absolute
-    __sincosf((float)(k * r), &snf, &csf);
-    const double sn = snf, cs = csf;
-    const double t = w * nat::kInv4Pi / r;  // w G = t e^{ikr}
-    if (p) {  // w p dG/dn_y = t dn/r^2 (ikr - 1) e^{ikr} p
-      const double2 pv = p[(size_t)s * M + j];
-      const double u = t * dn / (r * r);
-      const double er = -cs - k * r * sn, ei = k * r * cs - sn;  // (ikr - 1) e^{ikr}
-      ar += u * (er * pv.x - ei * pv.y);
-      ai += u * (er * pv.y + ei * pv.x);
-    }
-    if (g) {  // - w g G
-      const double2 gv = g[(size_t)s * M + j];
-      ar -= t * (cs * gv.x - sn * gv.y);
-      ai -= t * (cs * gv.y + sn * gv.x);
-    }
-  }
-  const size_t q = (size_t)s * M + i;
-  double2 o = R[q];
-  R[q] = make_double2(o.x + ar, o.y + ai);
-}
-
-// Fused epilogue of the MC operators: sum of the split-K partials (fixed order), the
-// fp64 close-pair contributions (same formula as mc_near_apply_kernel) and the disk /
-// diagonal terms:  apply: out = 1/2 p - R;  rhs: b = R - (eps/2) g.
-__global__ void mc_finish_kernel(int nsys, int64_t M, const double* __restrict__ smp,
-                                 const int32_t* __restrict__ rp, const int32_t* __restrict__ col, KArr ka,
-                                 double w, const double2* __restrict__ part, int n_split,
-                                 const double2* __restrict__ p, const double2* __restrict__ g, double eps,
-                                 double2* __restrict__ out, const unsigned long long* __restrict__ skip) {
+// Fused epilogue of the MC operators: sum of the split-K partials, the fp64 close-pair
+// contributions and the disk / diagonal terms:  apply: out = 1/2 p - R;  rhs:
+// b = R - (eps/2) g.  Eight lanes per output (fixed assignment: lane l takes splits
+// l, l+8, ... and close pairs l, l+8, ...; fixed xor-tree across the lanes).
+constexpr int kFinLanes = 8;
+__global__ void __launch_bounds__(256) mc_finish_kernel(int nsys, int64_t M, const double* __restrict__ smp,
+                                                        const int32_t* __restrict__ rp,
+                                                        const int32_t* __restrict__ col, KArr ka, double w,
+                                                        const double2* part, int n_split,  // may alias out
+                                                        const double2* __restrict__ p,
+                                                        const double2* __restrict__ g, double eps,
+                                                        double2* out,
+                                                        const unsigned long long* __restrict__ skip) {
   if (skip && *skip == 0ull) return;
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int sub = threadIdx.x % kFinLanes;
+  const int64_t i = blockIdx.x * (int64_t)(blockDim.x / kFinLanes) + threadIdx.x / kFinLanes;
   const int s = blockIdx.y;
-  if (i >= M) return;
-  const size_t q = (size_t)s * M + i;
+  const bool valid = i < M;  // whole 8-lane groups
+  const size_t q = (size_t)s * M + (valid ? i : 0);
   const size_t stride = (size_t)nsys * M;
   double ar = 0.0, ai = 0.0;
-  // split order is fixed; loads issued 8 at a time (latency, not bandwidth, bound)
-  for (int sp0 = 0; sp0 < n_split; sp0 += 8) {
-    double2 v[8];
+  if (valid) {
+    for (int sp0 = sub; sp0 < n_split; sp0 += 4 * kFinLanes) {
+      double2 v[4];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) v[u] = sp0 + u < n_split ? part[(sp0 + u) * stride + q] : make_double2(0.0, 0.0);
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      ar += v[u].x;
-      ai += v[u].y;
-    }
-  }
-  if (rp) {
-    const double k = ka.k[s];
-    const double xi = smp[i], yi = smp[M + i], zi = smp[2 * M + i];
-    for (int e = rp[i]; e < rp[i + 1]; ++e) {
-      const int64_t j = col[e];
-      const double dx = smp[j] - xi, dy = smp[M + j] - yi, dz = smp[2 * M + j] - zi;
-      const double r = sqrt(dx * dx + dy * dy + dz * dz);
-      float snf, csf;
-      __sincosf((float)(k * r), &snf, &csf);
-      const double sn = snf, cs = csf;
-      const double t = w * nat::kInv4Pi / r;
-      if (p) {
-        const double dn = dx * smp[3 * M + j] + dy * smp[4 * M + j] + dz * smp[5 * M + j];
-        const double2 pv = p[(size_t)s * M + j];
-        const double u = t * dn / (r * r);
-        const double er = -cs - k * r * sn, ei = k * r * cs - sn;
-        ar += u * (er * pv.x - ei * pv.y);
-        ai += u * (er * pv.y + ei * pv.x);
+      for (int u = 0; u < 4; ++u) {
+        const int sp = sp0 + u * kFinLanes;
+        v[u] = sp < n_split ? part[sp * stride + q] : make_double2(0.0, 0.0);
       }
-      if (g) {
-        const double2 gv = g[(size_t)s * M + j];
-        ar -= t * (cs * gv.x - sn * gv.y);
-        ai -= t * (cs * gv.y + sn * gv.x);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        ar += v[u].x;
+        ai += v[u].y;
       }
     }
+    if (rp) {
+      const double k = ka.k[s];
+      const double xi = smp[i], yi = smp[M + i], zi = smp[2 * M + i];
+      for (int e = rp[i] + sub; e < rp[i + 1]; e += kFinLanes) {
+        const int64_t j = col[e];
+        const double dx = smp[j] - xi, dy = smp[M + j] - yi, dz = smp[2 * M + j] - zi;
+        const double r = sqrt(dx * dx + dy * dy + dz * dz);
+        float snf, csf;  // |kr| < 2 k eps: the fp32 phase is accurate to ~1e-7 absolute
+        __sincosf((float)(k * r), &snf, &csf);
+        const double sn = snf, cs = csf;
+        const double t = w * nat::kInv4Pi / r;  // w G = t e^{ikr}
+        if (p) {  // w p dG/dn_y = t dn/r^2 (ikr - 1) e^{ikr} p
+          const double dn = dx * smp[3 * M + j] + dy * smp[4 * M + j] + dz * smp[5 * M + j];
+          const double2 pv = p[(size_t)s * M + j];
+          const double u = t * dn / (r * r);
+          const double er = -cs - k * r * sn, ei = k * r * cs - sn;  // (ikr - 1) e^{ikr}
+          ar += u * (er * pv.x - ei * pv.y);
+          ai += u * (er * pv.y + ei * pv.x);
+        }
+        if (g) {  // - w g G
+          const double2 gv = g[(size_t)s * M + j];
+          ar -= t * (cs * gv.x - sn * gv.y);
+          ai -= t * (cs * gv.y + sn * gv.x);
+        }
+      }
+    }
   }
+#pragma unroll
+  for (int o = kFinLanes / 2; o > 0; o >>= 1) {
+    ar += __shfl_xor_sync(0xffffffffu, ar, o, kFinLanes);
+    ai += __shfl_xor_sync(0xffffffffu, ai, o, kFinLanes);
+  }
+  if (!valid || sub != 0) return;
   if (p) {
     const double2 pv = p[q];
     out[q] = make_double2(0.5 * pv.x - ar, 0.5 * pv.y - ai);
@@ -379,21 +326,6 @@ nat_status build_near(NearPairs& np, int64_t M, const double* smp, const double*
   return NAT_OK;
 }
 
-nat_status near_apply(const NearPairs& np, int nsys, int64_t M, const double* smp, const double* k, double w,
-                      const double2* p, const double2* g, double2* R, cudaStream_t s) {
-  if (!np.on) return NAT_OK;
-  for (int s0 = 0; s0 < nsys; s0 += 64) {
-    const int nb = (nsys - s0) < 64 ? (nsys - s0) : 64;
-    KArr ka{};
-    for (int q = 0; q < nb; ++q) ka.k[q] = k[s0 + q];
-    mc_near_apply_kernel<<<dim3((unsigned)((M + 255) / 256), nb), 256, 0, s>>>(
-        nb, M, smp, np.rp, np.col, ka, w, p ? p + (size_t)s0 * M : nullptr, g ? g + (size_t)s0 * M : nullptr,
-        R + (size_t)s0 * M);
-  }
-  NAT_LAUNCH_CHECK();
-  return NAT_OK;
-}
-
 nat::RadInput self_input(int64_t M, const double* smp, int nsys, double w) {
   nat::RadInput in{};
   in.n_src = M;
@@ -416,7 +348,7 @@ nat_status finish_op(const nat::RadInput& in, nat_prec prec, int64_t M, const do
   if (st != NAT_OK) return st;
   KArr ka{};
   for (int q = 0; q < nsys && q < 64; ++q) ka.k[q] = k[q];
-  mc_finish_kernel<<<dim3((unsigned)((M + 255) / 256), nsys), 256, 0, s>>>(
+  mc_finish_kernel<<<dim3((unsigned)((M + 256 / kFinLanes - 1) / (256 / kFinLanes)), nsys), 256, 0, s>>>(
       nsys, M, smp, np.on ? np.rp : nullptr, np.on ? np.col : nullptr, ka, w, keep.part, keep.n_split, p, g, eps, out,
       in.skip);
   NAT_LAUNCH_CHECK();

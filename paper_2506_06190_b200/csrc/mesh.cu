@@ -67,10 +67,20 @@ __global__ void __launch_bounds__(1024) cdf_kernel(int64_t nt, const double* __r
     for (int t = threadIdx.x; t < len; t += blockDim.x) buf[t] = area[c0 + t];
     __syncthreads();
     if (threadIdx.x == 0) {
-#pragma unroll 8
-      for (int t = 0; t < len; ++t) {
-        s = __dadd_rn(s, buf[t]);
-        buf[t] = s;
+      // 8 loads, 8 dependent adds, 8 stores: only the fp64 add latency stays serial
+      // (adding the 0.0 padding past `len` leaves s unchanged)
+      for (int t = 0; t < len; t += 8) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = t + u < len ? buf[t + u] : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          s = __dadd_rn(s, v[u]);
+          v[u] = s;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (t + u < len) buf[t + u] = v[u];
       }
     }
     __syncthreads();

@@ -38,6 +38,35 @@ struct Carver {
 
 int device_sm_count();
 
+// Exclusive scan of one int64 per thread over a 1024-thread block (warp shuffles, exact);
+// sh: 33 int64 of shared memory; *total (optional) receives the block sum.
+__device__ __forceinline__ int64_t block_exscan_1024(int64_t v, int64_t* sh, int64_t* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int64_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) sh[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    const int64_t w = sh[lane];
+    int64_t z = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, z, o);
+      if (lane >= o) z += y;
+    }
+    sh[lane] = z - w;
+    if (lane == 31) sh[32] = z;
+  }
+  __syncthreads();
+  const int64_t r = sh[warp] + x - v;
+  if (total) *total = sh[32];
+  return r;
+}
+
 }  // namespace nat
 
 #define NAT_CUDA_TRY(expr)                                                                   \

@@ -72,10 +72,11 @@ _SIGS = {
     "nat_last_error": (C.c_char_p, []),
     "nat_mesh_prepare_workspace": (_SZ, [_I64, _I64]),
     "nat_mesh_prepare": (C.c_int, [C.POINTER(_Mesh), C.POINTER(_Geom), _P, _SZ, _P]),
+    "nat_bem_near_workspace": (_SZ, [_I64]),
     "nat_bem_near_count": (C.c_int, [C.POINTER(_Mesh), C.POINTER(_Geom), C.POINTER(_QuadOpts),
-                                     _I64, _I64, _P, C.POINTER(_I64), _P]),
+                                     _I64, _I64, _P, C.POINTER(_I64), _P, _SZ, _P]),
     "nat_bem_near_build": (C.c_int, [C.POINTER(_Mesh), C.POINTER(_Geom), C.POINTER(_QuadOpts),
-                                     _I64, _I64, _P, _P, _P, _P]),
+                                     _I64, _I64, _P, _P, _P, _P, _SZ, _P]),
     "nat_bem_assemble_workspace": (_SZ, [_I64, _I64, _I64, C.c_int]),
     "nat_bem_assemble": (C.c_int, [C.POINTER(_Mesh), C.POINTER(_Geom), C.POINTER(_QuadOpts),
                                    _P, _P, _P, _D, C.c_int, _I64, _I64, C.c_int, _P, _P, _I64,
@@ -335,14 +336,15 @@ def nat_bem_near_list(mesh: Mesh, geom: Geom, row_begin=0, row_end=None, opts=No
     dev = mesh.vxyz.device
     o = opts or quad_opts()
     rp = torch.empty(row_end - row_begin + 1, dtype=torch.int64, device=dev)
+    ws = _ws(lib().nat_bem_near_workspace(mesh.n_tri), dev)
     nnz = C.c_int64(0)
     _check(lib().nat_bem_near_count(C.byref(mesh.c()), C.byref(geom.c()), C.byref(o), row_begin,
-                                    row_end, _ptr(rp), C.byref(nnz), _stream()))
+                                    row_end, _ptr(rp), C.byref(nnz), _ptr(ws), ws.numel(), _stream()))
     col = torch.empty(max(nnz.value, 1), dtype=torch.int32, device=dev)[: nnz.value]
     cls = torch.empty(max(nnz.value, 1), dtype=torch.uint8, device=dev)[: nnz.value]
     _check(lib().nat_bem_near_build(C.byref(mesh.c()), C.byref(geom.c()), C.byref(o), row_begin,
                                     row_end, _ptr(rp), C.c_void_p(col.data_ptr()),
-                                    C.c_void_p(cls.data_ptr()), _stream()))
+                                    C.c_void_p(cls.data_ptr()), _ptr(ws), ws.numel(), _stream()))
     return NearList(row_begin, row_end, rp, col, cls)
 
 
