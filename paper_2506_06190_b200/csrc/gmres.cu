@@ -251,14 +251,14 @@ __device__ void givens_block(const GivensArgs& g, int q, double2* gsm) {
   for (int i = tid; i <= j + 1; i += nt) Hc[i] = col[i];
 }
 
-// w[s][i] -= sum_{k < nvec} h2[s][k] V_k[s][i]; with norm_slot >= 0 also
+// w[s][i] = w_in[s][i] - sum_{k < nvec} h2[s][k] V_k[s][i] (w_in may be w); with norm_slot >= 0 also
 // h[s][norm_slot] = ||w[s]|| (block partials, last block sums them in fixed order), and
 // with `giv` that last block then runs the Givens step of system s (dynamic smem).
 __global__ void __launch_bounds__(kT) update_kernel(const double2* __restrict__ V, size_t vstride_k, int64_t ldv,
                                                    int64_t n, int nvec, int mp2, uint64_t active,
                                                    const unsigned long long* __restrict__ dmask,
-                                                   const double2* __restrict__ h2, double2* __restrict__ w,
-                                                   int norm_slot, double2* __restrict__ h,
+                                                   const double2* __restrict__ h2, const double2* w_in,
+                                                   double2* w, int norm_slot, double2* __restrict__ h,
                                                    double2* __restrict__ npart, unsigned* __restrict__ cnt,
                                                    bool giv, GivensArgs ga) {
   extern __shared__ double2 gsm[];
@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(kT) update_kernel(const double2* __restrict__ 
       acc.x += c.x * v.x - c.y * v.y;
       acc.y += c.x * v.y + c.y * v.x;
     }
-    o = w[(size_t)s * ldv + i];
+    o = w_in[(size_t)s * ldv + i];
     o = make_double2(o.x - acc.x, o.y - acc.y);
     w[(size_t)s * ldv + i] = o;
   }
@@ -332,30 +332,30 @@ __global__ void __launch_bounds__(kBackT) backsolve_kernel(int m, int mp1, const
   for (int i = tid; i < k; i += kBackT) y[(size_t)q * m + i] = yy[i];
 }
 
-// x[s][i] = sum_{k < k_s} y[s][k] V_k[s][i]
-__global__ void combine_kernel(const double2* __restrict__ V, size_t vstride_k, int64_t ldv, int64_t n, int m,
-                               const double2* __restrict__ y, const DevSys* __restrict__ sys,
-                               double2* __restrict__ x) {
+// x[s][i] = sum_{k < k_s} y[s][k] V_k[s][i] and, from the operator products W_k = A V_k
+// saved during the iteration, r[s][i] = b[s][i] - sum_k y[s][k] W_k[s][i] = (b - A x)[s][i]
+// (linearity: the true residual without another operator application).
+__global__ void combine_kernel(const double2* __restrict__ V, const double2* __restrict__ W, size_t vstride_k,
+                               int64_t ldv, int64_t n, int m, const double2* __restrict__ y,
+                               const DevSys* __restrict__ sys, const double2* __restrict__ b,
+                               double2* __restrict__ x, double2* __restrict__ r) {
   const int s = blockIdx.y;
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int kmax = (sys[s].flags & kSysNonFinite) ? 0 : sys[s].k;
-  double2 acc = make_double2(0.0, 0.0);
+  double2 acc = make_double2(0.0, 0.0), ax = make_double2(0.0, 0.0);
   for (int k = 0; k < kmax; ++k) {
-    double2 c = y[(size_t)s * m + k];
-    double2 v = V[k * vstride_k + (size_t)s * ldv + i];
+    const double2 c = y[(size_t)s * m + k];
+    const double2 v = V[k * vstride_k + (size_t)s * ldv + i];
+    const double2 u = W[k * vstride_k + (size_t)s * ldv + i];
     acc.x += c.x * v.x - c.y * v.y;
     acc.y += c.x * v.y + c.y * v.x;
+    ax.x += c.x * u.x - c.y * u.y;
+    ax.y += c.x * u.y + c.y * u.x;
   }
   x[(size_t)s * ldv + i] = acc;
-}
-
-__global__ void sub_kernel(const double2* __restrict__ b, int64_t ldv, int64_t n, double2* __restrict__ w) {
-  const int s = blockIdx.y;
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  double2 a = b[(size_t)s * ldv + i], c = w[(size_t)s * ldv + i];
-  w[(size_t)s * ldv + i] = make_double2(a.x - c.x, a.y - c.y);
+  const double2 bb = b[(size_t)s * ldv + i];
+  r[(size_t)s * ldv + i] = make_double2(bb.x - ax.x, bb.y - ax.y);
 }
 
 // Per-thread, per-device host resources: a pinned ring for the convergence mask and
@@ -403,6 +403,7 @@ size_t krylov_workspace(int nsys, int64_t n, int64_t ldv, int max_iter, Carver& 
   const int nchunk = (int)((n + kKrylovChunk - 1) / kKrylovChunk);
   KrylovWs t;
   t.V = c.take<double2>((size_t)(m + 1) * nsys * ldv);
+  t.W = c.take<double2>((size_t)(m > 0 ? m : 1) * nsys * ldv);
   t.w = c.take<double2>((size_t)nsys * ldv);
   t.part = c.take<double2>((size_t)nsys * (m + 1) * nchunk);
   t.h = c.take<double2>((size_t)nsys * (m + 2));
@@ -454,24 +455,26 @@ nat_status gmres_batched(int nsys, int64_t n, int64_t ldv, const double2* b, dou
   int n_timed = 0;
   auto enqueue = [&](int j, uint64_t host_active) -> nat_status {
     double2* Vj = ws.V + (size_t)j * vstride;
+    double2* Wj = ws.W + (size_t)j * vstride;  // A V_j, kept for the final residual
     if (t_op_s) {
       cudaEvent_t e0 = timing_event(0, 2 * j), e1 = timing_event(0, 2 * j + 1);
       if (!e0 || !e1) return fail(NAT_ERR_CUDA, "timing events");
       NAT_CUDA_TRY(cudaEventRecord(e0, s));
-      nat_status stt = op(Vj, ws.w, host_active, ws.mask, s);
+      nat_status stt = op(Vj, Wj, host_active, ws.mask, s);
       if (stt != NAT_OK) return stt;
       NAT_CUDA_TRY(cudaEventRecord(e1, s));
       n_timed = j + 1;
     } else {
-      nat_status stt = op(Vj, ws.w, host_active, ws.mask, s);
+      nat_status stt = op(Vj, Wj, host_active, ws.mask, s);
       if (stt != NAT_OK) return stt;
     }
-    for (int pass = 0; pass < 2; ++pass) {  // CGS2; the second update also forms ||w||
-      dots(ws.V, vstride, ws.w, j + 1, ws.mask, pass, 0);
+    for (int pass = 0; pass < 2; ++pass) {  // CGS2 (w = W_j minus its projections); pass 1 also forms ||w||
+      const double2* win = pass == 0 ? Wj : ws.w;
+      dots(ws.V, vstride, win, j + 1, ws.mask, pass, 0);
       ga.j = j;
       update_kernel<<<dim3(gx, nsys), kT, pass == 1 ? gsmem : 0, s>>>(
-          ws.V, vstride, ldv, n, j + 1, mp2, all, ws.mask, ws.h2, ws.w, pass == 1 ? j + 1 : -1, ws.h, ws.npart,
-          ws.cnt + 64, pass == 1, ga);
+          ws.V, vstride, ldv, n, j + 1, mp2, all, ws.mask, ws.h2, win, ws.w, pass == 1 ? j + 1 : -1, ws.h,
+          ws.npart, ws.cnt + 64, pass == 1, ga);
     }
     scale_kernel<<<dim3(gx, nsys), kT, 0, s>>>(ws.w, ldv, n, mp2, j + 1, all, ws.mask, ws.h,
                                                ws.V + (size_t)(j + 1) * vstride, hs->ring_dev + j % kRing);
@@ -513,13 +516,10 @@ nat_status gmres_batched(int nsys, int64_t n, int64_t ldv, const double2* b, dou
       NAT_CUDA_TRY(cudaFuncSetAttribute(backsolve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     backsolve_kernel<<<nsys, kBackT, smem, s>>>(m, mp1, ws.H, ws.gam, ws.sys, ws.y, (int)smem);
   }
-  combine_kernel<<<dim3(gx, nsys), kT, 0, s>>>(ws.V, vstride, ldv, n, m, ws.y, ws.sys, x);
-  NAT_LAUNCH_CHECK();
-  // true residual ||b - A x|| / beta
-  nat_status stt = op(x, ws.w, all, nullptr, s);
-  if (stt != NAT_OK) return stt;
-  sub_kernel<<<dim3(gx, nsys), kT, 0, s>>>(b, ldv, n, ws.w);
+  // x = V y and the true residual b - A x = b - sum_k y_k (A V_k), then ||b - A x|| / beta
+  combine_kernel<<<dim3(gx, nsys), kT, 0, s>>>(ws.V, ws.W, vstride, ldv, n, m, ws.y, ws.sys, b, x, ws.w);
   dots(ws.w, 0, ws.w, 1, nullptr, 2, 0);
+  NAT_LAUNCH_CHECK();
   NAT_LAUNCH_CHECK();
   std::vector<double2> hbuf((size_t)nsys * mp2);
   std::vector<DevSys> sys(nsys);

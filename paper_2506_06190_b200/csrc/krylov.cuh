@@ -21,7 +21,8 @@ constexpr int kSysConverged = 1;
 constexpr int kSysNonFinite = 2;
 
 struct KrylovWs {
-  double2* V;     // [(m+1)][nsys][ldv]
+  double2* V;     // [(m+1)][nsys][ldv] Arnoldi basis
+  double2* W;     // [m][nsys][ldv] operator products A V_j (final residual by linearity)
   double2* w;     // [nsys][ldv]
   double2* part;  // [nsys][m+1][nchunk]
   double2* h;     // [nsys][m+2]  current Arnoldi column

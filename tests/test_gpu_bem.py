@@ -125,6 +125,10 @@ def test_gmres_parity_and_contract(prec):
     xo, io = gmres.gmres(lambda z: Aq @ z, b, tol=1e-13, max_iter=300)
     assert info["converged"] == 1 and info["rel_residual"] <= tol
     assert rel_l2(to_np(x), xo) <= (1e-5 if prec == "fp32" else 1e-11)
+    # the reported residual (b - sum_k y_k A v_k, from the saved operator products) is the
+    # true ||b - A x|| / ||b|| up to the matvec rounding (fp32 products: ~1e-7)
+    direct = np.linalg.norm(b - Aq @ to_np(x)) / np.linalg.norm(b)
+    assert abs(info["rel_residual"] - direct) <= (1e-6 if prec == "fp32" else 1e-13)
     # zero right-hand side -> 0 iterations, x = 0
     x0, i0 = nat.nat_bem_solve(At, torch.zeros(n, dtype=torch.complex128, device="cuda"), n)
     assert i0["iters"] == 0 and torch.count_nonzero(x0) == 0
