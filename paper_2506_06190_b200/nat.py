@@ -525,7 +525,7 @@ def nat_mc_surface_pressure(mesh: Mesh, geom: Geom, k, g_tri, M: int, seed: int 
                                        _ptr(p), _ptr(ws), ws.numel(), infos, _stream())
     _check(st, allow_warn=True)
     return smp, tri, p, [dict(iters=i.iters, converged=i.converged, rel_residual=i.rel_residual,
-                              t_total_s=i.t_total_s) for i in infos]
+                              t_total_s=i.t_total_s, t_matvec_s=i.t_matvec_s) for i in infos]
 
 
 def row_range(n: int, rank: int, world: int):

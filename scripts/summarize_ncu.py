@@ -45,5 +45,6 @@ for d in data:
           f"{g(d, 'sm__cycles_elapsed.avg.per_second', unit_scale('sm__cycles_elapsed.avg.per_second')) / 1e9:.3f} |")
     base = name.split("<")[0]
     traffic.setdefault(base, rd + wr)
+    traffic.setdefault(name.strip(), rd + wr)
 if out_json:
     json.dump(traffic, open(out_json, "w"), indent=1)
