@@ -265,6 +265,17 @@ nat_status nat_listener_grid(const double* center /* [host] 3 */, double R, int 
                              int n_r, double r_lo, double r_hi, double* out,
                              nat_stream_t stream); /* (async) */
 
+/* a12 (optional form, "randomly sample theta, phi, and r within an enclosing
+ * sphere"; reading R-listen-rand): n points uniform in the volume of the shell
+ * R r_lo <= |x - center| <= R r_hi.  Point t: Philox4x32-10 counter (t, 1, stream_lo,
+ * stream_hi), key = seed, u_a = (o_a + 1/2) 2^-32; cos(phi) = 1 - 2 u0,
+ * sin(phi) = 2 sqrt(u0 (1 - u0)), theta = -pi + 2 pi u1, r = R cbrt(r_lo^3 + u2 (r_hi^3 - r_lo^3)).
+ * out: [3][n] fp64 SoA (caller-owned device buffer).  Async.  NAT_ERR_INVALID_ARG for
+ * n < 1, R <= 0, r_lo <= 0, r_hi < r_lo or a host / null out.                            */
+nat_status nat_listener_random_shell(const double* center /* [host] 3 */, double R, int64_t n, double r_lo,
+                                     double r_hi, uint64_t seed, uint64_t stream_id, double* out,
+                                     nat_stream_t stream); /* (async) */
+
 #ifdef __cplusplus
 }
 #endif

@@ -16,27 +16,10 @@
 #include "krylov.cuh"
 #include "nat_internal.cuh"
 #include "pair.cuh"
+#include "philox.cuh"
 #include "radiate.cuh"
 
 namespace {
-
-__device__ __forceinline__ void philox4x32_10(uint32_t& c0, uint32_t& c1, uint32_t& c2, uint32_t& c3,
-                                              uint32_t k0, uint32_t k1) {
-#pragma unroll
-  for (int r = 0; r < 10; ++r) {
-    if (r > 0) {
-      k0 += 0x9E3779B9u;
-      k1 += 0xBB67AE85u;
-    }
-    const uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
-    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
-    const uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
-    c0 = n0;
-    c1 = lo1;
-    c2 = n2;
-    c3 = lo0;
-  }
-}
 
 __global__ void mc_sample_kernel(int64_t M, uint64_t seed, uint64_t stream_id, int64_t nv, int64_t nt,
                                  const double* __restrict__ vx, const int32_t* __restrict__ tri,
@@ -45,7 +28,7 @@ __global__ void mc_sample_kernel(int64_t M, uint64_t seed, uint64_t stream_id, i
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (j >= M) return;
   uint32_t c0 = (uint32_t)j, c1 = 0u, c2 = (uint32_t)stream_id, c3 = (uint32_t)(stream_id >> 32);
-  philox4x32_10(c0, c1, c2, c3, (uint32_t)seed, (uint32_t)(seed >> 32));
+  nat::philox4x32_10(c0, c1, c2, c3, (uint32_t)seed, (uint32_t)(seed >> 32));
   const double two32 = 2.3283064365386963e-10;  // 2^-32
   const double u0 = __dmul_rn(__dadd_rn((double)c0, 0.5), two32);
   const double u1 = __dmul_rn(__dadd_rn((double)c1, 0.5), two32);

@@ -6,6 +6,7 @@
 // intrinsics (__dadd_rn, __dmul_rn, ...) so nvcc cannot contract it into an FMA:
 // the results are bit-identical to any IEEE implementation of the same formula.
 #include "nat_internal.cuh"
+#include "philox.cuh"
 
 namespace {
 
@@ -164,6 +165,28 @@ __global__ void listener_grid_kernel(double cx, double cy, double cz, double R, 
   out[2 * n + i] = cz + r * cp;
 }
 
+// Reading R-listen-rand: point t of a random shell, uniform in volume
+// (SPEC's design note to P:166): Philox counter (t, 1, stream_lo, stream_hi), key = seed,
+// u_a = (o_a + 1/2) 2^-32;  cos(phi) = 1 - 2 u0, sin(phi) = 2 sqrt(u0 (1 - u0)),
+// theta = -pi + 2 pi u1,  r = R cbrt(r_lo^3 + u2 (r_hi^3 - r_lo^3)).
+__global__ void listener_random_kernel(double cx, double cy, double cz, double R, int64_t n, double r_lo,
+                                       double r_hi, uint64_t seed, uint64_t stream_id, double* __restrict__ out) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  uint32_t c0 = (uint32_t)t, c1 = 1u, c2 = (uint32_t)stream_id, c3 = (uint32_t)(stream_id >> 32);
+  nat::philox4x32_10(c0, c1, c2, c3, (uint32_t)seed, (uint32_t)(seed >> 32));
+  const double two32 = 2.3283064365386963e-10;  // 2^-32
+  const double u0 = ((double)c0 + 0.5) * two32, u1 = ((double)c1 + 0.5) * two32, u2 = ((double)c2 + 0.5) * two32;
+  const double cp = 1.0 - 2.0 * u0, sp = 2.0 * sqrt(u0 * (1.0 - u0));
+  double st, ct;
+  sincos(-nat::kPi + 2.0 * nat::kPi * u1, &st, &ct);
+  const double lo3 = r_lo * r_lo * r_lo, hi3 = r_hi * r_hi * r_hi;
+  const double r = R * cbrt(lo3 + u2 * (hi3 - lo3));
+  out[t] = cx + r * (sp * ct);
+  out[n + t] = cy + r * (sp * st);
+  out[2 * n + t] = cz + r * cp;
+}
+
 }  // namespace
 
 extern "C" size_t nat_mesh_prepare_workspace(int64_t n_vert, int64_t n_tri) {
@@ -230,6 +253,19 @@ extern "C" nat_status nat_listener_grid(const double* center, double R, int n_th
   int64_t n = (int64_t)n_theta * n_phi * n_r;
   listener_grid_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
       center[0], center[1], center[2], R, n_theta, n_phi, n_r, r_lo, r_hi, out);
+  NAT_LAUNCH_CHECK();
+  return NAT_OK;
+}
+
+extern "C" nat_status nat_listener_random_shell(const double* center, double R, int64_t n, double r_lo,
+                                                double r_hi, uint64_t seed, uint64_t stream_id, double* out,
+                                                nat_stream_t stream) {
+  NAT_REQUIRE(center, "center must be a host array of 3");
+  NAT_REQUIRE(n >= 1, "need n >= 1");
+  NAT_REQUIRE(R > 0 && r_lo > 0 && r_hi >= r_lo, "need R > 0, 0 < r_lo <= r_hi");
+  NAT_REQUIRE_DEV(out);
+  listener_random_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      center[0], center[1], center[2], R, n, r_lo, r_hi, seed, stream_id, out);
   NAT_LAUNCH_CHECK();
   return NAT_OK;
 }

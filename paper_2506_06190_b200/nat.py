@@ -110,6 +110,8 @@ _SIGS = {
                                     _P, _SZ, _P]),
     "nat_listener_grid": (C.c_int, [C.POINTER(_D), _D, C.c_int, C.c_int, C.c_int, _D, _D, _P,
                                     _P]),
+    "nat_listener_random_shell": (C.c_int, [C.POINTER(_D), _D, _I64, _D, _D, C.c_uint64, C.c_uint64, _P,
+                                            _P]),
 }
 
 _lib = None
@@ -256,6 +258,16 @@ def nat_listener_grid(center, R, n_theta, n_phi, n_r, r_lo=1.5, r_hi=3.0, device
     c = (C.c_double * 3)(*[float(x) for x in center])
     _check(lib().nat_listener_grid(c, float(R), n_theta, n_phi, n_r, float(r_lo), float(r_hi),
                                    _ptr(out), _stream()))
+    return out
+
+
+def nat_listener_random_shell(center, R, n, r_lo=1.5, r_hi=3.0, seed=0, stream_id=0, device="cuda"):
+    """n listener points uniform in the volume of the shell R r_lo <= |x - c| <= R r_hi
+    (Philox tag 1; reading R-listen-rand).  Returns (3, n) float64."""
+    out = torch.empty(3, n, dtype=torch.float64, device=device)
+    c = (C.c_double * 3)(*[float(x) for x in center])
+    _check(lib().nat_listener_random_shell(c, float(R), int(n), float(r_lo), float(r_hi), int(seed),
+                                           int(stream_id), _ptr(out), _stream()))
     return out
 
 

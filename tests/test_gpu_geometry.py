@@ -52,3 +52,24 @@ def test_listener_grid(dims):
     x = nat.nat_listener_grid(c, R, *dims)
     ref = listeners.shell_grid(np.array(c), R, *dims)
     np.testing.assert_allclose(soa_to_aos(x), ref, rtol=0, atol=4e-16 * 3 * R * 4)
+
+
+@pytest.mark.parametrize("n,seed,stream", [(1, 0, 0), (1000, 20250606, 3), (262_147, 7, 1 << 33)])
+def test_listener_random_shell(n, seed, stream):
+    """Reading R-listen-rand: same Philox draws (tag 1) and formula as the oracle; only
+    the libm / CUDA transcendentals (cbrt, sincos, sqrt) differ, by ulps."""
+    nat = _nat()
+    c, R = (0.1, -0.2, 0.05), 0.37
+    x = nat.nat_listener_random_shell(c, R, n, seed=seed, stream_id=stream)
+    ref = listeners.random_shell(np.array(c), R, n, seed=seed, stream_id=stream)
+    np.testing.assert_allclose(soa_to_aos(x), ref, rtol=0, atol=1e-15 * 3 * R * 8)
+
+
+def test_listener_random_shell_errors():
+    nat = _nat()
+    from paper_2506_06190_b200.nat import NatError
+    for bad in (dict(n=0), dict(R=-1.0), dict(r_lo=0.0), dict(r_lo=2.0, r_hi=1.0)):
+        kw = dict(center=(0, 0, 0), R=1.0, n=4)
+        kw.update(bad)
+        with pytest.raises(NatError):
+            nat.nat_listener_random_shell(kw.pop("center"), kw.pop("R"), kw.pop("n"), **kw)
