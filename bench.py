@@ -164,7 +164,12 @@ class Step:
         self.solve_ws = [ws] * len(KAS)
         self.S_bem = 3 * self.n
         self.n_lis = self.l1 - self.l0
-        self.rad_plan_bem = nat.RadiatePlan(self.S_bem, len(KAS), self.n_lis, "fp32", dev)
+        # BEM radiation groups: the solutions of each group of wavenumbers radiate in one
+        # fused launch as soon as the group's last solve is done (NAT_BENCH_RADGROUPS,
+        # e.g. "012" = one launch after the last solve, "01,2", "0,1,2")
+        self.rad_groups = [[int(c) for c in g] for g in os.environ.get("NAT_BENCH_RADGROUPS", "012").split(",")]
+        self.rad_plan_bem = {len(g): nat.RadiatePlan(self.S_bem, len(g), self.n_lis, "fp32", dev)
+                             for g in self.rad_groups}
         self.out_bem = torch.empty(len(KAS), self.n_lis, dtype=torch.complex128, device=dev)
         self.x_bem = torch.empty(len(KAS), self.n, dtype=torch.complex128, device=dev)
         self.g3 = self.g.expand(len(KAS), -1).contiguous()
@@ -179,6 +184,7 @@ class Step:
         prio = os.environ.get("NAT_BENCH_PRIO", "mc")
         self.s_bem = torch.cuda.Stream(priority=-1 if prio == "bem" else 0)
         self.s_mc = torch.cuda.Stream(priority=-1 if prio == "mc" else 0)
+        self.s_rad = torch.cuda.Stream()
 
     def _ev(self, name, tag=""):
         """Event on the current stream; `tag` keeps the start/end events of concurrent
@@ -223,13 +229,15 @@ class Step:
         if not hasattr(self, "nS"):   # class counts for the pair accounting (first step only)
             self.nS = int((near.cls == 1).sum().item())
 
-        def bem_all():
+        def bem_all(side=None):
             for q in range(len(KAS)):
                 self._bem_one(q, geo, near, counts)
+                for grp in self.rad_groups:
+                    if grp[-1] == q:
+                        self._bem_radiate(geo, lis, grp, side)
 
         if not overlap:
             bem_all()
-            self._bem_radiate(geo, lis)
             if self.mc_idx:
                 self._mc_chain(geo, lis, counts)
         else:
@@ -246,7 +254,7 @@ class Step:
                 except BaseException as ex:  # re-raised on the main thread
                     err.append(ex)
 
-            ths = [threading.Thread(target=worker, args=(self.s_bem, bem_all))]
+            ths = [threading.Thread(target=worker, args=(self.s_bem, bem_all, self.s_rad))]
             if self.mc_idx:
                 ths.append(threading.Thread(target=worker, args=(self.s_mc, self._mc_chain, geo, lis, counts)))
             for t in ths:
@@ -256,7 +264,7 @@ class Step:
             if err:
                 raise err[0]
             cur.wait_stream(self.s_bem)
-            self._bem_radiate(geo, lis)
+            cur.wait_stream(self.s_rad)
             cur.wait_stream(self.s_mc)
         if host_inputs:
             hb, hm = self.host["out_pinned"]
@@ -287,13 +295,26 @@ class Step:
             counts["gemv_s"] += info["t_matvec_s"]
             counts["iters"].append((q, info["iters"]))
 
-    def _bem_radiate(self, geo, lis):
-        """a11: the three solutions radiate in one launch (shared r, 1/r, d.n per pair)."""
-        nat = self.nat
-        src = nat.nat_bem_sources(self.mesh, geo, self.x_bem, self.g3)
-        self._ev("rad0")
-        nat.nat_radiate_field(src, list(KAS), lis, "fp32", out=self.out_bem, plan=self.rad_plan_bem)
-        self._ev("rad1")
+    def _bem_radiate(self, geo, lis, grp, side=None):
+        """a11 for the solutions of the wavenumbers in grp (contiguous indices), one fused
+        launch (shared r, 1/r, d.n per pair).  side: a stream that waits for the solves
+        and runs the radiation beside the next assembly / solve."""
+        nat, torch = self.nat, self.torch
+        a, b = grp[0], grp[-1] + 1
+
+        def go():
+            src = nat.nat_bem_sources(self.mesh, geo, self.x_bem[a:b], self.g3[a:b])
+            self._ev("rad0", str(a))
+            nat.nat_radiate_field(src, list(KAS[a:b]), lis, "fp32", out=self.out_bem[a:b],
+                                  plan=self.rad_plan_bem[b - a])
+            self._ev("rad1", str(a))
+
+        if side is None:
+            go()
+        else:
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):
+                go()
 
     def _mc_chain(self, geo, lis, counts):
         """a8-a10 (batched over the rank's wavenumbers), then a11 of the MC solution."""

@@ -48,17 +48,33 @@ __device__ __forceinline__ double2 block_reduce(double2 v, double2* sm) {
   return s;
 }
 
-// Fixed-order sum of the nvec x nchunk partials of system s into h / h2:
-// mode 0: h = h2 = sum;  mode 1: h2 = sum, h += sum;  mode 2: h[s][slot] = (sqrt(Re sum), 0)
+// Sum of p[0..cnt) by one warp: lane l takes l, l+32, ... (loads in flight together),
+// then a fixed xor tree; every lane returns the total.  Deterministic.
+__device__ __forceinline__ double2 warp_sum_partials(const double2* p, int cnt) {
+  const int lane = threadIdx.x & 31;
+  double2 t = make_double2(0.0, 0.0);
+  for (int c = lane; c < cnt; c += 32) {
+    const double2 v = __ldcg(&p[c]);
+    t.x += v.x;
+    t.y += v.y;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    t.x += __shfl_xor_sync(0xffffffffu, t.x, o);
+    t.y += __shfl_xor_sync(0xffffffffu, t.y, o);
+  }
+  return t;
+}
+
+// Fixed-order sum of the nvec x nchunk partials of system s into h / h2 (one warp per
+// vector):  mode 0: h = h2 = sum;  mode 1: h2 = sum, h += sum;  mode 2: h[s][slot] =
+// (sqrt(Re sum), 0)
 __device__ void finish_sums(const double2* __restrict__ part, int s, int nvec, int nchunk, int mp1, int mp2,
                             int mode, int slot, double2* __restrict__ h, double2* __restrict__ h2) {
-  for (int k = threadIdx.x; k < nvec; k += blockDim.x) {
-    double2 t = make_double2(0.0, 0.0);
-    for (int c = 0; c < nchunk; ++c) {
-      const double2 v = __ldcg(&part[((size_t)s * mp1 + k) * nchunk + c]);
-      t.x += v.x;
-      t.y += v.y;
-    }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int k = warp; k < nvec; k += nw) {
+    const double2 t = warp_sum_partials(part + ((size_t)s * mp1 + k) * nchunk, nchunk);
+    if (lane != 0) continue;
     if (mode == 0) {
       h[(size_t)s * mp2 + k] = t;
       h2[(size_t)s * mp2 + k] = t;
@@ -284,10 +300,9 @@ __global__ void __launch_bounds__(kT) update_kernel(const double2* __restrict__ 
   const double2 r = block_reduce(make_double2(o.x * o.x + o.y * o.y, 0.0), sm);
   if (threadIdx.x == 0) npart[(size_t)s * gridDim.x + blockIdx.x] = r;
   if (last_block(&cnt[s], gridDim.x, &flag)) {
-    if (threadIdx.x == 0) {
-      double t = 0.0;
-      for (unsigned b = 0; b < gridDim.x; ++b) t += __ldcg(&npart[(size_t)s * gridDim.x + b]).x;
-      h[(size_t)s * mp2 + norm_slot] = make_double2(sqrt(t), 0.0);
+    if (threadIdx.x < 32) {
+      const double t = warp_sum_partials(npart + (size_t)s * gridDim.x, (int)gridDim.x).x;
+      if (threadIdx.x == 0) h[(size_t)s * mp2 + norm_slot] = make_double2(sqrt(t), 0.0);
     }
     if (giv) {
       __syncthreads();
