@@ -20,6 +20,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <type_traits>
 #include <vector>
 
 #include "f32x2.cuh"
@@ -312,7 +313,7 @@ __global__ void __launch_bounds__(kThreads) far_kernel(FarArgs<R> a) {
 // quadrature point and row: 11 packed-pipe instructions + 1 FMUL.RZ + 3 MUFU.  The kernel
 // accumulates -K directly (A_ij = -K_ij off the diagonal) and V g for the RHS.
 template <int NQ, int NR>
-__global__ void __launch_bounds__(kThreads, 3) far_kernel_x2(FarArgs<float> a) {
+__global__ void __launch_bounds__(kThreads, 2) far_kernel_x2(FarArgs<float> a) {
   static_assert(kTI % 2 == 0, "row pairs");
   constexpr int TP = kTI / 2;
   constexpr int NRr = NR > 0 ? NR : 1;
@@ -343,72 +344,89 @@ __global__ void __launch_bounds__(kThreads, 3) far_kernel_x2(FarArgs<float> a) {
 #pragma unroll
     for (int q = 0; q < NRr; ++q) br[t][q] = bi[t][q] = 0ull;
 
-  for (int cc = 0; cc < kCC; ++cc) {
-    const int64_t j = (int64_t)blockIdx.x * (kThreads * kCC) + cc * kThreads + tid;
-    const bool valid = j < n;
-    const int64_t jj = valid ? j : 0;
-    f2r y[NQ][3], w[NQ];
+  // full row blocks (all but the last) run without per-row guards, so the row pairs of a
+  // column form one straight-line block the scheduler can interleave
+  auto columns = [&](auto full_tag) {
+    constexpr bool FULL = decltype(full_tag)::value;
+    for (int cc = 0; cc < kCC; ++cc) {
+      const int64_t j = (int64_t)blockIdx.x * (kThreads * kCC) + cc * kThreads + tid;
+      const bool valid = j < n;
+      const int64_t jj = valid ? j : 0;
+      f2r y[NQ][3], w[NQ];
 #pragma unroll
-    for (int q = 0; q < NQ; ++q) {
+      for (int q = 0; q < NQ; ++q) {
 #pragma unroll
-      for (int d = 0; d < 3; ++d) {
-        const float v = a.cols.qxyz[((size_t)q * 3 + d) * n + jj];
-        y[q][d] = f2pack(v, v);
+        for (int d = 0; d < 3; ++d) {
+          const float v = a.cols.qxyz[((size_t)q * 3 + d) * n + jj];
+          y[q][d] = f2pack(v, v);
+        }
+        const float wv = valid ? a.cols.qw[(size_t)q * n + jj] : 0.f;
+        w[q] = f2pack(wv, wv);
       }
-      const float wv = valid ? a.cols.qw[(size_t)q * n + jj] : 0.f;
-      w[q] = f2pack(wv, wv);
-    }
-    const float nxs = a.cols.nrm[jj], nys = a.cols.nrm[n + jj], nzs = a.cols.nrm[2 * n + jj];
-    const f2r nx = f2pack(nxs, nxs), ny = f2pack(nys, nys), nz = f2pack(nzs, nzs);
-    f2r gr[NRr], gi[NRr], ngi[NRr];
+      const float nxs = a.cols.nrm[jj], nys = a.cols.nrm[n + jj], nzs = a.cols.nrm[2 * n + jj];
+      const f2r nx = f2pack(nxs, nxs), ny = f2pack(nys, nys), nz = f2pack(nzs, nzs);
+      // d.n = y_q.n - c.n: the column part once per column, the row part once per row pair
+      f2r yn[NQ];
 #pragma unroll
-    for (int q = 0; q < NR; ++q) {
-      const double2 gv = valid ? a.g[(size_t)(a.rhs0 + q) * n + jj] : make_double2(0.0, 0.0);
-      gr[q] = f2pack((float)gv.x, (float)gv.x);
-      gi[q] = f2pack((float)gv.y, (float)gv.y);
-      ngi[q] = f2pack(-(float)gv.y, -(float)gv.y);
-    }
-    // running pointer to A[i0 + 2t][j] (one 64-bit add per row pair instead of a
-    // 64-bit multiply per store)
-    float2* arow = reinterpret_cast<float2*>(a.A) + (size_t)i0 * a.lda + jj;
-    const int64_t ld = a.lda;
+      for (int q = 0; q < NQ; ++q) {
+        const float v = fmaf(f2lo(y[q][2]), nzs, fmaf(f2lo(y[q][1]), nys, f2lo(y[q][0]) * nxs));
+        yn[q] = f2pack(v, v);
+      }
+      f2r gr[NRr], gi[NRr], ngi[NRr];
 #pragma unroll
-    for (int t = 0; t < TP; ++t, arow += 2 * ld) {
-      if (2 * t < nrows) {
-        const f2r cx = s_c[0][t], cy = s_c[1][t], cz = s_c[2][t];
-        f2r Vr = 0ull, Vi = 0ull, Kr = 0ull, Ki = 0ull;  // K here is -K
+      for (int q = 0; q < NR; ++q) {
+        const double2 gv = valid ? a.g[(size_t)(a.rhs0 + q) * n + jj] : make_double2(0.0, 0.0);
+        gr[q] = f2pack((float)gv.x, (float)gv.x);
+        gi[q] = f2pack((float)gv.y, (float)gv.y);
+        ngi[q] = f2pack(-(float)gv.y, -(float)gv.y);
+      }
+      // running pointer to A[i0 + 2t][j] (one 64-bit add per row pair instead of a
+      // 64-bit multiply per store)
+      float2* arow = reinterpret_cast<float2*>(a.A) + (size_t)i0 * a.lda + jj;
+      const int64_t ld = a.lda;
 #pragma unroll
-        for (int q = 0; q < NQ; ++q) {
-          const f2r dx = f2sub(y[q][0], cx), dy = f2sub(y[q][1], cy), dz = f2sub(y[q][2], cz);
-          const f2r r2 = f2fma(dz, dz, f2fma(dy, dy, f2mul(dx, dx)));
-          const f2r dn = f2fma(dz, nz, f2fma(dy, ny, f2mul(dx, nx)));
-          const f2r rho = f2pack(nat::pair_rsqrt(f2lo(r2)), nat::pair_rsqrt(f2hi(r2)));
-          const f2r rr = f2mul(r2, rho);
-          const f2r kr = f2mul(rr, kk), nkr = f2mul(rr, nkk);
-          float s0, c0, s1, c1;
-          __sincosf(f2lo(kr), &s0, &c0);
-          __sincosf(f2hi(kr), &s1, &c1);
-          const f2r sn = f2pack(s0, s1), cs = f2pack(c0, c1);
-          const f2r tq = f2mul(w[q], rho);               // w G-part: tq e^{ikr}
-          Vr = f2fma(tq, cs, Vr);
-          Vi = f2fma(tq, sn, Vi);
-          const f2r u = f2mul(tq, f2mul(dn, f2mul(rho, rho)));
-          // -K += u (c + kr s) + i u (s - kr c)   [K = u (ikr - 1) e^{ikr}]
-          Kr = f2fma(u, f2fma(kr, sn, cs), Kr);
-          Ki = f2fma(u, f2fma(nkr, cs, sn), Ki);
-        }
-        if (a.store_A && valid) {
-          arow[0] = make_float2(f2lo(Kr), f2lo(Ki));
-          if (2 * t + 1 < nrows) arow[ld] = make_float2(f2hi(Kr), f2hi(Ki));
-        }
+      for (int t = 0; t < TP; ++t, arow += 2 * ld) {
+        if (FULL || 2 * t < nrows) {
+          const f2r cx = s_c[0][t], cy = s_c[1][t], cz = s_c[2][t];
+          const f2r cn = f2fma(cz, nz, f2fma(cy, ny, f2mul(cx, nx)));
+          f2r Vr = 0ull, Vi = 0ull, Kr = 0ull, Ki = 0ull;  // K here is -K
 #pragma unroll
-        for (int q = 0; q < NR; ++q) {
-          br[t][q] = f2fma(Vr, gr[q], f2fma(Vi, ngi[q], br[t][q]));
-          bi[t][q] = f2fma(Vr, gi[q], f2fma(Vi, gr[q], bi[t][q]));
+          for (int q = 0; q < NQ; ++q) {
+            const f2r dx = f2sub(y[q][0], cx), dy = f2sub(y[q][1], cy), dz = f2sub(y[q][2], cz);
+            const f2r r2 = f2fma(dz, dz, f2fma(dy, dy, f2mul(dx, dx)));
+            const f2r dn = f2sub(yn[q], cn);
+            const f2r rho = f2pack(nat::pair_rsqrt(f2lo(r2)), nat::pair_rsqrt(f2hi(r2)));
+            const f2r rr = f2mul(r2, rho);
+            const f2r kr = f2mul(rr, kk), nkr = f2mul(rr, nkk);
+            float s0, c0, s1, c1;
+            __sincosf(f2lo(kr), &s0, &c0);
+            __sincosf(f2hi(kr), &s1, &c1);
+            const f2r sn = f2pack(s0, s1), cs = f2pack(c0, c1);
+            const f2r tq = f2mul(w[q], rho);               // w G-part: tq e^{ikr}
+            Vr = f2fma(tq, cs, Vr);
+            Vi = f2fma(tq, sn, Vi);
+            const f2r u = f2mul(tq, f2mul(dn, f2mul(rho, rho)));
+            // -K += u (c + kr s) + i u (s - kr c)   [K = u (ikr - 1) e^{ikr}]
+            Kr = f2fma(u, f2fma(kr, sn, cs), Kr);
+            Ki = f2fma(u, f2fma(nkr, cs, sn), Ki);
+          }
+          if (a.store_A && valid) {
+            arow[0] = make_float2(f2lo(Kr), f2lo(Ki));
+            if (FULL || 2 * t + 1 < nrows) arow[ld] = make_float2(f2hi(Kr), f2hi(Ki));
+          }
+#pragma unroll
+          for (int q = 0; q < NR; ++q) {
+            br[t][q] = f2fma(Vr, gr[q], f2fma(Vi, ngi[q], br[t][q]));
+            bi[t][q] = f2fma(Vr, gi[q], f2fma(Vi, gr[q], bi[t][q]));
+          }
         }
       }
     }
-  }
+  };
+  if (nrows == kTI)
+    columns(std::integral_constant<bool, true>{});
+  else
+    columns(std::integral_constant<bool, false>{});
   if constexpr (NR > 0) {
 #pragma unroll
     for (int t = 0; t < kTI; ++t)
