@@ -33,11 +33,12 @@ from . import gmres as _gmres
 from . import kernel, philox
 
 
-def sample_uniform(v, t, geom, M, seed, stream_id=0):
-    """Returns (y (M,3), n (M,3), tri (M,) int32)."""
+def sample_uniform(v, t, geom, M, seed, stream_id=0, tag=0):
+    """Returns (y (M,3), n (M,3), tri (M,) int32).  tag 0: boundary samples (a8); tag 2:
+    Poisson-disk candidates (oracle/poisson.py)."""
     v = np.asarray(v, dtype=np.float64)
     t = np.asarray(t, dtype=np.int64)
-    u = philox.uniforms(np.arange(M), 0, stream_id, seed)
+    u = philox.uniforms(np.arange(M), tag, stream_id, seed)
     cdf = geom["cdf"]
     tri = np.searchsorted(cdf, u[:, 0] * cdf[-1], side="right")
     tri = np.minimum(tri, len(cdf) - 1)
