@@ -265,6 +265,21 @@ nat_status nat_listener_grid(const double* center /* [host] 3 */, double R, int 
                              int n_r, double r_lo, double r_hi, double* out,
                              nat_stream_t stream); /* (async) */
 
+/* NEXT-3 — Poisson-disk boundary samples ("parallel Poisson disk sampling";
+ * reading R-poisson): phase-group dart throwing over 30 M_target candidates (the a8
+ * construction with Philox tag 2), minimum distance r (r <= 0 => 0.7 sqrt(|Gamma| / M_target)),
+ * cells of size r / sqrt(3) over geom->center +- geom->bound_radius.  Writes M samples,
+ * ascending by candidate index, to samples_out [6][M] (xyz, normal; stride M) and
+ * sample_tri_out [M]; *M_out = M, *r_out = r (optional).  Synchronous (M is a host output).
+ * NAT_ERR_WORKSPACE when ws_bytes < nat_mc_poisson_workspace(...) or M > cap (M_out is
+ * still set); NAT_ERR_INVALID_ARG for M_target < 1, a grid over 1280^3 cells or bad
+ * pointers.  The samples feed nat_mc_surface_pressure through opts->samples_in.           */
+size_t nat_mc_poisson_workspace(const nat_geom* geom, int64_t M_target, double r);
+nat_status nat_mc_poisson_sample(const nat_mesh* mesh, const nat_geom* geom, int64_t M_target, double r,
+                                 uint64_t seed, uint64_t stream_id, double* samples_out, int32_t* sample_tri_out,
+                                 int64_t cap, int64_t* M_out /* [host] */, double* r_out /* [host] or NULL */,
+                                 void* ws, size_t ws_bytes, nat_stream_t stream); /* (sync) */
+
 /* a12 (optional form, "randomly sample theta, phi, and r within an enclosing
  * sphere"; reading R-listen-rand): n points uniform in the volume of the shell
  * R r_lo <= |x - center| <= R r_hi.  Point t: Philox4x32-10 counter (t, 1, stream_lo,

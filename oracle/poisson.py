@@ -56,13 +56,15 @@ def cell_index(y, origin, h, n):
     return np.clip(q, 0, n - 1)
 
 
-def sample(v, t, geom, M_target, seed, stream_id=0, r=None, order=None):
+def sample(v, t, geom, M_target, seed, stream_id=0, r=None, order=None, frame=None):
     """Returns (y (M,3), n (M,3), tri (M,), cand (M,) candidate indices, r).
-    order: optional np.random.Generator shuffling the in-phase cell order (test only)."""
+    order: optional np.random.Generator shuffling the in-phase cell order (test only);
+    frame: optional (centre, R) of the cell grid (default geom's centre / bounding radius)."""
     r = default_radius(geom["total_area"], M_target) if r is None or r <= 0 else float(r)
     n_cand = N_CAND_PER_TARGET * M_target
     y, nrm, tri = mc.sample_uniform(v, t, geom, n_cand, seed, stream_id, tag=2)
-    h, n, origin = grid_of(geom["center"], geom["bound_radius"], r)
+    centre, R = frame if frame is not None else (geom["center"], geom["bound_radius"])
+    h, n, origin = grid_of(centre, R, r)
     ijk = cell_index(y, origin, h, n)
     key = (ijk[:, 2] * n + ijk[:, 1]) * n + ijk[:, 0]
     perm = np.argsort(key, kind="stable")              # candidates by cell, then by index

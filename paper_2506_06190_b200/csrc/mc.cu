@@ -17,17 +17,18 @@
 #include "nat_internal.cuh"
 #include "pair.cuh"
 #include "philox.cuh"
+#include "sampling.cuh"
 #include "radiate.cuh"
 
 namespace {
 
-__global__ void mc_sample_kernel(int64_t M, uint64_t seed, uint64_t stream_id, int64_t nv, int64_t nt,
+__global__ void mc_sample_kernel(int64_t M, uint64_t seed, uint64_t stream_id, uint32_t tag, int64_t nv, int64_t nt,
                                  const double* __restrict__ vx, const int32_t* __restrict__ tri,
                                  const double* __restrict__ nrm, const double* __restrict__ cdf,
                                  double* __restrict__ smp, int32_t* __restrict__ stri) {
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (j >= M) return;
-  uint32_t c0 = (uint32_t)j, c1 = 0u, c2 = (uint32_t)stream_id, c3 = (uint32_t)(stream_id >> 32);
+  uint32_t c0 = (uint32_t)j, c1 = tag, c2 = (uint32_t)stream_id, c3 = (uint32_t)(stream_id >> 32);
   nat::philox4x32_10(c0, c1, c2, c3, (uint32_t)seed, (uint32_t)(seed >> 32));
   const double two32 = 2.3283064365386963e-10;  // 2^-32
   const double u0 = __dmul_rn(__dadd_rn((double)c0, 0.5), two32);
@@ -383,8 +384,14 @@ extern "C" nat_status nat_mc_sample(const nat_mesh* mesh, const nat_geom* geom, 
   NAT_REQUIRE_DEV(geom->area_cdf);
   NAT_REQUIRE_DEV(samples);
   NAT_REQUIRE_DEV(sample_tri);
-  mc_sample_kernel<<<(unsigned)((M + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
-      M, seed, stream_id, mesh->n_vert, mesh->n_tri, mesh->vxyz, mesh->tri, geom->normal, geom->area_cdf,
+  return nat::mc_sample_tagged(mesh, geom, M, seed, stream_id, 0u, samples, sample_tri, (cudaStream_t)stream);
+}
+
+nat_status nat::mc_sample_tagged(const nat_mesh* mesh, const nat_geom* geom, int64_t M, uint64_t seed,
+                                 uint64_t stream_id, uint32_t tag, double* samples, int32_t* sample_tri,
+                                 cudaStream_t stream) {
+  mc_sample_kernel<<<(unsigned)((M + 255) / 256), 256, 0, stream>>>(
+      M, seed, stream_id, tag, mesh->n_vert, mesh->n_tri, mesh->vxyz, mesh->tri, geom->normal, geom->area_cdf,
       samples, sample_tri);
   NAT_LAUNCH_CHECK();
   return NAT_OK;

@@ -110,6 +110,9 @@ _SIGS = {
                                     _P, _SZ, _P]),
     "nat_listener_grid": (C.c_int, [C.POINTER(_D), _D, C.c_int, C.c_int, C.c_int, _D, _D, _P,
                                     _P]),
+    "nat_mc_poisson_workspace": (_SZ, [C.POINTER(_Geom), _I64, _D]),
+    "nat_mc_poisson_sample": (C.c_int, [C.POINTER(_Mesh), C.POINTER(_Geom), _I64, _D, C.c_uint64, C.c_uint64,
+                                        _P, _P, _I64, C.POINTER(_I64), C.POINTER(_D), _P, _SZ, _P]),
     "nat_listener_random_shell": (C.c_int, [C.POINTER(_D), _D, _I64, _D, _D, C.c_uint64, C.c_uint64, _P,
                                             _P]),
 }
@@ -469,6 +472,24 @@ def nat_mc_gather_neumann(g_tri: torch.Tensor, sample_tri: torch.Tensor, out=Non
     out = torch.empty(n_sys, M, dtype=torch.complex128, device=g_tri.device) if out is None else out
     _check(lib().nat_mc_gather_neumann(n_sys, M, n_tri, _ptr(g_tri), _ptr(sample_tri), _ptr(out), _stream()))
     return out
+
+
+def nat_mc_poisson_sample(mesh: Mesh, geom: Geom, M_target: int, seed: int = 0, stream_id: int = 0, r: float = 0.0):
+    """Poisson-disk boundary samples (NEXT-3, reading R-poisson).  Returns (samples (6, M)
+    float64, sample_tri (M,) int32, r)."""
+    dev = mesh.vxyz.device
+    gc = geom.c()
+    ws = _ws(lib().nat_mc_poisson_workspace(C.byref(gc), int(M_target), float(r)), dev)
+    cap = 2 * int(M_target) + 16
+    smp = torch.empty(6 * cap, dtype=torch.float64, device=dev)
+    tri = torch.empty(cap, dtype=torch.int32, device=dev)
+    M = C.c_int64(0)
+    rr = C.c_double(0.0)
+    _check(lib().nat_mc_poisson_sample(C.byref(mesh.c()), C.byref(gc), int(M_target), float(r), int(seed),
+                                       int(stream_id), _ptr(smp), _ptr(tri), cap, C.byref(M), C.byref(rr),
+                                       _ptr(ws), ws.numel(), _stream()))
+    M = M.value
+    return smp[: 6 * M].view(6, M), tri[:M], rr.value
 
 
 def mc_weights(total_area: float, M: int, eps: float = 0.0):
