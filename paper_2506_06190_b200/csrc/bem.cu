@@ -23,11 +23,14 @@
 #include <type_traits>
 #include <vector>
 
+#include <cooperative_groups.h>
+
 #include "f32x2.cuh"
 #include "nat_internal.cuh"
 #include "pair.cuh"
 
 namespace {
+namespace cg = cooperative_groups;
 
 using nat::C2;
 
@@ -748,7 +751,8 @@ __global__ void rhs_final_kernel(int64_t rows, int n_rhs, int n_colblk, const do
 // ------------------------------------------------------------------------------------
 // a6: y = A x, fp64 accumulation; CTA = 8 rows x 256 threads, x reused across rows.
 // ------------------------------------------------------------------------------------
-constexpr int kGemvRows = 8;   // c128 kernel
+constexpr int kGemvRows = 4;   // c128 kernel: rows per cluster
+constexpr int kGemvCS = 4;     // c128 kernel: column chunks = CTAs per cluster
 constexpr int kGemvRows32 = 4; // c64 kernel
 
 // c64 (NAT_FP32) matvec, HBM-bound: CTA = 4 rows x 256 threads, each thread streams two
@@ -865,29 +869,56 @@ __global__ void __launch_bounds__(kThreads, 3) gemv_c64_kernel(int64_t rows, int
   }
 }
 
-__global__ void __launch_bounds__(kThreads) gemv_c128_kernel(int64_t rows, int64_t n, const double2* __restrict__ A,
-                                                            int64_t lda, const double2* __restrict__ x,
-                                                            double2* __restrict__ y,
-                                                            const unsigned long long* __restrict__ skip) {
-  if (skip && *skip == 0ull) return;
+// c128 GEMV: a cluster of kGemvCS CTAs shares one block of kGemvRows rows, each CTA one
+// of kGemvCS fixed column chunks; the chunk partials are summed through distributed shared
+// memory by the cluster's rank-0 CTA in chunk order.  Fixed chunking (independent of the
+// number of rows) keeps every row's summation order, and so y, identical for any row
+// split (bit-identical GMRES iterates across GPU counts).
+__global__ void __cluster_dims__(kGemvCS, 1, 1) __launch_bounds__(kThreads)
+    gemv_c128_kernel(int64_t rows, int64_t n, const double2* __restrict__ A, int64_t lda,
+                     const double2* __restrict__ x, double2* __restrict__ y,
+                     const unsigned long long* __restrict__ skip) {
+  if (skip && *skip == 0ull) return;  // uniform over the grid: whole clusters return
   __shared__ double2 red[kThreads / 32][kGemvRows];
+  __shared__ double2 part[kGemvRows];
+  cg::cluster_group cl = cg::this_cluster();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t r0 = (int64_t)blockIdx.x * kGemvRows;
+  const int chunk = (int)cl.block_rank();
+  const int64_t r0 = (int64_t)(blockIdx.x / kGemvCS) * kGemvRows;
   const int nr = (int)nat::min64(kGemvRows, rows - r0);
+  const int64_t clen = (n + kGemvCS - 1) / kGemvCS;
+  const int64_t c0 = chunk * clen, c1 = nat::min64(n, c0 + clen);
+  // rows past the end re-read the last valid row (results discarded)
+  const double2* Ar[kGemvRows];
+#pragma unroll
+  for (int r = 0; r < kGemvRows; ++r) Ar[r] = A + (r0 + (r < nr ? r : 0)) * lda;
   double ar[kGemvRows], ai[kGemvRows];
 #pragma unroll
   for (int r = 0; r < kGemvRows; ++r) ar[r] = ai[r] = 0.0;
-#pragma unroll 2
-  for (int64_t c = tid; c < n; c += kThreads) {
-    const double2 xv = __ldg(&x[c]);
-    double2 av[kGemvRows];
+  int64_t c = c0 + tid;
+  for (; c + kThreads < c1; c += 2 * kThreads) {  // 2 x (kGemvRows + 1) 16-byte loads in flight
+    double2 av[2][kGemvRows], xv[2];
 #pragma unroll
-    for (int r = 0; r < kGemvRows; ++r)
-      av[r] = r < nr ? __ldcs(&A[(r0 + r) * lda + c]) : make_double2(0.0, 0.0);
+    for (int u = 0; u < 2; ++u) {
+      xv[u] = __ldg(&x[c + u * kThreads]);
+#pragma unroll
+      for (int r = 0; r < kGemvRows; ++r) av[u][r] = __ldcs(&Ar[r][c + u * kThreads]);
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+      for (int r = 0; r < kGemvRows; ++r) {
+        ar[r] = fma(av[u][r].x, xv[u].x, fma(-av[u][r].y, xv[u].y, ar[r]));
+        ai[r] = fma(av[u][r].x, xv[u].y, fma(av[u][r].y, xv[u].x, ai[r]));
+      }
+  }
+  for (; c < c1; c += kThreads) {
+    const double2 xv = __ldg(&x[c]);
 #pragma unroll
     for (int r = 0; r < kGemvRows; ++r) {
-      ar[r] = fma(av[r].x, xv.x, fma(-av[r].y, xv.y, ar[r]));
-      ai[r] = fma(av[r].x, xv.y, fma(av[r].y, xv.x, ai[r]));
+      const double2 av = __ldcs(&Ar[r][c]);
+      ar[r] = fma(av.x, xv.x, fma(-av.y, xv.y, ar[r]));
+      ai[r] = fma(av.x, xv.y, fma(av.y, xv.x, ai[r]));
     }
   }
 #pragma unroll
@@ -900,14 +931,25 @@ __global__ void __launch_bounds__(kThreads) gemv_c128_kernel(int64_t rows, int64
     if (lane == 0) red[warp][r] = make_double2(ar[r], ai[r]);
   }
   __syncthreads();
-  if (tid < nr) {
+  if (tid < kGemvRows) {
     double2 s = red[0][tid];
     for (int w = 1; w < kThreads / 32; ++w) {
       s.x += red[w][tid].x;
       s.y += red[w][tid].y;
     }
+    part[tid] = s;
+  }
+  cl.sync();
+  if (chunk == 0 && tid < nr) {
+    double2 s = part[tid];
+    for (int q = 1; q < kGemvCS; ++q) {
+      const double2 v = cl.map_shared_rank(part, q)[tid];
+      s.x += v.x;
+      s.y += v.y;
+    }
     y[r0 + tid] = s;
   }
+  cl.sync();  // the other CTAs' shared memory stays alive until rank 0 has read it
 }
 
 // ------------------------------------------------------------------------------------
@@ -1176,6 +1218,20 @@ extern "C" nat_status nat_bem_assemble(const nat_mesh* mesh, const nat_geom* geo
 #undef NAT_ASM
 }
 
+namespace {
+void launch_gemv(nat_prec prec, int64_t rows, int64_t n, const void* A, int64_t lda, const void* x, void* y,
+                 const unsigned long long* skip, cudaStream_t s) {
+  if (prec == NAT_FP32) {
+    const unsigned grid = (unsigned)((rows + kGemvRows32 - 1) / kGemvRows32);
+    gemv_c64_kernel<<<grid, kThreads, 0, s>>>(rows, n, (const float2*)A, lda, (const double2*)x, (double2*)y, skip);
+  } else {
+    const unsigned grid = (unsigned)(kGemvCS * ((rows + kGemvRows - 1) / kGemvRows));
+    gemv_c128_kernel<<<grid, kThreads, 0, s>>>(rows, n, (const double2*)A, lda, (const double2*)x, (double2*)y,
+                                               skip);
+  }
+}
+}  // namespace
+
 extern "C" nat_status nat_bem_matvec(nat_prec prec, int64_t rows, int64_t n, const void* A, int64_t lda,
                                      const void* x, void* y, nat_stream_t stream) {
   NAT_REQUIRE(prec == NAT_FP32 || prec == NAT_FP64, "bad precision %d", (int)prec);
@@ -1185,14 +1241,7 @@ extern "C" nat_status nat_bem_matvec(nat_prec prec, int64_t rows, int64_t n, con
   NAT_REQUIRE_DEV(A);
   NAT_REQUIRE_DEV(x);
   NAT_REQUIRE_DEV(y);
-  const int rb = prec == NAT_FP32 ? kGemvRows32 : kGemvRows;
-  unsigned grid = (unsigned)((rows + rb - 1) / rb);
-  if (prec == NAT_FP32)
-    gemv_c64_kernel<<<grid, kThreads, 0, (cudaStream_t)stream>>>(rows, n, (const float2*)A, lda,
-                                                                 (const double2*)x, (double2*)y, nullptr);
-  else
-    gemv_c128_kernel<<<grid, kThreads, 0, (cudaStream_t)stream>>>(rows, n, (const double2*)A, lda,
-                                                                  (const double2*)x, (double2*)y, nullptr);
+  launch_gemv(prec, rows, n, A, lda, x, y, nullptr, (cudaStream_t)stream);
   NAT_LAUNCH_CHECK();
   return NAT_OK;
 }
@@ -1201,13 +1250,7 @@ namespace nat {
 // Used by the GMRES driver (gmres.cu).
 nat_status matvec_internal(nat_prec prec, int64_t rows, int64_t n, const void* A, int64_t lda,
                            const void* x, void* y, cudaStream_t s, const unsigned long long* skip) {
-  const int rb = prec == NAT_FP32 ? kGemvRows32 : kGemvRows;
-  unsigned grid = (unsigned)((rows + rb - 1) / rb);
-  if (prec == NAT_FP32)
-    gemv_c64_kernel<<<grid, kThreads, 0, s>>>(rows, n, (const float2*)A, lda, (const double2*)x, (double2*)y, skip);
-  else
-    gemv_c128_kernel<<<grid, kThreads, 0, s>>>(rows, n, (const double2*)A, lda, (const double2*)x, (double2*)y,
-                                               skip);
+  launch_gemv(prec, rows, n, A, lda, x, y, skip, s);
   NAT_LAUNCH_CHECK();
   return NAT_OK;
 }

@@ -1,0 +1,161 @@
+"""Per-config measurements beside bench.py's C2 step (BASELINE.json configs C1, C3, C4, C5
+and the NEXT-3 Poisson sampler): device time with CUDA events (1 warm-up + 3 timed runs,
+median), rates in the units of SURVEY.md §8(d).  Writes one JSON object to stdout.
+
+    python scripts/bench_configs.py > profiles/r01_configs.json
+"""
+import json
+import os
+import statistics
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import nat_inputs as I  # noqa: E402
+from paper_2506_06190_b200 import nat  # noqa: E402
+
+R_PIPE = 148 * 128 * 1965e6 / 24.0
+
+
+def timed(fn, reps=3):
+    fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        out = fn()
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b) * 1e-3)
+    return statistics.median(ts), out
+
+
+def c1(prec):
+    m = I.icosphere(3)
+    mesh = nat.Mesh.from_numpy(m.v, m.t)
+    g = torch.ones(1, m.n_tri, dtype=torch.complex128, device="cuda")
+    lis = nat.nat_listener_grid((0, 0, 0), 1.0, 4, 4, 4)
+
+    def run():
+        geo = nat.nat_mesh_prepare(mesh)
+        near = nat.nat_bem_near_list(mesh, geo)
+        A, b = nat.nat_bem_assemble(mesh, geo, near, 1.0, g, prec=prec)
+        x, info = nat.nat_bem_solve(A, b[0], m.n_tri, tol=1e-6 if prec == "fp32" else 1e-12)
+        src = nat.nat_bem_sources(mesh, geo, x[None], g)
+        return nat.nat_radiate_field(src, [1.0], lis, prec)
+
+    t, out = timed(run)
+    x = lis.T.cpu().numpy()
+    r = np.linalg.norm(x, axis=1)
+    exact = np.exp(1j * (r - 1.0)) / ((1j - 1.0) * r)          # pulsating sphere, a = g = k = 1
+    err = np.linalg.norm(out[0].cpu().numpy() - exact) / np.linalg.norm(exact)
+    return {"seconds": t, "analytic_rel_l2": float(err), "note": "mesh prep + near list + assembly + GMRES + "
+            "radiation to 4^3 listeners, icosphere L3 (1280 tri), g = 1, k = 1"}
+
+
+def c3():
+    m = I.bowl()
+    mesh = nat.Mesh.from_numpy(m.v, m.t)
+    geo = nat.nat_mesh_prepare(mesh)
+    ks = list(I.c3_wavenumbers())
+    g = torch.from_numpy(I.neumann_harmonics(m, 32)).cuda()
+    M = 4096
+    plan = nat.McPlan(M, 32, "fp32", 200, "cuda")
+    t, (smp, stri, p, infos) = timed(lambda: nat.nat_mc_surface_pressure(mesh, geo, ks, g, M, seed=I.SEED,
+                                                                         prec="fp32", plan=plan))
+    iters = [i["iters"] for i in infos]
+    pairs = sum(M * (M - 1) * (1 + it) for it in iters)
+    gs = nat.nat_mc_gather_neumann(g, stri)
+    src = nat.nat_mc_sources(smp, geo.total_area, p, gs, center=geo.center)
+    lis = nat.nat_listener_grid(geo.center, geo.bound_radius, 32, 32, 32)
+    rplan = nat.RadiatePlan(M, 32, lis.shape[1], "fp32", "cuda")
+    out = torch.empty(32, lis.shape[1], dtype=torch.complex128, device="cuda")
+    tr, _ = timed(lambda: nat.nat_radiate_field(src, ks, lis, "fp32", out=out, plan=rplan))
+    tp, (psmp, pstri, r) = timed(lambda: nat.nat_mc_poisson_sample(mesh, geo, M, seed=I.SEED))
+    Mp = psmp.shape[1]
+    plan_p = nat.McPlan(Mp, 32, "fp32", 200, "cuda")
+    tq, (_, _, _, pinfos) = timed(lambda: nat.nat_mc_surface_pressure(
+        mesh, geo, ks, g, Mp, prec="fp32", samples_in=psmp.contiguous(), sample_tri_in=pstri, plan=plan_p))
+    return {"mc_solve_seconds": t, "mc_iters": iters, "mc_pair_evals_per_s": pairs / t,
+            "mc_frac_R_pipe": pairs / t / R_PIPE,
+            "radiation_seconds": tr, "radiation_pair_modes_per_s": M * lis.shape[1] * 32 / tr,
+            "radiation_listener_pt_modes_per_s": lis.shape[1] * 32 / tr,
+            "poisson_sample_seconds": tp, "poisson_M": Mp, "poisson_r": r,
+            "mc_solve_poisson_seconds": tq, "mc_iters_poisson": [i["iters"] for i in pinfos],
+            "note": "bowl 49,664 tri, 32 modes (k a = 0.5 .. 8), M = 4096 uniform samples, tol 1e-6; radiation "
+                    "of the 32 modes fused to the 32^3 grid; Poisson-disk sampler (M_target 4096) and the MC "
+                    "solve on its samples"}
+
+
+def c4(gi=0):
+    m, g8, D = I.c4_geometry(gi)
+    ks = list(I.c4_wavenumbers(D))
+    g = torch.from_numpy(np.tile(g8, (8, 1))).cuda()
+    mesh = nat.Mesh.from_numpy(m.v, m.t)
+    geo = nat.nat_mesh_prepare(mesh)
+    M = 2048
+    plan = nat.McPlan(M, 64, "fp32", 200, "cuda")
+    t, (smp, stri, p, infos) = timed(lambda: nat.nat_mc_surface_pressure(mesh, geo, ks, g, M, seed=I.SEED,
+                                                                         stream_id=gi, prec="fp32", plan=plan))
+    iters = [i["iters"] for i in infos]
+    gs = nat.nat_mc_gather_neumann(g, stri)
+    src = nat.nat_mc_sources(smp, geo.total_area, p, gs, center=geo.center)
+    lis = nat.nat_listener_grid(geo.center, geo.bound_radius, 64, 64, 64)
+    rplan = nat.RadiatePlan(M, 64, lis.shape[1], "fp32", "cuda")
+    out = torch.empty(64, lis.shape[1], dtype=torch.complex128, device="cuda")
+    tr, _ = timed(lambda: nat.nat_radiate_field(src, ks, lis, "fp32", out=out, plan=rplan))
+    pm = M * lis.shape[1] * 64
+    return {"n_tri": m.n_tri, "mc_solve_seconds": t, "mc_iters_min_max": [min(iters), max(iters)],
+            "radiation_seconds": tr, "radiation_pair_modes_per_s": pm / tr,
+            "radiation_listener_pt_modes_per_s": lis.shape[1] * 64 / tr,
+            "radiation_frac_R_sfu_multimode": pm / tr / 2.31e12,
+            "note": f"geometry {gi} (bowl over slab), M = 2048, 64 wavenumbers batched; radiation of all 64 fused "
+                    "to the 64^3 grid (roofline per pair-mode for fused modes: R_sfu 2.31e12, SURVEY §8d)"}
+
+
+def c5(rows=1024):
+    m = I.cubed_sphere(129)
+    gt = torch.from_numpy(I.neumann_rigid_z(m)[None]).cuda()
+    mesh = nat.Mesh.from_numpy(m.v, m.t)
+    geo = nat.nat_mesh_prepare(mesh)
+    near = nat.nat_bem_near_list(mesh, geo, 0, rows)
+    A = torch.empty(rows, m.n_tri, dtype=torch.complex128, device="cuda")
+    ta, _ = timed(lambda: nat.nat_bem_assemble(mesh, geo, near, 8.0, gt, prec="fp64", A=A, lda=m.n_tri))
+    nS = int((near.cls == 1).sum().item())
+    pairs = rows * m.n_tri * 3 + nS * 448 + (near.nnz - nS) * 28 + rows * 48
+    x = torch.from_numpy(I.random_complex(m.n_tri, 1)).cuda()
+    y = torch.empty(rows, dtype=torch.complex128, device="cuda")
+    tg, _ = timed(lambda: nat.nat_bem_matvec(A, x, n=m.n_tri, out=y), reps=5)
+    pv = torch.from_numpy(I.random_complex(m.n_tri, 2)[None]).cuda()
+    src = nat.nat_bem_sources(mesh, geo, pv, gt)
+    lis = nat.nat_listener_grid((0, 0, 0), 1.0, 8, 8, 8)
+    tr, _ = timed(lambda: nat.nat_radiate_field(src, [8.0], lis, "fp64"), reps=1)
+    return {"rows": rows, "n_tri": m.n_tri, "fp64_assembly_seconds": ta, "fp64_assembly_pair_evals_per_s": pairs / ta,
+            "c128_gemv_seconds": tg, "c128_gemv_GBps": rows * m.n_tri * 16 / tg / 1e9,
+            "fp64_radiation_seconds": tr, "fp64_radiation_listener_pts_per_s": lis.shape[1] / tr,
+            "fp64_radiation_pair_evals_per_s": 3 * m.n_tri * lis.shape[1] / tr,
+            "note": "cubed sphere 199,692 tri, one rank's row block at ka = 8 (fp64, c128 matrix), its GEMV, fp64 "
+                    "radiation of all 599,076 sources to an 8^3 grid"}
+
+
+def main():
+    torch.cuda.set_device(0)
+    nat.lib()
+    res = {"device": torch.cuda.get_device_name(0)}
+    for name, fn in (("C1_fp32", lambda: c1("fp32")), ("C1_fp64", lambda: c1("fp64")), ("C3", c3), ("C4", c4),
+                     ("C5", c5)):
+        try:
+            res[name] = fn()
+        except Exception as ex:  # pragma: no cover - reported, not fatal
+            res[name] = {"error": repr(ex)}
+        print(f"[configs] {name} done", file=sys.stderr, flush=True)
+    print(json.dumps(res, indent=1))
+
+
+if __name__ == "__main__":
+    main()
