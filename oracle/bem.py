@@ -18,6 +18,15 @@ The oracle forms every entry directly with its final rule (no far-then-correct).
 Pinned by tests/test_oracle_bem.py: Gauss identity at k = 0, sphere eigenvalues of V
 and K, brute-force entries on tiny meshes, pulsating/oscillating sphere and interior
 point-source solutions within 2%.
+
+NEXT-1, Burton-Miller (``bm=True``): Eq. BM exactly as printed (l.176-177), beta = i/k,
+with outward normals (reading R-bm):
+    1/2 p - K p - beta W p = -V g - beta K' g - (beta/2) g,
+    K'_ij = int_{T_j} dG/dn_x(c_i, y) dS,  W_ij = int_{T_j} d2G/dn_x dn_y(c_i, y) dS,
+same rules per class; self: K'_ii = 0 (flat triangle), W_ii by the polar finite part of
+quadrature.self_hypersingular.  Pinned by tests/test_oracle_bm.py (finite-difference
+kernels, the finite part against a punctured polar integral, sphere eigenvalues of W and
+K', solutions at a CBIE-singular wavenumber).
 """
 import numpy as np
 
@@ -33,8 +42,9 @@ def _opts(opts):
     return o
 
 
-def _entries(x, v1, v2, v3, n, area, lam, w, k):
-    """K, V for one collocation point x against triangles (m,3) with rule (lam, w)."""
+def _entries(x, v1, v2, v3, n, area, lam, w, k, nx=None):
+    """K, V (and with the collocation normal nx also K', W) for one collocation point x
+    against triangles (m,3) with rule (lam, w)."""
     # points (m, Q, 3)
     y = (lam[None, :, 0:1] * v1[:, None, :] + lam[None, :, 1:2] * v2[:, None, :]) \
         + lam[None, :, 2:3] * v3[:, None, :]
@@ -42,11 +52,17 @@ def _entries(x, v1, v2, v3, n, area, lam, w, k):
     dG = kernel.green_dn_y(x[None, None, :], y, n[:, None, :], k)
     K = area * np.sum(w[None, :] * dG, axis=1)
     V = area * np.sum(w[None, :] * G, axis=1)
-    return K, V
+    if nx is None:
+        return K, V
+    dGx = kernel.green_dn_x(x[None, None, :], y, nx[None, None, :], k)
+    d2G = kernel.green_dn_x_dn_y(x[None, None, :], y, nx[None, None, :], n[:, None, :], k)
+    Kp = area * np.sum(w[None, :] * dGx, axis=1)
+    W = area * np.sum(w[None, :] * d2G, axis=1)
+    return K, V, Kp, W
 
 
-def assemble(v, t, geom, k, g=None, rows=None, opts=None, near=None, return_V=False):
-    """Rows ``rows`` (default all) of A and b = -V g.
+def assemble(v, t, geom, k, g=None, rows=None, opts=None, near=None, return_V=False, bm=False):
+    """Rows ``rows`` (default all) of A and b = -V g (bm: the Burton-Miller A and b).
 
     v (V,3), t (N,3); geom from geometry.mesh_prepare; g (n_rhs, N) complex or None.
     Returns A (len(rows), N) complex128, b (n_rhs, len(rows)) [, V rows]."""
@@ -63,29 +79,43 @@ def assemble(v, t, geom, k, g=None, rows=None, opts=None, near=None, return_V=Fa
     if near is None:
         near = nearlist.near_list(t, c, geom["diam"], o["near_eta"], rows=rows)
     rp, col, cls = near
+    if bm and not k > 0:
+        raise ValueError("Burton-Miller needs k > 0 (beta = i/k)")
+    beta = 1j / k if bm else 0.0
     A = np.zeros((len(rows), N), dtype=np.complex128)
-    Vm = np.zeros((len(rows), N), dtype=np.complex128)
+    Vm = np.zeros((len(rows), N), dtype=np.complex128)   # V (+ beta K' with bm): the RHS operator
     for r, i in enumerate(rows):
         x = c[i]
+        nx = nrm[i] if bm else None
         idx = np.arange(N)
         idx = idx[idx != i]
         K, V = np.zeros(N, np.complex128), np.zeros(N, np.complex128)
-        K[idx], V[idx] = _entries(x, V1[idx], V2[idx], V3[idx], nrm[idx], area[idx],
-                                  lam_f, w_f, k)
+        Kp, W = np.zeros(N, np.complex128), np.zeros(N, np.complex128)
+        parts = [(idx, lam_f, w_f)]
         js, cl = col[rp[r]:rp[r + 1]], cls[rp[r]:rp[r + 1]]
         for code, lam, w in ((nearlist.CLS_S, lam_s, w_s), (nearlist.CLS_N, lam_n, w_n)):
             j = js[cl == code]
             if j.size:
-                K[j], V[j] = _entries(x, V1[j], V2[j], V3[j], nrm[j], area[j], lam, w, k)
+                parts.append((j, lam, w))
+        for j, lam, w in parts:     # near rules overwrite the far ones
+            e = _entries(x, V1[j], V2[j], V3[j], nrm[j], area[j], lam, w, k, nx)
+            K[j], V[j] = e[0], e[1]
+            if bm:
+                Kp[j], W[j] = e[2], e[3]
         K[i] = 0.0
         V[i] = quadrature.self_single_layer(V1[i], V2[i], V3[i], k, o["self_theta_pts"])
-        A[r] = -K
+        if bm:
+            Kp[i] = 0.0
+            W[i] = quadrature.self_hypersingular(V1[i], V2[i], V3[i], k, o["self_theta_pts"])
+        A[r] = -K - beta * W
         A[r, i] += 0.5
-        Vm[r] = V
+        Vm[r] = V + beta * Kp
     b = None
     if g is not None:
         g = np.atleast_2d(np.asarray(g, dtype=np.complex128))
         b = -(Vm @ g.T).T
+        if bm:
+            b -= 0.5 * beta * g[:, rows]
     return (A, b, Vm) if return_V else (A, b)
 
 

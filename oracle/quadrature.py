@@ -134,3 +134,43 @@ def self_single_layer_k0_closed(v1, v2, v3):
         s0, s1 = np.dot(a - foot, u), np.dot(b - foot, u)
         tot += h * (math.asinh(s1 / h) - math.asinh(s0 / h))
     return tot / (4.0 * np.pi)
+
+
+def self_hypersingular(v1, v2, v3, k, n_gl: int = 16):
+    """W_ii = f.p. int_T d2G/dn_x dn_y(c, y) dS(y) at the centroid c of the flat triangle
+    (reading R-bm-self): there d.n_x = d.n_y = 0 and n_x.n_y = 1, so the integrand is
+    e^{ikr}(1 - ikr)/(4 pi r^3); in polar coordinates about c, with
+    int_0^R e^{ik rho}(1 - ik rho)/rho^2 d rho = [-e^{ik rho}/rho], the Hadamard finite part is
+        W_ii = ik/2 - (1/4pi) oint e^{ik R(theta)} / R(theta) d theta,
+    and per edge (distance h_e, s = h sinh u along the edge) d theta / R = du / (h cosh^2 u):
+        W_ii = ik/2 - (1/4pi) sum_e (1/h_e) int e^{ik h_e cosh u} / cosh^2 u du   (GL n_gl in u)."""
+    v1, v2, v3 = (np.asarray(a, dtype=np.float64) for a in (v1, v2, v3))
+    c = ((v1 + v2) + v3) / 3.0
+    xg, wg = np.polynomial.legendre.leggauss(n_gl)
+    total = 0.0 + 0.0j
+    for a, b in ((v1, v2), (v2, v3), (v3, v1)):
+        L = np.linalg.norm(b - a)
+        e = (b - a) / L
+        foot = a + np.dot(c - a, e) * e
+        h = np.linalg.norm(c - foot)
+        s0, s1 = np.dot(a - foot, e), np.dot(b - foot, e)
+        u0, u1 = math.asinh(s0 / h), math.asinh(s1 / h)
+        half, mid = (u1 - u0) / 2, (u1 + u0) / 2
+        u = mid + half * xg
+        ch = np.cosh(u)
+        total += np.sum(wg * half * np.exp(1j * k * h * ch) / (ch * ch)) / h
+    return 0.5j * k - total / (4.0 * np.pi)
+
+
+def self_hypersingular_k0_closed(v1, v2, v3):
+    """k = 0: W_ii = -(1/4pi) sum_e (sin a1 - sin a0)/h_e, sin a = s / sqrt(s^2 + h^2)."""
+    v1, v2, v3 = (np.asarray(a, dtype=np.float64) for a in (v1, v2, v3))
+    c = (v1 + v2 + v3) / 3.0
+    tot = 0.0
+    for a, b in ((v1, v2), (v2, v3), (v3, v1)):
+        e = (b - a) / np.linalg.norm(b - a)
+        foot = a + np.dot(c - a, e) * e
+        h = np.linalg.norm(c - foot)
+        s0, s1 = np.dot(a - foot, e), np.dot(b - foot, e)
+        tot += (s1 / math.hypot(s1, h) - s0 / math.hypot(s0, h)) / h
+    return -tot / (4.0 * np.pi)
