@@ -94,6 +94,9 @@ typedef struct {
   int near_levels_N;  /* same for close pairs, default 1                                     */
   double near_eta;    /* class N: |c_i - c_j| < near_eta * diam_j, default 4                 */
   int self_theta_pts; /* Gauss-Legendre points per edge of the polar self term, default 16   */
+  int burton_miller;  /* NEXT-1: 0 = the CBIE (beta = 0, default); 1 = Eq. BM as printed with    */
+                      /* beta = i/k (reading R-bm): A = 1/2 I - K - beta W,            */
+                      /* b = -(V + beta K') g - (beta/2) g; needs k > 0                            */
 } nat_quad_opts;
 
 /* ---------------------------------------------------------------------------------

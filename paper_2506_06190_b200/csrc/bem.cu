@@ -149,11 +149,13 @@ void gauss_legendre(int n, std::vector<double>& x, std::vector<double>& w) {
 struct Opts {
   int far_pts, lev_S, lev_N, gl;
   double eta;
+  bool bm;  // Burton-Miller (NEXT-1, reading R-bm)
 };
 
 Opts opts_of(const nat_quad_opts* o) {
-  Opts r{3, 3, 1, 16, 4.0};
+  Opts r{3, 3, 1, 16, 4.0, false};
   if (o) {
+    r.bm = o->burton_miller != 0;
     if (o->far_pts) r.far_pts = o->far_pts;
     if (o->near_levels_S) r.lev_S = o->near_levels_S;
     if (o->near_levels_N) r.lev_N = o->near_levels_N;
@@ -205,6 +207,20 @@ __device__ __forceinline__ void far_entry(const R (&y)[NQ][3], const R (&w)[NQ],
                             Kr, Ki);
 }
 
+// Far-rule RHS operator entry of Burton-Miller: (V + beta K')_ij with beta = i/k, i.e.
+// (V.x - K'.y / k, V.y + K'.x / k); m = the target's normal n_x.
+template <typename R, int NQ>
+__device__ __forceinline__ void far_entry_bm_rhs(const R (&y)[NQ][3], const R (&w)[NQ], R nx, R ny, R nz, R mx,
+                                                 R my, R mz, R cx, R cy, R cz, R k, R& Br, R& Bi) {
+  nat::C2<R> V{R(0), R(0)}, K{R(0), R(0)}, Kp{R(0), R(0)}, W{R(0), R(0)};
+#pragma unroll
+  for (int q = 0; q < NQ; ++q)
+    nat::pair_accumulate_bm<R>(y[q][0] - cx, y[q][1] - cy, y[q][2] - cz, nx, ny, nz, mx, my, mz, w[q], k, V, K,
+                               Kp, W);
+  Br = V.x - Kp.y / k;
+  Bi = V.y + Kp.x / k;
+}
+
 template <typename R>
 __device__ __forceinline__ void store_entry(void* A, size_t idx, R re, R im) {
   if constexpr (sizeof(R) == 4)
@@ -218,6 +234,7 @@ struct FarArgs {
   int64_t n, row_begin, rows, lda;
   FarCols<R> cols;
   const double* cen;     // geom centroid [3][n]
+  const double* nrm;     // geom normal [3][n] (Burton-Miller: the rows' n_x)
   double cx, cy, cz;
   R k;
   int n_rhs, rhs0;       // this pass covers rhs [rhs0, rhs0 + NR)
@@ -227,9 +244,12 @@ struct FarArgs {
   double2* bpart;        // [n_colblk][n_rhs][rows]
 };
 
-template <typename R, int NQ, int NR>
+// Generic far assembly (fp64, and fp32 Burton-Miller).  BM: A_ij = -K_ij - beta W_ij and
+// the RHS operator V + beta K' (beta = i/k, reading R-bm).
+template <typename R, int NQ, int NR, bool BM = false>
 __global__ void __launch_bounds__(kThreads) far_kernel(FarArgs<R> a) {
   __shared__ R s_c[3][kTI];
+  __shared__ R s_m[3][kTI];  // BM: row normals
   __shared__ double2 s_red[kThreads / 32][kTI][NR > 0 ? NR : 1];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t i0 = (int64_t)blockIdx.y * kTI;
@@ -240,6 +260,11 @@ __global__ void __launch_bounds__(kThreads) far_kernel(FarArgs<R> a) {
     s_c[0][tid] = (R)(a.cen[i] - a.cx);
     s_c[1][tid] = (R)(a.cen[n + i] - a.cy);
     s_c[2][tid] = (R)(a.cen[2 * n + i] - a.cz);
+    if constexpr (BM) {
+      s_m[0][tid] = (R)a.nrm[i];
+      s_m[1][tid] = (R)a.nrm[n + i];
+      s_m[2][tid] = (R)a.nrm[2 * n + i];
+    }
   }
   __syncthreads();
   const int nrows = (int)nat::min64(kTI, a.rows - i0);
@@ -272,7 +297,20 @@ __global__ void __launch_bounds__(kThreads) far_kernel(FarArgs<R> a) {
     for (int t = 0; t < kTI; ++t) {
       if (t < nrows) {
         R Vr, Vi, Kr, Ki;
-        far_entry<R, NQ>(y, w, nx, ny, nz, s_c[0][t], s_c[1][t], s_c[2][t], a.k, Vr, Vi, Kr, Ki);
+        if constexpr (BM) {
+          C2<R> V{R(0), R(0)}, K{R(0), R(0)}, Kp{R(0), R(0)}, W{R(0), R(0)};
+#pragma unroll
+          for (int q = 0; q < NQ; ++q)
+            nat::pair_accumulate_bm<R>(y[q][0] - s_c[0][t], y[q][1] - s_c[1][t], y[q][2] - s_c[2][t], nx, ny, nz,
+                                       s_m[0][t], s_m[1][t], s_m[2][t], w[q], a.k, V, K, Kp, W);
+          // A = -K - (i/k) W;  RHS operator V + (i/k) K'
+          Kr = K.x - W.y / a.k;
+          Ki = K.y + W.x / a.k;
+          Vr = V.x - Kp.y / a.k;
+          Vi = V.y + Kp.x / a.k;
+        } else {
+          far_entry<R, NQ>(y, w, nx, ny, nz, s_c[0][t], s_c[1][t], s_c[2][t], a.k, Vr, Vi, Kr, Ki);
+        }
         if (a.store_A && valid) store_entry<R>(a.A, (size_t)(i0 + t) * a.lda + j, -Kr, -Ki);
 #pragma unroll
         for (int q = 0; q < NR; ++q) {
@@ -460,8 +498,10 @@ __global__ void __launch_bounds__(kThreads, 2) far_kernel_x2(FarArgs<float> a) {
 }
 
 template <typename R, int NQ, int NR>
-void launch_far(dim3 grid, const FarArgs<R>& fa, cudaStream_t s) {
-  if constexpr (sizeof(R) == 4)
+void launch_far(dim3 grid, const FarArgs<R>& fa, bool bm, cudaStream_t s) {
+  if (bm)
+    far_kernel<R, NQ, NR, true><<<grid, kThreads, 0, s>>>(fa);
+  else if constexpr (sizeof(R) == 4)
     far_kernel_x2<NQ, NR><<<grid, kThreads, 0, s>>>(fa);
   else
     far_kernel<R, NQ, NR><<<grid, kThreads, 0, s>>>(fa);
@@ -497,11 +537,11 @@ struct NearArgs {
 // The rule table is staged in shared memory (all groups walk it in the same order).
 constexpr int kMaxNearPts = 7 << 8;  // up to 4 subdivision levels x 7 points (S: 448 at 3)
 
-template <typename R, int NQ, int G>
+template <typename R, int NQ, int G, bool BM>
 __device__ __forceinline__ void near_item(const NearArgs<R>& a, int64_t gid, int lig, const float4* s_rf,
                                           const double4* s_rd);
 
-template <typename R, int NQ, int G>
+template <typename R, int NQ, int G, bool BM = false>
 __global__ void __launch_bounds__(kThreads) near_kernel(NearArgs<R> a) {
   extern __shared__ __align__(16) unsigned char near_smem[];
   float4* s_rf = reinterpret_cast<float4*>(near_smem);
@@ -519,10 +559,10 @@ __global__ void __launch_bounds__(kThreads) near_kernel(NearArgs<R> a) {
   const int lig = threadIdx.x % G;
   const int64_t stride = (int64_t)gridDim.x * (blockDim.x / G);
   for (int64_t gid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G; gid < nitems; gid += stride)
-    near_item<R, NQ, G>(a, gid, lig, s_rf, s_rd);
+    near_item<R, NQ, G, BM>(a, gid, lig, s_rf, s_rd);
 }
 
-template <typename R, int NQ, int G>
+template <typename R, int NQ, int G, bool BM>
 __device__ __forceinline__ void near_item(const NearArgs<R>& a, int64_t gid, int lig, const float4* s_rf,
                                           const double4* s_rd) {
   const int2 item = a.items[gid];
@@ -540,7 +580,15 @@ __device__ __forceinline__ void near_item(const NearArgs<R>& a, int64_t gid, int
     for (int d = 0; d < 3; ++d) v[p][d] = a.vx[d * a.nv + vid[p]];
   const R nx = (R)a.nrm[j], ny = (R)a.nrm[n + j], nz = (R)a.nrm[2 * n + j];
   const double wA = a.area[j] * nat::kInv4Pi;
-  R Vr = 0, Vi = 0, Kr = 0, Ki = 0;
+  // Burton-Miller: the row's normal n_x (reading R-bm)
+  const R mx = BM ? (R)a.nrm[i] : R(0), my = BM ? (R)a.nrm[n + i] : R(0), mz = BM ? (R)a.nrm[2 * n + i] : R(0);
+  C2<R> V{R(0), R(0)}, K{R(0), R(0)}, Kp{R(0), R(0)}, W{R(0), R(0)};
+  auto acc = [&](R dx, R dy, R dz, R wq) {
+    if constexpr (BM)
+      nat::pair_accumulate_bm<R>(dx, dy, dz, nx, ny, nz, mx, my, mz, wq, a.k, V, K, Kp, W);
+    else
+      nat::pair_accumulate<R>(dx, dy, dz, nx, ny, nz, wq, a.k, V.x, V.y, K.x, K.y);
+  };
   if constexpr (sizeof(R) == 4) {
     // fp32 path: vertex offsets from the collocation point are formed in fp64 once per
     // pair and rounded (|v - c_i| ~ element size, so the rounding is relative to r);
@@ -556,7 +604,7 @@ __device__ __forceinline__ void near_item(const NearArgs<R>& a, int64_t gid, int
       float d[3];
 #pragma unroll
       for (int c = 0; c < 3; ++c) d[c] = fmaf(L.z, e[2][c], fmaf(L.y, e[1][c], L.x * e[0][c]));
-      nat::pair_accumulate<float>(d[0], d[1], d[2], nx, ny, nz, L.w * wAf, a.k, Vr, Vi, Kr, Ki);
+      acc(d[0], d[1], d[2], L.w * wAf);
     }
   } else {
     for (int q = lig; q < a.npts; q += G) {
@@ -564,19 +612,33 @@ __device__ __forceinline__ void near_item(const NearArgs<R>& a, int64_t gid, int
       R d[3];
 #pragma unroll
       for (int c = 0; c < 3; ++c) d[c] = (R)(((L.x * v[0][c] + L.y * v[1][c]) + L.z * v[2][c]) - ci[c]);
-      nat::pair_accumulate<R>(d[0], d[1], d[2], nx, ny, nz, (R)(L.w * wA), a.k, Vr, Vi, Kr, Ki);
+      acc(d[0], d[1], d[2], (R)(L.w * wA));
     }
   }
   if constexpr (G > 1) {
     const unsigned mask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << ((threadIdx.x & 31) / G * G));
+    auto red = [&](R& x) {
 #pragma unroll
-    for (int o = G / 2; o > 0; o >>= 1) {
-      Vr += __shfl_xor_sync(mask, Vr, o, G);
-      Vi += __shfl_xor_sync(mask, Vi, o, G);
-      Kr += __shfl_xor_sync(mask, Kr, o, G);
-      Ki += __shfl_xor_sync(mask, Ki, o, G);
+      for (int o = G / 2; o > 0; o >>= 1) x += __shfl_xor_sync(mask, x, o, G);
+    };
+    red(V.x);
+    red(V.y);
+    red(K.x);
+    red(K.y);
+    if constexpr (BM) {
+      red(Kp.x);
+      red(Kp.y);
+      red(W.x);
+      red(W.y);
     }
     if (lig != 0) return;
+  }
+  R Vr = V.x, Vi = V.y, Kr = K.x, Ki = K.y;
+  if constexpr (BM) {  // A = -K - (i/k) W;  RHS operator V + (i/k) K'
+    Kr = K.x - W.y / a.k;
+    Ki = K.y + W.x / a.k;
+    Vr = V.x - Kp.y / a.k;
+    Vi = V.y + Kp.x / a.k;
   }
   store_entry<R>(a.A, (size_t)r * a.lda + j, -Kr, -Ki);
   if (a.n_rhs > 0) {
@@ -589,8 +651,12 @@ __device__ __forceinline__ void near_item(const NearArgs<R>& a, int64_t gid, int
       w[q] = a.cols.qw[(size_t)q * n + j];
     }
     R fVr, fVi, fKr, fKi;
-    far_entry<R, NQ>(y, w, a.cols.nrm[j], a.cols.nrm[n + j], a.cols.nrm[2 * n + j],
-                     (R)(ci[0] - a.cx), (R)(ci[1] - a.cy), (R)(ci[2] - a.cz), a.k, fVr, fVi, fKr, fKi);
+    if constexpr (BM)
+      far_entry_bm_rhs<R, NQ>(y, w, a.cols.nrm[j], a.cols.nrm[n + j], a.cols.nrm[2 * n + j], mx, my, mz,
+                              (R)(ci[0] - a.cx), (R)(ci[1] - a.cy), (R)(ci[2] - a.cz), a.k, fVr, fVi);
+    else
+      far_entry<R, NQ>(y, w, a.cols.nrm[j], a.cols.nrm[n + j], a.cols.nrm[2 * n + j],
+                       (R)(ci[0] - a.cx), (R)(ci[1] - a.cy), (R)(ci[2] - a.cz), a.k, fVr, fVi, fKr, fKi);
     const double dVr = (double)Vr - (double)fVr, dVi = (double)Vi - (double)fVi;
     for (int q = 0; q < a.n_rhs; ++q) {
       double2 gv = a.g[(size_t)q * n + j];
@@ -640,25 +706,68 @@ __device__ void self_single_layer(const double (&v)[3][3], const double (&c)[3],
   Vi *= nat::kInv4Pi;
 }
 
-template <typename R, int NQ>
+// Polar finite part of the hypersingular self term (reading R-bm-self):
+// W_ii = ik/2 - 1/(4 pi) sum_e (1/h_e) int e^{ik h_e cosh u} / cosh^2 u du.
+__device__ void self_hypersingular(const double (&v)[3][3], const double (&c)[3], double k, const double* glx,
+                                   const double* glw, int ngl, double& Wr, double& Wi) {
+  double tr = 0, ti = 0;
+  for (int e = 0; e < 3; ++e) {
+    const double* A = v[e];
+    const double* B = v[(e + 1) % 3];
+    double ab[3] = {B[0] - A[0], B[1] - A[1], B[2] - A[2]};
+    double L = sqrt(ab[0] * ab[0] + ab[1] * ab[1] + ab[2] * ab[2]);
+    double u[3] = {ab[0] / L, ab[1] / L, ab[2] / L};
+    double ca[3] = {c[0] - A[0], c[1] - A[1], c[2] - A[2]};
+    double tproj = ca[0] * u[0] + ca[1] * u[1] + ca[2] * u[2];
+    double foot[3] = {A[0] + tproj * u[0], A[1] + tproj * u[1], A[2] + tproj * u[2]};
+    double hv[3] = {c[0] - foot[0], c[1] - foot[1], c[2] - foot[2]};
+    double h = sqrt(hv[0] * hv[0] + hv[1] * hv[1] + hv[2] * hv[2]);
+    double s0 = (A[0] - foot[0]) * u[0] + (A[1] - foot[1]) * u[1] + (A[2] - foot[2]) * u[2];
+    double s1 = (B[0] - foot[0]) * u[0] + (B[1] - foot[1]) * u[1] + (B[2] - foot[2]) * u[2];
+    double u0 = asinh(s0 / h), u1 = asinh(s1 / h);
+    double half = 0.5 * (u1 - u0), mid = 0.5 * (u1 + u0);
+    double er = 0, ei = 0;
+    for (int g = 0; g < ngl; ++g) {
+      const double ch = cosh(mid + half * glx[g]);
+      double sn, cs;
+      sincos(k * h * ch, &sn, &cs);
+      const double wq = glw[g] / (ch * ch);
+      er += wq * cs;
+      ei += wq * sn;
+    }
+    tr += half * er / h;
+    ti += half * ei / h;
+  }
+  Wr = -tr * nat::kInv4Pi;
+  Wi = 0.5 * k - ti * nat::kInv4Pi;
+}
+
+template <typename R, int NQ, bool BM = false>
 __global__ void self_kernel(int64_t n, int64_t nv, int64_t row_begin, int64_t rows, int64_t lda,
                             const double* __restrict__ vx, const int32_t* __restrict__ tri,
-                            const double* __restrict__ cen, FarCols<R> cols, double cx, double cy,
+                            const double* __restrict__ cen, const double* __restrict__ nrm_rows,
+                            FarCols<R> cols, double cx, double cy,
                             double cz, double k, const double* glx, const double* glw, int ngl,
                             int n_rhs, const double2* __restrict__ g, void* A,
                             double2* __restrict__ corr_self) {
   int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (r >= rows) return;
   int64_t i = row_begin + r;
-  store_entry<R>(A, (size_t)r * lda + i, R(0.5), R(0));  // K_ii = 0 on a flat triangle
-  if (n_rhs == 0) return;
   double v[3][3], c[3] = {cen[i], cen[n + i], cen[2 * n + i]};
   for (int p = 0; p < 3; ++p) {
     int vi = tri[p * n + i];
     for (int d = 0; d < 3; ++d) v[p][d] = vx[d * nv + vi];
   }
+  if constexpr (BM) {  // A_ii = 1/2 - (i/k) W_ii  (K_ii = 0 on a flat triangle)
+    double Wr, Wi;
+    self_hypersingular(v, c, k, glx, glw, ngl, Wr, Wi);
+    store_entry<R>(A, (size_t)r * lda + i, (R)(0.5 + Wi / k), (R)(-Wr / k));
+  } else {
+    store_entry<R>(A, (size_t)r * lda + i, R(0.5), R(0));  // K_ii = 0 on a flat triangle
+  }
+  if (n_rhs == 0) return;
   double Vr, Vi;
-  self_single_layer(v, c, k, glx, glw, ngl, Vr, Vi);
+  self_single_layer(v, c, k, glx, glw, ngl, Vr, Vi);  // K'_ii = 0 too: the RHS operator is V_ii
   R y[NQ][3], w[NQ];
 #pragma unroll
   for (int q = 0; q < NQ; ++q) {
@@ -668,12 +777,22 @@ __global__ void self_kernel(int64_t n, int64_t nv, int64_t row_begin, int64_t ro
     w[q] = cols.qw[(size_t)q * n + i];
   }
   R fVr, fVi, fKr, fKi;
-  far_entry<R, NQ>(y, w, cols.nrm[i], cols.nrm[n + i], cols.nrm[2 * n + i], (R)(c[0] - cx),
-                   (R)(c[1] - cy), (R)(c[2] - cz), (R)k, fVr, fVi, fKr, fKi);
+  const R mx = (R)nrm_rows[i], my = (R)nrm_rows[n + i], mz = (R)nrm_rows[2 * n + i];
+  if constexpr (BM)
+    far_entry_bm_rhs<R, NQ>(y, w, cols.nrm[i], cols.nrm[n + i], cols.nrm[2 * n + i], mx, my, mz, (R)(c[0] - cx),
+                            (R)(c[1] - cy), (R)(c[2] - cz), (R)k, fVr, fVi);
+  else
+    far_entry<R, NQ>(y, w, cols.nrm[i], cols.nrm[n + i], cols.nrm[2 * n + i], (R)(c[0] - cx),
+                     (R)(c[1] - cy), (R)(c[2] - cz), (R)k, fVr, fVi, fKr, fKi);
   double dVr = Vr - (double)fVr, dVi = Vi - (double)fVi;
   for (int q = 0; q < n_rhs; ++q) {
     double2 gv = g[(size_t)q * n + i];
-    corr_self[(size_t)r * n_rhs + q] = make_double2(-(dVr * gv.x - dVi * gv.y), -(dVr * gv.y + dVi * gv.x));
+    double2 cs = make_double2(-(dVr * gv.x - dVi * gv.y), -(dVr * gv.y + dVi * gv.x));
+    if constexpr (BM) {  // - (beta/2) g_i = -(i / 2k) g_i
+      cs.x += gv.y / (2.0 * k);
+      cs.y -= gv.x / (2.0 * k);
+    }
+    corr_self[(size_t)r * n_rhs + q] = cs;
   }
 }
 
@@ -1020,6 +1139,7 @@ nat_status assemble_impl(const nat_mesh* mesh, const nat_geom* geom, const Opts&
   fa.lda = lda;
   fa.cols = cols;
   fa.cen = geom->centroid;
+  fa.nrm = geom->normal;
   fa.cx = cx;
   fa.cy = cy;
   fa.cz = cz;
@@ -1032,15 +1152,15 @@ nat_status assemble_impl(const nat_mesh* mesh, const nat_geom* geom, const Opts&
   dim3 grid((unsigned)n_colblk, (unsigned)((rows + kTI - 1) / kTI));
   if (n_rhs == 0) {
     fa.store_A = true;
-    launch_far<R, NQ, 0>(grid, fa, s);
+    launch_far<R, NQ, 0>(grid, fa, o.bm, s);
   } else {
     for (int q0 = 0; q0 < n_rhs; q0 += kNRmax) {
       fa.rhs0 = q0;
       fa.store_A = (q0 == 0);
       if (n_rhs - q0 >= 2)
-        launch_far<R, NQ, 2>(grid, fa, s);
+        launch_far<R, NQ, 2>(grid, fa, o.bm, s);
       else
-        launch_far<R, NQ, 1>(grid, fa, s);
+        launch_far<R, NQ, 1>(grid, fa, o.bm, s);
     }
   }
   NAT_LAUNCH_CHECK();
@@ -1083,20 +1203,31 @@ nat_status assemble_impl(const nat_mesh* mesh, const nat_geom* geom, const Opts&
     na.npts = (int)pS.size();
     na.items = w.listS;
     na.nitems = w.cntS + rows;
-    near_kernel<R, NQ, 4><<<(unsigned)std::min(cap, (nnz * 4 + kThreads - 1) / kThreads), kThreads,
-                            na.npts * rsz, s>>>(na);
+    const unsigned gS = (unsigned)std::min(cap, (nnz * 4 + kThreads - 1) / kThreads);
+    if (o.bm)
+      near_kernel<R, NQ, 4, true><<<gS, kThreads, na.npts * rsz, s>>>(na);
+    else
+      near_kernel<R, NQ, 4><<<gS, kThreads, na.npts * rsz, s>>>(na);
     na.rule = w.rule_N;  // class N: one thread per pair
     na.rule_f = w.rule_Nf;
     na.npts = (int)pN.size();
     na.items = w.listN;
     na.nitems = w.cntN + rows;
-    near_kernel<R, NQ, 1><<<(unsigned)std::min(cap, (nnz + kThreads - 1) / kThreads), kThreads, na.npts * rsz,
-                            s>>>(na);
+    const unsigned gN = (unsigned)std::min(cap, (nnz + kThreads - 1) / kThreads);
+    if (o.bm)
+      near_kernel<R, NQ, 1, true><<<gN, kThreads, na.npts * rsz, s>>>(na);
+    else
+      near_kernel<R, NQ, 1><<<gN, kThreads, na.npts * rsz, s>>>(na);
     NAT_LAUNCH_CHECK();
   }
-  self_kernel<R, NQ><<<(unsigned)((rows + 127) / 128), 128, 0, s>>>(
-      n, mesh->n_vert, row_begin, rows, lda, mesh->vxyz, mesh->tri, geom->centroid, cols, cx, cy, cz,
-      k, w.gl, w.gl + o.gl, o.gl, n_rhs, g, A, w.corr_self);
+  if (o.bm)
+    self_kernel<R, NQ, true><<<(unsigned)((rows + 127) / 128), 128, 0, s>>>(
+        n, mesh->n_vert, row_begin, rows, lda, mesh->vxyz, mesh->tri, geom->centroid, geom->normal, cols, cx, cy,
+        cz, k, w.gl, w.gl + o.gl, o.gl, n_rhs, g, A, w.corr_self);
+  else
+    self_kernel<R, NQ><<<(unsigned)((rows + 127) / 128), 128, 0, s>>>(
+        n, mesh->n_vert, row_begin, rows, lda, mesh->vxyz, mesh->tri, geom->centroid, geom->normal, cols, cx, cy,
+        cz, k, w.gl, w.gl + o.gl, o.gl, n_rhs, g, A, w.corr_self);
   NAT_LAUNCH_CHECK();
   if (n_rhs > 0) {
     int64_t t = rows * n_rhs;
@@ -1129,6 +1260,7 @@ extern "C" nat_status nat_bem_assemble(const nat_mesh* mesh, const nat_geom* geo
   NAT_REQUIRE(0 <= row_begin && row_begin < row_end && row_end <= n, "bad row range");
   NAT_REQUIRE(lda >= n, "lda (%lld) < n_tri (%lld)", (long long)lda, (long long)n);
   NAT_REQUIRE(k >= 0.0 && k < 1e300, "k = %g must be finite and >= 0", k);
+  NAT_REQUIRE(!(opts && opts->burton_miller) || k > 0.0, "Burton-Miller needs k > 0 (beta = i/k)");
   NAT_REQUIRE(n_rhs >= 0 && (n_rhs == 0) == (g == nullptr), "g must be NULL iff n_rhs == 0");
   Opts o = opts_of(opts);
   NAT_REQUIRE(o.far_pts == 1 || o.far_pts == 3 || o.far_pts == 6 || o.far_pts == 7,

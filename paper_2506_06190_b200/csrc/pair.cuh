@@ -41,6 +41,39 @@ __device__ __forceinline__ void pair_accumulate(R dx, R dy, R dz, R nx, R ny, R 
   Ki += u * (kr * c - s);
 }
 
+// Burton-Miller pair (Eq. BM; reading R-bm): with the target normal n_x also
+//   K' += w (-d.n_x) rho^3 (ikr - 1) e^{ikr}                         (4 pi dG/dn_x)
+//   W  += w rho^3 [-(d.n_x)(d.n_y) rho^2 (3 - 3ikr - k^2 r^2) - (n_x.n_y)(ikr - 1)] e^{ikr}
+//                                                                     (4 pi d2G/dn_x dn_y)
+template <typename R>
+__device__ __forceinline__ void pair_accumulate_bm(R dx, R dy, R dz, R nx, R ny, R nz, R mx, R my, R mz, R w,
+                                                   R k, C2<R>& V, C2<R>& K, C2<R>& Kp, C2<R>& W) {
+  const R r2 = dx * dx + dy * dy + dz * dz;
+  const R dn = dx * nx + dy * ny + dz * nz;   // d . n_y
+  const R dm = dx * mx + dy * my + dz * mz;   // d . n_x
+  const R nn = nx * mx + ny * my + nz * mz;   // n_x . n_y
+  const R rho = pair_rsqrt(r2);
+  const R rr = r2 * rho;
+  const R kr = k * rr;
+  R s, c;
+  pair_sincos(kr, &s, &c);
+  const R t = w * rho;
+  V.x += t * c;
+  V.y += t * s;
+  const R rho2 = rho * rho;
+  const R er = -c - kr * s, ei = kr * c - s;  // (ikr - 1) e^{ikr}
+  const R uy = t * dn * rho2, ux = -t * dm * rho2;
+  K.x += uy * er;
+  K.y += uy * ei;
+  Kp.x += ux * er;
+  Kp.y += ux * ei;
+  const R q1 = -dn * dm * rho2;
+  const R br = q1 * (R(3) - kr * kr) + nn, bi = -kr * (R(3) * q1 + nn);  // bracket
+  const R tw = t * rho2;
+  W.x += tw * (br * c - bi * s);
+  W.y += tw * (br * s + bi * c);
+}
+
 }  // namespace nat
 
 namespace nat {
