@@ -178,6 +178,48 @@ nat_status nat_bem_solve(nat_comm* comm, nat_prec prec, int64_t n, int64_t row_b
                          nat_stream_t stream); /* (sync) */
 
 /* ---------------------------------------------------------------------------------
+ * NEXT-3 — matrix-free dense BEM operator for meshes whose stored matrix
+ * does not fit (C5 on 1-2 GPUs: 199,692^2 x 16 B = 638 GB).  The operator is the same
+ * A as nat_bem_assemble (P:174-191 with the rules of reading R-colloc), applied as
+ *   (A x)_i = sum_j A^far_ij x_j + sum_{e in near(i)} delta_e x_col[e] + diag_i x_i,
+ * where A^far_ij = -K^far_ij is the far rule on EVERY pair (re-evaluated per product,
+ * nothing stored), delta_e = A_ij - A^far_ij on the near list and diag_i = A_ii -
+ * A^far_ii.  Rows [row_begin, row_end) of one rank; the near list is the one
+ * nat_bem_near_build made for the same rows and opts.  Burton-Miller is not supported.
+ * near_delta: c128 [nnz], diag_delta: c128 [rows], caller-owned, written by
+ * nat_bem_mf_prepare (which also forms rhs = -V g as nat_bem_assemble does, when
+ * n_rhs > 0).  x: c128 [n_tri]; y: c128 [rows].  The far sums run in `prec` (fp32:
+ * packed FP32x2 with per-CTA fp64 reductions; fp64), the partial sums and corrections
+ * in fp64 in a fixed order (deterministic, independent of the row split).
+ * Workspace: nat_bem_mf_workspace(op, nnz, n_rhs) bytes for prepare / matvec;
+ * nat_bem_mf_solve_workspace(op, max_iter, world) for the solve.
+ * ------------------------------------------------------------------------------- */
+typedef struct {
+  const nat_mesh* mesh;
+  const nat_geom* geom;
+  const nat_quad_opts* opts;   /* NULL => defaults; burton_miller must be 0         */
+  double k;
+  nat_prec prec;
+  int64_t row_begin, row_end;
+  const int64_t* near_row_ptr; /* [rows + 1]                                        */
+  const int32_t* near_col;     /* [nnz]                                             */
+  const uint8_t* near_cls;     /* [nnz]                                             */
+  void* near_delta;            /* [nnz] c128 (prepare writes, matvec reads)          */
+  void* diag_delta;            /* [rows] c128                                        */
+} nat_bem_mf;
+size_t nat_bem_mf_workspace(const nat_bem_mf* op, int64_t nnz, int n_rhs);
+nat_status nat_bem_mf_prepare(const nat_bem_mf* op, int n_rhs, const void* g, void* rhs, void* ws,
+                              size_t ws_bytes, nat_stream_t stream); /* (async after one nnz read) */
+nat_status nat_bem_mf_matvec(const nat_bem_mf* op, const void* x, void* y, void* ws, size_t ws_bytes,
+                             nat_stream_t stream); /* (async) */
+/* GMRES (as nat_bem_solve: same row ownership, all-gather, tolerances and info) over the
+ * matrix-free operator; x c128 [n_tri] identical on all ranks.  (sync)                  */
+size_t nat_bem_mf_solve_workspace(const nat_bem_mf* op, int max_iter, int world);
+nat_status nat_bem_mf_solve(nat_comm* comm, const nat_bem_mf* op, const void* b_local, void* x, double tol,
+                            int max_iter, void* ws, size_t ws_bytes, nat_solve_info* info /* [host] */,
+                            nat_stream_t stream);
+
+/* ---------------------------------------------------------------------------------
  * (b) Monte-Carlo BEM (Eq. BIE / SYS; disk terms P:215-236; readings
  * R-mc-sample, R-eps, R-weight, R-disk).
  *

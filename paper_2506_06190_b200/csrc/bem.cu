@@ -242,12 +242,17 @@ struct FarArgs {
   void* A;
   bool store_A;
   double2* bpart;        // [n_colblk][n_rhs][rows]
+  const unsigned long long* skip;  // MV (matrix-free operator inside GMRES): return when *skip == 0
 };
 
 // Generic far assembly (fp64, and fp32 Burton-Miller).  BM: A_ij = -K_ij - beta W_ij and
 // the RHS operator V + beta K' (beta = i/k, reading R-bm).
-template <typename R, int NQ, int NR, bool BM = false>
+// MV (matrix-free matvec, NEXT-3): NR = 1, g = the iterate x; accumulates (A^far x)_i =
+// sum_j (-K_ij) x_j over the CTA's columns instead of storing A (bpart gets +sum).
+template <typename R, int NQ, int NR, bool BM = false, bool MV = false>
 __global__ void __launch_bounds__(kThreads) far_kernel(FarArgs<R> a) {
+  static_assert(!MV || (NR == 1 && !BM), "matrix-free: one iterate, conventional BIE");
+  if (MV && a.skip && *a.skip == 0ull) return;
   __shared__ R s_c[3][kTI];
   __shared__ R s_m[3][kTI];  // BM: row normals
   __shared__ double2 s_red[kThreads / 32][kTI][NR > 0 ? NR : 1];
@@ -311,11 +316,16 @@ __global__ void __launch_bounds__(kThreads) far_kernel(FarArgs<R> a) {
         } else {
           far_entry<R, NQ>(y, w, nx, ny, nz, s_c[0][t], s_c[1][t], s_c[2][t], a.k, Vr, Vi, Kr, Ki);
         }
-        if (a.store_A && valid) store_entry<R>(a.A, (size_t)(i0 + t) * a.lda + j, -Kr, -Ki);
+        if (!MV && a.store_A && valid) store_entry<R>(a.A, (size_t)(i0 + t) * a.lda + j, -Kr, -Ki);
+        if constexpr (MV) {  // (-K) x_j
+          bacc[t][0].x -= Kr * gj[0].x - Ki * gj[0].y;
+          bacc[t][0].y -= Kr * gj[0].y + Ki * gj[0].x;
+        } else {
 #pragma unroll
-        for (int q = 0; q < NR; ++q) {
-          bacc[t][q].x += Vr * gj[q].x - Vi * gj[q].y;
-          bacc[t][q].y += Vr * gj[q].y + Vi * gj[q].x;
+          for (int q = 0; q < NR; ++q) {
+            bacc[t][q].x += Vr * gj[q].x - Vi * gj[q].y;
+            bacc[t][q].y += Vr * gj[q].y + Vi * gj[q].x;
+          }
         }
       }
     }
@@ -342,8 +352,9 @@ __global__ void __launch_bounds__(kThreads) far_kernel(FarArgs<R> a) {
           s.x += s_red[wv][t][q].x;
           s.y += s_red[wv][t][q].y;
         }
-        // b = -V g
-        a.bpart[((size_t)blockIdx.x * a.n_rhs + a.rhs0 + q) * a.rows + i0 + t] = make_double2(-s.x, -s.y);
+        // b = -V g  (MV: + sum_j A^far_ij x_j)
+        a.bpart[((size_t)blockIdx.x * a.n_rhs + a.rhs0 + q) * a.rows + i0 + t] =
+            MV ? s : make_double2(-s.x, -s.y);
       }
     }
   }
@@ -353,9 +364,13 @@ __global__ void __launch_bounds__(kThreads) far_kernel(FarArgs<R> a) {
 // each instruction, the column's quadrature data is broadcast into both halves.  Per
 // quadrature point and row: 11 packed-pipe instructions + 1 FMUL.RZ + 3 MUFU.  The kernel
 // accumulates -K directly (A_ij = -K_ij off the diagonal) and V g for the RHS.
-template <int NQ, int NR>
+// MV (matrix-free matvec, NEXT-3): NR = 1 and g = the iterate x; the row sums are
+// sum_j (-K_ij) x_j = (A^far x)_i (no store, V unused).
+template <int NQ, int NR, bool MV = false>
 __global__ void __launch_bounds__(kThreads, 2) far_kernel_x2(FarArgs<float> a) {
   static_assert(kTI % 2 == 0, "row pairs");
+  static_assert(!MV || NR == 1, "matrix-free: one iterate");
+  if (MV && a.skip && *a.skip == 0ull) return;
   constexpr int TP = kTI / 2;
   constexpr int NRr = NR > 0 ? NR : 1;
   __shared__ __align__(16) f2r s_c[3][TP];
@@ -451,14 +466,19 @@ __global__ void __launch_bounds__(kThreads, 2) far_kernel_x2(FarArgs<float> a) {
             Kr = f2fma(u, f2fma(kr, sn, cs), Kr);
             Ki = f2fma(u, f2fma(nkr, cs, sn), Ki);
           }
-          if (a.store_A && valid) {
+          if (!MV && a.store_A && valid) {
             arow[0] = make_float2(f2lo(Kr), f2lo(Ki));
             if (FULL || 2 * t + 1 < nrows) arow[ld] = make_float2(f2hi(Kr), f2hi(Ki));
           }
+          if constexpr (MV) {  // (-K) x_j  (Kr, Ki hold -K)
+            br[t][0] = f2fma(Kr, gr[0], f2fma(Ki, ngi[0], br[t][0]));
+            bi[t][0] = f2fma(Kr, gi[0], f2fma(Ki, gr[0], bi[t][0]));
+          } else {
 #pragma unroll
-          for (int q = 0; q < NR; ++q) {
-            br[t][q] = f2fma(Vr, gr[q], f2fma(Vi, ngi[q], br[t][q]));
-            bi[t][q] = f2fma(Vr, gi[q], f2fma(Vi, gr[q], bi[t][q]));
+            for (int q = 0; q < NR; ++q) {
+              br[t][q] = f2fma(Vr, gr[q], f2fma(Vi, ngi[q], br[t][q]));
+              bi[t][q] = f2fma(Vr, gi[q], f2fma(Vi, gr[q], bi[t][q]));
+            }
           }
         }
       }
@@ -491,7 +511,8 @@ __global__ void __launch_bounds__(kThreads, 2) far_kernel_x2(FarArgs<float> a) {
           s.x += s_red[wv][t][q].x;
           s.y += s_red[wv][t][q].y;
         }
-        a.bpart[((size_t)blockIdx.x * a.n_rhs + a.rhs0 + q) * a.rows + i0 + t] = make_double2(-s.x, -s.y);
+        a.bpart[((size_t)blockIdx.x * a.n_rhs + a.rhs0 + q) * a.rows + i0 + t] =
+            MV ? s : make_double2(-s.x, -s.y);
       }
     }
   }
@@ -530,6 +551,7 @@ struct NearArgs {
   const double2* g;
   void* A;
   double2* corr;           // [nnz][n_rhs]
+  double2* delta;          // matrix-free (NEXT-3): [nnz] A^near_ij - A^far_ij instead of storing A
 };
 
 // One G-lane group per near pair of one class (compacted list `items` = (entry, row)):
@@ -640,8 +662,8 @@ __device__ __forceinline__ void near_item(const NearArgs<R>& a, int64_t gid, int
     Vr = V.x - Kp.y / a.k;
     Vi = V.y + Kp.x / a.k;
   }
-  store_entry<R>(a.A, (size_t)r * a.lda + j, -Kr, -Ki);
-  if (a.n_rhs > 0) {
+  if (!a.delta) store_entry<R>(a.A, (size_t)r * a.lda + j, -Kr, -Ki);
+  if (a.n_rhs > 0 || a.delta) {
     R y[NQ][3], w[NQ];
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
@@ -657,6 +679,9 @@ __device__ __forceinline__ void near_item(const NearArgs<R>& a, int64_t gid, int
     else
       far_entry<R, NQ>(y, w, a.cols.nrm[j], a.cols.nrm[n + j], a.cols.nrm[2 * n + j],
                        (R)(ci[0] - a.cx), (R)(ci[1] - a.cy), (R)(ci[2] - a.cz), a.k, fVr, fVi, fKr, fKi);
+    if constexpr (!BM) {  // matrix-free: A_ij = A^far_ij + delta_e with A = -K
+      if (a.delta) a.delta[e] = make_double2((double)fKr - (double)Kr, (double)fKi - (double)Ki);
+    }
     const double dVr = (double)Vr - (double)fVr, dVi = (double)Vi - (double)fVi;
     for (int q = 0; q < a.n_rhs; ++q) {
       double2 gv = a.g[(size_t)q * n + j];
@@ -749,7 +774,7 @@ __global__ void self_kernel(int64_t n, int64_t nv, int64_t row_begin, int64_t ro
                             FarCols<R> cols, double cx, double cy,
                             double cz, double k, const double* glx, const double* glw, int ngl,
                             int n_rhs, const double2* __restrict__ g, void* A,
-                            double2* __restrict__ corr_self) {
+                            double2* __restrict__ corr_self, double2* __restrict__ diag_delta) {
   int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (r >= rows) return;
   int64_t i = row_begin + r;
@@ -762,12 +787,10 @@ __global__ void self_kernel(int64_t n, int64_t nv, int64_t row_begin, int64_t ro
     double Wr, Wi;
     self_hypersingular(v, c, k, glx, glw, ngl, Wr, Wi);
     store_entry<R>(A, (size_t)r * lda + i, (R)(0.5 + Wi / k), (R)(-Wr / k));
-  } else {
+  } else if (!diag_delta) {
     store_entry<R>(A, (size_t)r * lda + i, R(0.5), R(0));  // K_ii = 0 on a flat triangle
   }
-  if (n_rhs == 0) return;
-  double Vr, Vi;
-  self_single_layer(v, c, k, glx, glw, ngl, Vr, Vi);  // K'_ii = 0 too: the RHS operator is V_ii
+  if (n_rhs == 0 && !diag_delta) return;
   R y[NQ][3], w[NQ];
 #pragma unroll
   for (int q = 0; q < NQ; ++q) {
@@ -784,6 +807,12 @@ __global__ void self_kernel(int64_t n, int64_t nv, int64_t row_begin, int64_t ro
   else
     far_entry<R, NQ>(y, w, cols.nrm[i], cols.nrm[n + i], cols.nrm[2 * n + i], (R)(c[0] - cx),
                      (R)(c[1] - cy), (R)(c[2] - cz), (R)k, fVr, fVi, fKr, fKi);
+  if constexpr (!BM) {  // matrix-free: A_ii = 1/2 = A^far_ii + delta_i with A^far_ii = -K^far_ii
+    if (diag_delta) diag_delta[r] = make_double2(0.5 + (double)fKr, (double)fKi);
+  }
+  if (n_rhs == 0) return;
+  double Vr, Vi;
+  self_single_layer(v, c, k, glx, glw, ngl, Vr, Vi);  // K'_ii = 0 too: the RHS operator is V_ii
   double dVr = Vr - (double)fVr, dVi = Vi - (double)fVi;
   for (int q = 0; q < n_rhs; ++q) {
     double2 gv = g[(size_t)q * n + i];
@@ -1118,12 +1147,20 @@ size_t carve(nat::Carver& c, AsmWs& w, int64_t n, int64_t rows, int64_t nnz, int
 constexpr int kMaxLevel = 4;
 constexpr int kMaxGL = 64;
 
+// Matrix-free outputs (NEXT-3): with `delta` set, assemble_impl writes the near/self
+// corrections of the operator A = A^far + (delta on the near list and the diagonal)
+// instead of A (A is not touched; the far kernel only runs for the RHS).
+struct MfOut {
+  double2* delta = nullptr;  // [nnz]
+  double2* diag = nullptr;   // [rows]
+};
+
 template <typename R, int NQ>
 nat_status assemble_impl(const nat_mesh* mesh, const nat_geom* geom, const Opts& o,
                          const int64_t* rp, const int32_t* col, const uint8_t* cls, int64_t nnz, double k,
                          int64_t row_begin, int64_t rows, int n_rhs, const double2* g, void* A,
                          int64_t lda, double2* rhs, AsmWs& w, const std::vector<Pt>& pS,
-                         const std::vector<Pt>& pN, cudaStream_t s) {
+                         const std::vector<Pt>& pN, cudaStream_t s, MfOut mf = MfOut{}) {
   const int64_t n = mesh->n_tri;
   const double cx = geom->center[0], cy = geom->center[1], cz = geom->center[2];
   FarCols<R> cols{(const R*)w.qxyz, (const R*)w.qw, (const R*)w.qn};
@@ -1152,11 +1189,11 @@ nat_status assemble_impl(const nat_mesh* mesh, const nat_geom* geom, const Opts&
   dim3 grid((unsigned)n_colblk, (unsigned)((rows + kTI - 1) / kTI));
   if (n_rhs == 0) {
     fa.store_A = true;
-    launch_far<R, NQ, 0>(grid, fa, o.bm, s);
+    if (!mf.delta) launch_far<R, NQ, 0>(grid, fa, o.bm, s);
   } else {
     for (int q0 = 0; q0 < n_rhs; q0 += kNRmax) {
       fa.rhs0 = q0;
-      fa.store_A = (q0 == 0);
+      fa.store_A = (q0 == 0) && !mf.delta;
       if (n_rhs - q0 >= 2)
         launch_far<R, NQ, 2>(grid, fa, o.bm, s);
       else
@@ -1195,6 +1232,7 @@ nat_status assemble_impl(const nat_mesh* mesh, const nat_geom* geom, const Opts&
     na.g = g;
     na.A = A;
     na.corr = w.corr;
+    na.delta = mf.delta;
     const size_t rsz = sizeof(R) == 4 ? sizeof(float4) : sizeof(double4);
     // persistent grids (the class counts stay on the device): at most one group per item
     const int64_t cap = (int64_t)nat::device_sm_count() * 64;
@@ -1223,11 +1261,11 @@ nat_status assemble_impl(const nat_mesh* mesh, const nat_geom* geom, const Opts&
   if (o.bm)
     self_kernel<R, NQ, true><<<(unsigned)((rows + 127) / 128), 128, 0, s>>>(
         n, mesh->n_vert, row_begin, rows, lda, mesh->vxyz, mesh->tri, geom->centroid, geom->normal, cols, cx, cy,
-        cz, k, w.gl, w.gl + o.gl, o.gl, n_rhs, g, A, w.corr_self);
+        cz, k, w.gl, w.gl + o.gl, o.gl, n_rhs, g, A, w.corr_self, mf.diag);
   else
     self_kernel<R, NQ><<<(unsigned)((rows + 127) / 128), 128, 0, s>>>(
         n, mesh->n_vert, row_begin, rows, lda, mesh->vxyz, mesh->tri, geom->centroid, geom->normal, cols, cx, cy,
-        cz, k, w.gl, w.gl + o.gl, o.gl, n_rhs, g, A, w.corr_self);
+        cz, k, w.gl, w.gl + o.gl, o.gl, n_rhs, g, A, w.corr_self, mf.diag);
   NAT_LAUNCH_CHECK();
   if (n_rhs > 0) {
     int64_t t = rows * n_rhs;
@@ -1247,18 +1285,18 @@ extern "C" size_t nat_bem_assemble_workspace(int64_t n_tri, int64_t rows, int64_
   return carve(c, w, n_tri, rows, nnz, n_rhs, kMaxFarQ, (int)nS, (int)nN, kMaxGL, sizeof(double));
 }
 
-extern "C" nat_status nat_bem_assemble(const nat_mesh* mesh, const nat_geom* geom,
-                                       const nat_quad_opts* opts, const int64_t* near_row_ptr,
-                                       const int32_t* near_col, const uint8_t* near_cls, double k,
-                                       nat_prec prec, int64_t row_begin, int64_t row_end, int n_rhs,
-                                       const void* g, void* A, int64_t lda, void* rhs, void* ws,
-                                       size_t ws_bytes, nat_stream_t stream) {
+namespace {
+// nat_bem_assemble and nat_bem_mf_prepare (mf.delta set: no A, corrections instead)
+nat_status assemble_entry(const nat_mesh* mesh, const nat_geom* geom, const nat_quad_opts* opts,
+                          const int64_t* near_row_ptr, const int32_t* near_col, const uint8_t* near_cls, double k,
+                          nat_prec prec, int64_t row_begin, int64_t row_end, int n_rhs, const void* g, void* A,
+                          int64_t lda, void* rhs, void* ws, size_t ws_bytes, nat_stream_t stream, MfOut mf) {
   NAT_REQUIRE(mesh && geom, "mesh and geom must be non-null");
   NAT_REQUIRE(prec == NAT_FP32 || prec == NAT_FP64, "bad precision %d", (int)prec);
   const int64_t n = mesh->n_tri;
   NAT_REQUIRE(geom->n_tri == n && n >= 1 && n < (1LL << 31), "inconsistent n_tri");
   NAT_REQUIRE(0 <= row_begin && row_begin < row_end && row_end <= n, "bad row range");
-  NAT_REQUIRE(lda >= n, "lda (%lld) < n_tri (%lld)", (long long)lda, (long long)n);
+  NAT_REQUIRE(mf.delta || lda >= n, "lda (%lld) < n_tri (%lld)", (long long)lda, (long long)n);
   NAT_REQUIRE(k >= 0.0 && k < 1e300, "k = %g must be finite and >= 0", k);
   NAT_REQUIRE(!(opts && opts->burton_miller) || k > 0.0, "Burton-Miller needs k > 0 (beta = i/k)");
   NAT_REQUIRE(n_rhs >= 0 && (n_rhs == 0) == (g == nullptr), "g must be NULL iff n_rhs == 0");
@@ -1268,8 +1306,14 @@ extern "C" nat_status nat_bem_assemble(const nat_mesh* mesh, const nat_geom* geo
   NAT_REQUIRE(o.lev_S >= 0 && o.lev_S <= kMaxLevel && o.lev_N >= 0 && o.lev_N <= kMaxLevel,
               "near levels must be in [0, %d]", kMaxLevel);
   NAT_REQUIRE(o.gl >= 2 && o.gl <= kMaxGL, "self_theta_pts must be in [2, %d]", kMaxGL);
+  NAT_REQUIRE(!mf.delta || !(opts && opts->burton_miller), "the matrix-free operator is the conventional BIE only");
   NAT_REQUIRE_DEV(near_row_ptr);
-  NAT_REQUIRE_DEV(A);
+  if (mf.delta) {
+    NAT_REQUIRE_DEV(mf.delta);
+    NAT_REQUIRE_DEV(mf.diag);
+  } else {
+    NAT_REQUIRE_DEV(A);
+  }
   NAT_REQUIRE_DEV(mesh->vxyz);
   NAT_REQUIRE_DEV(mesh->tri);
   NAT_REQUIRE_DEV(geom->centroid);
@@ -1331,7 +1375,7 @@ extern "C" nat_status nat_bem_assemble(const nat_mesh* mesh, const nat_geom* geo
   double2* bb = (double2*)rhs;
 #define NAT_ASM(R, NQ)                                                                         \
   assemble_impl<R, NQ>(mesh, geom, o, near_row_ptr, near_col, near_cls, nnz, k, row_begin, rows, \
-                       n_rhs, gg, A, lda, bb, w, pS, pN, s)
+                       n_rhs, gg, A, lda, bb, w, pS, pN, s, mf)
   if (prec == NAT_FP32) {
     switch (o.far_pts) {
       case 1: return NAT_ASM(float, 1);
@@ -1348,6 +1392,17 @@ extern "C" nat_status nat_bem_assemble(const nat_mesh* mesh, const nat_geom* geo
     }
   }
 #undef NAT_ASM
+}
+}  // namespace
+
+extern "C" nat_status nat_bem_assemble(const nat_mesh* mesh, const nat_geom* geom,
+                                       const nat_quad_opts* opts, const int64_t* near_row_ptr,
+                                       const int32_t* near_col, const uint8_t* near_cls, double k,
+                                       nat_prec prec, int64_t row_begin, int64_t row_end, int n_rhs,
+                                       const void* g, void* A, int64_t lda, void* rhs, void* ws,
+                                       size_t ws_bytes, nat_stream_t stream) {
+  return assemble_entry(mesh, geom, opts, near_row_ptr, near_col, near_cls, k, prec, row_begin, row_end, n_rhs, g,
+                        A, lda, rhs, ws, ws_bytes, stream, MfOut{});
 }
 
 namespace {
@@ -1387,3 +1442,213 @@ nat_status matvec_internal(nat_prec prec, int64_t rows, int64_t n, const void* A
   return NAT_OK;
 }
 }  // namespace nat
+
+// ------------------------------------------------------------------------------------
+// NEXT-3: matrix-free dense operator (include/nat.h, nat_bem_mf_*).
+//   (A x)_i = sum_j A^far_ij x_j  [far kernel in MV mode, every pair, nothing stored]
+//           + sum_{e in near(i)} delta_e x_col[e] + diag_i x_i   [mf_final_kernel]
+// ------------------------------------------------------------------------------------
+namespace {
+
+struct MfWs {
+  double4* rule_far;
+  void* qxyz;
+  void* qw;
+  void* qn;
+  double2* bpart;  // [n_colblk][rows]
+};
+
+size_t mf_carve(nat::Carver& c, MfWs& w, int64_t n, int64_t rows, size_t rsz) {
+  const int64_t n_colblk = (n + kThreads * kCC - 1) / (kThreads * kCC);
+  w.rule_far = c.take<double4>(kMaxFarQ);
+  w.qxyz = c.take<char>(rsz * kMaxFarQ * 3 * n);
+  w.qw = c.take<char>(rsz * kMaxFarQ * n);
+  w.qn = c.take<char>(rsz * 3 * n);
+  w.bpart = c.take<double2>((size_t)n_colblk * rows);
+  return c.bytes();
+}
+
+// y_r = sum over column blocks of the far partial sums (fixed block order) + the near
+// corrections in CSR order + the diagonal correction.
+__global__ void mf_final_kernel(int64_t rows, int64_t row_begin, int n_colblk, const double2* __restrict__ bpart,
+                                const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                                const double2* __restrict__ delta, const double2* __restrict__ diag,
+                                const double2* __restrict__ x, double2* __restrict__ y,
+                                const unsigned long long* __restrict__ skip) {
+  if (skip && *skip == 0ull) return;
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  double sx = 0.0, sy = 0.0;
+#pragma unroll 4
+  for (int cb = 0; cb < n_colblk; ++cb) {
+    const double2 v = bpart[(size_t)cb * rows + r];
+    sx += v.x;
+    sy += v.y;
+  }
+  const int64_t e1 = rp[r + 1];
+#pragma unroll 4
+  for (int64_t e = rp[r]; e < e1; ++e) {
+    const double2 d = delta[e], xv = x[col[e]];
+    sx += d.x * xv.x - d.y * xv.y;
+    sy += d.x * xv.y + d.y * xv.x;
+  }
+  const double2 d = diag[r], xv = x[row_begin + r];
+  sx += d.x * xv.x - d.y * xv.y;
+  sy += d.x * xv.y + d.y * xv.x;
+  y[r] = make_double2(sx, sy);
+}
+
+nat_status mf_check(const nat_bem_mf* op) {
+  NAT_REQUIRE(op && op->mesh && op->geom, "op, op->mesh and op->geom must be non-null");
+  NAT_REQUIRE(op->prec == NAT_FP32 || op->prec == NAT_FP64, "bad precision %d", (int)op->prec);
+  const int64_t n = op->mesh->n_tri;
+  NAT_REQUIRE(op->geom->n_tri == n && n >= 1 && n < (1LL << 31), "inconsistent n_tri");
+  NAT_REQUIRE(0 <= op->row_begin && op->row_begin < op->row_end && op->row_end <= n, "bad row range");
+  NAT_REQUIRE(op->k >= 0.0 && op->k < 1e300, "k = %g must be finite and >= 0", op->k);
+  NAT_REQUIRE(!(op->opts && op->opts->burton_miller), "the matrix-free operator is the conventional BIE only");
+  const int fp = opts_of(op->opts).far_pts;
+  NAT_REQUIRE(fp == 1 || fp == 3 || fp == 6 || fp == 7, "far_pts must be 1, 3, 6 or 7");
+  NAT_REQUIRE_DEV(op->near_row_ptr);
+  NAT_REQUIRE_DEV(op->near_delta);
+  NAT_REQUIRE_DEV(op->diag_delta);
+  NAT_REQUIRE_DEV(op->mesh->vxyz);
+  NAT_REQUIRE_DEV(op->mesh->tri);
+  NAT_REQUIRE_DEV(op->geom->centroid);
+  NAT_REQUIRE_DEV(op->geom->normal);
+  NAT_REQUIRE_DEV(op->geom->area);
+  return NAT_OK;
+}
+
+size_t mf_ws_bytes(const nat_bem_mf* op) {
+  nat::Carver c(nullptr);
+  MfWs w;
+  return mf_carve(c, w, op->mesh->n_tri, op->row_end - op->row_begin, op->prec == NAT_FP32 ? 4 : 8);
+}
+
+template <typename R, int NQ>
+nat_status mf_launch(const nat_bem_mf* op, const MfWs& w, const double2* x, double2* y,
+                     const unsigned long long* skip, cudaStream_t s) {
+  const int64_t n = op->mesh->n_tri, rows = op->row_end - op->row_begin;
+  FarArgs<R> fa{};
+  fa.n = n;
+  fa.row_begin = op->row_begin;
+  fa.rows = rows;
+  fa.lda = 0;
+  fa.cols = FarCols<R>{(const R*)w.qxyz, (const R*)w.qw, (const R*)w.qn};
+  fa.cen = op->geom->centroid;
+  fa.nrm = op->geom->normal;
+  fa.cx = op->geom->center[0];
+  fa.cy = op->geom->center[1];
+  fa.cz = op->geom->center[2];
+  fa.k = (R)op->k;
+  fa.n_rhs = 1;
+  fa.rhs0 = 0;
+  fa.g = x;
+  fa.A = nullptr;
+  fa.store_A = false;
+  fa.bpart = w.bpart;
+  fa.skip = skip;
+  const int64_t n_colblk = (n + kThreads * kCC - 1) / (kThreads * kCC);
+  dim3 grid((unsigned)n_colblk, (unsigned)((rows + kTI - 1) / kTI));
+  if constexpr (sizeof(R) == 4)
+    far_kernel_x2<NQ, 1, true><<<grid, kThreads, 0, s>>>(fa);
+  else
+    far_kernel<R, NQ, 1, false, true><<<grid, kThreads, 0, s>>>(fa);
+  NAT_LAUNCH_CHECK();
+  mf_final_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, s>>>(
+      rows, op->row_begin, (int)n_colblk, w.bpart, op->near_row_ptr, op->near_col, (const double2*)op->near_delta,
+      (const double2*)op->diag_delta, x, y, skip);
+  NAT_LAUNCH_CHECK();
+  return NAT_OK;
+}
+
+}  // namespace
+
+namespace nat {
+size_t mf_apply_ws(const nat_bem_mf* op) { return mf_ws_bytes(op); }
+
+// Column rule data into the workspace (once per operator; the far points depend only on
+// the mesh and the rule).
+nat_status mf_begin(const nat_bem_mf* op, void* ws, size_t ws_bytes, cudaStream_t s) {
+  nat_status st = mf_check(op);
+  if (st != NAT_OK) return st;
+  Carver c(ws);
+  MfWs w;
+  const int64_t n = op->mesh->n_tri;
+  const size_t need = mf_carve(c, w, n, op->row_end - op->row_begin, op->prec == NAT_FP32 ? 4 : 8);
+  if (ws_bytes < need) return fail(NAT_ERR_WORKSPACE, "workspace %zu < %zu", ws_bytes, need);
+  NAT_REQUIRE_DEV(ws);
+  const Opts o = opts_of(op->opts);
+  std::vector<Pt> pF;
+  base_rule(o.far_pts, pF);
+  NAT_CUDA_TRY(cudaMemcpyAsync(w.rule_far, pF.data(), pF.size() * sizeof(Pt), cudaMemcpyHostToDevice, s));
+  const double cx = op->geom->center[0], cy = op->geom->center[1], cz = op->geom->center[2];
+  if (op->prec == NAT_FP32)
+    far_prep_kernel<float><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(
+        op->mesh->n_vert, n, op->mesh->vxyz, op->mesh->tri, op->geom->normal, op->geom->area, w.rule_far, o.far_pts,
+        cx, cy, cz, (float*)w.qxyz, (float*)w.qw, (float*)w.qn);
+  else
+    far_prep_kernel<double><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(
+        op->mesh->n_vert, n, op->mesh->vxyz, op->mesh->tri, op->geom->normal, op->geom->area, w.rule_far, o.far_pts,
+        cx, cy, cz, (double*)w.qxyz, (double*)w.qw, (double*)w.qn);
+  NAT_LAUNCH_CHECK();
+  return NAT_OK;
+}
+
+// y[rows] = (A x) on this rank's rows; x [n] (after mf_begin on the same ws).
+nat_status mf_apply(const nat_bem_mf* op, void* ws, const double2* x, double2* y, const unsigned long long* skip,
+                    cudaStream_t s) {
+  Carver c(ws);
+  MfWs w;
+  mf_carve(c, w, op->mesh->n_tri, op->row_end - op->row_begin, op->prec == NAT_FP32 ? 4 : 8);
+  const int fp = opts_of(op->opts).far_pts;
+#define NAT_MF(R, NQ) mf_launch<R, NQ>(op, w, x, y, skip, s)
+  if (op->prec == NAT_FP32) {
+    switch (fp) {
+      case 1: return NAT_MF(float, 1);
+      case 3: return NAT_MF(float, 3);
+      case 6: return NAT_MF(float, 6);
+      default: return NAT_MF(float, 7);
+    }
+  } else {
+    switch (fp) {
+      case 1: return NAT_MF(double, 1);
+      case 3: return NAT_MF(double, 3);
+      case 6: return NAT_MF(double, 6);
+      default: return NAT_MF(double, 7);
+    }
+  }
+#undef NAT_MF
+}
+}  // namespace nat
+
+extern "C" size_t nat_bem_mf_workspace(const nat_bem_mf* op, int64_t nnz, int n_rhs) {
+  if (!op || !op->mesh || op->row_end <= op->row_begin) return 0;
+  const int64_t n = op->mesh->n_tri, rows = op->row_end - op->row_begin;
+  const size_t a = nat_bem_assemble_workspace(n, rows, nnz, n_rhs);
+  const size_t b = mf_ws_bytes(op);
+  return a > b ? a : b;
+}
+
+extern "C" nat_status nat_bem_mf_prepare(const nat_bem_mf* op, int n_rhs, const void* g, void* rhs, void* ws,
+                                         size_t ws_bytes, nat_stream_t stream) {
+  nat_status st = mf_check(op);
+  if (st != NAT_OK) return st;
+  MfOut mf;
+  mf.delta = (double2*)op->near_delta;
+  mf.diag = (double2*)op->diag_delta;
+  return assemble_entry(op->mesh, op->geom, op->opts, op->near_row_ptr, op->near_col, op->near_cls, op->k, op->prec,
+                        op->row_begin, op->row_end, n_rhs, g, nullptr, 0, rhs, ws, ws_bytes, stream, mf);
+}
+
+extern "C" nat_status nat_bem_mf_matvec(const nat_bem_mf* op, const void* x, void* y, void* ws, size_t ws_bytes,
+                                        nat_stream_t stream) {
+  nat_status st = mf_check(op);
+  if (st != NAT_OK) return st;
+  NAT_REQUIRE_DEV(x);
+  NAT_REQUIRE_DEV(y);
+  cudaStream_t s = (cudaStream_t)stream;
+  st = nat::mf_begin(op, ws, ws_bytes, s);
+  if (st != NAT_OK) return st;
+  return nat::mf_apply(op, ws, (const double2*)x, (double2*)y, nullptr, s);
+}

@@ -23,6 +23,7 @@ namespace {
 
 constexpr int kT = 256;
 constexpr int kRing = 4;  // pinned mask slots / events in flight
+constexpr int kKU = 8;    // basis vectors loaded together by the update / combine kernels
 
 __device__ __forceinline__ bool sys_on(uint64_t active, const unsigned long long* dmask, int s) {
   uint64_t a = active;
@@ -285,12 +286,25 @@ __global__ void __launch_bounds__(kT) update_kernel(const double2* __restrict__ 
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   double2 o = make_double2(0.0, 0.0);
   if (i < n) {
+    // groups of kKU basis vectors: their loads are issued together (a long basis is
+    // otherwise one dependent L2 round trip per vector), summed in ascending k
     double2 acc = make_double2(0.0, 0.0);
-    for (int k = 0; k < nvec; ++k) {
-      double2 c = h2[(size_t)s * mp2 + k];
-      double2 v = V[k * vstride_k + (size_t)s * ldv + i];
-      acc.x += c.x * v.x - c.y * v.y;
-      acc.y += c.x * v.y + c.y * v.x;
+    const double2* vi = V + (size_t)s * ldv + i;
+    for (int k0 = 0; k0 < nvec; k0 += kKU) {
+      double2 v[kKU], c[kKU];
+#pragma unroll
+      for (int u = 0; u < kKU; ++u) {
+        const int k = k0 + u;
+        v[u] = k < nvec ? vi[k * vstride_k] : make_double2(0.0, 0.0);
+        c[u] = k < nvec ? h2[(size_t)s * mp2 + k] : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int u = 0; u < kKU; ++u) {
+        if (k0 + u < nvec) {
+          acc.x += c[u].x * v[u].x - c[u].y * v[u].y;
+          acc.y += c[u].x * v[u].y + c[u].y * v[u].x;
+        }
+      }
     }
     o = w_in[(size_t)s * ldv + i];
     o = make_double2(o.x - acc.x, o.y - acc.y);
@@ -359,14 +373,26 @@ __global__ void combine_kernel(const double2* __restrict__ V, const double2* __r
   if (i >= n) return;
   const int kmax = (sys[s].flags & kSysNonFinite) ? 0 : sys[s].k;
   double2 acc = make_double2(0.0, 0.0), ax = make_double2(0.0, 0.0);
-  for (int k = 0; k < kmax; ++k) {
-    const double2 c = y[(size_t)s * m + k];
-    const double2 v = V[k * vstride_k + (size_t)s * ldv + i];
-    const double2 u = W[k * vstride_k + (size_t)s * ldv + i];
-    acc.x += c.x * v.x - c.y * v.y;
-    acc.y += c.x * v.y + c.y * v.x;
-    ax.x += c.x * u.x - c.y * u.y;
-    ax.y += c.x * u.y + c.y * u.x;
+  const size_t off = (size_t)s * ldv + i;
+  for (int k0 = 0; k0 < kmax; k0 += kKU) {  // loads of kKU vectors in flight, ascending sums
+    double2 c[kKU], v[kKU], u[kKU];
+#pragma unroll
+    for (int q = 0; q < kKU; ++q) {
+      const int k = k0 + q;
+      const bool on = k < kmax;
+      c[q] = on ? y[(size_t)s * m + k] : make_double2(0.0, 0.0);
+      v[q] = on ? V[k * vstride_k + off] : make_double2(0.0, 0.0);
+      u[q] = on ? W[k * vstride_k + off] : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int q = 0; q < kKU; ++q) {
+      if (k0 + q < kmax) {
+        acc.x += c[q].x * v[q].x - c[q].y * v[q].y;
+        acc.y += c[q].x * v[q].y + c[q].y * v[q].x;
+        ax.x += c[q].x * u[q].x - c[q].y * u[q].y;
+        ax.y += c[q].x * u[q].y + c[q].y * u[q].x;
+      }
+    }
   }
   x[(size_t)s * ldv + i] = acc;
   const double2 bb = b[(size_t)s * ldv + i];
@@ -674,6 +700,98 @@ extern "C" nat_status nat_bem_solve(nat_comm* comm, nat_prec prec, int64_t n, in
   for (int c = 0; c < n_comm; ++c) {
     float ms = 0.f;
     NAT_CUDA_TRY(cudaEventElapsedTime(&ms, nat::timing_event(1, 2 * c), nat::timing_event(1, 2 * c + 1)));
+    t_comm += 1e-3 * ms;
+  }
+  if (info) {
+    info->iters = res[0].iters;
+    info->converged = res[0].converged;
+    info->rel_residual = res[0].rel_residual;
+    info->t_matvec_s = t_op;
+    info->t_comm_s = t_comm;
+    info->t_total_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+  }
+  return res[0].converged ? NAT_OK : NAT_WARN_NOT_CONVERGED;
+}
+
+// ------------------------------------------------------------------------------------
+// NEXT-3: the same row-sharded GMRES over the matrix-free operator (nat_bem_mf_*)
+// ------------------------------------------------------------------------------------
+extern "C" size_t nat_bem_mf_solve_workspace(const nat_bem_mf* op, int max_iter, int world) {
+  if (!op || !op->mesh) return 0;
+  if (max_iter <= 0) max_iter = 200;
+  if (world < 1) world = 1;
+  const int64_t n = op->mesh->n_tri;
+  const int64_t ldv = (n + world - 1) / world * world;
+  nat::Carver c(nullptr);
+  nat::krylov_workspace(1, n, ldv, max_iter, c, nullptr);
+  c.take<double2>(ldv);
+  c.take<double2>(ldv);
+  c.take<char>(nat::mf_apply_ws(op));
+  return c.bytes();
+}
+
+extern "C" nat_status nat_bem_mf_solve(nat_comm* comm, const nat_bem_mf* op, const void* b_local, void* x,
+                                       double tol, int max_iter, void* ws, size_t ws_bytes, nat_solve_info* info,
+                                       nat_stream_t stream) {
+  auto t_start = std::chrono::steady_clock::now();
+  NAT_REQUIRE(op && op->mesh, "op must be non-null");
+  const int64_t n = op->mesh->n_tri;
+  if (tol <= 0) tol = 1e-6;
+  if (max_iter <= 0) max_iter = 200;
+  SolveLayout L = layout(comm, n);
+  NAT_REQUIRE(L.world <= 64, "world size %d > 64", L.world);
+  const int64_t rb = L.rank * L.rpr, re = nat::min64(n, rb + L.rpr);
+  NAT_REQUIRE(op->row_begin == rb && op->row_end == re,
+              "rank %d must own rows [%lld, %lld) (rows_per_rank = ceil(n/world)); got [%lld, %lld)", L.rank,
+              (long long)rb, (long long)re, (long long)op->row_begin, (long long)op->row_end);
+  NAT_REQUIRE_DEV(b_local);
+  NAT_REQUIRE_DEV(x);
+  NAT_REQUIRE_DEV(ws);
+  nat::Carver c(ws);
+  nat::KrylovWs kw;
+  double2 *bfull, *xfull;
+  solve_ws(comm, n, max_iter, c, &kw, &bfull, &xfull);
+  const size_t mfb = nat::mf_apply_ws(op);
+  void* mfws = c.take<char>(mfb);
+  const size_t need = c.bytes();
+  if (ws_bytes < need) return nat::fail(NAT_ERR_WORKSPACE, "workspace %zu < %zu", ws_bytes, need);
+  cudaStream_t s = (cudaStream_t)stream;
+  nat_status st = nat::mf_begin(op, mfws, mfb, s);
+  if (st != NAT_OK) return st;
+  const int64_t rows = re - rb;
+  int n_comm = 0;
+  NAT_CUDA_TRY(cudaMemsetAsync(bfull, 0, sizeof(double2) * L.ldv, s));
+  NAT_CUDA_TRY(cudaMemcpyAsync(bfull + rb, b_local, sizeof(double2) * rows, cudaMemcpyDeviceToDevice, s));
+  if (L.world > 1) {
+    st = nat::allgather_inplace(comm, (double*)bfull, (size_t)L.rpr * 2, s);
+    if (st != NAT_OK) return st;
+  }
+  auto opf = [&](const double2* in, double2* out, uint64_t, const unsigned long long* dmask,
+                 cudaStream_t ss) -> nat_status {
+    nat_status stt = nat::mf_apply(op, mfws, in, out + rb, dmask, ss);
+    if (stt != NAT_OK) return stt;
+    if (L.world > 1) {
+      cudaEvent_t e0 = info ? nat::timing_event(1, 2 * n_comm) : nullptr;
+      cudaEvent_t e1 = info ? nat::timing_event(1, 2 * n_comm + 1) : nullptr;
+      if (e0 && e1) NAT_CUDA_TRY(cudaEventRecord(e0, ss));
+      stt = nat::allgather_inplace(comm, (double*)out, (size_t)L.rpr * 2, ss);
+      if (e0 && e1) {
+        NAT_CUDA_TRY(cudaEventRecord(e1, ss));
+        ++n_comm;
+      }
+    }
+    return stt;
+  };
+  std::vector<nat::KrylovResult> res;
+  double t_op = 0;
+  st = nat::gmres_batched(1, n, L.ldv, bfull, xfull, opf, tol, max_iter, kw, res, s, info ? &t_op : nullptr);
+  if (st != NAT_OK) return st;
+  NAT_CUDA_TRY(cudaMemcpyAsync(x, xfull, sizeof(double2) * n, cudaMemcpyDeviceToDevice, s));
+  NAT_CUDA_TRY(cudaStreamSynchronize(s));
+  double t_comm = 0;
+  for (int q = 0; q < n_comm; ++q) {
+    float ms = 0.f;
+    NAT_CUDA_TRY(cudaEventElapsedTime(&ms, nat::timing_event(1, 2 * q), nat::timing_event(1, 2 * q + 1)));
     t_comm += 1e-3 * ms;
   }
   if (info) {

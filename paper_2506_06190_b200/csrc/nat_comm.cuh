@@ -11,6 +11,11 @@ struct nat_comm {
 
 namespace nat {
 nat_status allgather_inplace(nat_comm* comm, double* buf, size_t count, cudaStream_t s);
+// matrix-free operator (bem.cu): workspace, per-operator setup, y = (A x) on the op's rows
+size_t mf_apply_ws(const nat_bem_mf* op);
+nat_status mf_begin(const nat_bem_mf* op, void* ws, size_t ws_bytes, cudaStream_t s);
+nat_status mf_apply(const nat_bem_mf* op, void* ws, const double2* x, double2* y, const unsigned long long* skip,
+                    cudaStream_t s);
 nat_status matvec_internal(nat_prec prec, int64_t rows, int64_t n, const void* A, int64_t lda,
                            const void* x, void* y, cudaStream_t s, const unsigned long long* skip = nullptr);
 }  // namespace nat

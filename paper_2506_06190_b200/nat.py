@@ -51,6 +51,13 @@ class _SolveInfo(C.Structure):
                 ("t_total_s", C.c_double), ("t_matvec_s", C.c_double), ("t_comm_s", C.c_double)]
 
 
+class _BemMf(C.Structure):
+    _fields_ = [("mesh", C.POINTER(_Mesh)), ("geom", C.POINTER(_Geom)), ("opts", C.POINTER(_QuadOpts)),
+                ("k", C.c_double), ("prec", C.c_int), ("row_begin", C.c_int64), ("row_end", C.c_int64),
+                ("near_row_ptr", C.c_void_p), ("near_col", C.c_void_p), ("near_cls", C.c_void_p),
+                ("near_delta", C.c_void_p), ("diag_delta", C.c_void_p)]
+
+
 class _McOpts(C.Structure):
     _fields_ = [("M", C.c_int64), ("seed", C.c_uint64), ("stream_id", C.c_uint64),
                 ("eps", C.c_double), ("samples_in", C.c_void_p), ("sample_tri_in", C.c_void_p)]
@@ -82,6 +89,12 @@ _SIGS = {
                                    _P, _P, _P, _D, C.c_int, _I64, _I64, C.c_int, _P, _P, _I64,
                                    _P, _P, _SZ, _P]),
     "nat_bem_matvec": (C.c_int, [C.c_int, _I64, _I64, _P, _I64, _P, _P, _P]),
+    "nat_bem_mf_workspace": (_SZ, [C.POINTER(_BemMf), _I64, C.c_int]),
+    "nat_bem_mf_prepare": (C.c_int, [C.POINTER(_BemMf), C.c_int, _P, _P, _P, _SZ, _P]),
+    "nat_bem_mf_matvec": (C.c_int, [C.POINTER(_BemMf), _P, _P, _P, _SZ, _P]),
+    "nat_bem_mf_solve_workspace": (_SZ, [C.POINTER(_BemMf), C.c_int, C.c_int]),
+    "nat_bem_mf_solve": (C.c_int, [_P, C.POINTER(_BemMf), _P, _P, _D, C.c_int, _P, _SZ, C.POINTER(_SolveInfo),
+                                   _P]),
     "nat_comm_unique_id": (C.c_int, [_P]),
     "nat_comm_create_from_id": (C.c_int, [C.POINTER(_P), _P, C.c_int, C.c_int]),
     "nat_comm_destroy": (C.c_int, [_P]),
@@ -582,6 +595,80 @@ def nat_bem_solve(A_local: torch.Tensor, b_local: torch.Tensor, n: int, row_begi
     st = lib().nat_bem_solve(comm.handle if comm else None, pr, n, row_begin, row_begin + rows, _ptr(A_local),
                              lda, _ptr(b_local.contiguous()), _ptr(x), float(tol), int(max_iter), _ptr(ws),
                              ws.numel(), C.byref(info), _stream())
+    _check(st, allow_warn=True)
+    return x, dict(iters=info.iters, converged=info.converged, rel_residual=info.rel_residual,
+                   t_total_s=info.t_total_s, t_matvec_s=info.t_matvec_s, t_comm_s=info.t_comm_s)
+
+
+# ------------------------------------------------------------------------------------
+# NEXT-3: matrix-free dense operator (include/nat.h, nat_bem_mf_*)
+# ------------------------------------------------------------------------------------
+class BemMf:
+    """The matrix-free operator of rows [near.row_begin, near.row_end): keeps the C
+    structs alive and owns the near / diagonal corrections (c128 tensors)."""
+
+    def __init__(self, mesh: Mesh, geom: Geom, near: NearList, k: float, prec="fp32", opts=None):
+        self.mesh, self.geom, self.near = mesh, geom, near
+        self.prec = _prec(prec)
+        self.k = float(k)
+        dev = mesh.vxyz.device
+        rows = near.row_end - near.row_begin
+        self.delta = torch.zeros(max(near.nnz, 1), dtype=torch.complex128, device=dev)
+        self.diag = torch.zeros(rows, dtype=torch.complex128, device=dev)
+        self._m = mesh.c()
+        self._g = geom.c()
+        self._o = opts or quad_opts()
+        self.c = _BemMf(C.pointer(self._m), C.pointer(self._g), C.pointer(self._o), self.k, self.prec,
+                        near.row_begin, near.row_end, _ptr(near.row_ptr), C.c_void_p(near.col.data_ptr()),
+                        C.c_void_p(near.cls.data_ptr()), _ptr(self.delta), _ptr(self.diag))
+        self._ws = None
+
+    @property
+    def rows(self):
+        return self.near.row_end - self.near.row_begin
+
+    def ws(self, n_rhs=0):
+        need = lib().nat_bem_mf_workspace(C.byref(self.c), self.near.nnz, n_rhs)
+        if self._ws is None or self._ws.numel() < need:
+            self._ws = _ws(need, self.mesh.vxyz.device)
+        return self._ws
+
+
+def nat_bem_mf_prepare(mesh: Mesh, geom: Geom, near: NearList, k: float, g=None, prec="fp32", opts=None):
+    """Builds the matrix-free operator (near / diagonal corrections) and rhs = -V g.
+    Returns (BemMf, rhs c128 [n_rhs][rows] or None)."""
+    op = BemMf(mesh, geom, near, k, prec, opts)
+    n_rhs, rhs = 0, None
+    if g is not None:
+        g = torch.atleast_2d(g).to(torch.complex128).contiguous()
+        n_rhs = g.shape[0]
+        rhs = torch.empty(n_rhs, op.rows, dtype=torch.complex128, device=mesh.vxyz.device)
+    ws = op.ws(n_rhs)
+    _check(lib().nat_bem_mf_prepare(C.byref(op.c), n_rhs, _ptr(g), _ptr(rhs), _ptr(ws), ws.numel(), _stream()))
+    return op, rhs
+
+
+def nat_bem_mf_matvec(op: BemMf, x: torch.Tensor, out=None):
+    """y = A x on the operator's rows (A re-evaluated, never stored)."""
+    out = torch.empty(op.rows, dtype=torch.complex128, device=x.device) if out is None else out
+    ws = op.ws()
+    _check(lib().nat_bem_mf_matvec(C.byref(op.c), _ptr(x.to(torch.complex128).contiguous()), _ptr(out), _ptr(ws),
+                                   ws.numel(), _stream()))
+    return out
+
+
+def nat_bem_mf_solve(op: BemMf, b_local: torch.Tensor, comm: Optional["Comm"] = None, tol=1e-6, max_iter=200,
+                     out=None):
+    """GMRES over the matrix-free operator (row-sharded like nat_bem_solve).
+    Returns (x c128 [n], info dict)."""
+    n = op.mesh.n_tri
+    dev = b_local.device
+    x = torch.empty(n, dtype=torch.complex128, device=dev) if out is None else out
+    world = comm.world if comm else 1
+    ws = _ws(lib().nat_bem_mf_solve_workspace(C.byref(op.c), max_iter, world), dev)
+    info = _SolveInfo()
+    st = lib().nat_bem_mf_solve(comm.handle if comm else None, C.byref(op.c), _ptr(b_local.contiguous()), _ptr(x),
+                                float(tol), int(max_iter), _ptr(ws), ws.numel(), C.byref(info), _stream())
     _check(st, allow_warn=True)
     return x, dict(iters=info.iters, converged=info.converged, rel_residual=info.rel_residual,
                    t_total_s=info.t_total_s, t_matvec_s=info.t_matvec_s, t_comm_s=info.t_comm_s)
