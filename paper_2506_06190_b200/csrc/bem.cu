@@ -36,6 +36,8 @@ using nat::C2;
 
 constexpr int kThreads = 256;
 constexpr int kTI = 16;       // rows per far CTA
+constexpr int kTI64 = 4;      // rows per CTA of the fp64 far kernel (16 unrolled fp64 rows -> 238
+                              // registers, 8 warps/SM; ncu r01 matrix-free C5 capture)
 constexpr int kCC = 8;        // column passes per far CTA (columns = 256 * kCC)
 constexpr int kMaxFarQ = 7;
 constexpr int kNRmax = 2;
@@ -249,17 +251,17 @@ struct FarArgs {
 // the RHS operator V + beta K' (beta = i/k, reading R-bm).
 // MV (matrix-free matvec, NEXT-3): NR = 1, g = the iterate x; accumulates (A^far x)_i =
 // sum_j (-K_ij) x_j over the CTA's columns instead of storing A (bpart gets +sum).
-template <typename R, int NQ, int NR, bool BM = false, bool MV = false>
+template <typename R, int NQ, int NR, bool BM = false, bool MV = false, int TI = kTI>
 __global__ void __launch_bounds__(kThreads) far_kernel(FarArgs<R> a) {
   static_assert(!MV || (NR == 1 && !BM), "matrix-free: one iterate, conventional BIE");
   if (MV && a.skip && *a.skip == 0ull) return;
-  __shared__ R s_c[3][kTI];
-  __shared__ R s_m[3][kTI];  // BM: row normals
-  __shared__ double2 s_red[kThreads / 32][kTI][NR > 0 ? NR : 1];
+  __shared__ R s_c[3][TI];
+  __shared__ R s_m[3][TI];  // BM: row normals
+  __shared__ double2 s_red[kThreads / 32][TI][NR > 0 ? NR : 1];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t i0 = (int64_t)blockIdx.y * kTI;
+  const int64_t i0 = (int64_t)blockIdx.y * TI;
   const int64_t n = a.n;
-  if (tid < kTI) {
+  if (tid < TI) {
     int64_t r = i0 + tid;
     int64_t i = a.row_begin + (r < a.rows ? r : 0);
     s_c[0][tid] = (R)(a.cen[i] - a.cx);
@@ -272,10 +274,10 @@ __global__ void __launch_bounds__(kThreads) far_kernel(FarArgs<R> a) {
     }
   }
   __syncthreads();
-  const int nrows = (int)nat::min64(kTI, a.rows - i0);
-  C2<R> bacc[kTI][NR > 0 ? NR : 1];
+  const int nrows = (int)nat::min64(TI, a.rows - i0);
+  C2<R> bacc[TI][NR > 0 ? NR : 1];
 #pragma unroll
-  for (int t = 0; t < kTI; ++t)
+  for (int t = 0; t < TI; ++t)
 #pragma unroll
     for (int q = 0; q < (NR > 0 ? NR : 1); ++q) bacc[t][q] = {R(0), R(0)};
 
@@ -299,7 +301,7 @@ __global__ void __launch_bounds__(kThreads) far_kernel(FarArgs<R> a) {
       gj[q] = {(R)gv.x, (R)gv.y};
     }
 #pragma unroll
-    for (int t = 0; t < kTI; ++t) {
+    for (int t = 0; t < TI; ++t) {
       if (t < nrows) {
         R Vr, Vi, Kr, Ki;
         if constexpr (BM) {
@@ -332,7 +334,7 @@ __global__ void __launch_bounds__(kThreads) far_kernel(FarArgs<R> a) {
   }
   if constexpr (NR > 0) {
 #pragma unroll
-    for (int t = 0; t < kTI; ++t)
+    for (int t = 0; t < TI; ++t)
 #pragma unroll
       for (int q = 0; q < NR; ++q) {
         double vx = (double)bacc[t][q].x, vy = (double)bacc[t][q].y;
@@ -344,7 +346,7 @@ __global__ void __launch_bounds__(kThreads) far_kernel(FarArgs<R> a) {
         if (lane == 0) s_red[warp][t][q] = make_double2(vx, vy);
       }
     __syncthreads();
-    if (tid < kTI * NR) {
+    if (tid < TI * NR) {
       const int t = tid / NR, q = tid % NR;
       if (t < nrows) {
         double2 s = s_red[0][t][q];
@@ -520,12 +522,14 @@ __global__ void __launch_bounds__(kThreads, 2) far_kernel_x2(FarArgs<float> a) {
 
 template <typename R, int NQ, int NR>
 void launch_far(dim3 grid, const FarArgs<R>& fa, bool bm, cudaStream_t s) {
-  if (bm)
+  if (bm) {
     far_kernel<R, NQ, NR, true><<<grid, kThreads, 0, s>>>(fa);
-  else if constexpr (sizeof(R) == 4)
+  } else if constexpr (sizeof(R) == 4) {
     far_kernel_x2<NQ, NR><<<grid, kThreads, 0, s>>>(fa);
-  else
-    far_kernel<R, NQ, NR><<<grid, kThreads, 0, s>>>(fa);
+  } else {
+    grid.y = (unsigned)((fa.rows + kTI64 - 1) / kTI64);
+    far_kernel<R, NQ, NR, false, false, kTI64><<<grid, kThreads, 0, s>>>(fa);
+  }
 }
 
 template <typename R>
@@ -1468,30 +1472,39 @@ size_t mf_carve(nat::Carver& c, MfWs& w, int64_t n, int64_t rows, size_t rsz) {
   return c.bytes();
 }
 
-// y_r = sum over column blocks of the far partial sums (fixed block order) + the near
-// corrections in CSR order + the diagonal correction.
-__global__ void mf_final_kernel(int64_t rows, int64_t row_begin, int n_colblk, const double2* __restrict__ bpart,
-                                const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
-                                const double2* __restrict__ delta, const double2* __restrict__ diag,
-                                const double2* __restrict__ x, double2* __restrict__ y,
-                                const unsigned long long* __restrict__ skip) {
+// y_r = sum over column blocks of the far partial sums + the near corrections + the
+// diagonal correction.  One warp per row: lane l takes column blocks l, l+32, ... and near
+// entries l, l+32, ... (loads in flight together), fixed xor tree -> deterministic and
+// independent of the row split.
+__global__ void __launch_bounds__(256) mf_final_kernel(int64_t rows, int64_t row_begin, int n_colblk,
+                                                       const double2* __restrict__ bpart,
+                                                       const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                                                       const double2* __restrict__ delta,
+                                                       const double2* __restrict__ diag,
+                                                       const double2* __restrict__ x, double2* __restrict__ y,
+                                                       const unsigned long long* __restrict__ skip) {
   if (skip && *skip == 0ull) return;
-  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (r >= rows) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t r = blockIdx.x * (int64_t)(blockDim.x / 32) + (threadIdx.x >> 5);
+  if (r >= rows) return;  // whole warps
   double sx = 0.0, sy = 0.0;
-#pragma unroll 4
-  for (int cb = 0; cb < n_colblk; ++cb) {
+  for (int cb = lane; cb < n_colblk; cb += 32) {
     const double2 v = bpart[(size_t)cb * rows + r];
     sx += v.x;
     sy += v.y;
   }
   const int64_t e1 = rp[r + 1];
-#pragma unroll 4
-  for (int64_t e = rp[r]; e < e1; ++e) {
+  for (int64_t e = rp[r] + lane; e < e1; e += 32) {
     const double2 d = delta[e], xv = x[col[e]];
     sx += d.x * xv.x - d.y * xv.y;
     sy += d.x * xv.y + d.y * xv.x;
   }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    sx += __shfl_xor_sync(0xffffffffu, sx, o);
+    sy += __shfl_xor_sync(0xffffffffu, sy, o);
+  }
+  if (lane != 0) return;
   const double2 d = diag[r], xv = x[row_begin + r];
   sx += d.x * xv.x - d.y * xv.y;
   sy += d.x * xv.y + d.y * xv.x;
@@ -1549,13 +1562,15 @@ nat_status mf_launch(const nat_bem_mf* op, const MfWs& w, const double2* x, doub
   fa.bpart = w.bpart;
   fa.skip = skip;
   const int64_t n_colblk = (n + kThreads * kCC - 1) / (kThreads * kCC);
-  dim3 grid((unsigned)n_colblk, (unsigned)((rows + kTI - 1) / kTI));
-  if constexpr (sizeof(R) == 4)
+  if constexpr (sizeof(R) == 4) {
+    dim3 grid((unsigned)n_colblk, (unsigned)((rows + kTI - 1) / kTI));
     far_kernel_x2<NQ, 1, true><<<grid, kThreads, 0, s>>>(fa);
-  else
-    far_kernel<R, NQ, 1, false, true><<<grid, kThreads, 0, s>>>(fa);
+  } else {
+    dim3 grid((unsigned)n_colblk, (unsigned)((rows + kTI64 - 1) / kTI64));
+    far_kernel<R, NQ, 1, false, true, kTI64><<<grid, kThreads, 0, s>>>(fa);
+  }
   NAT_LAUNCH_CHECK();
-  mf_final_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, s>>>(
+  mf_final_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, s>>>(
       rows, op->row_begin, (int)n_colblk, w.bpart, op->near_row_ptr, op->near_col, (const double2*)op->near_delta,
       (const double2*)op->diag_delta, x, y, skip);
   NAT_LAUNCH_CHECK();

@@ -62,6 +62,29 @@ __global__ void k_sin(float* out, float a) {
   out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+__global__ void k_dfma(float* out, float a) {
+  double x[8];
+  const double ad = a;
+  for (int i = 0; i < 8; ++i) x[i] = threadIdx.x + i;
+  for (int it = 0; it < kIters; ++it)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = fma(x[i], ad, 0.5);
+  double s = 0;
+  for (int i = 0; i < 8; ++i) s += x[i];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = (float)s;
+}
+
+__global__ void k_rsq(float* out, float a) {
+  float x[8];
+  for (int i = 0; i < 8; ++i) x[i] = (threadIdx.x + i) * 1e-3f + 1.f;
+  for (int it = 0; it < kIters; ++it)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) asm("rsqrt.approx.ftz.f32 %0, %0;" : "+f"(x[i]));
+  float s = 0;
+  for (int i = 0; i < 8; ++i) s += x[i];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
 template <typename K>
 double run(K k, float* out, int blocks, int threads) {
   cudaEvent_t a, b;
@@ -94,5 +117,9 @@ int main() {
   printf("MUFU.EX2: %.3e lane-ops/s = %.1f per SM per clk\n", ops / t, ops / t / sms / (mhz * 1e3));
   t = run(k_sin, out, blocks, threads);
   printf("__sinf (FMUL.RZ+MUFU.SIN): %.3e /s = %.1f per SM per clk\n", ops / t, ops / t / sms / (mhz * 1e3));
+  t = run(k_rsq, out, blocks, threads);
+  printf("MUFU.RSQ: %.3e lane-ops/s = %.1f per SM per clk\n", ops / t, ops / t / sms / (mhz * 1e3));
+  t = run(k_dfma, out, blocks, threads);
+  printf("DFMA  : %.3e lane-ops/s = %.1f per SM per clk (FP64 pipe)\n", ops / t, ops / t / sms / (mhz * 1e3));
   return 0;
 }
