@@ -97,6 +97,13 @@ typedef struct {
   int burton_miller;  /* NEXT-1: 0 = the CBIE (beta = 0, default); 1 = Eq. BM as printed with    */
                       /* beta = i/k (reading R-bm): A = 1/2 I - K - beta W,            */
                       /* b = -(V + beta K') g - (beta/2) g; needs k > 0                            */
+  int galerkin;       /* NEXT-2: 0 = P0 centroid collocation (default); 1 = P0 Galerkin of the CBIE */
+                      /* (reading R-galerkin): A_ij = 1/2 |T_i| delta_ij - int_Ti int_Tj  */
+                      /* dG/dn_y, b_i = -sum_j int_Ti int_Tj G g_j; far pairs far_pts x far_pts     */
+                      /* tensor points, class N (R7 x near_levels_N)^2 tensor points, class S and   */
+                      /* self Sauter-Schwab (common vertex / edge / identical); near_levels_S and    */
+                      /* self_theta_pts unused; not with burton_miller or the matrix-free operator  */
+  int ss_order;       /* Gauss-Legendre points per cube dimension of Sauter-Schwab, default 4 (1..8) */
 } nat_quad_opts;
 
 /* ---------------------------------------------------------------------------------

@@ -152,6 +152,8 @@ struct Opts {
   int far_pts, lev_S, lev_N, gl;
   double eta;
   bool bm;  // Burton-Miller (NEXT-1, reading R-bm)
+  bool gal = false;  // Galerkin (NEXT-2, reading R-galerkin)
+  int ss = 4;        // Sauter-Schwab order
 };
 
 Opts opts_of(const nat_quad_opts* o) {
@@ -163,6 +165,8 @@ Opts opts_of(const nat_quad_opts* o) {
     if (o->near_levels_N) r.lev_N = o->near_levels_N;
     if (o->self_theta_pts) r.gl = o->self_theta_pts;
     if (o->near_eta > 0) r.eta = o->near_eta;
+    r.gal = o->galerkin != 0;
+    if (o->ss_order) r.ss = o->ss_order;
   }
   return r;
 }
@@ -245,17 +249,58 @@ struct FarArgs {
   bool store_A;
   double2* bpart;        // [n_colblk][n_rhs][rows]
   const unsigned long long* skip;  // MV (matrix-free operator inside GMRES): return when *skip == 0
+  // Galerkin (NEXT-2, NTQ > 1 test points per row): row triangles' vertices and areas,
+  // the test rule (the far rule, barycentric + weight)
+  const double* vx;
+  const int32_t* tri;
+  int64_t nv;
+  const double* area;
+  const double4* rule;
 };
+
+// Row test points of the far kernels, relative to the centre (cx, cy, cz): NTQ = 1 is the
+// centroid (collocation, weight 1); NTQ > 1 the far rule on T_i with weights w_t |T_i|
+// (Galerkin, reading R-galerkin).
+template <typename R, int NTQ>
+__device__ __forceinline__ void row_points(const FarArgs<R>& a, int64_t i, double (&c)[NTQ][3], double (&wt)[NTQ]) {
+  const int64_t n = a.n;
+  if constexpr (NTQ == 1) {
+    c[0][0] = a.cen[i] - a.cx;
+    c[0][1] = a.cen[n + i] - a.cy;
+    c[0][2] = a.cen[2 * n + i] - a.cz;
+    wt[0] = 1.0;
+  } else {
+    double v[3][3];
+#pragma unroll
+    for (int p = 0; p < 3; ++p) {
+      const int vi = a.tri[p * n + i];
+#pragma unroll
+      for (int d = 0; d < 3; ++d) v[p][d] = a.vx[d * a.nv + vi];
+    }
+    const double cen[3] = {a.cx, a.cy, a.cz};
+#pragma unroll
+    for (int t = 0; t < NTQ; ++t) {
+      const double4 L = a.rule[t];
+#pragma unroll
+      for (int d = 0; d < 3; ++d) c[t][d] = ((L.x * v[0][d] + L.y * v[1][d]) + L.z * v[2][d]) - cen[d];
+      wt[t] = L.w * a.area[i];
+    }
+  }
+}
 
 // Generic far assembly (fp64, and fp32 Burton-Miller).  BM: A_ij = -K_ij - beta W_ij and
 // the RHS operator V + beta K' (beta = i/k, reading R-bm).
 // MV (matrix-free matvec, NEXT-3): NR = 1, g = the iterate x; accumulates (A^far x)_i =
 // sum_j (-K_ij) x_j over the CTA's columns instead of storing A (bpart gets +sum).
-template <typename R, int NQ, int NR, bool BM = false, bool MV = false, int TI = kTI>
+// NTQ > 1 (Galerkin, NEXT-2): each entry sums NTQ test points of T_i with weights
+// w_t |T_i|; the diagonal j == i is left to the Sauter-Schwab self kernel (0 here).
+template <typename R, int NQ, int NR, bool BM = false, bool MV = false, int TI = kTI, int NTQ = 1>
 __global__ void __launch_bounds__(kThreads) far_kernel(FarArgs<R> a) {
   static_assert(!MV || (NR == 1 && !BM), "matrix-free: one iterate, conventional BIE");
+  static_assert(NTQ == 1 || (!BM && !MV), "Galerkin: conventional BIE, stored operator");
   if (MV && a.skip && *a.skip == 0ull) return;
-  __shared__ R s_c[3][TI];
+  __shared__ R s_c[NTQ][3][TI];
+  __shared__ R s_wt[NTQ][TI];
   __shared__ R s_m[3][TI];  // BM: row normals
   __shared__ double2 s_red[kThreads / 32][TI][NR > 0 ? NR : 1];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -264,9 +309,15 @@ __global__ void __launch_bounds__(kThreads) far_kernel(FarArgs<R> a) {
   if (tid < TI) {
     int64_t r = i0 + tid;
     int64_t i = a.row_begin + (r < a.rows ? r : 0);
-    s_c[0][tid] = (R)(a.cen[i] - a.cx);
-    s_c[1][tid] = (R)(a.cen[n + i] - a.cy);
-    s_c[2][tid] = (R)(a.cen[2 * n + i] - a.cz);
+    double c[NTQ][3], wt[NTQ];
+    row_points<R, NTQ>(a, i, c, wt);
+#pragma unroll
+    for (int t = 0; t < NTQ; ++t) {
+      s_c[t][0][tid] = (R)c[t][0];
+      s_c[t][1][tid] = (R)c[t][1];
+      s_c[t][2][tid] = (R)c[t][2];
+      s_wt[t][tid] = (R)wt[t];
+    }
     if constexpr (BM) {
       s_m[0][tid] = (R)a.nrm[i];
       s_m[1][tid] = (R)a.nrm[n + i];
@@ -308,15 +359,29 @@ __global__ void __launch_bounds__(kThreads) far_kernel(FarArgs<R> a) {
           C2<R> V{R(0), R(0)}, K{R(0), R(0)}, Kp{R(0), R(0)}, W{R(0), R(0)};
 #pragma unroll
           for (int q = 0; q < NQ; ++q)
-            nat::pair_accumulate_bm<R>(y[q][0] - s_c[0][t], y[q][1] - s_c[1][t], y[q][2] - s_c[2][t], nx, ny, nz,
+            nat::pair_accumulate_bm<R>(y[q][0] - s_c[0][0][t], y[q][1] - s_c[0][1][t], y[q][2] - s_c[0][2][t], nx, ny, nz,
                                        s_m[0][t], s_m[1][t], s_m[2][t], w[q], a.k, V, K, Kp, W);
           // A = -K - (i/k) W;  RHS operator V + (i/k) K'
           Kr = K.x - W.y / a.k;
           Ki = K.y + W.x / a.k;
           Vr = V.x - Kp.y / a.k;
           Vi = V.y + Kp.x / a.k;
+        } else if constexpr (NTQ == 1) {
+          far_entry<R, NQ>(y, w, nx, ny, nz, s_c[0][0][t], s_c[0][1][t], s_c[0][2][t], a.k, Vr, Vi, Kr, Ki);
         } else {
-          far_entry<R, NQ>(y, w, nx, ny, nz, s_c[0][t], s_c[1][t], s_c[2][t], a.k, Vr, Vi, Kr, Ki);
+          Vr = Vi = Kr = Ki = R(0);
+#pragma unroll
+          for (int tq = 0; tq < NTQ; ++tq) {
+            R vr, vi, kr, ki;
+            far_entry<R, NQ>(y, w, nx, ny, nz, s_c[tq][0][t], s_c[tq][1][t], s_c[tq][2][t], a.k, vr, vi, kr, ki);
+            const R wt = s_wt[tq][t];
+            Vr += wt * vr;
+            Vi += wt * vi;
+            Kr += wt * kr;
+            Ki += wt * ki;
+          }
+          // self pair (Sauter-Schwab kernel) and padding columns (jj = 0 may be the row)
+          if (!valid || j == a.row_begin + i0 + t) Vr = Vi = Kr = Ki = R(0);
         }
         if (!MV && a.store_A && valid) store_entry<R>(a.A, (size_t)(i0 + t) * a.lda + j, -Kr, -Ki);
         if constexpr (MV) {  // (-K) x_j
@@ -368,30 +433,36 @@ __global__ void __launch_bounds__(kThreads) far_kernel(FarArgs<R> a) {
 // accumulates -K directly (A_ij = -K_ij off the diagonal) and V g for the RHS.
 // MV (matrix-free matvec, NEXT-3): NR = 1 and g = the iterate x; the row sums are
 // sum_j (-K_ij) x_j = (A^far x)_i (no store, V unused).
-template <int NQ, int NR, bool MV = false>
+// NTQ > 1 (Galerkin, NEXT-2): NTQ test points per row with weights w_t |T_i| (staged in
+// shared memory); the self pair and padding columns are zeroed (Sauter-Schwab self kernel).
+template <int NQ, int NR, bool MV = false, int NTQ = 1>
 __global__ void __launch_bounds__(kThreads, 2) far_kernel_x2(FarArgs<float> a) {
   static_assert(kTI % 2 == 0, "row pairs");
   static_assert(!MV || NR == 1, "matrix-free: one iterate");
+  static_assert(NTQ == 1 || !MV, "Galerkin: stored operator");
   if (MV && a.skip && *a.skip == 0ull) return;
   constexpr int TP = kTI / 2;
   constexpr int NRr = NR > 0 ? NR : 1;
-  __shared__ __align__(16) f2r s_c[3][TP];
+  __shared__ __align__(16) f2r s_c[NTQ][3][TP];
+  __shared__ __align__(16) f2r s_wt[NTQ][TP];
   __shared__ double2 s_red[kThreads / 32][kTI][NRr];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t i0 = (int64_t)blockIdx.y * kTI;
   const int64_t n = a.n;
   if (tid < TP) {
-    float c[2][3];
+    double c[2][NTQ][3], wt[2][NTQ];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int64_t r = i0 + 2 * tid + h;
       const int64_t i = a.row_begin + (r < a.rows ? r : 0);
-      c[h][0] = (float)(a.cen[i] - a.cx);
-      c[h][1] = (float)(a.cen[n + i] - a.cy);
-      c[h][2] = (float)(a.cen[2 * n + i] - a.cz);
+      row_points<float, NTQ>(a, i, c[h], wt[h]);
     }
 #pragma unroll
-    for (int d = 0; d < 3; ++d) s_c[d][tid] = f2pack(c[0][d], c[1][d]);
+    for (int t = 0; t < NTQ; ++t) {
+#pragma unroll
+      for (int d = 0; d < 3; ++d) s_c[t][d][tid] = f2pack((float)c[0][t][d], (float)c[1][t][d]);
+      s_wt[t][tid] = f2pack((float)wt[0][t], (float)wt[1][t]);
+    }
   }
   __syncthreads();
   const int nrows = (int)nat::min64(kTI, a.rows - i0);
@@ -445,9 +516,16 @@ __global__ void __launch_bounds__(kThreads, 2) far_kernel_x2(FarArgs<float> a) {
 #pragma unroll
       for (int t = 0; t < TP; ++t, arow += 2 * ld) {
         if (FULL || 2 * t < nrows) {
-          const f2r cx = s_c[0][t], cy = s_c[1][t], cz = s_c[2][t];
-          const f2r cn = f2fma(cz, nz, f2fma(cy, ny, f2mul(cx, nx)));
           f2r Vr = 0ull, Vi = 0ull, Kr = 0ull, Ki = 0ull;  // K here is -K
+#pragma unroll
+          for (int tq = 0; tq < NTQ; ++tq) {
+          const f2r cx = s_c[tq][0][t], cy = s_c[tq][1][t], cz = s_c[tq][2][t];
+          const f2r cn = f2fma(cz, nz, f2fma(cy, ny, f2mul(cx, nx)));
+          f2r vr = 0ull, vi = 0ull, kr_ = 0ull, ki_ = 0ull;
+          f2r& Vr_ = NTQ == 1 ? Vr : vr;
+          f2r& Vi_ = NTQ == 1 ? Vi : vi;
+          f2r& Kr_ = NTQ == 1 ? Kr : kr_;
+          f2r& Ki_ = NTQ == 1 ? Ki : ki_;
 #pragma unroll
           for (int q = 0; q < NQ; ++q) {
             const f2r dx = f2sub(y[q][0], cx), dy = f2sub(y[q][1], cy), dz = f2sub(y[q][2], cz);
@@ -460,13 +538,31 @@ __global__ void __launch_bounds__(kThreads, 2) far_kernel_x2(FarArgs<float> a) {
             __sincosf(f2lo(kr), &s0, &c0);
             __sincosf(f2hi(kr), &s1, &c1);
             const f2r sn = f2pack(s0, s1), cs = f2pack(c0, c1);
-            const f2r tq = f2mul(w[q], rho);               // w G-part: tq e^{ikr}
-            Vr = f2fma(tq, cs, Vr);
-            Vi = f2fma(tq, sn, Vi);
-            const f2r u = f2mul(tq, f2mul(dn, f2mul(rho, rho)));
+            const f2r tw = f2mul(w[q], rho);               // w G-part: tw e^{ikr}
+            Vr_ = f2fma(tw, cs, Vr_);
+            Vi_ = f2fma(tw, sn, Vi_);
+            const f2r u = f2mul(tw, f2mul(dn, f2mul(rho, rho)));
             // -K += u (c + kr s) + i u (s - kr c)   [K = u (ikr - 1) e^{ikr}]
-            Kr = f2fma(u, f2fma(kr, sn, cs), Kr);
-            Ki = f2fma(u, f2fma(nkr, cs, sn), Ki);
+            Kr_ = f2fma(u, f2fma(kr, sn, cs), Kr_);
+            Ki_ = f2fma(u, f2fma(nkr, cs, sn), Ki_);
+          }
+          if constexpr (NTQ > 1) {  // test weight w_t |T_i|
+            const f2r wt = s_wt[tq][t];
+            Vr = f2fma(wt, vr, Vr);
+            Vi = f2fma(wt, vi, Vi);
+            Kr = f2fma(wt, kr_, Kr);
+            Ki = f2fma(wt, ki_, Ki);
+          }
+          }
+          if constexpr (NTQ > 1) {  // self pair and padding columns -> 0 (select, NaN-safe)
+            const int64_t ri = a.row_begin + i0 + 2 * t;
+            const bool z0 = !valid || j == ri, z1 = !valid || j == ri + 1;
+            if (z0 || z1) {
+              Vr = f2pack(z0 ? 0.f : f2lo(Vr), z1 ? 0.f : f2hi(Vr));
+              Vi = f2pack(z0 ? 0.f : f2lo(Vi), z1 ? 0.f : f2hi(Vi));
+              Kr = f2pack(z0 ? 0.f : f2lo(Kr), z1 ? 0.f : f2hi(Kr));
+              Ki = f2pack(z0 ? 0.f : f2lo(Ki), z1 ? 0.f : f2hi(Ki));
+            }
           }
           if (!MV && a.store_A && valid) {
             arow[0] = make_float2(f2lo(Kr), f2lo(Ki));
@@ -521,14 +617,20 @@ __global__ void __launch_bounds__(kThreads, 2) far_kernel_x2(FarArgs<float> a) {
 }
 
 template <typename R, int NQ, int NR>
-void launch_far(dim3 grid, const FarArgs<R>& fa, bool bm, cudaStream_t s) {
+void launch_far(dim3 grid, const FarArgs<R>& fa, bool bm, bool gal, cudaStream_t s) {
   if (bm) {
     far_kernel<R, NQ, NR, true><<<grid, kThreads, 0, s>>>(fa);
   } else if constexpr (sizeof(R) == 4) {
-    far_kernel_x2<NQ, NR><<<grid, kThreads, 0, s>>>(fa);
+    if (gal)
+      far_kernel_x2<NQ, NR, false, NQ><<<grid, kThreads, 0, s>>>(fa);
+    else
+      far_kernel_x2<NQ, NR><<<grid, kThreads, 0, s>>>(fa);
   } else {
     grid.y = (unsigned)((fa.rows + kTI64 - 1) / kTI64);
-    far_kernel<R, NQ, NR, false, false, kTI64><<<grid, kThreads, 0, s>>>(fa);
+    if (gal)
+      far_kernel<R, NQ, NR, false, false, kTI64, NQ><<<grid, kThreads, 0, s>>>(fa);
+    else
+      far_kernel<R, NQ, NR, false, false, kTI64><<<grid, kThreads, 0, s>>>(fa);
   }
 }
 
@@ -829,6 +931,259 @@ __global__ void self_kernel(int64_t n, int64_t nv, int64_t row_begin, int64_t ro
   }
 }
 
+// ------------------------------------------------------------------------------------
+// NEXT-2: Galerkin P0 near-field and self integrals (reading R-galerkin).
+// One warp per element pair — the paper's "single CUDA block for each element-to-element
+// integration" for adjacent or identical elements, at warp granularity:
+//   class N  (no shared vertex): tensor product of the class-N rule on T_i and on T_j;
+//   class S  (shared edge / vertex) and the self pair: Sauter-Schwab cube rules on the
+//            reference triangle {0 <= x2 <= x1 <= 1}, chi(x) = a + x1 (b - a) + x2 (c - b),
+//            shared vertices first (in T_i's order) so chi_i and chi_j agree on them.
+// Points are formed relative to T_i's first (ordered) vertex from fp64 edge vectors, so
+// d = y - x keeps its relative accuracy as r -> 0 in the fp32 path.  The lanes take rule
+// points l, l+32, ...; fixed xor-tree reduction (deterministic).
+// ------------------------------------------------------------------------------------
+constexpr int kSSMaxOrder = 8;
+constexpr int kSSRegions = 6 + 5 + 2;  // identical | edge | vertex
+
+struct SSTable {  // [P][5] = (x1, x2, y1, y2, w) per case, w includes the cube Jacobians
+  int off[4];     // case c occupies [off[c], off[c+1]); 0 identical, 1 edge, 2 vertex
+};
+
+// Host: the Sauter-Schwab rules (Sauter & Schwab, Boundary Element Methods, §5.2) with n
+// Gauss-Legendre points per cube dimension; sum of the weights of each case = 1/4.
+void ss_build(int n, std::vector<double>& out, SSTable& tab) {
+  std::vector<double> gx, gw;
+  gauss_legendre(n, gx, gw);
+  for (int q = 0; q < n; ++q) {
+    gx[q] = 0.5 * (gx[q] + 1.0);
+    gw[q] *= 0.5;
+  }
+  out.clear();
+  auto put = [&](double x1, double x2, double y1, double y2, double w) {
+    out.push_back(x1);
+    out.push_back(x2);
+    out.push_back(y1);
+    out.push_back(y2);
+    out.push_back(w);
+  };
+  for (int c = 0; c < 3; ++c) {
+    tab.off[c] = (int)(out.size() / 5);
+    for (int a = 0; a < n; ++a)
+      for (int b = 0; b < n; ++b)
+        for (int d = 0; d < n; ++d)
+          for (int e = 0; e < n; ++e) {
+            const double xi = gx[a], e1 = gx[b], e2 = gx[d], e3 = gx[e];
+            const double w4 = gw[a] * gw[b] * gw[d] * gw[e];
+            if (c == 0) {  // identical panels: 6 regions, Jacobian xi^3 e1^2 e2
+              const double f = w4 * xi * xi * xi * e1 * e1 * e2;
+              put(xi, xi * (1 - e1 + e1 * e2), xi * (1 - e1 * e2 * e3), xi * (1 - e1), f);
+              put(xi * (1 - e1 * e2 * e3), xi * (1 - e1), xi, xi * (1 - e1 + e1 * e2), f);
+              put(xi, xi * e1 * (1 - e2 + e2 * e3), xi * (1 - e1 * e2), xi * e1 * (1 - e2), f);
+              put(xi * (1 - e1 * e2), xi * e1 * (1 - e2), xi, xi * e1 * (1 - e2 + e2 * e3), f);
+              put(xi * (1 - e1 * e2 * e3), xi * e1 * (1 - e2 * e3), xi, xi * e1 * (1 - e2), f);
+              put(xi, xi * e1 * (1 - e2), xi * (1 - e1 * e2 * e3), xi * e1 * (1 - e2 * e3), f);
+            } else if (c == 1) {  // common edge x2 = 0: 5 regions
+              const double f1 = w4 * xi * xi * xi * e1 * e1, f = f1 * e2;
+              put(xi, xi * e1 * e3, xi * (1 - e1 * e2), xi * e1 * (1 - e2), f1);
+              put(xi, xi * e1, xi * (1 - e1 * e2 * e3), xi * e1 * e2 * (1 - e3), f);
+              put(xi * (1 - e1 * e2), xi * e1 * (1 - e2), xi, xi * e1 * e2 * e3, f);
+              put(xi * (1 - e1 * e2 * e3), xi * e1 * e2 * (1 - e3), xi, xi * e1, f);
+              put(xi * (1 - e1 * e2 * e3), xi * e1 * (1 - e2 * e3), xi, xi * e1 * e2, f);
+            } else {  // common vertex (0, 0): 2 regions, Jacobian xi^3 e2
+              const double f = w4 * xi * xi * xi * e2;
+              put(xi, xi * e1, xi * e2, xi * e2 * e3, f);
+              put(xi * e2, xi * e2 * e3, xi, xi * e1, f);
+            }
+          }
+  }
+  tab.off[3] = (int)(out.size() / 5);
+}
+
+template <typename R>
+struct GalArgs {
+  int64_t n, nv, row_begin, rows, lda;
+  const int32_t* col;
+  const double* vx;
+  const int32_t* tri;
+  const double* nrm;
+  const double* area;
+  const double4* rule_far;  // far rule (test and trial), NQ points
+  const double4* rule_N;    // class-N rule
+  int nN;
+  const double* ss;         // Sauter-Schwab points [P][5]
+  SSTable tab;
+  const int2* items;        // (entry, row) of this launch's class (class lists)
+  const int32_t* nitems;    // [device]
+  bool cls_S;
+  R k;
+  int n_rhs;
+  const double2* g;
+  void* A;
+  double2* corr;            // [nnz][n_rhs]
+  double2* corr_self;       // [rows][n_rhs]
+};
+
+template <typename R>
+__device__ __forceinline__ void warp_sum4(R& a, R& b, R& c, R& d) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+    c += __shfl_xor_sync(0xffffffffu, c, o);
+    d += __shfl_xor_sync(0xffffffffu, d, o);
+  }
+}
+
+// Integrals over T_i x T_j of (G, dG/dn_y) for one pair, warp-cooperative.  oi / oj: vertex
+// indices in Sauter-Schwab order; ss_case < 0 -> tensor rule (class N).  Returns (in
+// double, every lane) V, K (times 4 pi already divided out) and the far-rule V.
+template <typename R, int NQ>
+__device__ void gal_pair(const GalArgs<R>& a, const int (&oi)[3], const int (&oj)[3], int64_t j, int ss_case,
+                         double& Vr, double& Vi, double& Kr, double& Ki, double& fVr, double& fVi) {
+  const int lane = threadIdx.x & 31;
+  double P[3][3], Q[3][3];
+#pragma unroll
+  for (int p = 0; p < 3; ++p)
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      P[p][d] = a.vx[d * a.nv + oi[p]];
+      Q[p][d] = a.vx[d * a.nv + oj[p]];
+    }
+  const R nx = (R)a.nrm[j], ny = (R)a.nrm[a.n + j], nz = (R)a.nrm[2 * a.n + j];
+  // offsets relative to P0 in fp64, rounded once
+  R pe[2][3], qe[3][3];  // pe: P1 - P0, P2 - P1 (SS) ; qe: Q0 - P0, Q1 - Q0, Q2 - Q1 (SS)
+  R pv[3][3], qv[3][3];  // tensor rule: vertices minus P0
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    pe[0][d] = (R)(P[1][d] - P[0][d]);
+    pe[1][d] = (R)(P[2][d] - P[1][d]);
+    qe[0][d] = (R)(Q[0][d] - P[0][d]);
+    qe[1][d] = (R)(Q[1][d] - Q[0][d]);
+    qe[2][d] = (R)(Q[2][d] - Q[1][d]);
+#pragma unroll
+    for (int p = 0; p < 3; ++p) {
+      pv[p][d] = (R)(P[p][d] - P[0][d]);
+      qv[p][d] = (R)(Q[p][d] - P[0][d]);
+    }
+  }
+  C2<R> V{R(0), R(0)}, K{R(0), R(0)}, F{R(0), R(0)};
+  R dummy_r = R(0), dummy_i = R(0);
+  if (ss_case >= 0) {
+    const int b0 = a.tab.off[ss_case], b1 = a.tab.off[ss_case + 1];
+    for (int q = b0 + lane; q < b1; q += 32) {
+      const double* e = a.ss + (size_t)q * 5;
+      const R x1 = (R)e[0], x2 = (R)e[1], y1 = (R)e[2], y2 = (R)e[3], w = (R)e[4];
+      R d[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+        d[c] = (qe[0][c] + (y1 * qe[1][c] + y2 * qe[2][c])) - (x1 * pe[0][c] + x2 * pe[1][c]);
+      nat::pair_accumulate<R>(d[0], d[1], d[2], nx, ny, nz, w, a.k, V.x, V.y, K.x, K.y);
+    }
+  } else {
+    const int nN = a.nN, tot = nN * nN;
+    for (int q = lane; q < tot; q += 32) {
+      const double4 L = a.rule_N[q / nN], M = a.rule_N[q % nN];
+      R d[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+        d[c] = ((R)M.x * qv[0][c] + ((R)M.y * qv[1][c] + (R)M.z * qv[2][c])) -
+               ((R)L.y * pv[1][c] + (R)L.z * pv[2][c]);
+      nat::pair_accumulate<R>(d[0], d[1], d[2], nx, ny, nz, (R)(L.w * M.w), a.k, V.x, V.y, K.x, K.y);
+    }
+  }
+  // far-rule value of the same pair (the far kernel added it to the RHS): lanes < NQ^2
+  if (lane < NQ * NQ) {
+    const double4 L = a.rule_far[lane / NQ], M = a.rule_far[lane % NQ];
+    R d[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+      d[c] = ((R)M.x * qv[0][c] + ((R)M.y * qv[1][c] + (R)M.z * qv[2][c])) -
+             ((R)L.y * pv[1][c] + (R)L.z * pv[2][c]);
+    nat::pair_accumulate<R>(d[0], d[1], d[2], nx, ny, nz, (R)(L.w * M.w), a.k, F.x, F.y, dummy_r, dummy_i);
+  }
+  double v0 = V.x, v1 = V.y, k0 = K.x, k1 = K.y, f0 = F.x, f1 = F.y, z0 = 0.0, z1 = 0.0;
+  warp_sum4(v0, v1, k0, k1);
+  warp_sum4(f0, f1, z0, z1);
+  Vr = v0;
+  Vi = v1;
+  Kr = k0;
+  Ki = k1;
+  fVr = f0;
+  fVi = f1;
+}
+
+// Near pairs of one class list: A_ij = -K_ij (Galerkin), b corrected by -(V - V^far) g_j.
+template <typename R, int NQ>
+__global__ void __launch_bounds__(256) gal_near_kernel(GalArgs<R> a) {
+  const int64_t nitems = *a.nitems;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x / 32);
+  for (int64_t it = blockIdx.x * (int64_t)(blockDim.x / 32) + (threadIdx.x >> 5); it < nitems; it += warps) {
+    const int2 item = a.items[it];
+    const int64_t e = item.x, r = item.y, i = a.row_begin + r, j = a.col[e];
+    const int n = (int)a.n;
+    const int ti[3] = {a.tri[i], a.tri[n + i], a.tri[2 * n + i]};
+    const int tj[3] = {a.tri[j], a.tri[n + j], a.tri[2 * n + j]};
+    int oi[3], oj[3], ss_case = -1;
+    if (a.cls_S) {  // shared vertices first, in T_i's order
+      int ns = 0, ni = 0, nj = 0;
+      int si[3], ri[3], rj[3];
+      for (int p = 0; p < 3; ++p) {
+        const bool sh = ti[p] == tj[0] || ti[p] == tj[1] || ti[p] == tj[2];
+        if (sh) si[ns++] = ti[p];
+        else ri[ni++] = ti[p];
+      }
+      for (int p = 0; p < 3; ++p) {
+        const bool sh = tj[p] == ti[0] || tj[p] == ti[1] || tj[p] == ti[2];
+        if (!sh) rj[nj++] = tj[p];
+      }
+      for (int p = 0; p < ns; ++p) oi[p] = oj[p] = si[p];
+      for (int p = 0; p < ni; ++p) oi[ns + p] = ri[p];
+      for (int p = 0; p < nj; ++p) oj[ns + p] = rj[p];
+      ss_case = ns == 2 ? 1 : 2;
+    } else {
+      for (int p = 0; p < 3; ++p) {
+        oi[p] = ti[p];
+        oj[p] = tj[p];
+      }
+    }
+    double Vr, Vi, Kr, Ki, fVr, fVi;
+    gal_pair<R, NQ>(a, oi, oj, j, ss_case, Vr, Vi, Kr, Ki, fVr, fVi);
+    if ((threadIdx.x & 31) != 0) continue;
+    const double Ai = a.area[i], Aj = a.area[j];
+    const double sc = ss_case >= 0 ? 4.0 * Ai * Aj : Ai * Aj;  // SS: |det chi_i| |det chi_j|
+    const double s4 = sc * nat::kInv4Pi;
+    store_entry<R>(a.A, (size_t)r * a.lda + j, (R)(-Kr * s4), (R)(-Ki * s4));
+    const double dVr = (Vr - fVr * (Ai * Aj / sc)) * s4, dVi = (Vi - fVi * (Ai * Aj / sc)) * s4;
+    for (int q = 0; q < a.n_rhs; ++q) {
+      const double2 gv = a.g[(size_t)q * n + j];
+      a.corr[(size_t)e * a.n_rhs + q] = make_double2(-(dVr * gv.x - dVi * gv.y), -(dVr * gv.y + dVi * gv.x));
+    }
+  }
+}
+
+// Self pairs (Sauter-Schwab identical panels): A_ii = |T_i| / 2 (K_ii = 0, flat), b corrected
+// by -V_ii g_i (the far kernel skipped the diagonal).
+template <typename R, int NQ>
+__global__ void __launch_bounds__(256) gal_self_kernel(GalArgs<R> a) {
+  const int64_t r = blockIdx.x * (int64_t)(blockDim.x / 32) + (threadIdx.x >> 5);
+  if (r >= a.rows) return;
+  const int64_t i = a.row_begin + r;
+  const int n = (int)a.n;
+  const int oi[3] = {a.tri[i], a.tri[n + i], a.tri[2 * n + i]};
+  double Vr, Vi, Kr, Ki, fVr, fVi;
+  gal_pair<R, NQ>(a, oi, oi, i, 0, Vr, Vi, Kr, Ki, fVr, fVi);
+  if ((threadIdx.x & 31) != 0) return;
+  const double Ai = a.area[i];
+  store_entry<R>(a.A, (size_t)r * a.lda + i, (R)(0.5 * Ai), R(0));
+  const double s4 = 4.0 * Ai * Ai * nat::kInv4Pi;
+  const double dVr = Vr * s4, dVi = Vi * s4;
+  for (int q = 0; q < a.n_rhs; ++q) {
+    const double2 gv = a.g[(size_t)q * n + i];
+    a.corr_self[(size_t)r * a.n_rhs + q] = make_double2(-(dVr * gv.x - dVi * gv.y), -(dVr * gv.y + dVi * gv.x));
+  }
+}
+
 // Per-class compaction of the near list (CSR order kept): cnt[c][r+1] = entries of class
 // c+1 in row r; after the scan, fill writes (entry, row) pairs into the class lists.
 __global__ void class_count_kernel(int64_t rows, const int64_t* __restrict__ rp, const uint8_t* __restrict__ cls,
@@ -1124,6 +1479,7 @@ struct AsmWs {
   double2* bpart;
   double2* corr;
   double2* corr_self;
+  double* ss;      // Galerkin: Sauter-Schwab points [P][5]
 };
 
 size_t carve(nat::Carver& c, AsmWs& w, int64_t n, int64_t rows, int64_t nnz, int n_rhs, int nfar,
@@ -1145,6 +1501,7 @@ size_t carve(nat::Carver& c, AsmWs& w, int64_t n, int64_t rows, int64_t nnz, int
   w.bpart = c.take<double2>((size_t)n_colblk * (n_rhs > 0 ? n_rhs : 1) * rows);
   w.corr = c.take<double2>((size_t)(nnz > 0 ? nnz : 1) * (n_rhs > 0 ? n_rhs : 1));
   w.corr_self = c.take<double2>((size_t)rows * (n_rhs > 0 ? n_rhs : 1));
+  w.ss = c.take<double>((size_t)kSSRegions * kSSMaxOrder * kSSMaxOrder * kSSMaxOrder * kSSMaxOrder * 5);
   return c.bytes();
 }
 
@@ -1164,7 +1521,8 @@ nat_status assemble_impl(const nat_mesh* mesh, const nat_geom* geom, const Opts&
                          const int64_t* rp, const int32_t* col, const uint8_t* cls, int64_t nnz, double k,
                          int64_t row_begin, int64_t rows, int n_rhs, const double2* g, void* A,
                          int64_t lda, double2* rhs, AsmWs& w, const std::vector<Pt>& pS,
-                         const std::vector<Pt>& pN, cudaStream_t s, MfOut mf = MfOut{}) {
+                         const std::vector<Pt>& pN, cudaStream_t s, MfOut mf = MfOut{},
+                         const SSTable* ss_tab = nullptr) {
   const int64_t n = mesh->n_tri;
   const double cx = geom->center[0], cy = geom->center[1], cz = geom->center[2];
   FarCols<R> cols{(const R*)w.qxyz, (const R*)w.qw, (const R*)w.qn};
@@ -1189,24 +1547,72 @@ nat_status assemble_impl(const nat_mesh* mesh, const nat_geom* geom, const Opts&
   fa.g = g;
   fa.A = A;
   fa.bpart = w.bpart;
+  fa.vx = mesh->vxyz;
+  fa.tri = mesh->tri;
+  fa.nv = mesh->n_vert;
+  fa.area = geom->area;
+  fa.rule = w.rule_far;
   const int64_t n_colblk = (n + kThreads * kCC - 1) / (kThreads * kCC);
   dim3 grid((unsigned)n_colblk, (unsigned)((rows + kTI - 1) / kTI));
   if (n_rhs == 0) {
     fa.store_A = true;
-    if (!mf.delta) launch_far<R, NQ, 0>(grid, fa, o.bm, s);
+    if (!mf.delta) launch_far<R, NQ, 0>(grid, fa, o.bm, o.gal, s);
   } else {
     for (int q0 = 0; q0 < n_rhs; q0 += kNRmax) {
       fa.rhs0 = q0;
       fa.store_A = (q0 == 0) && !mf.delta;
       if (n_rhs - q0 >= 2)
-        launch_far<R, NQ, 2>(grid, fa, o.bm, s);
+        launch_far<R, NQ, 2>(grid, fa, o.bm, o.gal, s);
       else
-        launch_far<R, NQ, 1>(grid, fa, o.bm, s);
+        launch_far<R, NQ, 1>(grid, fa, o.bm, o.gal, s);
     }
   }
   NAT_LAUNCH_CHECK();
+  if (o.gal) {  // NEXT-2: Galerkin near / self integrals (warp per pair)
+    GalArgs<R> ga{};
+    ga.n = n;
+    ga.nv = mesh->n_vert;
+    ga.row_begin = row_begin;
+    ga.rows = rows;
+    ga.lda = lda;
+    ga.col = col;
+    ga.vx = mesh->vxyz;
+    ga.tri = mesh->tri;
+    ga.nrm = geom->normal;
+    ga.area = geom->area;
+    ga.rule_far = w.rule_far;
+    ga.rule_N = w.rule_N;
+    ga.nN = (int)pN.size();
+    ga.ss = w.ss;
+    ga.tab = *ss_tab;
+    ga.k = (R)k;
+    ga.n_rhs = n_rhs;
+    ga.g = g;
+    ga.A = A;
+    ga.corr = w.corr;
+    ga.corr_self = w.corr_self;
+    if (nnz > 0) {
+      const unsigned rb = (unsigned)((rows + 255) / 256);
+      class_count_kernel<<<rb, 256, 0, s>>>(rows, rp, cls, w.cntS, w.cntN);
+      scan_i32_kernel<<<2, 1024, 0, s>>>(w.cntS, w.cntN, rows);
+      class_fill_kernel<<<rb, 256, 0, s>>>(rows, rp, cls, w.cntS, w.cntN, w.listS, w.listN);
+      NAT_LAUNCH_CHECK();
+      const unsigned gw = (unsigned)std::min<int64_t>((int64_t)nat::device_sm_count() * 16, (nnz + 7) / 8);
+      ga.items = w.listS;
+      ga.nitems = w.cntS + rows;
+      ga.cls_S = true;
+      gal_near_kernel<R, NQ><<<gw, 256, 0, s>>>(ga);
+      ga.items = w.listN;
+      ga.nitems = w.cntN + rows;
+      ga.cls_S = false;
+      gal_near_kernel<R, NQ><<<gw, 256, 0, s>>>(ga);
+      NAT_LAUNCH_CHECK();
+    }
+    gal_self_kernel<R, NQ><<<(unsigned)((rows + 7) / 8), 256, 0, s>>>(ga);
+    NAT_LAUNCH_CHECK();
+  }
   // a5: near pairs overwrite A and correct b; self term
-  if (nnz > 0) {
+  if (nnz > 0 && !o.gal) {
     const unsigned rb = (unsigned)((rows + 255) / 256);
     class_count_kernel<<<rb, 256, 0, s>>>(rows, rp, cls, w.cntS, w.cntN);
     scan_i32_kernel<<<2, 1024, 0, s>>>(w.cntS, w.cntN, rows);
@@ -1262,7 +1668,9 @@ nat_status assemble_impl(const nat_mesh* mesh, const nat_geom* geom, const Opts&
       near_kernel<R, NQ, 1><<<gN, kThreads, na.npts * rsz, s>>>(na);
     NAT_LAUNCH_CHECK();
   }
-  if (o.bm)
+  if (o.gal) {
+    // done above
+  } else if (o.bm)
     self_kernel<R, NQ, true><<<(unsigned)((rows + 127) / 128), 128, 0, s>>>(
         n, mesh->n_vert, row_begin, rows, lda, mesh->vxyz, mesh->tri, geom->centroid, geom->normal, cols, cx, cy,
         cz, k, w.gl, w.gl + o.gl, o.gl, n_rhs, g, A, w.corr_self, mf.diag);
@@ -1311,6 +1719,10 @@ nat_status assemble_entry(const nat_mesh* mesh, const nat_geom* geom, const nat_
               "near levels must be in [0, %d]", kMaxLevel);
   NAT_REQUIRE(o.gl >= 2 && o.gl <= kMaxGL, "self_theta_pts must be in [2, %d]", kMaxGL);
   NAT_REQUIRE(!mf.delta || !(opts && opts->burton_miller), "the matrix-free operator is the conventional BIE only");
+  NAT_REQUIRE(!(opts && opts->galerkin) || !(opts->burton_miller || mf.delta),
+              "Galerkin assembly is the stored conventional BIE (no Burton-Miller / matrix-free)");
+  NAT_REQUIRE(!(opts && opts->galerkin) || (opts->ss_order >= 0 && opts->ss_order <= kSSMaxOrder),
+              "ss_order must be in [1, %d]", kSSMaxOrder);
   NAT_REQUIRE_DEV(near_row_ptr);
   if (mf.delta) {
     NAT_REQUIRE_DEV(mf.delta);
@@ -1375,11 +1787,18 @@ nat_status assemble_entry(const nat_mesh* mesh, const nat_geom* geom, const nat_
     NAT_CUDA_TRY(cudaMemcpyAsync(base, blob.data(), total, cudaMemcpyHostToDevice, s));
   }
 
+  SSTable tab{};
+  if (o.gal) {
+    std::vector<double> ssv;
+    ss_build(o.ss, ssv, tab);
+    // pageable source: staged before the call returns
+    NAT_CUDA_TRY(cudaMemcpyAsync(w.ss, ssv.data(), ssv.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+  }
   const double2* gg = (const double2*)g;
   double2* bb = (double2*)rhs;
 #define NAT_ASM(R, NQ)                                                                         \
   assemble_impl<R, NQ>(mesh, geom, o, near_row_ptr, near_col, near_cls, nnz, k, row_begin, rows, \
-                       n_rhs, gg, A, lda, bb, w, pS, pN, s, mf)
+                       n_rhs, gg, A, lda, bb, w, pS, pN, s, mf, &tab)
   if (prec == NAT_FP32) {
     switch (o.far_pts) {
       case 1: return NAT_ASM(float, 1);

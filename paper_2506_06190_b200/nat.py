@@ -43,7 +43,8 @@ class _Geom(C.Structure):
 
 class _QuadOpts(C.Structure):
     _fields_ = [("far_pts", C.c_int), ("near_levels_S", C.c_int), ("near_levels_N", C.c_int),
-                ("near_eta", C.c_double), ("self_theta_pts", C.c_int), ("burton_miller", C.c_int)]
+                ("near_eta", C.c_double), ("self_theta_pts", C.c_int), ("burton_miller", C.c_int),
+                ("galerkin", C.c_int), ("ss_order", C.c_int)]
 
 
 class _SolveInfo(C.Structure):
@@ -243,9 +244,12 @@ class Sources:
                         self.p.shape[0], _ptr(self.p), _ptr(self.g), (C.c_double * 3)(*self.center))
 
 
-def quad_opts(far_pts=0, near_levels_S=0, near_levels_N=0, near_eta=0.0, self_theta_pts=0, burton_miller=False):
-    """nat_quad_opts (zeros = defaults); burton_miller selects Eq. BM with beta = i/k (NEXT-1)."""
-    return _QuadOpts(far_pts, near_levels_S, near_levels_N, near_eta, self_theta_pts, int(bool(burton_miller)))
+def quad_opts(far_pts=0, near_levels_S=0, near_levels_N=0, near_eta=0.0, self_theta_pts=0, burton_miller=False,
+              galerkin=False, ss_order=0):
+    """nat_quad_opts (zeros = defaults); burton_miller selects Eq. BM with beta = i/k (NEXT-1);
+    galerkin the P0 Galerkin discretisation with Sauter-Schwab singular quadrature (NEXT-2)."""
+    return _QuadOpts(far_pts, near_levels_S, near_levels_N, near_eta, self_theta_pts, int(bool(burton_miller)),
+                     int(bool(galerkin)), int(ss_order))
 
 
 # ------------------------------------------------------------------------------------
