@@ -1009,9 +1009,13 @@ struct GalArgs {
   const double* nrm;
   const double* area;
   const double4* rule_far;  // far rule (test and trial), NQ points
-  const double4* rule_N;    // class-N rule
+  const double4* rule_N;    // class-N rule (fp64, fp32)
+  const float4* rule_Nf;
   int nN;
-  const double* ss;         // Sauter-Schwab points [P][5]
+  const float4* ssx;        // Sauter-Schwab points (x1, x2, y1, y2) [P] in R's rounding ...
+  const double4* ssx64;
+  const double* ssw;        // ... and weights [P] (fp64, fp32)
+  const float* ssw32;
   SSTable tab;
   const int2* items;        // (entry, row) of this launch's class (class lists)
   const int32_t* nitems;    // [device]
@@ -1037,11 +1041,14 @@ __device__ __forceinline__ void warp_sum4(R& a, R& b, R& c, R& d) {
 
 // Integrals over T_i x T_j of (G, dG/dn_y) for one pair, warp-cooperative.  oi / oj: vertex
 // indices in Sauter-Schwab order; ss_case < 0 -> tensor rule (class N).  Returns (in
-// double, every lane) V, K (times 4 pi already divided out) and the far-rule V.
+// double, every lane) V, K (4 pi G form, unscaled rule sums) and the far-rule V.
+// Class N: the warp stages 32 test points at a time in shared memory (broadcast reads),
+// lane l owns trial point b = l (+32 ...), so the inner loop is LDS + 3 FADD + the pair.
 template <typename R, int NQ>
 __device__ void gal_pair(const GalArgs<R>& a, const int (&oi)[3], const int (&oj)[3], int64_t j, int ss_case,
                          double& Vr, double& Vi, double& Kr, double& Ki, double& fVr, double& fVi) {
-  const int lane = threadIdx.x & 31;
+  __shared__ __align__(16) R s_pts[8][32][4];  // per warp: test points (x, y, z, w)
+  const int lane = threadIdx.x & 31, wib = (threadIdx.x >> 5) & 7;
   double P[3][3], Q[3][3];
 #pragma unroll
   for (int p = 0; p < 3; ++p)
@@ -1072,8 +1079,19 @@ __device__ void gal_pair(const GalArgs<R>& a, const int (&oi)[3], const int (&oj
   if (ss_case >= 0) {
     const int b0 = a.tab.off[ss_case], b1 = a.tab.off[ss_case + 1];
     for (int q = b0 + lane; q < b1; q += 32) {
-      const double* e = a.ss + (size_t)q * 5;
-      const R x1 = (R)e[0], x2 = (R)e[1], y1 = (R)e[2], y2 = (R)e[3], w = (R)e[4];
+      R x1, x2, y1, y2;
+      if constexpr (sizeof(R) == 4) {
+        const float4 e = a.ssx[q];
+        x1 = e.x, x2 = e.y, y1 = e.z, y2 = e.w;
+      } else {
+        const double4 e = a.ssx64[q];
+        x1 = e.x, x2 = e.y, y1 = e.z, y2 = e.w;
+      }
+      R w;
+      if constexpr (sizeof(R) == 4)
+        w = a.ssw32[q];
+      else
+        w = a.ssw[q];
       R d[3];
 #pragma unroll
       for (int c = 0; c < 3; ++c)
@@ -1081,15 +1099,32 @@ __device__ void gal_pair(const GalArgs<R>& a, const int (&oi)[3], const int (&oj
       nat::pair_accumulate<R>(d[0], d[1], d[2], nx, ny, nz, w, a.k, V.x, V.y, K.x, K.y);
     }
   } else {
-    const int nN = a.nN, tot = nN * nN;
-    for (int q = lane; q < tot; q += 32) {
-      const double4 L = a.rule_N[q / nN], M = a.rule_N[q % nN];
-      R d[3];
+    const int nN = a.nN;
+    for (int bb = 0; bb < nN; bb += 32) {
+      const int b = bb + lane;
+      R y[3] = {R(0), R(0), R(0)}, wb = R(0);
+      if (b < nN) {
+        const double4 M = a.rule_N[b];
 #pragma unroll
-      for (int c = 0; c < 3; ++c)
-        d[c] = ((R)M.x * qv[0][c] + ((R)M.y * qv[1][c] + (R)M.z * qv[2][c])) -
-               ((R)L.y * pv[1][c] + (R)L.z * pv[2][c]);
-      nat::pair_accumulate<R>(d[0], d[1], d[2], nx, ny, nz, (R)(L.w * M.w), a.k, V.x, V.y, K.x, K.y);
+        for (int c = 0; c < 3; ++c) y[c] = (R)((M.x * (double)qv[0][c] + M.y * (double)qv[1][c]) + M.z * (double)qv[2][c]);
+        wb = (R)M.w;
+      }
+      for (int aa = 0; aa < nN; aa += 32) {
+        __syncwarp();
+        if (aa + lane < nN) {
+          const double4 L = a.rule_N[aa + lane];
+#pragma unroll
+          for (int c = 0; c < 3; ++c) s_pts[wib][lane][c] = (R)(L.y * (double)pv[1][c] + L.z * (double)pv[2][c]);
+          s_pts[wib][lane][3] = (R)L.w;
+        }
+        __syncwarp();
+        const int na = min(32, nN - aa);
+        if (b < nN)
+          for (int t = 0; t < na; ++t) {
+            const R x0 = s_pts[wib][t][0], x1 = s_pts[wib][t][1], x2 = s_pts[wib][t][2], wa = s_pts[wib][t][3];
+            nat::pair_accumulate<R>(y[0] - x0, y[1] - x1, y[2] - x2, nx, ny, nz, wa * wb, a.k, V.x, V.y, K.x, K.y);
+          }
+      }
     }
   }
   // far-rule value of the same pair (the far kernel added it to the RHS): lanes < NQ^2
@@ -1155,6 +1190,112 @@ __global__ void __launch_bounds__(256) gal_near_kernel(GalArgs<R> a) {
     const double s4 = sc * nat::kInv4Pi;
     store_entry<R>(a.A, (size_t)r * a.lda + j, (R)(-Kr * s4), (R)(-Ki * s4));
     const double dVr = (Vr - fVr * (Ai * Aj / sc)) * s4, dVi = (Vi - fVi * (Ai * Aj / sc)) * s4;
+    for (int q = 0; q < a.n_rhs; ++q) {
+      const double2 gv = a.g[(size_t)q * n + j];
+      a.corr[(size_t)e * a.n_rhs + q] = make_double2(-(dVr * gv.x - dVi * gv.y), -(dVr * gv.y + dVi * gv.x));
+    }
+  }
+}
+
+// Class-N pairs (tensor rule, no shared vertex) with kGN lanes per pair, so a warp keeps
+// 32 / kGN pairs in flight (the index -> vertex load chain of one pair is longer than its
+// 784 evaluations spread over a whole warp): lane l of a group owns trial points
+// b = l, l + kGN, ... (up to kNB in registers per pass) and sweeps every test point.
+constexpr int kGN = 4;
+constexpr int kNB = 8;
+template <typename R, int NQ>
+__global__ void __launch_bounds__(256) gal_near_n_kernel(GalArgs<R> a) {
+  const int64_t nitems = *a.nitems;
+  const int lane = threadIdx.x & 31, lg = lane % kGN;
+  const unsigned gmask = ((1u << kGN) - 1u) << (lane / kGN * kGN);
+  const int64_t groups = (int64_t)gridDim.x * (blockDim.x / kGN);
+  const int nN = a.nN;
+  for (int64_t it = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / kGN; it < nitems; it += groups) {
+    const int2 item = a.items[it];
+    const int64_t e = item.x, r = item.y, i = a.row_begin + r, j = a.col[e];
+    const int n = (int)a.n;
+    double P[3][3], Q[3][3];
+#pragma unroll
+    for (int p = 0; p < 3; ++p) {
+      const int vi = a.tri[p * n + i], vj = a.tri[p * n + j];
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        P[p][d] = a.vx[d * a.nv + vi];
+        Q[p][d] = a.vx[d * a.nv + vj];
+      }
+    }
+    const R nx = (R)a.nrm[j], ny = (R)a.nrm[n + j], nz = (R)a.nrm[2 * n + j];
+    R pv[3][3], qv[3][3];  // vertices minus P0, rounded once
+#pragma unroll
+    for (int p = 0; p < 3; ++p)
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        pv[p][d] = (R)(P[p][d] - P[0][d]);
+        qv[p][d] = (R)(Q[p][d] - P[0][d]);
+      }
+    C2<R> V{R(0), R(0)}, K{R(0), R(0)}, F{R(0), R(0)};
+    R dr = R(0), di = R(0);
+    for (int b0 = lg; b0 < nN; b0 += kGN * kNB) {
+      R y[kNB][3], wb[kNB];
+#pragma unroll
+      for (int u = 0; u < kNB; ++u) {
+        const int b = b0 + u * kGN;
+        if (b < nN) {
+          R Mx, My, Mz, Mw;
+          if constexpr (sizeof(R) == 4) {
+            const float4 M = a.rule_Nf[b];
+            Mx = M.x, My = M.y, Mz = M.z, Mw = M.w;
+          } else {
+            const double4 M = a.rule_N[b];
+            Mx = M.x, My = M.y, Mz = M.z, Mw = M.w;
+          }
+#pragma unroll
+          for (int c = 0; c < 3; ++c) y[u][c] = Mx * qv[0][c] + (My * qv[1][c] + Mz * qv[2][c]);
+          wb[u] = Mw;
+        } else {
+          y[u][0] = y[u][1] = y[u][2] = R(1e3);  // far away, zero weight
+          wb[u] = R(0);
+        }
+      }
+      for (int t = 0; t < nN; ++t) {
+        R Lx, Ly, Lz, Lw;
+        if constexpr (sizeof(R) == 4) {
+          const float4 L = a.rule_Nf[t];
+          Ly = L.y, Lz = L.z, Lw = L.w;
+          (void)Lx;
+        } else {
+          const double4 L = a.rule_N[t];
+          Ly = L.y, Lz = L.z, Lw = L.w;
+          (void)Lx;
+        }
+        R x[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) x[c] = Ly * pv[1][c] + Lz * pv[2][c];
+#pragma unroll
+        for (int u = 0; u < kNB; ++u)
+          nat::pair_accumulate<R>(y[u][0] - x[0], y[u][1] - x[1], y[u][2] - x[2], nx, ny, nz, Lw * wb[u], a.k, V.x,
+                                  V.y, K.x, K.y);
+      }
+    }
+    for (int q = lg; q < NQ * NQ; q += kGN) {  // far-rule value of the pair
+      const double4 L = a.rule_far[q / NQ], M = a.rule_far[q % NQ];
+      R d[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+        d[c] = ((R)M.x * qv[0][c] + ((R)M.y * qv[1][c] + (R)M.z * qv[2][c])) -
+               ((R)L.y * pv[1][c] + (R)L.z * pv[2][c]);
+      nat::pair_accumulate<R>(d[0], d[1], d[2], nx, ny, nz, (R)(L.w * M.w), a.k, F.x, F.y, dr, di);
+    }
+    double v[6] = {V.x, V.y, K.x, K.y, F.x, F.y};
+#pragma unroll
+    for (int o = kGN / 2; o > 0; o >>= 1)
+#pragma unroll
+      for (int q = 0; q < 6; ++q) v[q] += __shfl_xor_sync(gmask, v[q], o, kGN);
+    if (lg != 0) continue;
+    const double Ai = a.area[i], Aj = a.area[j];
+    const double s4 = Ai * Aj * nat::kInv4Pi;
+    store_entry<R>(a.A, (size_t)r * a.lda + j, (R)(-v[2] * s4), (R)(-v[3] * s4));
+    const double dVr = (v[0] - v[4]) * s4, dVi = (v[1] - v[5]) * s4;
     for (int q = 0; q < a.n_rhs; ++q) {
       const double2 gv = a.g[(size_t)q * n + j];
       a.corr[(size_t)e * a.n_rhs + q] = make_double2(-(dVr * gv.x - dVi * gv.y), -(dVr * gv.y + dVi * gv.x));
@@ -1479,7 +1620,10 @@ struct AsmWs {
   double2* bpart;
   double2* corr;
   double2* corr_self;
-  double* ss;      // Galerkin: Sauter-Schwab points [P][5]
+  float4* ssx;     // Galerkin: Sauter-Schwab points (x1, x2, y1, y2) fp32 / fp64, weights
+  double4* ssx64;
+  double* ssw;
+  float* ssw32;
 };
 
 size_t carve(nat::Carver& c, AsmWs& w, int64_t n, int64_t rows, int64_t nnz, int n_rhs, int nfar,
@@ -1501,7 +1645,11 @@ size_t carve(nat::Carver& c, AsmWs& w, int64_t n, int64_t rows, int64_t nnz, int
   w.bpart = c.take<double2>((size_t)n_colblk * (n_rhs > 0 ? n_rhs : 1) * rows);
   w.corr = c.take<double2>((size_t)(nnz > 0 ? nnz : 1) * (n_rhs > 0 ? n_rhs : 1));
   w.corr_self = c.take<double2>((size_t)rows * (n_rhs > 0 ? n_rhs : 1));
-  w.ss = c.take<double>((size_t)kSSRegions * kSSMaxOrder * kSSMaxOrder * kSSMaxOrder * kSSMaxOrder * 5);
+  const size_t ssn = (size_t)kSSRegions * kSSMaxOrder * kSSMaxOrder * kSSMaxOrder * kSSMaxOrder;
+  w.ssx = c.take<float4>(ssn);
+  w.ssx64 = c.take<double4>(ssn);
+  w.ssw = c.take<double>(ssn);
+  w.ssw32 = c.take<float>(ssn);
   return c.bytes();
 }
 
@@ -1583,7 +1731,11 @@ nat_status assemble_impl(const nat_mesh* mesh, const nat_geom* geom, const Opts&
     ga.rule_far = w.rule_far;
     ga.rule_N = w.rule_N;
     ga.nN = (int)pN.size();
-    ga.ss = w.ss;
+    ga.rule_Nf = w.rule_Nf;
+    ga.ssx = w.ssx;
+    ga.ssx64 = w.ssx64;
+    ga.ssw = w.ssw;
+    ga.ssw32 = w.ssw32;
     ga.tab = *ss_tab;
     ga.k = (R)k;
     ga.n_rhs = n_rhs;
@@ -1605,7 +1757,9 @@ nat_status assemble_impl(const nat_mesh* mesh, const nat_geom* geom, const Opts&
       ga.items = w.listN;
       ga.nitems = w.cntN + rows;
       ga.cls_S = false;
-      gal_near_kernel<R, NQ><<<gw, 256, 0, s>>>(ga);
+      const unsigned gn = (unsigned)std::min<int64_t>((int64_t)nat::device_sm_count() * 16,
+                                                      (nnz + 256 / kGN - 1) / (256 / kGN));
+      gal_near_n_kernel<R, NQ><<<gn, 256, 0, s>>>(ga);
       NAT_LAUNCH_CHECK();
     }
     gal_self_kernel<R, NQ><<<(unsigned)((rows + 7) / 8), 256, 0, s>>>(ga);
@@ -1791,8 +1945,23 @@ nat_status assemble_entry(const nat_mesh* mesh, const nat_geom* geom, const nat_
   if (o.gal) {
     std::vector<double> ssv;
     ss_build(o.ss, ssv, tab);
-    // pageable source: staged before the call returns
-    NAT_CUDA_TRY(cudaMemcpyAsync(w.ss, ssv.data(), ssv.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+    const size_t np = ssv.size() / 5;
+    std::vector<float4> xf(np);
+    std::vector<double4> xd(np);
+    std::vector<double> wv(np);
+    std::vector<float> wf(np);
+    for (size_t q = 0; q < np; ++q) {
+      const double* e = &ssv[5 * q];
+      xf[q] = make_float4((float)e[0], (float)e[1], (float)e[2], (float)e[3]);
+      xd[q] = make_double4(e[0], e[1], e[2], e[3]);
+      wv[q] = e[4];
+      wf[q] = (float)e[4];
+    }
+    // pageable sources: staged before the call returns
+    NAT_CUDA_TRY(cudaMemcpyAsync(w.ssx, xf.data(), np * sizeof(float4), cudaMemcpyHostToDevice, s));
+    NAT_CUDA_TRY(cudaMemcpyAsync(w.ssx64, xd.data(), np * sizeof(double4), cudaMemcpyHostToDevice, s));
+    NAT_CUDA_TRY(cudaMemcpyAsync(w.ssw, wv.data(), np * sizeof(double), cudaMemcpyHostToDevice, s));
+    NAT_CUDA_TRY(cudaMemcpyAsync(w.ssw32, wf.data(), np * sizeof(float), cudaMemcpyHostToDevice, s));
   }
   const double2* gg = (const double2*)g;
   double2* bb = (double2*)rhs;

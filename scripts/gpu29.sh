@@ -1,0 +1,11 @@
+# Galerkin measurements at C2 + ncu of its kernels
+python -m paper_2506_06190_b200.build > /dev/null || exit 1
+timeout 600 python scripts/bench_configs.py GAL_C2 BM_C2 > gpurun_out/configs_gal.json 2> gpurun_out/configs_gal.err; echo "cfg rc=$?"
+cat gpurun_out/configs_gal.json
+python scripts/prof_gal.py > /dev/null 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:"far_kernel|gal_" -c 4 \
+    -o /tmp/prof_gal python scripts/prof_gal.py > gpurun_out/ncu_gal.log 2>&1
+echo "ncu rc=$?"
+python scripts/summarize_ncu.py /tmp/prof_gal.ncu-rep > gpurun_out/prof_gal_summary.md
+python scripts/stalls.py /tmp/prof_gal.ncu-rep > gpurun_out/prof_gal_stalls.txt
+cat gpurun_out/prof_gal_summary.md gpurun_out/prof_gal_stalls.txt
