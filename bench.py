@@ -520,6 +520,14 @@ def main():
     # per-kernel rooflines and phase times come from the same steps with the two chains
     # serialised (overlapped kernels share the SMs, so their spans would not be per-kernel)
     ms_seq, totals_seq, phases = timed(False) if args.overlap else (ms, totals, step.phase_ms())
+    # per-kernel device time: CUDA events on the launching stream around each main kernel
+    # (libnat's kernel timer), K more serialised steps so the passes above stay unperturbed
+    nat.nat_kernel_timer_enable(True)
+    timed(False)
+    ktimes = {name: nat.nat_kernel_timer_read(cat) for name, cat in
+              (("mc_op", nat.KTIMER_MC_OP), ("mc_rhs", nat.KTIMER_MC_RHS), ("radiate", nat.KTIMER_RADIATE),
+               ("far", nat.KTIMER_FAR))}
+    nat.nat_kernel_timer_enable(False)
     ms_t = torch.tensor([ms], dtype=torch.float64, device="cuda")
     pairs_t = torch.tensor([float(pairs_of(totals)), float(totals["rad"])], dtype=torch.float64, device="cuda")
     if world > 1:
@@ -601,8 +609,24 @@ def main():
                  "traffic": traffic.get("gemv_c64_kernel"), "traffic_kernel": "gemv_c64_kernel",
                  "peak_note": "measured HBM copy bandwidth, MEASURED_PEAKS.json"},
     }
-    # dominant kernel by device time (the MC solve phase itself is not one kernel)
-    share = {"radiate": t_rad, "bem_assembly": t_asm, "mc_operator": totals_seq["mc_op_s"], "gemv": t_gemv}
+    # single kernels, timed per launch with CUDA events on their stream (libnat kernel timer)
+    kt_names = {"mc_op": ("radiate_f32x2_kernel<R,MB,1,NT> (a10 MC operator main kernel)",
+                          "radiate_f32x2_kernel<2, 3, 1, 256>"),
+                "radiate": ("radiate_f32x2_kernel<R,MB,0,NT> (a11 radiation main kernel)",
+                            "radiate_f32x2_kernel<2, 3, 0, 256>"),
+                "far": ("far_kernel_x2<3,1> (a4 far assembly + fused RHS, 8 B store per entry)", "far_kernel_x2<3, 1>"),
+                "mc_rhs": ("radiate_f32x2_kernel<R,MB,2,NT> (a9 MC right-hand side main kernel)",
+                           "radiate_f32x2_kernel<2, 3, 2, 256>")}
+    for key, (name, tkey) in kt_names.items():
+        sec, pairs_k, nl = ktimes[key]
+        if nl:
+            r = alu(name, pairs_k, sec, tkey)
+            r["launches_per_step"] = nl / args.steps
+            r["ms_per_step"] = 1e3 * sec / args.steps
+            roof[key + "_kernel"] = r
+    # dominant KERNEL by device time per step (single kernels; the GEMV is one kernel per call)
+    share = {k + "_kernel": ktimes[k][0] for k in kt_names if ktimes[k][2]}
+    share["gemv"] = t_gemv
     dom = max(share, key=share.get)
     roofline = dict(roof[dom])
     roofline["share_of_step"] = share[dom] / (ms_seq * 1e-3)

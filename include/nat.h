@@ -55,6 +55,17 @@ typedef enum {
 int nat_abi_version(void);
 const char* nat_last_error(void);
 
+/* Diagnostics (bench.py's roofline pass): CUDA events on the launching stream around the
+ * main kernel of each category — 0: MC operator (a10), 1: MC right-hand side (a9),
+ * 2: radiation (a11), 3: far assembly (a4).  Off by default (no events, no overhead).
+ * nat_kernel_timer_enable resets the totals and switches the timer on/off;
+ * nat_kernel_timer_read synchronises the recorded events and returns, for one category,
+ * the summed kernel time, the algorithmic pair-evaluations of those launches and their
+ * count (launches that returned at once because GMRES had already converged are not
+ * counted).  [host] outputs. */
+void nat_kernel_timer_enable(int on);
+nat_status nat_kernel_timer_read(int category, double* seconds, double* pairs, int64_t* launches);
+
 /* ---------------------------------------------------------------------------------
  * a1 — mesh preparation ("construct the scene and obtain its surface triangle
  * mesh"; reading R-geom).  Per triangle t with vertices (v1, v2, v3):

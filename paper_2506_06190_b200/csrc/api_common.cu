@@ -1,4 +1,7 @@
 // Error handling and small shared utilities of libnat.
+#include <mutex>
+#include <vector>
+
 #include "nat_internal.cuh"
 
 namespace nat {
@@ -41,7 +44,123 @@ int device_sm_count() {
   return n;
 }
 
+// ------------------------------------------------------------------------------------
+// Kernel timer (diagnostics, off by default): CUDA events on the launching stream around
+// the main kernel of each category; the skip word (GMRES iterations enqueued after
+// convergence) is copied next to the events so skipped launches are not counted.
+// ------------------------------------------------------------------------------------
+namespace {
+struct TimerEntry {
+  cudaEvent_t e0, e1;
+  int cat;
+  double pairs;
+  int slot;  // pinned skip-word slot or -1
+};
+struct KTimer {
+  std::mutex mu;
+  bool on = false;
+  std::vector<TimerEntry> live;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pool;
+  unsigned long long* slots = nullptr;  // pinned host
+  int n_slots = 0, used_slots = 0;
+  double sec[kTimerCats] = {}, pairs[kTimerCats] = {};
+  long long launches[kTimerCats] = {};
+};
+KTimer& timer() {
+  static KTimer t;
+  return t;
+}
+thread_local TimerEntry t_open{nullptr, nullptr, -1, 0.0, -1};
+
+// sums the recorded entries (synchronising their events) into the totals
+void drain(KTimer& t) {
+  for (auto& e : t.live) {
+    if (cudaEventSynchronize(e.e1) != cudaSuccess) {
+      cudaGetLastError();
+      continue;
+    }
+    const bool skipped = e.slot >= 0 && t.slots[e.slot] == 0ull;
+    float ms = 0.f;
+    if (!skipped && cudaEventElapsedTime(&ms, e.e0, e.e1) == cudaSuccess) {
+      t.sec[e.cat] += 1e-3 * ms;
+      t.pairs[e.cat] += e.pairs;
+      t.launches[e.cat] += 1;
+    }
+    cudaGetLastError();
+    t.pool.push_back({e.e0, e.e1});
+  }
+  t.live.clear();
+  t.used_slots = 0;
+}
+}  // namespace
+
+bool ktimer_on() { return timer().on; }
+
+void ktimer_begin(int cat, cudaStream_t s) {
+  KTimer& t = timer();
+  std::lock_guard<std::mutex> lk(t.mu);
+  if (!t.on) return;
+  std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
+  if (!t.pool.empty()) {
+    ev = t.pool.back();
+    t.pool.pop_back();
+  } else if (cudaEventCreate(&ev.first) != cudaSuccess || cudaEventCreate(&ev.second) != cudaSuccess) {
+    cudaGetLastError();
+    return;
+  }
+  cudaEventRecord(ev.first, s);
+  t_open = TimerEntry{ev.first, ev.second, cat, 0.0, -1};
+}
+
+void ktimer_end(int cat, cudaStream_t s, double pairs, const unsigned long long* skip) {
+  KTimer& t = timer();
+  std::lock_guard<std::mutex> lk(t.mu);
+  if (!t.on || t_open.cat != cat || !t_open.e0) return;
+  TimerEntry e = t_open;
+  t_open = TimerEntry{nullptr, nullptr, -1, 0.0, -1};
+  cudaEventRecord(e.e1, s);
+  e.pairs = pairs;
+  if (skip) {
+    if (t.used_slots >= t.n_slots) drain(t);  // (rare) recycle the slots
+    e.slot = t.used_slots++;
+    cudaMemcpyAsync(&t.slots[e.slot], skip, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s);
+  }
+  t.live.push_back(e);
+}
+
 }  // namespace nat
+
+extern "C" void nat_kernel_timer_enable(int on) {
+  nat::KTimer& t = nat::timer();
+  std::lock_guard<std::mutex> lk(t.mu);
+  nat::drain(t);
+  for (int c = 0; c < nat::kTimerCats; ++c) {
+    t.sec[c] = t.pairs[c] = 0.0;
+    t.launches[c] = 0;
+  }
+  if (on && !t.slots) {
+    t.n_slots = 4096;
+    if (cudaHostAlloc(&t.slots, sizeof(unsigned long long) * t.n_slots, cudaHostAllocDefault) != cudaSuccess) {
+      cudaGetLastError();
+      t.slots = nullptr;
+      t.n_slots = 0;
+      return;
+    }
+  }
+  t.on = on != 0;
+}
+
+extern "C" nat_status nat_kernel_timer_read(int category, double* seconds, double* pairs, int64_t* launches) {
+  NAT_REQUIRE(category >= 0 && category < nat::kTimerCats, "category %d out of range", category);
+  NAT_REQUIRE(seconds && pairs && launches, "outputs must be non-null host pointers");
+  nat::KTimer& t = nat::timer();
+  std::lock_guard<std::mutex> lk(t.mu);
+  nat::drain(t);
+  *seconds = t.sec[category];
+  *pairs = t.pairs[category];
+  *launches = t.launches[category];
+  return NAT_OK;
+}
 
 extern "C" int nat_abi_version(void) { return NAT_ABI_VERSION; }
 

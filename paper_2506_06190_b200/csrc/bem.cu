@@ -1702,6 +1702,8 @@ nat_status assemble_impl(const nat_mesh* mesh, const nat_geom* geom, const Opts&
   fa.rule = w.rule_far;
   const int64_t n_colblk = (n + kThreads * kCC - 1) / (kThreads * kCC);
   dim3 grid((unsigned)n_colblk, (unsigned)((rows + kTI - 1) / kTI));
+  const bool timed = nat::ktimer_on() && !mf.delta;
+  if (timed) nat::ktimer_begin(nat::kTimerFar, s);
   if (n_rhs == 0) {
     fa.store_A = true;
     if (!mf.delta) launch_far<R, NQ, 0>(grid, fa, o.bm, o.gal, s);
@@ -1716,6 +1718,8 @@ nat_status assemble_impl(const nat_mesh* mesh, const nat_geom* geom, const Opts&
     }
   }
   NAT_LAUNCH_CHECK();
+  if (timed)  // far rule on every pair of the row block (test points x trial points)
+    nat::ktimer_end(nat::kTimerFar, s, (double)rows * (double)n * NQ * (o.gal ? NQ : 1), nullptr);
   if (o.gal) {  // NEXT-2: Galerkin near / self integrals (warp per pair)
     GalArgs<R> ga{};
     ga.n = n;

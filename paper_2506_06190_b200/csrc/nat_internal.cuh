@@ -38,6 +38,14 @@ struct Carver {
 
 int device_sm_count();
 
+// Kernel timer (nat_kernel_timer_*, diagnostics): events around the main kernel of a
+// category on the launching stream; `pairs` = algorithmic pair-evaluations of the launch;
+// `skip` (optional device word) marks launches that returned at once (not counted).
+enum { kTimerMcOp = 0, kTimerMcRhs = 1, kTimerRadiate = 2, kTimerFar = 3, kTimerCats = 4 };
+bool ktimer_on();
+void ktimer_begin(int cat, cudaStream_t s);
+void ktimer_end(int cat, cudaStream_t s, double pairs, const unsigned long long* skip);
+
 // Exclusive scan of one int64 per thread over a 1024-thread block (warp shuffles, exact);
 // sh: 33 int64 of shared memory; *total (optional) receives the block sum.
 __device__ __forceinline__ int64_t block_exscan_1024(int64_t v, int64_t* sh, int64_t* total) {

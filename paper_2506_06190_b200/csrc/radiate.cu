@@ -755,6 +755,9 @@ nat_status radiate_internal(const RadInput& in, nat_prec prec, const double* k, 
     prm.self_r2 = in.self_r2;
     prm.skip = in.skip;
     cudaError_t e = cudaSuccess;
+    const int tcat = kind == 0 ? kTimerRadiate : kind == 1 ? kTimerMcOp : kTimerMcRhs;
+    const bool timed = ktimer_on();
+    if (timed) ktimer_begin(tcat, s);
     if (pl.fp64) {
       auto kern = radiate_f64_kernel<2>;
       e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
@@ -768,6 +771,8 @@ nat_status radiate_internal(const RadInput& in, nat_prec prec, const double* k, 
                                                    : launch_f32_mb<2>(pl, prm, s);
     }
     if (e != cudaSuccess) return fail(NAT_ERR_CUDA, "radiate launch: %s", cudaGetErrorString(e));
+    if (timed)  // algorithmic pairs: the self kinds skip the diagonal
+      ktimer_end(tcat, s, (double)nm * (double)n_lis * (double)(self ? in.n_src - 1 : in.n_src), in.skip);
     if (keep) {  // the caller reduces the partials in its own epilogue
       keep->part = pl.n_split > 1 ? part : dst;
       keep->n_split = pl.n_split;

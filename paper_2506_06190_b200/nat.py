@@ -96,6 +96,8 @@ _SIGS = {
     "nat_bem_mf_solve_workspace": (_SZ, [C.POINTER(_BemMf), C.c_int, C.c_int]),
     "nat_bem_mf_solve": (C.c_int, [_P, C.POINTER(_BemMf), _P, _P, _D, C.c_int, _P, _SZ, C.POINTER(_SolveInfo),
                                    _P]),
+    "nat_kernel_timer_enable": (None, [C.c_int]),
+    "nat_kernel_timer_read": (C.c_int, [C.c_int, C.POINTER(_D), C.POINTER(_D), C.POINTER(_I64)]),
     "nat_comm_unique_id": (C.c_int, [_P]),
     "nat_comm_create_from_id": (C.c_int, [C.POINTER(_P), _P, C.c_int, C.c_int]),
     "nat_comm_destroy": (C.c_int, [_P]),
@@ -676,3 +678,20 @@ def nat_bem_mf_solve(op: BemMf, b_local: torch.Tensor, comm: Optional["Comm"] = 
     _check(st, allow_warn=True)
     return x, dict(iters=info.iters, converged=info.converged, rel_residual=info.rel_residual,
                    t_total_s=info.t_total_s, t_matvec_s=info.t_matvec_s, t_comm_s=info.t_comm_s)
+
+
+# ------------------------------------------------------------------------------------
+# diagnostics: per-kernel CUDA-event timer (nat_kernel_timer_*)
+# ------------------------------------------------------------------------------------
+KTIMER_MC_OP, KTIMER_MC_RHS, KTIMER_RADIATE, KTIMER_FAR = 0, 1, 2, 3
+
+
+def nat_kernel_timer_enable(on: bool = True):
+    lib().nat_kernel_timer_enable(int(bool(on)))
+
+
+def nat_kernel_timer_read(category: int):
+    """(seconds, pair-evaluations, launches) of the category's main kernel since enable."""
+    sec, pairs, n = C.c_double(0.0), C.c_double(0.0), C.c_int64(0)
+    _check(lib().nat_kernel_timer_read(int(category), C.byref(sec), C.byref(pairs), C.byref(n)))
+    return sec.value, pairs.value, n.value
