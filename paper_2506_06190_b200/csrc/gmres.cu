@@ -23,7 +23,7 @@ namespace {
 
 constexpr int kT = 256;
 constexpr int kRing = 4;  // pinned mask slots / events in flight
-constexpr int kKU = 8;    // basis vectors loaded together by the update / combine kernels
+constexpr int kKU = 16;   // basis vectors loaded together by the update / combine kernels
 
 __device__ __forceinline__ bool sys_on(uint64_t active, const unsigned long long* dmask, int s) {
   uint64_t a = active;
@@ -73,6 +73,33 @@ __device__ __forceinline__ double2 warp_sum_partials(const double2* p, int cnt) 
 __device__ void finish_sums(const double2* __restrict__ part, int s, int nvec, int nchunk, int mp1, int mp2,
                             int mode, int slot, double2* __restrict__ h, double2* __restrict__ h2) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if (nchunk <= 32) {
+    // one thread per vector, partials summed in chunk order with all loads in flight: a
+    // single L2 round trip instead of one per group of 8 vectors (ncu r01: tail of dots)
+    for (int k = threadIdx.x; k < nvec; k += blockDim.x) {
+      const double2* pk = part + ((size_t)s * mp1 + k) * nchunk;
+      double2 v[32];
+#pragma unroll
+      for (int c = 0; c < 32; ++c) v[c] = c < nchunk ? __ldcg(&pk[c]) : make_double2(0.0, 0.0);
+      double2 t = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int c = 0; c < 32; ++c) {
+        t.x += v[c].x;
+        t.y += v[c].y;
+      }
+      if (mode == 0) {
+        h[(size_t)s * mp2 + k] = t;
+        h2[(size_t)s * mp2 + k] = t;
+      } else if (mode == 1) {
+        h2[(size_t)s * mp2 + k] = t;
+        const double2 o = h[(size_t)s * mp2 + k];
+        h[(size_t)s * mp2 + k] = make_double2(o.x + t.x, o.y + t.y);
+      } else {
+        h[(size_t)s * mp2 + slot] = make_double2(sqrt(t.x), 0.0);
+      }
+    }
+    return;
+  }
   for (int k = warp; k < nvec; k += nw) {
     const double2 t = warp_sum_partials(part + ((size_t)s * mp1 + k) * nchunk, nchunk);
     if (lane != 0) continue;
