@@ -597,7 +597,7 @@ def main():
         "radiate": alu("nat_radiate_field (stage + radiate_f32x2_kernel + split reduce)", totals_seq["rad"], t_rad,
                        "radiate_f32x2_kernel<2, 3, 0, 256>"),
         "bem_assembly": alu("nat_bem_assemble (far_kernel_x2 + near/self kernels)",
-                            totals_seq["far"] + totals_seq["near"] + totals_seq["self"], t_asm, "far_kernel_x2<3, 1>"),
+                            totals_seq["far"] + totals_seq["near"] + totals_seq["self"], t_asm, "far_kernel_x2<3, 1, 0, 1>"),
         "mc_solve": alu("MC solve phase (a8-a10: samples, close pairs, RHS, operator, GMRES)",
                         totals_seq["mc_op"] + totals_seq["mc_rhs"], t_mc, None),
         "mc_operator": alu("MC operator application (stage + radiate_f32x2_kernel<R,MB,1,NT> + mc_finish_kernel)",
@@ -614,7 +614,7 @@ def main():
                           "radiate_f32x2_kernel<2, 3, 1, 256>"),
                 "radiate": ("radiate_f32x2_kernel<R,MB,0,NT> (a11 radiation main kernel)",
                             "radiate_f32x2_kernel<2, 3, 0, 256>"),
-                "far": ("far_kernel_x2<3,1> (a4 far assembly + fused RHS, 8 B store per entry)", "far_kernel_x2<3, 1>"),
+                "far": ("far_kernel_x2<3,1> (a4 far assembly + fused RHS, 8 B store per entry)", "far_kernel_x2<3, 1, 0, 1>"),
                 "mc_rhs": ("radiate_f32x2_kernel<R,MB,2,NT> (a9 MC right-hand side main kernel)",
                            "radiate_f32x2_kernel<2, 3, 2, 256>")}
     for key, (name, tkey) in kt_names.items():

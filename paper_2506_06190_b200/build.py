@@ -46,6 +46,7 @@ def build(verbose=False, clean=False):
     objs = []
     flags = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
              "--expt-relaxed-constexpr", "-I", inc] + ARCH
+    flags += os.environ.get("NAT_NVCC_EXTRA", "").split()   # tuning experiments only (-D...)
     for s in srcs:
         o = os.path.join(BUILD, os.path.basename(s)[:-3] + ".o")
         objs.append(o)

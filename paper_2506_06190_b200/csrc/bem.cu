@@ -36,6 +36,10 @@ using nat::C2;
 
 constexpr int kThreads = 256;
 constexpr int kTI = 16;       // rows per far CTA
+#ifndef NAT_FAR_UNROLL
+#define NAT_FAR_UNROLL 1       // column passes interleaved by the packed far kernel (tuning)
+#endif
+constexpr int kFarUnroll = NAT_FAR_UNROLL;
 constexpr int kTI64 = 4;      // rows per CTA of the fp64 far kernel (16 unrolled fp64 rows -> 238
                               // registers, 8 warps/SM; ncu r01 matrix-free C5 capture)
 constexpr int kCC = 8;        // column passes per far CTA (columns = 256 * kCC)
@@ -477,6 +481,7 @@ __global__ void __launch_bounds__(kThreads, 2) far_kernel_x2(FarArgs<float> a) {
   // column form one straight-line block the scheduler can interleave
   auto columns = [&](auto full_tag) {
     constexpr bool FULL = decltype(full_tag)::value;
+#pragma unroll kFarUnroll
     for (int cc = 0; cc < kCC; ++cc) {
       const int64_t j = (int64_t)blockIdx.x * (kThreads * kCC) + cc * kThreads + tid;
       const bool valid = j < n;
