@@ -156,12 +156,16 @@ class Step:
         self.g_mc = self.g.expand(len(self.mc_idx), -1).contiguous() if self.mc_idx else None
         rows = self.r1 - self.r0
         self.lda = self.n + (self.n & 1)
+        # dense-chain order: "interleave" (assembly + solve per wavenumber: one matrix, one
+        # workspace) or "asm_first" (all assemblies, then the solves: one matrix per ka);
         # the three ka run one after the other in the dense-BEM chain (one NCCL communicator,
-        # collectives issued in the same order on every rank): one matrix, one workspace
-        A = torch.empty(rows, self.lda, dtype=torch.complex64, device=dev)
-        ws = nat._ws(nat.lib().nat_bem_solve_workspace(nat.NAT_FP32, self.n, rows, 200), dev)
-        self.A = [A] * len(KAS)
-        self.solve_ws = [ws] * len(KAS)
+        # collectives issued in the same order on every rank).  NAT_BENCH_ORDER overrides.
+        self.order = os.environ.get("NAT_BENCH_ORDER", "interleave")
+        n_mat = len(KAS) if self.order == "asm_first" else 1
+        mats = [torch.empty(rows, self.lda, dtype=torch.complex64, device=dev) for _ in range(n_mat)]
+        wss = [nat._ws(nat.lib().nat_bem_solve_workspace(nat.NAT_FP32, self.n, rows, 200), dev) for _ in range(n_mat)]
+        self.A = [mats[q % n_mat] for q in range(len(KAS))]
+        self.solve_ws = [wss[q % n_mat] for q in range(len(KAS))]
         self.S_bem = 3 * self.n
         self.n_lis = self.l1 - self.l0
         # BEM radiation groups: the solutions of each group of wavenumbers radiate in one
@@ -172,6 +176,8 @@ class Step:
                              for g in self.rad_groups}
         self.out_bem = torch.empty(len(KAS), self.n_lis, dtype=torch.complex128, device=dev)
         self.x_bem = torch.empty(len(KAS), self.n, dtype=torch.complex128, device=dev)
+        self.b_bem = torch.empty(len(KAS), 1, self.r1 - self.r0, dtype=torch.complex128, device=dev)
+
         self.g3 = self.g.expand(len(KAS), -1).contiguous()
         if self.mc_idx:
             self.mc_plan = nat.McPlan(M_MC, len(self.mc_idx), "fp32", 200, dev)
@@ -229,12 +235,34 @@ class Step:
         if not hasattr(self, "nS"):   # class counts for the pair accounting (first step only)
             self.nS = int((near.cls == 1).sum().item())
 
+        asm_done = threading.Event()   # host-side: the dense chain has enqueued its assemblies
+        asm_ev = torch.cuda.Event()
+
         def bem_all(side=None):
+            if self.order == "asm_first":
+                # all assemblies first (FP32/MUFU-bound), then the HBM-bound GMRES solves,
+                # which the MC chain's FP32/MUFU-bound operators overlap
+                for q in range(len(KAS)):
+                    self._bem_one(q, geo, near, counts, solve=False)
+                asm_ev.record(torch.cuda.current_stream())
+                asm_done.set()
+                for q in range(len(KAS)):
+                    self._bem_one(q, geo, near, counts, assemble=False)
+                    for grp in self.rad_groups:
+                        if grp[-1] == q:
+                            self._bem_radiate(geo, lis, grp, side)
+                return
             for q in range(len(KAS)):
                 self._bem_one(q, geo, near, counts)
                 for grp in self.rad_groups:
                     if grp[-1] == q:
                         self._bem_radiate(geo, lis, grp, side)
+
+        def mc_after_asm(*a):
+            if self.order == "asm_first":
+                asm_done.wait()
+                torch.cuda.current_stream().wait_event(asm_ev)
+            self._mc_chain(*a)
 
         if not overlap:
             bem_all()
@@ -256,7 +284,7 @@ class Step:
 
             ths = [threading.Thread(target=worker, args=(self.s_bem, bem_all, self.s_rad))]
             if self.mc_idx:
-                ths.append(threading.Thread(target=worker, args=(self.s_mc, self._mc_chain, geo, lis, counts)))
+                ths.append(threading.Thread(target=worker, args=(self.s_mc, mc_after_asm, geo, lis, counts)))
             for t in ths:
                 t.start()
             for t in ths:
@@ -273,23 +301,29 @@ class Step:
                 hm[: self.out_mc.shape[0]].copy_(self.out_mc, non_blocking=True)
         return counts
 
-    def _bem_one(self, q, geo, near, counts):
+    def _bem_one(self, q, geo, near, counts, assemble=True, solve=True):
         """a4-a7 for KAS[q] (row-sharded across ranks)."""
         nat = self.nat
         mesh, g = self.mesh, self.g
         nS, nN = self.nS, near.nnz - self.nS
         rows = self.r1 - self.r0
         tag = str(q)
-        self._ev("asm0", tag)
-        A, b = nat.nat_bem_assemble(mesh, geo, near, KAS[q], g, prec="fp32", A=self.A[q], lda=self.lda)  # a4+a5
-        self._ev("asm1", tag)
-        _, info = nat.nat_bem_solve(A, b[0], self.n, self.r0, self.comm, tol=1e-6, max_iter=200,
+        if assemble:
+            self._ev("asm0", tag)
+            A, b = nat.nat_bem_assemble(mesh, geo, near, KAS[q], g, prec="fp32", A=self.A[q], lda=self.lda,
+                                        rhs=self.b_bem[q])                                          # a4+a5
+            self._ev("asm1", tag)
+            with self.lock:
+                counts["far"] += rows * self.n * 3
+                counts["near"] += nS * 448 + nN * 28
+                counts["self"] += rows * 48
+        if not solve:
+            return
+        self._ev("solve0", tag)
+        _, info = nat.nat_bem_solve(self.A[q], self.b_bem[q][0], self.n, self.r0, self.comm, tol=1e-6, max_iter=200,
                                     ws=self.solve_ws[q], out=self.x_bem[q])                       # a6+a7
         self._ev("solve1", tag)
         with self.lock:
-            counts["far"] += rows * self.n * 3
-            counts["near"] += nS * 448 + nN * 28
-            counts["self"] += rows * 48
             counts["rad"] += self.S_bem * self.n_lis
             counts["gemv_bytes"] += info["iters"] * rows * self.lda * 8
             counts["gemv_s"] += info["t_matvec_s"]
@@ -345,7 +379,7 @@ class Step:
             return sum(x.elapsed_time(y) for t in ea for x, y in zip(ea[t], eb.get(t, [])))
         return {"geometry": span("geom0", "geom1"), "near_list": span("near0", "near1"),
                 "assembly": span("asm0", "asm1"),
-                "bem_solve": span("asm1", "solve1"), "radiate_bem": span("rad0", "rad1"),
+                "bem_solve": span("solve0", "solve1"), "radiate_bem": span("rad0", "rad1"),
                 "mc_solve": span("mc0", "mc1"), "radiate_mc": span("radmc0", "radmc1")}
 
 

@@ -384,7 +384,8 @@ def nat_bem_near_list(mesh: Mesh, geom: Geom, row_begin=0, row_end=None, opts=No
 
 
 def nat_bem_assemble(mesh: Mesh, geom: Geom, near: NearList, k: float, g=None, prec="fp32",
-                     opts=None, A: Optional[torch.Tensor] = None, lda: Optional[int] = None):
+                     opts=None, A: Optional[torch.Tensor] = None, lda: Optional[int] = None,
+                     rhs: Optional[torch.Tensor] = None):
     """Rows [near.row_begin, near.row_end) of A (c64 for fp32, c128 for fp64) and
     rhs = -V g (c128 [n_rhs][rows]).  Returns (A, rhs)."""
     pr = _prec(prec)
@@ -396,11 +397,13 @@ def nat_bem_assemble(mesh: Mesh, geom: Geom, near: NearList, k: float, g=None, p
     if A is None:
         A = torch.empty(rows, lda, dtype=cdt, device=dev)
     n_rhs = 0
-    rhs = None
-    if g is not None:
+    if g is None:
+        rhs = None
+    else:
         g = torch.atleast_2d(g).to(torch.complex128).contiguous()
         n_rhs = g.shape[0]
-        rhs = torch.empty(n_rhs, rows, dtype=torch.complex128, device=dev)
+        if rhs is None:
+            rhs = torch.empty(n_rhs, rows, dtype=torch.complex128, device=dev)
     o = opts or quad_opts()
     ws = _ws(lib().nat_bem_assemble_workspace(n, rows, near.nnz, n_rhs), dev)
     _check(lib().nat_bem_assemble(C.byref(mesh.c()), C.byref(geom.c()), C.byref(o), _ptr(near.row_ptr),
