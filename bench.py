@@ -672,6 +672,9 @@ def main():
                "seconds": t}
     K = args.steps
     per_step_launch = n_nat
+    bsm_meas = (phases["assembly"] + phases["bem_solve"]) * 1e-3 / (K * len(KAS))
+    bsm_roof = ((totals_seq["far"] + totals_seq["near"] + totals_seq["self"]) / R_PIPE
+                + totals_seq["gemv_bytes"] / (hbm * 1e9)) / (K * len(KAS))
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
         "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
@@ -681,6 +684,16 @@ def main():
         "listener_pts_per_s": (K * step.P * (len(KAS) + len(KAS))) / (ms_max * 1e-3) if world == 1 else None,
         "radiate_listener_pts_per_s": (step.n_lis * (len(KAS) + len(step.mc_idx)) * K) / t_rad if t_rad > 0 else None,
         "pairs_per_step": pairs_all / K,
+        # BEM solve seconds per mode against its roofline
+        # (a4 + a5 evaluations / R_pipe + the GEMV bytes of its iterations / HBM copy bandwidth)
+        "bem_s_per_mode": {
+            "measured": bsm_meas, "roofline": bsm_roof, "frac": bsm_roof / bsm_meas if bsm_meas > 0 else None,
+            "note": "per wavenumber: assembly + GMRES (serialised pass); roofline = pair-evals / R_pipe + "
+                    "matrix bytes streamed / measured HBM copy bandwidth"},
+        # radiation listener points (x wavenumbers, BEM 61,440 + MC 10,000 sources) per second
+        # at the pair roofline: the same points / (their pair-evaluations / R_pipe)
+        "radiate_listener_pts_roofline_per_s": (step.n_lis * (len(KAS) + len(step.mc_idx)) * K) * R_PIPE
+                                               / totals_seq["rad"] if totals_seq["rad"] else None,
         "phase_ms_per_step": {k: v / K for k, v in phases.items()},
         "phase_note": ("phases and rooflines from K more steps with the two chains serialised "
                        f"({ms_seq / K:.3f} ms/step); value/ms_per_step from the overlapped steps")
