@@ -168,7 +168,13 @@ typedef struct nat_comm nat_comm;
 nat_status nat_comm_unique_id(uint8_t* id /* [host] 128 B */);
 nat_status nat_comm_create_from_id(nat_comm** comm, const uint8_t* id /* [host] 128 B */, int rank,
                                    int world);
-nat_status nat_comm_destroy(nat_comm* comm);
+/* Wraps a caller-owned ncclComm_t (void* to keep NCCL out of this header; e.g. the
+ * communicator of torch.distributed's NCCL backend): its rank / size must equal
+ * rank / world (checked, NAT_ERR_INVALID_ARG otherwise); NULL with world == 1 is a
+ * single-rank communicator.  nat_comm_destroy never destroys a borrowed ncclComm_t. */
+nat_status nat_comm_create(nat_comm** comm, void* nccl_comm /* borrowed ncclComm_t or NULL */, int rank,
+                           int world);
+nat_status nat_comm_destroy(nat_comm* comm); /* destroys the ncclComm_t only if the library made it */
 
 /* ---------------------------------------------------------------------------------
  * a7 — unrestarted GMRES (tol 1e-6, max 200; reading R-gmres) on the

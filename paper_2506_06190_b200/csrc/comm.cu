@@ -36,9 +36,31 @@ extern "C" nat_status nat_comm_create_from_id(nat_comm** comm, const uint8_t* id
   return NAT_OK;
 }
 
+// Wraps a caller-owned ncclComm_t (e.g. the one torch.distributed's NCCL backend holds);
+// nat_comm_destroy never destroys a borrowed communicator.  NULL => world 1.
+extern "C" nat_status nat_comm_create(nat_comm** comm, void* nccl_comm, int rank, int world) {
+  NAT_REQUIRE(comm, "comm must be non-null");
+  NAT_REQUIRE(world >= 1 && rank >= 0 && rank < world, "bad rank %d / world %d", rank, world);
+  NAT_REQUIRE(nccl_comm || world == 1, "a NULL ncclComm_t needs world == 1");
+  if (nccl_comm) {
+    int n = 0, rk = 0;
+    ncclResult_t r = ncclCommCount((ncclComm_t)nccl_comm, &n);
+    if (r == ncclSuccess) r = ncclCommUserRank((ncclComm_t)nccl_comm, &rk);
+    if (r != ncclSuccess) return nat::fail(NAT_ERR_NCCL, "ncclCommCount/UserRank: %s", ncclGetErrorString(r));
+    NAT_REQUIRE(n == world && rk == rank, "ncclComm_t has rank %d of %d, expected %d of %d", rk, n, rank, world);
+  }
+  nat_comm* c = new nat_comm();
+  c->nccl = (ncclComm_t)nccl_comm;
+  c->rank = rank;
+  c->world = world;
+  c->borrowed = true;
+  *comm = c;
+  return NAT_OK;
+}
+
 extern "C" nat_status nat_comm_destroy(nat_comm* comm) {
   if (!comm) return NAT_OK;
-  ncclResult_t r = ncclCommDestroy(comm->nccl);
+  ncclResult_t r = (comm->borrowed || !comm->nccl) ? ncclSuccess : ncclCommDestroy(comm->nccl);
   delete comm;
   if (r != ncclSuccess) return nat::fail(NAT_ERR_NCCL, "ncclCommDestroy: %s", ncclGetErrorString(r));
   return NAT_OK;

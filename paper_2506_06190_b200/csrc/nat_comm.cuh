@@ -7,6 +7,7 @@
 struct nat_comm {
   ncclComm_t nccl = nullptr;
   int rank = 0, world = 1;
+  bool borrowed = false;  // nat_comm_create: the caller owns the ncclComm_t
 };
 
 namespace nat {

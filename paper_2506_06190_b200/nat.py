@@ -100,6 +100,7 @@ _SIGS = {
     "nat_kernel_timer_read": (C.c_int, [C.c_int, C.POINTER(_D), C.POINTER(_D), C.POINTER(_I64)]),
     "nat_comm_unique_id": (C.c_int, [_P]),
     "nat_comm_create_from_id": (C.c_int, [C.POINTER(_P), _P, C.c_int, C.c_int]),
+    "nat_comm_create": (C.c_int, [C.POINTER(_P), _P, C.c_int, C.c_int]),
     "nat_comm_destroy": (C.c_int, [_P]),
     "nat_bem_solve_workspace": (_SZ, [C.c_int, _I64, _I64, C.c_int]),
     "nat_bem_solve": (C.c_int, [_P, C.c_int, _I64, _I64, _I64, _P, _I64, _P, _P, _D, C.c_int,
@@ -426,11 +427,19 @@ def nat_bem_matvec(A: torch.Tensor, x: torch.Tensor, n: Optional[int] = None, ou
 class Comm:
     """NCCL communicator built from a torch.distributed-broadcast unique id."""
 
-    def __init__(self, rank: int, world: int, uid: bytes):
+    def __init__(self, rank: int, world: int, uid: Optional[bytes] = None, nccl_comm: Optional[int] = None):
         self.rank, self.world = rank, world
         self.handle = C.c_void_p()
+        if uid is None:   # borrow a caller-owned ncclComm_t (or none: world 1)
+            _check(lib().nat_comm_create(C.byref(self.handle), C.c_void_p(nccl_comm), rank, world))
+            return
         buf = (C.c_uint8 * 128).from_buffer_copy(uid)
         _check(lib().nat_comm_create_from_id(C.byref(self.handle), buf, rank, world))
+
+    @classmethod
+    def borrow(cls, nccl_comm: Optional[int], rank: int = 0, world: int = 1):
+        """Wraps an existing ncclComm_t (address as int; None => single rank); never destroyed here."""
+        return cls(rank, world, None, nccl_comm)
 
     @staticmethod
     def unique_id() -> bytes:

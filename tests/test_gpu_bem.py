@@ -194,3 +194,21 @@ def test_c2_launch_configuration(ka):
     p = to_np(nat.nat_radiate_field(src, [ka], lis))[0]
     pe = analytic.oscillating_sphere(soa_to_aos(lis), ka)
     assert rel_l2(p, pe) <= 0.02
+
+
+def test_borrowed_single_rank_communicator_matches_no_communicator():
+    """nat_comm_create with a NULL ncclComm_t (world 1): the row-sharded solve with a
+    borrowed communicator equals the solve without one, bit for bit."""
+    nat = _nat()
+    m = I.icosphere(3)
+    g = I.neumann_rigid_z(m)
+    mesh, gg = _gpu_case(m)
+    nl = nat.nat_bem_near_list(mesh, gg)
+    A, b = nat.nat_bem_assemble(mesh, gg, nl, 2.0, torch.from_numpy(g[None]).cuda(), prec="fp32")
+    x0, i0 = nat.nat_bem_solve(A, b[0], m.n_tri, tol=1e-6)
+    comm = nat.Comm.borrow(None)
+    x1, i1 = nat.nat_bem_solve(A, b[0], m.n_tri, comm=comm, tol=1e-6)
+    comm.close()
+    assert i0["iters"] == i1["iters"] and torch.equal(x0, x1)
+    with pytest.raises(nat.NatError):
+        nat.Comm.borrow(None, 0, 2)     # a NULL ncclComm_t cannot have two ranks
