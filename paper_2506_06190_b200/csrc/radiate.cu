@@ -432,7 +432,7 @@ __global__ void __launch_bounds__(kThreads) radiate_f64_kernel(RadParams prm) {
         const double rho = r2 > 0.0 ? 1.0 / rr : 0.0;  // self pair (MC operators) -> 0
         const double qq = dn * (rho * rho);
         double sn, cs;
-        sincos(k * rr, &sn, &cs);
+        nat::pair_sincos(k * rr, &sn, &cs);
         const double cr = fma(qq, fma(rho, f[6], f[7]), rho * f[10]);
         const double ci = fma(qq, fma(rho, f[9], f[8]), rho * f[11]);
         ar[r] = fma(cs, cr, fma(-sn, ci, ar[r]));
