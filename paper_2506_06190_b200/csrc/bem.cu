@@ -40,6 +40,10 @@ constexpr int kTI = 16;       // rows per far CTA
 #define NAT_FAR_UNROLL 1       // column passes interleaved by the packed far kernel (tuning)
 #endif
 constexpr int kFarUnroll = NAT_FAR_UNROLL;
+#ifndef NAT_FAR_MINB
+#define NAT_FAR_MINB 2         // resident CTAs per SM the packed far kernel is compiled for (tuning)
+#endif
+constexpr int kFarMinBlocks = NAT_FAR_MINB;
 constexpr int kTI64 = 4;      // rows per CTA of the fp64 far kernel (16 unrolled fp64 rows -> 238
                               // registers, 8 warps/SM; ncu r01 matrix-free C5 capture)
 constexpr int kCC = 8;        // column passes per far CTA (columns = 256 * kCC)
@@ -440,7 +444,7 @@ __global__ void __launch_bounds__(kThreads) far_kernel(FarArgs<R> a) {
 // NTQ > 1 (Galerkin, NEXT-2): NTQ test points per row with weights w_t |T_i| (staged in
 // shared memory); the self pair and padding columns are zeroed (Sauter-Schwab self kernel).
 template <int NQ, int NR, bool MV = false, int NTQ = 1>
-__global__ void __launch_bounds__(kThreads, 2) far_kernel_x2(FarArgs<float> a) {
+__global__ void __launch_bounds__(kThreads, kFarMinBlocks) far_kernel_x2(FarArgs<float> a) {
   static_assert(kTI % 2 == 0, "row pairs");
   static_assert(!MV || NR == 1, "matrix-free: one iterate");
   static_assert(NTQ == 1 || !MV, "Galerkin: stored operator");
