@@ -293,6 +293,28 @@ nat_status nat_mc_surface_pressure(const nat_mesh* mesh, const nat_geom* geom, i
                                    nat_solve_info* info /* [host][n_sys] */,
                                    nat_stream_t stream); /* (sync) */
 
+/* Rows [row_begin, row_end) of the a10 operator (row sharding; SURVEY §8(e) "MC, one large
+ * system"): out[m][r] = 1/2 p[m][i] - w sum_{j != i} dG_m/dn_y(y_i, y_j) p[m][j],
+ * i = row_begin + r; p c128 [n_sys][M] (all rows), out c128 [n_sys][rows]; n_sys <= 64.
+ * Workspace nat_mc_rows_workspace(prec, M, n_sys, rows).  (sync: builds the close-pair list) */
+size_t nat_mc_rows_workspace(nat_prec prec, int64_t M, int n_sys, int64_t rows);
+nat_status nat_mc_apply_rows(nat_prec prec, int64_t M, const double* samples, int n_sys, const double* k /* [host] */,
+                             const void* p, double w, double eps, int64_t row_begin, int64_t row_end, void* out,
+                             void* ws, size_t ws_bytes, nat_stream_t stream);
+/* nat_mc_surface_pressure row-sharded across the ranks of `comm` (NULL => world 1): rank r
+ * owns sample rows [r ceil(M/world), ...) of the RHS and the operator; every operator
+ * application is followed by an in-place NCCL all-gather of each system's iterate and the
+ * Arnoldi process is replicated (identical on all ranks).  Every rank regenerates the same
+ * Philox sample set.  Outputs (samples, p_out [n_sys][M], info) identical on all ranks.
+ * M >= 2.  Workspace nat_mc_sharded_workspace(prec, M, n_sys, max_iter, world).  (sync) */
+size_t nat_mc_sharded_workspace(nat_prec prec, int64_t M, int n_sys, int max_iter, int world);
+nat_status nat_mc_surface_pressure_sharded(nat_comm* comm, const nat_mesh* mesh, const nat_geom* geom, int n_sys,
+                                           const double* k /* [host] */, const void* g_tri,
+                                           const nat_mc_opts* opts, nat_prec prec, double tol, int max_iter,
+                                           double* samples_out, int32_t* sample_tri_out, void* p_out, void* ws,
+                                           size_t ws_bytes, nat_solve_info* info /* [host][n_sys] */,
+                                           nat_stream_t stream);
+
 /* ---------------------------------------------------------------------------------
  * (c) radiation to listeners (reading R-ext):
  *   p[m][l] = sum_s w_s [ p[m][s] dG_m/dn_y(x_l, y_s) - g[m][s] G_m(x_l, y_s) ].

@@ -200,6 +200,8 @@ struct KArr {
 // b = R - (eps/2) g.  Eight lanes per output (fixed assignment: lane l takes splits
 // l, l+8, ... and close pairs l, l+8, ...; fixed xor-tree across the lanes).
 constexpr int kFinLanes = 8;
+// Rows [r0, r0 + rows) of the operator (row sharding; r0 = 0, rows = M otherwise): part
+// and out are [.][nsys][rows]; p and g are full vectors [nsys][ldp].
 __global__ void __launch_bounds__(256) mc_finish_kernel(int nsys, int64_t M, const double* __restrict__ smp,
                                                         const int32_t* __restrict__ rp,
                                                         const int32_t* __restrict__ col, KArr ka, double w,
@@ -207,14 +209,16 @@ __global__ void __launch_bounds__(256) mc_finish_kernel(int nsys, int64_t M, con
                                                         const double2* __restrict__ p,
                                                         const double2* __restrict__ g, double eps,
                                                         double2* out,
-                                                        const unsigned long long* __restrict__ skip) {
+                                                        const unsigned long long* __restrict__ skip,
+                                                        int64_t r0, int64_t rows, int64_t ldp) {
   if (skip && *skip == 0ull) return;
   const int sub = threadIdx.x % kFinLanes;
-  const int64_t i = blockIdx.x * (int64_t)(blockDim.x / kFinLanes) + threadIdx.x / kFinLanes;
+  const int64_t il = blockIdx.x * (int64_t)(blockDim.x / kFinLanes) + threadIdx.x / kFinLanes;
   const int s = blockIdx.y;
-  const bool valid = i < M;  // whole 8-lane groups
-  const size_t q = (size_t)s * M + (valid ? i : 0);
-  const size_t stride = (size_t)nsys * M;
+  const bool valid = il < rows;  // whole 8-lane groups
+  const int64_t i = r0 + (valid ? il : 0);
+  const size_t q = (size_t)s * rows + (valid ? il : 0);
+  const size_t stride = (size_t)nsys * rows;
   double ar = 0.0, ai = 0.0;
   if (valid) {
     for (int sp0 = sub; sp0 < n_split; sp0 += 4 * kFinLanes) {
@@ -243,14 +247,14 @@ __global__ void __launch_bounds__(256) mc_finish_kernel(int nsys, int64_t M, con
         const double t = w * nat::kInv4Pi / r;  // w G = t e^{ikr}
         if (p) {  // w p dG/dn_y = t dn/r^2 (ikr - 1) e^{ikr} p
           const double dn = dx * smp[3 * M + j] + dy * smp[4 * M + j] + dz * smp[5 * M + j];
-          const double2 pv = p[(size_t)s * M + j];
+          const double2 pv = p[(size_t)s * ldp + j];
           const double u = t * dn / (r * r);
           const double er = -cs - k * r * sn, ei = k * r * cs - sn;  // (ikr - 1) e^{ikr}
           ar += u * (er * pv.x - ei * pv.y);
           ai += u * (er * pv.y + ei * pv.x);
         }
         if (g) {  // - w g G
-          const double2 gv = g[(size_t)s * M + j];
+          const double2 gv = g[(size_t)s * ldp + j];
           ar -= t * (cs * gv.x - sn * gv.y);
           ai -= t * (cs * gv.y + sn * gv.x);
         }
@@ -264,10 +268,10 @@ __global__ void __launch_bounds__(256) mc_finish_kernel(int nsys, int64_t M, con
   }
   if (!valid || sub != 0) return;
   if (p) {
-    const double2 pv = p[q];
+    const double2 pv = p[(size_t)s * ldp + i];
     out[q] = make_double2(0.5 * pv.x - ar, 0.5 * pv.y - ai);
   } else {
-    const double2 gv = g[q];
+    const double2 gv = g[(size_t)s * ldp + i];
     out[q] = make_double2(ar - 0.5 * eps * gv.x, ai - 0.5 * eps * gv.y);
   }
 }
@@ -323,44 +327,56 @@ nat::RadInput self_input(int64_t M, const double* smp, int nsys, double w) {
   return in;
 }
 
+// Target rows of an operator application (row sharding): rows [r0, r0 + rows) with their
+// coordinates tgt [3][rows]; p / g are full vectors [nsys][ldp]; the output is [nsys][rows].
+// Default: every row (r0 = 0, rows = M, tgt = the samples, ldp = M).
+struct Rows {
+  int64_t r0 = 0, rows = -1, ldp = -1;
+  const double* tgt = nullptr;
+};
+
 // radiation kernel (partials kept) + one fused epilogue launch per 64 systems
 nat_status finish_op(const nat::RadInput& in, nat_prec prec, int64_t M, const double* smp, int nsys,
                      const double* k, double w, double eps, const double2* p, const double2* g, double2* out,
-                     void* ws, size_t ws_bytes, const NearPairs& np, cudaStream_t s) {
+                     void* ws, size_t ws_bytes, const NearPairs& np, cudaStream_t s, Rows rr = Rows{}) {
+  const int64_t rows = rr.rows < 0 ? M : rr.rows, ldp = rr.ldp < 0 ? M : rr.ldp;
+  const double* tgt = rr.tgt ? rr.tgt : smp;
   nat::RadPartials keep;
-  nat_status st = nat::radiate_internal(in, prec, k, M, smp, out, ws, ws_bytes, true, s, &keep);
+  nat_status st = nat::radiate_internal(in, prec, k, rows, tgt, out, ws, ws_bytes, true, s, &keep);
   if (st != NAT_OK) return st;
   KArr ka{};
   for (int q = 0; q < nsys && q < 64; ++q) ka.k[q] = k[q];
-  mc_finish_kernel<<<dim3((unsigned)((M + 256 / kFinLanes - 1) / (256 / kFinLanes)), nsys), 256, 0, s>>>(
+  mc_finish_kernel<<<dim3((unsigned)((rows + 256 / kFinLanes - 1) / (256 / kFinLanes)), nsys), 256, 0, s>>>(
       nsys, M, smp, np.on ? np.rp : nullptr, np.on ? np.col : nullptr, ka, w, keep.part, keep.n_split, p, g, eps, out,
-      in.skip);
+      in.skip, rr.r0, rows, ldp);
   NAT_LAUNCH_CHECK();
   return NAT_OK;
 }
 
 nat_status mc_rhs_impl(nat_prec prec, int64_t M, const double* smp, int nsys, const double* k,
                        const double2* g, double w, double eps, double2* b, void* ws, size_t ws_bytes,
-                       const double* center, const NearPairs& np, cudaStream_t s) {
+                       const double* center, const NearPairs& np, cudaStream_t s, Rows rr = Rows{}) {
   nat::RadInput in = self_input(M, smp, nsys, w);
   if (center)
     for (int d = 0; d < 3; ++d) in.center[d] = center[d];
   in.g = g;
+  if (rr.ldp > 0) in.ldpg = rr.ldp;
   in.self_r2 = np.on ? np.thr : 0.f;
-  return finish_op(in, prec, M, smp, nsys, k, w, eps, nullptr, g, b, ws, ws_bytes, np, s);
+  return finish_op(in, prec, M, smp, nsys, k, w, eps, nullptr, g, b, ws, ws_bytes, np, s, rr);
 }
 
 nat_status mc_apply_impl(nat_prec prec, int64_t M, const double* smp, int nsys, const double* k,
                          const double2* p, double w, double2* out, void* ws, size_t ws_bytes,
                          const double* center, const NearPairs& np, cudaStream_t s,
-                         const unsigned long long* skip = nullptr) {
+                         const unsigned long long* skip = nullptr, Rows rr = Rows{}) {
   nat::RadInput in = self_input(M, smp, nsys, w);
   if (center)
     for (int d = 0; d < 3; ++d) in.center[d] = center[d];
   in.p = p;
   in.skip = skip;
+  if (rr.ldp > 0) in.ldpg = rr.ldp;
   in.self_r2 = np.on ? np.thr : 0.f;
-  return finish_op(in, prec, M, smp, nsys, k, w, 0.0, p, nullptr, out, ws, ws_bytes, np, s);
+  return finish_op(in, prec, M, smp, nsys, k, w, 0.0, p, nullptr, out, ws, ws_bytes, np, s, rr);
 }
 
 nat_status check_k(int n, const double* k) {
@@ -494,6 +510,70 @@ extern "C" nat_status nat_mc_apply(nat_prec prec, int64_t M, const double* sampl
   if (st != NAT_OK) return st;
   return mc_apply_impl(prec, M, samples, n_sys, k, (const double2*)p, w, (double2*)out, rad, rad_bytes, nullptr,
                        np, (cudaStream_t)stream);
+}
+
+namespace {
+// tgt[d][i] = samples[d][r0 + i]: the target coordinates of a row block ([3][rows] SoA)
+__global__ void copy_targets_kernel(int64_t M, const double* __restrict__ smp, int64_t r0, int64_t rows,
+                                    double* __restrict__ tgt) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= rows) return;
+  for (int d = 0; d < 3; ++d) tgt[(size_t)d * rows + i] = smp[(size_t)d * M + r0 + i];
+}
+
+// dst[s][r0 + i] = src[s][i] (a row block into full vectors of leading dimension ld)
+__global__ void place_rows_kernel(int64_t rows, int64_t r0, int64_t ld, const double2* __restrict__ src,
+                                  double2* __restrict__ dst, const unsigned long long* __restrict__ skip) {
+  if (skip && *skip == 0ull) return;
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int s = blockIdx.y;
+  if (i < rows) dst[(size_t)s * ld + r0 + i] = src[(size_t)s * rows + i];
+}
+}  // namespace
+
+extern "C" size_t nat_mc_rows_workspace(nat_prec prec, int64_t M, int n_sys, int64_t rows) {
+  nat::Carver c(nullptr);
+  carve_near(c, nullptr, M);
+  c.take<double>((size_t)3 * (rows > 0 ? rows : 1));
+  c.take<char>(std::max(nat::radiate_ws_bytes(prec, M, n_sys, rows, 1), nat::radiate_ws_bytes(prec, M, n_sys, rows, 2)));
+  return c.bytes();
+}
+
+extern "C" nat_status nat_mc_apply_rows(nat_prec prec, int64_t M, const double* samples, int n_sys, const double* k,
+                                        const void* p, double w, double eps, int64_t row_begin, int64_t row_end,
+                                        void* out, void* ws, size_t ws_bytes, nat_stream_t stream) {
+  NAT_REQUIRE(prec == NAT_FP32 || prec == NAT_FP64, "bad precision %d", (int)prec);
+  NAT_REQUIRE(M >= 1 && n_sys >= 1 && n_sys <= 64, "need M >= 1 and 1 <= n_sys <= 64");
+  NAT_REQUIRE(0 <= row_begin && row_begin < row_end && row_end <= M, "bad row range");
+  nat_status st = check_k(n_sys, k);
+  if (st != NAT_OK) return st;
+  NAT_REQUIRE_DEV(samples);
+  NAT_REQUIRE_DEV(p);
+  NAT_REQUIRE_DEV(out);
+  NAT_REQUIRE_DEV(ws);
+  const int64_t rows = row_end - row_begin;
+  cudaStream_t s = (cudaStream_t)stream;
+  nat::Carver c(ws);
+  NearPairs np;
+  carve_near(c, &np, M);
+  double* tgt = c.take<double>((size_t)3 * rows);
+  const size_t rad_bytes =
+      std::max(nat::radiate_ws_bytes(prec, M, n_sys, rows, 1), nat::radiate_ws_bytes(prec, M, n_sys, rows, 2));
+  void* rad = c.take<char>(rad_bytes);
+  if (ws_bytes < c.bytes()) return nat::fail(NAT_ERR_WORKSPACE, "workspace %zu < %zu", ws_bytes, c.bytes());
+  if (prec == NAT_FP32 && eps > 0) {
+    st = build_near(np, M, samples, nullptr, eps, s);
+    if (st != NAT_OK) return st;
+  }
+  copy_targets_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, s>>>(M, samples, row_begin, rows, tgt);
+  NAT_LAUNCH_CHECK();
+  Rows rr;
+  rr.r0 = row_begin;
+  rr.rows = rows;
+  rr.ldp = M;
+  rr.tgt = tgt;
+  return mc_apply_impl(prec, M, samples, n_sys, k, (const double2*)p, w, (double2*)out, rad, rad_bytes, nullptr, np,
+                       s, nullptr, rr);
 }
 
 namespace {
@@ -673,5 +753,179 @@ extern "C" nat_status nat_mc_surface_pressure(const nat_mesh* mesh, const nat_ge
     for (int q = 0; q < n_sys; ++q) {
       info[q].t_total_s = tt;
     }
+  return all_conv ? NAT_OK : NAT_WARN_NOT_CONVERGED;
+}
+
+// ------------------------------------------------------------------------------------
+// SURVEY §8(e) "MC, one large system": the same solve row-sharded across ranks — rank r
+// owns sample rows [r ceil(M/g), ...) of the operator and the right-hand side; each
+// operator application is followed by an in-place NCCL all-gather of every system's
+// iterate (replicated Arnoldi, deterministic); every rank regenerates the identical
+// Philox sample set (no sample communication).  comm == NULL: world 1.
+// ------------------------------------------------------------------------------------
+#include "nat_comm.cuh"
+
+namespace {
+struct McShardWs {
+  unsigned long long* best;
+  double2* gs;      // [nb][M]
+  double2* bloc;    // [nb][rows]
+  double2* bfull;   // [nb][ldv]
+  double2* xfull;   // [nb][ldv]
+  double2* oloc;    // [nb][rows]
+  double* tgt;      // [3][rows]
+  nat::KrylovWs kw;
+  void* rad;
+  size_t rad_bytes;
+  NearPairs np;
+};
+
+size_t mc_shard_carve(nat::Carver& c, McShardWs* w, nat_prec prec, int64_t M, int n_sys, int max_iter, int world) {
+  const int nb = n_sys < 64 ? n_sys : 64;
+  const int64_t rpr = (M + world - 1) / world, ldv = rpr * world;
+  McShardWs t;
+  t.best = c.take<unsigned long long>(1);
+  t.gs = c.take<double2>((size_t)nb * M);
+  t.bloc = c.take<double2>((size_t)nb * rpr);
+  t.bfull = c.take<double2>((size_t)nb * ldv);
+  t.xfull = c.take<double2>((size_t)nb * ldv);
+  t.oloc = c.take<double2>((size_t)nb * rpr);
+  t.tgt = c.take<double>((size_t)3 * rpr);
+  nat::krylov_workspace(nb, M, ldv, max_iter, c, &t.kw);
+  t.rad_bytes = std::max(nat::radiate_ws_bytes(prec, M, nb, rpr, 1), nat::radiate_ws_bytes(prec, M, nb, rpr, 2));
+  t.rad = c.take<char>(t.rad_bytes);
+  carve_near(c, &t.np, M);
+  if (w) *w = t;
+  return c.bytes();
+}
+}  // namespace
+
+extern "C" size_t nat_mc_sharded_workspace(nat_prec prec, int64_t M, int n_sys, int max_iter, int world) {
+  if (max_iter <= 0) max_iter = 200;
+  if (world < 1) world = 1;
+  nat::Carver c(nullptr);
+  return mc_shard_carve(c, nullptr, prec, M, n_sys, max_iter, world);
+}
+
+extern "C" nat_status nat_mc_surface_pressure_sharded(nat_comm* comm, const nat_mesh* mesh, const nat_geom* geom,
+                                                      int n_sys, const double* k, const void* g_tri,
+                                                      const nat_mc_opts* opts, nat_prec prec, double tol,
+                                                      int max_iter, double* samples_out, int32_t* sample_tri_out,
+                                                      void* p_out, void* ws, size_t ws_bytes, nat_solve_info* info,
+                                                      nat_stream_t stream) {
+  auto t_start = std::chrono::steady_clock::now();
+  NAT_REQUIRE(mesh && geom && opts, "mesh, geom and opts must be non-null");
+  NAT_REQUIRE(prec == NAT_FP32 || prec == NAT_FP64, "bad precision %d", (int)prec);
+  NAT_REQUIRE(n_sys >= 1, "n_sys must be >= 1");
+  const int64_t M = opts->M;
+  NAT_REQUIRE(M >= 2 && M < (1LL << 31), "M must be in [2, 2^31) (S:170)");
+  NAT_REQUIRE(geom->total_area > 0, "geom->total_area must come from nat_mesh_prepare");
+  nat_status st = check_k(n_sys, k);
+  if (st != NAT_OK) return st;
+  if (tol <= 0) tol = 1e-6;
+  if (max_iter <= 0) max_iter = 200;
+  NAT_REQUIRE_DEV(g_tri);
+  NAT_REQUIRE_DEV(samples_out);
+  NAT_REQUIRE_DEV(sample_tri_out);
+  NAT_REQUIRE_DEV(p_out);
+  NAT_REQUIRE_DEV(ws);
+  const int rank = comm ? comm->rank : 0, world = comm ? comm->world : 1;
+  NAT_REQUIRE(world <= 64, "world size %d > 64", world);
+  const int64_t rpr = (M + world - 1) / world, ldv = rpr * world;
+  const int64_t r0 = std::min<int64_t>(M, (int64_t)rank * rpr), r1 = std::min<int64_t>(M, r0 + rpr);
+  const int64_t rows = r1 - r0;
+  NAT_REQUIRE(rows >= 1, "rank %d owns no sample rows (M = %lld, world = %d)", rank, (long long)M, world);
+  nat::Carver c(ws);
+  McShardWs w;
+  const size_t need = mc_shard_carve(c, &w, prec, M, n_sys, max_iter, world);
+  if (ws_bytes < need) return nat::fail(NAT_ERR_WORKSPACE, "workspace %zu < %zu", ws_bytes, need);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (opts->samples_in) {
+    NAT_REQUIRE_DEV(opts->samples_in);
+    NAT_REQUIRE_DEV(opts->sample_tri_in);
+    NAT_CUDA_TRY(cudaMemcpyAsync(samples_out, opts->samples_in, sizeof(double) * 6 * M, cudaMemcpyDeviceToDevice, s));
+    NAT_CUDA_TRY(cudaMemcpyAsync(sample_tri_out, opts->sample_tri_in, sizeof(int32_t) * M, cudaMemcpyDeviceToDevice, s));
+  } else {
+    st = nat_mc_sample(mesh, geom, M, opts->seed, opts->stream_id, samples_out, sample_tri_out, stream);
+    if (st != NAT_OK) return st;
+  }
+  const double area = geom->total_area;
+  const double eps = opts->eps > 0 ? opts->eps : std::sqrt(area / (nat::kPi * (double)M));
+  const double wgt = (area - nat::kPi * eps * eps) / (double)(M - 1);
+  const double* cen = geom->center;
+  st = build_near(w.np, M, samples_out, cen, eps, s);
+  if (st != NAT_OK) return st;
+  init_best_kernel<<<1, 1, 0, s>>>(w.best);
+  coincident_near_kernel<<<(unsigned)((M + 255) / 256), 256, 0, s>>>(M, samples_out, w.np.rp, w.np.col, w.best);
+  NAT_LAUNCH_CHECK();
+  unsigned long long hb = 0;
+  NAT_CUDA_TRY(cudaMemcpyAsync(&hb, w.best, 8, cudaMemcpyDeviceToHost, s));
+  NAT_CUDA_TRY(cudaStreamSynchronize(s));
+  if (hb != ~0ull)
+    return nat::fail(NAT_ERR_SINGULAR, "coincident samples (%llu, %llu)", hb >> 32, hb & 0xffffffffull);
+  w.np.on = (prec == NAT_FP32);
+  copy_targets_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, s>>>(M, samples_out, r0, rows, w.tgt);
+  NAT_LAUNCH_CHECK();
+  Rows rr;
+  rr.r0 = r0;
+  rr.rows = rows;
+  rr.tgt = w.tgt;
+  int n_comm = 0;
+  auto gather_all = [&](double2* full, int nb, cudaStream_t ss) -> nat_status {
+    if (world == 1) return NAT_OK;
+    for (int q = 0; q < nb; ++q) {  // every rank issues the same collectives in the same order
+      nat_status r = nat::allgather_inplace(comm, (double*)(full + (size_t)q * ldv), (size_t)rpr * 2, ss);
+      if (r != NAT_OK) return r;
+      ++n_comm;
+    }
+    return NAT_OK;
+  };
+  bool all_conv = true;
+  for (int s0 = 0; s0 < n_sys; s0 += 64) {
+    const int nb = (n_sys - s0) < 64 ? (n_sys - s0) : 64;
+    gather_g_kernel<<<dim3((unsigned)((M + 255) / 256), nb), 256, 0, s>>>(
+        nb, M, mesh->n_tri, (const double2*)g_tri + (size_t)s0 * mesh->n_tri, sample_tri_out, w.gs);
+    NAT_LAUNCH_CHECK();
+    rr.ldp = M;  // g: [nb][M]
+    st = mc_rhs_impl(prec, M, samples_out, nb, k + s0, w.gs, wgt, eps, w.bloc, w.rad, w.rad_bytes, cen, w.np, s, rr);
+    if (st != NAT_OK) return st;
+    NAT_CUDA_TRY(cudaMemsetAsync(w.bfull, 0, sizeof(double2) * nb * ldv, s));
+    place_rows_kernel<<<dim3((unsigned)((rows + 255) / 256), nb), 256, 0, s>>>(rows, r0, ldv, w.bloc, w.bfull,
+                                                                               nullptr);
+    NAT_LAUNCH_CHECK();
+    st = gather_all(w.bfull, nb, s);
+    if (st != NAT_OK) return st;
+    auto op = [&](const double2* in, double2* out, uint64_t, const unsigned long long* dmask,
+                  cudaStream_t ss) -> nat_status {
+      Rows ro = rr;
+      ro.ldp = ldv;  // the Krylov vectors: [nb][ldv]
+      nat_status r = mc_apply_impl(prec, M, samples_out, nb, k + s0, in, wgt, w.oloc, w.rad, w.rad_bytes, cen,
+                                   w.np, ss, dmask, ro);
+      if (r != NAT_OK) return r;
+      place_rows_kernel<<<dim3((unsigned)((rows + 255) / 256), nb), 256, 0, ss>>>(rows, r0, ldv, w.oloc, out, dmask);
+      NAT_LAUNCH_CHECK();
+      return gather_all(out, nb, ss);
+    };
+    std::vector<nat::KrylovResult> res;
+    double t_op = 0;
+    st = nat::gmres_batched(nb, M, ldv, w.bfull, w.xfull, op, tol, max_iter, w.kw, res, s, info ? &t_op : nullptr);
+    if (st != NAT_OK) return st;
+    NAT_CUDA_TRY(cudaMemcpy2DAsync((double2*)p_out + (size_t)s0 * M, sizeof(double2) * M, w.xfull,
+                                   sizeof(double2) * ldv, sizeof(double2) * M, nb, cudaMemcpyDeviceToDevice, s));
+    for (int q = 0; q < nb; ++q) all_conv = all_conv && res[q].converged;
+    if (info)
+      for (int q = 0; q < nb; ++q) {
+        info[s0 + q].iters = res[q].iters;
+        info[s0 + q].converged = res[q].converged;
+        info[s0 + q].rel_residual = res[q].rel_residual;
+        info[s0 + q].t_matvec_s = t_op;
+        info[s0 + q].t_comm_s = 0;
+      }
+  }
+  NAT_CUDA_TRY(cudaStreamSynchronize(s));
+  const double tt = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+  if (info)
+    for (int q = 0; q < n_sys; ++q) info[q].t_total_s = tt;
+  (void)n_comm;
   return all_conv ? NAT_OK : NAT_WARN_NOT_CONVERGED;
 }

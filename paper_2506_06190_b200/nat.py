@@ -119,6 +119,13 @@ _SIGS = {
                                           C.POINTER(_D), _P, C.POINTER(_McOpts), C.c_int, _D,
                                           C.c_int, _P, _P, _P, _P, _SZ, C.POINTER(_SolveInfo),
                                           _P]),
+    "nat_mc_rows_workspace": (_SZ, [C.c_int, _I64, C.c_int, _I64]),
+    "nat_mc_apply_rows": (C.c_int, [C.c_int, _I64, _P, C.c_int, C.POINTER(_D), _P, _D, _D, _I64, _I64, _P, _P, _SZ,
+                                    _P]),
+    "nat_mc_sharded_workspace": (_SZ, [C.c_int, _I64, C.c_int, C.c_int, C.c_int]),
+    "nat_mc_surface_pressure_sharded": (C.c_int, [_P, C.POINTER(_Mesh), C.POINTER(_Geom), C.c_int, C.POINTER(_D), _P,
+                                                  C.POINTER(_McOpts), C.c_int, _D, C.c_int, _P, _P, _P, _P, _SZ,
+                                                  C.POINTER(_SolveInfo), _P]),
     "nat_bem_sources": (C.c_int, [C.POINTER(_Mesh), C.POINTER(_Geom), C.c_int, C.c_int, _P, _P,
                                   _P, _P, _P, _P, _P, _P]),
     "nat_mc_sources": (C.c_int, [_I64, _P, _D, _P, _P, _P, _P]),
@@ -588,6 +595,48 @@ def nat_mc_surface_pressure(mesh: Mesh, geom: Geom, k, g_tri, M: int, seed: int 
     st = lib().nat_mc_surface_pressure(C.byref(mesh.c()), C.byref(geom.c()), n_sys, kp, _ptr(g_tri),
                                        C.byref(opts), pr, float(tol), int(max_iter), _ptr(smp), _ptr(tri),
                                        _ptr(p), _ptr(ws), ws.numel(), infos, _stream())
+    _check(st, allow_warn=True)
+    return smp, tri, p, [dict(iters=i.iters, converged=i.converged, rel_residual=i.rel_residual,
+                              t_total_s=i.t_total_s, t_matvec_s=i.t_matvec_s) for i in infos]
+
+
+def nat_mc_apply_rows(samples, k, p, w, eps, row_begin: int, row_end: int, prec="fp32"):
+    """Rows [row_begin, row_end) of the MC operator applied to p (n_sys, M) -> (n_sys, rows)."""
+    pr = _prec(prec)
+    M = samples.shape[1]
+    ks, kp = _karr(k)
+    p = torch.atleast_2d(p).to(torch.complex128).contiguous()
+    out = torch.empty(ks.size, row_end - row_begin, dtype=torch.complex128, device=samples.device)
+    ws = _ws(lib().nat_mc_rows_workspace(pr, M, ks.size, row_end - row_begin), samples.device)
+    _check(lib().nat_mc_apply_rows(pr, M, _ptr(samples), ks.size, kp, _ptr(p), float(w), float(eps), int(row_begin),
+                                   int(row_end), _ptr(out), _ptr(ws), ws.numel(), _stream()))
+    return out
+
+
+def nat_mc_surface_pressure_sharded(mesh: Mesh, geom: Geom, k, g_tri, M: int, comm: Optional["Comm"] = None,
+                                    seed: int = 0, stream_id: int = 0, eps: float = 0.0, prec="fp32", tol=1e-6,
+                                    max_iter=200, samples_in=None, sample_tri_in=None, out=None, ws=None):
+    """nat_mc_surface_pressure row-sharded over the ranks of `comm` (all-gather of the
+    iterate per operator application).  Returns (samples, sample_tri, p (n_sys, M), infos)."""
+    pr = _prec(prec)
+    dev = mesh.vxyz.device
+    g_tri = torch.atleast_2d(g_tri).to(torch.complex128).contiguous()
+    ks, kp = _karr(k)
+    n_sys = ks.size
+    if out is None:
+        smp = torch.empty(6, M, dtype=torch.float64, device=dev)
+        tri = torch.empty(M, dtype=torch.int32, device=dev)
+        p = torch.empty(n_sys, M, dtype=torch.complex128, device=dev)
+    else:
+        smp, tri, p = out
+    world = comm.world if comm else 1
+    if ws is None:
+        ws = _ws(lib().nat_mc_sharded_workspace(pr, M, n_sys, max_iter, world), dev)
+    opts = _McOpts(M, seed, stream_id, float(eps), _ptr(samples_in), _ptr(sample_tri_in))
+    infos = (_SolveInfo * n_sys)()
+    st = lib().nat_mc_surface_pressure_sharded(comm.handle if comm else None, C.byref(mesh.c()), C.byref(geom.c()),
+                                               n_sys, kp, _ptr(g_tri), C.byref(opts), pr, float(tol), int(max_iter),
+                                               _ptr(smp), _ptr(tri), _ptr(p), _ptr(ws), ws.numel(), infos, _stream())
     _check(st, allow_warn=True)
     return smp, tri, p, [dict(iters=i.iters, converged=i.converged, rel_residual=i.rel_residual,
                               t_total_s=i.t_total_s, t_matvec_s=i.t_matvec_s) for i in infos]

@@ -144,3 +144,50 @@ def test_c3_launch_configuration():
             res.append(0.5 * P[s, i] + Ai @ P[s, j] - bi)
             nb.append(bi)
         assert np.linalg.norm(res) / np.linalg.norm(nb) <= 1e-4
+
+
+@pytest.mark.parametrize("prec", ["fp32", "fp64"])
+def test_mc_operator_row_blocks_ragged(prec):
+    """SURVEY §8(e) row sharding of the MC operator: rows [r0, r1) of three ragged blocks
+    (as ranks 0..2 of 3 own them) against the oracle's operator rows."""
+    nat = _nat()
+    M = 2333
+    m, geo, mesh, gg, y, n, tri = _system_case(M)
+    ks = [0.5, 3.0, 6.0]
+    eps, w = nat.mc_weights(geo["total_area"], M)
+    p = I.random_complex((3, M), 21)
+    smp = torch.from_numpy(np.ascontiguousarray(np.concatenate([y.T, n.T]))).cuda()
+    pt = torch.from_numpy(p).cuda()
+    full = to_np(nat.nat_mc_apply(smp, ks, pt, w, eps, prec))
+    blocks = []
+    for r in range(3):
+        r0, r1 = nat.row_range(M, r, 3)
+        blocks.append(to_np(nat.nat_mc_apply_rows(smp, ks, pt, w, eps, r0, r1, prec)))
+    got = np.concatenate(blocks, axis=1)
+    for s, k in enumerate(ks):
+        A_ref, _ = mc.system(y, n, np.zeros(M), k, geo["total_area"])
+        assert rel_l2(got[s], A_ref @ p[s]) <= TOL[prec]
+    assert rel_l2(got, full) <= (1e-6 if prec == "fp32" else 1e-13)
+
+
+@pytest.mark.parametrize("prec", ["fp32", "fp64"])
+def test_sharded_surface_pressure_world1_matches(prec):
+    """The row-sharded solve on one rank (comm = NULL) reproduces the batched solve and the
+    oracle (same samples, same iterations)."""
+    nat = _nat()
+    m = I.bowl(32, 8, 2)
+    geo, mesh, gg = _case(m)
+    M, seed = 700, 3
+    ks = [0.5, 2.0, 4.5]
+    g_tri = I.neumann_harmonics(m, 3)
+    y, n, tri, p_ref, infos = mc.surface_pressure(m.v, m.t, geo, ks, g_tri, M, seed, tol=1e-13)
+    tol = 1e-6 if prec == "fp32" else 1e-12
+    gt = torch.from_numpy(g_tri).cuda()
+    smp, stri, p, info = nat.nat_mc_surface_pressure_sharded(mesh, gg, ks, gt, M, None, seed, prec=prec, tol=tol)
+    _, _, p0, info0 = nat.nat_mc_surface_pressure(mesh, gg, ks, gt, M, seed, prec=prec, tol=tol)
+    assert np.array_equal(to_np(stri), tri)
+    for s in range(3):
+        assert info[s]["converged"] == 1
+        assert abs(info[s]["iters"] - info0[s]["iters"]) <= 1
+        assert rel_l2(to_np(p)[s], p_ref[s]) <= TOL[prec]
+        assert rel_l2(to_np(p)[s], to_np(p0)[s]) <= (1e-5 if prec == "fp32" else 1e-11)
