@@ -148,7 +148,13 @@ class Step:
         P = GRID[0] * GRID[1] * GRID[2]
         self.P = P
         self.l0, self.l1 = shard(P, rank, world)
-        self.mc_idx = mc_share(len(KAS), rank, world)
+        # BEM-MC on > 1 rank: row-sharded (every rank owns sample rows of all the systems, one
+        # all-gather per operator application) or, NAT_BENCH_MC=systems, whole
+        # wavenumbers dealt round-robin (no collective)
+        mc_mode = os.environ.get("NAT_BENCH_MC", "rows")   # rows | systems | rows_always (1-rank check)
+        self.mc_sharded = (world > 1 and mc_mode == "rows") or mc_mode == "rows_always"
+        self.mc_idx = list(range(len(KAS))) if self.mc_sharded else mc_share(len(KAS), rank, world)
+        self.mc_r0, self.mc_r1 = shard(M_MC, rank, world) if self.mc_sharded else (0, M_MC)
         self.lock = threading.Lock()
         # device-resident inputs and buffers (allocated once, outside the timed region)
         self.mesh = nat.Mesh.from_numpy(m.v, m.t, device=dev)
@@ -181,6 +187,9 @@ class Step:
         self.g3 = self.g.expand(len(KAS), -1).contiguous()
         if self.mc_idx:
             self.mc_plan = nat.McPlan(M_MC, len(self.mc_idx), "fp32", 200, dev)
+            if self.mc_sharded:
+                self.mc_shard_ws = nat._ws(nat.lib().nat_mc_sharded_workspace(nat.NAT_FP32, M_MC, len(self.mc_idx),
+                                                                              200, world), dev)
             self.rad_plan_mc = nat.RadiatePlan(M_MC, len(self.mc_idx), self.n_lis, "fp32", dev)
             self.out_mc = torch.empty(len(self.mc_idx), self.n_lis, dtype=torch.complex128, device=dev)
         self.ev = {}
@@ -355,9 +364,14 @@ class Step:
         nat = self.nat
         ks = [KAS[i] for i in self.mc_idx]
         self._ev("mc0")
-        smp, stri, p, infos = nat.nat_mc_surface_pressure(self.mesh, geo, ks, self.g_mc, M_MC, seed=20250606,
-                                                          stream_id=0, prec="fp32", tol=1e-6,
-                                                          plan=self.mc_plan)                    # a8-a10
+        if self.mc_sharded:
+            smp, stri, p, infos = nat.nat_mc_surface_pressure_sharded(
+                self.mesh, geo, ks, self.g_mc, M_MC, self.comm, seed=20250606, stream_id=0, prec="fp32", tol=1e-6,
+                ws=self.mc_shard_ws)                                                                 # a8-a10, rows
+        else:
+            smp, stri, p, infos = nat.nat_mc_surface_pressure(self.mesh, geo, ks, self.g_mc, M_MC, seed=20250606,
+                                                              stream_id=0, prec="fp32", tol=1e-6,
+                                                              plan=self.mc_plan)                # a8-a10
         self._ev("mc1")
         gs = nat.nat_mc_gather_neumann(self.g_mc, stri)
         src = nat.nat_mc_sources(smp, geo.total_area, p, gs)
@@ -366,9 +380,10 @@ class Step:
         self._ev("radmc1")
         with self.lock:
             counts["mc_op_s"] += infos[0]["t_matvec_s"] if infos else 0.0   # one batch: shared
+            mc_rows = self.mc_r1 - self.mc_r0   # this rank's operator rows
             for inf in infos:
-                counts["mc_rhs"] += M_MC * (M_MC - 1)
-                counts["mc_op"] += inf["iters"] * M_MC * (M_MC - 1)
+                counts["mc_rhs"] += mc_rows * (M_MC - 1)
+                counts["mc_op"] += inf["iters"] * mc_rows * (M_MC - 1)
                 counts["mc_iters"].append(inf["iters"])
             counts["rad"] += M_MC * self.n_lis * len(ks)
 

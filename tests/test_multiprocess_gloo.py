@@ -4,7 +4,9 @@
 * the row ownership the library enforces (rows_per_rank = ceil(n / world)) and the
   bench's listener / MC-wavenumber sharding tile their index sets exactly;
 * the row-sharded GMRES protocol (local rows -> all-gather of the iterate -> replicated
-  Arnoldi) emulated with the oracle's rows reproduces the single-process solution;
+  Arnoldi) emulated with the oracle's rows reproduces the single-process solution, for
+  the dense BEM and for the row-sharded BEM-MC system (identical Philox samples
+  regenerated on every rank, SURVEY §8(e));
 * the bench's max-over-ranks timing reduction and sum-over-ranks work reduction.
 """
 import os
@@ -130,6 +132,51 @@ def test_row_sharded_gmres_protocol_matches_single_process():
         assert out[r][1] == info["iters"]
         np.testing.assert_allclose(out[r][0], x, rtol=0, atol=1e-12 * np.abs(x).max())
     assert np.array_equal(out[0][0], out[1][0])   # replicated Arnoldi: identical on ranks
+
+
+def _mc_gmres_fn(rank, world):
+    """Row-sharded BEM-MC: every rank regenerates the same samples, forms its rows of the
+    MC system (oracle arithmetic) and runs the replicated GMRES with an all-gather."""
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import nat_inputs as I
+    from oracle import geometry, gmres, mc
+    from paper_2506_06190_b200.nat import row_range
+    m = I.icosphere(2)
+    geo = geometry.mesh_prepare(m.v, m.t)
+    M = 301
+    y, n, tri = mc.sample_uniform(m.v, m.t, geo, M, 5)
+    g = I.neumann_constant(m)[tri]
+    A, b = mc.system(y, n, g, 1.5, geo["total_area"])
+    r0, r1 = row_range(M, rank, world)
+    A_loc, b_loc = A[r0:r1], b[r0:r1]
+    rpr = -(-M // world)
+
+    def gather(v_loc):
+        buf = torch.zeros(rpr, dtype=torch.complex128)
+        buf[: v_loc.size] = torch.from_numpy(v_loc)
+        parts = [torch.zeros(rpr, dtype=torch.complex128) for _ in range(world)]
+        dist.all_gather(parts, buf)
+        return torch.cat(parts).numpy()[:M]
+
+    x, info = gmres.gmres(lambda z: gather(A_loc @ z), gather(b_loc), tol=1e-12, max_iter=200)
+    return x, info["iters"], tri
+
+
+def test_row_sharded_mc_protocol_matches_single_process():
+    import nat_inputs as I
+    from oracle import geometry, gmres, mc
+    out = _run(_mc_gmres_fn)
+    m = I.icosphere(2)
+    geo = geometry.mesh_prepare(m.v, m.t)
+    y, n, tri = mc.sample_uniform(m.v, m.t, geo, 301, 5)
+    A, b = mc.system(y, n, I.neumann_constant(m)[tri], 1.5, geo["total_area"])
+    x, info = gmres.gmres(lambda z: A @ z, b, tol=1e-12, max_iter=200)
+    for r in range(WORLD):
+        assert np.array_equal(out[r][2], tri)          # identical samples on every rank
+        assert out[r][1] == info["iters"]
+        np.testing.assert_allclose(out[r][0], x, rtol=0, atol=1e-12 * np.abs(x).max())
+    assert np.array_equal(out[0][0], out[1][0])
 
 
 def _reduce_fn(rank, world):
