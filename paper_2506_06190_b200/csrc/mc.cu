@@ -521,13 +521,27 @@ __global__ void copy_targets_kernel(int64_t M, const double* __restrict__ smp, i
   for (int d = 0; d < 3; ++d) tgt[(size_t)d * rows + i] = smp[(size_t)d * M + r0 + i];
 }
 
-// dst[s][r0 + i] = src[s][i] (a row block into full vectors of leading dimension ld)
+struct SysIdx {  // system q of a compacted batch -> its slot in the full batch
+  int idx[64];
+};
+
+// dst[sys(s)][r0 + i] = src[s][i] (a row block into full vectors of leading dimension ld;
+// sys(s) = s, or ix.idx[s] for a compacted batch of the systems still iterating)
 __global__ void place_rows_kernel(int64_t rows, int64_t r0, int64_t ld, const double2* __restrict__ src,
-                                  double2* __restrict__ dst, const unsigned long long* __restrict__ skip) {
+                                  double2* __restrict__ dst, const unsigned long long* __restrict__ skip,
+                                  SysIdx ix, bool use_ix) {
   if (skip && *skip == 0ull) return;
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int s = blockIdx.y;
-  if (i < rows) dst[(size_t)s * ld + r0 + i] = src[(size_t)s * rows + i];
+  const int d = use_ix ? ix.idx[s] : s;
+  if (i < rows) dst[(size_t)d * ld + r0 + i] = src[(size_t)s * rows + i];
+}
+
+// dst[s][:] = src[ix.idx[s]][:] over rows of length ld (compaction of the active systems)
+__global__ void gather_sys_kernel(int64_t ld, SysIdx ix, const double2* __restrict__ src, double2* __restrict__ dst) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int s = blockIdx.y;
+  if (j < ld) dst[(size_t)s * ld + j] = src[(size_t)ix.idx[s] * ld + j];
 }
 }  // namespace
 
@@ -774,6 +788,7 @@ struct McShardWs {
   double2* xfull;   // [nb][ldv]
   double2* oloc;    // [nb][rows]
   double* tgt;      // [3][rows]
+  double2* tin;     // [nb][ldv] compacted operator input
   nat::KrylovWs kw;
   void* rad;
   size_t rad_bytes;
@@ -791,6 +806,7 @@ size_t mc_shard_carve(nat::Carver& c, McShardWs* w, nat_prec prec, int64_t M, in
   t.xfull = c.take<double2>((size_t)nb * ldv);
   t.oloc = c.take<double2>((size_t)nb * rpr);
   t.tgt = c.take<double>((size_t)3 * rpr);
+  t.tin = c.take<double2>((size_t)nb * ldv);
   nat::krylov_workspace(nb, M, ldv, max_iter, c, &t.kw);
   t.rad_bytes = std::max(nat::radiate_ws_bytes(prec, M, nb, rpr, 1), nat::radiate_ws_bytes(prec, M, nb, rpr, 2));
   t.rad = c.take<char>(t.rad_bytes);
@@ -891,19 +907,38 @@ extern "C" nat_status nat_mc_surface_pressure_sharded(nat_comm* comm, const nat_
     if (st != NAT_OK) return st;
     NAT_CUDA_TRY(cudaMemsetAsync(w.bfull, 0, sizeof(double2) * nb * ldv, s));
     place_rows_kernel<<<dim3((unsigned)((rows + 255) / 256), nb), 256, 0, s>>>(rows, r0, ldv, w.bloc, w.bfull,
-                                                                               nullptr);
+                                                                               nullptr, SysIdx{}, false);
     NAT_LAUNCH_CHECK();
     st = gather_all(w.bfull, nb, s);
     if (st != NAT_OK) return st;
-    auto op = [&](const double2* in, double2* out, uint64_t, const unsigned long long* dmask,
+    const uint64_t all = nb == 64 ? ~0ull : ((1ull << nb) - 1);
+    auto op = [&](const double2* in, double2* out, uint64_t active, const unsigned long long* dmask,
                   cudaStream_t ss) -> nat_status {
       Rows ro = rr;
       ro.ldp = ldv;  // the Krylov vectors: [nb][ldv]
-      nat_status r = mc_apply_impl(prec, M, samples_out, nb, k + s0, in, wgt, w.oloc, w.rad, w.rad_bytes, cen,
-                                   w.np, ss, dmask, ro);
-      if (r != NAT_OK) return r;
-      place_rows_kernel<<<dim3((unsigned)((rows + 255) / 256), nb), 256, 0, ss>>>(rows, r0, ldv, w.oloc, out, dmask);
-      NAT_LAUNCH_CHECK();
+      // only the systems still iterating (host mask, one iteration late): compact them
+      SysIdx ix{};
+      double kc[64];
+      int na = 0;
+      for (int q = 0; q < nb; ++q)
+        if (((active & all) >> q) & 1ull) {
+          ix.idx[na] = q;
+          kc[na++] = k[s0 + q];
+        }
+      const bool compact = na < nb;
+      if (na > 0) {
+        const double2* src = in;
+        if (compact) {
+          gather_sys_kernel<<<dim3((unsigned)((ldv + 255) / 256), na), 256, 0, ss>>>(ldv, ix, in, w.tin);
+          src = w.tin;
+        }
+        nat_status r = mc_apply_impl(prec, M, samples_out, na, compact ? kc : k + s0, src, wgt, w.oloc, w.rad,
+                                     w.rad_bytes, cen, w.np, ss, dmask, ro);
+        if (r != NAT_OK) return r;
+        place_rows_kernel<<<dim3((unsigned)((rows + 255) / 256), na), 256, 0, ss>>>(rows, r0, ldv, w.oloc, out, dmask,
+                                                                                   ix, compact);
+        NAT_LAUNCH_CHECK();
+      }
       return gather_all(out, nb, ss);
     };
     std::vector<nat::KrylovResult> res;
