@@ -674,11 +674,11 @@ struct NearArgs {
 // The rule table is staged in shared memory (all groups walk it in the same order).
 constexpr int kMaxNearPts = 7 << 8;  // up to 4 subdivision levels x 7 points (S: 448 at 3)
 
-template <typename R, int NQ, int G, bool BM>
+template <typename R, int NQ, int G, bool BM, bool MFD>
 __device__ __forceinline__ void near_item(const NearArgs<R>& a, int64_t gid, int lig, const float4* s_rf,
                                           const double4* s_rd);
 
-template <typename R, int NQ, int G, bool BM = false>
+template <typename R, int NQ, int G, bool BM = false, bool MFD = false>
 __global__ void __launch_bounds__(kThreads) near_kernel(NearArgs<R> a) {
   extern __shared__ __align__(16) unsigned char near_smem[];
   float4* s_rf = reinterpret_cast<float4*>(near_smem);
@@ -696,10 +696,12 @@ __global__ void __launch_bounds__(kThreads) near_kernel(NearArgs<R> a) {
   const int lig = threadIdx.x % G;
   const int64_t stride = (int64_t)gridDim.x * (blockDim.x / G);
   for (int64_t gid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G; gid < nitems; gid += stride)
-    near_item<R, NQ, G, BM>(a, gid, lig, s_rf, s_rd);
+    near_item<R, NQ, G, BM, MFD>(a, gid, lig, s_rf, s_rd);
 }
 
-template <typename R, int NQ, int G, bool BM>
+// MFD: matrix-free corrections (a.delta) instead of storing A (compile-time, so the
+// stored-matrix kernels keep their register budget)
+template <typename R, int NQ, int G, bool BM, bool MFD>
 __device__ __forceinline__ void near_item(const NearArgs<R>& a, int64_t gid, int lig, const float4* s_rf,
                                           const double4* s_rd) {
   const int2 item = a.items[gid];
@@ -777,8 +779,8 @@ __device__ __forceinline__ void near_item(const NearArgs<R>& a, int64_t gid, int
     Vr = V.x - Kp.y / a.k;
     Vi = V.y + Kp.x / a.k;
   }
-  if (!a.delta) store_entry<R>(a.A, (size_t)r * a.lda + j, -Kr, -Ki);
-  if (a.n_rhs > 0 || a.delta) {
+  if (!MFD) store_entry<R>(a.A, (size_t)r * a.lda + j, -Kr, -Ki);
+  if (a.n_rhs > 0 || MFD) {
     R y[NQ][3], w[NQ];
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
@@ -794,8 +796,8 @@ __device__ __forceinline__ void near_item(const NearArgs<R>& a, int64_t gid, int
     else
       far_entry<R, NQ>(y, w, a.cols.nrm[j], a.cols.nrm[n + j], a.cols.nrm[2 * n + j],
                        (R)(ci[0] - a.cx), (R)(ci[1] - a.cy), (R)(ci[2] - a.cz), a.k, fVr, fVi, fKr, fKi);
-    if constexpr (!BM) {  // matrix-free: A_ij = A^far_ij + delta_e with A = -K
-      if (a.delta) a.delta[e] = make_double2((double)fKr - (double)Kr, (double)fKi - (double)Ki);
+    if constexpr (MFD && !BM) {  // matrix-free: A_ij = A^far_ij + delta_e with A = -K
+      a.delta[e] = make_double2((double)fKr - (double)Kr, (double)fKi - (double)Ki);
     }
     const double dVr = (double)Vr - (double)fVr, dVi = (double)Vi - (double)fVi;
     for (int q = 0; q < a.n_rhs; ++q) {
@@ -1822,7 +1824,7 @@ nat_status assemble_impl(const nat_mesh* mesh, const nat_geom* geom, const Opts&
     if (o.bm)
       near_kernel<R, NQ, 4, true><<<gS, kThreads, na.npts * rsz, s>>>(na);
     else
-      near_kernel<R, NQ, 4><<<gS, kThreads, na.npts * rsz, s>>>(na);
+      (mf.delta ? near_kernel<R, NQ, 4, false, true> : near_kernel<R, NQ, 4>)<<<gS, kThreads, na.npts * rsz, s>>>(na);
     na.rule = w.rule_N;  // class N: one thread per pair
     na.rule_f = w.rule_Nf;
     na.npts = (int)pN.size();
@@ -1832,7 +1834,7 @@ nat_status assemble_impl(const nat_mesh* mesh, const nat_geom* geom, const Opts&
     if (o.bm)
       near_kernel<R, NQ, 1, true><<<gN, kThreads, na.npts * rsz, s>>>(na);
     else
-      near_kernel<R, NQ, 1><<<gN, kThreads, na.npts * rsz, s>>>(na);
+      (mf.delta ? near_kernel<R, NQ, 1, false, true> : near_kernel<R, NQ, 1>)<<<gN, kThreads, na.npts * rsz, s>>>(na);
     NAT_LAUNCH_CHECK();
   }
   if (o.gal) {
