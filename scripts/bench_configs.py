@@ -118,6 +118,44 @@ def c4(gi=0):
                     "to the 64^3 grid (roofline per pair-mode for fused modes: R_sfu 2.31e12, SURVEY §8d)"}
 
 
+def c4_sweep(n_geo=64):
+    """C4 end to end on one GPU: all 64 scene geometries (8 heights x 8 sizes), each with
+    64 wavenumbers (8 materials x 8 modes): mesh preparation, Philox samples, the batched
+    MC solve and the fused radiation to its 64^3 listener grid.  Meshes are uploaded before
+    the timed region; device time with CUDA events over the whole sweep."""
+    scenes = []
+    for gi in range(n_geo):
+        m, g8, D = I.c4_geometry(gi)
+        scenes.append((gi, nat.Mesh.from_numpy(m.v, m.t), torch.from_numpy(np.tile(g8, (8, 1))).cuda(),
+                       list(I.c4_wavenumbers(D)), m.n_tri))
+    M = 2048
+    plan = nat.McPlan(M, 64, "fp32", 200, "cuda")
+    P = 64 ** 3
+    rplan = nat.RadiatePlan(M, 64, P, "fp32", "cuda")
+    out = torch.empty(64, P, dtype=torch.complex128, device="cuda")
+    iters = []
+
+    def run():
+        for gi, mesh, g, ks, _ in scenes:
+            geo = nat.nat_mesh_prepare(mesh)
+            smp, stri, p, infos = nat.nat_mc_surface_pressure(mesh, geo, ks, g, M, seed=I.SEED, stream_id=gi,
+                                                              prec="fp32", plan=plan)
+            iters.append(sum(i["iters"] for i in infos))
+            src = nat.nat_mc_sources(smp, geo.total_area, p, nat.nat_mc_gather_neumann(g, stri), center=geo.center)
+            lis = nat.nat_listener_grid(geo.center, geo.bound_radius, 64, 64, 64)
+            nat.nat_radiate_field(src, ks, lis, "fp32", out=out, plan=rplan)
+        return None
+
+    t, _ = timed(run, reps=1)
+    n = len(scenes)
+    return {"geometries": n, "wavenumbers_per_geometry": 64, "configs": n * 8, "seconds": t,
+            "seconds_per_geometry": t / n, "listener_pt_modes_per_s": n * 64 * P / t,
+            "mean_gmres_iters_per_system": float(np.mean(iters[-n:]) / 64),
+            "note": "the NAT training-data sweep (BASELINE configs[3]) on one GPU: 64 geometries x 64 "
+                    "wavenumbers = 512 configs x 8 modes; per geometry mesh prep + M = 2048 samples + batched MC "
+                    "solve + fused radiation to 64^3 listeners (262,144 x 64 field values); 8 GPUs deal geometries"}
+
+
 def c5(rows=1024):
     m = I.cubed_sphere(129)
     gt = torch.from_numpy(I.neumann_rigid_z(m)[None]).cuda()
@@ -248,7 +286,8 @@ def main():
     res = {"device": torch.cuda.get_device_name(0)}
     sel = set(sys.argv[1:])
     for name, fn in (("C1_fp32", lambda: c1("fp32")), ("C1_fp64", lambda: c1("fp64")), ("C3", c3), ("C4", c4),
-                     ("C5", c5), ("BM_C2", bm_c2), ("C5_MF", c5_mf), ("C2_MF", c2_mf), ("GAL_C2", gal_c2)):
+                     ("C5", c5), ("BM_C2", bm_c2), ("C5_MF", c5_mf), ("C2_MF", c2_mf), ("GAL_C2", gal_c2),
+                     ("C4_SWEEP", c4_sweep)):
         if sel and name not in sel:
             continue
         try:
