@@ -139,6 +139,7 @@ class ClockSampler:
 class Step:
     def __init__(self, nat, torch, rank, world, comm, host):
         self.nat, self.torch, self.rank, self.world, self.comm = nat, torch, rank, world, comm
+        self.comm_mc = None   # the BEM-MC chain's communicator (set by main at N > 1)
         self.host = host
         dev = torch.device("cuda")
         self.dev = dev
@@ -366,7 +367,7 @@ class Step:
         self._ev("mc0")
         if self.mc_sharded:
             smp, stri, p, infos = nat.nat_mc_surface_pressure_sharded(
-                self.mesh, geo, ks, self.g_mc, M_MC, self.comm, seed=20250606, stream_id=0, prec="fp32", tol=1e-6,
+                self.mesh, geo, ks, self.g_mc, M_MC, self.comm_mc, seed=20250606, stream_id=0, prec="fp32", tol=1e-6,
                 ws=self.mc_shard_ws)                                                                 # a8-a10, rows
         else:
             smp, stri, p, infos = nat.nat_mc_surface_pressure(self.mesh, geo, ks, self.g_mc, M_MC, seed=20250606,
@@ -514,12 +515,17 @@ def main():
     torch.cuda.set_device(local)
     from paper_2506_06190_b200 import nat
     nat.lib()
-    comm = None
+    comm = comm_mc = None
     if world > 1:
         dist.init_process_group("nccl", init_method="env://", device_id=torch.device("cuda", local))
         comm = nat.Comm.from_torch_distributed()
+        # the BEM-MC chain runs beside the dense chain from another host thread: its
+        # all-gathers get their own communicator, so each communicator sees its collectives
+        # in the same order on every rank (two threads interleaving on one would deadlock)
+        comm_mc = nat.Comm.from_torch_distributed()
     host = load_host()
     step = Step(nat, torch, rank, world, comm, host)
+    step.comm_mc = comm_mc
     step.overlap = args.overlap
     # pinned host copies for the e2e measurement
     m = host["mesh"]
