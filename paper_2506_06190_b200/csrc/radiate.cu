@@ -428,8 +428,9 @@ __global__ void __launch_bounds__(kThreads) radiate_f64_kernel(RadParams prm) {
         const double dx = f[0] - tx[r], dy = f[1] - ty[r], dz = f[2] - tz[r];
         const double r2 = fma(dz, dz, fma(dy, dy, dx * dx));
         const double dn = fma(dz, f[5], fma(dy, f[4], dx * f[3]));
-        const double rr = sqrt(r2);
-        const double rho = r2 > 0.0 ? 1.0 / rr : 0.0;  // self pair (MC operators) -> 0
+        // 1/r by rsqrt (MUFU.RSQ64H + Newton) instead of sqrt and a DP division; r = r^2 / r
+        const double rho = r2 > 0.0 ? rsqrt(r2) : 0.0;  // self pair (MC operators) -> 0
+        const double rr = r2 * rho;
         const double qq = dn * (rho * rho);
         double sn, cs;
         nat::pair_sincos(k * rr, &sn, &cs);
