@@ -606,8 +606,9 @@ def nat_mc_apply_rows(samples, k, p, w, eps, row_begin: int, row_end: int, prec=
     M = samples.shape[1]
     ks, kp = _karr(k)
     p = torch.atleast_2d(p).to(torch.complex128).contiguous()
-    out = torch.empty(ks.size, row_end - row_begin, dtype=torch.complex128, device=samples.device)
-    ws = _ws(lib().nat_mc_rows_workspace(pr, M, ks.size, row_end - row_begin), samples.device)
+    rows = max(int(row_end) - int(row_begin), 1)   # the library validates the range
+    out = torch.empty(ks.size, rows, dtype=torch.complex128, device=samples.device)
+    ws = _ws(lib().nat_mc_rows_workspace(pr, M, ks.size, rows), samples.device)
     _check(lib().nat_mc_apply_rows(pr, M, _ptr(samples), ks.size, kp, _ptr(p), float(w), float(eps), int(row_begin),
                                    int(row_end), _ptr(out), _ptr(ws), ws.numel(), _stream()))
     return out

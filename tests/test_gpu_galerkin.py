@@ -147,3 +147,14 @@ def test_galerkin_rejects_burton_miller():
         o = nat.quad_opts(galerkin=True, burton_miller=True)
         nl = nat.nat_bem_near_list(mesh, gg, opts=o)
         nat.nat_bem_assemble(mesh, gg, nl, 2.0, prec="fp32", opts=o)
+
+
+def test_galerkin_option_errors():
+    nat = _nat()
+    m = I.icosphere(1)
+    mesh = nat.Mesh.from_numpy(m.v, m.t)
+    gg = nat.nat_mesh_prepare(mesh)
+    o = nat.quad_opts(galerkin=True, ss_order=9)
+    nl = nat.nat_bem_near_list(mesh, gg, opts=o)
+    with pytest.raises(nat.NatError, match="ss_order"):
+        nat.nat_bem_assemble(mesh, gg, nl, 2.0, prec="fp32", opts=o)

@@ -191,3 +191,20 @@ def test_sharded_surface_pressure_world1_matches(prec):
         assert abs(info[s]["iters"] - info0[s]["iters"]) <= 1
         assert rel_l2(to_np(p)[s], p_ref[s]) <= TOL[prec]
         assert rel_l2(to_np(p)[s], to_np(p0)[s]) <= (1e-5 if prec == "fp32" else 1e-11)
+
+
+def test_row_api_errors():
+    nat = _nat()
+    M = 300
+    m, geo, mesh, gg, y, n, tri = _system_case(M)
+    eps, w = nat.mc_weights(geo["total_area"], M)
+    smp = torch.from_numpy(np.ascontiguousarray(np.concatenate([y.T, n.T]))).cuda()
+    p = torch.ones(1, M, dtype=torch.complex128, device="cuda")
+    for r0, r1 in ((0, 0), (5, 3), (0, M + 1), (-1, 10)):
+        with pytest.raises(nat.NatError, match="row range"):
+            nat.nat_mc_apply_rows(smp, [1.0], p, w, eps, r0, r1)
+    with pytest.raises(nat.NatError):
+        nat.nat_mc_apply_rows(smp, [1.0], p.cpu(), w, eps, 0, 10)     # host tensor
+    with pytest.raises(nat.NatError, match="M must be"):
+        nat.nat_mc_surface_pressure_sharded(mesh, gg, [1.0], torch.ones(1, m.n_tri, dtype=torch.complex128,
+                                                                         device="cuda"), 1)
