@@ -6,6 +6,7 @@
 The library links the NCCL shipped with torch's pip wheel (nvidia-nccl 2.28.x), not the
 system copy, so it shares one libnccl.so.2 with torch.distributed.
 """
+import concurrent.futures
 import glob
 import os
 import subprocess
@@ -47,14 +48,19 @@ def build(verbose=False, clean=False):
     flags = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
              "--expt-relaxed-constexpr", "-I", inc] + ARCH
     flags += os.environ.get("NAT_NVCC_EXTRA", "").split()   # tuning experiments only (-D...)
+    todo = []
     for s in srcs:
         o = os.path.join(BUILD, os.path.basename(s)[:-3] + ".o")
         objs.append(o)
         if not clean and os.path.exists(o) and os.path.getmtime(o) > max(os.path.getmtime(s), hdr_mtime):
             continue
-        out = _run([NVCC] + flags + ["-c", s, "-o", o])
-        if verbose:
-            print(out)
+        todo.append([NVCC] + flags + ["-c", s, "-o", o])
+    # one nvcc per translation unit, in parallel (bem.cu dominates the serial build time)
+    jobs = max(1, min(len(todo), int(os.environ.get("NAT_BUILD_JOBS", os.cpu_count() or 1))))
+    with concurrent.futures.ThreadPoolExecutor(jobs) as ex:
+        for out in ex.map(_run, todo):
+            if verbose:
+                print(out)
     lib_needs = clean or not os.path.exists(LIB) or any(os.path.getmtime(o) > os.path.getmtime(LIB) for o in objs)
     if lib_needs:
         _run([NVCC] + ARCH + ["-shared", "-o", LIB + ".tmp"] + objs +
