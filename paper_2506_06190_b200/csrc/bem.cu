@@ -35,7 +35,10 @@ namespace cg = cooperative_groups;
 using nat::C2;
 
 constexpr int kThreads = 256;
-constexpr int kTI = 16;       // rows per far CTA
+#ifndef NAT_FAR_TI
+#define NAT_FAR_TI 16          // rows per far CTA (tuning)
+#endif
+constexpr int kTI = NAT_FAR_TI;  // rows per far CTA
 #ifndef NAT_FAR_UNROLL
 #define NAT_FAR_UNROLL 1       // column passes interleaved by the packed far kernel (tuning)
 #endif
@@ -46,7 +49,10 @@ constexpr int kFarUnroll = NAT_FAR_UNROLL;
 constexpr int kFarMinBlocks = NAT_FAR_MINB;
 constexpr int kTI64 = 4;      // rows per CTA of the fp64 far kernel (16 unrolled fp64 rows -> 238
                               // registers, 8 warps/SM; ncu r01 matrix-free C5 capture)
-constexpr int kCC = 8;        // column passes per far CTA (columns = 256 * kCC)
+#ifndef NAT_FAR_CC
+#define NAT_FAR_CC 16          // column passes per far CTA (tuning; A/B profiles/r01_ab_far_cc.txt)
+#endif
+constexpr int kCC = NAT_FAR_CC;  // column passes per far CTA (columns = 256 * kCC)
 constexpr int kMaxFarQ = 7;
 constexpr int kNRmax = 2;
 
