@@ -13,7 +13,9 @@ rounds every operation) so that the integer decisions that depend on these value
   c   = ((v1 + v2) + v3) / 3
   diam = longest edge, each length sqrt((d_x*d_x + d_y*d_y) + d_z*d_z)
   cdf  = sequential prefix sum of area (np.cumsum),  |Gamma| = cdf[-1]
-  centre = sum_t A_t c_t / |Gamma|,  R = max_vertices |v - centre|
+  centre = sum_t A_t c_t / |Gamma|, each sum sequential left to right over t (the
+           definition's order, as for the cdf; np.cumsum is that sequential accumulate),
+  R = max_vertices sqrt((dx*dx + dy*dy) + dz*dz),  d = v - centre
 Validation: every area > 0; signed volume sum_t v1.(v2 x v3)/6 > 0 (outward).
 Pinned by tests/test_oracle_geometry.py (sphere area/volume convergence, hand triangle,
 closed-surface identity sum A n = 0).
@@ -50,7 +52,9 @@ def mesh_prepare(v, t):
         raise ValueError("mesh is not outward-oriented (signed volume <= 0)")
     cdf = np.cumsum(area)
     total = float(cdf[-1])
-    centre = np.sum(area[:, None] * centroid, axis=0) / total
-    R = float(np.max(np.sqrt(np.sum((v - centre) ** 2, axis=1))))
+    ac = area[:, None] * centroid
+    centre = np.array([np.cumsum(ac[:, d])[-1] for d in range(3)]) / total
+    dv = v - centre[None, :]
+    R = float(np.max(_norm(dv)))
     return dict(centroid=centroid, normal=normal, area=area, diam=diam, cdf=cdf,
                 total_area=total, center=centre, bound_radius=R, volume=float(vol))

@@ -56,14 +56,13 @@ def cell_index(y, origin, h, n):
     return np.clip(q, 0, n - 1)
 
 
-def sample(v, t, geom, M_target, seed, stream_id=0, r=None, order=None, frame=None):
+def sample(v, t, geom, M_target, seed, stream_id=0, r=None, order=None):
     """Returns (y (M,3), n (M,3), tri (M,), cand (M,) candidate indices, r).
-    order: optional np.random.Generator shuffling the in-phase cell order (test only);
-    frame: optional (centre, R) of the cell grid (default geom's centre / bounding radius)."""
+    order: optional np.random.Generator shuffling the in-phase cell order (test only)."""
     r = default_radius(geom["total_area"], M_target) if r is None or r <= 0 else float(r)
     n_cand = N_CAND_PER_TARGET * M_target
     y, nrm, tri = mc.sample_uniform(v, t, geom, n_cand, seed, stream_id, tag=2)
-    centre, R = frame if frame is not None else (geom["center"], geom["bound_radius"])
+    centre, R = geom["center"], geom["bound_radius"]
     h, n, origin = grid_of(centre, R, r)
     ijk = cell_index(y, origin, h, n)
     key = (ijk[:, 2] * n + ijk[:, 1]) * n + ijk[:, 0]

@@ -92,44 +92,72 @@ __global__ void __launch_bounds__(1024) cdf_kernel(int64_t nt, const double* __r
 
 constexpr int RB = 1024;
 
-// One block: deterministic tree reductions of sum(A c), sum(vol_term).
+// One block.  centre = sum_t A_t c_t / |Gamma| with the sums taken sequentially, left to
+// right, every product and sum rounded (no FMA): the definition's order, so the result is
+// bit-identical with the oracle (which accumulates the same products with np.cumsum).
+// The block stages RB products per component in shared memory; lane 0 of warps 0..2 runs
+// the dependent chain of component 0..2 (8 loads, then 8 adds, per step).  The signed
+// volume only decides the orientation check (tree sum; any order).
 __global__ void __launch_bounds__(RB) centre_kernel(int64_t nt, const double* __restrict__ area,
                                                     const double* __restrict__ cen,
                                                     const double* __restrict__ vol_term,
                                                     const double* __restrict__ cdf, PrepScalars* sc) {
-  __shared__ double red[4][RB];
-  double s[4] = {0, 0, 0, 0};
-  for (int64_t t = threadIdx.x; t < nt; t += RB) {
-    double a = area[t];
-    s[0] += a * cen[t];
-    s[1] += a * cen[nt + t];
-    s[2] += a * cen[2 * nt + t];
-    s[3] += vol_term[t];
-  }
-  for (int q = 0; q < 4; ++q) red[q][threadIdx.x] = s[q];
-  __syncthreads();
-  for (int w = RB / 2; w > 0; w >>= 1) {
-    if (threadIdx.x < w)
-      for (int q = 0; q < 4; ++q) red[q][threadIdx.x] += red[q][threadIdx.x + w];
+  __shared__ double prod[3][RB];
+  __shared__ double red[RB];
+  double acc = 0.0, vol = 0.0;  // acc: the chain of component (warp id) in lane 0 of warps 0..2
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int64_t c0 = 0; c0 < nt; c0 += RB) {
+    const int len = (int)nat::min64(RB, nt - c0);
+    if (threadIdx.x < len) {
+      const int64_t t = c0 + threadIdx.x;
+      const double a = area[t];
+      prod[0][threadIdx.x] = __dmul_rn(a, cen[t]);
+      prod[1][threadIdx.x] = __dmul_rn(a, cen[nt + t]);
+      prod[2][threadIdx.x] = __dmul_rn(a, cen[2 * nt + t]);
+      vol += vol_term[t];
+    }
+    __syncthreads();
+    if (warp < 3 && lane == 0) {
+      const double* pd = prod[warp];
+      for (int t = 0; t < len; t += 8) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = t + u < len ? pd[t + u] : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (t + u < len) acc = __dadd_rn(acc, v[u]);
+      }
+    }
     __syncthreads();
   }
+  red[threadIdx.x] = vol;
+  __syncthreads();
+  for (int w = RB / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  const double tot = cdf[nt - 1];
+  if (warp < 3 && lane == 0) {
+    const double c = __ddiv_rn(acc, tot);
+    if (warp == 0) sc->cx = c;
+    if (warp == 1) sc->cy = c;
+    if (warp == 2) sc->cz = c;
+  }
   if (threadIdx.x == 0) {
-    double tot = cdf[nt - 1];
     sc->total_area = tot;
-    sc->cx = red[0][0] / tot;
-    sc->cy = red[1][0] / tot;
-    sc->cz = red[2][0] / tot;
-    sc->volume = red[3][0] / 6.0;
+    sc->volume = red[0] / 6.0;
   }
 }
 
+// R = max over vertices of |v - centre|, each distance sqrt((dx dx + dy dy) + dz dz) with
+// every operation rounded (the oracle's order); max is order-free.
 __global__ void __launch_bounds__(RB) radius_kernel(int64_t nv, const double* __restrict__ vx,
                                                     PrepScalars* sc) {
   __shared__ double red[RB];
   double cx = sc->cx, cy = sc->cy, cz = sc->cz, m = 0.0;
   for (int64_t v = threadIdx.x; v < nv; v += RB) {
-    double dx = vx[v] - cx, dy = vx[nv + v] - cy, dz = vx[2 * nv + v] - cz;
-    m = fmax(m, sqrt(dx * dx + dy * dy + dz * dz));
+    const double dx = __dsub_rn(vx[v], cx), dy = __dsub_rn(vx[nv + v], cy), dz = __dsub_rn(vx[2 * nv + v], cz);
+    m = fmax(m, dnorm_rn(dx, dy, dz));
   }
   red[threadIdx.x] = m;
   __syncthreads();

@@ -29,8 +29,8 @@ def test_mesh_prepare_bitwise(name):
         assert np.array_equal(to_np(getattr(geo, key)), ref[key]), key
     assert np.array_equal(to_np(geo.area_cdf), ref["cdf"])       # sequential order
     assert geo.total_area == ref["total_area"]
-    np.testing.assert_allclose(geo.center, ref["center"], rtol=0, atol=1e-14 * ref["bound_radius"])
-    assert abs(geo.bound_radius - ref["bound_radius"]) <= 1e-14 * ref["bound_radius"]
+    assert tuple(geo.center) == tuple(ref["center"])          # sequential sums, every op rounded
+    assert geo.bound_radius == ref["bound_radius"]
     assert abs(geo.volume - ref["volume"]) <= 1e-12 * abs(ref["volume"])
 
 

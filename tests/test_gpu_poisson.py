@@ -30,8 +30,8 @@ def test_poisson_bitwise(name, M, seed, sid):
     m = {"ico3": lambda: I.icosphere(3), "bowl": lambda: I.bowl(48, 12, 2), "cube": lambda: I.cubed_sphere(4)}[name]()
     geo, mesh, gg = _case(m)
     smp, stri, r = nat.nat_mc_poisson_sample(mesh, gg, M, seed=seed, stream_id=sid)
-    # the grid frame is an input of the step: the oracle uses the GPU's centre / radius
-    y, n, tri, cand, r_o = poisson.sample(m.v, m.t, geo, M, seed, sid, frame=(np.array(gg.center), gg.bound_radius))
+    # the oracle uses its own a1 frame (centre and radius are bit-identical, test_gpu_geometry)
+    y, n, tri, cand, r_o = poisson.sample(m.v, m.t, geo, M, seed, sid)
     assert r == r_o
     assert np.array_equal(to_np(stri), tri)
     x = soa_to_aos(smp[:3])

@@ -50,3 +50,20 @@ def test_bowl_volume_and_centre():
     exact = 2 / 3 * math.pi * (1 - 0.9 ** 3)
     assert abs(g["volume"] - exact) / exact < 5e-3
     assert abs(g["center"][0]) < 1e-12 and abs(g["center"][1]) < 1e-12
+
+
+def test_centre_is_the_area_weighted_surface_centroid():
+    """centre = sum A_t c_t / |Gamma| (R-geom): a box's centre is its centre (exact up to
+    rounding) and R its half diagonal; the thick bowl's centre converges O(h^2) to the
+    analytic surface centroid z = (2 pi (-1/2) + 2 pi 0.81 (-0.45)) / (3.81 pi) (outer and
+    inner hemispherical surfaces, rim annulus at z = 0)."""
+    m = I.slab(0.4, 0.3, 0.2, 4, 3, 2, centre=(0.1, -0.2, 0.3))
+    g = geometry.mesh_prepare(m.v, m.t)
+    np.testing.assert_allclose(g["center"], [0.1, -0.2, 0.3], rtol=0, atol=2e-16)
+    assert abs(g["bound_radius"] - math.sqrt(0.2 ** 2 + 0.15 ** 2 + 0.1 ** 2)) < 2e-16
+    exact = -1.729 / 3.81
+    errs = []
+    for n_az, n_psi in ((32, 8), (64, 16), (128, 32)):
+        z = geometry.mesh_prepare(*(lambda b: (b.v, b.t))(I.bowl(n_az, n_psi, 2)))["center"][2]
+        errs.append(abs(z - exact))
+    assert errs[0] / errs[1] > 3.5 and errs[1] / errs[2] > 3.5 and errs[2] < 2e-4
