@@ -62,9 +62,15 @@ const char* nat_last_error(void);
  * nat_kernel_timer_read synchronises the recorded events and returns, for one category,
  * the summed kernel time, the algorithmic pair-evaluations of those launches and their
  * count (launches that returned at once because GMRES had already converged are not
- * counted).  [host] outputs. */
+ * counted).  Pairs are pair-evaluations x wavenumbers.  nat_kernel_timer_read_modes returns
+ * the same totals restricted to the launches that evaluated n_modes wavenumbers per pair
+ * (1..64; 0 = every launch, = nat_kernel_timer_read), for per-launch rooflines whose
+ * shared work (r, 1/r, d.n) is amortised over n_modes.  [host] outputs;
+ * NAT_ERR_INVALID_ARG for a category or n_modes out of range. */
 void nat_kernel_timer_enable(int on);
 nat_status nat_kernel_timer_read(int category, double* seconds, double* pairs, int64_t* launches);
+nat_status nat_kernel_timer_read_modes(int category, int n_modes, double* seconds, double* pairs,
+                                       int64_t* launches);
 
 /* ---------------------------------------------------------------------------------
  * a1 — mesh preparation ("construct the scene and obtain its surface triangle

@@ -433,6 +433,19 @@ struct HostSync {
   unsigned long long* ring_dev = nullptr;  // its device alias
   cudaEvent_t ev[kRing] = {};
   std::vector<cudaEvent_t> timing[2];
+  HostSync() = default;
+  HostSync(const HostSync&) = delete;
+  HostSync& operator=(const HostSync&) = delete;
+  // released when the owning thread exits (worker threads of a sweep come and go);
+  // errors at process teardown (context already gone) are ignored
+  ~HostSync() {
+    if (ring) cudaFreeHost(ring);
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+    for (auto& v : timing)
+      for (auto& e : v) cudaEventDestroy(e);
+    cudaGetLastError();
+  }
 };
 
 HostSync* host_sync() {

@@ -44,7 +44,8 @@ int device_sm_count();
 enum { kTimerMcOp = 0, kTimerMcRhs = 1, kTimerRadiate = 2, kTimerFar = 3, kTimerCats = 4 };
 bool ktimer_on();
 void ktimer_begin(int cat, cudaStream_t s);
-void ktimer_end(int cat, cudaStream_t s, double pairs, const unsigned long long* skip);
+// n_modes: wavenumbers evaluated per pair by the launch (roofline bucket; 0 = none)
+void ktimer_end(int cat, cudaStream_t s, double pairs, const unsigned long long* skip, int n_modes = 0);
 
 // Exclusive scan of one int64 per thread over a 1024-thread block (warp shuffles, exact);
 // sh: 33 int64 of shared memory; *total (optional) receives the block sum.

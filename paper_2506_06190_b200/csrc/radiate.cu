@@ -118,7 +118,8 @@ __global__ void __launch_bounds__(kStageSrc) stage_kernel(int64_t n_src, int64_t
     ny = nz = 0.0;
     ws = 0.0;
   }
-  for (int c = 0; c < n_mchunk; ++c) {
+  // one mode chunk per blockIdx.y (MC shapes: 16 source blocks x up to 64 chunks)
+  for (int c = blockIdx.y; c < n_mchunk; c += gridDim.y) {
     if (threadIdx.x < nblk) {
       T* r = sm + (size_t)threadIdx.x * NF;
       const RecWriter<T, DUP> wr{r};
@@ -759,7 +760,7 @@ nat_status radiate_internal(const RadInput& in, nat_prec prec, const double* k, 
     }
     const double2* p = in.p ? in.p + (size_t)m0 * in.ldpg : nullptr;
     const double2* g = in.g ? in.g + (size_t)m0 * in.ldpg : nullptr;
-    unsigned sblocks = (unsigned)((pl.n_src_pad + kStageSrc - 1) / kStageSrc);
+    const dim3 sblocks((unsigned)((pl.n_src_pad + kStageSrc - 1) / kStageSrc), (unsigned)pl.n_mchunk);
     if (pl.fp64)
       stage_kernel<double><<<sblocks, kStageSrc, 0, s>>>(in.n_src, pl.n_src_pad, pl.NF, pl.MB, pl.n_mchunk, 0,
           in.xyz, in.nrm, in.w, in.w_const, p, g, in.ldpg, kv, nm, in.center[0], in.center[1],
@@ -803,7 +804,7 @@ nat_status radiate_internal(const RadInput& in, nat_prec prec, const double* k, 
     }
     if (e != cudaSuccess) return fail(NAT_ERR_CUDA, "radiate launch: %s", cudaGetErrorString(e));
     if (timed)  // algorithmic pairs: the self kinds skip the diagonal
-      ktimer_end(tcat, s, (double)nm * (double)n_lis * (double)(self ? in.n_src - 1 : in.n_src), in.skip);
+      ktimer_end(tcat, s, (double)nm * (double)n_lis * (double)(self ? in.n_src - 1 : in.n_src), in.skip, nm);
     if (keep) {  // the caller reduces the partials in its own epilogue
       keep->part = pl.n_split > 1 ? part : dst;
       keep->n_split = pl.n_split;

@@ -98,6 +98,7 @@ _SIGS = {
                                    _P]),
     "nat_kernel_timer_enable": (None, [C.c_int]),
     "nat_kernel_timer_read": (C.c_int, [C.c_int, C.POINTER(_D), C.POINTER(_D), C.POINTER(_I64)]),
+    "nat_kernel_timer_read_modes": (C.c_int, [C.c_int, C.c_int, C.POINTER(_D), C.POINTER(_D), C.POINTER(_I64)]),
     "nat_comm_unique_id": (C.c_int, [_P]),
     "nat_comm_create_from_id": (C.c_int, [C.POINTER(_P), _P, C.c_int, C.c_int]),
     "nat_comm_create": (C.c_int, [C.POINTER(_P), _P, C.c_int, C.c_int]),
@@ -283,9 +284,9 @@ def nat_mesh_prepare(mesh: Mesh) -> Geom:
     return geo
 
 
-def nat_listener_grid(center, R, n_theta, n_phi, n_r, r_lo=1.5, r_hi=3.0, device="cuda"):
+def nat_listener_grid(center, R, n_theta, n_phi, n_r, r_lo=1.5, r_hi=3.0, device="cuda", out=None):
     n = n_theta * n_phi * n_r
-    out = torch.empty(3, n, dtype=torch.float64, device=device)
+    out = torch.empty(3, n, dtype=torch.float64, device=device) if out is None else out
     c = (C.c_double * 3)(*[float(x) for x in center])
     _check(lib().nat_listener_grid(c, float(R), n_theta, n_phi, n_r, float(r_lo), float(r_hi),
                                    _ptr(out), _stream()))
@@ -752,8 +753,9 @@ def nat_kernel_timer_enable(on: bool = True):
     lib().nat_kernel_timer_enable(int(bool(on)))
 
 
-def nat_kernel_timer_read(category: int):
-    """(seconds, pair-evaluations, launches) of the category's main kernel since enable."""
+def nat_kernel_timer_read(category: int, n_modes: int = 0):
+    """(seconds, pair-evaluations x wavenumbers, launches) of the category's main kernel
+    since enable; n_modes > 0: only the launches with that many wavenumbers per pair."""
     sec, pairs, n = C.c_double(0.0), C.c_double(0.0), C.c_int64(0)
-    _check(lib().nat_kernel_timer_read(int(category), C.byref(sec), C.byref(pairs), C.byref(n)))
+    _check(lib().nat_kernel_timer_read_modes(int(category), int(n_modes), C.byref(sec), C.byref(pairs), C.byref(n)))
     return sec.value, pairs.value, n.value

@@ -24,6 +24,8 @@ def test_kernel_timer_counts_mc_operator_and_far_launches():
     sec, pairs, n = nat.nat_kernel_timer_read(nat.KTIMER_MC_OP)
     assert n == infos[0]["iters"] and sec > 0
     assert pairs == n * M * (M - 1)
+    assert nat.nat_kernel_timer_read(nat.KTIMER_MC_OP, 1) == (sec, pairs, n)   # one wavenumber per launch
+    assert nat.nat_kernel_timer_read(nat.KTIMER_MC_OP, 2)[2] == 0
     sec, pairs, n = nat.nat_kernel_timer_read(nat.KTIMER_MC_RHS)
     assert n == 1 and pairs == M * (M - 1)
     sec, pairs, n = nat.nat_kernel_timer_read(nat.KTIMER_FAR)

@@ -73,11 +73,13 @@ def _shard_fn(rank, world):
     import sys
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     import bench
+    import bench_secondary
     from paper_2506_06190_b200.nat import row_range
     res = {}
     for n in (1, 7, 1280, 20480, 199692):
-        res[n] = (row_range(n, rank, world), bench.shard(n, rank, world))
-    res["mc"] = bench.mc_share(3, rank, world)
+        res[n] = (row_range(n, rank, world), bench_secondary.shard(n, rank, world))
+    res["mc"] = bench_secondary.mc_share(3, rank, world)
+    res["geo"] = bench.geo_share(64, rank, world)
     return res
 
 
@@ -92,6 +94,9 @@ def test_row_listener_and_wavenumber_sharding_tile_exactly():
         assert all(a == min(n, r * rpr) for r, (a, b) in enumerate(rows))
     ks = sorted(sum((out[r]["mc"] for r in range(WORLD)), []))
     assert ks == [0, 1, 2]
+    # C4: every geometry on exactly one rank, equal counts (64 / world)
+    geos = sorted(sum((out[r]["geo"] for r in range(WORLD)), []))
+    assert geos == list(range(64)) and len({len(out[r]["geo"]) for r in range(WORLD)}) == 1
 
 
 def _gmres_fn(rank, world):

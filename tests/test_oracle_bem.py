@@ -129,3 +129,30 @@ def test_interior_point_source_manufactured():
     assert np.linalg.norm(p - pe) / np.linalg.norm(pe) < 0.02
     pb = analytic.point_source(geo["centroid"], xs, k)
     assert np.linalg.norm(x - pb) / np.linalg.norm(pb) < 0.02
+
+
+def _thin_wall_case(n_az, n_psi, k=2.0):
+    """SURVEY §8(d) C3 acceptance (thin-wall sanity pin; the idea is P:398's analytic point
+    source): x_s = (0, 0, -0.95) inside the 0.1-thick wall of the bowl, g_t = dG(c_t, x_s)/dn_t;
+    the exterior field must approach G(x, x_s)."""
+    m = I.bowl(n_az, n_psi, 2)
+    geo = geometry.mesh_prepare(m.v, m.t)
+    xs = np.array([0.0, 0.0, -0.95])
+    g = analytic.point_source_dn(geo["centroid"], geo["normal"], xs, k)
+    A, b = bem.assemble(m.v, m.t, geo, k, g[None])
+    x, info = gmres.gmres(lambda z: A @ z, b[0], 1e-10, 400)
+    L = listeners.shell_grid(geo["center"], geo["bound_radius"], 8, 8, 4)
+    p = radiate.radiate(radiate.bem_sources(m.v, m.t, geo, x[None], g[None]), [k], L)[0]
+    pe = analytic.point_source(L, xs, k)
+    return np.linalg.norm(p - pe) / np.linalg.norm(pe)
+
+
+def test_thin_wall_point_source_converges():
+    """The source sits about one element from both faces of the wall, so P0 collocation is
+    far from its 2% sphere accuracy on coarse bowls; the pin is convergence: the field
+    error at 3,200 triangles is below 0.3 and below half of the 832-triangle error
+    (measured: 0.60 -> 0.26).  The 12,544-triangle case runs on the GPU
+    (tests/test_gpu_configs.py) with the tolerance set from these oracle errors."""
+    e0 = _thin_wall_case(32, 6)
+    e1 = _thin_wall_case(64, 12)
+    assert e1 < 0.3 and e1 < 0.5 * e0

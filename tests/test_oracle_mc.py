@@ -94,3 +94,50 @@ def test_pulsating_sphere_statistics():
     assert np.linalg.norm(f - pe) / np.linalg.norm(pe) < 0.05
     pb = analytic.pulsating_sphere(1.0, k)
     assert abs(np.mean(means) - pb) / abs(pb) < 0.10
+
+
+@pytest.mark.parametrize("M", [2, 5, 10])
+def test_weight_at_a_caller_eps_conserves_the_sampling_surface(M):
+    """Reading R-weight ("reduction in the sampling surface corresponding to the area
+    of the small disk"): the M - 1 off-disk weights and the disk area add up to |Gamma| for
+    any caller eps, and only the default eps gives |Gamma| / M."""
+    area = 3.7
+    for eps in (1e-3, 0.05, 0.3, mc.default_eps(area, M)):
+        w = mc.weight(area, M, eps)
+        assert abs(w * (M - 1) + math.pi * eps * eps - area) < 1e-14 * area
+    assert abs(mc.weight(area, M, 0.3) - area / M) > 1e-3
+
+
+@pytest.mark.parametrize("M,k,eps", [(3, 0.0, None), (7, 2.5, 0.11), (10, 6.0, 0.02)])
+def test_small_system_entries_brute_force(M, k, eps):
+    """M <= 10 hand systems: every entry against properties that do not reuse
+    the oracle's kernel formulas — A_ij (i != j) is -w times the central finite difference of
+    G(y_i, .) along n_j at y_j (pins the derivative, its sign and which normal enters);
+    with g = e_j, b_i = -w G(y_i, y_j) has modulus w / (4 pi r_ij) and phase k r_ij + pi,
+    and b_j = -(eps/2) (the disk term at the caller's eps); A_ii = 1/2."""
+    rng = np.random.default_rng(M)
+    d = rng.normal(size=(M, 3))
+    y = d / np.linalg.norm(d, axis=1, keepdims=True)
+    n = y.copy()
+    area = 4 * math.pi
+    e = mc.default_eps(area, M) if eps is None else eps
+    w = mc.weight(area, M, e)
+    for j in range(M):
+        g = np.zeros(M)
+        g[j] = 1.0
+        A, b = mc.system(y, n, g, k, area, eps)
+        assert A[j, j] == 0.5
+        assert abs(b[j] - (-0.5 * e)) < 1e-15
+        for i in range(M):
+            if i == j:
+                continue
+            h = 1e-5
+            gp = np.exp(1j * k * np.linalg.norm(y[j] + h * n[j] - y[i])) / (4 * math.pi * np.linalg.norm(y[j] + h * n[j] - y[i]))
+            gm = np.exp(1j * k * np.linalg.norm(y[j] - h * n[j] - y[i])) / (4 * math.pi * np.linalg.norm(y[j] - h * n[j] - y[i]))
+            fd = (gp - gm) / (2 * h)
+            assert abs(A[i, j] - (-w * fd)) < 1e-6 * max(1.0, abs(w * fd))   # O(h^2) FD error
+            r = np.linalg.norm(y[i] - y[j])
+            assert abs(abs(b[i]) - w / (4 * math.pi * r)) < 1e-14
+            if k > 0:
+                ph = (np.angle(b[i]) - (k * r + math.pi)) % (2 * math.pi)
+                assert min(ph, 2 * math.pi - ph) < 1e-12
