@@ -15,6 +15,8 @@
 #include <algorithm>
 #include <map>
 
+#include <cooperative_groups.h>
+
 #include "krylov.cuh"
 #include "nat_comm.cuh"
 
@@ -426,6 +428,226 @@ __global__ void combine_kernel(const double2* __restrict__ V, const double2* __r
   r[(size_t)s * ldv + i] = make_double2(bb.x - ax.x, bb.y - ax.y);
 }
 
+// ------------------------------------------------------------------------------------
+// Fused Arnoldi step for short vectors (n <= kFusedMaxN; the MC systems, M = 2048-10,000):
+// one thread-block cluster of kCL CTAs per system runs the whole CGS2 iteration after the
+// operator product — both projection passes (dots + update), the norm, the Givens step of
+// the system and the scaling of the new basis vector — in ONE launch.  CTA c owns rows
+// [c rpc, (c+1) rpc) of the system; the per-CTA partial dot products are exchanged through
+// distributed shared memory and summed by every CTA in CTA order (deterministic, the same
+// in every CTA).  A cluster touches its system's basis slice four times within a few
+// microseconds, so three of the four passes hit L2 (the multi-kernel path streams the
+// whole batched basis from HBM in every pass).  Requesting kFusedSmem bytes of shared
+// memory caps residency at one CTA per SM, which keeps the basis slices of the clusters in
+// flight (~18 systems) inside the 126 MB L2.
+// ------------------------------------------------------------------------------------
+constexpr int kCL = 8;                         // CTAs per system (portable cluster size)
+constexpr int kFusedMaxRT = 8;                 // rows per thread
+constexpr int64_t kFusedMaxN = (int64_t)kCL * kT * kFusedMaxRT;
+constexpr int kFusedSmem = 120 * 1024;         // residency cap (1 CTA / SM)
+
+__global__ void publish_mask_kernel(const unsigned long long* __restrict__ mask, volatile unsigned long long* out) {
+  *out = *mask;
+  __threadfence_system();
+}
+
+// Threads: NTH = KG x 256.  Dots: NTH / 32 warps, each two basis vectors at a time (16
+// loads of 16 B in flight per lane).  Update: group g (256 threads, RT rows each) sums the
+// basis vectors k = g, g + KG, ... in ascending order; group 0 adds the KG partial sums in
+// group order (deterministic) and keeps w in registers.
+template <int RT, int NTH>
+__global__ void __cluster_dims__(kCL, 1, 1) __launch_bounds__(NTH, 1)
+    arnoldi_fused_kernel(const double2* __restrict__ V, size_t vstride, int64_t ldv, int64_t n, int64_t rpc,
+                         const double2* __restrict__ Wj, double2* __restrict__ Vnext, uint64_t active,
+                         GivensArgs ga) {
+  namespace cg = cooperative_groups;
+  constexpr int KG = NTH / kT, NW = NTH / 32;
+  // [rpc] w | [2][mp1] partials | [mp1] h | [mp1] pass-1 coefficients | [KG-1][rpc] update partials
+  extern __shared__ __align__(16) double2 fsm[];
+  __shared__ double red[kT / 32];
+  __shared__ double nrm_part, nrm_all;
+  cg::cluster_group cl = cg::this_cluster();
+  const int s = blockIdx.y;
+  const int c = (int)cl.block_rank();
+  const int j = ga.j, mp1 = ga.mp1, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int grp = tid / kT, tr = tid % kT;
+  // whole clusters skip (the mask bit of system s only changes in the Givens step after this)
+  if (!sys_on(active, ga.mask, s)) return;
+  double2* wsh = fsm;
+  double2* hp = fsm + rpc;         // [2][mp1]
+  double2* hs = hp + 2 * mp1;      // [mp1]
+  double2* hc1 = hs + mp1;         // [mp1]
+  double2* upd = hc1 + mp1;        // [KG-1][rpc]
+  const int64_t r0 = (int64_t)c * rpc;
+  const int rows = (int)max((int64_t)0, min(rpc, n - r0));
+  const double2* Vs = V + (size_t)s * ldv + r0;
+  double2 w[RT];
+  if (grp == 0) {
+#pragma unroll
+    for (int q = 0; q < RT; ++q) {
+      const int r = tr + q * kT;
+      w[q] = r < rows ? Wj[(size_t)s * ldv + r0 + r] : make_double2(0.0, 0.0);
+      if (r < rows) wsh[r] = w[q];
+    }
+  }
+  __syncthreads();
+  for (int pass = 0; pass < 2; ++pass) {
+    double2* part = hp + pass * mp1;
+    for (int k = warp; k <= j; k += 2 * NW) {
+      const int k2 = k + NW;
+      const double2* vk = Vs + (size_t)k * vstride;
+      const double2* vk2 = Vs + (size_t)(k2 <= j ? k2 : k) * vstride;
+      double ax = 0.0, ay = 0.0, bx = 0.0, by = 0.0;
+      for (int r0l = 0; r0l < rows; r0l += 32 * 8) {
+        double2 v[8], v2[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int r = r0l + q * 32 + lane;
+          v[q] = r < rows ? __ldcg(&vk[r]) : make_double2(0.0, 0.0);
+          v2[q] = r < rows ? __ldcg(&vk2[r]) : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int r = r0l + q * 32 + lane;
+          const double2 u = r < rows ? wsh[r] : make_double2(0.0, 0.0);
+          ax += v[q].x * u.x + v[q].y * u.y;
+          ay += v[q].x * u.y - v[q].y * u.x;
+          bx += v2[q].x * u.x + v2[q].y * u.y;
+          by += v2[q].x * u.y - v2[q].y * u.x;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        ax += __shfl_xor_sync(0xffffffffu, ax, o);
+        ay += __shfl_xor_sync(0xffffffffu, ay, o);
+        bx += __shfl_xor_sync(0xffffffffu, bx, o);
+        by += __shfl_xor_sync(0xffffffffu, by, o);
+      }
+      if (lane == 0) {
+        part[k] = make_double2(ax, ay);
+        if (k2 <= j) part[k2] = make_double2(bx, by);
+      }
+    }
+    cl.sync();
+    // this pass's coefficients = sum over the cluster's CTAs in rank order (the same in
+    // every CTA); pass 0 keeps them in hp[1] (its partial slot is free until pass 1)
+    double2* hc = pass == 0 ? hp + mp1 : hc1;
+    for (int k = tid; k <= j; k += NTH) {
+      double2 t = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int q = 0; q < kCL; ++q) {
+        const double2 p = cl.map_shared_rank(part, q)[k];
+        t.x += p.x;
+        t.y += p.y;
+      }
+      hs[k] = pass == 0 ? t : make_double2(hs[k].x + t.x, hs[k].y + t.y);
+      hc[k] = t;
+    }
+    __syncthreads();
+    // w_i -= sum_k hc[k] V_k[i]: group g takes k = g, g + KG, ... (8 loads in flight)
+#pragma unroll
+    for (int q = 0; q < RT; ++q) {
+      const int r = tr + q * kT;
+      if (r >= rows) continue;
+      double2 acc = make_double2(0.0, 0.0);
+      const double2* vi = Vs + r;
+      for (int k0 = grp; k0 <= j; k0 += 8 * KG) {
+        double2 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int k = k0 + u * KG;
+          v[u] = k <= j ? __ldcg(&vi[(size_t)k * vstride]) : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int k = k0 + u * KG;
+          const double2 cc = k <= j ? hc[k] : make_double2(0.0, 0.0);
+          acc.x += cc.x * v[u].x - cc.y * v[u].y;
+          acc.y += cc.x * v[u].y + cc.y * v[u].x;
+        }
+      }
+      if (grp > 0) upd[(size_t)(grp - 1) * rpc + r] = acc;
+      else w[q] = acc;  // group 0's partial, combined below
+    }
+    __syncthreads();
+    if (grp == 0) {
+#pragma unroll
+      for (int q = 0; q < RT; ++q) {
+        const int r = tr + q * kT;
+        if (r >= rows) continue;
+        double2 acc = w[q];
+#pragma unroll
+        for (int g = 1; g < KG; ++g) {
+          const double2 u = upd[(size_t)(g - 1) * rpc + r];
+          acc.x += u.x;
+          acc.y += u.y;
+        }
+        const double2 wo = wsh[r];
+        w[q] = make_double2(wo.x - acc.x, wo.y - acc.y);
+      }
+    }
+    if (pass == 0) {
+      // pass 1 writes its partials into hp[1] (which held the pass-0 coefficients) only
+      // after every CTA of the cluster is done with its pass-0 update
+      cl.sync();
+      if (grp == 0) {
+#pragma unroll
+        for (int q = 0; q < RT; ++q) {
+          const int r = tr + q * kT;
+          if (r < rows) wsh[r] = w[q];
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // ||w||^2: group-0 partial, cluster sum in rank order
+  if (grp == 0) {
+    double t = 0.0;
+#pragma unroll
+    for (int q = 0; q < RT; ++q) t += w[q].x * w[q].x + w[q].y * w[q].y;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (lane == 0) red[warp] = t;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double b = 0.0;
+    for (int q = 0; q < kT / 32; ++q) b += red[q];
+    nrm_part = b;
+  }
+  cl.sync();
+  if (tid == 0) {
+    double a = 0.0;
+    for (int q = 0; q < kCL; ++q) a += *cl.map_shared_rank(&nrm_part, q);
+    nrm_all = sqrt(a);
+  }
+  __syncthreads();
+  const double nv = nrm_all;
+  if (grp == 0) {  // V_{j+1} = w / ||w|| (zero on breakdown, as scale_kernel)
+#pragma unroll
+    for (int q = 0; q < RT; ++q) {
+      const int r = tr + q * kT;
+      if (r < rows)
+        Vnext[(size_t)s * ldv + r0 + r] = nv > 0 ? make_double2(w[q].x / nv, w[q].y / nv) : make_double2(0.0, 0.0);
+    }
+  }
+  if (c == 0) {  // the Hessenberg column of system s (its Givens step: givens_kernel)
+    double2* hq = const_cast<double2*>(ga.h) + (size_t)s * ga.mp2;
+    for (int k = tid; k <= j; k += NTH) hq[k] = hs[k];
+    if (tid == 0) hq[j + 1] = make_double2(nv, 0.0);
+  }
+  cl.sync();  // no CTA exits while another may still read its shared memory
+}
+
+// The Givens steps of every active system in parallel (one warp each), after the fused
+// Arnoldi step; the sequential rotation chain of one system no longer holds a cluster.
+__global__ void __launch_bounds__(32) givens_kernel(uint64_t active, GivensArgs ga) {
+  extern __shared__ __align__(16) double2 gsm2[];
+  const int s = blockIdx.x;
+  if (!sys_on(active, ga.mask, s)) return;
+  givens_block(ga, s, gsm2);
+}
+
 // Per-thread, per-device host resources: a pinned ring for the convergence mask and
 // its events, plus reusable timing events.
 struct HostSync {
@@ -533,6 +755,31 @@ nat_status gmres_batched(int nsys, int64_t n, int64_t ldv, const double2* b, dou
   NAT_LAUNCH_CHECK();
 
   GivensArgs ga{0, m, mp1, mp2, tol, ws.h, ws.H, ws.cs, ws.sn, ws.gam, ws.sys, ws.mask};
+  // fused Arnoldi step (one cluster launch per iteration) for short vectors; NAT_GMRES_FUSED=0
+  // selects the multi-kernel path (A/B comparisons)
+  static const bool fused_env = [] {
+    const char* e = std::getenv("NAT_GMRES_FUSED");
+    return !(e && e[0] == '0');
+  }();
+  const bool fused = fused_env && n <= kFusedMaxN;
+  const int64_t rpc = (n + kCL - 1) / kCL;
+  const int need_rt = (int)((rpc + kT - 1) / kT);
+  const int fused_rt = need_rt <= 1 ? 1 : need_rt <= 2 ? 2 : need_rt <= 4 ? 4 : 8;
+  static const size_t fused_cap = [] {  // NAT_FUSED_SMEM_KB: residency cap (tuning A/B only)
+    const char* e = std::getenv("NAT_FUSED_SMEM_KB");
+    return e ? (size_t)std::atoi(e) * 1024 : (size_t)kFusedSmem;
+  }();
+  const int fused_kg = fused_rt <= 2 ? 3 : 2;  // update groups (NTH / 256)
+  const size_t fsmem = std::max(fused_cap, sizeof(double2) * ((size_t)rpc * fused_kg + 4 * (size_t)mp1));
+  if (fused) {
+    if (fsmem > (size_t)kBackSmemMax) return fail(NAT_ERR_INVALID_ARG, "max_iter %d too large", m);
+    if (gsmem > 48 * 1024)
+      NAT_CUDA_TRY(cudaFuncSetAttribute(givens_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsmem));
+    auto set = [&](const void* f) { return cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem); };
+    NAT_CUDA_TRY(fused_rt == 1 ? set((const void*)arnoldi_fused_kernel<1, 768>)
+                 : fused_rt == 2 ? set((const void*)arnoldi_fused_kernel<2, 768>)
+                 : fused_rt == 4 ? set((const void*)arnoldi_fused_kernel<4, 512>) : set((const void*)arnoldi_fused_kernel<8, 512>));
+  }
   int n_timed = 0;
   auto enqueue = [&](int j, uint64_t host_active) -> nat_status {
     double2* Vj = ws.V + (size_t)j * vstride;
@@ -549,17 +796,33 @@ nat_status gmres_batched(int nsys, int64_t n, int64_t ldv, const double2* b, dou
       nat_status stt = op(Vj, Wj, host_active, ws.mask, s);
       if (stt != NAT_OK) return stt;
     }
-    for (int pass = 0; pass < 2; ++pass) {  // CGS2 (w = W_j minus its projections); pass 1 also forms ||w||
-      const double2* win = pass == 0 ? Wj : ws.w;
-      dots(ws.V, vstride, win, j + 1, ws.mask, pass, 0);
-      ga.j = j;
-      update_kernel<<<dim3(gx, nsys), kT, pass == 1 ? gsmem : 0, s>>>(
-          ws.V, vstride, ldv, n, j + 1, mp2, all, ws.mask, ws.h2, win, ws.w, pass == 1 ? j + 1 : -1, ws.h,
-          ws.npart, ws.cnt + 64, pass == 1, ga);
+    ga.j = j;
+    if (fused) {  // short vectors: the whole CGS2 step in one cluster launch per iteration
+      const dim3 grid(kCL, nsys);
+      cudaError_t e = cudaSuccess;
+      switch (fused_rt) {
+        case 1: arnoldi_fused_kernel<1, 768><<<grid, 768, fsmem, s>>>(ws.V, vstride, ldv, n, rpc, Wj, ws.V + (size_t)(j + 1) * vstride, all, ga); break;
+        case 2: arnoldi_fused_kernel<2, 768><<<grid, 768, fsmem, s>>>(ws.V, vstride, ldv, n, rpc, Wj, ws.V + (size_t)(j + 1) * vstride, all, ga); break;
+        case 4: arnoldi_fused_kernel<4, 512><<<grid, 512, fsmem, s>>>(ws.V, vstride, ldv, n, rpc, Wj, ws.V + (size_t)(j + 1) * vstride, all, ga); break;
+        default: arnoldi_fused_kernel<8, 512><<<grid, 512, fsmem, s>>>(ws.V, vstride, ldv, n, rpc, Wj, ws.V + (size_t)(j + 1) * vstride, all, ga); break;
+      }
+      e = cudaGetLastError();
+      if (e != cudaSuccess) return fail(NAT_ERR_CUDA, "fused Arnoldi launch: %s", cudaGetErrorString(e));
+      givens_kernel<<<nsys, 32, gsmem, s>>>(all, ga);
+      publish_mask_kernel<<<1, 1, 0, s>>>(ws.mask, hs->ring_dev + j % kRing);
+      NAT_LAUNCH_CHECK();
+    } else {
+      for (int pass = 0; pass < 2; ++pass) {  // CGS2 (w = W_j minus its projections); pass 1 also forms ||w||
+        const double2* win = pass == 0 ? Wj : ws.w;
+        dots(ws.V, vstride, win, j + 1, ws.mask, pass, 0);
+        update_kernel<<<dim3(gx, nsys), kT, pass == 1 ? gsmem : 0, s>>>(
+            ws.V, vstride, ldv, n, j + 1, mp2, all, ws.mask, ws.h2, win, ws.w, pass == 1 ? j + 1 : -1, ws.h,
+            ws.npart, ws.cnt + 64, pass == 1, ga);
+      }
+      scale_kernel<<<dim3(gx, nsys), kT, 0, s>>>(ws.w, ldv, n, mp2, j + 1, all, ws.mask, ws.h,
+                                                 ws.V + (size_t)(j + 1) * vstride, hs->ring_dev + j % kRing);
+      NAT_LAUNCH_CHECK();
     }
-    scale_kernel<<<dim3(gx, nsys), kT, 0, s>>>(ws.w, ldv, n, mp2, j + 1, all, ws.mask, ws.h,
-                                               ws.V + (size_t)(j + 1) * vstride, hs->ring_dev + j % kRing);
-    NAT_LAUNCH_CHECK();
     NAT_CUDA_TRY(cudaEventRecord(hs->ev[j % kRing], s));
     return NAT_OK;
   };

@@ -9,8 +9,8 @@
 //  * main kernel: CTA = 256 threads x R targets each (registers); source tiles of
 //    128 records are streamed into shared memory with TMA bulk copies (cp.async.bulk +
 //    mbarrier, double buffered) and read back as warp-broadcast LDS.128; MB wavenumbers
-//    share r, 1/r and d.n; fp32 math with MUFU rsqrt/sin/cos; per-tile fp32 sums are
-//    added into fp64 accumulators kept in shared memory;
+//    share r, 1/r and d.n; fp32 math with MUFU rsqrt/sin/cos; a CTA sums its source
+//    chunk (<= 8 tiles = 1024 sources) in fp32 registers and writes one fp64 partial;
 //  * split-K over source chunks when the target grid is too small for 148 SMs, with a
 //    fixed-order fp64 reduction (deterministic, no atomics).
 #include <cstdio>
@@ -28,6 +28,7 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kTile = 128;  // sources per shared-memory tile (fp32)
 constexpr int kTile64 = 64; // sources per tile (fp64)
+constexpr int kMaxChunkTiles = 8;  // fp32 kernel: sources per CTA <= 8 x 128 = 1024 (fp32 sums)
 
 template <int MB>
 struct Rec {
@@ -207,7 +208,6 @@ __global__ void __launch_bounds__(NT) radiate_f32x2_kernel(RadParams prm) {
   constexpr int kTileFloats = kTile * NF;
   extern __shared__ __align__(128) unsigned char smem[];
   float* buf = reinterpret_cast<float*>(smem);
-  double2* dacc = reinterpret_cast<double2*>(smem + 2 * kTileFloats * sizeof(float));
   __shared__ __align__(8) uint64_t bars[2];
   if (prm.skip && *prm.skip == 0ull) return;
 
@@ -239,8 +239,13 @@ __global__ void __launch_bounds__(NT) radiate_f32x2_kernel(RadParams prm) {
     kk[m] = f2pack(k, k);
   }
   const f2r minus1 = f2pack(-1.f, -1.f);
+  // fp32 sums over the CTA's whole source chunk (<= kMaxChunkTiles tiles = 1024 sources,
+  // the fp32 budget of SURVEY §8(c-8)); the split-K partials are then summed in fp64
+  f2r ar[RP][MB], ai[RP][MB], br[RP][MB], bi[RP][MB];  // br / bi: ACC4 only
 #pragma unroll
-  for (int q = 0; q < R * MB; ++q) dacc[q * NT + tid] = make_double2(0.0, 0.0);
+  for (int p = 0; p < RP; ++p)
+#pragma unroll
+    for (int m = 0; m < MB; ++m) ar[p][m] = ai[p][m] = br[p][m] = bi[p][m] = 0ull;
 
   const int t0 = split * prm.chunk_tiles;
   const int t1 = min(t0 + prm.chunk_tiles, prm.n_tiles);
@@ -264,11 +269,6 @@ __global__ void __launch_bounds__(NT) radiate_f32x2_kernel(RadParams prm) {
     const int st = it & 1;
     nat::mbar_wait(&bars[st], (it >> 1) & 1);
     const ulonglong2* b4 = reinterpret_cast<const ulonglong2*>(buf + st * kTileFloats);
-    f2r ar[RP][MB], ai[RP][MB], br[RP][MB], bi[RP][MB];  // br / bi: ACC4 only
-#pragma unroll
-    for (int p = 0; p < RP; ++p)
-#pragma unroll
-      for (int m = 0; m < MB; ++m) ar[p][m] = ai[p][m] = br[p][m] = bi[p][m] = 0ull;
 
     // short bodies (one target pair, one wavenumber) need a deeper unroll so the
     // shared-memory loads of later sources overlap the arithmetic (ncu r01: LDS-wait)
@@ -330,26 +330,6 @@ __global__ void __launch_bounds__(NT) radiate_f32x2_kernel(RadParams prm) {
         }
       }
     }
-#pragma unroll
-    for (int p = 0; p < RP; ++p)
-#pragma unroll
-      for (int m = 0; m < MB; ++m) {
-        const int q0 = (2 * p) * MB + m, q1 = (2 * p + 1) * MB + m;
-        double2 d0 = dacc[q0 * NT + tid], d1 = dacc[q1 * NT + tid];
-        if constexpr (ACC4) {
-          d0.x += (double)f2lo(ar[p][m]) - (double)f2lo(br[p][m]);
-          d0.y += (double)f2lo(ai[p][m]) + (double)f2lo(bi[p][m]);
-          d1.x += (double)f2hi(ar[p][m]) - (double)f2hi(br[p][m]);
-          d1.y += (double)f2hi(ai[p][m]) + (double)f2hi(bi[p][m]);
-        } else {
-          d0.x += (double)f2lo(ar[p][m]);
-          d0.y += (double)f2lo(ai[p][m]);
-          d1.x += (double)f2hi(ar[p][m]);
-          d1.y += (double)f2hi(ai[p][m]);
-        }
-        dacc[q0 * NT + tid] = d0;
-        dacc[q1 * NT + tid] = d1;
-      }
     __syncthreads();  // every thread is done with buf[st]
     if (tid == 0 && t0 + it + 2 < t1) {
       nat::fence_proxy_async_smem();
@@ -359,16 +339,26 @@ __global__ void __launch_bounds__(NT) radiate_f32x2_kernel(RadParams prm) {
   }
 
 #pragma unroll
-  for (int r = 0; r < R; ++r) {
-    int64_t l = tbase + r * NT + tid;
-    if (l >= prm.n_lis) continue;
+  for (int p = 0; p < RP; ++p)
 #pragma unroll
-    for (int m = 0; m < MB; ++m) {
-      int mode = mch * MB + m;
-      if (mode < prm.n_modes)
-        prm.out[((size_t)split * prm.n_modes + mode) * prm.n_lis + l] = dacc[(r * MB + m) * NT + tid];
+    for (int h = 0; h < 2; ++h) {
+      const int64_t l = tbase + (2 * p + h) * NT + tid;
+      if (l >= prm.n_lis) continue;
+#pragma unroll
+      for (int m = 0; m < MB; ++m) {
+        const int mode = mch * MB + m;
+        if (mode >= prm.n_modes) continue;
+        double re, im;
+        if constexpr (ACC4) {
+          re = h ? (double)f2hi(ar[p][m]) - (double)f2hi(br[p][m]) : (double)f2lo(ar[p][m]) - (double)f2lo(br[p][m]);
+          im = h ? (double)f2hi(ai[p][m]) + (double)f2hi(bi[p][m]) : (double)f2lo(ai[p][m]) + (double)f2lo(bi[p][m]);
+        } else {
+          re = h ? (double)f2hi(ar[p][m]) : (double)f2lo(ar[p][m]);
+          im = h ? (double)f2hi(ai[p][m]) : (double)f2lo(ai[p][m]);
+        }
+        prm.out[((size_t)split * prm.n_modes + mode) * prm.n_lis + l] = make_double2(re, im);
+      }
     }
-  }
 }
 
 // ------------------------------------------------------------------------------------
@@ -613,14 +603,16 @@ Plan make_plan(nat_prec prec, int64_t n_src, int n_modes, int64_t n_lis, int kin
       const int R = pl.fp64 ? 2 : r_opts[ri];
       const int NT = pl.fp64 ? kThreads : nt_opts[ni];
       const size_t smem = pl.fp64 ? 2 * (size_t)kTile64 * 12 * sizeof(double)
-                                  : 2 * (size_t)kTile * pl.NF * sizeof(float) + (size_t)R * pl.MB * NT * 16;
+                                  : 2 * (size_t)kTile * pl.NF * sizeof(float);
       const int occ = occupancy(pl.fp64, pl.kind, R, pl.MB, NT, smem);
       const int64_t tgt = (n_lis + (int64_t)R * NT - 1) / ((int64_t)R * NT);
       const int64_t base = tgt * pl.n_mchunk;
       const int tile = pl.fp64 ? kTile64 : kTile;
       // per-SM pair throughput at the MUFU roofline (~1.0e10 pairs/s per SM, fp32)
       const double sm_rate = pl.fp64 ? 1.2e9 : 1.0e10;
-      for (int c = 1; c <= pl.n_tiles; ++c) {
+      // fp32 kernel: a CTA sums at most kMaxChunkTiles tiles in fp32 (then fp64 split-K)
+      const int c_max = pl.fp64 ? pl.n_tiles : std::min(pl.n_tiles, kMaxChunkTiles);
+      for (int c = 1; c <= c_max; ++c) {
         const int64_t ns = (pl.n_tiles + c - 1) / c;
         if (c > 1 && (pl.n_tiles + c - 2) / (c - 1) == ns) continue;  // same split count, more work
         // the busiest SM runs cpsm CTAs of work W in rounds of `occ` resident CTAs; a round
@@ -674,9 +666,9 @@ Plan make_plan(nat_prec prec, int64_t n_src, int n_modes, int64_t n_lis, int kin
         (NT == 128 || NT == 256) && c >= 1) {
       pl.R = R;
       pl.NT = NT;
-      pl.chunk_tiles = std::min(c, pl.n_tiles);
+      pl.chunk_tiles = std::min(std::min(c, pl.n_tiles), kMaxChunkTiles);
       pl.tgt_tiles = (n_lis + (int64_t)R * NT - 1) / ((int64_t)R * NT);
-      pl.smem = 2 * (size_t)kTile * pl.NF * sizeof(float) + (size_t)R * pl.MB * NT * 16;
+      pl.smem = 2 * (size_t)kTile * pl.NF * sizeof(float);
     }
   }
   pl.n_split = (pl.n_tiles + pl.chunk_tiles - 1) / pl.chunk_tiles;
