@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define NAT_ABI_VERSION 1
+#define NAT_ABI_VERSION 2  /* 2: nat_bem_assemble takes nnz; nat_bem_mf.nnz */
 
 typedef struct CUstream_st* nat_stream_t; /* == cudaStream_t (torch.cuda.Stream.cuda_stream) */
 
@@ -153,10 +153,13 @@ nat_status nat_bem_near_build(const nat_mesh* mesh, const nat_geom* geom, const 
  * A: row-major [rows][lda], c64 (NAT_FP32) or c128 (NAT_FP64).  g: c128 [n_rhs][n_tri]
  * (may be NULL iff n_rhs == 0).  rhs: c128 [n_rhs][rows].  k >= 0 finite.
  * ------------------------------------------------------------------------------- */
+/* nnz: the host value nat_bem_near_count returned (= near_row_ptr[rows]); the call never
+ * reads the device copy back, so it is fully asynchronous (a wrong nnz is not detected).
+ * The rule tables reach the workspace by one asynchronous copy from pinned host memory. */
 size_t nat_bem_assemble_workspace(int64_t n_tri, int64_t rows, int64_t nnz, int n_rhs); /* nnz from near_count */
 nat_status nat_bem_assemble(const nat_mesh* mesh, const nat_geom* geom, const nat_quad_opts* opts,
                             const int64_t* near_row_ptr, const int32_t* near_col,
-                            const uint8_t* near_cls, double k, nat_prec prec, int64_t row_begin,
+                            const uint8_t* near_cls, int64_t nnz, double k, nat_prec prec, int64_t row_begin,
                             int64_t row_end, int n_rhs, const void* g, void* A, int64_t lda,
                             void* rhs, void* ws, size_t ws_bytes, nat_stream_t stream); /* (async) */
 
@@ -181,6 +184,14 @@ nat_status nat_comm_create_from_id(nat_comm** comm, const uint8_t* id /* [host] 
 nat_status nat_comm_create(nat_comm** comm, void* nccl_comm /* borrowed ncclComm_t or NULL */, int rank,
                            int world);
 nat_status nat_comm_destroy(nat_comm* comm); /* destroys the ncclComm_t only if the library made it */
+/* Host-staged communicator (test backend, e.g. world > 1 on one GPU over a gloo group): each
+ * in-place all-gather copies this rank's block (count doubles at buf + rank*count) to a
+ * pinned host buffer owned by the communicator, synchronises the stream, calls
+ * fn(user, host_buf, count, rank, world) — which must fill every rank's block of host_buf
+ * (count * world doubles) and return 0 — and copies the buffer back (asynchronously).
+ * No kernel waits on another rank.  Nonzero fn return -> NAT_ERR_NCCL. */
+typedef int (*nat_allgather_fn)(void* user, double* host_buf, size_t count, int rank, int world);
+nat_status nat_comm_create_host(nat_comm** comm, int rank, int world, nat_allgather_fn fn, void* user);
 
 /* ---------------------------------------------------------------------------------
  * a7 — unrestarted GMRES (tol 1e-6, max 200; reading R-gmres) on the
@@ -194,7 +205,9 @@ nat_status nat_comm_destroy(nat_comm* comm); /* destroys the ncclComm_t only if 
  * ------------------------------------------------------------------------------- */
 typedef struct {
   int iters, converged;
-  double rel_residual; /* true residual from one extra matvec            */
+  double rel_residual; /* true ||b - A x|| / ||b||, formed by linearity from the operator
+                          products saved during the iteration (b - sum_k y_k (A v_k); no extra
+                          operator application; reading R-gmres)                               */
   double t_total_s;  /* host wall time of the call                                         */
   double t_matvec_s; /* device time (CUDA events) of the operator applications: matvec and,
                         on > 1 rank, the all-gather (bem_solve) / MC operator (mc)          */
@@ -234,12 +247,13 @@ typedef struct {
   const int64_t* near_row_ptr; /* [rows + 1]                                        */
   const int32_t* near_col;     /* [nnz]                                             */
   const uint8_t* near_cls;     /* [nnz]                                             */
+  int64_t nnz;                 /* [host] near_row_ptr[rows] (nat_bem_near_count)    */
   void* near_delta;            /* [nnz] c128 (prepare writes, matvec reads)          */
   void* diag_delta;            /* [rows] c128                                        */
 } nat_bem_mf;
 size_t nat_bem_mf_workspace(const nat_bem_mf* op, int64_t nnz, int n_rhs);
 nat_status nat_bem_mf_prepare(const nat_bem_mf* op, int n_rhs, const void* g, void* rhs, void* ws,
-                              size_t ws_bytes, nat_stream_t stream); /* (async after one nnz read) */
+                              size_t ws_bytes, nat_stream_t stream); /* (async) */
 nat_status nat_bem_mf_matvec(const nat_bem_mf* op, const void* x, void* y, void* ws, size_t ws_bytes,
                              nat_stream_t stream); /* (async) */
 /* GMRES (as nat_bem_solve: same row ownership, all-gather, tolerances and info) over the
@@ -259,7 +273,11 @@ nat_status nat_bem_mf_solve(nat_comm* comm, const nat_bem_mf* op, const void* b_
  *     Bit-identical with the oracle.  (async)
  * a9  nat_mc_rhs: b[m][i] = -w sum_{j != i} G_m(y_i, y_j) g[m][j] - (eps/2) g[m][i].
  * a10 nat_mc_apply: out[m][i] = 1/2 p[m][i] - w sum_{j != i} dG_m/dn_y(y_i, y_j) p[m][j].
- *     w = (|Gamma| - pi eps^2)/(M - 1);  k [host][n_sys];  g, p, b, out c128 [n_sys][M].
+ *     The library derives eps and w from total_area = |Gamma| (nat_mesh_prepare) and M:
+ *     eps = sqrt(|Gamma| / (pi M)) unless eps > 0 is given (R-eps), and
+ *     w = (|Gamma| - pi eps^2)/(M - 1) (R-weight; w = 0 for M = 1);
+ *     NAT_ERR_INVALID_ARG for total_area <= 0 or pi eps^2 > |Gamma|.
+ *     k [host][n_sys];  g, p, b, out c128 [n_sys][M].
  *     NAT_FP32: sample pairs closer than 2 eps (the disk diameter) are evaluated in fp64
  *     (their fp32 coordinates cannot resolve d.n); all other pairs in fp32.
  * nat_mc_surface_pressure: a8 (or caller samples) -> a9 -> batched GMRES over a10
@@ -279,11 +297,11 @@ nat_status nat_mc_sample(const nat_mesh* mesh, const nat_geom* geom, int64_t M, 
                          nat_stream_t stream); /* (async) */
 size_t nat_mc_op_workspace(nat_prec prec, int64_t M, int n_sys);
 nat_status nat_mc_rhs(nat_prec prec, int64_t M, const double* samples, int n_sys, const double* k,
-                      const void* g, double w, double eps, void* b, void* ws, size_t ws_bytes,
-                      nat_stream_t stream); /* (async) */
+                      const void* g, double total_area, double eps, void* b, void* ws, size_t ws_bytes,
+                      nat_stream_t stream); /* (sync: builds the close-pair list) */
 nat_status nat_mc_apply(nat_prec prec, int64_t M, const double* samples, int n_sys, const double* k,
-                        const void* p, double w, double eps, void* out, void* ws, size_t ws_bytes,
-                        nat_stream_t stream); /* (async) */
+                        const void* p, double total_area, double eps, void* out, void* ws, size_t ws_bytes,
+                        nat_stream_t stream); /* (sync: builds the close-pair list) */
 /* g_out[m][j] = g_tri[m][sample_tri[j]] (piecewise-constant Neumann data at the samples,
  * P:164; c128 [n_sys][n_tri] -> c128 [n_sys][M]).  (async)                              */
 nat_status nat_mc_gather_neumann(int n_sys, int64_t M, int64_t n_tri, const void* g_tri,
@@ -300,13 +318,14 @@ nat_status nat_mc_surface_pressure(const nat_mesh* mesh, const nat_geom* geom, i
                                    nat_stream_t stream); /* (sync) */
 
 /* Rows [row_begin, row_end) of the a10 operator (row sharding; SURVEY §8(e) "MC, one large
- * system"): out[m][r] = 1/2 p[m][i] - w sum_{j != i} dG_m/dn_y(y_i, y_j) p[m][j],
+ * system"), eps and w derived as for nat_mc_apply:
+ * out[m][r] = 1/2 p[m][i] - w sum_{j != i} dG_m/dn_y(y_i, y_j) p[m][j],
  * i = row_begin + r; p c128 [n_sys][M] (all rows), out c128 [n_sys][rows]; n_sys <= 64.
  * Workspace nat_mc_rows_workspace(prec, M, n_sys, rows).  (sync: builds the close-pair list) */
 size_t nat_mc_rows_workspace(nat_prec prec, int64_t M, int n_sys, int64_t rows);
 nat_status nat_mc_apply_rows(nat_prec prec, int64_t M, const double* samples, int n_sys, const double* k /* [host] */,
-                             const void* p, double w, double eps, int64_t row_begin, int64_t row_end, void* out,
-                             void* ws, size_t ws_bytes, nat_stream_t stream);
+                             const void* p, double total_area, double eps, int64_t row_begin, int64_t row_end,
+                             void* out, void* ws, size_t ws_bytes, nat_stream_t stream);
 /* nat_mc_surface_pressure row-sharded across the ranks of `comm` (NULL => world 1): rank r
  * owns sample rows [r ceil(M/world), ...) of the RHS and the operator; every operator
  * application is followed by an in-place NCCL all-gather of each system's iterate and the

@@ -20,6 +20,9 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <type_traits>
 #include <vector>
 
@@ -62,6 +65,11 @@ constexpr int kNRmax = 2;
 struct Pt {
   double l1, l2, l3, w;
 };
+
+// The 1- and 7-point far rules contain the centroid, i.e. the collocation point of the row's
+// own triangle: their far-rule self pair is singular and is zeroed by the far kernels.
+template <int NQ>
+constexpr bool kCentroidRule = (NQ == 1 || NQ == 7);
 
 bool base_rule(int npts, std::vector<Pt>& out) {
   out.clear();
@@ -397,6 +405,12 @@ __global__ void __launch_bounds__(kThreads) far_kernel(FarArgs<R> a) {
           // self pair (Sauter-Schwab kernel) and padding columns (jj = 0 may be the row)
           if (!valid || j == a.row_begin + i0 + t) Vr = Vi = Kr = Ki = R(0);
         }
+        if constexpr (NTQ == 1 && kCentroidRule<NQ>) {
+          // the 1- and 7-point rules contain the centroid = the collocation point: the self
+          // pair is singular under the far rule; it is zeroed (the self kernel adds the exact
+          // value and subtracts nothing) — a select, NaN-safe
+          if (!valid || j == a.row_begin + i0 + t) Vr = Vi = Kr = Ki = R(0);
+        }
         if (!MV && a.store_A && valid) store_entry<R>(a.A, (size_t)(i0 + t) * a.lda + j, -Kr, -Ki);
         if constexpr (MV) {  // (-K) x_j
           bacc[t][0].x -= Kr * gj[0].x - Ki * gj[0].y;
@@ -569,7 +583,7 @@ __global__ void __launch_bounds__(kThreads, kFarMinBlocks) far_kernel_x2(FarArgs
             Ki = f2fma(wt, ki_, Ki);
           }
           }
-          if constexpr (NTQ > 1) {  // self pair and padding columns -> 0 (select, NaN-safe)
+          if constexpr (NTQ > 1 || kCentroidRule<NQ>) {  // self pair and padding columns -> 0 (select, NaN-safe)
             const int64_t ri = a.row_begin + i0 + 2 * t;
             const bool z0 = !valid || j == ri, z1 = !valid || j == ri + 1;
             if (z0 || z1) {
@@ -924,7 +938,9 @@ __global__ void self_kernel(int64_t n, int64_t nv, int64_t row_begin, int64_t ro
   }
   R fVr, fVi, fKr, fKi;
   const R mx = (R)nrm_rows[i], my = (R)nrm_rows[n + i], mz = (R)nrm_rows[2 * n + i];
-  if constexpr (BM)
+  if constexpr (kCentroidRule<NQ>)  // the far kernels zeroed the self pair: nothing to subtract
+    fVr = fVi = fKr = fKi = R(0);
+  else if constexpr (BM)
     far_entry_bm_rhs<R, NQ>(y, w, cols.nrm[i], cols.nrm[n + i], cols.nrm[2 * n + i], mx, my, mz, (R)(c[0] - cx),
                             (R)(c[1] - cy), (R)(c[2] - cz), (R)k, fVr, fVi);
   else
@@ -1670,6 +1686,31 @@ size_t carve(nat::Carver& c, AsmWs& w, int64_t n, int64_t rows, int64_t nnz, int
   return c.bytes();
 }
 
+// Immutable pinned host copies of rule tables, built once per option set and process:
+// every call copies its tables into the workspace with an asynchronous copy from pinned
+// memory (no pageable staging, no host stall).  Entries are never freed or modified.
+struct PinnedBlob {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+};
+const PinnedBlob* pinned_blob(const std::tuple<int, int, int, int, int, int>& key,
+                              const std::vector<char>& (*build)(const std::tuple<int, int, int, int, int, int>&)) {
+  static std::mutex mu;
+  static std::map<std::tuple<int, int, int, int, int, int>, PinnedBlob> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) return &it->second;
+  const std::vector<char>& src = build(key);
+  PinnedBlob b;
+  b.bytes = src.size();
+  if (cudaHostAlloc(&b.ptr, b.bytes > 0 ? b.bytes : 1, cudaHostAllocDefault) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  std::memcpy(b.ptr, src.data(), b.bytes);
+  return &(cache[key] = b);
+}
+
 constexpr int kMaxLevel = 4;
 constexpr int kMaxGL = 64;
 
@@ -1875,7 +1916,8 @@ extern "C" size_t nat_bem_assemble_workspace(int64_t n_tri, int64_t rows, int64_
 namespace {
 // nat_bem_assemble and nat_bem_mf_prepare (mf.delta set: no A, corrections instead)
 nat_status assemble_entry(const nat_mesh* mesh, const nat_geom* geom, const nat_quad_opts* opts,
-                          const int64_t* near_row_ptr, const int32_t* near_col, const uint8_t* near_cls, double k,
+                          const int64_t* near_row_ptr, const int32_t* near_col, const uint8_t* near_cls, int64_t nnz,
+                          double k,
                           nat_prec prec, int64_t row_begin, int64_t row_end, int n_rhs, const void* g, void* A,
                           int64_t lda, void* rhs, void* ws, size_t ws_bytes, nat_stream_t stream, MfOut mf) {
   NAT_REQUIRE(mesh && geom, "mesh and geom must be non-null");
@@ -1916,9 +1958,8 @@ nat_status assemble_entry(const nat_mesh* mesh, const nat_geom* geom, const nat_
   }
   const int64_t rows = row_end - row_begin;
   cudaStream_t s = (cudaStream_t)stream;
-  int64_t nnz = 0;
-  NAT_CUDA_TRY(cudaMemcpyAsync(&nnz, near_row_ptr + rows, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-  NAT_CUDA_TRY(cudaStreamSynchronize(s));
+  // nnz is the caller's (nat_bem_near_count's) host value of near_row_ptr[rows]: the call
+  // never reads it back (asynchronous)
   NAT_REQUIRE(nnz >= 0 && nnz < (1LL << 31), "near list has %lld entries", (long long)nnz);
   if (nnz > 0) {
     NAT_REQUIRE_DEV(near_col);
@@ -1937,52 +1978,83 @@ nat_status assemble_entry(const nat_mesh* mesh, const nat_geom* geom, const nat_
   size_t need = carve(c, w, n, rows, nnz, n_rhs, kMaxFarQ, (int)pS.size(), (int)pN.size(), o.gl, rsz);
   if (ws_bytes < need) return nat::fail(NAT_ERR_WORKSPACE, "workspace %zu < %zu", ws_bytes, need);
   NAT_REQUIRE_DEV(ws);
-  // rule tables -> workspace in one copy (they are carved contiguously; pageable source:
-  // staged before the call returns)
-  {
-    std::vector<float4> fS(pS.size()), fN(pN.size());
-    for (size_t q = 0; q < pS.size(); ++q)
-      fS[q] = make_float4((float)pS[q].l1, (float)pS[q].l2, (float)pS[q].l3, (float)pS[q].w);
-    for (size_t q = 0; q < pN.size(); ++q)
-      fN[q] = make_float4((float)pN[q].l1, (float)pN[q].l2, (float)pN[q].l3, (float)pN[q].w);
-    std::vector<double> gl(glx);
-    gl.insert(gl.end(), glw.begin(), glw.end());
-    char* base = reinterpret_cast<char*>(w.rule_far);
-    const size_t total = (size_t)(reinterpret_cast<char*>(w.rule_Nf + fN.size()) - base);
-    std::vector<char> blob(total, 0);
-    auto put = [&](const void* dst, const void* src, size_t bytes) {
-      std::memcpy(blob.data() + (reinterpret_cast<const char*>(dst) - base), src, bytes);
-    };
-    put(w.rule_far, pF.data(), pF.size() * sizeof(Pt));
-    put(w.rule_S, pS.data(), pS.size() * sizeof(Pt));
-    put(w.rule_N, pN.data(), pN.size() * sizeof(Pt));
-    put(w.gl, gl.data(), gl.size() * sizeof(double));
-    put(w.rule_Sf, fS.data(), fS.size() * sizeof(float4));
-    put(w.rule_Nf, fN.data(), fN.size() * sizeof(float4));
-    NAT_CUDA_TRY(cudaMemcpyAsync(base, blob.data(), total, cudaMemcpyHostToDevice, s));
-  }
-
+  // rule tables -> workspace: one asynchronous copy from an immutable pinned blob built
+  // once per option set (far / class-S / class-N rules, Gauss-Legendre self rule, and the
+  // Sauter-Schwab points for Galerkin), laid out exactly as the workspace carve
   SSTable tab{};
   if (o.gal) {
     std::vector<double> ssv;
-    ss_build(o.ss, ssv, tab);
-    const size_t np = ssv.size() / 5;
-    std::vector<float4> xf(np);
-    std::vector<double4> xd(np);
-    std::vector<double> wv(np);
-    std::vector<float> wf(np);
-    for (size_t q = 0; q < np; ++q) {
-      const double* e = &ssv[5 * q];
-      xf[q] = make_float4((float)e[0], (float)e[1], (float)e[2], (float)e[3]);
-      xd[q] = make_double4(e[0], e[1], e[2], e[3]);
-      wv[q] = e[4];
-      wf[q] = (float)e[4];
+    ss_build(o.ss, ssv, tab);  // the case offsets (host arithmetic; the points come from the blob)
+  }
+  {
+    char* base = reinterpret_cast<char*>(w.rule_far);
+    const size_t total = (size_t)(reinterpret_cast<char*>(w.rule_Nf + pN.size()) - base);
+    const auto key = std::make_tuple(o.far_pts, o.lev_S, o.lev_N, o.gl, o.gal ? o.ss : 0, 0);
+    auto build = [](const std::tuple<int, int, int, int, int, int>& kk) -> const std::vector<char>& {
+      static thread_local std::vector<char> blob;
+      std::vector<Pt> F, S, N;
+      base_rule(std::get<0>(kk), F);
+      composite_rule(std::get<1>(kk), S);
+      composite_rule(std::get<2>(kk), N);
+      std::vector<double> glx, glw;
+      gauss_legendre(std::get<3>(kk), glx, glw);
+      // the same carve as assemble_entry: rule_far[kMaxFarQ] rule_S rule_N gl[2 ngl] rule_Sf rule_Nf
+      nat::Carver cc(reinterpret_cast<void*>((uintptr_t)1 << 20));  // offsets only (never dereferenced)
+      double4* rf = cc.take<double4>(kMaxFarQ);
+      double4* rs = cc.take<double4>(S.size());
+      double4* rn = cc.take<double4>(N.size());
+      double* gl = cc.take<double>(2 * glx.size());
+      float4* sf = cc.take<float4>(S.size());
+      float4* nf = cc.take<float4>(N.size());
+      const size_t tables = (size_t)(reinterpret_cast<char*>(nf + N.size()) - reinterpret_cast<char*>(rf));
+      std::vector<double> ssv;
+      SSTable t{};
+      if (std::get<4>(kk)) ss_build(std::get<4>(kk), ssv, t);
+      const size_t np = ssv.size() / 5;
+      blob.assign(tables + np * (sizeof(float4) + sizeof(double4) + sizeof(double) + sizeof(float)), 0);
+      auto off = [&](const void* q) { return (size_t)(reinterpret_cast<const char*>(q) - reinterpret_cast<char*>(rf)); };
+      std::memcpy(blob.data() + off(rf), F.data(), F.size() * sizeof(Pt));
+      std::memcpy(blob.data() + off(rs), S.data(), S.size() * sizeof(Pt));
+      std::memcpy(blob.data() + off(rn), N.data(), N.size() * sizeof(Pt));
+      std::vector<double> g2(glx);
+      g2.insert(g2.end(), glw.begin(), glw.end());
+      std::memcpy(blob.data() + off(gl), g2.data(), g2.size() * sizeof(double));
+      for (size_t q = 0; q < S.size(); ++q) {
+        const float4 v = make_float4((float)S[q].l1, (float)S[q].l2, (float)S[q].l3, (float)S[q].w);
+        std::memcpy(blob.data() + off(sf + q), &v, sizeof v);
+      }
+      for (size_t q = 0; q < N.size(); ++q) {
+        const float4 v = make_float4((float)N[q].l1, (float)N[q].l2, (float)N[q].l3, (float)N[q].w);
+        std::memcpy(blob.data() + off(nf + q), &v, sizeof v);
+      }
+      // Sauter-Schwab: [np] float4 | [np] double4 | [np] double | [np] float after the tables
+      char* p0 = blob.data() + tables;
+      for (size_t q = 0; q < np; ++q) {
+        const double* e = &ssv[5 * q];
+        const float4 xf = make_float4((float)e[0], (float)e[1], (float)e[2], (float)e[3]);
+        const double4 xd = make_double4(e[0], e[1], e[2], e[3]);
+        const double wv = e[4];
+        const float wf = (float)e[4];
+        std::memcpy(p0 + q * sizeof(float4), &xf, sizeof xf);
+        std::memcpy(p0 + np * sizeof(float4) + q * sizeof(double4), &xd, sizeof xd);
+        std::memcpy(p0 + np * (sizeof(float4) + sizeof(double4)) + q * sizeof(double), &wv, sizeof wv);
+        std::memcpy(p0 + np * (sizeof(float4) + sizeof(double4) + sizeof(double)) + q * sizeof(float), &wf, sizeof wf);
+      }
+      return blob;
+    };
+    const PinnedBlob* pb = pinned_blob(key, build);
+    if (!pb) return nat::fail(NAT_ERR_CUDA, "pinned rule tables: %s", cudaGetErrorString(cudaGetLastError()));
+    NAT_CUDA_TRY(cudaMemcpyAsync(base, pb->ptr, total, cudaMemcpyHostToDevice, s));
+    if (o.gal) {
+      const size_t np = (pb->bytes - total) / (sizeof(float4) + sizeof(double4) + sizeof(double) + sizeof(float));
+      const char* p0 = reinterpret_cast<const char*>(pb->ptr) + total;
+      NAT_CUDA_TRY(cudaMemcpyAsync(w.ssx, p0, np * sizeof(float4), cudaMemcpyHostToDevice, s));
+      NAT_CUDA_TRY(cudaMemcpyAsync(w.ssx64, p0 + np * sizeof(float4), np * sizeof(double4), cudaMemcpyHostToDevice, s));
+      NAT_CUDA_TRY(cudaMemcpyAsync(w.ssw, p0 + np * (sizeof(float4) + sizeof(double4)), np * sizeof(double),
+                                   cudaMemcpyHostToDevice, s));
+      NAT_CUDA_TRY(cudaMemcpyAsync(w.ssw32, p0 + np * (sizeof(float4) + sizeof(double4) + sizeof(double)),
+                                   np * sizeof(float), cudaMemcpyHostToDevice, s));
     }
-    // pageable sources: staged before the call returns
-    NAT_CUDA_TRY(cudaMemcpyAsync(w.ssx, xf.data(), np * sizeof(float4), cudaMemcpyHostToDevice, s));
-    NAT_CUDA_TRY(cudaMemcpyAsync(w.ssx64, xd.data(), np * sizeof(double4), cudaMemcpyHostToDevice, s));
-    NAT_CUDA_TRY(cudaMemcpyAsync(w.ssw, wv.data(), np * sizeof(double), cudaMemcpyHostToDevice, s));
-    NAT_CUDA_TRY(cudaMemcpyAsync(w.ssw32, wf.data(), np * sizeof(float), cudaMemcpyHostToDevice, s));
   }
   const double2* gg = (const double2*)g;
   double2* bb = (double2*)rhs;
@@ -2010,12 +2082,13 @@ nat_status assemble_entry(const nat_mesh* mesh, const nat_geom* geom, const nat_
 
 extern "C" nat_status nat_bem_assemble(const nat_mesh* mesh, const nat_geom* geom,
                                        const nat_quad_opts* opts, const int64_t* near_row_ptr,
-                                       const int32_t* near_col, const uint8_t* near_cls, double k,
+                                       const int32_t* near_col, const uint8_t* near_cls, int64_t nnz, double k,
                                        nat_prec prec, int64_t row_begin, int64_t row_end, int n_rhs,
                                        const void* g, void* A, int64_t lda, void* rhs, void* ws,
                                        size_t ws_bytes, nat_stream_t stream) {
-  return assemble_entry(mesh, geom, opts, near_row_ptr, near_col, near_cls, k, prec, row_begin, row_end, n_rhs, g,
-                        A, lda, rhs, ws, ws_bytes, stream, MfOut{});
+  NAT_TRACE();
+  return assemble_entry(mesh, geom, opts, near_row_ptr, near_col, near_cls, nnz, k, prec, row_begin, row_end, n_rhs,
+                        g, A, lda, rhs, ws, ws_bytes, stream, MfOut{});
 }
 
 namespace {
@@ -2034,6 +2107,7 @@ void launch_gemv(nat_prec prec, int64_t rows, int64_t n, const void* A, int64_t 
 
 extern "C" nat_status nat_bem_matvec(nat_prec prec, int64_t rows, int64_t n, const void* A, int64_t lda,
                                      const void* x, void* y, nat_stream_t stream) {
+  NAT_TRACE();
   NAT_REQUIRE(prec == NAT_FP32 || prec == NAT_FP64, "bad precision %d", (int)prec);
   NAT_REQUIRE(rows >= 1 && n >= 1 && lda >= n, "need rows, n >= 1 and lda >= n");
   NAT_REQUIRE(prec == NAT_FP64 || (lda % 2 == 0 && ((uintptr_t)A % 16) == 0),
@@ -2203,9 +2277,17 @@ nat_status mf_begin(const nat_bem_mf* op, void* ws, size_t ws_bytes, cudaStream_
   if (ws_bytes < need) return fail(NAT_ERR_WORKSPACE, "workspace %zu < %zu", ws_bytes, need);
   NAT_REQUIRE_DEV(ws);
   const Opts o = opts_of(op->opts);
-  std::vector<Pt> pF;
-  base_rule(o.far_pts, pF);
-  NAT_CUDA_TRY(cudaMemcpyAsync(w.rule_far, pF.data(), pF.size() * sizeof(Pt), cudaMemcpyHostToDevice, s));
+  // the far rule from an immutable pinned blob (asynchronous copy, no pageable staging)
+  auto build = [](const std::tuple<int, int, int, int, int, int>& kk) -> const std::vector<char>& {
+    static thread_local std::vector<char> blob;
+    std::vector<Pt> F;
+    base_rule(std::get<0>(kk), F);
+    blob.assign(reinterpret_cast<const char*>(F.data()), reinterpret_cast<const char*>(F.data() + F.size()));
+    return blob;
+  };
+  const PinnedBlob* pb = pinned_blob(std::make_tuple(o.far_pts, 0, 0, 0, 0, 1), build);
+  if (!pb) return fail(NAT_ERR_CUDA, "pinned rule table: %s", cudaGetErrorString(cudaGetLastError()));
+  NAT_CUDA_TRY(cudaMemcpyAsync(w.rule_far, pb->ptr, pb->bytes, cudaMemcpyHostToDevice, s));
   const double cx = op->geom->center[0], cy = op->geom->center[1], cz = op->geom->center[2];
   if (op->prec == NAT_FP32)
     far_prep_kernel<float><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(
@@ -2256,17 +2338,20 @@ extern "C" size_t nat_bem_mf_workspace(const nat_bem_mf* op, int64_t nnz, int n_
 
 extern "C" nat_status nat_bem_mf_prepare(const nat_bem_mf* op, int n_rhs, const void* g, void* rhs, void* ws,
                                          size_t ws_bytes, nat_stream_t stream) {
+  NAT_TRACE();
   nat_status st = mf_check(op);
   if (st != NAT_OK) return st;
   MfOut mf;
   mf.delta = (double2*)op->near_delta;
   mf.diag = (double2*)op->diag_delta;
-  return assemble_entry(op->mesh, op->geom, op->opts, op->near_row_ptr, op->near_col, op->near_cls, op->k, op->prec,
+  return assemble_entry(op->mesh, op->geom, op->opts, op->near_row_ptr, op->near_col, op->near_cls, op->nnz, op->k,
+                        op->prec,
                         op->row_begin, op->row_end, n_rhs, g, nullptr, 0, rhs, ws, ws_bytes, stream, mf);
 }
 
 extern "C" nat_status nat_bem_mf_matvec(const nat_bem_mf* op, const void* x, void* y, void* ws, size_t ws_bytes,
                                         nat_stream_t stream) {
+  NAT_TRACE();
   nat_status st = mf_check(op);
   if (st != NAT_OK) return st;
   NAT_REQUIRE_DEV(x);

@@ -944,6 +944,7 @@ extern "C" nat_status nat_bem_solve(nat_comm* comm, nat_prec prec, int64_t n, in
                                     const void* A_local, int64_t lda, const void* b_local, void* x, double tol,
                                     int max_iter, void* ws, size_t ws_bytes, nat_solve_info* info,
                                     nat_stream_t stream) {
+  NAT_TRACE();
   auto t_start = std::chrono::steady_clock::now();
   NAT_REQUIRE(prec == NAT_FP32 || prec == NAT_FP64, "bad precision %d", (int)prec);
   NAT_REQUIRE(n >= 1 && lda >= n, "need n >= 1 and lda >= n");
@@ -951,6 +952,9 @@ extern "C" nat_status nat_bem_solve(nat_comm* comm, nat_prec prec, int64_t n, in
   if (max_iter <= 0) max_iter = 200;
   SolveLayout L = layout(comm, n);
   NAT_REQUIRE(L.world <= 64, "world size %d > 64", L.world);
+  // the same condition on every rank (no rank fails alone before a collective)
+  NAT_REQUIRE((int64_t)(L.world - 1) * L.rpr < n, "the last of %d ranks owns no rows (n = %lld)", L.world,
+              (long long)n);
   const int64_t rb = L.rank * L.rpr, re = nat::min64(n, rb + L.rpr);
   NAT_REQUIRE(row_begin == rb && row_end == re,
               "rank %d must own rows [%lld, %lld) (rows_per_rank = ceil(n/world)); got [%lld, %lld)", L.rank,
@@ -1036,6 +1040,7 @@ extern "C" size_t nat_bem_mf_solve_workspace(const nat_bem_mf* op, int max_iter,
 extern "C" nat_status nat_bem_mf_solve(nat_comm* comm, const nat_bem_mf* op, const void* b_local, void* x,
                                        double tol, int max_iter, void* ws, size_t ws_bytes, nat_solve_info* info,
                                        nat_stream_t stream) {
+  NAT_TRACE();
   auto t_start = std::chrono::steady_clock::now();
   NAT_REQUIRE(op && op->mesh, "op must be non-null");
   const int64_t n = op->mesh->n_tri;
@@ -1043,6 +1048,8 @@ extern "C" nat_status nat_bem_mf_solve(nat_comm* comm, const nat_bem_mf* op, con
   if (max_iter <= 0) max_iter = 200;
   SolveLayout L = layout(comm, n);
   NAT_REQUIRE(L.world <= 64, "world size %d > 64", L.world);
+  NAT_REQUIRE((int64_t)(L.world - 1) * L.rpr < n, "the last of %d ranks owns no rows (n = %lld)", L.world,
+              (long long)n);
   const int64_t rb = L.rank * L.rpr, re = nat::min64(n, rb + L.rpr);
   NAT_REQUIRE(op->row_begin == rb && op->row_end == re,
               "rank %d must own rows [%lld, %lld) (rows_per_rank = ceil(n/world)); got [%lld, %lld)", L.rank,

@@ -361,6 +361,7 @@ nat_status mc_rhs_impl(nat_prec prec, int64_t M, const double* smp, int nsys, co
     for (int d = 0; d < 3; ++d) in.center[d] = center[d];
   in.g = g;
   if (rr.ldp > 0) in.ldpg = rr.ldp;
+  in.plan_lis = M;  // a row block sums its rows exactly as the full operator does
   in.self_r2 = np.on ? np.thr : 0.f;
   return finish_op(in, prec, M, smp, nsys, k, w, eps, nullptr, g, b, ws, ws_bytes, np, s, rr);
 }
@@ -375,8 +376,20 @@ nat_status mc_apply_impl(nat_prec prec, int64_t M, const double* smp, int nsys, 
   in.p = p;
   in.skip = skip;
   if (rr.ldp > 0) in.ldpg = rr.ldp;
+  in.plan_lis = M;  // a row block sums its rows exactly as the full operator does
   in.self_r2 = np.on ? np.thr : 0.f;
   return finish_op(in, prec, M, smp, nsys, k, w, 0.0, p, nullptr, out, ws, ws_bytes, np, s, rr);
+}
+
+// Disk radius and off-disk weight (readings R-eps, R-weight):
+//   eps = sqrt(|Gamma| / (pi M)) unless the caller gives eps > 0,
+//   w = (|Gamma| - pi eps^2) / (M - 1)   (w = 0 for M = 1: the single-sample row).
+nat_status mc_eps_w(double area, int64_t M, double eps_in, double* eps, double* w) {
+  NAT_REQUIRE(area > 0 && area < 1e300, "total_area = %g must be finite and > 0", area);
+  *eps = eps_in > 0 ? eps_in : std::sqrt(area / (nat::kPi * (double)M));
+  *w = M > 1 ? (area - nat::kPi * *eps * *eps) / (double)(M - 1) : 0.0;
+  NAT_REQUIRE(*w >= 0, "eps = %g: the disk area pi eps^2 exceeds |Gamma| = %g", *eps, area);
+  return NAT_OK;
 }
 
 nat_status check_k(int n, const double* k) {
@@ -391,6 +404,7 @@ nat_status check_k(int n, const double* k) {
 extern "C" nat_status nat_mc_sample(const nat_mesh* mesh, const nat_geom* geom, int64_t M, uint64_t seed,
                                     uint64_t stream_id, double* samples, int32_t* sample_tri,
                                     nat_stream_t stream) {
+  NAT_TRACE();
   NAT_REQUIRE(mesh && geom, "mesh and geom must be non-null");
   NAT_REQUIRE(M >= 1 && M < (1LL << 32), "M must be in [1, 2^32)");
   NAT_REQUIRE(geom->n_tri == mesh->n_tri && mesh->n_tri >= 1, "inconsistent n_tri");
@@ -415,6 +429,7 @@ nat_status nat::mc_sample_tagged(const nat_mesh* mesh, const nat_geom* geom, int
 
 extern "C" nat_status nat_mc_check_coincident(int64_t M, const double* samples, int64_t* pair, void* ws,
                                               size_t ws_bytes, nat_stream_t stream) {
+  NAT_TRACE();
   NAT_REQUIRE(M >= 1 && pair, "need M >= 1 and a host pair[2]");
   NAT_REQUIRE(ws_bytes >= 8, "workspace must hold 8 bytes");
   NAT_REQUIRE_DEV(samples);
@@ -438,6 +453,7 @@ extern "C" nat_status nat_mc_check_coincident(int64_t M, const double* samples, 
 
 extern "C" nat_status nat_mc_gather_neumann(int n_sys, int64_t M, int64_t n_tri, const void* g_tri,
                                             const int32_t* sample_tri, void* g_out, nat_stream_t stream) {
+  NAT_TRACE();
   NAT_REQUIRE(n_sys >= 1 && M >= 1 && n_tri >= 1, "need n_sys, M, n_tri >= 1");
   NAT_REQUIRE_DEV(g_tri);
   NAT_REQUIRE_DEV(sample_tri);
@@ -473,11 +489,15 @@ nat_status op_setup(nat_prec prec, int64_t M, int n_sys, const double* smp, doub
 }  // namespace
 
 extern "C" nat_status nat_mc_rhs(nat_prec prec, int64_t M, const double* samples, int n_sys, const double* k,
-                                 const void* g, double w, double eps, void* b, void* ws, size_t ws_bytes,
+                                 const void* g, double total_area, double eps_in, void* b, void* ws, size_t ws_bytes,
                                  nat_stream_t stream) {
+  NAT_TRACE();
   NAT_REQUIRE(prec == NAT_FP32 || prec == NAT_FP64, "bad precision %d", (int)prec);
   NAT_REQUIRE(M >= 1 && n_sys >= 1, "need M >= 1 and n_sys >= 1");
   nat_status st = check_k(n_sys, k);
+  if (st != NAT_OK) return st;
+  double eps, w;
+  st = mc_eps_w(total_area, M, eps_in, &eps, &w);
   if (st != NAT_OK) return st;
   NAT_REQUIRE_DEV(samples);
   NAT_REQUIRE_DEV(g);
@@ -493,11 +513,15 @@ extern "C" nat_status nat_mc_rhs(nat_prec prec, int64_t M, const double* samples
 }
 
 extern "C" nat_status nat_mc_apply(nat_prec prec, int64_t M, const double* samples, int n_sys, const double* k,
-                                   const void* p, double w, double eps, void* out, void* ws, size_t ws_bytes,
-                                   nat_stream_t stream) {
+                                   const void* p, double total_area, double eps_in, void* out, void* ws,
+                                   size_t ws_bytes, nat_stream_t stream) {
+  NAT_TRACE();
   NAT_REQUIRE(prec == NAT_FP32 || prec == NAT_FP64, "bad precision %d", (int)prec);
   NAT_REQUIRE(M >= 1 && n_sys >= 1, "need M >= 1 and n_sys >= 1");
   nat_status st = check_k(n_sys, k);
+  if (st != NAT_OK) return st;
+  double eps, w;
+  st = mc_eps_w(total_area, M, eps_in, &eps, &w);
   if (st != NAT_OK) return st;
   NAT_REQUIRE_DEV(samples);
   NAT_REQUIRE_DEV(p);
@@ -549,17 +573,21 @@ extern "C" size_t nat_mc_rows_workspace(nat_prec prec, int64_t M, int n_sys, int
   nat::Carver c(nullptr);
   carve_near(c, nullptr, M);
   c.take<double>((size_t)3 * (rows > 0 ? rows : 1));
-  c.take<char>(std::max(nat::radiate_ws_bytes(prec, M, n_sys, rows, 1), nat::radiate_ws_bytes(prec, M, n_sys, rows, 2)));
+  c.take<char>(std::max(nat::radiate_ws_bytes(prec, M, n_sys, rows, 1, M), nat::radiate_ws_bytes(prec, M, n_sys, rows, 2, M)));
   return c.bytes();
 }
 
 extern "C" nat_status nat_mc_apply_rows(nat_prec prec, int64_t M, const double* samples, int n_sys, const double* k,
-                                        const void* p, double w, double eps, int64_t row_begin, int64_t row_end,
-                                        void* out, void* ws, size_t ws_bytes, nat_stream_t stream) {
+                                        const void* p, double total_area, double eps_in, int64_t row_begin,
+                                        int64_t row_end, void* out, void* ws, size_t ws_bytes, nat_stream_t stream) {
+  NAT_TRACE();
   NAT_REQUIRE(prec == NAT_FP32 || prec == NAT_FP64, "bad precision %d", (int)prec);
   NAT_REQUIRE(M >= 1 && n_sys >= 1 && n_sys <= 64, "need M >= 1 and 1 <= n_sys <= 64");
   NAT_REQUIRE(0 <= row_begin && row_begin < row_end && row_end <= M, "bad row range");
   nat_status st = check_k(n_sys, k);
+  if (st != NAT_OK) return st;
+  double eps, w;
+  st = mc_eps_w(total_area, M, eps_in, &eps, &w);
   if (st != NAT_OK) return st;
   NAT_REQUIRE_DEV(samples);
   NAT_REQUIRE_DEV(p);
@@ -572,7 +600,7 @@ extern "C" nat_status nat_mc_apply_rows(nat_prec prec, int64_t M, const double* 
   carve_near(c, &np, M);
   double* tgt = c.take<double>((size_t)3 * rows);
   const size_t rad_bytes =
-      std::max(nat::radiate_ws_bytes(prec, M, n_sys, rows, 1), nat::radiate_ws_bytes(prec, M, n_sys, rows, 2));
+      std::max(nat::radiate_ws_bytes(prec, M, n_sys, rows, 1, M), nat::radiate_ws_bytes(prec, M, n_sys, rows, 2, M));
   void* rad = c.take<char>(rad_bytes);
   if (ws_bytes < c.bytes()) return nat::fail(NAT_ERR_WORKSPACE, "workspace %zu < %zu", ws_bytes, c.bytes());
   if (prec == NAT_FP32 && eps > 0) {
@@ -662,6 +690,7 @@ extern "C" nat_status nat_mc_surface_pressure(const nat_mesh* mesh, const nat_ge
                                               nat_prec prec, double tol, int max_iter, double* samples_out,
                                               int32_t* sample_tri_out, void* p_out, void* ws, size_t ws_bytes,
                                               nat_solve_info* info, nat_stream_t stream) {
+  NAT_TRACE();
   auto t_start = std::chrono::steady_clock::now();
   NAT_REQUIRE(mesh && geom && opts, "mesh, geom and opts must be non-null");
   NAT_REQUIRE(prec == NAT_FP32 || prec == NAT_FP64, "bad precision %d", (int)prec);
@@ -694,9 +723,9 @@ extern "C" nat_status nat_mc_surface_pressure(const nat_mesh* mesh, const nat_ge
     if (st != NAT_OK) return st;
   }
   // disk radius and off-disk weight (readings R-eps, R-weight)
-  const double area = geom->total_area;
-  const double eps = opts->eps > 0 ? opts->eps : std::sqrt(area / (nat::kPi * (double)M));
-  const double wgt = M > 1 ? (area - nat::kPi * eps * eps) / (double)(M - 1) : 0.0;
+  double eps, wgt;
+  st = mc_eps_w(geom->total_area, M, opts->eps, &eps, &wgt);
+  if (st != NAT_OK) return st;
   const double* cen = geom->center;
   if (M > 1) {
     // close pairs (fp32 r <= 2 eps); every coincident pair (fp64 r < 1e-12) is among them,
@@ -808,7 +837,11 @@ size_t mc_shard_carve(nat::Carver& c, McShardWs* w, nat_prec prec, int64_t M, in
   t.tgt = c.take<double>((size_t)3 * rpr);
   t.tin = c.take<double2>((size_t)nb * ldv);
   nat::krylov_workspace(nb, M, ldv, max_iter, c, &t.kw);
-  t.rad_bytes = std::max(nat::radiate_ws_bytes(prec, M, nb, rpr, 1), nat::radiate_ws_bytes(prec, M, nb, rpr, 2));
+  // the operator shrinks to the active systems: the largest workspace over 1..nb systems
+  t.rad_bytes = 0;
+  for (int m = 1; m <= nb; ++m)
+    t.rad_bytes = std::max(t.rad_bytes, std::max(nat::radiate_ws_bytes(prec, M, m, rpr, 1, M),
+                                                 nat::radiate_ws_bytes(prec, M, m, rpr, 2, M)));
   t.rad = c.take<char>(t.rad_bytes);
   carve_near(c, &t.np, M);
   if (w) *w = t;
@@ -829,6 +862,7 @@ extern "C" nat_status nat_mc_surface_pressure_sharded(nat_comm* comm, const nat_
                                                       int max_iter, double* samples_out, int32_t* sample_tri_out,
                                                       void* p_out, void* ws, size_t ws_bytes, nat_solve_info* info,
                                                       nat_stream_t stream) {
+  NAT_TRACE();
   auto t_start = std::chrono::steady_clock::now();
   NAT_REQUIRE(mesh && geom && opts, "mesh, geom and opts must be non-null");
   NAT_REQUIRE(prec == NAT_FP32 || prec == NAT_FP64, "bad precision %d", (int)prec);
@@ -848,9 +882,11 @@ extern "C" nat_status nat_mc_surface_pressure_sharded(nat_comm* comm, const nat_
   const int rank = comm ? comm->rank : 0, world = comm ? comm->world : 1;
   NAT_REQUIRE(world <= 64, "world size %d > 64", world);
   const int64_t rpr = (M + world - 1) / world, ldv = rpr * world;
+  // every rank evaluates the same condition (no rank fails alone before a collective)
+  NAT_REQUIRE((int64_t)(world - 1) * rpr < M, "the last of %d ranks owns no sample rows (M = %lld)", world,
+              (long long)M);
   const int64_t r0 = std::min<int64_t>(M, (int64_t)rank * rpr), r1 = std::min<int64_t>(M, r0 + rpr);
   const int64_t rows = r1 - r0;
-  NAT_REQUIRE(rows >= 1, "rank %d owns no sample rows (M = %lld, world = %d)", rank, (long long)M, world);
   nat::Carver c(ws);
   McShardWs w;
   const size_t need = mc_shard_carve(c, &w, prec, M, n_sys, max_iter, world);
@@ -865,9 +901,9 @@ extern "C" nat_status nat_mc_surface_pressure_sharded(nat_comm* comm, const nat_
     st = nat_mc_sample(mesh, geom, M, opts->seed, opts->stream_id, samples_out, sample_tri_out, stream);
     if (st != NAT_OK) return st;
   }
-  const double area = geom->total_area;
-  const double eps = opts->eps > 0 ? opts->eps : std::sqrt(area / (nat::kPi * (double)M));
-  const double wgt = (area - nat::kPi * eps * eps) / (double)(M - 1);
+  double eps, wgt;
+  st = mc_eps_w(geom->total_area, M, opts->eps, &eps, &wgt);
+  if (st != NAT_OK) return st;
   const double* cen = geom->center;
   st = build_near(w.np, M, samples_out, cen, eps, s);
   if (st != NAT_OK) return st;
@@ -887,11 +923,19 @@ extern "C" nat_status nat_mc_surface_pressure_sharded(nat_comm* comm, const nat_
   rr.rows = rows;
   rr.tgt = w.tgt;
   int n_comm = 0;
+  // one grouped all-gather of every system's iterate per operator application (every rank
+  // issues the same groups in the same order); CUDA events around each for t_comm_s
   auto gather_all = [&](double2* full, int nb, cudaStream_t ss) -> nat_status {
     if (world == 1) return NAT_OK;
-    for (int q = 0; q < nb; ++q) {  // every rank issues the same collectives in the same order
-      nat_status r = nat::allgather_inplace(comm, (double*)(full + (size_t)q * ldv), (size_t)rpr * 2, ss);
-      if (r != NAT_OK) return r;
+    std::vector<double*> bufs(nb);
+    for (int q = 0; q < nb; ++q) bufs[q] = (double*)(full + (size_t)q * ldv);
+    cudaEvent_t e0 = info ? nat::timing_event(1, 2 * n_comm) : nullptr;
+    cudaEvent_t e1 = info ? nat::timing_event(1, 2 * n_comm + 1) : nullptr;
+    if (e0 && e1) NAT_CUDA_TRY(cudaEventRecord(e0, ss));
+    nat_status r = nat::allgather_inplace_many(comm, bufs.data(), nb, (size_t)rpr * 2, ss);
+    if (r != NAT_OK) return r;
+    if (e0 && e1) {
+      NAT_CUDA_TRY(cudaEventRecord(e1, ss));
       ++n_comm;
     }
     return NAT_OK;
@@ -954,13 +998,20 @@ extern "C" nat_status nat_mc_surface_pressure_sharded(nat_comm* comm, const nat_
         info[s0 + q].converged = res[q].converged;
         info[s0 + q].rel_residual = res[q].rel_residual;
         info[s0 + q].t_matvec_s = t_op;
-        info[s0 + q].t_comm_s = 0;
       }
   }
   NAT_CUDA_TRY(cudaStreamSynchronize(s));
   const double tt = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+  double t_comm = 0.0;
+  for (int q = 0; q < n_comm; ++q) {
+    float ms = 0.f;
+    NAT_CUDA_TRY(cudaEventElapsedTime(&ms, nat::timing_event(1, 2 * q), nat::timing_event(1, 2 * q + 1)));
+    t_comm += 1e-3 * ms;
+  }
   if (info)
-    for (int q = 0; q < n_sys; ++q) info[q].t_total_s = tt;
-  (void)n_comm;
+    for (int q = 0; q < n_sys; ++q) {
+      info[q].t_total_s = tt;
+      info[q].t_comm_s = t_comm;  // device time of the grouped all-gathers (all systems)
+    }
   return all_conv ? NAT_OK : NAT_WARN_NOT_CONVERGED;
 }

@@ -227,6 +227,7 @@ extern "C" size_t nat_mesh_prepare_workspace(int64_t n_vert, int64_t n_tri) {
 
 extern "C" nat_status nat_mesh_prepare(const nat_mesh* mesh, nat_geom* geom, void* ws,
                                        size_t ws_bytes, nat_stream_t stream) {
+  NAT_TRACE();
   NAT_REQUIRE(mesh && geom, "mesh and geom must be non-null");
   NAT_REQUIRE(mesh->n_vert >= 3 && mesh->n_tri >= 1, "need n_vert >= 3 and n_tri >= 1");
   NAT_REQUIRE(geom->n_tri == mesh->n_tri, "geom->n_tri (%lld) != mesh->n_tri (%lld)",
@@ -274,6 +275,7 @@ extern "C" nat_status nat_mesh_prepare(const nat_mesh* mesh, nat_geom* geom, voi
 extern "C" nat_status nat_listener_grid(const double* center, double R, int n_theta, int n_phi,
                                         int n_r, double r_lo, double r_hi, double* out,
                                         nat_stream_t stream) {
+  NAT_TRACE();
   NAT_REQUIRE(center, "center must be a host pointer to 3 doubles");
   NAT_REQUIRE(n_theta > 0 && n_phi > 0 && n_r > 0, "grid sizes must be positive");
   NAT_REQUIRE(R > 0 && r_lo > 0 && r_hi >= r_lo, "need R > 0, 0 < r_lo <= r_hi");
@@ -288,6 +290,7 @@ extern "C" nat_status nat_listener_grid(const double* center, double R, int n_th
 extern "C" nat_status nat_listener_random_shell(const double* center, double R, int64_t n, double r_lo,
                                                 double r_hi, uint64_t seed, uint64_t stream_id, double* out,
                                                 nat_stream_t stream) {
+  NAT_TRACE();
   NAT_REQUIRE(center, "center must be a host array of 3");
   NAT_REQUIRE(n >= 1, "need n >= 1");
   NAT_REQUIRE(R > 0 && r_lo > 0 && r_hi >= r_lo, "need R > 0, 0 < r_lo <= r_hi");

@@ -1,5 +1,6 @@
 // Internal helpers of libnat (not part of the ABI).
 #pragma once
+#include <nvtx3/nvToolsExt.h>
 #include <cuda_runtime.h>
 
 #include <cstdarg>
@@ -20,6 +21,16 @@ constexpr double kInv4Pi = 0.0795774715459476678844418816862571810;
 constexpr int kNumSMs = 148;
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// NVTX range around every nat_* entry point (named after the call; header-only NVTX v3,
+// a no-op unless a tool such as nsys / ncu --nvtx is attached).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+#define NAT_TRACE() ::nat::NvtxRange nat_nvtx_range_(__func__)
 
 // Carves sub-buffers out of a caller workspace (256-byte aligned pieces).
 struct Carver {

@@ -306,6 +306,7 @@ extern "C" nat_status nat_bem_near_count(const nat_mesh* mesh, const nat_geom* g
                                          const nat_quad_opts* opts, int64_t row_begin,
                                          int64_t row_end, int64_t* row_ptr, int64_t* nnz, void* ws,
                                          size_t ws_bytes, nat_stream_t stream) {
+  NAT_TRACE();
   nat_status st = check_args(mesh, geom, row_begin, row_end);
   if (st != NAT_OK) return st;
   NAT_REQUIRE(nnz, "nnz must be a host pointer");
@@ -335,6 +336,7 @@ extern "C" nat_status nat_bem_near_build(const nat_mesh* mesh, const nat_geom* g
                                          const nat_quad_opts* opts, int64_t row_begin,
                                          int64_t row_end, const int64_t* row_ptr, int32_t* col,
                                          uint8_t* cls, void* ws, size_t ws_bytes, nat_stream_t stream) {
+  NAT_TRACE();
   nat_status st = check_args(mesh, geom, row_begin, row_end);
   if (st != NAT_OK) return st;
   NAT_REQUIRE_DEV(row_ptr);

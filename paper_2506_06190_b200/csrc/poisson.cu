@@ -283,6 +283,7 @@ extern "C" nat_status nat_mc_poisson_sample(const nat_mesh* mesh, const nat_geom
                                             uint64_t seed, uint64_t stream_id, double* samples_out,
                                             int32_t* sample_tri_out, int64_t cap, int64_t* M_out, double* r_out,
                                             void* ws, size_t ws_bytes, nat_stream_t stream) {
+  NAT_TRACE();
   NAT_REQUIRE(mesh && geom && M_out, "mesh, geom and M_out must be non-null");
   NAT_REQUIRE(geom->n_tri == mesh->n_tri && mesh->n_tri >= 1, "inconsistent n_tri");
   PoissonPlan p;

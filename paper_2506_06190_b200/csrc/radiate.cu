@@ -672,6 +672,11 @@ Plan make_plan(nat_prec prec, int64_t n_src, int n_modes, int64_t n_lis, int kin
     }
   }
   pl.n_split = (pl.n_tiles + pl.chunk_tiles - 1) / pl.chunk_tiles;
+  static const bool dbg = std::getenv("NAT_DEBUG_PLAN") != nullptr;
+  if (dbg)
+    std::fprintf(stderr, "[plan] kind %d modes %d src %lld lis %lld: R %d NT %d MB %d chunk %d split %d tgt %lld occ %d smem %zu\n",
+                 pl.kind, n_modes, (long long)n_src, (long long)n_lis, pl.R, pl.NT, pl.MB, pl.chunk_tiles, pl.n_split,
+                 (long long)pl.tgt_tiles, occupancy(pl.fp64, pl.kind, pl.R, pl.MB, pl.NT, pl.smem), pl.smem);
   pl.rec_elems = (size_t)pl.n_mchunk * pl.n_src_pad * pl.NF;
   return pl;
 }
@@ -713,10 +718,17 @@ cudaError_t launch_f32_mb(const Plan& pl, const RadParams& prm, cudaStream_t s) 
 
 namespace nat {
 
-size_t radiate_ws_bytes(nat_prec prec, int64_t n_src, int n_modes, int64_t n_lis, int kind) {
+// The launch shape for n_lis targets, chosen as for plan_lis targets when plan_lis > 0.
+Plan plan_for(nat_prec prec, int64_t n_src, int nm, int64_t n_lis, int kind, int64_t plan_lis) {
+  Plan pl = make_plan(prec, n_src, nm, plan_lis > 0 ? plan_lis : n_lis, kind);
+  pl.tgt_tiles = (n_lis + (int64_t)pl.R * pl.NT - 1) / ((int64_t)pl.R * pl.NT);
+  return pl;
+}
+
+size_t radiate_ws_bytes(nat_prec prec, int64_t n_src, int n_modes, int64_t n_lis, int kind, int64_t plan_lis) {
   if (n_src <= 0 || n_modes <= 0 || n_lis <= 0) return 0;
   const int nm = n_modes < kMaxModes ? n_modes : kMaxModes;
-  Plan pl = make_plan(prec, n_src, nm, n_lis, kind);
+  Plan pl = plan_for(prec, n_src, nm, n_lis, kind, plan_lis);
   Carver c(nullptr);
   void* rec;
   double2* part;
@@ -739,7 +751,7 @@ nat_status radiate_internal(const RadInput& in, nat_prec prec, const double* k, 
   const int kind = !self ? 0 : (in.p ? 1 : 2);
   for (int m0 = 0; m0 < in.n_modes; m0 += kMaxModes) {
     const int nm = (in.n_modes - m0) < kMaxModes ? (in.n_modes - m0) : kMaxModes;
-    Plan pl = make_plan(prec, in.n_src, nm, n_lis, kind);
+    Plan pl = plan_for(prec, in.n_src, nm, n_lis, kind, in.plan_lis);
     Carver c(ws);
     void* rec;
     double2* part;
@@ -818,6 +830,7 @@ extern "C" size_t nat_radiate_workspace(nat_prec prec, int64_t n_src, int n_mode
 extern "C" nat_status nat_radiate_field(const nat_sources* src, nat_prec prec, const double* k,
                                         int64_t n_lis, const double* lis_xyz, void* p_out, void* ws,
                                         size_t ws_bytes, nat_stream_t stream) {
+  NAT_TRACE();
   NAT_REQUIRE(src && k, "src and k must be non-null");
   NAT_REQUIRE(prec == NAT_FP32 || prec == NAT_FP64, "bad precision %d", (int)prec);
   NAT_REQUIRE(src->n_src > 0 && src->n_modes > 0 && n_lis > 0, "need n_src, n_modes, n_lis > 0");
@@ -871,6 +884,7 @@ extern "C" nat_status nat_bem_sources(const nat_mesh* mesh, const nat_geom* geom
                                       int n_modes, const void* p_tri, const void* g_tri, double* xyz,
                                       double* nrm, double* w, void* p_src, void* g_src,
                                       nat_stream_t stream) {
+  NAT_TRACE();
   NAT_REQUIRE(mesh && geom, "mesh and geom must be non-null");
   if (q_rad == 0) q_rad = 3;
   double lam[9], wq[3];
@@ -902,6 +916,7 @@ extern "C" nat_status nat_bem_sources(const nat_mesh* mesh, const nat_geom* geom
 
 extern "C" nat_status nat_mc_sources(int64_t M, const double* samples, double total_area, double* xyz,
                                      double* nrm, double* w, nat_stream_t stream) {
+  NAT_TRACE();
   NAT_REQUIRE(M >= 1 && total_area > 0, "need M >= 1 and total_area > 0");
   NAT_REQUIRE_DEV(samples);
   NAT_REQUIRE_DEV(xyz);

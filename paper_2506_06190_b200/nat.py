@@ -56,7 +56,7 @@ class _BemMf(C.Structure):
     _fields_ = [("mesh", C.POINTER(_Mesh)), ("geom", C.POINTER(_Geom)), ("opts", C.POINTER(_QuadOpts)),
                 ("k", C.c_double), ("prec", C.c_int), ("row_begin", C.c_int64), ("row_end", C.c_int64),
                 ("near_row_ptr", C.c_void_p), ("near_col", C.c_void_p), ("near_cls", C.c_void_p),
-                ("near_delta", C.c_void_p), ("diag_delta", C.c_void_p)]
+                ("nnz", C.c_int64), ("near_delta", C.c_void_p), ("diag_delta", C.c_void_p)]
 
 
 class _McOpts(C.Structure):
@@ -87,7 +87,7 @@ _SIGS = {
                                      _I64, _I64, _P, _P, _P, _P, _SZ, _P]),
     "nat_bem_assemble_workspace": (_SZ, [_I64, _I64, _I64, C.c_int]),
     "nat_bem_assemble": (C.c_int, [C.POINTER(_Mesh), C.POINTER(_Geom), C.POINTER(_QuadOpts),
-                                   _P, _P, _P, _D, C.c_int, _I64, _I64, C.c_int, _P, _P, _I64,
+                                   _P, _P, _P, _I64, _D, C.c_int, _I64, _I64, C.c_int, _P, _P, _I64,
                                    _P, _P, _SZ, _P]),
     "nat_bem_matvec": (C.c_int, [C.c_int, _I64, _I64, _P, _I64, _P, _P, _P]),
     "nat_bem_mf_workspace": (_SZ, [C.POINTER(_BemMf), _I64, C.c_int]),
@@ -103,6 +103,7 @@ _SIGS = {
     "nat_comm_create_from_id": (C.c_int, [C.POINTER(_P), _P, C.c_int, C.c_int]),
     "nat_comm_create": (C.c_int, [C.POINTER(_P), _P, C.c_int, C.c_int]),
     "nat_comm_destroy": (C.c_int, [_P]),
+    "nat_comm_create_host": (C.c_int, [C.POINTER(_P), C.c_int, C.c_int, _P, _P]),
     "nat_bem_solve_workspace": (_SZ, [C.c_int, _I64, _I64, C.c_int]),
     "nat_bem_solve": (C.c_int, [_P, C.c_int, _I64, _I64, _I64, _P, _I64, _P, _P, _D, C.c_int,
                                 _P, _SZ, C.POINTER(_SolveInfo), _P]),
@@ -417,7 +418,7 @@ def nat_bem_assemble(mesh: Mesh, geom: Geom, near: NearList, k: float, g=None, p
     ws = _ws(lib().nat_bem_assemble_workspace(n, rows, near.nnz, n_rhs), dev)
     _check(lib().nat_bem_assemble(C.byref(mesh.c()), C.byref(geom.c()), C.byref(o), _ptr(near.row_ptr),
                                   C.c_void_p(near.col.data_ptr()), C.c_void_p(near.cls.data_ptr()),
-                                  float(k), pr, near.row_begin, near.row_end, n_rhs, _ptr(g), _ptr(A),
+                                  int(near.nnz), float(k), pr, near.row_begin, near.row_end, n_rhs, _ptr(g), _ptr(A),
                                   lda, _ptr(rhs), _ptr(ws), ws.numel(), _stream()))
     return A, rhs
 
@@ -432,12 +433,21 @@ def nat_bem_matvec(A: torch.Tensor, x: torch.Tensor, n: Optional[int] = None, ou
     return out
 
 
-class Comm:
-    """NCCL communicator built from a torch.distributed-broadcast unique id."""
+_AllGatherFn = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.c_size_t, C.c_int, C.c_int)
 
-    def __init__(self, rank: int, world: int, uid: Optional[bytes] = None, nccl_comm: Optional[int] = None):
+
+class Comm:
+    """NCCL communicator built from a torch.distributed-broadcast unique id (or, for tests
+    of the world > 1 path on one GPU, the host-staged backend over a gloo group)."""
+
+    def __init__(self, rank: int, world: int, uid: Optional[bytes] = None, nccl_comm: Optional[int] = None,
+                 _host_fn=None):
         self.rank, self.world = rank, world
         self.handle = C.c_void_p()
+        if _host_fn is not None:   # nat_comm_create_host (keeps the callback alive)
+            self._cb = _AllGatherFn(_host_fn)
+            _check(lib().nat_comm_create_host(C.byref(self.handle), rank, world, C.cast(self._cb, C.c_void_p), None))
+            return
         if uid is None:   # borrow a caller-owned ncclComm_t (or none: world 1)
             _check(lib().nat_comm_create(C.byref(self.handle), C.c_void_p(nccl_comm), rank, world))
             return
@@ -467,6 +477,27 @@ class Comm:
             t.copy_(torch.frombuffer(bytearray(uid), dtype=torch.uint8))
         dist.broadcast(t, 0)
         return bytes(t.cpu().numpy().tobytes())
+
+    @classmethod
+    def host(cls, group=None):
+        """Host-staged communicator: every all-gather of the library runs as
+        torch.distributed.all_gather on `group` (e.g. gloo) over a pinned host buffer.  No
+        kernel waits on another rank, so several ranks may share one GPU (tests)."""
+        import torch.distributed as dist
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+
+        def fn(user, buf, count, rk, ws):
+            try:
+                arr = np.ctypeslib.as_array(buf, shape=(int(count) * ws,))
+                t = torch.from_numpy(arr)
+                parts = [t[r * count:(r + 1) * count] for r in range(ws)]
+                mine = parts[rk].clone()
+                dist.all_gather(parts, mine, group=group)
+                return 0
+            except Exception:  # reported by the library as NAT_ERR_NCCL
+                return 1
+
+        return cls(rank, world, _host_fn=fn)
 
     @classmethod
     def from_torch_distributed(cls):
@@ -532,35 +563,28 @@ def nat_mc_poisson_sample(mesh: Mesh, geom: Geom, M_target: int, seed: int = 0, 
     return smp[: 6 * M].view(6, M), tri[:M], rr.value
 
 
-def mc_weights(total_area: float, M: int, eps: float = 0.0):
-    """(eps, w) of readings R-eps / R-weight: eps = sqrt(|Gamma|/(pi M)),
-    w = (|Gamma| - pi eps^2)/(M - 1)."""
-    import math
-    eps = eps if eps > 0 else math.sqrt(total_area / (math.pi * M))
-    w = (total_area - math.pi * eps * eps) / (M - 1) if M > 1 else 0.0
-    return eps, w
-
-
-def nat_mc_rhs(samples, k, g, w, eps, prec="fp32"):
+def nat_mc_rhs(samples, k, g, total_area, eps=0.0, prec="fp32"):
+    """a9 right-hand sides; the library derives eps (unless eps > 0) and w from total_area."""
     pr = _prec(prec)
     M = samples.shape[1]
     g = torch.atleast_2d(g).to(torch.complex128).contiguous()
     ks, kp = _karr(k)
     b = torch.empty_like(g)
     ws = _ws(lib().nat_mc_op_workspace(pr, M, g.shape[0]), samples.device)
-    _check(lib().nat_mc_rhs(pr, M, _ptr(samples), g.shape[0], kp, _ptr(g), float(w), float(eps), _ptr(b),
+    _check(lib().nat_mc_rhs(pr, M, _ptr(samples), g.shape[0], kp, _ptr(g), float(total_area), float(eps), _ptr(b),
                             _ptr(ws), ws.numel(), _stream()))
     return b
 
 
-def nat_mc_apply(samples, k, p, w, eps, prec="fp32"):
+def nat_mc_apply(samples, k, p, total_area, eps=0.0, prec="fp32"):
+    """a10 operator applied to p; eps (unless > 0) and w derived from total_area by the library."""
     pr = _prec(prec)
     M = samples.shape[1]
     p = torch.atleast_2d(p).to(torch.complex128).contiguous()
     ks, kp = _karr(k)
     out = torch.empty_like(p)
     ws = _ws(lib().nat_mc_op_workspace(pr, M, p.shape[0]), samples.device)
-    _check(lib().nat_mc_apply(pr, M, _ptr(samples), p.shape[0], kp, _ptr(p), float(w), float(eps), _ptr(out), _ptr(ws),
+    _check(lib().nat_mc_apply(pr, M, _ptr(samples), p.shape[0], kp, _ptr(p), float(total_area), float(eps), _ptr(out), _ptr(ws),
                               ws.numel(), _stream()))
     return out
 
@@ -601,7 +625,7 @@ def nat_mc_surface_pressure(mesh: Mesh, geom: Geom, k, g_tri, M: int, seed: int 
                               t_total_s=i.t_total_s, t_matvec_s=i.t_matvec_s) for i in infos]
 
 
-def nat_mc_apply_rows(samples, k, p, w, eps, row_begin: int, row_end: int, prec="fp32"):
+def nat_mc_apply_rows(samples, k, p, total_area, eps, row_begin: int, row_end: int, prec="fp32"):
     """Rows [row_begin, row_end) of the MC operator applied to p (n_sys, M) -> (n_sys, rows)."""
     pr = _prec(prec)
     M = samples.shape[1]
@@ -610,7 +634,7 @@ def nat_mc_apply_rows(samples, k, p, w, eps, row_begin: int, row_end: int, prec=
     rows = max(int(row_end) - int(row_begin), 1)   # the library validates the range
     out = torch.empty(ks.size, rows, dtype=torch.complex128, device=samples.device)
     ws = _ws(lib().nat_mc_rows_workspace(pr, M, ks.size, rows), samples.device)
-    _check(lib().nat_mc_apply_rows(pr, M, _ptr(samples), ks.size, kp, _ptr(p), float(w), float(eps), int(row_begin),
+    _check(lib().nat_mc_apply_rows(pr, M, _ptr(samples), ks.size, kp, _ptr(p), float(total_area), float(eps), int(row_begin),
                                    int(row_end), _ptr(out), _ptr(ws), ws.numel(), _stream()))
     return out
 
@@ -689,7 +713,7 @@ class BemMf:
         self._o = opts or quad_opts()
         self.c = _BemMf(C.pointer(self._m), C.pointer(self._g), C.pointer(self._o), self.k, self.prec,
                         near.row_begin, near.row_end, _ptr(near.row_ptr), C.c_void_p(near.col.data_ptr()),
-                        C.c_void_p(near.cls.data_ptr()), _ptr(self.delta), _ptr(self.diag))
+                        C.c_void_p(near.cls.data_ptr()), int(near.nnz), _ptr(self.delta), _ptr(self.diag))
         self._ws = None
 
     @property

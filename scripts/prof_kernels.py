@@ -24,11 +24,11 @@ def main():
         src = nat.nat_bem_sources(mesh, geo, x3, torch.cat([g, g, g]))
         nat.nat_radiate_field(src, [0.5, 2.0, 8.0], lis, "fp32")   # the bench's 3 fused wavenumbers
         smp, stri = nat.nat_mc_sample(mesh, geo, 10000, 20250606)
-        eps, w = nat.mc_weights(geo.total_area, 10000)
+        area = geo.total_area
         p = torch.ones(3, 10000, dtype=torch.complex128, device="cuda")
-        nat.nat_mc_apply(smp, [0.5, 2.0, 8.0], p, w, eps, "fp32")
-        nat.nat_mc_apply(smp, [8.0], p[:1], w, eps, "fp32")
-        nat.nat_mc_rhs(smp, [0.5, 2.0, 8.0], p, w, eps, "fp32")
+        nat.nat_mc_apply(smp, [0.5, 2.0, 8.0], p, area, 0.0, "fp32")
+        nat.nat_mc_apply(smp, [8.0], p[:1], area, 0.0, "fp32")
+        nat.nat_mc_rhs(smp, [0.5, 2.0, 8.0], p, area, 0.0, "fp32")
         torch.cuda.synchronize()
     print("ok")
 

@@ -31,7 +31,7 @@ def test_library_exports_every_declared_symbol():
     missing = [n for n in _declared() if not hasattr(L, n)]
     assert not missing, missing
     assert set(_declared()) == set(nat.exported_symbols())
-    assert L.nat_abi_version() == 1
+    assert L.nat_abi_version() == 2
 
 
 def test_binding_refuses_cpu_tensors():

@@ -212,3 +212,29 @@ def test_borrowed_single_rank_communicator_matches_no_communicator():
     assert i0["iters"] == i1["iters"] and torch.equal(x0, x1)
     with pytest.raises(nat.NatError):
         nat.Comm.borrow(None, 0, 2)     # a NULL ncclComm_t cannot have two ranks
+
+
+@pytest.mark.parametrize("prec", ["fp32", "fp64"])
+@pytest.mark.parametrize("far_pts", [1, 6, 7])
+def test_assembly_other_far_rules(prec, far_pts):
+    """nat_quad_opts.far_pts 1 / 6 / 7 (R-colloc): the 1- and 7-point rules contain the
+    centroid, i.e. the row's own collocation point, so the far rule is singular on the self
+    pair; the far kernels zero it and the self kernel adds the exact polar value.  Parity
+    with the oracle using the same rule, and finite everywhere (matrix-free operator too)."""
+    nat = _nat()
+    m, geo, near = _oracle_case("ico2")
+    g = I.neumann_rigid_z(m)[None]
+    A_ref, b_ref = bem.assemble(m.v, m.t, geo, 2.0, g, near=near, opts=dict(far_pts=far_pts))
+    mesh, gg = _gpu_case(m)
+    o = nat.quad_opts(far_pts=far_pts)
+    nl = nat.nat_bem_near_list(mesh, gg, opts=o)
+    A, b = nat.nat_bem_assemble(mesh, gg, nl, 2.0, torch.from_numpy(g).cuda(), prec=prec, opts=o)
+    A = to_np(A)[:, : m.n_tri]
+    assert np.all(np.isfinite(A)) and np.all(np.isfinite(to_np(b)))
+    assert rel_l2(A, A_ref) <= TOL[prec]
+    assert rel_l2(to_np(b)[0], b_ref[0]) <= TOL[prec]
+    op, rhs = nat.nat_bem_mf_prepare(mesh, gg, nl, 2.0, torch.from_numpy(g).cuda(), prec=prec, opts=o)
+    x = I.random_complex(m.n_tri, 4)
+    y = to_np(nat.nat_bem_mf_matvec(op, torch.from_numpy(x).cuda()))
+    assert np.all(np.isfinite(y)) and rel_l2(y, A_ref @ x) <= TOL[prec]
+    assert rel_l2(to_np(rhs)[0], b_ref[0]) <= TOL[prec]

@@ -49,20 +49,23 @@ def _system_case(M, seed=5):
 
 
 @pytest.mark.parametrize("prec", ["fp32", "fp64"])
-@pytest.mark.parametrize("n_sys", [1, 3, 6])
-def test_mc_operator_and_rhs_parity(prec, n_sys):
+@pytest.mark.parametrize("n_sys,eps", [(1, 0.0), (3, 0.0), (6, 0.0), (3, 0.004), (1, 0.05)])
+def test_mc_operator_and_rhs_parity(prec, n_sys, eps):
+    """a9 / a10 against the oracle's dense Eq. SYS; eps = 0 lets the library derive the
+    default disk radius, eps > 0 is a caller radius (readings R-eps / R-weight: the library
+    forms w = (|Gamma| - pi eps^2) / (M - 1) itself; the larger radius widens the fp64
+    close-pair band of the fp32 path)."""
     nat = _nat()
     M = 2333     # dense enough that random samples form close pairs (fp64 path)
     m, geo, mesh, gg, y, n, tri = _system_case(M)
     ks = list(np.linspace(0.5, 6.0, n_sys))
-    eps, w = nat.mc_weights(geo["total_area"], M)
     g = I.random_complex((n_sys, M), 11)
     p = I.random_complex((n_sys, M), 12)
     smp = torch.from_numpy(np.ascontiguousarray(np.concatenate([y.T, n.T]))).cuda()
-    b = to_np(nat.nat_mc_rhs(smp, ks, torch.from_numpy(g).cuda(), w, eps, prec))
-    Ap = to_np(nat.nat_mc_apply(smp, ks, torch.from_numpy(p).cuda(), w, eps, prec))
+    b = to_np(nat.nat_mc_rhs(smp, ks, torch.from_numpy(g).cuda(), geo["total_area"], eps, prec))
+    Ap = to_np(nat.nat_mc_apply(smp, ks, torch.from_numpy(p).cuda(), geo["total_area"], eps, prec))
     for s, k in enumerate(ks):
-        A_ref, b_ref = mc.system(y, n, g[s], k, geo["total_area"])
+        A_ref, b_ref = mc.system(y, n, g[s], k, geo["total_area"], eps if eps > 0 else None)
         assert rel_l2(b[s], b_ref) <= TOL[prec]
         assert rel_l2(Ap[s], A_ref @ p[s]) <= TOL[prec]
 
@@ -154,15 +157,15 @@ def test_mc_operator_row_blocks_ragged(prec):
     M = 2333
     m, geo, mesh, gg, y, n, tri = _system_case(M)
     ks = [0.5, 3.0, 6.0]
-    eps, w = nat.mc_weights(geo["total_area"], M)
+    area, eps = geo["total_area"], 0.0
     p = I.random_complex((3, M), 21)
     smp = torch.from_numpy(np.ascontiguousarray(np.concatenate([y.T, n.T]))).cuda()
     pt = torch.from_numpy(p).cuda()
-    full = to_np(nat.nat_mc_apply(smp, ks, pt, w, eps, prec))
+    full = to_np(nat.nat_mc_apply(smp, ks, pt, area, eps, prec))
     blocks = []
     for r in range(3):
         r0, r1 = nat.row_range(M, r, 3)
-        blocks.append(to_np(nat.nat_mc_apply_rows(smp, ks, pt, w, eps, r0, r1, prec)))
+        blocks.append(to_np(nat.nat_mc_apply_rows(smp, ks, pt, area, eps, r0, r1, prec)))
     got = np.concatenate(blocks, axis=1)
     for s, k in enumerate(ks):
         A_ref, _ = mc.system(y, n, np.zeros(M), k, geo["total_area"])
@@ -197,14 +200,39 @@ def test_row_api_errors():
     nat = _nat()
     M = 300
     m, geo, mesh, gg, y, n, tri = _system_case(M)
-    eps, w = nat.mc_weights(geo["total_area"], M)
+    area = geo["total_area"]
     smp = torch.from_numpy(np.ascontiguousarray(np.concatenate([y.T, n.T]))).cuda()
     p = torch.ones(1, M, dtype=torch.complex128, device="cuda")
     for r0, r1 in ((0, 0), (5, 3), (0, M + 1), (-1, 10)):
         with pytest.raises(nat.NatError, match="row range"):
-            nat.nat_mc_apply_rows(smp, [1.0], p, w, eps, r0, r1)
+            nat.nat_mc_apply_rows(smp, [1.0], p, area, 0.0, r0, r1)
     with pytest.raises(nat.NatError):
-        nat.nat_mc_apply_rows(smp, [1.0], p.cpu(), w, eps, 0, 10)     # host tensor
+        nat.nat_mc_apply_rows(smp, [1.0], p.cpu(), area, 0.0, 0, 10)     # host tensor
+    with pytest.raises(nat.NatError, match="total_area"):
+        nat.nat_mc_apply(smp, [1.0], p, -1.0)
+    with pytest.raises(nat.NatError, match="disk area"):
+        nat.nat_mc_apply(smp, [1.0], p, area, 10.0)                       # pi eps^2 > |Gamma|
     with pytest.raises(nat.NatError, match="M must be"):
         nat.nat_mc_surface_pressure_sharded(mesh, gg, [1.0], torch.ones(1, m.n_tri, dtype=torch.complex128,
                                                                          device="cuda"), 1)
+
+
+@pytest.mark.parametrize("prec", ["fp32", "fp64"])
+def test_surface_pressure_caller_eps(prec):
+    """The whole solve at a caller disk radius (opts->eps > 0; readings R-eps, R-weight:
+    the library forms w = (|Gamma| - pi eps^2)/(M - 1)) against the oracle at the same eps."""
+    nat = _nat()
+    m = I.bowl(32, 8, 2)
+    geo, mesh, gg = _case(m)
+    M, seed, eps = 500, 5, 0.03
+    ks = [1.0, 3.0]
+    g_tri = I.neumann_harmonics(m, 2)
+    y, n, tri, p_ref, _ = mc.surface_pressure(m.v, m.t, geo, ks, g_tri, M, seed, eps=eps, tol=1e-13)
+    _, _, _, p_def, _ = mc.surface_pressure(m.v, m.t, geo, ks, g_tri, M, seed, tol=1e-13)
+    tol = 1e-6 if prec == "fp32" else 1e-12
+    _, _, p, info = nat.nat_mc_surface_pressure(mesh, gg, ks, torch.from_numpy(g_tri).cuda(), M, seed, eps=eps,
+                                                prec=prec, tol=tol)
+    for s in range(2):
+        assert info[s]["converged"] == 1
+        assert rel_l2(to_np(p)[s], p_ref[s]) <= TOL[prec]
+        assert rel_l2(p_def[s], p_ref[s]) > 100 * TOL[prec]   # the radius changes the solution
