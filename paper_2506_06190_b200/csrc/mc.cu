@@ -296,8 +296,10 @@ void carve_near(nat::Carver& c, NearPairs* np, int64_t M) {
   if (np) *np = t;
 }
 
+// check = false: no read-back; the caller checks *np.overflow after its own final sync
+// (the MC solve never stalls the host before its Krylov loop)
 nat_status build_near(NearPairs& np, int64_t M, const double* smp, const double* center, double eps,
-                      cudaStream_t s) {
+                      cudaStream_t s, bool check = true) {
   np.on = true;
   np.thr = (float)(4.0 * eps * eps);
   const double cx = center ? center[0] : 0.0, cy = center ? center[1] : 0.0, cz = center ? center[2] : 0.0;
@@ -307,6 +309,7 @@ nat_status build_near(NearPairs& np, int64_t M, const double* smp, const double*
   scan32_kernel<<<1, 1024, 0, s>>>(np.rp, M, np.cap, np.overflow);
   mc_near_kernel<true><<<grid, kNT, 0, s>>>(M, smp, cx, cy, cz, np.thr, np.rp, np.col, np.cap, np.overflow);
   NAT_LAUNCH_CHECK();
+  if (!check) return NAT_OK;
   int ov = 0;
   NAT_CUDA_TRY(cudaMemcpyAsync(&ov, np.overflow, sizeof(int), cudaMemcpyDeviceToHost, s));
   NAT_CUDA_TRY(cudaStreamSynchronize(s));
@@ -729,19 +732,28 @@ extern "C" nat_status nat_mc_surface_pressure(const nat_mesh* mesh, const nat_ge
   const double* cen = geom->center;
   if (M > 1) {
     // close pairs (fp32 r <= 2 eps); every coincident pair (fp64 r < 1e-12) is among them,
-    // so the singularity check only scans this list
-    st = build_near(w.np, M, samples_out, cen, eps, s);
+    // so the singularity check only scans this list.  Both checks are read back
+    // after the solve (deferred): the host does not stall before the Krylov loop, and a
+    // failed check still returns its error with no valid output.
+    st = build_near(w.np, M, samples_out, cen, eps, s, false);
     if (st != NAT_OK) return st;
     init_best_kernel<<<1, 1, 0, s>>>(w.best);
     coincident_near_kernel<<<(unsigned)((M + 255) / 256), 256, 0, s>>>(M, samples_out, w.np.rp, w.np.col, w.best);
     NAT_LAUNCH_CHECK();
+    w.np.on = (prec == NAT_FP32);  // the fp64 kernel resolves close pairs itself
+  }
+  auto deferred = [&](nat_status solve_st) -> nat_status {
+    if (M <= 1) return solve_st;
     unsigned long long hb = 0;
+    int ov = 0;
     NAT_CUDA_TRY(cudaMemcpyAsync(&hb, w.best, 8, cudaMemcpyDeviceToHost, s));
+    NAT_CUDA_TRY(cudaMemcpyAsync(&ov, w.np.overflow, sizeof(int), cudaMemcpyDeviceToHost, s));
     NAT_CUDA_TRY(cudaStreamSynchronize(s));
     if (hb != ~0ull)
       return nat::fail(NAT_ERR_SINGULAR, "coincident samples (%llu, %llu)", hb >> 32, hb & 0xffffffffull);
-    w.np.on = (prec == NAT_FP32);  // the fp64 kernel resolves close pairs itself
-  }
+    if (ov) return nat::fail(NAT_ERR_WORKSPACE, "more than %lld close sample pairs", (long long)w.np.cap);
+    return solve_st;
+  };
   bool all_conv = true;
   for (int s0 = 0; s0 < n_sys; s0 += 64) {
     const int nb = (n_sys - s0) < 64 ? (n_sys - s0) : 64;
@@ -749,7 +761,7 @@ extern "C" nat_status nat_mc_surface_pressure(const nat_mesh* mesh, const nat_ge
         nb, M, mesh->n_tri, (const double2*)g_tri + (size_t)s0 * mesh->n_tri, sample_tri_out, w.gs);
     NAT_LAUNCH_CHECK();
     st = mc_rhs_impl(prec, M, samples_out, nb, k + s0, w.gs, wgt, eps, w.b, w.rad, w.rad_bytes, cen, w.np, s);
-    if (st != NAT_OK) return st;
+    if (st != NAT_OK) return deferred(st);
     const uint64_t all = nb == 64 ? ~0ull : ((1ull << nb) - 1);
     auto op = [&](const double2* in, double2* out, uint64_t active, const unsigned long long* dmask,
                   cudaStream_t ss) -> nat_status {
@@ -779,7 +791,7 @@ extern "C" nat_status nat_mc_surface_pressure(const nat_mesh* mesh, const nat_ge
     double t_op = 0;
     st = nat::gmres_batched(nb, M, M, w.b, (double2*)p_out + (size_t)s0 * M, op, tol, max_iter, w.kw, res, s,
                             info ? &t_op : nullptr);
-    if (st != NAT_OK) return st;
+    if (st != NAT_OK) return deferred(st);
     for (int q = 0; q < nb; ++q) all_conv = all_conv && res[q].converged;
     if (info)
       for (int q = 0; q < nb; ++q) {
@@ -790,6 +802,8 @@ extern "C" nat_status nat_mc_surface_pressure(const nat_mesh* mesh, const nat_ge
         info[s0 + q].t_comm_s = 0;
       }
   }
+  st = deferred(NAT_OK);
+  if (st != NAT_OK) return st;
   NAT_CUDA_TRY(cudaStreamSynchronize(s));
   double tt = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
   if (info)
