@@ -48,8 +48,8 @@ struct KVals {
 // A1 A2 A3 A4;  kind 2: x y z | B1 B2.  Padded to a multiple of 4 floats (16-byte loads).
 __host__ __device__ constexpr int rec_geo(int kind) { return kind == 2 ? 3 : 6; }
 __host__ __device__ constexpr int rec_per_mode(int kind) { return kind == 0 ? 6 : kind == 1 ? 4 : 2; }
-__host__ __device__ constexpr int rec_nf(int kind, int MB) {  // duplicated floats
-  return (2 * (rec_geo(kind) + rec_per_mode(kind) * MB) + 3) / 4 * 4;
+__host__ __device__ constexpr int rec_nf(int kind, int MB) {  // floats per record, padded to 16 B
+  return ((rec_geo(kind) + rec_per_mode(kind) * MB) + 3) / 4 * 4;
 }
 
 struct RadParams {
@@ -89,7 +89,7 @@ struct RecWriter {
 constexpr int kStageSrc = 128;
 constexpr int kStageMaxBytes = 64 * 4;  // per source: <= 64 floats (fp32) or 32 doubles
 
-template <typename T, bool DUP = false>
+template <typename T, bool DUP = false, int SGN = 1>
 __global__ void __launch_bounds__(kStageSrc) stage_kernel(int64_t n_src, int64_t n_src_pad, int NF, int MB,
                                                          int n_mchunk, int kind,
                              const double* __restrict__ xyz, const double* __restrict__ nrm,
@@ -146,11 +146,11 @@ __global__ void __launch_bounds__(kStageSrc) stage_kernel(int64_t n_src, int64_t
           k = kv.d[mode];
         }
         const int q = G + F * m;
-        if (kind != 2) {
-          wr.put(q + 0, -ar);
-          wr.put(q + 1, -k * ai);
-          wr.put(q + 2, k * ar);
-          wr.put(q + 3, -ai);
+        if (kind != 2) {  // fp32 records (SGN = -1): the kernel forms -d.n (see the main kernel)
+          wr.put(q + 0, SGN * -ar);
+          wr.put(q + 1, SGN * -k * ai);
+          wr.put(q + 2, SGN * k * ar);
+          wr.put(q + 3, SGN * -ai);
         }
         if (kind == 0) {
           wr.put(q + 4, -br);
@@ -268,25 +268,32 @@ __global__ void __launch_bounds__(NT) radiate_f32x2_kernel(RadParams prm) {
   for (int it = 0; t0 + it < t1; ++it) {
     const int st = it & 1;
     nat::mbar_wait(&bars[st], (it >> 1) & 1);
-    const ulonglong2* b4 = reinterpret_cast<const ulonglong2*>(buf + st * kTileFloats);
+    const float4* b4 = reinterpret_cast<const float4*>(buf + st * kTileFloats);
 
     // short bodies (one target pair, one wavenumber) need a deeper unroll so the
     // shared-memory loads of later sources overlap the arithmetic (ncu r01: LDS-wait)
     constexpr int kUnroll = (RP * MB <= 1) ? 4 : 2;
 #pragma unroll kUnroll
     for (int s = 0; s < kTile; ++s) {
-      f2r f[NF / 2];
+      // one scalar per record field (LDS.128 broadcast), used as the .F32 operand of the
+      // packed instructions (both targets of the pair share it)
+      float fs[NF];
 #pragma unroll
       for (int q = 0; q < NF / 4; ++q) {
-        const ulonglong2 v = b4[s * (NF / 4) + q];
-        f[2 * q] = v.x;
-        f[2 * q + 1] = v.y;
+        const float4 v = b4[s * (NF / 4) + q];
+        fs[4 * q] = v.x;
+        fs[4 * q + 1] = v.y;
+        fs[4 * q + 2] = v.z;
+        fs[4 * q + 3] = v.w;
       }
+      auto B = [&](int i) { return f2pack(fs[i], fs[i]); };
 #pragma unroll
       for (int p = 0; p < RP; ++p) {
-        const f2r dx = f2sub(f[0], tx[p]);
-        const f2r dy = f2sub(f[1], ty[p]);
-        const f2r dz = f2sub(f[2], tz[p]);
+        // e = x - y = -d (the record is the broadcast operand); the staged A coefficients
+        // carry the matching sign (d.n = -e.n)
+        const f2r dx = f2sub(tx[p], B(0));
+        const f2r dy = f2sub(ty[p], B(1));
+        const f2r dz = f2sub(tz[p], B(2));
         const f2r r2 = f2fma(dz, dz, f2fma(dy, dy, f2mul(dx, dx)));
         const float r2a = f2lo(r2), r2b = f2hi(r2);
         const float ra = SELF ? (r2a > prm.self_r2 ? rsqrt_approx(r2a) : 0.f) : rsqrt_approx(r2a);
@@ -294,7 +301,7 @@ __global__ void __launch_bounds__(NT) radiate_f32x2_kernel(RadParams prm) {
         const f2r rho = f2pack(ra, rb);
         f2r qq = 0ull;
         if constexpr (KIND != 2) {
-          const f2r dn = f2fma(dz, f[5], f2fma(dy, f[4], f2mul(dx, f[3])));
+          const f2r dn = f2fma(dz, B(5), f2fma(dy, B(4), f2mul(dx, B(3))));  // = -d.n
           qq = f2mul(dn, f2mul(rho, rho));
         }
         const f2r rr = f2mul(r2, rho);
@@ -305,17 +312,17 @@ __global__ void __launch_bounds__(NT) radiate_f32x2_kernel(RadParams prm) {
           __sincosf(f2lo(kr), &sa, &ca);
           __sincosf(f2hi(kr), &sb, &cb);
           const f2r sn = f2pack(sa, sb), cs = f2pack(ca, cb);
-          const f2r* c = f + G + F * m;  // kind 0: A1 A2 A3 A4 B1 B2; 1: A1..A4; 2: B1 B2
+          const int c = G + F * m;  // kind 0: -A1 -A2 -A3 -A4 B1 B2; 1: -A1..-A4; 2: B1 B2
           f2r cr, ci;
           if constexpr (KIND == 0) {
-            cr = f2fma(qq, f2fma(rho, c[0], c[1]), f2mul(rho, c[4]));
-            ci = f2fma(qq, f2fma(rho, c[3], c[2]), f2mul(rho, c[5]));
+            cr = f2fma(qq, f2fma(rho, B(c), B(c + 1)), f2mul(rho, B(c + 4)));
+            ci = f2fma(qq, f2fma(rho, B(c + 3), B(c + 2)), f2mul(rho, B(c + 5)));
           } else if constexpr (KIND == 1) {
-            cr = f2mul(qq, f2fma(rho, c[0], c[1]));
-            ci = f2mul(qq, f2fma(rho, c[3], c[2]));
+            cr = f2mul(qq, f2fma(rho, B(c), B(c + 1)));
+            ci = f2mul(qq, f2fma(rho, B(c + 3), B(c + 2)));
           } else {
-            cr = f2mul(rho, c[0]);
-            ci = f2mul(rho, c[1]);
+            cr = f2mul(rho, B(c));
+            ci = f2mul(rho, B(c + 1));
           }
           if constexpr (ACC4) {  // (ar - br) + i (ai + bi)
             ar[p][m] = f2fma(cs, cr, ar[p][m]);
@@ -514,8 +521,14 @@ struct Plan {
   int NT;  // threads per CTA of the fp32 kernel
 };
 
+// wavenumbers per launch chunk: up to 8 share r, 1/r and d.n (MUFU 2 + 1/MB per pair-mode);
+// NAT_MAX_MB (4 or 8) caps it for A/B comparisons
 int pick_mb(int n_modes) {
-  if (n_modes >= 8) return 4;
+  static const int cap = [] {
+    const char* e = std::getenv("NAT_MAX_MB");
+    return (e && std::atoi(e) == 4) ? 4 : 8;
+  }();
+  if (n_modes >= 8 && cap >= 8) return 8;
   if (n_modes >= 4) return 4;
   if (n_modes == 3) return 3;
   if (n_modes == 2) return 2;
@@ -537,7 +550,8 @@ int occ_of(size_t smem) {
 template <int R, int KIND, int NT>
 int occ_mb(int MB, size_t smem) {
   return MB == 1 ? occ_of<R, 1, KIND, NT>(smem) : MB == 2 ? occ_of<R, 2, KIND, NT>(smem)
-       : MB == 3 ? occ_of<R, 3, KIND, NT>(smem) : occ_of<R, 4, KIND, NT>(smem);
+       : MB == 3 ? occ_of<R, 3, KIND, NT>(smem) : MB == 4 ? occ_of<R, 4, KIND, NT>(smem)
+       : occ_of<R, 8, KIND, NT>(smem);
 }
 template <int R, int NT>
 int occ_kind(int kind, int MB, size_t smem) {
@@ -546,7 +560,7 @@ int occ_kind(int kind, int MB, size_t smem) {
 
 // Resident CTAs per SM of the radiation kernel instance (cached per configuration).
 int occupancy(bool fp64, int kind, int R, int MB, int NT, size_t smem) {
-  static int cache[2][3][5][5][2];  // [fp64][kind][R][MB][NT == 128], 0 = unknown
+  static int cache[2][3][5][9][2];  // [fp64][kind][R][MB][NT == 128], 0 = unknown
   int& c = cache[fp64 ? 1 : 0][fp64 ? 0 : kind][R][MB][NT == 128 ? 1 : 0];
   if (c) return c;
   if (fp64) {
@@ -578,7 +592,7 @@ Plan make_plan(nat_prec prec, int64_t n_src, int n_modes, int64_t n_lis, int kin
   } else {
     pl.MB = pick_mb(n_modes);
     pl.R = 4;
-    pl.NF = rec_nf(pl.kind, pl.MB);  // duplicated records of the FP32x2 kernel
+    pl.NF = rec_nf(pl.kind, pl.MB);  // records of the FP32x2 kernel (scalars, broadcast operands)
     pl.tile = kTile;
   }
   pl.NT = kThreads;
@@ -660,10 +674,15 @@ Plan make_plan(nat_prec prec, int64_t n_src, int n_modes, int64_t n_lis, int kin
         pl.smem = q.smem;
       }
   }
-  if (const char* ov = std::getenv("NAT_RAD_PLAN")) {  // tuning sweeps only: "R,NT,c"
-    int R = 0, NT = 0, c = 0;
-    if (!pl.fp64 && std::sscanf(ov, "%d,%d,%d", &R, &NT, &c) == 3 && (R == 2 || R == 4) &&
-        (NT == 128 || NT == 256) && c >= 1) {
+  if (const char* ov = std::getenv("NAT_RAD_PLAN")) {  // tuning sweeps only: "R,NT,c[,MB[,kind]]"
+    int R = 0, NT = 0, c = 0, MB = 0, kd = -1;
+    const int nf = pl.fp64 ? 0 : std::sscanf(ov, "%d,%d,%d,%d,%d", &R, &NT, &c, &MB, &kd);
+    if (nf >= 3 && (R == 2 || R == 4) && (NT == 128 || NT == 256) && c >= 1 && (kd < 0 || kd == pl.kind)) {
+      if (nf >= 4 && (MB == 1 || MB == 2 || MB == 3 || MB == 4 || MB == 8)) {
+        pl.MB = MB;
+        pl.NF = rec_nf(pl.kind, pl.MB);
+        pl.n_mchunk = (n_modes + pl.MB - 1) / pl.MB;
+      }
       pl.R = R;
       pl.NT = NT;
       pl.chunk_tiles = std::min(std::min(c, pl.n_tiles), kMaxChunkTiles);
@@ -703,7 +722,8 @@ cudaError_t launch_f32_r(const Plan& pl, const RadParams& prm, cudaStream_t s) {
     case 1: return launch_f32<R, 1, KIND, NT>(pl, prm, s);
     case 2: return launch_f32<R, 2, KIND, NT>(pl, prm, s);
     case 3: return launch_f32<R, 3, KIND, NT>(pl, prm, s);
-    default: return launch_f32<R, 4, KIND, NT>(pl, prm, s);
+    case 4: return launch_f32<R, 4, KIND, NT>(pl, prm, s);
+    default: return launch_f32<R, 8, KIND, NT>(pl, prm, s);
   }
 }
 
@@ -770,7 +790,7 @@ nat_status radiate_internal(const RadInput& in, nat_prec prec, const double* k, 
           in.xyz, in.nrm, in.w, in.w_const, p, g, in.ldpg, kv, nm, in.center[0], in.center[1],
           in.center[2], (double*)rec, in.skip);
     else
-      stage_kernel<float, true><<<sblocks, kStageSrc, 0, s>>>(in.n_src, pl.n_src_pad, pl.NF, pl.MB, pl.n_mchunk, pl.kind,
+      stage_kernel<float, false, -1><<<sblocks, kStageSrc, 0, s>>>(in.n_src, pl.n_src_pad, pl.NF, pl.MB, pl.n_mchunk, pl.kind,
           in.xyz, in.nrm, in.w, in.w_const, p, g, in.ldpg, kv, nm, in.center[0], in.center[1],
           in.center[2], (float*)rec, in.skip);
     NAT_LAUNCH_CHECK();
