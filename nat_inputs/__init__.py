@@ -357,3 +357,31 @@ def random_points_in_shell(n: int, r_lo: float, r_hi: float, seed: int) -> np.nd
 def random_complex(shape, seed: int) -> np.ndarray:
     rng = np.random.default_rng(seed)
     return rng.normal(size=shape) + 1j * rng.normal(size=shape)
+
+
+# ----------------------------------------------------------------------------------
+# NEXT-4 neural field: seeded parameters and training samples (inputs only)
+# ----------------------------------------------------------------------------------
+
+def nf_init_params(shapes, seed: int, grid_scale: float = 1e-4) -> np.ndarray:
+    """Flat float32 parameter vector for the given block shapes (grid tables [rows][4]
+    first, then per layer W [out][in], b [out]): grid features U(-grid_scale, grid_scale)
+    (instant-NGP's small init), W Xavier-uniform, b = 0."""
+    rng = np.random.default_rng(seed)
+    parts = []
+    for shp in shapes:
+        shp = tuple(shp)
+        if len(shp) == 2 and shp[1] == 4:          # feature table
+            parts.append(rng.uniform(-grid_scale, grid_scale, size=shp))
+        elif len(shp) == 2:                        # W [out][in]
+            lim = math.sqrt(6.0 / (shp[0] + shp[1]))
+            parts.append(rng.uniform(-lim, lim, size=shp))
+        else:                                      # bias
+            parts.append(np.zeros(shp))
+    return np.concatenate([p.reshape(-1) for p in parts]).astype(np.float32)
+
+
+def nf_samples(n: int, n_v: int, seed: int) -> np.ndarray:
+    """n training inputs [n][3 + n_v] uniform in [0, 1) (normalised theta, phi, r and the
+    condition variables)."""
+    return np.random.default_rng(seed).random((n, 3 + n_v)).astype(np.float32)
