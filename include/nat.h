@@ -407,6 +407,39 @@ nat_status nat_listener_random_shell(const double* center /* [host] 3 */, double
                                      double r_hi, uint64_t seed, uint64_t stream_id, double* out,
                                      nat_stream_t stream); /* (async) */
 
+/* ---------------------------------------------------------------------------------
+ * NEXT-4 — the NAT neural acoustic transfer field (reading R-nf):
+ *   Phi(x, v) = MLP[ G(x) ; P(v) ],  x = (theta^, phi^, r^) in [0,1]^3, v in [0,1]^n_v;
+ *   G: 4 feature lattices over x, resolutions 8, 16, 32, 64, 4 features per vertex,
+ *      trilinear interpolation (dense tables: (N+1)^3 <= 2^19 rows; instant-NGP hash above);
+ *   P: sin / cos(2^k pi v_d), k = 0..5;  input = [G (16) ; P (12 n_v) ; 0] padded to 64;
+ *   MLP 64 -> 128 -> 128 -> 128 -> 128 -> n_out, ReLU after the hidden layers;
+ *   loss = mean squared error (l.124); Adam (beta 0.9 / 0.999, eps 1e-8, bias-corrected).
+ * Parameters: one fp32 vector in the order grid0..grid3 [rows][4], then per layer W [out][in]
+ * (row-major) and b [out].  Every layer product runs on the tcgen05 tensor cores with bf16
+ * operands (activations, weights, gradients) and fp32 accumulation; everything else fp32.
+ * inputs: fp32 [n][3 + n_v]; targets, out: fp32 [n][n_out].  n_v <= 4, 1 <= n_out <= 16.
+ * ------------------------------------------------------------------------------- */
+typedef struct {
+  int n_v;    /* condition variables (C4: height, size, material = 3) */
+  int n_out;  /* outputs (C4: |p| of the 8 modes)                      */
+} nat_nf_config;
+int64_t nat_nf_param_count(const nat_nf_config* cfg);     /* -1 for an invalid cfg        */
+size_t nat_nf_workspace(const nat_nf_config* cfg, int64_t n);
+nat_status nat_nf_forward(const nat_nf_config* cfg, const float* params, int64_t n, const float* inputs,
+                          float* out, void* ws, size_t ws_bytes, nat_stream_t stream); /* (async) */
+/* forward, MSE, backward, Adam (in place on params, adam_m, adam_v; step >= 1 counts Adam
+ * steps); loss: device fp32 [1] (the loss before the update); grad_out: optional device
+ * fp32 [param_count] (the gradient).  (async) */
+nat_status nat_nf_train_step(const nat_nf_config* cfg, float* params, float* adam_m, float* adam_v, int step,
+                             float lr, int64_t n, const float* inputs, const float* targets, float* loss,
+                             float* grad_out, void* ws, size_t ws_bytes, nat_stream_t stream);
+/* The layers' tensor-core product alone: C (fp32 [M][ldc]) = A B^T with A bf16 [M][K]
+ * (a_mn = 0) or [K][M] (a_mn = 1), B bf16 [N][K] (b_mn = 0) or [K][N] (b_mn = 1);
+ * N in {16, 32, 64, 128}; lda, ldb multiples of 8.  (async) */
+nat_status nat_nf_gemm_bf16(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int a_mn, const void* B,
+                            int64_t ldb, int b_mn, float* C, int64_t ldc, nat_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

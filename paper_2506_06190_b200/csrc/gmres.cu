@@ -264,12 +264,29 @@ __device__ void givens_block(const GivensArgs& g, int q, double2* gsm) {
       atomicAnd(g.mask, ~(1ull << q));
     } else {
       const bool breakdown = nrm == 0.0;
-      for (int i = 0; i < j; ++i) {
-        const double2 hi = col[i], hi1 = col[i + 1];
-        col[i] = cadd(cjmul(sc[i], hi), cjmul(ss[i], hi1));
-        const double2 t = cmul(ss[i], hi);
-        col[i + 1] = cadd(make_double2(-t.x, -t.y), cmul(sc[i], hi1));
+      // the rotation chain: the rotated entry i + 1 carries to step i + 1 in registers, the
+      // original entries and the rotations of the next 8 steps are loaded ahead (the same
+      // operations in the same order as one step at a time)
+      double2 carry = col[0];
+      for (int i0 = 0; i0 < j; i0 += 8) {
+        double2 b[8], cc[8], sv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int i = i0 + u < j ? i0 + u : j - 1;
+          b[u] = col[i + 1];
+          cc[u] = sc[i];
+          sv[u] = ss[i];
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (i0 + u >= j) break;
+          const double2 hi = carry, hi1 = b[u];
+          col[i0 + u] = cadd(cjmul(cc[u], hi), cjmul(sv[u], hi1));
+          const double2 t = cmul(sv[u], hi);
+          carry = cadd(make_double2(-t.x, -t.y), cmul(cc[u], hi1));
+        }
       }
+      col[j] = carry;
       const double2 a = col[j], bb = col[j + 1];
       const double den = sqrt((a.x * a.x + a.y * a.y) + (bb.x * bb.x + bb.y * bb.y));
       double2 cj = make_double2(1.0, 0.0), sj = make_double2(0.0, 0.0);

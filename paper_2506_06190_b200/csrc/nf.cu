@@ -1,0 +1,779 @@
+// NEXT-4 — the NAT neural acoustic transfer field (§3.2-3.3, l.120-162;
+// reading R-nf): multi-resolution feature grid G(theta, phi, r) (4 levels,
+// 8..64, 4 features, trilinear), NeRF positional encoding of the condition variables
+// (2^0..2^5), a 4 x 128 ReLU MLP, MSE loss and Adam — forward and one training step.
+//
+// B200 design: every layer product (forward, input gradient, weight gradient) runs on the
+// 5th-generation tensor cores: `tcgen05.mma.cta_group::1.kind::f16` (bf16 operands, fp32
+// accumulators in TMEM), issued by one thread per CTA, operands staged in shared memory in
+// the canonical no-swizzle core-matrix layout (K-major or MN-major, so row-major
+// activations serve both as [batch][features] and transposed without copies), two smem
+// stages with tcgen05.commit -> mbarrier handshakes, TMEM -> registers with tcgen05.ld for
+// fused epilogues (bias + ReLU + bf16, ReLU-mask, fp32 split-K partials).  Encoding,
+// loss, grid scatter and Adam are elementwise kernels.
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "async_copy.cuh"
+#include "nat_internal.cuh"
+
+namespace {
+
+using bf16 = __nv_bfloat16;
+
+constexpr int kLevels = 4, kFeat = 4, kBaseRes = 8, kTable = 1 << 19, kPeFreq = 6;
+constexpr int kInPad = 64, kHidden = 128, kNHidden = 4, kOutPad = 16;
+constexpr int kNLayers = kNHidden + 1;
+
+__host__ __device__ constexpr int level_res(int l) { return kBaseRes << l; }
+__host__ __device__ constexpr int64_t level_rows(int l) {  // dense when the lattice fits the table
+  return (int64_t)(level_res(l) + 1) * (level_res(l) + 1) * (level_res(l) + 1) <= kTable
+             ? (int64_t)(level_res(l) + 1) * (level_res(l) + 1) * (level_res(l) + 1)
+             : (int64_t)kTable;
+}
+__device__ __forceinline__ int64_t vertex_row(int l, int64_t i, int64_t j, int64_t k) {
+  const int64_t n = level_res(l) + 1;
+  if (n * n * n <= kTable) return i + n * (j + n * k);
+  const uint64_t h = ((uint64_t)i * 1ull) ^ ((uint64_t)j * 2654435761ull) ^ ((uint64_t)k * 805459861ull);
+  return (int64_t)(h % (uint64_t)kTable);
+}
+
+// ---- parameter layout (the oracle's order): grid0..3 [rows][4], then W_q [out][in], b_q ----
+struct Layout {
+  int64_t grid[kLevels];
+  int64_t W[kNLayers], b[kNLayers];
+  int in[kNLayers], out[kNLayers];
+  int64_t total;
+};
+Layout layout_of(int n_out) {
+  Layout L{};
+  int64_t o = 0;
+  for (int l = 0; l < kLevels; ++l) {
+    L.grid[l] = o;
+    o += level_rows(l) * kFeat;
+  }
+  for (int q = 0; q < kNLayers; ++q) {
+    L.in[q] = q == 0 ? kInPad : kHidden;
+    L.out[q] = q == kNHidden ? n_out : kHidden;
+    L.W[q] = o;
+    o += (int64_t)L.in[q] * L.out[q];
+    L.b[q] = o;
+    o += L.out[q];
+  }
+  L.total = o;
+  return L;
+}
+
+// =====================================================================================
+// tcgen05 GEMM: C[M x N] = A[M x K] * B[N x K]^T, bf16 operands, fp32 accumulation in TMEM.
+// A is K-major (A[m * lda + k]) or MN-major (A[k * lda + m]); likewise B (B[n * ldb + k] or
+// B[k * ldb + n]).  One CTA = 128 rows x N (N in {16, 32, 64, 128}), K in chunks of 64.
+// =====================================================================================
+constexpr int kGM = 128, kBK = 64, kGT = 128;
+
+enum Epi : int {
+  kEpiBiasReluBf16 = 0,  // Cb = bf16(relu(acc + bias))
+  kEpiBiasF32 = 1,       // C = acc + bias        (columns < n_valid)
+  kEpiMaskBf16 = 2,      // v = acc * (H > 0): Cb = bf16(v), column sums of v -> colpart[tile][n]
+  kEpiF32 = 3,           // C = acc
+  kEpiPartial = 4,       // C[split][M][N] = acc  (split-K partial)
+};
+
+struct GemmArgs {
+  const bf16* A;
+  int64_t lda;
+  const bf16* B;
+  int64_t ldb;
+  int64_t M, N, K, k_per_cta;
+  int epi, n_valid;
+  float* C;
+  int64_t ldc;
+  bf16* Cb;
+  const float* bias;
+  const bf16* H;
+  int64_t ldh;
+  float* colpart;  // kEpiMaskBf16: [gridDim.x][N]
+};
+
+__device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((addr & 0x3FFFFu) >> 4);          // start address, bits [0, 14)
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;       // leading (K-group) byte offset, [16, 30)
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;       // stride (MN-group) byte offset, [32, 46)
+  d |= (uint64_t)1 << 46;                            // descriptor version 1 (sm_100)
+  return d;                                          // base offset 0, no swizzle (layout 0)
+}
+
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, bool a_mn, bool b_mn) {
+  return (1u << 4)                                   // D format f32
+         | (1u << 7) | (1u << 10)                    // A, B format bf16
+         | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16)
+         | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_bf16(uint32_t tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   nat::smem_u32(bar))
+               : "memory");
+}
+
+// 16-byte unit of 8 bf16 (zero outside the matrix)
+__device__ __forceinline__ uint4 ld16(const bf16* p, bool ok) {
+  return ok ? *reinterpret_cast<const uint4*>(p) : make_uint4(0u, 0u, 0u, 0u);
+}
+
+// Stages rows [r0, r0 + R) x k [k0, k0 + 64) of an operand into the core-matrix layout:
+//   K-major : unit (r, kc) at ((r/8)*8 + kc)*128 + (r%8)*16   (LBO = 128, SBO = 1024)
+//   MN-major: unit (kk, rc) at ((kk/8)*(R/8) + rc)*128 + (kk%8)*16 (SBO = 128, LBO = R*16)
+template <int R, bool MN>
+__device__ __forceinline__ void stage_operand(const bf16* P, int64_t ld, int64_t rows, int64_t K, int64_t r0,
+                                              int64_t k0, char* smem) {
+  constexpr int kUnits = R * (kBK / 8);
+  for (int u = threadIdx.x; u < kUnits; u += kGT) {
+    if constexpr (!MN) {
+      const int r = u / (kBK / 8), kc = u % (kBK / 8);
+      const int64_t gr = r0 + r, gk = k0 + kc * 8;
+      const uint4 v = ld16(P + gr * ld + gk, gr < rows && gk < K);
+      *reinterpret_cast<uint4*>(smem + ((r / 8) * (kBK / 8) + kc) * 128 + (r % 8) * 16) = v;
+    } else {
+      const int kk = u / (R / 8), rc = u % (R / 8);
+      const int64_t gk = k0 + kk, gr = r0 + rc * 8;
+      const uint4 v = ld16(P + gk * ld + gr, gk < K && gr < rows);
+      *reinterpret_cast<uint4*>(smem + ((kk / 8) * (R / 8) + rc) * 128 + (kk % 8) * 16) = v;
+    }
+  }
+}
+
+template <int BN, bool AMN, bool BMN>
+__global__ void __launch_bounds__(kGT) nf_gemm_kernel(GemmArgs g) {
+  constexpr uint32_t kABytes = kGM * kBK * 2, kBBytes = BN * kBK * 2;
+  constexpr uint32_t kCols = BN < 32 ? 32 : BN;  // TMEM columns (power of 2 >= 32)
+  extern __shared__ __align__(1024) char gsm[];
+  __shared__ __align__(8) uint64_t bars[2];
+  __shared__ uint32_t tmem_base;
+  __shared__ float colsum[4][BN];
+  char* sA[2] = {gsm, gsm + kABytes + kBBytes};
+  char* sB[2] = {gsm + kABytes, gsm + 2 * kABytes + kBBytes};
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t m0 = (int64_t)blockIdx.x * kGM;
+  const int split = blockIdx.y;
+  const int64_t kb = (int64_t)split * g.k_per_cta, ke = min(g.K, kb + g.k_per_cta);
+  const int nchunk = (int)((ke - kb + kBK - 1) / kBK);
+
+  if (tid == 0) {
+    nat::mbar_init(&bars[0], 1);
+    nat::mbar_init(&bars[1], 1);
+    nat::fence_mbar_init();
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(nat::smem_u32(&tmem_base)),
+                 "r"(kCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = tmem_base;
+  constexpr uint32_t idesc = idesc_bf16(kGM, BN, AMN, BMN);
+  // descriptor strides (bytes): K-group (LBO) and MN-group (SBO)
+  constexpr uint32_t a_lbo = AMN ? kGM * 16 : 128, a_sbo = AMN ? 128 : (kBK / 8) * 128;
+  constexpr uint32_t b_lbo = BMN ? BN * 16 : 128, b_sbo = BMN ? 128 : (kBK / 8) * 128;
+
+  for (int c = 0; c < nchunk; ++c) {
+    const int s = c & 1;
+    if (c >= 2) nat::mbar_wait(&bars[s], ((c - 2) >> 1) & 1);  // the MMAs of chunk c-2 are done
+    const int64_t k0 = kb + (int64_t)c * kBK;
+    stage_operand<kGM, AMN>(g.A, g.lda, g.M, ke, m0, k0, sA[s]);
+    stage_operand<BN, BMN>(g.B, g.ldb, g.N, ke, 0, k0, sB[s]);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core reads
+    __syncthreads();
+    if (tid == 0) {
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const uint32_t a0 = nat::smem_u32(sA[s]), b0 = nat::smem_u32(sB[s]);
+#pragma unroll
+      for (int kk = 0; kk < kBK / 16; ++kk)
+        mma_bf16(tmem, sdesc(a0 + kk * 2 * a_lbo, a_lbo, a_sbo), sdesc(b0 + kk * 2 * b_lbo, b_lbo, b_sbo), idesc,
+                 (c > 0 || kk > 0) ? 1u : 0u);
+      mma_commit(&bars[s]);
+    }
+  }
+  if (nchunk > 0) nat::mbar_wait(&bars[(nchunk - 1) & 1], ((nchunk - 1) >> 1) & 1);
+  asm volatile("tcgen05.fence::after_thread_sync;");
+
+  // epilogue: warp w owns rows (TMEM lanes) 32w .. 32w + 31; 32 columns per tcgen05.ld
+  const int64_t m = m0 + warp * 32 + lane;
+  const bool row_ok = m < g.M && nchunk > 0;
+#pragma unroll 1
+  for (int n0 = 0; n0 < BN; n0 += 32) {
+    uint32_t v[32];
+    const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)n0;
+    if constexpr (BN >= 32) {
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+          "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+            "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+            "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+            "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
+            "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+          : "r"(taddr));
+    } else {  // BN == 16
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+            "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+            "=r"(v[15])
+          : "r"(taddr));
+      for (int q = 16; q < 32; ++q) v[q] = 0u;
+    }
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    constexpr int W = BN < 32 ? BN : 32;
+    float f[32];
+#pragma unroll
+    for (int q = 0; q < 32; ++q) f[q] = __uint_as_float(v[q]);
+    if (g.epi == kEpiBiasReluBf16 || g.epi == kEpiMaskBf16) {
+      if (g.epi == kEpiBiasReluBf16) {
+#pragma unroll
+        for (int q = 0; q < W; ++q) f[q] = fmaxf(f[q] + g.bias[n0 + q], 0.f);
+      } else {
+#pragma unroll
+        for (int q = 0; q < W; q += 8) {
+          const uint4 hv = row_ok ? *reinterpret_cast<const uint4*>(g.H + m * g.ldh + n0 + q) : make_uint4(0, 0, 0, 0);
+          const bf16* hb = reinterpret_cast<const bf16*>(&hv);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) f[q + e] = (row_ok && __bfloat162float(hb[e]) > 0.f) ? f[q + e] : 0.f;
+        }
+        // column sums of the masked gradient (bias gradient): warp tree, then the 4 warps
+#pragma unroll
+        for (int q = 0; q < W; ++q) {
+          float t = f[q];
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+          if (lane == 0) colsum[warp][n0 + q] = t;
+        }
+      }
+      if (row_ok) {
+#pragma unroll
+        for (int q = 0; q < W; q += 8) {
+          uint4 o;
+          __nv_bfloat162* ob = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) ob[e] = __floats2bfloat162_rn(f[q + 2 * e], f[q + 2 * e + 1]);
+          *reinterpret_cast<uint4*>(g.Cb + m * g.ldc + n0 + q) = o;
+        }
+      }
+    } else if (g.epi == kEpiPartial) {
+      if (row_ok) {
+        float* dst = g.C + ((size_t)split * g.M + m) * g.ldc + n0;
+#pragma unroll
+        for (int q = 0; q < W; q += 4) *reinterpret_cast<float4*>(dst + q) = make_float4(f[q], f[q + 1], f[q + 2], f[q + 3]);
+      }
+    } else {  // kEpiBiasF32, kEpiF32
+      if (row_ok)
+        for (int q = 0; q < W; ++q)
+          if (n0 + q < g.n_valid) g.C[m * g.ldc + n0 + q] = f[q] + (g.epi == kEpiBiasF32 ? g.bias[n0 + q] : 0.f);
+    }
+  }
+  if (g.epi == kEpiMaskBf16) {
+    __syncthreads();
+    for (int n = tid; n < BN; n += kGT)
+      g.colpart[(size_t)blockIdx.x * BN + n] = ((colsum[0][n] + colsum[1][n]) + colsum[2][n]) + colsum[3][n];
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kCols));
+}
+
+template <int BN, bool AMN, bool BMN>
+cudaError_t launch_gemm_t(const GemmArgs& g, int splits, cudaStream_t s) {
+  const size_t smem = 2 * ((size_t)kGM * kBK * 2 + (size_t)BN * kBK * 2);
+  auto k = nf_gemm_kernel<BN, AMN, BMN>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const dim3 grid((unsigned)((g.M + kGM - 1) / kGM), (unsigned)splits);
+  k<<<grid, kGT, smem, s>>>(g);
+  return cudaGetLastError();
+}
+
+template <bool AMN, bool BMN>
+cudaError_t launch_gemm_n(const GemmArgs& g, int splits, cudaStream_t s) {
+  switch (g.N) {
+    case 16: return launch_gemm_t<16, AMN, BMN>(g, splits, s);
+    case 32: return launch_gemm_t<32, AMN, BMN>(g, splits, s);
+    case 64: return launch_gemm_t<64, AMN, BMN>(g, splits, s);
+    case 128: return launch_gemm_t<128, AMN, BMN>(g, splits, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_gemm(const GemmArgs& g, bool a_mn, bool b_mn, int splits, cudaStream_t s) {
+  if (!a_mn && !b_mn) return launch_gemm_n<false, false>(g, splits, s);
+  if (!a_mn && b_mn) return launch_gemm_n<false, true>(g, splits, s);
+  if (a_mn && !b_mn) return launch_gemm_n<true, false>(g, splits, s);
+  return launch_gemm_n<true, true>(g, splits, s);
+}
+
+// =====================================================================================
+// encoding, loss, grid scatter, reductions, Adam
+// =====================================================================================
+// X[b][0..16) = grid features (level-major), X[b][16..16 + 12 n_v) = PE(v), rest 0 (bf16)
+__global__ void nf_encode_kernel(int64_t n, int n_v, const float* __restrict__ in, const float* __restrict__ params,
+                                 Layout L, bf16* __restrict__ X) {
+  const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (b >= n) return;
+  const float* x = in + b * (3 + n_v);
+  float out[kInPad];
+#pragma unroll
+  for (int q = 0; q < kInPad; ++q) out[q] = 0.f;
+#pragma unroll
+  for (int l = 0; l < kLevels; ++l) {
+    const int N = level_res(l);
+    int64_t i0[3];
+    float fr[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const float p = x[d] * (float)N;
+      const float fl = fminf(fmaxf(floorf(p), 0.f), (float)(N - 1));
+      i0[d] = (int64_t)fl;
+      fr[d] = p - fl;
+    }
+    const float* G = params + L.grid[l];
+    float acc[kFeat] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int dx = c & 1, dy = (c >> 1) & 1, dz = (c >> 2) & 1;
+      const float wx = dx ? fr[0] : 1.f - fr[0], wy = dy ? fr[1] : 1.f - fr[1], wz = dz ? fr[2] : 1.f - fr[2];
+      const float w = __fmul_rn(__fmul_rn(wx, wy), wz);
+      const float4 f = *reinterpret_cast<const float4*>(G + vertex_row(l, i0[0] + dx, i0[1] + dy, i0[2] + dz) * kFeat);
+      acc[0] = __fadd_rn(acc[0], __fmul_rn(w, f.x));
+      acc[1] = __fadd_rn(acc[1], __fmul_rn(w, f.y));
+      acc[2] = __fadd_rn(acc[2], __fmul_rn(w, f.z));
+      acc[3] = __fadd_rn(acc[3], __fmul_rn(w, f.w));
+    }
+#pragma unroll
+    for (int f = 0; f < kFeat; ++f) out[l * kFeat + f] = acc[f];
+  }
+  for (int d = 0; d < n_v; ++d)
+    for (int k = 0; k < kPeFreq; ++k) {
+      const float a = (float)(1 << k) * 3.14159265358979323846f * x[3 + d];
+      float sn, cs;
+      sincosf(a, &sn, &cs);
+      out[kLevels * kFeat + 2 * (d * kPeFreq + k)] = sn;
+      out[kLevels * kFeat + 2 * (d * kPeFreq + k) + 1] = cs;
+    }
+  uint4* dst = reinterpret_cast<uint4*>(X + b * kInPad);
+#pragma unroll
+  for (int q = 0; q < kInPad; q += 8) {
+    uint4 o;
+    __nv_bfloat162* ob = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) ob[e] = __floats2bfloat162_rn(out[q + 2 * e], out[q + 2 * e + 1]);
+    dst[q / 8] = o;
+  }
+}
+
+// dY = 2 (Y - T) / (n n_out) (bf16 [n][16], zero padded); per-block partial sums of the
+// squared error (loss) and of dY per column (output-layer bias gradient), fixed order.
+constexpr int kLossT = 256;
+__global__ void __launch_bounds__(kLossT) nf_loss_kernel(int64_t n, int n_out, const float* __restrict__ Y,
+                                                         const float* __restrict__ T, bf16* __restrict__ dY,
+                                                         double* __restrict__ lpart, float* __restrict__ bpart) {
+  __shared__ double sl[kLossT];
+  __shared__ float sb[kOutPad][kLossT / 32];
+  const int64_t b = blockIdx.x * (int64_t)kLossT + threadIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double se = 0.0;
+  float d[kOutPad];
+#pragma unroll
+  for (int q = 0; q < kOutPad; ++q) d[q] = 0.f;
+  if (b < n) {
+    const float scale = 2.f / (float)((double)n * n_out);
+    for (int q = 0; q < n_out; ++q) {
+      const float e = Y[b * kOutPad + q] - T[b * n_out + q];
+      se += (double)e * (double)e;
+      d[q] = scale * e;
+    }
+    uint4 o[2];
+    __nv_bfloat162* ob = reinterpret_cast<__nv_bfloat162*>(o);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) ob[e] = __floats2bfloat162_rn(d[2 * e], d[2 * e + 1]);
+    reinterpret_cast<uint4*>(dY + b * kOutPad)[0] = o[0];
+    reinterpret_cast<uint4*>(dY + b * kOutPad)[1] = o[1];
+  }
+  sl[threadIdx.x] = se;
+#pragma unroll
+  for (int q = 0; q < kOutPad; ++q) {
+    float t = d[q];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (lane == 0) sb[q][warp] = t;
+  }
+  __syncthreads();
+  for (int w = kLossT / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) sl[threadIdx.x] += sl[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) lpart[blockIdx.x] = sl[0];
+  if (threadIdx.x < kOutPad) {
+    float t = 0.f;
+    for (int w = 0; w < kLossT / 32; ++w) t += sb[threadIdx.x][w];
+    bpart[(size_t)blockIdx.x * kOutPad + threadIdx.x] = t;
+  }
+}
+
+// out[j] = sum_p part[p][j] (p ascending) — split-K and per-tile partials, fixed order.
+// transpose: out holds [cols][rows] of a [rows][cols] partial layout (dW of the last layer).
+__global__ void nf_reduce_kernel(int64_t nparts, int64_t rows, int64_t cols, const float* __restrict__ part,
+                                 float* __restrict__ out, int64_t out_rows, int64_t out_cols, bool transpose,
+                                 float scale) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= rows * cols) return;
+  float t = 0.f;
+  for (int64_t p = 0; p < nparts; ++p) t += part[p * rows * cols + j];
+  const int64_t r = j / cols, c = j % cols;
+  if (!transpose) {
+    if (r < out_rows && c < out_cols) out[r * out_cols + c] = scale * t;
+  } else {
+    if (c < out_rows && r < out_cols) out[c * out_cols + r] = scale * t;
+  }
+}
+
+__global__ void nf_loss_finish_kernel(int64_t nparts, const double* __restrict__ lpart, int64_t count,
+                                      float* __restrict__ loss) {
+  double t = 0.0;
+  for (int64_t p = 0; p < nparts; ++p) t += lpart[p];
+  *loss = (float)(t / (double)count);
+}
+
+// dGrid[level][row] += w_corner * dX[b][level*4 + f]   (atomics: order-free sums)
+__global__ void nf_grid_backward_kernel(int64_t n, int n_v, const float* __restrict__ in, const float* __restrict__ dX,
+                                        Layout L, float* __restrict__ grad) {
+  const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (b >= n) return;
+  const float* x = in + b * (3 + n_v);
+#pragma unroll
+  for (int l = 0; l < kLevels; ++l) {
+    const int N = level_res(l);
+    int64_t i0[3];
+    float fr[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const float p = x[d] * (float)N;
+      const float fl = fminf(fmaxf(floorf(p), 0.f), (float)(N - 1));
+      i0[d] = (int64_t)fl;
+      fr[d] = p - fl;
+    }
+    const float4 g = *reinterpret_cast<const float4*>(dX + b * kInPad + l * kFeat);
+    float* G = grad + L.grid[l];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int dx = c & 1, dy = (c >> 1) & 1, dz = (c >> 2) & 1;
+      const float wx = dx ? fr[0] : 1.f - fr[0], wy = dy ? fr[1] : 1.f - fr[1], wz = dz ? fr[2] : 1.f - fr[2];
+      const float w = (wx * wy) * wz;
+      float* r = G + vertex_row(l, i0[0] + dx, i0[1] + dy, i0[2] + dz) * kFeat;
+      atomicAdd(r + 0, w * g.x);
+      atomicAdd(r + 1, w * g.y);
+      atomicAdd(r + 2, w * g.z);
+      atomicAdd(r + 3, w * g.w);
+    }
+  }
+}
+
+// Adam (Kingma & Ba) with bias correction; step counts from 1.
+__global__ void nf_adam_kernel(int64_t n, float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
+                               float* __restrict__ v, float lr, float b1, float b2, float eps, float c1, float c2) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float gi = g[i];
+  const float mi = b1 * m[i] + (1.f - b1) * gi;
+  const float vi = b2 * v[i] + (1.f - b2) * gi * gi;
+  m[i] = mi;
+  v[i] = vi;
+  p[i] -= lr * (mi / c1) / (sqrtf(vi / c2) + eps);
+}
+
+// bf16 copies of the layer weights: Wb_q [out_pad][in] (rows >= out zero)
+__global__ void nf_cast_weights_kernel(const float* __restrict__ params, Layout L, bf16* __restrict__ Wb) {
+  const int q = blockIdx.y;
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int out_pad = q == kNHidden ? kOutPad : kHidden;
+  const int64_t off = (int64_t)q * kHidden * kHidden;  // slot per layer
+  if (j >= (int64_t)out_pad * L.in[q]) return;
+  const int64_t r = j / L.in[q], c = j % L.in[q];
+  Wb[off + j] = r < L.out[q] ? __float2bfloat16_rn(params[L.W[q] + r * L.in[q] + c]) : __float2bfloat16_rn(0.f);
+}
+
+struct NfWs {
+  bf16* X;        // [n][64]
+  bf16* H[kNHidden];  // [n][128]
+  float* Y;       // [n][16]
+  bf16* dY;       // [n][16]
+  bf16* dH[2];    // [n][128]
+  float* dX;      // [n][64]
+  float* grad;    // [n_params]
+  bf16* Wb;       // [5][128][128] bf16 weight slots
+  float* wpart;   // [splits][128][128]
+  float* cpart;   // [tiles][128]
+  double* lpart;  // loss partials
+  float* bpart;   // [loss blocks][16]
+  int64_t splits, tiles, lblocks;
+};
+
+constexpr int64_t kSplitRows = 1024;  // batch rows per split-K CTA of the weight gradients
+
+size_t nf_carve(nat::Carver& c, NfWs* w, int64_t n, int64_t n_params) {
+  NfWs t{};
+  t.X = c.take<bf16>((size_t)n * kInPad);
+  for (int q = 0; q < kNHidden; ++q) t.H[q] = c.take<bf16>((size_t)n * kHidden);
+  t.Y = c.take<float>((size_t)n * kOutPad);
+  t.dY = c.take<bf16>((size_t)n * kOutPad);
+  t.dH[0] = c.take<bf16>((size_t)n * kHidden);
+  t.dH[1] = c.take<bf16>((size_t)n * kHidden);
+  t.dX = c.take<float>((size_t)n * kInPad);
+  t.grad = c.take<float>((size_t)n_params);
+  t.Wb = c.take<bf16>((size_t)kNLayers * kHidden * kHidden);
+  t.splits = (n + kSplitRows - 1) / kSplitRows;
+  t.tiles = (n + kGM - 1) / kGM;
+  t.lblocks = (n + kLossT - 1) / kLossT;
+  t.wpart = c.take<float>((size_t)t.splits * kHidden * kHidden);
+  t.cpart = c.take<float>((size_t)t.tiles * kHidden);
+  t.lpart = c.take<double>((size_t)t.lblocks);
+  t.bpart = c.take<float>((size_t)t.lblocks * kOutPad);
+  if (w) *w = t;
+  return c.bytes();
+}
+
+nat_status check_cfg(const nat_nf_config* cfg) {
+  NAT_REQUIRE(cfg, "cfg must be non-null");
+  NAT_REQUIRE(cfg->n_v >= 0 && 16 + 12 * cfg->n_v <= kInPad, "n_v = %d: need 16 + 12 n_v <= 64", cfg->n_v);
+  NAT_REQUIRE(cfg->n_out >= 1 && cfg->n_out <= kOutPad, "n_out = %d must be in [1, 16]", cfg->n_out);
+  return NAT_OK;
+}
+
+#define NF_LAUNCH(expr)                                                                        \
+  do {                                                                                         \
+    cudaError_t _e = (expr);                                                                   \
+    if (_e != cudaSuccess) return nat::fail(NAT_ERR_CUDA, "%s: %s", #expr, cudaGetErrorString(_e)); \
+  } while (0)
+
+// forward through the 5 layers (weights already cast); H[q] stored for the backward pass
+nat_status forward_impl(const Layout& L, int64_t n, const float* params, NfWs& w, cudaStream_t s) {
+  const bf16* act = w.X;
+  for (int q = 0; q < kNLayers; ++q) {
+    GemmArgs g{};
+    g.A = act;
+    g.lda = L.in[q];
+    g.B = w.Wb + (size_t)q * kHidden * kHidden;
+    g.ldb = L.in[q];
+    g.M = n;
+    g.K = L.in[q];
+    g.k_per_cta = L.in[q];
+    g.bias = params + L.b[q];
+    if (q < kNHidden) {
+      g.N = kHidden;
+      g.epi = kEpiBiasReluBf16;
+      g.Cb = w.H[q];
+      g.ldc = kHidden;
+      act = w.H[q];
+    } else {
+      g.N = kOutPad;
+      g.epi = kEpiBiasF32;
+      g.n_valid = L.out[q];
+      g.C = w.Y;
+      g.ldc = kOutPad;
+    }
+    NF_LAUNCH(launch_gemm(g, false, false, 1, s));
+  }
+  return NAT_OK;
+}
+
+}  // namespace
+
+extern "C" int64_t nat_nf_param_count(const nat_nf_config* cfg) {
+  if (check_cfg(cfg) != NAT_OK) return -1;
+  return layout_of(cfg->n_out).total;
+}
+
+extern "C" size_t nat_nf_workspace(const nat_nf_config* cfg, int64_t n) {
+  if (check_cfg(cfg) != NAT_OK || n < 1) return 0;
+  nat::Carver c(nullptr);
+  return nf_carve(c, nullptr, n, layout_of(cfg->n_out).total);
+}
+
+extern "C" nat_status nat_nf_forward(const nat_nf_config* cfg, const float* params, int64_t n, const float* inputs,
+                                     float* out, void* ws, size_t ws_bytes, nat_stream_t stream) {
+  NAT_TRACE();
+  nat_status st = check_cfg(cfg);
+  if (st != NAT_OK) return st;
+  NAT_REQUIRE(n >= 1, "need n >= 1 samples");
+  NAT_REQUIRE_DEV(params);
+  NAT_REQUIRE_DEV(inputs);
+  NAT_REQUIRE_DEV(out);
+  NAT_REQUIRE_DEV(ws);
+  const Layout L = layout_of(cfg->n_out);
+  nat::Carver c(ws);
+  NfWs w;
+  const size_t need = nf_carve(c, &w, n, L.total);
+  if (ws_bytes < need) return nat::fail(NAT_ERR_WORKSPACE, "workspace %zu < %zu", ws_bytes, need);
+  cudaStream_t s = (cudaStream_t)stream;
+  nf_cast_weights_kernel<<<dim3((kHidden * kHidden + 255) / 256, kNLayers), 256, 0, s>>>(params, L, w.Wb);
+  nf_encode_kernel<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(n, cfg->n_v, inputs, params, L, w.X);
+  NAT_LAUNCH_CHECK();
+  st = forward_impl(L, n, params, w, s);
+  if (st != NAT_OK) return st;
+  NAT_CUDA_TRY(cudaMemcpy2DAsync(out, sizeof(float) * cfg->n_out, w.Y, sizeof(float) * kOutPad,
+                                 sizeof(float) * cfg->n_out, n, cudaMemcpyDeviceToDevice, s));
+  return NAT_OK;
+}
+
+extern "C" nat_status nat_nf_train_step(const nat_nf_config* cfg, float* params, float* adam_m, float* adam_v,
+                                        int step, float lr, int64_t n, const float* inputs, const float* targets,
+                                        float* loss, float* grad_out, void* ws, size_t ws_bytes,
+                                        nat_stream_t stream) {
+  NAT_TRACE();
+  nat_status st = check_cfg(cfg);
+  if (st != NAT_OK) return st;
+  NAT_REQUIRE(n >= 1 && step >= 1, "need n >= 1 samples and step >= 1");
+  NAT_REQUIRE(lr >= 0.f && lr < 1e30f, "bad learning rate");
+  NAT_REQUIRE_DEV(params);
+  NAT_REQUIRE_DEV(adam_m);
+  NAT_REQUIRE_DEV(adam_v);
+  NAT_REQUIRE_DEV(inputs);
+  NAT_REQUIRE_DEV(targets);
+  NAT_REQUIRE_DEV(loss);
+  NAT_REQUIRE_DEV(ws);
+  if (grad_out) NAT_REQUIRE_DEV(grad_out);
+  const Layout L = layout_of(cfg->n_out);
+  nat::Carver c(ws);
+  NfWs w;
+  const size_t need = nf_carve(c, &w, n, L.total);
+  if (ws_bytes < need) return nat::fail(NAT_ERR_WORKSPACE, "workspace %zu < %zu", ws_bytes, need);
+  cudaStream_t s = (cudaStream_t)stream;
+  nf_cast_weights_kernel<<<dim3((kHidden * kHidden + 255) / 256, kNLayers), 256, 0, s>>>(params, L, w.Wb);
+  nf_encode_kernel<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(n, cfg->n_v, inputs, params, L, w.X);
+  NAT_LAUNCH_CHECK();
+  st = forward_impl(L, n, params, w, s);
+  if (st != NAT_OK) return st;
+  // loss and dY (MSE, l.124)
+  nf_loss_kernel<<<(unsigned)w.lblocks, kLossT, 0, s>>>(n, cfg->n_out, w.Y, targets, w.dY, w.lpart, w.bpart);
+  nf_loss_finish_kernel<<<1, 1, 0, s>>>(w.lblocks, w.lpart, n * cfg->n_out, loss);
+  NAT_CUDA_TRY(cudaMemsetAsync(w.grad, 0, sizeof(float) * L.total, s));
+  // output-layer bias gradient: column sums of dY
+  nf_reduce_kernel<<<1, kOutPad, 0, s>>>(w.lblocks, 1, kOutPad, w.bpart, w.grad + L.b[kNHidden], 1, L.out[kNHidden],
+                                         false, 1.f);
+  // backward through the layers: d = gradient with respect to layer q's output
+  const bf16* d = w.dY;
+  int dcols = kOutPad;
+  for (int q = kNHidden; q >= 0; --q) {
+    const bf16* h_in = q == 0 ? w.X : w.H[q - 1];
+    const int in = L.in[q];
+    // dW_q = d^T h_in  (split-K over the batch): M = out (or in for the 16-wide last layer)
+    GemmArgs gw{};
+    gw.K = n;
+    gw.k_per_cta = kSplitRows;
+    gw.epi = kEpiPartial;
+    gw.C = w.wpart;
+    if (q == kNHidden) {  // C[in][out_pad] = h_in^T d: A = h_in (MN-major), B = dY (MN-major)
+      gw.A = h_in;
+      gw.lda = in;
+      gw.M = in;
+      gw.B = d;
+      gw.ldb = dcols;
+      gw.N = kOutPad;
+      gw.ldc = kOutPad;
+    } else {  // C[out][in] = d^T h_in
+      gw.A = d;
+      gw.lda = dcols;
+      gw.M = kHidden;
+      gw.B = h_in;
+      gw.ldb = in;
+      gw.N = in;
+      gw.ldc = in;
+    }
+    NF_LAUNCH(launch_gemm(gw, true, true, (int)w.splits, s));
+    const int64_t rows = gw.M, cols = gw.N;
+    nf_reduce_kernel<<<(unsigned)((rows * cols + 255) / 256), 256, 0, s>>>(
+        w.splits, rows, cols, w.wpart, w.grad + L.W[q], L.out[q], in, q == kNHidden, 1.f);
+    NAT_LAUNCH_CHECK();
+    // d_in = (d W_q) * relu'(h_in): M = n, N = in, K = out; B = W_q as [K = out][N = in] (MN-major)
+    GemmArgs gd{};
+    gd.A = d;
+    gd.lda = dcols;
+    gd.B = w.Wb + (size_t)q * kHidden * kHidden;
+    gd.ldb = in;
+    gd.M = n;
+    gd.N = in;
+    gd.K = q == kNHidden ? kOutPad : kHidden;
+    gd.k_per_cta = gd.K;
+    if (q > 0) {
+      gd.epi = kEpiMaskBf16;
+      gd.H = h_in;
+      gd.ldh = in;
+      gd.Cb = w.dH[q & 1];
+      gd.ldc = in;
+      gd.colpart = w.cpart;
+      NF_LAUNCH(launch_gemm(gd, false, true, 1, s));
+      // bias gradient of layer q - 1: column sums of the masked gradient, tile order
+      nf_reduce_kernel<<<1, kHidden, 0, s>>>(w.tiles, 1, kHidden, w.cpart, w.grad + L.b[q - 1], 1, kHidden, false,
+                                             1.f);
+      NAT_LAUNCH_CHECK();
+      d = w.dH[q & 1];
+      dcols = in;
+    } else {
+      gd.epi = kEpiF32;
+      gd.n_valid = in;
+      gd.C = w.dX;
+      gd.ldc = kInPad;
+      NF_LAUNCH(launch_gemm(gd, false, true, 1, s));
+    }
+  }
+  nf_grid_backward_kernel<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(n, cfg->n_v, inputs, w.dX, L, w.grad);
+  NAT_LAUNCH_CHECK();
+  if (grad_out) NAT_CUDA_TRY(cudaMemcpyAsync(grad_out, w.grad, sizeof(float) * L.total, cudaMemcpyDeviceToDevice, s));
+  const float b1 = 0.9f, b2 = 0.999f;
+  const float c1 = 1.f - std::pow(b1, (float)step), c2 = 1.f - std::pow(b2, (float)step);
+  nf_adam_kernel<<<(unsigned)((L.total + 255) / 256), 256, 0, s>>>(L.total, params, w.grad, adam_m, adam_v, lr, b1,
+                                                                  b2, 1e-8f, c1, c2);
+  NAT_LAUNCH_CHECK();
+  return NAT_OK;
+}
+
+// The tensor-core product of the layers on its own (tests / benchmarks): C (fp32 [M][N]) =
+// A * B^T with A [M][K] (a_mn = 0) or [K][M] (a_mn = 1) and B [N][K] (b_mn = 0) or [K][N]
+// (b_mn = 1), bf16, N in {16, 32, 64, 128}, K any, leading dimensions multiples of 8.
+extern "C" nat_status nat_nf_gemm_bf16(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int a_mn,
+                                       const void* B, int64_t ldb, int b_mn, float* C, int64_t ldc,
+                                       nat_stream_t stream) {
+  NAT_TRACE();
+  NAT_REQUIRE(M >= 1 && K >= 1 && (N == 16 || N == 32 || N == 64 || N == 128), "bad shape");
+  NAT_REQUIRE(lda % 8 == 0 && ldb % 8 == 0 && ldc >= N, "leading dimensions must be multiples of 8");
+  NAT_REQUIRE_DEV(A);
+  NAT_REQUIRE_DEV(B);
+  NAT_REQUIRE_DEV(C);
+  GemmArgs g{};
+  g.A = (const bf16*)A;
+  g.lda = lda;
+  g.B = (const bf16*)B;
+  g.ldb = ldb;
+  g.M = M;
+  g.N = N;
+  g.K = K;
+  g.k_per_cta = (K + kBK - 1) / kBK * kBK;
+  g.epi = kEpiF32;
+  g.n_valid = (int)N;
+  g.C = C;
+  g.ldc = ldc;
+  NF_LAUNCH(launch_gemm(g, a_mn != 0, b_mn != 0, 1, (cudaStream_t)stream));
+  return NAT_OK;
+}

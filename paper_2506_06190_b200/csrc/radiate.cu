@@ -28,7 +28,7 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kTile = 128;  // sources per shared-memory tile (fp32)
 constexpr int kTile64 = 64; // sources per tile (fp64)
-constexpr int kMaxChunkTiles = 8;  // fp32 kernel: sources per CTA <= 8 x 128 = 1024 (fp32 sums)
+constexpr int kMaxChunkTiles = 8;  // fp32 kernel: sources summed in fp32 <= 8 x 128 = 1024, then flushed
 
 template <int MB>
 struct Rec {
@@ -239,13 +239,49 @@ __global__ void __launch_bounds__(NT) radiate_f32x2_kernel(RadParams prm) {
     kk[m] = f2pack(k, k);
   }
   const f2r minus1 = f2pack(-1.f, -1.f);
-  // fp32 sums over the CTA's whole source chunk (<= kMaxChunkTiles tiles = 1024 sources,
-  // the fp32 budget of SURVEY §8(c-8)); the split-K partials are then summed in fp64
+  // fp32 sums over at most kMaxChunkTiles tiles (1024 sources, the fp32 budget of SURVEY
+  // §8(c-8)); split-K partials are then summed in fp64
   f2r ar[RP][MB], ai[RP][MB], br[RP][MB], bi[RP][MB];  // br / bi: ACC4 only
 #pragma unroll
   for (int p = 0; p < RP; ++p)
 #pragma unroll
     for (int m = 0; m < MB; ++m) ar[p][m] = ai[p][m] = br[p][m] = bi[p][m] = 0ull;
+  // fp32 sums flushed to the fp64 output every kMaxChunkTiles tiles (<= 1024 sources in
+  // fp32); later flushes of a chunk longer than that add to the output the
+  // CTA itself wrote (fixed order, no other CTA touches it)
+  auto flush = [&](bool add) {
+#pragma unroll
+    for (int p = 0; p < RP; ++p)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t l = tbase + (2 * p + h) * NT + tid;
+        if (l >= prm.n_lis) continue;
+#pragma unroll
+        for (int m = 0; m < MB; ++m) {
+          const int mode = mch * MB + m;
+          if (mode >= prm.n_modes) continue;
+          double re, im;
+          if constexpr (ACC4) {
+            re = h ? (double)f2hi(ar[p][m]) - (double)f2hi(br[p][m]) : (double)f2lo(ar[p][m]) - (double)f2lo(br[p][m]);
+            im = h ? (double)f2hi(ai[p][m]) + (double)f2hi(bi[p][m]) : (double)f2lo(ai[p][m]) + (double)f2lo(bi[p][m]);
+          } else {
+            re = h ? (double)f2hi(ar[p][m]) : (double)f2lo(ar[p][m]);
+            im = h ? (double)f2hi(ai[p][m]) : (double)f2lo(ai[p][m]);
+          }
+          double2* o = prm.out + ((size_t)split * prm.n_modes + mode) * prm.n_lis + l;
+          if (add) {
+            const double2 v = *o;
+            re += v.x;
+            im += v.y;
+          }
+          *o = make_double2(re, im);
+        }
+      }
+#pragma unroll
+    for (int p = 0; p < RP; ++p)
+#pragma unroll
+      for (int m = 0; m < MB; ++m) ar[p][m] = ai[p][m] = br[p][m] = bi[p][m] = 0ull;
+  };
 
   const int t0 = split * prm.chunk_tiles;
   const int t1 = min(t0 + prm.chunk_tiles, prm.n_tiles);
@@ -337,6 +373,7 @@ __global__ void __launch_bounds__(NT) radiate_f32x2_kernel(RadParams prm) {
         }
       }
     }
+    if ((it + 1) % kMaxChunkTiles == 0) flush(it + 1 > kMaxChunkTiles);
     __syncthreads();  // every thread is done with buf[st]
     if (tid == 0 && t0 + it + 2 < t1) {
       nat::fence_proxy_async_smem();
@@ -345,27 +382,7 @@ __global__ void __launch_bounds__(NT) radiate_f32x2_kernel(RadParams prm) {
     }
   }
 
-#pragma unroll
-  for (int p = 0; p < RP; ++p)
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int64_t l = tbase + (2 * p + h) * NT + tid;
-      if (l >= prm.n_lis) continue;
-#pragma unroll
-      for (int m = 0; m < MB; ++m) {
-        const int mode = mch * MB + m;
-        if (mode >= prm.n_modes) continue;
-        double re, im;
-        if constexpr (ACC4) {
-          re = h ? (double)f2hi(ar[p][m]) - (double)f2hi(br[p][m]) : (double)f2lo(ar[p][m]) - (double)f2lo(br[p][m]);
-          im = h ? (double)f2hi(ai[p][m]) + (double)f2hi(bi[p][m]) : (double)f2lo(ai[p][m]) + (double)f2lo(bi[p][m]);
-        } else {
-          re = h ? (double)f2hi(ar[p][m]) : (double)f2lo(ar[p][m]);
-          im = h ? (double)f2hi(ai[p][m]) : (double)f2lo(ai[p][m]);
-        }
-        prm.out[((size_t)split * prm.n_modes + mode) * prm.n_lis + l] = make_double2(re, im);
-      }
-    }
+  if (((t1 - t0) % kMaxChunkTiles) != 0 || t1 == t0) flush(t1 - t0 > kMaxChunkTiles);
 }
 
 // ------------------------------------------------------------------------------------
@@ -624,8 +641,9 @@ Plan make_plan(nat_prec prec, int64_t n_src, int n_modes, int64_t n_lis, int kin
       const int tile = pl.fp64 ? kTile64 : kTile;
       // per-SM pair throughput at the MUFU roofline (~1.0e10 pairs/s per SM, fp32)
       const double sm_rate = pl.fp64 ? 1.2e9 : 1.0e10;
-      // fp32 kernel: a CTA sums at most kMaxChunkTiles tiles in fp32 (then fp64 split-K)
-      const int c_max = pl.fp64 ? pl.n_tiles : std::min(pl.n_tiles, kMaxChunkTiles);
+      // fp32 kernel: a CTA's source chunk may span more than kMaxChunkTiles tiles (its fp32
+      // sums are flushed to fp64 every kMaxChunkTiles tiles)
+      const int c_max = pl.n_tiles;
       for (int c = 1; c <= c_max; ++c) {
         const int64_t ns = (pl.n_tiles + c - 1) / c;
         if (c > 1 && (pl.n_tiles + c - 2) / (c - 1) == ns) continue;  // same split count, more work
@@ -685,7 +703,7 @@ Plan make_plan(nat_prec prec, int64_t n_src, int n_modes, int64_t n_lis, int kin
       }
       pl.R = R;
       pl.NT = NT;
-      pl.chunk_tiles = std::min(std::min(c, pl.n_tiles), kMaxChunkTiles);
+      pl.chunk_tiles = std::min(c, pl.n_tiles);
       pl.tgt_tiles = (n_lis + (int64_t)R * NT - 1) / ((int64_t)R * NT);
       pl.smem = 2 * (size_t)kTile * pl.NF * sizeof(float);
     }

@@ -64,6 +64,10 @@ class _McOpts(C.Structure):
                 ("eps", C.c_double), ("samples_in", C.c_void_p), ("sample_tri_in", C.c_void_p)]
 
 
+class _NfConfig(C.Structure):
+    _fields_ = [("n_v", C.c_int), ("n_out", C.c_int)]
+
+
 class _Sources(C.Structure):
     _fields_ = [("n_src", C.c_int64), ("xyz", C.c_void_p), ("nrm", C.c_void_p),
                 ("w", C.c_void_p), ("n_modes", C.c_int), ("p", C.c_void_p), ("g", C.c_void_p),
@@ -141,6 +145,12 @@ _SIGS = {
                                         _P, _P, _I64, C.POINTER(_I64), C.POINTER(_D), _P, _SZ, _P]),
     "nat_listener_random_shell": (C.c_int, [C.POINTER(_D), _D, _I64, _D, _D, C.c_uint64, C.c_uint64, _P,
                                             _P]),
+    "nat_nf_param_count": (_I64, [C.POINTER(_NfConfig)]),
+    "nat_nf_workspace": (_SZ, [C.POINTER(_NfConfig), _I64]),
+    "nat_nf_forward": (C.c_int, [C.POINTER(_NfConfig), _P, _I64, _P, _P, _P, _SZ, _P]),
+    "nat_nf_train_step": (C.c_int, [C.POINTER(_NfConfig), _P, _P, _P, C.c_int, C.c_float, _I64, _P, _P, _P, _P, _P,
+                                    _SZ, _P]),
+    "nat_nf_gemm_bf16": (C.c_int, [_I64, _I64, _I64, _P, _I64, C.c_int, _P, _I64, C.c_int, _P, _I64, _P]),
 }
 
 _lib = None
@@ -783,3 +793,59 @@ def nat_kernel_timer_read(category: int, n_modes: int = 0):
     sec, pairs, n = C.c_double(0.0), C.c_double(0.0), C.c_int64(0)
     _check(lib().nat_kernel_timer_read_modes(int(category), int(n_modes), C.byref(sec), C.byref(pairs), C.byref(n)))
     return sec.value, pairs.value, n.value
+
+
+# ------------------------------------------------------------------------------------
+# NEXT-4: the NAT neural field (include/nat.h, nat_nf_*)
+# ------------------------------------------------------------------------------------
+class NeuralField:
+    """Parameters (fp32, device), Adam moments and a workspace for batches of up to
+    `max_batch` samples.  Inputs [n][3 + n_v] (normalised theta, phi, r, conditions),
+    outputs [n][n_out]."""
+
+    def __init__(self, n_v: int, n_out: int, params: torch.Tensor, max_batch: int):
+        self.cfg = _NfConfig(int(n_v), int(n_out))
+        n = lib().nat_nf_param_count(C.byref(self.cfg))
+        if n < 0:
+            raise NatError(-1, f"bad neural-field config n_v = {n_v}, n_out = {n_out}")
+        if params.numel() != n:
+            raise NatError(-1, f"{params.numel()} parameters, the layout has {n}")
+        self.params = params.to(torch.float32).contiguous()
+        self.m = torch.zeros_like(self.params)
+        self.v = torch.zeros_like(self.params)
+        self.step = 0
+        self.max_batch = int(max_batch)
+        self.ws = _ws(lib().nat_nf_workspace(C.byref(self.cfg), self.max_batch), self.params.device)
+        self.loss = torch.zeros(1, dtype=torch.float32, device=self.params.device)
+
+    @staticmethod
+    def param_count(n_v: int, n_out: int) -> int:
+        return int(lib().nat_nf_param_count(C.byref(_NfConfig(int(n_v), int(n_out)))))
+
+    def forward(self, inputs: torch.Tensor, out=None):
+        n = inputs.shape[0]
+        out = torch.empty(n, self.cfg.n_out, dtype=torch.float32, device=inputs.device) if out is None else out
+        _check(lib().nat_nf_forward(C.byref(self.cfg), _ptr(self.params), n, _ptr(inputs), _ptr(out), _ptr(self.ws),
+                                    self.ws.numel(), _stream()))
+        return out
+
+    def train_step(self, inputs: torch.Tensor, targets: torch.Tensor, lr: float, grad_out=None):
+        """One forward / MSE / backward / Adam step; returns the loss tensor (device, before
+        the update)."""
+        self.step += 1
+        _check(lib().nat_nf_train_step(C.byref(self.cfg), _ptr(self.params), _ptr(self.m), _ptr(self.v), self.step,
+                                       float(lr), inputs.shape[0], _ptr(inputs), _ptr(targets), _ptr(self.loss),
+                                       _ptr(grad_out), _ptr(self.ws), self.ws.numel(), _stream()))
+        return self.loss
+
+
+def nat_nf_gemm_bf16(A: torch.Tensor, B: torch.Tensor, a_mn=False, b_mn=False, out=None):
+    """C = A B^T on the tcgen05 tensor cores: A bf16 [M][K] (or [K][M] with a_mn), B bf16
+    [N][K] (or [K][N] with b_mn); returns fp32 [M][N]."""
+    M = A.shape[1] if a_mn else A.shape[0]
+    K = A.shape[0] if a_mn else A.shape[1]
+    N = B.shape[1] if b_mn else B.shape[0]
+    out = torch.empty(M, N, dtype=torch.float32, device=A.device) if out is None else out
+    _check(lib().nat_nf_gemm_bf16(M, N, K, _ptr(A), A.shape[1], int(bool(a_mn)), _ptr(B), B.shape[1],
+                                  int(bool(b_mn)), _ptr(out), out.shape[1], _stream()))
+    return out

@@ -25,7 +25,8 @@ def g(d, name, scale=1.0):
 
 def unit_scale(name):
     u = units[col[name]] if name in col else ""
-    return {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0, "ms": 1e-3, "us": 1e-6, "ns": 1e-9}.get(u, 1.0)
+    return {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0, "ms": 1e-3, "us": 1e-6, "ns": 1e-9,
+            "Ghz": 1e9, "Mhz": 1e6, "hz": 1.0}.get(u, 1.0)
 
 
 print("| kernel | duration (us) | DRAM read (MB) | DRAM write (MB) | FMA pipe % | XU (MUFU) % | issue active % | warps active % | regs | SM clock (GHz) |")
