@@ -557,6 +557,12 @@ def main():
             secondary["C3"] = S.run_c3(nat, torch, rank, world, min(args.steps, 5), barrier, allreduce_max_sum)
         except Exception as ex:
             secondary["C3"] = {"error": repr(ex)}
+        try:
+            pk = os.path.join(ROOT, "MEASURED_PEAKS.json")
+            secondary["NEXT4"] = S.run_nf(nat, torch, max(args.steps, 5),
+                                          peaks=json.load(open(pk)) if os.path.exists(pk) else None)
+        except Exception as ex:
+            secondary["NEXT4"] = {"error": repr(ex)}
 
     if rank != 0:
         if world > 1:

@@ -385,3 +385,54 @@ def run_c3(nat, torch, rank, world, steps, barrier, allreduce_max_sum):
             "value": pairs_all / (ms_max * 1e-3) / 1e9, "unit": "Gpair-evals/s", "ms_per_step": ms_max / steps,
             "steps": steps, "parallelism": f"modes dealt x{world}" if world > 1 else "1 GPU",
             "mc_iters": iters}
+
+
+def run_nf(nat, torch, steps, batch=262144, peaks=None):
+    """NEXT-4 secondary line: training steps of the NAT neural field on
+    C4-shaped samples — one config's 64^3 listener set per batch (normalised theta, phi, r;
+    height, size, material), 8 outputs (|p| of the modes), synthetic smooth targets.
+    Device time per step (CUDA events) and the tensor-core products' throughput
+    (nat kernel timer: 2 M N K flops per product) against the measured bf16 peak."""
+    import nat_inputs as I
+    n_v, n_out = 3, 8
+    shapes = nat.NeuralField.param_shapes(n_v, n_out)
+    flat = torch.from_numpy(I.nf_init_params(shapes, 20250606, grid_scale=1e-4)).cuda()
+    x = torch.from_numpy(I.nf_samples(batch, n_v, 20250607)).cuda()
+    tgt = torch.stack([torch.sin(3 * x[:, 0] + q) * torch.cos(2 * x[:, 1]) * (1 + x[:, 3 + q % 3])
+                       for q in range(n_out)], 1).contiguous()
+    net = nat.NeuralField(n_v, n_out, flat, batch)
+    for _ in range(3):
+        net.train_step(x, tgt, 1e-3)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        loss = net.train_step(x, tgt, 1e-3)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    nat.nat_kernel_timer_enable(True)
+    net.train_step(x, tgt, 1e-3)
+    sec, flops, nl = nat.nat_kernel_timer_read(nat.KTIMER_NF_GEMM)
+    nat.nat_kernel_timer_enable(False)
+    peak = (peaks or {}).get("bf16_tflops", 1590.0)
+    hbm = (peaks or {}).get("hbm_gbs", 6650.0)
+    # algorithmic HBM bytes of the 15 products per step (bf16 activations / gradients read
+    # once and written once; weights negligible): forward, input gradients, weight gradients
+    dims = [64, 128, 128, 128, 128, 16]
+    fwd = sum(batch * 2 * (dims[q] + dims[q + 1]) for q in range(5))
+    bwd_in = sum(batch * 2 * (dims[q + 1] + 2 * dims[q]) for q in range(5))
+    bwd_w = sum(batch * 2 * (dims[q + 1] + dims[q]) for q in range(5))
+    gemm_bytes = fwd + bwd_in + bwd_w
+    return {"workload": f"NEXT-4 NAT neural field training step (hash grid 4 x 8..64, PE(6), 4 x 128 MLP, MSE, "
+                        f"Adam), batch {batch} samples, 3 condition variables, 8 outputs, synthetic targets",
+            "ms_per_step": ms, "samples_per_s": batch / (ms * 1e-3), "loss": float(loss.item()),
+            "gemm": {"bound": "tensor", "achieved": flops / sec / 1e12 if sec > 0 else None, "peak": peak,
+                     "unit": "TFLOP/s", "frac": (flops / sec / 1e12 / peak) if sec > 0 else None,
+                     "launches_per_step": nl, "flops_per_step": flops, "gemm_ms_per_step": 1e3 * sec,
+                     "peak_note": "MEASURED_PEAKS.json bf16_tflops (cuBLAS burst)",
+                     "hbm_view": {"bound": "hbm", "bytes_per_step": gemm_bytes,
+                                  "achieved": gemm_bytes / sec / 1e9 if sec > 0 else None, "peak": hbm,
+                                  "unit": "GB/s", "frac": (gemm_bytes / sec / 1e9 / hbm) if sec > 0 else None,
+                                  "note": "K <= 128: each product moves ~2 bytes per flop x 1/64 .. 1/128; the "
+                                          "activations' HBM traffic, not the tensor pipe, bounds these layers"}}}

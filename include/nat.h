@@ -57,7 +57,8 @@ const char* nat_last_error(void);
 
 /* Diagnostics (bench.py's roofline pass): CUDA events on the launching stream around the
  * main kernel of each category — 0: MC operator (a10), 1: MC right-hand side (a9),
- * 2: radiation (a11), 3: far assembly (a4).  Off by default (no events, no overhead).
+ * 2: radiation (a11), 3: far assembly (a4), 4: the neural field's tensor-core products
+ * (NEXT-4; "pairs" = flops 2 M N K).  Off by default (no events, no overhead).
  * nat_kernel_timer_enable resets the totals and switches the timer on/off;
  * nat_kernel_timer_read synchronises the recorded events and returns, for one category,
  * the summed kernel time, the algorithmic pair-evaluations of those launches and their

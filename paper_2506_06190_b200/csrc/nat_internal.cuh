@@ -52,7 +52,7 @@ int device_sm_count();
 // Kernel timer (nat_kernel_timer_*, diagnostics): events around the main kernel of a
 // category on the launching stream; `pairs` = algorithmic pair-evaluations of the launch;
 // `skip` (optional device word) marks launches that returned at once (not counted).
-enum { kTimerMcOp = 0, kTimerMcRhs = 1, kTimerRadiate = 2, kTimerFar = 3, kTimerCats = 4 };
+enum { kTimerMcOp = 0, kTimerMcRhs = 1, kTimerRadiate = 2, kTimerFar = 3, kTimerNfGemm = 4, kTimerCats = 5 };
 bool ktimer_on();
 void ktimer_begin(int cat, cudaStream_t s);
 // n_modes: wavenumbers evaluated per pair by the launch (roofline bucket; 0 = none)

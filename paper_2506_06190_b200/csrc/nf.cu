@@ -128,9 +128,12 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                : "memory");
 }
 
-// 16-byte unit of 8 bf16 (zero outside the matrix)
-__device__ __forceinline__ uint4 ld16(const bf16* p, bool ok) {
-  return ok ? *reinterpret_cast<const uint4*>(p) : make_uint4(0u, 0u, 0u, 0u);
+// 16-byte asynchronous global -> shared copy (cp.async, LDGSTS); zero-filled outside the
+// matrix (src-size 0)
+__device__ __forceinline__ void cp16(char* dst, const bf16* src, bool ok) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(nat::smem_u32(dst)),
+               "l"(ok ? src : nullptr), "r"(ok ? 16 : 0)
+               : "memory");
 }
 
 // Stages rows [r0, r0 + R) x k [k0, k0 + 64) of an operand into the core-matrix layout:
@@ -140,19 +143,19 @@ template <int R, bool MN>
 __device__ __forceinline__ void stage_operand(const bf16* P, int64_t ld, int64_t rows, int64_t K, int64_t r0,
                                               int64_t k0, char* smem) {
   constexpr int kUnits = R * (kBK / 8);
+#pragma unroll 4
   for (int u = threadIdx.x; u < kUnits; u += kGT) {
     if constexpr (!MN) {
       const int r = u / (kBK / 8), kc = u % (kBK / 8);
       const int64_t gr = r0 + r, gk = k0 + kc * 8;
-      const uint4 v = ld16(P + gr * ld + gk, gr < rows && gk < K);
-      *reinterpret_cast<uint4*>(smem + ((r / 8) * (kBK / 8) + kc) * 128 + (r % 8) * 16) = v;
+      cp16(smem + ((r / 8) * (kBK / 8) + kc) * 128 + (r % 8) * 16, P + gr * ld + gk, gr < rows && gk < K);
     } else {
       const int kk = u / (R / 8), rc = u % (R / 8);
       const int64_t gk = k0 + kk, gr = r0 + rc * 8;
-      const uint4 v = ld16(P + gk * ld + gr, gk < K && gr < rows);
-      *reinterpret_cast<uint4*>(smem + ((kk / 8) * (R / 8) + rc) * 128 + (kk % 8) * 16) = v;
+      cp16(smem + ((kk / 8) * (R / 8) + rc) * 128 + (kk % 8) * 16, P + gk * ld + gr, gk < K && gr < rows);
     }
   }
+  asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
 template <int BN, bool AMN, bool BMN>
@@ -196,7 +199,8 @@ __global__ void __launch_bounds__(kGT) nf_gemm_kernel(GemmArgs g) {
     const int64_t k0 = kb + (int64_t)c * kBK;
     stage_operand<kGM, AMN>(g.A, g.lda, g.M, ke, m0, k0, sA[s]);
     stage_operand<BN, BMN>(g.B, g.ldb, g.N, ke, 0, k0, sB[s]);
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core reads
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // smem writes -> tensor core reads
     __syncthreads();
     if (tid == 0) {
       asm volatile("tcgen05.fence::after_thread_sync;");
@@ -254,13 +258,32 @@ __global__ void __launch_bounds__(kGT) nf_gemm_kernel(GemmArgs g) {
 #pragma unroll
           for (int e = 0; e < 8; ++e) f[q + e] = (row_ok && __bfloat162float(hb[e]) > 0.f) ? f[q + e] : 0.f;
         }
-        // column sums of the masked gradient (bias gradient): warp tree, then the 4 warps
+        // column sums of the masked gradient (bias gradient): a transposing butterfly over the
+        // warp (31 shuffles for 32 columns; lane l ends with column l's sum over the 32 rows),
+        // then the 4 warps in warp order
+        if constexpr (W == 32) {
+          float t[32];
 #pragma unroll
-        for (int q = 0; q < W; ++q) {
-          float t = f[q];
+          for (int q = 0; q < 32; ++q) t[q] = f[q];
 #pragma unroll
-          for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-          if (lane == 0) colsum[warp][n0 + q] = t;
+          for (int o = 16; o > 0; o >>= 1) {
+            const bool up = (lane & o) != 0;
+#pragma unroll
+            for (int q = 0; q < o; ++q) {
+              const float send = up ? t[q] : t[q + o];
+              const float recv = __shfl_xor_sync(0xffffffffu, send, o);
+              t[q] = (up ? t[q + o] : t[q]) + recv;
+            }
+          }
+          colsum[warp][n0 + lane] = t[0];
+        } else {
+#pragma unroll
+          for (int q = 0; q < W; ++q) {
+            float t = f[q];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+            if (lane == 0) colsum[warp][n0 + q] = t;
+          }
         }
       }
       if (row_ok) {
@@ -318,10 +341,15 @@ cudaError_t launch_gemm_n(const GemmArgs& g, int splits, cudaStream_t s) {
 }
 
 cudaError_t launch_gemm(const GemmArgs& g, bool a_mn, bool b_mn, int splits, cudaStream_t s) {
-  if (!a_mn && !b_mn) return launch_gemm_n<false, false>(g, splits, s);
-  if (!a_mn && b_mn) return launch_gemm_n<false, true>(g, splits, s);
-  if (a_mn && !b_mn) return launch_gemm_n<true, false>(g, splits, s);
-  return launch_gemm_n<true, true>(g, splits, s);
+  const bool timed = nat::ktimer_on();  // diagnostics: flops = 2 M N K of the product
+  if (timed) nat::ktimer_begin(nat::kTimerNfGemm, s);
+  cudaError_t e;
+  if (!a_mn && !b_mn) e = launch_gemm_n<false, false>(g, splits, s);
+  else if (!a_mn && b_mn) e = launch_gemm_n<false, true>(g, splits, s);
+  else if (a_mn && !b_mn) e = launch_gemm_n<true, false>(g, splits, s);
+  else e = launch_gemm_n<true, true>(g, splits, s);
+  if (timed) nat::ktimer_end(nat::kTimerNfGemm, s, 2.0 * (double)g.M * (double)g.N * (double)g.K, nullptr);
+  return e;
 }
 
 // =====================================================================================
@@ -432,20 +460,39 @@ __global__ void __launch_bounds__(kLossT) nf_loss_kernel(int64_t n, int n_out, c
   }
 }
 
-// out[j] = sum_p part[p][j] (p ascending) — split-K and per-tile partials, fixed order.
+// Split-K / per-tile partial sums: out[j] = sum_p part[p][j] in a fixed order.
 // transpose: out holds [cols][rows] of a [rows][cols] partial layout (dW of the last layer).
-__global__ void nf_reduce_kernel(int64_t nparts, int64_t rows, int64_t cols, const float* __restrict__ part,
-                                 float* __restrict__ out, int64_t out_rows, int64_t out_cols, bool transpose,
-                                 float scale) {
-  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (j >= rows * cols) return;
+// 8 partial groups per output (group g takes p = g, g + 8, ... in
+// ascending order, then the 8 group sums in group order): deterministic, coalesced over
+// 32 consecutive outputs per block.
+__global__ void __launch_bounds__(256) nf_reduce_wide_kernel(int64_t nparts, int64_t rows, int64_t cols,
+                                                             const float* __restrict__ part, float* __restrict__ out,
+                                                             int64_t out_rows, int64_t out_cols, bool transpose) {
+  __shared__ float sm[8][33];
+  const int lane = threadIdx.x & 31, grp = threadIdx.x >> 5;
+  const int64_t j = blockIdx.x * 32 + lane;
+  const int64_t total = rows * cols;
   float t = 0.f;
-  for (int64_t p = 0; p < nparts; ++p) t += part[p * rows * cols + j];
-  const int64_t r = j / cols, c = j % cols;
-  if (!transpose) {
-    if (r < out_rows && c < out_cols) out[r * out_cols + c] = scale * t;
-  } else {
-    if (c < out_rows && r < out_cols) out[c * out_cols + r] = scale * t;
+  if (j < total) {
+    int64_t p = grp;
+    for (; p + 24 < nparts; p += 32) {
+      const float a = part[p * total + j], b = part[(p + 8) * total + j], c = part[(p + 16) * total + j],
+                  d = part[(p + 24) * total + j];
+      t = (((t + a) + b) + c) + d;
+    }
+    for (; p < nparts; p += 8) t += part[p * total + j];
+  }
+  sm[grp][lane] = t;
+  __syncthreads();
+  if (grp == 0 && j < total) {
+    float u = sm[0][lane];
+    for (int g = 1; g < 8; ++g) u += sm[g][lane];
+    const int64_t r = j / cols, c = j % cols;
+    if (!transpose) {
+      if (r < out_rows && c < out_cols) out[r * out_cols + c] = u;
+    } else {
+      if (c < out_rows && r < out_cols) out[c * out_cols + r] = u;
+    }
   }
 }
 
@@ -456,36 +503,53 @@ __global__ void nf_loss_finish_kernel(int64_t nparts, const double* __restrict__
   *loss = (float)(t / (double)count);
 }
 
-// dGrid[level][row] += w_corner * dX[b][level*4 + f]   (atomics: order-free sums)
-__global__ void nf_grid_backward_kernel(int64_t n, int n_v, const float* __restrict__ in, const float* __restrict__ dX,
-                                        Layout L, float* __restrict__ grad) {
-  const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (b >= n) return;
-  const float* x = in + b * (3 + n_v);
+// dGrid[level][row] += w_corner * dX[b][level*4 + f]   (atomics: order-free sums).
+// Persistent CTAs; the two coarse lattices (729 + 4913 rows, every sample hits them) are
+// accumulated in shared memory and flushed once per CTA, the fine ones atomically in HBM.
+constexpr int kSmemLevels = 2;
+__host__ __device__ constexpr int64_t smem_grid_rows() { return level_rows(0) + level_rows(1); }
+
+__global__ void __launch_bounds__(256) nf_grid_backward_kernel(int64_t n, int n_v, const float* __restrict__ in,
+                                                               const float* __restrict__ dX, Layout L,
+                                                               float* __restrict__ grad) {
+  extern __shared__ float sg[];  // [smem_grid_rows][4]
+  for (int64_t i = threadIdx.x; i < smem_grid_rows() * kFeat; i += blockDim.x) sg[i] = 0.f;
+  __syncthreads();
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < n; b += (int64_t)gridDim.x * blockDim.x) {
+    const float* x = in + b * (3 + n_v);
 #pragma unroll
-  for (int l = 0; l < kLevels; ++l) {
-    const int N = level_res(l);
-    int64_t i0[3];
-    float fr[3];
+    for (int l = 0; l < kLevels; ++l) {
+      const int N = level_res(l);
+      int64_t i0[3];
+      float fr[3];
 #pragma unroll
-    for (int d = 0; d < 3; ++d) {
-      const float p = x[d] * (float)N;
-      const float fl = fminf(fmaxf(floorf(p), 0.f), (float)(N - 1));
-      i0[d] = (int64_t)fl;
-      fr[d] = p - fl;
+      for (int d = 0; d < 3; ++d) {
+        const float p = x[d] * (float)N;
+        const float fl = fminf(fmaxf(floorf(p), 0.f), (float)(N - 1));
+        i0[d] = (int64_t)fl;
+        fr[d] = p - fl;
+      }
+      const float4 g = *reinterpret_cast<const float4*>(dX + b * kInPad + l * kFeat);
+      float* G = l < kSmemLevels ? sg + (l == 0 ? 0 : level_rows(0) * kFeat) : grad + L.grid[l];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const int dx = c & 1, dy = (c >> 1) & 1, dz = (c >> 2) & 1;
+        const float wx = dx ? fr[0] : 1.f - fr[0], wy = dy ? fr[1] : 1.f - fr[1], wz = dz ? fr[2] : 1.f - fr[2];
+        const float w = (wx * wy) * wz;
+        float* r = G + vertex_row(l, i0[0] + dx, i0[1] + dy, i0[2] + dz) * kFeat;
+        atomicAdd(r + 0, w * g.x);
+        atomicAdd(r + 1, w * g.y);
+        atomicAdd(r + 2, w * g.z);
+        atomicAdd(r + 3, w * g.w);
+      }
     }
-    const float4 g = *reinterpret_cast<const float4*>(dX + b * kInPad + l * kFeat);
-    float* G = grad + L.grid[l];
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      const int dx = c & 1, dy = (c >> 1) & 1, dz = (c >> 2) & 1;
-      const float wx = dx ? fr[0] : 1.f - fr[0], wy = dy ? fr[1] : 1.f - fr[1], wz = dz ? fr[2] : 1.f - fr[2];
-      const float w = (wx * wy) * wz;
-      float* r = G + vertex_row(l, i0[0] + dx, i0[1] + dy, i0[2] + dz) * kFeat;
-      atomicAdd(r + 0, w * g.x);
-      atomicAdd(r + 1, w * g.y);
-      atomicAdd(r + 2, w * g.z);
-      atomicAdd(r + 3, w * g.w);
+  }
+  __syncthreads();
+  for (int64_t i = threadIdx.x; i < smem_grid_rows() * kFeat; i += blockDim.x) {
+    const float v = sg[i];
+    if (v != 0.f) {
+      const int64_t l0 = level_rows(0) * kFeat;
+      atomicAdd(grad + (i < l0 ? L.grid[0] + i : L.grid[1] + (i - l0)), v);
     }
   }
 }
@@ -670,8 +734,8 @@ extern "C" nat_status nat_nf_train_step(const nat_nf_config* cfg, float* params,
   nf_loss_finish_kernel<<<1, 1, 0, s>>>(w.lblocks, w.lpart, n * cfg->n_out, loss);
   NAT_CUDA_TRY(cudaMemsetAsync(w.grad, 0, sizeof(float) * L.total, s));
   // output-layer bias gradient: column sums of dY
-  nf_reduce_kernel<<<1, kOutPad, 0, s>>>(w.lblocks, 1, kOutPad, w.bpart, w.grad + L.b[kNHidden], 1, L.out[kNHidden],
-                                         false, 1.f);
+  nf_reduce_wide_kernel<<<1, 256, 0, s>>>(w.lblocks, 1, kOutPad, w.bpart, w.grad + L.b[kNHidden], 1,
+                                          L.out[kNHidden], false);
   // backward through the layers: d = gradient with respect to layer q's output
   const bf16* d = w.dY;
   int dcols = kOutPad;
@@ -703,8 +767,8 @@ extern "C" nat_status nat_nf_train_step(const nat_nf_config* cfg, float* params,
     }
     NF_LAUNCH(launch_gemm(gw, true, true, (int)w.splits, s));
     const int64_t rows = gw.M, cols = gw.N;
-    nf_reduce_kernel<<<(unsigned)((rows * cols + 255) / 256), 256, 0, s>>>(
-        w.splits, rows, cols, w.wpart, w.grad + L.W[q], L.out[q], in, q == kNHidden, 1.f);
+    nf_reduce_wide_kernel<<<(unsigned)((rows * cols + 31) / 32), 256, 0, s>>>(
+        w.splits, rows, cols, w.wpart, w.grad + L.W[q], L.out[q], in, q == kNHidden);
     NAT_LAUNCH_CHECK();
     // d_in = (d W_q) * relu'(h_in): M = n, N = in, K = out; B = W_q as [K = out][N = in] (MN-major)
     GemmArgs gd{};
@@ -725,8 +789,8 @@ extern "C" nat_status nat_nf_train_step(const nat_nf_config* cfg, float* params,
       gd.colpart = w.cpart;
       NF_LAUNCH(launch_gemm(gd, false, true, 1, s));
       // bias gradient of layer q - 1: column sums of the masked gradient, tile order
-      nf_reduce_kernel<<<1, kHidden, 0, s>>>(w.tiles, 1, kHidden, w.cpart, w.grad + L.b[q - 1], 1, kHidden, false,
-                                             1.f);
+      nf_reduce_wide_kernel<<<kHidden / 32, 256, 0, s>>>(w.tiles, 1, kHidden, w.cpart, w.grad + L.b[q - 1], 1,
+                                                          kHidden, false);
       NAT_LAUNCH_CHECK();
       d = w.dH[q & 1];
       dcols = in;
@@ -738,7 +802,12 @@ extern "C" nat_status nat_nf_train_step(const nat_nf_config* cfg, float* params,
       NF_LAUNCH(launch_gemm(gd, false, true, 1, s));
     }
   }
-  nf_grid_backward_kernel<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(n, cfg->n_v, inputs, w.dX, L, w.grad);
+  {
+    const size_t gsm = sizeof(float) * smem_grid_rows() * kFeat;
+    NAT_CUDA_TRY(cudaFuncSetAttribute(nf_grid_backward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsm));
+    const int64_t ctas = std::min<int64_t>(2 * (int64_t)nat::device_sm_count(), (n + 255) / 256);
+    nf_grid_backward_kernel<<<(unsigned)ctas, 256, gsm, s>>>(n, cfg->n_v, inputs, w.dX, L, w.grad);
+  }
   NAT_LAUNCH_CHECK();
   if (grad_out) NAT_CUDA_TRY(cudaMemcpyAsync(grad_out, w.grad, sizeof(float) * L.total, cudaMemcpyDeviceToDevice, s));
   const float b1 = 0.9f, b2 = 0.999f;

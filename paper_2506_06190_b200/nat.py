@@ -780,7 +780,7 @@ def nat_bem_mf_solve(op: BemMf, b_local: torch.Tensor, comm: Optional["Comm"] = 
 # ------------------------------------------------------------------------------------
 # diagnostics: per-kernel CUDA-event timer (nat_kernel_timer_*)
 # ------------------------------------------------------------------------------------
-KTIMER_MC_OP, KTIMER_MC_RHS, KTIMER_RADIATE, KTIMER_FAR = 0, 1, 2, 3
+KTIMER_MC_OP, KTIMER_MC_RHS, KTIMER_RADIATE, KTIMER_FAR, KTIMER_NF_GEMM = 0, 1, 2, 3, 4
 
 
 def nat_kernel_timer_enable(on: bool = True):
@@ -821,6 +821,19 @@ class NeuralField:
     @staticmethod
     def param_count(n_v: int, n_out: int) -> int:
         return int(lib().nat_nf_param_count(C.byref(_NfConfig(int(n_v), int(n_out)))))
+
+    @staticmethod
+    def param_shapes(n_v: int, n_out: int):
+        """Block shapes of the parameter vector as include/nat.h documents it: 4 lattices
+        [(N+1)^3][4], N = 8, 16, 32, 64, then W [out][in] and b [out] of the 5 layers."""
+        shapes = [((8 << l) + 1) ** 3 for l in range(4)]
+        shapes = [(min(r, 1 << 19), 4) for r in shapes]
+        dims = [64, 128, 128, 128, 128, int(n_out)]
+        for q in range(5):
+            shapes += [(dims[q + 1], dims[q]), (dims[q + 1],)]
+        if sum(int(np.prod(s)) for s in shapes) != NeuralField.param_count(n_v, n_out):
+            raise NatError(-1, "parameter layout mismatch with libnat")
+        return shapes
 
     def forward(self, inputs: torch.Tensor, out=None):
         n = inputs.shape[0]

@@ -43,6 +43,8 @@ def test_param_layout_matches_oracle():
     nat = _nat()
     for n_v, n_out in ((3, 8), (1, 1), (4, 16)):
         assert nat.NeuralField.param_count(n_v, n_out) == sum(int(np.prod(s)) for _, s in NF.param_layout(n_v, n_out))
+        assert [tuple(s) for s in nat.NeuralField.param_shapes(n_v, n_out)] == \
+            [tuple(s) for _, s in NF.param_layout(n_v, n_out)]
 
 
 @pytest.mark.parametrize("n", [128, 1000, 8192])
