@@ -446,8 +446,8 @@ __global__ void combine_kernel(const double2* __restrict__ V, const double2* __r
 }
 
 // ------------------------------------------------------------------------------------
-// Fused Arnoldi step for short vectors (n <= kFusedMaxN; the MC systems, M = 2048-10,000):
-// one thread-block cluster of kCL CTAs per system runs the whole CGS2 iteration after the
+// Fused Arnoldi step for short vectors (n <= CL x 2048; the MC systems, M = 2048-10,000):
+// one thread-block cluster of CL CTAs per system runs the whole CGS2 iteration after the
 // operator product — both projection passes (dots + update), the norm, the Givens step of
 // the system and the scaling of the new basis vector — in ONE launch.  CTA c owns rows
 // [c rpc, (c+1) rpc) of the system; the per-CTA partial dot products are exchanged through
@@ -458,9 +458,7 @@ __global__ void combine_kernel(const double2* __restrict__ V, const double2* __r
 // memory caps residency at one CTA per SM, which keeps the basis slices of the clusters in
 // flight (~18 systems) inside the 126 MB L2.
 // ------------------------------------------------------------------------------------
-constexpr int kCL = 8;                         // CTAs per system (portable cluster size)
-constexpr int kFusedMaxRT = 8;                 // rows per thread
-constexpr int64_t kFusedMaxN = (int64_t)kCL * kT * kFusedMaxRT;
+constexpr int kFusedMaxRT = 8;                 // rows per thread (n <= CL x 256 x 8)
 constexpr int kFusedSmem = 120 * 1024;         // residency cap (1 CTA / SM)
 
 __global__ void publish_mask_kernel(const unsigned long long* __restrict__ mask, volatile unsigned long long* out) {
@@ -472,8 +470,8 @@ __global__ void publish_mask_kernel(const unsigned long long* __restrict__ mask,
 // loads of 16 B in flight per lane).  Update: group g (256 threads, RT rows each) sums the
 // basis vectors k = g, g + KG, ... in ascending order; group 0 adds the KG partial sums in
 // group order (deterministic) and keeps w in registers.
-template <int RT, int NTH>
-__global__ void __cluster_dims__(kCL, 1, 1) __launch_bounds__(NTH, 1)
+template <int RT, int NTH, int CL>
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NTH, 1)
     arnoldi_fused_kernel(const double2* __restrict__ V, size_t vstride, int64_t ldv, int64_t n, int64_t rpc,
                          const double2* __restrict__ Wj, double2* __restrict__ Vnext, uint64_t active,
                          GivensArgs ga) {
@@ -552,7 +550,7 @@ __global__ void __cluster_dims__(kCL, 1, 1) __launch_bounds__(NTH, 1)
     for (int k = tid; k <= j; k += NTH) {
       double2 t = make_double2(0.0, 0.0);
 #pragma unroll
-      for (int q = 0; q < kCL; ++q) {
+      for (int q = 0; q < CL; ++q) {
         const double2 p = cl.map_shared_rank(part, q)[k];
         t.x += p.x;
         t.y += p.y;
@@ -635,7 +633,7 @@ __global__ void __cluster_dims__(kCL, 1, 1) __launch_bounds__(NTH, 1)
   cl.sync();
   if (tid == 0) {
     double a = 0.0;
-    for (int q = 0; q < kCL; ++q) a += *cl.map_shared_rank(&nrm_part, q);
+    for (int q = 0; q < CL; ++q) a += *cl.map_shared_rank(&nrm_part, q);
     nrm_all = sqrt(a);
   }
   __syncthreads();
@@ -778,8 +776,12 @@ nat_status gmres_batched(int nsys, int64_t n, int64_t ldv, const double2* b, dou
     const char* e = std::getenv("NAT_GMRES_FUSED");
     return !(e && e[0] == '0');
   }();
-  const bool fused = fused_env && n <= kFusedMaxN;
-  const int64_t rpc = (n + kCL - 1) / kCL;
+  static const int fused_cl = [] {  // CTAs per system: NAT_FUSED_CL = 4 (default) or 8
+    const char* e = std::getenv("NAT_FUSED_CL");
+    return (e && std::atoi(e) == 8) ? 8 : 4;
+  }();
+  const bool fused = fused_env && n <= (int64_t)fused_cl * kT * kFusedMaxRT;
+  const int64_t rpc = (n + fused_cl - 1) / fused_cl;
   const int need_rt = (int)((rpc + kT - 1) / kT);
   const int fused_rt = need_rt <= 1 ? 1 : need_rt <= 2 ? 2 : need_rt <= 4 ? 4 : 8;
   static const size_t fused_cap = [] {  // NAT_FUSED_SMEM_KB: residency cap (tuning A/B only)
@@ -787,15 +789,22 @@ nat_status gmres_batched(int nsys, int64_t n, int64_t ldv, const double2* b, dou
     return e ? (size_t)std::atoi(e) * 1024 : (size_t)kFusedSmem;
   }();
   const int fused_kg = fused_rt <= 2 ? 3 : 2;  // update groups (NTH / 256)
+  const int fused_nth = fused_kg * kT;
   const size_t fsmem = std::max(fused_cap, sizeof(double2) * ((size_t)rpc * fused_kg + 4 * (size_t)mp1));
+  using FusedFn = void (*)(const double2*, size_t, int64_t, int64_t, int64_t, const double2*, double2*, uint64_t,
+                           GivensArgs);
+  FusedFn fused_fn = nullptr;
+  if (fused_cl == 8)
+    fused_fn = fused_rt == 1 ? arnoldi_fused_kernel<1, 768, 8> : fused_rt == 2 ? arnoldi_fused_kernel<2, 768, 8>
+             : fused_rt == 4 ? arnoldi_fused_kernel<4, 512, 8> : arnoldi_fused_kernel<8, 512, 8>;
+  else
+    fused_fn = fused_rt == 1 ? arnoldi_fused_kernel<1, 768, 4> : fused_rt == 2 ? arnoldi_fused_kernel<2, 768, 4>
+             : fused_rt == 4 ? arnoldi_fused_kernel<4, 512, 4> : arnoldi_fused_kernel<8, 512, 4>;
   if (fused) {
     if (fsmem > (size_t)kBackSmemMax) return fail(NAT_ERR_INVALID_ARG, "max_iter %d too large", m);
     if (gsmem > 48 * 1024)
       NAT_CUDA_TRY(cudaFuncSetAttribute(givens_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsmem));
-    auto set = [&](const void* f) { return cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem); };
-    NAT_CUDA_TRY(fused_rt == 1 ? set((const void*)arnoldi_fused_kernel<1, 768>)
-                 : fused_rt == 2 ? set((const void*)arnoldi_fused_kernel<2, 768>)
-                 : fused_rt == 4 ? set((const void*)arnoldi_fused_kernel<4, 512>) : set((const void*)arnoldi_fused_kernel<8, 512>));
+    NAT_CUDA_TRY(cudaFuncSetAttribute((const void*)fused_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem));
   }
   int n_timed = 0;
   auto enqueue = [&](int j, uint64_t host_active) -> nat_status {
@@ -815,14 +824,9 @@ nat_status gmres_batched(int nsys, int64_t n, int64_t ldv, const double2* b, dou
     }
     ga.j = j;
     if (fused) {  // short vectors: the whole CGS2 step in one cluster launch per iteration
-      const dim3 grid(kCL, nsys);
+      const dim3 grid(fused_cl, nsys);
       cudaError_t e = cudaSuccess;
-      switch (fused_rt) {
-        case 1: arnoldi_fused_kernel<1, 768><<<grid, 768, fsmem, s>>>(ws.V, vstride, ldv, n, rpc, Wj, ws.V + (size_t)(j + 1) * vstride, all, ga); break;
-        case 2: arnoldi_fused_kernel<2, 768><<<grid, 768, fsmem, s>>>(ws.V, vstride, ldv, n, rpc, Wj, ws.V + (size_t)(j + 1) * vstride, all, ga); break;
-        case 4: arnoldi_fused_kernel<4, 512><<<grid, 512, fsmem, s>>>(ws.V, vstride, ldv, n, rpc, Wj, ws.V + (size_t)(j + 1) * vstride, all, ga); break;
-        default: arnoldi_fused_kernel<8, 512><<<grid, 512, fsmem, s>>>(ws.V, vstride, ldv, n, rpc, Wj, ws.V + (size_t)(j + 1) * vstride, all, ga); break;
-      }
+      fused_fn<<<grid, fused_nth, fsmem, s>>>(ws.V, vstride, ldv, n, rpc, Wj, ws.V + (size_t)(j + 1) * vstride, all, ga);
       e = cudaGetLastError();
       if (e != cudaSuccess) return fail(NAT_ERR_CUDA, "fused Arnoldi launch: %s", cudaGetErrorString(e));
       givens_kernel<<<nsys, 32, gsmem, s>>>(all, ga);
