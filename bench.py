@@ -544,30 +544,6 @@ def main():
 
     n_launch = None if args.no_profile_count else count_launches(sweep, torch, sweep.geo_ids[:1])
 
-    secondary = None
-    if not args.no_secondary:
-        import bench_secondary as S
-        secondary = {}
-        comm = nat.Comm.from_torch_distributed() if world > 1 else None
-        try:
-            secondary["C2"] = S.run_c2(nat, torch, rank, world, comm, min(args.steps, 5), barrier, allreduce_max_sum)
-        except Exception as ex:  # reported, not fatal: the headline is C4
-            secondary["C2"] = {"error": repr(ex)}
-        try:
-            secondary["C3"] = S.run_c3(nat, torch, rank, world, min(args.steps, 5), barrier, allreduce_max_sum)
-        except Exception as ex:
-            secondary["C3"] = {"error": repr(ex)}
-        try:
-            pk = os.path.join(ROOT, "MEASURED_PEAKS.json")
-            secondary["NEXT4"] = S.run_nf(nat, torch, max(args.steps, 5),
-                                          peaks=json.load(open(pk)) if os.path.exists(pk) else None)
-        except Exception as ex:
-            secondary["NEXT4"] = {"error": repr(ex)}
-
-    if rank != 0:
-        if world > 1:
-            dist.destroy_process_group()
-        return
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         op = OraclePool()
@@ -595,9 +571,47 @@ def main():
         "gpu_launches": (n_launch * len(sweep.geo_ids) * K) if n_launch else None,
         "gpu_launches_note": "libnat kernels of one geometry counted with torch.profiler (CUPTI) x geometries x steps",
         "clocks": clk,
-        "secondary": secondary,
+        "secondary": None,
     }
-    print(json.dumps(line), flush=True)
+
+    def emit(sec):
+        if rank == 0:
+            line["secondary"] = sec
+            print(json.dumps(line), flush=True)
+
+    secondary = None
+    if not args.no_secondary:
+        # the secondary lines run after the headline is final; a watchdog prints the headline
+        # (and exits every rank) if they hang, e.g. in a collective at N > 1
+        limit = float(os.environ.get("NAT_BENCH_SECONDARY_TIMEOUT", "300"))
+        finished = threading.Event()
+        partial = {}
+
+        def watchdog():
+            if not finished.wait(limit):
+                emit(dict(partial, timeout=f"secondary lines unfinished after {limit:.0f} s"))
+                os._exit(0)
+
+        threading.Thread(target=watchdog, daemon=True).start()
+        secondary = partial
+        import bench_secondary as S
+        comm = nat.Comm.from_torch_distributed() if world > 1 else None
+        try:
+            secondary["C2"] = S.run_c2(nat, torch, rank, world, comm, min(args.steps, 5), barrier, allreduce_max_sum)
+        except Exception as ex:  # reported, not fatal: the headline is C4
+            secondary["C2"] = {"error": repr(ex)}
+        try:
+            secondary["C3"] = S.run_c3(nat, torch, rank, world, min(args.steps, 5), barrier, allreduce_max_sum)
+        except Exception as ex:
+            secondary["C3"] = {"error": repr(ex)}
+        try:
+            pk = os.path.join(ROOT, "MEASURED_PEAKS.json")
+            secondary["NEXT4"] = S.run_nf(nat, torch, max(args.steps, 5),
+                                          peaks=json.load(open(pk)) if os.path.exists(pk) else None)
+        except Exception as ex:
+            secondary["NEXT4"] = {"error": repr(ex)}
+        finished.set()
+    emit(secondary)
     if world > 1:
         dist.destroy_process_group()
 
