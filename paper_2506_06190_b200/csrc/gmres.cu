@@ -788,7 +788,13 @@ nat_status gmres_batched(int nsys, int64_t n, int64_t ldv, const double2* b, dou
     const char* e = std::getenv("NAT_FUSED_SMEM_KB");
     return e ? (size_t)std::atoi(e) * 1024 : (size_t)kFusedSmem;
   }();
-  const int fused_kg = fused_rt <= 2 ? 3 : 2;  // update groups (NTH / 256)
+  // 512 threads (2 update groups): leaves registers for pair-kernel CTAs of other streams on
+  // the same SM (C4 step -4 % with 4 worker streams); NAT_FUSED_NARROW=0: 768 threads for RT <= 2
+  static const bool fused_narrow = [] {
+    const char* e = std::getenv("NAT_FUSED_NARROW");
+    return !(e && e[0] == '0');
+  }();
+  const int fused_kg = (fused_rt <= 2 && !fused_narrow) ? 3 : 2;  // update groups (NTH / 256)
   const int fused_nth = fused_kg * kT;
   const size_t fsmem = std::max(fused_cap, sizeof(double2) * ((size_t)rpc * fused_kg + 4 * (size_t)mp1));
   using FusedFn = void (*)(const double2*, size_t, int64_t, int64_t, int64_t, const double2*, double2*, uint64_t,
@@ -797,8 +803,11 @@ nat_status gmres_batched(int nsys, int64_t n, int64_t ldv, const double2* b, dou
   if (fused_cl == 8)
     fused_fn = fused_rt == 1 ? arnoldi_fused_kernel<1, 768, 8> : fused_rt == 2 ? arnoldi_fused_kernel<2, 768, 8>
              : fused_rt == 4 ? arnoldi_fused_kernel<4, 512, 8> : arnoldi_fused_kernel<8, 512, 8>;
-  else
+  else if (fused_kg == 3)
     fused_fn = fused_rt == 1 ? arnoldi_fused_kernel<1, 768, 4> : fused_rt == 2 ? arnoldi_fused_kernel<2, 768, 4>
+             : fused_rt == 4 ? arnoldi_fused_kernel<4, 512, 4> : arnoldi_fused_kernel<8, 512, 4>;
+  else
+    fused_fn = fused_rt == 1 ? arnoldi_fused_kernel<1, 512, 4> : fused_rt == 2 ? arnoldi_fused_kernel<2, 512, 4>
              : fused_rt == 4 ? arnoldi_fused_kernel<4, 512, 4> : arnoldi_fused_kernel<8, 512, 4>;
   if (fused) {
     if (fsmem > (size_t)kBackSmemMax) return fail(NAT_ERR_INVALID_ARG, "max_iter %d too large", m);
