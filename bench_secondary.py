@@ -66,8 +66,8 @@ class Step:
         # workspace) or "asm_first" (all assemblies, then the solves: one matrix per ka);
         # the three ka run one after the other in the dense-BEM chain (one NCCL communicator,
         # collectives issued in the same order on every rank).  NAT_BENCH_ORDER overrides.
-        self.order = os.environ.get("NAT_BENCH_ORDER", "interleave")
-        n_mat = len(KAS) if self.order == "asm_first" else 1
+        self.order = os.environ.get("NAT_BENCH_ORDER", "multi")
+        n_mat = len(KAS) if self.order in ("asm_first", "multi") else 1
         mats = [torch.empty(rows, self.lda, dtype=torch.complex64, device=dev) for _ in range(n_mat)]
         wss = [nat._ws(nat.lib().nat_bem_solve_workspace(nat.NAT_FP32, self.n, rows, 200), dev) for _ in range(n_mat)]
         self.A = [mats[q % n_mat] for q in range(len(KAS))]
@@ -148,6 +148,25 @@ class Step:
         asm_ev = torch.cuda.Event()
 
         def bem_all(side=None):
+            if self.order == "multi":
+                # one far pass forms the three matrices (nat_bem_assemble_multi), then the solves
+                self._ev("asm0", "m")
+                nat.nat_bem_assemble_multi(self.mesh, geo, near, list(KAS), self.g, prec="fp32", A=self.A, lda=self.lda,
+                                           rhs=self.b_bem)
+                self._ev("asm1", "m")
+                rows = self.r1 - self.r0
+                with self.lock:
+                    counts["far"] += rows * self.n * 3 * len(KAS)
+                    counts["near"] += (self.nS * 448 + (near.nnz - self.nS) * 28) * len(KAS)
+                    counts["self"] += rows * 48 * len(KAS)
+                asm_ev.record(torch.cuda.current_stream())
+                asm_done.set()
+                for q in range(len(KAS)):
+                    self._bem_one(q, geo, near, counts, assemble=False)
+                    for grp in self.rad_groups:
+                        if grp[-1] == q:
+                            self._bem_radiate(geo, lis, grp, side)
+                return
             if self.order == "asm_first":
                 # all assemblies first (FP32/MUFU-bound), then the HBM-bound GMRES solves,
                 # which the MC chain's FP32/MUFU-bound operators overlap
@@ -168,7 +187,7 @@ class Step:
                         self._bem_radiate(geo, lis, grp, side)
 
         def mc_after_asm(*a):
-            if self.order == "asm_first":
+            if self.order in ("asm_first", "multi"):
                 asm_done.wait()
                 torch.cuda.current_stream().wait_event(asm_ev)
             self._mc_chain(*a)

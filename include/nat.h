@@ -164,6 +164,19 @@ nat_status nat_bem_assemble(const nat_mesh* mesh, const nat_geom* geom, const na
                             int64_t row_end, int n_rhs, const void* g, void* A, int64_t lda,
                             void* rhs, void* ws, size_t ws_bytes, nat_stream_t stream); /* (async) */
 
+/* a4 + a5 for n_k wavenumbers on the same mesh and rows in one call (round 2): A[q] (host
+ * array of n_k device matrices, [rows][lda] each) and rhs c128 [n_k][n_rhs][rows] are those
+ * nat_bem_assemble writes for k[q].  NAT_FP32 collocation of the conventional BIE with
+ * n_rhs <= 1 runs ONE far pass for all wavenumbers (shared geometry, rsqrt and d.n per
+ * quadrature point; per wavenumber kr, sincos, the V / K sums and the store); other variants
+ * loop over the wavenumbers.  1 <= n_k <= 4.  Workspace nat_bem_assemble_multi_workspace.  (async) */
+size_t nat_bem_assemble_multi_workspace(int64_t n_tri, int64_t rows, int64_t nnz, int n_rhs, int n_k);
+nat_status nat_bem_assemble_multi(const nat_mesh* mesh, const nat_geom* geom, const nat_quad_opts* opts,
+                                  const int64_t* near_row_ptr, const int32_t* near_col, const uint8_t* near_cls,
+                                  int64_t nnz, int n_k, const double* k /* [host] */, nat_prec prec, int64_t row_begin,
+                                  int64_t row_end, int n_rhs, const void* g, void* const* A /* [host][n_k] */,
+                                  int64_t lda, void* rhs, void* ws, size_t ws_bytes, nat_stream_t stream);
+
 /* a6 — y = A x, A [rows][lda] in `prec`, x c128 [n], y c128 [rows]; fp64 accumulation
  * in a fixed per-row order (independent of the number of GPUs).                       */
 nat_status nat_bem_matvec(nat_prec prec, int64_t rows, int64_t n, const void* A, int64_t lda,

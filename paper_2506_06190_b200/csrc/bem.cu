@@ -645,6 +645,163 @@ __global__ void __launch_bounds__(kThreads, kFarMinBlocks) far_kernel_x2(FarArgs
   }
 }
 
+// Multi-wavenumber far assembly (fp32, collocation, conventional BIE; round 2): one pass over
+// the pairs forms the far entries of NK matrices A_k = -K_k (k = the NK wavenumbers of the
+// call) and their right-hand-side sums V_k g, sharing per quadrature point the geometry
+// (d, r^2, rsqrt, r, d.n, the weights): per pair-evaluation x wavenumber 1/NK of the shared
+// work + kr, sincos and the V/K accumulation.  CTA = kTIM rows x 256 * kCC columns (the
+// column blocking of the one-wavenumber kernel, so the partial-sum layout is the same).
+constexpr int kTIM = 8;
+constexpr int kMaxK = 4;
+struct FarMultiArgs {
+  FarArgs<float> b;          // n, row_begin, rows, lda, cols, cen, centre, g (one RHS), rhs0 = 0
+  float k[kMaxK];
+  float2* A[kMaxK];          // c64 [rows][lda]
+  double2* bpart[kMaxK];     // [n_colblk][1][rows]
+};
+
+template <int NQ, int NK>
+__global__ void __launch_bounds__(kThreads, 2) far_kernel_multi(FarMultiArgs m) {
+  constexpr int TP = kTIM / 2;
+  const FarArgs<float>& a = m.b;
+  __shared__ __align__(16) f2r s_c[3][TP];
+  __shared__ double2 s_red[kThreads / 32][kTIM][NK];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t i0 = (int64_t)blockIdx.y * kTIM;
+  const int64_t n = a.n;
+  if (tid < TP) {
+    double c[2][3];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t r = i0 + 2 * tid + h;
+      const int64_t i = a.row_begin + (r < a.rows ? r : 0);
+      c[h][0] = a.cen[i] - a.cx;
+      c[h][1] = a.cen[n + i] - a.cy;
+      c[h][2] = a.cen[2 * n + i] - a.cz;
+    }
+#pragma unroll
+    for (int d = 0; d < 3; ++d) s_c[d][tid] = f2pack((float)c[0][d], (float)c[1][d]);
+  }
+  __syncthreads();
+  const int nrows = (int)nat::min64(kTIM, a.rows - i0);
+  f2r kk[NK], nkk[NK];
+#pragma unroll
+  for (int q = 0; q < NK; ++q) {
+    kk[q] = f2pack(m.k[q], m.k[q]);
+    nkk[q] = f2pack(-m.k[q], -m.k[q]);
+  }
+  const bool rhs = a.n_rhs > 0;
+  f2r br[TP][NK], bi[TP][NK];
+#pragma unroll
+  for (int t = 0; t < TP; ++t)
+#pragma unroll
+    for (int q = 0; q < NK; ++q) br[t][q] = bi[t][q] = 0ull;
+#pragma unroll 1
+  for (int cc = 0; cc < kCC; ++cc) {
+    const int64_t j = (int64_t)blockIdx.x * (kThreads * kCC) + cc * kThreads + tid;
+    const bool valid = j < n;
+    const int64_t jj = valid ? j : 0;
+    f2r y[NQ][3], w[NQ], yn[NQ];
+    const float nxs = a.cols.nrm[jj], nys = a.cols.nrm[n + jj], nzs = a.cols.nrm[2 * n + jj];
+    const f2r nx = f2pack(nxs, nxs), ny = f2pack(nys, nys), nz = f2pack(nzs, nzs);
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      float v[3];
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        v[d] = a.cols.qxyz[((size_t)q * 3 + d) * n + jj];
+        y[q][d] = f2pack(v[d], v[d]);
+      }
+      const float wv = valid ? a.cols.qw[(size_t)q * n + jj] : 0.f;
+      w[q] = f2pack(wv, wv);
+      const float vn = fmaf(v[2], nzs, fmaf(v[1], nys, v[0] * nxs));
+      yn[q] = f2pack(vn, vn);
+    }
+    f2r gr = 0ull, gi = 0ull, ngi = 0ull;
+    if (rhs) {
+      const double2 gv = valid ? a.g[jj] : make_double2(0.0, 0.0);
+      gr = f2pack((float)gv.x, (float)gv.x);
+      gi = f2pack((float)gv.y, (float)gv.y);
+      ngi = f2pack(-(float)gv.y, -(float)gv.y);
+    }
+#pragma unroll
+    for (int t = 0; t < TP; ++t) {
+      if (2 * t >= nrows) continue;
+      const f2r cx = s_c[0][t], cy = s_c[1][t], cz = s_c[2][t];
+      const f2r cn = f2fma(cz, nz, f2fma(cy, ny, f2mul(cx, nx)));
+      f2r Vr[NK], Vi[NK], Kr[NK], Ki[NK];  // K here is -K
+#pragma unroll
+      for (int q = 0; q < NK; ++q) Vr[q] = Vi[q] = Kr[q] = Ki[q] = 0ull;
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        const f2r dx = f2sub(y[q][0], cx), dy = f2sub(y[q][1], cy), dz = f2sub(y[q][2], cz);
+        const f2r r2 = f2fma(dz, dz, f2fma(dy, dy, f2mul(dx, dx)));
+        const f2r dn = f2sub(yn[q], cn);
+        const f2r rho = f2pack(nat::pair_rsqrt(f2lo(r2)), nat::pair_rsqrt(f2hi(r2)));
+        const f2r rr = f2mul(r2, rho);
+        const f2r tw = f2mul(w[q], rho);
+        const f2r u = f2mul(tw, f2mul(dn, f2mul(rho, rho)));
+#pragma unroll
+        for (int kw = 0; kw < NK; ++kw) {
+          const f2r kr = f2mul(rr, kk[kw]), nkr = f2mul(rr, nkk[kw]);
+          float s0, c0, s1, c1;
+          __sincosf(f2lo(kr), &s0, &c0);
+          __sincosf(f2hi(kr), &s1, &c1);
+          const f2r sn = f2pack(s0, s1), cs = f2pack(c0, c1);
+          Vr[kw] = f2fma(tw, cs, Vr[kw]);
+          Vi[kw] = f2fma(tw, sn, Vi[kw]);
+          Kr[kw] = f2fma(u, f2fma(kr, sn, cs), Kr[kw]);
+          Ki[kw] = f2fma(u, f2fma(nkr, cs, sn), Ki[kw]);
+        }
+      }
+      const int64_t ri = a.row_begin + i0 + 2 * t;
+      const bool z0 = !valid || (kCentroidRule<NQ> && j == ri), z1 = !valid || (kCentroidRule<NQ> && j == ri + 1);
+#pragma unroll
+      for (int kw = 0; kw < NK; ++kw) {
+        if (z0 || z1) {  // padding columns (and the centroid rules' self pair) -> 0, NaN-safe
+          Vr[kw] = f2pack(z0 ? 0.f : f2lo(Vr[kw]), z1 ? 0.f : f2hi(Vr[kw]));
+          Vi[kw] = f2pack(z0 ? 0.f : f2lo(Vi[kw]), z1 ? 0.f : f2hi(Vi[kw]));
+          Kr[kw] = f2pack(z0 ? 0.f : f2lo(Kr[kw]), z1 ? 0.f : f2hi(Kr[kw]));
+          Ki[kw] = f2pack(z0 ? 0.f : f2lo(Ki[kw]), z1 ? 0.f : f2hi(Ki[kw]));
+        }
+        if (valid) {
+          float2* arow = m.A[kw] + (size_t)(i0 + 2 * t) * a.lda + j;
+          arow[0] = make_float2(f2lo(Kr[kw]), f2lo(Ki[kw]));
+          if (2 * t + 1 < nrows) arow[a.lda] = make_float2(f2hi(Kr[kw]), f2hi(Ki[kw]));
+        }
+        br[t][kw] = f2fma(Vr[kw], gr, f2fma(Vi[kw], ngi, br[t][kw]));
+        bi[t][kw] = f2fma(Vr[kw], gi, f2fma(Vi[kw], gr, bi[t][kw]));
+      }
+    }
+  }
+  if (!rhs) return;
+#pragma unroll
+  for (int t = 0; t < kTIM; ++t)
+#pragma unroll
+    for (int kw = 0; kw < NK; ++kw) {
+      const f2r pr = br[t / 2][kw], pi = bi[t / 2][kw];
+      double vx = (double)((t & 1) ? f2hi(pr) : f2lo(pr)), vy = (double)((t & 1) ? f2hi(pi) : f2lo(pi));
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        vx += __shfl_xor_sync(0xffffffffu, vx, o);
+        vy += __shfl_xor_sync(0xffffffffu, vy, o);
+      }
+      if (lane == 0) s_red[warp][t][kw] = make_double2(vx, vy);
+    }
+  __syncthreads();
+  if (tid < kTIM * NK) {
+    const int t = tid / NK, kw = tid % NK;
+    if (t < nrows) {
+      double2 sum = s_red[0][t][kw];
+      for (int wv = 1; wv < kThreads / 32; ++wv) {
+        sum.x += s_red[wv][t][kw].x;
+        sum.y += s_red[wv][t][kw].y;
+      }
+      m.bpart[kw][(size_t)blockIdx.x * a.rows + i0 + t] = make_double2(-sum.x, -sum.y);  // b = -V g
+    }
+  }
+}
+
 template <typename R, int NQ, int NR>
 void launch_far(dim3 grid, const FarArgs<R>& fa, bool bm, bool gal, cudaStream_t s) {
   if (bm) {
@@ -1728,14 +1885,16 @@ nat_status assemble_impl(const nat_mesh* mesh, const nat_geom* geom, const Opts&
                          int64_t row_begin, int64_t rows, int n_rhs, const double2* g, void* A,
                          int64_t lda, double2* rhs, AsmWs& w, const std::vector<Pt>& pS,
                          const std::vector<Pt>& pN, cudaStream_t s, MfOut mf = MfOut{},
-                         const SSTable* ss_tab = nullptr) {
+                         const SSTable* ss_tab = nullptr, bool far_done = false) {
   const int64_t n = mesh->n_tri;
   const double cx = geom->center[0], cy = geom->center[1], cz = geom->center[2];
   FarCols<R> cols{(const R*)w.qxyz, (const R*)w.qw, (const R*)w.qn};
+  if (!far_done) {
   far_prep_kernel<R><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(
       mesh->n_vert, n, mesh->vxyz, mesh->tri, geom->normal, geom->area, w.rule_far, NQ, cx, cy, cz,
       (R*)w.qxyz, (R*)w.qw, (R*)w.qn);
   NAT_LAUNCH_CHECK();
+  }
   // a4: far rule on every pair, RHS partial sums
   FarArgs<R> fa{};
   fa.n = n;
@@ -1760,7 +1919,8 @@ nat_status assemble_impl(const nat_mesh* mesh, const nat_geom* geom, const Opts&
   fa.rule = w.rule_far;
   const int64_t n_colblk = (n + kThreads * kCC - 1) / (kThreads * kCC);
   dim3 grid((unsigned)n_colblk, (unsigned)((rows + kTI - 1) / kTI));
-  const bool timed = nat::ktimer_on() && !mf.delta;
+  const bool timed = nat::ktimer_on() && !mf.delta && !far_done;
+  if (!far_done) {
   if (timed) nat::ktimer_begin(nat::kTimerFar, s);
   if (n_rhs == 0) {
     fa.store_A = true;
@@ -1777,7 +1937,8 @@ nat_status assemble_impl(const nat_mesh* mesh, const nat_geom* geom, const Opts&
   }
   NAT_LAUNCH_CHECK();
   if (timed)  // far rule on every pair of the row block (test points x trial points)
-    nat::ktimer_end(nat::kTimerFar, s, (double)rows * (double)n * NQ * (o.gal ? NQ : 1), nullptr);
+    nat::ktimer_end(nat::kTimerFar, s, (double)rows * (double)n * NQ * (o.gal ? NQ : 1), nullptr, 1);
+  }  // far_done: the multi-wavenumber pass formed the far entries and bpart
   if (o.gal) {  // NEXT-2: Galerkin near / self integrals (warp per pair)
     GalArgs<R> ga{};
     ga.n = n;
@@ -1915,11 +2076,73 @@ extern "C" size_t nat_bem_assemble_workspace(int64_t n_tri, int64_t rows, int64_
 
 namespace {
 // nat_bem_assemble and nat_bem_mf_prepare (mf.delta set: no A, corrections instead)
+// Several wavenumbers in one call (nat_bem_assemble_multi): A[q], rhs + q n_rhs rows
+struct MultiK {
+  int n_k = 1;
+  const double* k = nullptr;  // [host][n_k]
+  void* const* A = nullptr;   // [host][n_k]
+};
+
+template <int NQ>
+nat_status assemble_multi_fp32(const nat_mesh* mesh, const nat_geom* geom, const Opts& o, const int64_t* rp,
+                               const int32_t* col, const uint8_t* cls, int64_t nnz, const MultiK& mk,
+                               int64_t row_begin, int64_t rows, int n_rhs, const double2* g, int64_t lda,
+                               double2* rhs, AsmWs& w, double2* extra_bpart, const std::vector<Pt>& pS,
+                               const std::vector<Pt>& pN, cudaStream_t s) {
+  const int64_t n = mesh->n_tri;
+  const double cx = geom->center[0], cy = geom->center[1], cz = geom->center[2];
+  far_prep_kernel<float><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(
+      mesh->n_vert, n, mesh->vxyz, mesh->tri, geom->normal, geom->area, w.rule_far, NQ, cx, cy, cz,
+      (float*)w.qxyz, (float*)w.qw, (float*)w.qn);
+  NAT_LAUNCH_CHECK();
+  const int64_t n_colblk = (n + kThreads * kCC - 1) / (kThreads * kCC);
+  const size_t bp = (size_t)n_colblk * (n_rhs > 0 ? n_rhs : 1) * rows;
+  FarMultiArgs m{};
+  FarArgs<float>& fa = m.b;
+  fa.n = n;
+  fa.row_begin = row_begin;
+  fa.rows = rows;
+  fa.lda = lda;
+  fa.cols = FarCols<float>{(const float*)w.qxyz, (const float*)w.qw, (const float*)w.qn};
+  fa.cen = geom->centroid;
+  fa.cx = cx;
+  fa.cy = cy;
+  fa.cz = cz;
+  fa.n_rhs = n_rhs;
+  fa.g = g;
+  for (int q = 0; q < mk.n_k; ++q) {
+    m.k[q] = (float)mk.k[q];
+    m.A[q] = (float2*)mk.A[q];
+    m.bpart[q] = q == 0 ? w.bpart : extra_bpart + (size_t)(q - 1) * bp;
+  }
+  const dim3 grid((unsigned)n_colblk, (unsigned)((rows + kTIM - 1) / kTIM));
+  const bool timed = nat::ktimer_on();
+  if (timed) nat::ktimer_begin(nat::kTimerFar, s);
+  switch (mk.n_k) {
+    case 2: far_kernel_multi<NQ, 2><<<grid, kThreads, 0, s>>>(m); break;
+    case 3: far_kernel_multi<NQ, 3><<<grid, kThreads, 0, s>>>(m); break;
+    default: far_kernel_multi<NQ, 4><<<grid, kThreads, 0, s>>>(m); break;
+  }
+  NAT_LAUNCH_CHECK();
+  if (timed) nat::ktimer_end(nat::kTimerFar, s, (double)rows * (double)n * NQ * mk.n_k, nullptr, mk.n_k);
+  // near / self corrections and the right-hand side, one wavenumber at a time
+  for (int q = 0; q < mk.n_k; ++q) {
+    AsmWs wq = w;
+    wq.bpart = m.bpart[q];
+    nat_status st = assemble_impl<float, NQ>(mesh, geom, o, rp, col, cls, nnz, mk.k[q], row_begin, rows, n_rhs, g,
+                                             mk.A[q], lda, rhs ? rhs + (size_t)q * n_rhs * rows : nullptr, wq, pS,
+                                             pN, s, MfOut{}, nullptr, true);
+    if (st != NAT_OK) return st;
+  }
+  return NAT_OK;
+}
+
 nat_status assemble_entry(const nat_mesh* mesh, const nat_geom* geom, const nat_quad_opts* opts,
                           const int64_t* near_row_ptr, const int32_t* near_col, const uint8_t* near_cls, int64_t nnz,
                           double k,
                           nat_prec prec, int64_t row_begin, int64_t row_end, int n_rhs, const void* g, void* A,
-                          int64_t lda, void* rhs, void* ws, size_t ws_bytes, nat_stream_t stream, MfOut mf) {
+                          int64_t lda, void* rhs, void* ws, size_t ws_bytes, nat_stream_t stream, MfOut mf,
+                          const MultiK* mk = nullptr) {
   NAT_REQUIRE(mesh && geom, "mesh and geom must be non-null");
   NAT_REQUIRE(prec == NAT_FP32 || prec == NAT_FP64, "bad precision %d", (int)prec);
   const int64_t n = mesh->n_tri;
@@ -1927,6 +2150,12 @@ nat_status assemble_entry(const nat_mesh* mesh, const nat_geom* geom, const nat_
   NAT_REQUIRE(0 <= row_begin && row_begin < row_end && row_end <= n, "bad row range");
   NAT_REQUIRE(mf.delta || lda >= n, "lda (%lld) < n_tri (%lld)", (long long)lda, (long long)n);
   NAT_REQUIRE(k >= 0.0 && k < 1e300, "k = %g must be finite and >= 0", k);
+  if (mk)
+    for (int q = 0; q < mk->n_k; ++q) {
+      NAT_REQUIRE(mk->k[q] >= 0.0 && mk->k[q] < 1e300, "k[%d] = %g must be finite and >= 0", q, mk->k[q]);
+      NAT_REQUIRE(!(opts && opts->burton_miller) || mk->k[q] > 0.0, "Burton-Miller needs k > 0 (beta = i/k)");
+      NAT_REQUIRE_DEV(mk->A[q]);
+    }
   NAT_REQUIRE(!(opts && opts->burton_miller) || k > 0.0, "Burton-Miller needs k > 0 (beta = i/k)");
   NAT_REQUIRE(n_rhs >= 0 && (n_rhs == 0) == (g == nullptr), "g must be NULL iff n_rhs == 0");
   Opts o = opts_of(opts);
@@ -1976,6 +2205,12 @@ nat_status assemble_entry(const nat_mesh* mesh, const nat_geom* geom, const nat_
   AsmWs w;
   size_t rsz = prec == NAT_FP32 ? sizeof(float) : sizeof(double);
   size_t need = carve(c, w, n, rows, nnz, n_rhs, kMaxFarQ, (int)pS.size(), (int)pN.size(), o.gl, rsz);
+  double2* extra_bpart = nullptr;
+  if (mk && mk->n_k > 1) {  // one more RHS partial-sum block per extra wavenumber
+    const int64_t n_colblk = (n + kThreads * kCC - 1) / (kThreads * kCC);
+    extra_bpart = c.take<double2>((size_t)(mk->n_k - 1) * n_colblk * (n_rhs > 0 ? n_rhs : 1) * rows);
+    need = c.bytes();
+  }
   if (ws_bytes < need) return nat::fail(NAT_ERR_WORKSPACE, "workspace %zu < %zu", ws_bytes, need);
   NAT_REQUIRE_DEV(ws);
   // rule tables -> workspace: one asynchronous copy from an immutable pinned blob built
@@ -2058,6 +2293,29 @@ nat_status assemble_entry(const nat_mesh* mesh, const nat_geom* geom, const nat_
   }
   const double2* gg = (const double2*)g;
   double2* bb = (double2*)rhs;
+  if (mk && mk->n_k > 1) {
+    const bool fused = prec == NAT_FP32 && !o.bm && !o.gal && n_rhs <= 1;
+    if (fused) {
+#define NAT_MULTI(NQ) \
+  assemble_multi_fp32<NQ>(mesh, geom, o, near_row_ptr, near_col, near_cls, nnz, *mk, row_begin, rows, n_rhs, gg, lda, \
+                          bb, w, extra_bpart, pS, pN, s)
+      switch (o.far_pts) {
+        case 1: return NAT_MULTI(1);
+        case 3: return NAT_MULTI(3);
+        case 6: return NAT_MULTI(6);
+        default: return NAT_MULTI(7);
+      }
+#undef NAT_MULTI
+    }
+    // other variants: one far pass per wavenumber
+    for (int q = 0; q < mk->n_k; ++q) {
+      nat_status st = assemble_entry(mesh, geom, opts, near_row_ptr, near_col, near_cls, nnz, mk->k[q], prec,
+                                     row_begin, row_end, n_rhs, g, mk->A[q], lda,
+                                     bb ? (void*)(bb + (size_t)q * n_rhs * rows) : nullptr, ws, ws_bytes, stream, mf);
+      if (st != NAT_OK) return st;
+    }
+    return NAT_OK;
+  }
 #define NAT_ASM(R, NQ)                                                                         \
   assemble_impl<R, NQ>(mesh, geom, o, near_row_ptr, near_col, near_cls, nnz, k, row_begin, rows, \
                        n_rhs, gg, A, lda, bb, w, pS, pN, s, mf, &tab)
@@ -2089,6 +2347,29 @@ extern "C" nat_status nat_bem_assemble(const nat_mesh* mesh, const nat_geom* geo
   NAT_TRACE();
   return assemble_entry(mesh, geom, opts, near_row_ptr, near_col, near_cls, nnz, k, prec, row_begin, row_end, n_rhs,
                         g, A, lda, rhs, ws, ws_bytes, stream, MfOut{});
+}
+
+extern "C" size_t nat_bem_assemble_multi_workspace(int64_t n_tri, int64_t rows, int64_t nnz, int n_rhs, int n_k) {
+  const size_t a = nat_bem_assemble_workspace(n_tri, rows, nnz, n_rhs);
+  if (n_k <= 1) return a;
+  const int64_t n_colblk = (n_tri + kThreads * kCC - 1) / (kThreads * kCC);
+  return a + nat::align_up(sizeof(double2) * (size_t)(n_k - 1) * n_colblk * (n_rhs > 0 ? n_rhs : 1) * rows, 256) + 256;
+}
+
+extern "C" nat_status nat_bem_assemble_multi(const nat_mesh* mesh, const nat_geom* geom, const nat_quad_opts* opts,
+                                             const int64_t* near_row_ptr, const int32_t* near_col,
+                                             const uint8_t* near_cls, int64_t nnz, int n_k, const double* k,
+                                             nat_prec prec, int64_t row_begin, int64_t row_end, int n_rhs,
+                                             const void* g, void* const* A, int64_t lda, void* rhs, void* ws,
+                                             size_t ws_bytes, nat_stream_t stream) {
+  NAT_TRACE();
+  NAT_REQUIRE(n_k >= 1 && n_k <= kMaxK && k && A, "need 1 <= n_k <= %d and host arrays k[n_k], A[n_k]", kMaxK);
+  MultiK mk;
+  mk.n_k = n_k;
+  mk.k = k;
+  mk.A = A;
+  return assemble_entry(mesh, geom, opts, near_row_ptr, near_col, near_cls, nnz, k[0], prec, row_begin, row_end, n_rhs,
+                        g, A[0], lda, rhs, ws, ws_bytes, stream, MfOut{}, &mk);
 }
 
 namespace {

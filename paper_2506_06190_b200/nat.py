@@ -93,6 +93,10 @@ _SIGS = {
     "nat_bem_assemble": (C.c_int, [C.POINTER(_Mesh), C.POINTER(_Geom), C.POINTER(_QuadOpts),
                                    _P, _P, _P, _I64, _D, C.c_int, _I64, _I64, C.c_int, _P, _P, _I64,
                                    _P, _P, _SZ, _P]),
+    "nat_bem_assemble_multi_workspace": (_SZ, [_I64, _I64, _I64, C.c_int, C.c_int]),
+    "nat_bem_assemble_multi": (C.c_int, [C.POINTER(_Mesh), C.POINTER(_Geom), C.POINTER(_QuadOpts),
+                                         _P, _P, _P, _I64, C.c_int, C.POINTER(_D), C.c_int, _I64, _I64, C.c_int,
+                                         _P, C.POINTER(_P), _I64, _P, _P, _SZ, _P]),
     "nat_bem_matvec": (C.c_int, [C.c_int, _I64, _I64, _P, _I64, _P, _P, _P]),
     "nat_bem_mf_workspace": (_SZ, [C.POINTER(_BemMf), _I64, C.c_int]),
     "nat_bem_mf_prepare": (C.c_int, [C.POINTER(_BemMf), C.c_int, _P, _P, _P, _SZ, _P]),
@@ -430,6 +434,41 @@ def nat_bem_assemble(mesh: Mesh, geom: Geom, near: NearList, k: float, g=None, p
                                   C.c_void_p(near.col.data_ptr()), C.c_void_p(near.cls.data_ptr()),
                                   int(near.nnz), float(k), pr, near.row_begin, near.row_end, n_rhs, _ptr(g), _ptr(A),
                                   lda, _ptr(rhs), _ptr(ws), ws.numel(), _stream()))
+    return A, rhs
+
+
+def nat_bem_assemble_multi(mesh: Mesh, geom: Geom, near: NearList, ks, g=None, prec="fp32", opts=None,
+                           A=None, lda: Optional[int] = None, rhs: Optional[torch.Tensor] = None, ws=None):
+    """a4 + a5 for several wavenumbers in one call (one far pass for all of them on the fp32
+    collocation path).  Returns (list of A, rhs c128 [n_k][n_rhs][rows] or None)."""
+    pr = _prec(prec)
+    dev = mesh.vxyz.device
+    n = mesh.n_tri
+    rows = near.row_end - near.row_begin
+    lda = lda or (n + (n & 1))
+    ks, kp = _karr(ks)
+    nk = ks.size
+    cdt = torch.complex64 if pr == NAT_FP32 else torch.complex128
+    if A is None:
+        A = [torch.empty(rows, lda, dtype=cdt, device=dev) for _ in range(nk)]
+    n_rhs = 0
+    if g is not None:
+        g = torch.atleast_2d(g).to(torch.complex128).contiguous()
+        n_rhs = g.shape[0]
+        if rhs is None:
+            rhs = torch.empty(nk, n_rhs, rows, dtype=torch.complex128, device=dev)
+    else:
+        rhs = None
+    o = opts or quad_opts()
+    if ws is None:
+        ws = _ws(lib().nat_bem_assemble_multi_workspace(n, rows, near.nnz, n_rhs, nk), dev)
+    ptrs = (C.c_void_p * nk)(*[a.data_ptr() for a in A])
+    for a in A:
+        _ptr(a)
+    _check(lib().nat_bem_assemble_multi(C.byref(mesh.c()), C.byref(geom.c()), C.byref(o), _ptr(near.row_ptr),
+                                        C.c_void_p(near.col.data_ptr()), C.c_void_p(near.cls.data_ptr()),
+                                        int(near.nnz), nk, kp, pr, near.row_begin, near.row_end, n_rhs, _ptr(g),
+                                        ptrs, lda, _ptr(rhs), _ptr(ws), ws.numel(), _stream()))
     return A, rhs
 
 

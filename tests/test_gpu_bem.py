@@ -238,3 +238,22 @@ def test_assembly_other_far_rules(prec, far_pts):
     y = to_np(nat.nat_bem_mf_matvec(op, torch.from_numpy(x).cuda()))
     assert np.all(np.isfinite(y)) and rel_l2(y, A_ref @ x) <= TOL[prec]
     assert rel_l2(to_np(rhs)[0], b_ref[0]) <= TOL[prec]
+
+
+@pytest.mark.parametrize("prec,n_rhs,far_pts", [("fp32", 1, 3), ("fp32", 0, 7), ("fp32", 2, 3), ("fp64", 1, 3)])
+def test_assemble_multi_equals_single_calls(prec, n_rhs, far_pts):
+    """nat_bem_assemble_multi (one far pass for several wavenumbers on the fp32 collocation
+    path, a loop elsewhere) writes exactly what separate nat_bem_assemble calls write."""
+    nat = _nat()
+    m, geo, near = _oracle_case("bowl")
+    mesh, gg = _gpu_case(m)
+    o = nat.quad_opts(far_pts=far_pts)
+    nl = nat.nat_bem_near_list(mesh, gg, 37, m.n_tri - 11, opts=o)     # a ragged row block
+    ks = [0.5, 2.0, 8.0]
+    g = torch.from_numpy(np.stack([I.neumann_rigid_z(m), I.random_complex(m.n_tri, 5)])[:n_rhs]).cuda() if n_rhs else None
+    As, rhs = nat.nat_bem_assemble_multi(mesh, gg, nl, ks, g, prec=prec, opts=o)
+    for q, k in enumerate(ks):
+        A1, b1 = nat.nat_bem_assemble(mesh, gg, nl, k, g, prec=prec, opts=o)
+        assert torch.equal(As[q], A1), (q, k)
+        if n_rhs:
+            assert torch.equal(rhs[q], b1), (q, k)
