@@ -461,11 +461,6 @@ __global__ void combine_kernel(const double2* __restrict__ V, const double2* __r
 constexpr int kFusedMaxRT = 8;                 // rows per thread (n <= CL x 256 x 8)
 constexpr int kFusedSmem = 120 * 1024;         // residency cap (1 CTA / SM)
 
-__global__ void publish_mask_kernel(const unsigned long long* __restrict__ mask, volatile unsigned long long* out) {
-  *out = *mask;
-  __threadfence_system();
-}
-
 // Threads: NTH = KG x 256.  Dots: NTH / 32 warps, each two basis vectors at a time (16
 // loads of 16 B in flight per lane).  Update: group g (256 threads, RT rows each) sums the
 // basis vectors k = g, g + KG, ... in ascending order; group 0 adds the KG partial sums in
@@ -654,13 +649,253 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NTH, 1)
   cl.sync();  // no CTA exits while another may still read its shared memory
 }
 
+// Fused Arnoldi step over a basis stored as TB (double2, or float2: the fp32 solves,
+// reading R-basis32 of DESIGN.md — the basis vectors are rounded to fp32 once when they
+// are formed, and the operator, the dots, the updates and x = V y all use those rounded
+// vectors, held exactly in fp64 in V and in fp32 in Vb; every product and sum is fp64).
+// Same CTA / cluster structure and summation orders as arnoldi_fused_kernel; the loops
+// keep more loads in flight per round trip: dots take UD rows per lane of two vectors at
+// once (a CTA's whole 512-row slice in one round for float2), updates load U basis
+// entries for each of the RT rows of a thread together.
+template <typename TB>
+__device__ __forceinline__ double2 to_d2(TB v) {
+  return make_double2((double)v.x, (double)v.y);
+}
+template <typename TB>
+__device__ __forceinline__ TB zero_tb() {
+  TB v;
+  v.x = 0;
+  v.y = 0;
+  return v;
+}
+
+template <typename TB, int RT, int NTH, int CL>
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NTH, 1)
+    arnoldi_fused_v2_kernel(const TB* __restrict__ Vb, size_t vstride, int64_t ldv, int64_t n, int64_t rpc,
+                            const double2* __restrict__ Wj, double2* Vnext, TB* Vbnext,
+                            uint64_t active, GivensArgs ga) {
+  namespace cg = cooperative_groups;
+  constexpr int KG = NTH / kT, NW = NTH / 32;
+  constexpr int UD = sizeof(TB) == 8 ? 16 : 8;   // rows per lane per dot round
+  constexpr int U0 = 16 / RT;
+  constexpr int U = U0 > 0 ? U0 : 1;             // basis vectors per update round (x RT rows)
+  extern __shared__ __align__(16) double2 fsm[];
+  __shared__ double red[kT / 32];
+  __shared__ double nrm_part, nrm_all;
+  cg::cluster_group cl = cg::this_cluster();
+  const int s = blockIdx.y;
+  const int c = (int)cl.block_rank();
+  const int j = ga.j, mp1 = ga.mp1, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int grp = tid / kT, tr = tid % kT;
+  if (!sys_on(active, ga.mask, s)) return;
+  double2* wsh = fsm;
+  double2* hp = fsm + rpc;         // [2][mp1]
+  double2* hs = hp + 2 * mp1;      // [mp1]
+  double2* hc1 = hs + mp1;         // [mp1]
+  double2* upd = hc1 + mp1;        // [KG-1][rpc]
+  const int64_t r0 = (int64_t)c * rpc;
+  const int rows = (int)max((int64_t)0, min(rpc, n - r0));
+  const TB* Vs = Vb + (size_t)s * ldv + r0;
+  double2 w[RT];
+  if (grp == 0) {
+#pragma unroll
+    for (int q = 0; q < RT; ++q) {
+      const int r = tr + q * kT;
+      w[q] = r < rows ? Wj[(size_t)s * ldv + r0 + r] : make_double2(0.0, 0.0);
+      if (r < rows) wsh[r] = w[q];
+    }
+  }
+  __syncthreads();
+  for (int pass = 0; pass < 2; ++pass) {
+    double2* part = hp + pass * mp1;
+    for (int k = warp; k <= j; k += 2 * NW) {
+      const int k2 = k + NW;
+      const TB* vk = Vs + (size_t)k * vstride;
+      const TB* vk2 = Vs + (size_t)(k2 <= j ? k2 : k) * vstride;
+      double ax = 0.0, ay = 0.0, bx = 0.0, by = 0.0;
+      for (int r0l = 0; r0l < rows; r0l += 32 * UD) {
+        TB v[UD], v2[UD];  // raw basis entries in flight, widened at use
+#pragma unroll
+        for (int q = 0; q < UD; ++q) {
+          const int r = r0l + q * 32 + lane;
+          v[q] = r < rows ? __ldcg(&vk[r]) : zero_tb<TB>();
+          v2[q] = r < rows ? __ldcg(&vk2[r]) : zero_tb<TB>();
+        }
+#pragma unroll
+        for (int q = 0; q < UD; ++q) {
+          const int r = r0l + q * 32 + lane;
+          const double2 u = r < rows ? wsh[r] : make_double2(0.0, 0.0);
+          const double2 a = to_d2(v[q]), b = to_d2(v2[q]);
+          ax += a.x * u.x + a.y * u.y;
+          ay += a.x * u.y - a.y * u.x;
+          bx += b.x * u.x + b.y * u.y;
+          by += b.x * u.y - b.y * u.x;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        ax += __shfl_xor_sync(0xffffffffu, ax, o);
+        ay += __shfl_xor_sync(0xffffffffu, ay, o);
+        bx += __shfl_xor_sync(0xffffffffu, bx, o);
+        by += __shfl_xor_sync(0xffffffffu, by, o);
+      }
+      if (lane == 0) {
+        part[k] = make_double2(ax, ay);
+        if (k2 <= j) part[k2] = make_double2(bx, by);
+      }
+    }
+    cl.sync();
+    double2* hc = pass == 0 ? hp + mp1 : hc1;
+    for (int k = tid; k <= j; k += NTH) {
+      double2 t = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int q = 0; q < CL; ++q) {
+        const double2 p = cl.map_shared_rank(part, q)[k];
+        t.x += p.x;
+        t.y += p.y;
+      }
+      hs[k] = pass == 0 ? t : make_double2(hs[k].x + t.x, hs[k].y + t.y);
+      hc[k] = t;
+    }
+    __syncthreads();
+    // w_i -= sum_k hc[k] V_k[i]: group g takes k = g, g + KG, ... (RT x U loads in flight)
+    double2 acc[RT];
+#pragma unroll
+    for (int q = 0; q < RT; ++q) acc[q] = make_double2(0.0, 0.0);
+    for (int k0 = grp; k0 <= j; k0 += U * KG) {
+      TB v[RT][U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int k = k0 + u * KG;
+#pragma unroll
+        for (int q = 0; q < RT; ++q) {
+          const int r = tr + q * kT;
+          v[q][u] = (k <= j && r < rows) ? __ldcg(&Vs[(size_t)k * vstride + r]) : zero_tb<TB>();
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int k = k0 + u * KG;
+        const double2 cc = k <= j ? hc[k] : make_double2(0.0, 0.0);
+#pragma unroll
+        for (int q = 0; q < RT; ++q) {
+          const double2 a = to_d2(v[q][u]);
+          acc[q].x += cc.x * a.x - cc.y * a.y;
+          acc[q].y += cc.x * a.y + cc.y * a.x;
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < RT; ++q) {
+      const int r = tr + q * kT;
+      if (r >= rows) continue;
+      if (grp > 0) upd[(size_t)(grp - 1) * rpc + r] = acc[q];
+      else w[q] = acc[q];
+    }
+    __syncthreads();
+    if (grp == 0) {
+#pragma unroll
+      for (int q = 0; q < RT; ++q) {
+        const int r = tr + q * kT;
+        if (r >= rows) continue;
+        double2 a = w[q];
+#pragma unroll
+        for (int g = 1; g < KG; ++g) {
+          const double2 u = upd[(size_t)(g - 1) * rpc + r];
+          a.x += u.x;
+          a.y += u.y;
+        }
+        const double2 wo = wsh[r];
+        w[q] = make_double2(wo.x - a.x, wo.y - a.y);
+      }
+    }
+    if (pass == 0) {
+      cl.sync();
+      if (grp == 0) {
+#pragma unroll
+        for (int q = 0; q < RT; ++q) {
+          const int r = tr + q * kT;
+          if (r < rows) wsh[r] = w[q];
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (grp == 0) {
+    double t = 0.0;
+#pragma unroll
+    for (int q = 0; q < RT; ++q) t += w[q].x * w[q].x + w[q].y * w[q].y;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (lane == 0) red[warp] = t;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double b = 0.0;
+    for (int q = 0; q < kT / 32; ++q) b += red[q];
+    nrm_part = b;
+  }
+  cl.sync();
+  if (tid == 0) {
+    double a = 0.0;
+    for (int q = 0; q < CL; ++q) a += *cl.map_shared_rank(&nrm_part, q);
+    nrm_all = sqrt(a);
+  }
+  __syncthreads();
+  const double nv = nrm_all;
+  if (grp == 0) {  // V_{j+1} = w / ||w|| (zero on breakdown), rounded to TB; V holds it exactly
+#pragma unroll
+    for (int q = 0; q < RT; ++q) {
+      const int r = tr + q * kT;
+      if (r >= rows) continue;
+      double2 v = nv > 0 ? make_double2(w[q].x / nv, w[q].y / nv) : make_double2(0.0, 0.0);
+      TB vb;
+      vb.x = v.x;
+      vb.y = v.y;
+      v = make_double2((double)vb.x, (double)vb.y);
+      Vnext[(size_t)s * ldv + r0 + r] = v;
+      if ((void*)Vbnext != (void*)Vnext) Vbnext[(size_t)s * ldv + r0 + r] = vb;
+    }
+  }
+  if (c == 0) {
+    double2* hq = const_cast<double2*>(ga.h) + (size_t)s * ga.mp2;
+    for (int k = tid; k <= j; k += NTH) hq[k] = hs[k];
+    if (tid == 0) hq[j + 1] = make_double2(nv, 0.0);
+  }
+  cl.sync();
+}
+
+// V_0 = b / beta rounded to fp32 (the fp32-basis solves): the fp32 copy and its exact fp64 value.
+__global__ void round_basis_kernel(double2* __restrict__ V, float2* __restrict__ Vf, int64_t ldv, int64_t n,
+                                   uint64_t active, const unsigned long long* __restrict__ dmask) {
+  const int s = blockIdx.y;
+  if (!sys_on(active, dmask, s)) return;
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double2 v = V[(size_t)s * ldv + i];
+  const float2 f = make_float2((float)v.x, (float)v.y);
+  Vf[(size_t)s * ldv + i] = f;
+  V[(size_t)s * ldv + i] = make_double2((double)f.x, (double)f.y);
+}
+
 // The Givens steps of every active system in parallel (one warp each), after the fused
 // Arnoldi step; the sequential rotation chain of one system no longer holds a cluster.
-__global__ void __launch_bounds__(32) givens_kernel(uint64_t active, GivensArgs ga) {
+__global__ void __launch_bounds__(32) givens_kernel(uint64_t active, GivensArgs ga, unsigned* done_cnt,
+                                                    volatile unsigned long long* publish) {
   extern __shared__ __align__(16) double2 gsm2[];
   const int s = blockIdx.x;
-  if (!sys_on(active, ga.mask, s)) return;
-  givens_block(ga, s, gsm2);
+  if (sys_on(active, ga.mask, s)) givens_block(ga, s, gsm2);
+  // the last block to finish publishes the convergence mask to the host ring
+  __syncwarp();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(done_cnt, 1u) == gridDim.x - 1) {
+      *done_cnt = 0u;
+      __threadfence();
+      *publish = *(volatile unsigned long long*)ga.mask;
+      __threadfence_system();
+    }
+  }
 }
 
 // Per-thread, per-device host resources: a pinned ring for the convergence mask and
@@ -722,6 +957,7 @@ size_t krylov_workspace(int nsys, int64_t n, int64_t ldv, int max_iter, Carver& 
   KrylovWs t;
   t.V = c.take<double2>((size_t)(m + 1) * nsys * ldv);
   t.W = c.take<double2>((size_t)(m > 0 ? m : 1) * nsys * ldv);
+  t.Vf = c.take<float2>((size_t)(m + 1) * nsys * ldv);
   t.w = c.take<double2>((size_t)nsys * ldv);
   t.part = c.take<double2>((size_t)nsys * (m + 1) * nchunk);
   t.h = c.take<double2>((size_t)nsys * (m + 2));
@@ -734,14 +970,14 @@ size_t krylov_workspace(int nsys, int64_t n, int64_t ldv, int max_iter, Carver& 
   t.gam = c.take<double2>((size_t)nsys * (m + 1));
   t.sys = c.take<DevSys>(nsys);
   t.mask = c.take<unsigned long long>(1);
-  t.cnt = c.take<unsigned>(2 * 64);
+  t.cnt = c.take<unsigned>(2 * 64 + 1);  // [128]: the Givens kernel's last-block counter
   if (w) *w = t;
   return c.bytes();
 }
 
 nat_status gmres_batched(int nsys, int64_t n, int64_t ldv, const double2* b, double2* x, const KrylovOp& op,
                          double tol, int max_iter, const KrylovWs& ws, std::vector<KrylovResult>& res,
-                         cudaStream_t s, double* t_op_s) {
+                         cudaStream_t s, double* t_op_s, bool basis32) {
   if (nsys < 1 || nsys > 64) return fail(NAT_ERR_INVALID_ARG, "batched GMRES supports 1..64 systems");
   const int m = max_iter, mp1 = m + 1, mp2 = m + 2;
   const int nchunk = (int)((n + kKrylovChunk - 1) / kKrylovChunk);
@@ -756,7 +992,7 @@ nat_status gmres_batched(int nsys, int64_t n, int64_t ldv, const double2* b, dou
   if (!hs) return fail(NAT_ERR_CUDA, "pinned host ring / events: %s", cudaGetErrorString(cudaGetLastError()));
   res.assign(nsys, KrylovResult{0, 1, 0.0});
 
-  NAT_CUDA_TRY(cudaMemsetAsync(ws.cnt, 0, sizeof(unsigned) * 2 * 64, s));
+  NAT_CUDA_TRY(cudaMemsetAsync(ws.cnt, 0, sizeof(unsigned) * (2 * 64 + 1), s));
   // dots of nvec basis vectors (or of w with itself) with w, reduced into h / h2
   auto dots = [&](const double2* Vb, size_t vs, const double2* w, int nvec, const unsigned long long* dm, int mode,
                   int slot) {
@@ -809,8 +1045,31 @@ nat_status gmres_batched(int nsys, int64_t n, int64_t ldv, const double2* b, dou
   else
     fused_fn = fused_rt == 1 ? arnoldi_fused_kernel<1, 512, 4> : fused_rt == 2 ? arnoldi_fused_kernel<2, 512, 4>
              : fused_rt == 4 ? arnoldi_fused_kernel<4, 512, 4> : arnoldi_fused_kernel<8, 512, 4>;
+  // fused v2 kernel: always for the fp32 basis; NAT_GMRES_V2 = 1 also for the fp64 basis
+  static const bool v2_env = [] {
+    const char* e = std::getenv("NAT_GMRES_V2");
+    return e && e[0] == '1';
+  }();
+  const bool b32 = basis32 && fused;
+  using FusedV2d = void (*)(const double2*, size_t, int64_t, int64_t, int64_t, const double2*, double2*, double2*,
+                            uint64_t, GivensArgs);
+  using FusedV2f = void (*)(const float2*, size_t, int64_t, int64_t, int64_t, const double2*, double2*, float2*,
+                            uint64_t, GivensArgs);
+  FusedV2d v2d = nullptr;
+  FusedV2f v2f = nullptr;
+  if (fused && fused_cl == 4 && fused_kg == 2) {
+    if (b32)
+      v2f = fused_rt == 1 ? arnoldi_fused_v2_kernel<float2, 1, 512, 4> : fused_rt == 2 ? arnoldi_fused_v2_kernel<float2, 2, 512, 4>
+          : fused_rt == 4 ? arnoldi_fused_v2_kernel<float2, 4, 512, 4> : arnoldi_fused_v2_kernel<float2, 8, 512, 4>;
+    else if (v2_env)
+      v2d = fused_rt == 1 ? arnoldi_fused_v2_kernel<double2, 1, 512, 4> : fused_rt == 2 ? arnoldi_fused_v2_kernel<double2, 2, 512, 4>
+          : fused_rt == 4 ? arnoldi_fused_v2_kernel<double2, 4, 512, 4> : arnoldi_fused_v2_kernel<double2, 8, 512, 4>;
+  }
+  const bool use_b32 = v2f != nullptr;
   if (fused) {
     if (fsmem > (size_t)kBackSmemMax) return fail(NAT_ERR_INVALID_ARG, "max_iter %d too large", m);
+    if (v2f) NAT_CUDA_TRY(cudaFuncSetAttribute((const void*)v2f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem));
+    if (v2d) NAT_CUDA_TRY(cudaFuncSetAttribute((const void*)v2d, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem));
     if (gsmem > 48 * 1024)
       NAT_CUDA_TRY(cudaFuncSetAttribute(givens_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsmem));
     NAT_CUDA_TRY(cudaFuncSetAttribute((const void*)fused_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem));
@@ -835,11 +1094,17 @@ nat_status gmres_batched(int nsys, int64_t n, int64_t ldv, const double2* b, dou
     if (fused) {  // short vectors: the whole CGS2 step in one cluster launch per iteration
       const dim3 grid(fused_cl, nsys);
       cudaError_t e = cudaSuccess;
-      fused_fn<<<grid, fused_nth, fsmem, s>>>(ws.V, vstride, ldv, n, rpc, Wj, ws.V + (size_t)(j + 1) * vstride, all, ga);
+      if (v2f)
+        v2f<<<grid, fused_nth, fsmem, s>>>(ws.Vf, vstride, ldv, n, rpc, Wj, ws.V + (size_t)(j + 1) * vstride,
+                                           ws.Vf + (size_t)(j + 1) * vstride, all, ga);
+      else if (v2d)
+        v2d<<<grid, fused_nth, fsmem, s>>>(ws.V, vstride, ldv, n, rpc, Wj, ws.V + (size_t)(j + 1) * vstride,
+                                           ws.V + (size_t)(j + 1) * vstride, all, ga);
+      else
+        fused_fn<<<grid, fused_nth, fsmem, s>>>(ws.V, vstride, ldv, n, rpc, Wj, ws.V + (size_t)(j + 1) * vstride, all, ga);
       e = cudaGetLastError();
       if (e != cudaSuccess) return fail(NAT_ERR_CUDA, "fused Arnoldi launch: %s", cudaGetErrorString(e));
-      givens_kernel<<<nsys, 32, gsmem, s>>>(all, ga);
-      publish_mask_kernel<<<1, 1, 0, s>>>(ws.mask, hs->ring_dev + j % kRing);
+      givens_kernel<<<nsys, 32, gsmem, s>>>(all, ga, ws.cnt + 128, hs->ring_dev + j % kRing);
       NAT_LAUNCH_CHECK();
     } else {
       for (int pass = 0; pass < 2; ++pass) {  // CGS2 (w = W_j minus its projections); pass 1 also forms ||w||
@@ -858,6 +1123,10 @@ nat_status gmres_batched(int nsys, int64_t n, int64_t ldv, const double2* b, dou
   };
   // Iteration j is enqueued with the mask read back after iteration j-2; the host then
   // waits for iteration j-1 while the GPU runs iteration j.
+  if (use_b32) {  // V_0 rounded to the fp32 basis (R-basis32)
+    round_basis_kernel<<<dim3(gx, nsys), kT, 0, s>>>(ws.V, ws.Vf, ldv, n, all, ws.mask);
+    NAT_LAUNCH_CHECK();
+  }
   if (m > 0) {
     nat_status stt = enqueue(0, all);
     if (stt != NAT_OK) return stt;

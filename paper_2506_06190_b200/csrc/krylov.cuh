@@ -23,6 +23,7 @@ constexpr int kSysNonFinite = 2;
 struct KrylovWs {
   double2* V;     // [(m+1)][nsys][ldv] Arnoldi basis
   double2* W;     // [m][nsys][ldv] operator products A V_j (final residual by linearity)
+  float2* Vf;     // [(m+1)][nsys][ldv] the basis in fp32 (fp32 solves, reading R-basis32)
   double2* w;     // [nsys][ldv]
   double2* part;  // [nsys][m+1][nchunk]
   double2* h;     // [nsys][m+2]  current Arnoldi column
@@ -35,7 +36,7 @@ struct KrylovWs {
   double2* gam;   // [nsys][m+1] rotated residual vector
   DevSys* sys;    // [nsys]
   unsigned long long* mask;  // [1] systems still iterating
-  unsigned* cnt;  // [2][64] last-block counters (zeroed at the start of every solve)
+  unsigned* cnt;  // [2][64] + 1 last-block counters (zeroed at the start of every solve)
 };
 
 constexpr int kKrylovChunk = 1024;
@@ -57,7 +58,8 @@ struct KrylovResult {
 // Solves A_s x_s = b_s (b, x: [nsys][ldv]; only the first n entries of each row used).
 nat_status gmres_batched(int nsys, int64_t n, int64_t ldv, const double2* b, double2* x,
                          const KrylovOp& op, double tol, int max_iter, const KrylovWs& ws,
-                         std::vector<KrylovResult>& res, cudaStream_t s, double* t_op_s = nullptr);
+                         std::vector<KrylovResult>& res, cudaStream_t s, double* t_op_s = nullptr,
+                         bool basis32 = false);
 
 // Reusable timing events of the calling thread on the current device (pool `slot`).
 cudaEvent_t timing_event(int slot, size_t i);

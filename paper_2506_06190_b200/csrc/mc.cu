@@ -197,82 +197,90 @@ struct KArr {
 
 // Fused epilogue of the MC operators: sum of the split-K partials, the fp64 close-pair
 // contributions and the disk / diagonal terms:  apply: out = 1/2 p - R;  rhs:
-// b = R - (eps/2) g.  Eight lanes per output (fixed assignment: lane l takes splits
-// l, l+8, ... and close pairs l, l+8, ...; fixed xor-tree across the lanes).
-constexpr int kFinLanes = 8;
+// b = R - (eps/2) g.  One thread per output: the partials in ascending split order (8
+// coalesced loads in flight; consecutive threads read consecutive rows), then the close
+// pairs of the row in CSR order, their loads issued kFinBatch pairs at a time.
+// (Tried: TMA bulk copies of each block's partial slices into shared memory — 1.9x slower.)
+constexpr int kFinThreads = 256, kFinBatch = 2;
 // Rows [r0, r0 + rows) of the operator (row sharding; r0 = 0, rows = M otherwise): part
 // and out are [.][nsys][rows]; p and g are full vectors [nsys][ldp].
-__global__ void __launch_bounds__(256) mc_finish_kernel(int nsys, int64_t M, const double* __restrict__ smp,
-                                                        const int32_t* __restrict__ rp,
-                                                        const int32_t* __restrict__ col, KArr ka, double w,
-                                                        const double2* part, int n_split,  // may alias out
-                                                        const double2* __restrict__ p,
-                                                        const double2* __restrict__ g, double eps,
-                                                        double2* out,
-                                                        const unsigned long long* __restrict__ skip,
-                                                        int64_t r0, int64_t rows, int64_t ldp) {
+__global__ void __launch_bounds__(kFinThreads) mc_finish_kernel(int nsys, int64_t M, const double* __restrict__ smp,
+                                                                const int32_t* __restrict__ rp,
+                                                                const int32_t* __restrict__ col, KArr ka, double w,
+                                                                const double2* part, int n_split,  // may alias out
+                                                                const double2* __restrict__ p,
+                                                                const double2* __restrict__ g, double eps,
+                                                                double2* out,
+                                                                const unsigned long long* __restrict__ skip,
+                                                                int64_t r0, int64_t rows, int64_t ldp) {
   if (skip && *skip == 0ull) return;
-  const int sub = threadIdx.x % kFinLanes;
-  const int64_t il = blockIdx.x * (int64_t)(blockDim.x / kFinLanes) + threadIdx.x / kFinLanes;
+  const int64_t il = blockIdx.x * (int64_t)kFinThreads + threadIdx.x;
   const int s = blockIdx.y;
-  const bool valid = il < rows;  // whole 8-lane groups
-  const int64_t i = r0 + (valid ? il : 0);
-  const size_t q = (size_t)s * rows + (valid ? il : 0);
+  if (il >= rows) return;
+  const int64_t i = r0 + il;
+  const size_t q = (size_t)s * rows + il;
   const size_t stride = (size_t)nsys * rows;
   double ar = 0.0, ai = 0.0;
-  if (valid) {
-    for (int sp0 = sub; sp0 < n_split; sp0 += 4 * kFinLanes) {
-      double2 v[4];
+  for (int sp0 = 0; sp0 < n_split; sp0 += 8) {
+    double2 v[8];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int sp = sp0 + u * kFinLanes;
-        v[u] = sp < n_split ? part[sp * stride + q] : make_double2(0.0, 0.0);
-      }
+    for (int u = 0; u < 8; ++u)
+      v[u] = sp0 + u < n_split ? part[(size_t)(sp0 + u) * stride + q] : make_double2(0.0, 0.0);
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        ar += v[u].x;
-        ai += v[u].y;
-      }
+    for (int u = 0; u < 8; ++u) {
+      ar += v[u].x;
+      ai += v[u].y;
     }
-    if (rp) {
-      const double k = ka.k[s];
-      const double xi = smp[i], yi = smp[M + i], zi = smp[2 * M + i];
-      for (int e = rp[i] + sub; e < rp[i + 1]; e += kFinLanes) {
-        const int64_t j = col[e];
-        const double dx = smp[j] - xi, dy = smp[M + j] - yi, dz = smp[2 * M + j] - zi;
-        const double r = sqrt(dx * dx + dy * dy + dz * dz);
+  }
+  if (rp) {
+    const double k = ka.k[s];
+    const double xi = smp[i], yi = smp[M + i], zi = smp[2 * M + i];
+    const int e1 = rp[i + 1];
+    for (int e0 = rp[i]; e0 < e1; e0 += kFinBatch) {
+      int32_t jj[kFinBatch];
+#pragma unroll
+      for (int u = 0; u < kFinBatch; ++u) jj[u] = e0 + u < e1 ? col[e0 + u] : -1;
+      double dx[kFinBatch], dy[kFinBatch], dz[kFinBatch], dn[kFinBatch];
+      double2 pv[kFinBatch], gv[kFinBatch];
+#pragma unroll
+      for (int u = 0; u < kFinBatch; ++u) {
+        const int64_t j = jj[u] >= 0 ? jj[u] : i;
+        dx[u] = smp[j] - xi;
+        dy[u] = smp[M + j] - yi;
+        dz[u] = smp[2 * M + j] - zi;
+        if (p) {
+          dn[u] = dx[u] * smp[3 * M + j] + dy[u] * smp[4 * M + j] + dz[u] * smp[5 * M + j];
+          pv[u] = p[(size_t)s * ldp + j];
+        }
+        if (g) gv[u] = g[(size_t)s * ldp + j];
+      }
+#pragma unroll
+      for (int u = 0; u < kFinBatch; ++u) {
+        if (jj[u] < 0) continue;
+        const double r = sqrt(dx[u] * dx[u] + dy[u] * dy[u] + dz[u] * dz[u]);
         float snf, csf;  // |kr| < 2 k eps: the fp32 phase is accurate to ~1e-7 absolute
         __sincosf((float)(k * r), &snf, &csf);
         const double sn = snf, cs = csf;
         const double t = w * nat::kInv4Pi / r;  // w G = t e^{ikr}
         if (p) {  // w p dG/dn_y = t dn/r^2 (ikr - 1) e^{ikr} p
-          const double dn = dx * smp[3 * M + j] + dy * smp[4 * M + j] + dz * smp[5 * M + j];
-          const double2 pv = p[(size_t)s * ldp + j];
-          const double u = t * dn / (r * r);
+          const double uu = t * dn[u] / (r * r);
           const double er = -cs - k * r * sn, ei = k * r * cs - sn;  // (ikr - 1) e^{ikr}
-          ar += u * (er * pv.x - ei * pv.y);
-          ai += u * (er * pv.y + ei * pv.x);
+          ar += uu * (er * pv[u].x - ei * pv[u].y);
+          ai += uu * (er * pv[u].y + ei * pv[u].x);
         }
         if (g) {  // - w g G
-          const double2 gv = g[(size_t)s * ldp + j];
-          ar -= t * (cs * gv.x - sn * gv.y);
-          ai -= t * (cs * gv.y + sn * gv.x);
+          ar -= t * (cs * gv[u].x - sn * gv[u].y);
+          ai -= t * (cs * gv[u].y + sn * gv[u].x);
         }
       }
     }
   }
-#pragma unroll
-  for (int o = kFinLanes / 2; o > 0; o >>= 1) {
-    ar += __shfl_xor_sync(0xffffffffu, ar, o, kFinLanes);
-    ai += __shfl_xor_sync(0xffffffffu, ai, o, kFinLanes);
-  }
-  if (!valid || sub != 0) return;
   if (p) {
-    const double2 pv = p[(size_t)s * ldp + i];
-    out[q] = make_double2(0.5 * pv.x - ar, 0.5 * pv.y - ai);
+    const double2 pi_ = p[(size_t)s * ldp + i];
+    out[q] = make_double2(0.5 * pi_.x - ar, 0.5 * pi_.y - ai);
   } else {
-    const double2 gv = g[(size_t)s * ldp + i];
-    out[q] = make_double2(ar - 0.5 * eps * gv.x, ai - 0.5 * eps * gv.y);
+    const double2 gi_ = g[(size_t)s * ldp + i];
+    out[q] = make_double2(ar - 0.5 * eps * gi_.x, ai - 0.5 * eps * gi_.y);
   }
 }
 
@@ -349,7 +357,7 @@ nat_status finish_op(const nat::RadInput& in, nat_prec prec, int64_t M, const do
   if (st != NAT_OK) return st;
   KArr ka{};
   for (int q = 0; q < nsys && q < 64; ++q) ka.k[q] = k[q];
-  mc_finish_kernel<<<dim3((unsigned)((rows + 256 / kFinLanes - 1) / (256 / kFinLanes)), nsys), 256, 0, s>>>(
+  mc_finish_kernel<<<dim3((unsigned)((rows + kFinThreads - 1) / kFinThreads), nsys), kFinThreads, 0, s>>>(
       nsys, M, smp, np.on ? np.rp : nullptr, np.on ? np.col : nullptr, ka, w, keep.part, keep.n_split, p, g, eps, out,
       in.skip, rr.r0, rows, ldp);
   NAT_LAUNCH_CHECK();
@@ -393,6 +401,15 @@ nat_status mc_eps_w(double area, int64_t M, double eps_in, double* eps, double* 
   *w = M > 1 ? (area - nat::kPi * *eps * *eps) / (double)(M - 1) : 0.0;
   NAT_REQUIRE(*w >= 0, "eps = %g: the disk area pi eps^2 exceeds |Gamma| = %g", *eps, area);
   return NAT_OK;
+}
+
+// The fp32 solves keep their Krylov basis in fp32 (reading R-basis32; NAT_BASIS32=0: fp64).
+bool basis32(nat_prec prec) {
+  static const bool off = [] {
+    const char* e = std::getenv("NAT_BASIS32");
+    return e && e[0] == '0';
+  }();
+  return prec == NAT_FP32 && !off;
 }
 
 nat_status check_k(int n, const double* k) {
@@ -790,7 +807,7 @@ extern "C" nat_status nat_mc_surface_pressure(const nat_mesh* mesh, const nat_ge
     std::vector<nat::KrylovResult> res;
     double t_op = 0;
     st = nat::gmres_batched(nb, M, M, w.b, (double2*)p_out + (size_t)s0 * M, op, tol, max_iter, w.kw, res, s,
-                            info ? &t_op : nullptr);
+                            info ? &t_op : nullptr, basis32(prec));
     if (st != NAT_OK) return deferred(st);
     for (int q = 0; q < nb; ++q) all_conv = all_conv && res[q].converged;
     if (info)
@@ -1001,7 +1018,8 @@ extern "C" nat_status nat_mc_surface_pressure_sharded(nat_comm* comm, const nat_
     };
     std::vector<nat::KrylovResult> res;
     double t_op = 0;
-    st = nat::gmres_batched(nb, M, ldv, w.bfull, w.xfull, op, tol, max_iter, w.kw, res, s, info ? &t_op : nullptr);
+    st = nat::gmres_batched(nb, M, ldv, w.bfull, w.xfull, op, tol, max_iter, w.kw, res, s, info ? &t_op : nullptr,
+                            basis32(prec));
     if (st != NAT_OK) return st;
     NAT_CUDA_TRY(cudaMemcpy2DAsync((double2*)p_out + (size_t)s0 * M, sizeof(double2) * M, w.xfull,
                                    sizeof(double2) * ldv, sizeof(double2) * M, nb, cudaMemcpyDeviceToDevice, s));
