@@ -14,6 +14,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <vector>
 
@@ -72,7 +73,7 @@ Layout layout_of(int n_out) {
 // A is K-major (A[m * lda + k]) or MN-major (A[k * lda + m]); likewise B (B[n * ldb + k] or
 // B[k * ldb + n]).  One CTA = 128 rows x N (N in {16, 32, 64, 128}), K in chunks of 64.
 // =====================================================================================
-constexpr int kGM = 128, kBK = 64, kGT = 128;
+constexpr int kGM = 128, kBK = 64, kGT = 256;  // 8 warps: warp w reads TMEM lanes 32 (w % 4)
 
 enum Epi : int {
   kEpiBiasReluBf16 = 0,  // Cb = bf16(relu(acc + bias))
@@ -93,6 +94,7 @@ struct GemmArgs {
   int64_t ldc;
   bf16* Cb;
   const float* bias;
+  int n_bias;       // bias entries (the rest of the tile reads 0)
   const bf16* H;
   int64_t ldh;
   float* colpart;  // kEpiMaskBf16: [gridDim.x][N]
@@ -155,73 +157,42 @@ __device__ __forceinline__ void stage_operand(const bf16* P, int64_t ld, int64_t
       cp16(smem + ((kk / 8) * (R / 8) + rc) * 128 + (kk % 8) * 16, P + gk * ld + gr, gk < K && gr < rows);
     }
   }
-  asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
-template <int BN, bool AMN, bool BMN>
-__global__ void __launch_bounds__(kGT) nf_gemm_kernel(GemmArgs g) {
-  constexpr uint32_t kABytes = kGM * kBK * 2, kBBytes = BN * kBK * 2;
-  constexpr uint32_t kCols = BN < 32 ? 32 : BN;  // TMEM columns (power of 2 >= 32)
-  extern __shared__ __align__(1024) char gsm[];
-  __shared__ __align__(8) uint64_t bars[2];
-  __shared__ uint32_t tmem_base;
-  __shared__ float colsum[4][BN];
-  char* sA[2] = {gsm, gsm + kABytes + kBBytes};
-  char* sB[2] = {gsm + kABytes, gsm + 2 * kABytes + kBBytes};
+// cp.async.wait_group with a run-time count (immediate operand): groups still allowed in flight
+__device__ __forceinline__ void cp_wait_pending(int n) {
+  switch (n) {
+    case 0: asm volatile("cp.async.wait_group 0;" ::: "memory"); break;
+    case 1: asm volatile("cp.async.wait_group 1;" ::: "memory"); break;
+    case 2: asm volatile("cp.async.wait_group 2;" ::: "memory"); break;
+    default: asm volatile("cp.async.wait_group 3;" ::: "memory"); break;
+  }
+}
+
+// shared-memory stages of the operand pipeline (<= 4; 3 for the 128-wide tiles so that two
+// CTAs share an SM)
+template <int BN>
+constexpr int gemm_stages() {
+  return BN >= 128 ? 3 : 4;
+}
+
+// Epilogue of one 128 x BN tile from TMEM (accumulator at column `tmem`): warp w owns rows
+// (TMEM lanes) 32 (w % 4) .. + 31 and column half w / 4 (BN >= 64; narrower tiles: warps 0-3
+// take all columns); 32 columns per tcgen05.ld.  colsum[4][BN] receives the masked
+// gradient's column sums per lane quarter (kEpiMaskBf16).
+template <int BN>
+__device__ __forceinline__ void gemm_epilogue(const GemmArgs& g, uint32_t tmem, int64_t m0, int split, bool have,
+                                              const float* bias_s, float (*colsum)[BN]) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int64_t m0 = (int64_t)blockIdx.x * kGM;
-  const int split = blockIdx.y;
-  const int64_t kb = (int64_t)split * g.k_per_cta, ke = min(g.K, kb + g.k_per_cta);
-  const int nchunk = (int)((ke - kb + kBK - 1) / kBK);
-
-  if (tid == 0) {
-    nat::mbar_init(&bars[0], 1);
-    nat::mbar_init(&bars[1], 1);
-    nat::fence_mbar_init();
-  }
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(nat::smem_u32(&tmem_base)),
-                 "r"(kCols));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;");
-  const uint32_t tmem = tmem_base;
-  constexpr uint32_t idesc = idesc_bf16(kGM, BN, AMN, BMN);
-  // descriptor strides (bytes): K-group (LBO) and MN-group (SBO)
-  constexpr uint32_t a_lbo = AMN ? kGM * 16 : 128, a_sbo = AMN ? 128 : (kBK / 8) * 128;
-  constexpr uint32_t b_lbo = BMN ? BN * 16 : 128, b_sbo = BMN ? 128 : (kBK / 8) * 128;
-
-  for (int c = 0; c < nchunk; ++c) {
-    const int s = c & 1;
-    if (c >= 2) nat::mbar_wait(&bars[s], ((c - 2) >> 1) & 1);  // the MMAs of chunk c-2 are done
-    const int64_t k0 = kb + (int64_t)c * kBK;
-    stage_operand<kGM, AMN>(g.A, g.lda, g.M, ke, m0, k0, sA[s]);
-    stage_operand<BN, BMN>(g.B, g.ldb, g.N, ke, 0, k0, sB[s]);
-    asm volatile("cp.async.wait_all;" ::: "memory");
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // smem writes -> tensor core reads
-    __syncthreads();
-    if (tid == 0) {
-      asm volatile("tcgen05.fence::after_thread_sync;");
-      const uint32_t a0 = nat::smem_u32(sA[s]), b0 = nat::smem_u32(sB[s]);
-#pragma unroll
-      for (int kk = 0; kk < kBK / 16; ++kk)
-        mma_bf16(tmem, sdesc(a0 + kk * 2 * a_lbo, a_lbo, a_sbo), sdesc(b0 + kk * 2 * b_lbo, b_lbo, b_sbo), idesc,
-                 (c > 0 || kk > 0) ? 1u : 0u);
-      mma_commit(&bars[s]);
-    }
-  }
-  if (nchunk > 0) nat::mbar_wait(&bars[(nchunk - 1) & 1], ((nchunk - 1) >> 1) & 1);
-  asm volatile("tcgen05.fence::after_thread_sync;");
-
-  // epilogue: warp w owns rows (TMEM lanes) 32w .. 32w + 31; 32 columns per tcgen05.ld
-  const int64_t m = m0 + warp * 32 + lane;
-  const bool row_ok = m < g.M && nchunk > 0;
+  const int wq = warp & 3, ch = warp >> 2;
+  const int64_t m = m0 + wq * 32 + lane;
+  const bool row_ok = m < g.M && have;
+  constexpr int kHalf = BN >= 64 ? BN / 2 : BN;
+  const bool epi_warp = BN >= 64 || ch == 0;
 #pragma unroll 1
-  for (int n0 = 0; n0 < BN; n0 += 32) {
+  for (int n0 = ch * kHalf; epi_warp && n0 < (ch + 1) * kHalf; n0 += 32) {
     uint32_t v[32];
-    const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)n0;
+    const uint32_t taddr = tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)n0;
     if constexpr (BN >= 32) {
       asm volatile(
           "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
@@ -249,7 +220,7 @@ __global__ void __launch_bounds__(kGT) nf_gemm_kernel(GemmArgs g) {
     if (g.epi == kEpiBiasReluBf16 || g.epi == kEpiMaskBf16) {
       if (g.epi == kEpiBiasReluBf16) {
 #pragma unroll
-        for (int q = 0; q < W; ++q) f[q] = fmaxf(f[q] + g.bias[n0 + q], 0.f);
+        for (int q = 0; q < W; ++q) f[q] = fmaxf(f[q] + bias_s[n0 + q], 0.f);
       } else {
 #pragma unroll
         for (int q = 0; q < W; q += 8) {
@@ -260,7 +231,7 @@ __global__ void __launch_bounds__(kGT) nf_gemm_kernel(GemmArgs g) {
         }
         // column sums of the masked gradient (bias gradient): a transposing butterfly over the
         // warp (31 shuffles for 32 columns; lane l ends with column l's sum over the 32 rows),
-        // then the 4 warps in warp order
+        // then the 4 lane quarters in order
         if constexpr (W == 32) {
           float t[32];
 #pragma unroll
@@ -275,14 +246,14 @@ __global__ void __launch_bounds__(kGT) nf_gemm_kernel(GemmArgs g) {
               t[q] = (up ? t[q + o] : t[q]) + recv;
             }
           }
-          colsum[warp][n0 + lane] = t[0];
+          colsum[wq][n0 + lane] = t[0];
         } else {
 #pragma unroll
           for (int q = 0; q < W; ++q) {
             float t = f[q];
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-            if (lane == 0) colsum[warp][n0 + q] = t;
+            if (lane == 0) colsum[wq][n0 + q] = t;
           }
         }
       }
@@ -303,11 +274,96 @@ __global__ void __launch_bounds__(kGT) nf_gemm_kernel(GemmArgs g) {
         for (int q = 0; q < W; q += 4) *reinterpret_cast<float4*>(dst + q) = make_float4(f[q], f[q + 1], f[q + 2], f[q + 3]);
       }
     } else {  // kEpiBiasF32, kEpiF32
-      if (row_ok)
-        for (int q = 0; q < W; ++q)
-          if (n0 + q < g.n_valid) g.C[m * g.ldc + n0 + q] = f[q] + (g.epi == kEpiBiasF32 ? g.bias[n0 + q] : 0.f);
+      if (g.epi == kEpiBiasF32) {
+#pragma unroll
+        for (int q = 0; q < W; ++q) f[q] += bias_s[n0 + q];
+      }
+      if (row_ok) {
+        float* dst = g.C + m * g.ldc + n0;
+        if (n0 + W <= g.n_valid && (g.ldc % 4) == 0) {
+#pragma unroll
+          for (int q = 0; q < W; q += 4) *reinterpret_cast<float4*>(dst + q) = make_float4(f[q], f[q + 1], f[q + 2], f[q + 3]);
+        } else {
+          for (int q = 0; q < W; ++q)
+            if (n0 + q < g.n_valid) dst[q] = f[q];
+        }
+      }
     }
   }
+}
+
+template <int BN, bool AMN, bool BMN>
+__global__ void __launch_bounds__(kGT) nf_gemm_kernel(GemmArgs g) {
+  constexpr uint32_t kABytes = kGM * kBK * 2, kBBytes = BN * kBK * 2;
+  constexpr uint32_t kCols = BN < 32 ? 32 : BN;  // TMEM columns (power of 2 >= 32)
+  constexpr int S = gemm_stages<BN>();
+  extern __shared__ __align__(1024) char gsm[];
+  __shared__ __align__(8) uint64_t bars[S];
+  __shared__ uint32_t tmem_base;
+  __shared__ float colsum[4][BN];
+  __shared__ float bias_s[BN];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int wq = warp & 3, ch = warp >> 2;  // TMEM lane quarter, column half of the epilogue
+  const int64_t m0 = (int64_t)blockIdx.x * kGM;
+  const int split = blockIdx.y;
+  const int64_t kb = (int64_t)split * g.k_per_cta, ke = min(g.K, kb + g.k_per_cta);
+  const int nchunk = (int)((ke - kb + kBK - 1) / kBK);
+  auto sA = [&](int st) { return gsm + (size_t)st * (kABytes + kBBytes); };
+  auto sB = [&](int st) { return gsm + (size_t)st * (kABytes + kBBytes) + kABytes; };
+  // chunk c -> stage c % S: both operands' 16-byte pieces, one cp.async group per chunk
+  auto stage = [&](int c) {
+    const int64_t k0 = kb + (int64_t)c * kBK;
+    stage_operand<kGM, AMN>(g.A, g.lda, g.M, ke, m0, k0, sA(c % S));
+    stage_operand<BN, BMN>(g.B, g.ldb, g.N, ke, 0, k0, sB(c % S));
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+
+  if (tid == 0) {
+    for (int q = 0; q < S; ++q) nat::mbar_init(&bars[q], 1);
+    nat::fence_mbar_init();
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(nat::smem_u32(&tmem_base)),
+                 "r"(kCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  // the first S chunks' loads are in flight before the TMEM handshake completes
+  for (int c = 0; c < S && c < nchunk; ++c) stage(c);
+  if (g.bias)
+    for (int n = tid; n < BN; n += kGT) bias_s[n] = n < g.n_bias ? g.bias[n] : 0.f;
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = tmem_base;
+  constexpr uint32_t idesc = idesc_bf16(kGM, BN, AMN, BMN);
+  // descriptor strides (bytes): K-group (LBO) and MN-group (SBO)
+  constexpr uint32_t a_lbo = AMN ? kGM * 16 : 128, a_sbo = AMN ? 128 : (kBK / 8) * 128;
+  constexpr uint32_t b_lbo = BMN ? BN * 16 : 128, b_sbo = BMN ? 128 : (kBK / 8) * 128;
+
+  for (int c = 0; c < nchunk; ++c) {
+    // groups committed so far: min(nchunk, c + S); chunk c's is done when at most
+    // min(nchunk, c + S) - (c + 1) younger ones are pending
+    cp_wait_pending(min(nchunk, c + S) - (c + 1));
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // smem writes -> tensor core reads
+    __syncthreads();
+    if (tid == 0) {
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const uint32_t a0 = nat::smem_u32(sA(c % S)), b0 = nat::smem_u32(sB(c % S));
+#pragma unroll
+      for (int kk = 0; kk < kBK / 16; ++kk)
+        mma_bf16(tmem, sdesc(a0 + kk * 2 * a_lbo, a_lbo, a_sbo), sdesc(b0 + kk * 2 * b_lbo, b_lbo, b_sbo), idesc,
+                 (c > 0 || kk > 0) ? 1u : 0u);
+      mma_commit(&bars[c % S]);
+    }
+    if (c + S < nchunk) {  // refill this stage once its MMAs have read it
+      nat::mbar_wait(&bars[c % S], (uint32_t)((c / S) & 1));
+      stage(c + S);
+    }
+  }
+  if (nchunk > 0) nat::mbar_wait(&bars[(nchunk - 1) % S], (uint32_t)(((nchunk - 1) / S) & 1));
+  asm volatile("tcgen05.fence::after_thread_sync;");
+
+  gemm_epilogue<BN>(g, tmem, m0, split, nchunk > 0, bias_s, colsum);
   if (g.epi == kEpiMaskBf16) {
     __syncthreads();
     for (int n = tid; n < BN; n += kGT)
@@ -318,9 +374,114 @@ __global__ void __launch_bounds__(kGT) nf_gemm_kernel(GemmArgs g) {
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kCols));
 }
 
+// Persistent variant for the products with K <= 128 over the batch (forward Y = X W^T and
+// input gradients dX = dY W): A = activations [M][K] K-major, B = the layer's weights,
+// staged ONCE per CTA.  The CTA walks the 128-row tiles t = blockIdx.x, + gridDim.x, ...
+// with two A buffers and two TMEM accumulators: while tile i's MMAs run, tile i+1's rows
+// are loading and tile i-1's epilogue drains its accumulator.
+template <int BN, bool BMN>
+__global__ void __launch_bounds__(kGT) nf_gemm_persist_kernel(GemmArgs g, int64_t n_tiles) {
+  constexpr uint32_t kABytes = kGM * kBK * 2, kBBytes = BN * kBK * 2;
+  constexpr uint32_t kCols = BN < 32 ? 32 : BN;
+  extern __shared__ __align__(1024) char gsm[];
+  __shared__ __align__(8) uint64_t bars[2];
+  __shared__ uint32_t tmem_base;
+  __shared__ float colsum[4][BN];
+  __shared__ float bias_s[BN];
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int nchunk = (int)((g.K + kBK - 1) / kBK);  // 1 or 2
+  char* sB = gsm;                                      // [2 chunks] weights
+  auto sA = [&](int buf) { return gsm + 2 * kBBytes + (size_t)buf * 2 * kABytes; };
+  const int64_t my_n = n_tiles > blockIdx.x ? (n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  auto stage_a = [&](int64_t i) {
+    const int64_t m0 = (blockIdx.x + i * gridDim.x) * (int64_t)kGM;
+    for (int c = 0; c < nchunk; ++c)
+      stage_operand<kGM, false>(g.A, g.lda, g.M, g.K, m0, (int64_t)c * kBK, sA((int)(i & 1)) + (size_t)c * kABytes);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  if (tid == 0) {
+    nat::mbar_init(&bars[0], 1);
+    nat::mbar_init(&bars[1], 1);
+    nat::fence_mbar_init();
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(nat::smem_u32(&tmem_base)),
+                 "r"(2 * kCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (my_n > 0) {
+    for (int c = 0; c < nchunk; ++c)
+      stage_operand<BN, BMN>(g.B, g.ldb, g.N, g.K, 0, (int64_t)c * kBK, sB + (size_t)c * kBBytes);
+    stage_a(0);  // group 0: weights + tile 0
+    if (my_n > 1) stage_a(1);
+  }
+  if (g.bias)
+    for (int n = tid; n < BN; n += kGT) bias_s[n] = n < g.n_bias ? g.bias[n] : 0.f;
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem0 = tmem_base;
+  constexpr uint32_t idesc = idesc_bf16(kGM, BN, false, BMN);
+  constexpr uint32_t a_lbo = 128, a_sbo = (kBK / 8) * 128;
+  constexpr uint32_t b_lbo = BMN ? BN * 16 : 128, b_sbo = BMN ? 128 : (kBK / 8) * 128;
+  auto drain = [&](int64_t i) {  // epilogue of tile i (its MMAs are complete)
+    const int64_t tile = blockIdx.x + i * gridDim.x;
+    gemm_epilogue<BN>(g, tmem0 + (uint32_t)(i & 1) * kCols, tile * kGM, 0, true, bias_s, colsum);
+    if (g.epi == kEpiMaskBf16) {
+      __syncthreads();
+      for (int n = tid; n < BN; n += kGT)
+        g.colpart[(size_t)tile * BN + n] = ((colsum[0][n] + colsum[1][n]) + colsum[2][n]) + colsum[3][n];
+    }
+  };
+  for (int64_t i = 0; i < my_n; ++i) {
+    if (i == 0 && my_n > 1) asm volatile("cp.async.wait_group 1;" ::: "memory");
+    else asm volatile("cp.async.wait_group 0;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (tid == 0) {
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const uint32_t a0 = nat::smem_u32(sA((int)(i & 1))), b0 = nat::smem_u32(sB);
+      const uint32_t acc = tmem0 + (uint32_t)(i & 1) * kCols;
+      for (int c = 0; c < nchunk; ++c)
+#pragma unroll
+        for (int kk = 0; kk < kBK / 16; ++kk)
+          mma_bf16(acc, sdesc(a0 + c * kABytes + kk * 2 * a_lbo, a_lbo, a_sbo),
+                   sdesc(b0 + c * kBBytes + kk * 2 * b_lbo, b_lbo, b_sbo), idesc, (c > 0 || kk > 0) ? 1u : 0u);
+      mma_commit(&bars[i & 1]);
+    }
+    if (i >= 1) {
+      nat::mbar_wait(&bars[(i - 1) & 1], (uint32_t)(((i - 1) >> 1) & 1));
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      if (i + 1 < my_n) stage_a(i + 1);  // into the buffer tile i-1's MMAs have released
+      drain(i - 1);
+    }
+  }
+  if (my_n > 0) {
+    nat::mbar_wait(&bars[(my_n - 1) & 1], (uint32_t)(((my_n - 1) >> 1) & 1));
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    drain(my_n - 1);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem0), "r"(2 * kCols));
+}
+
+template <int BN, bool BMN>
+cudaError_t launch_persist_t(const GemmArgs& g, cudaStream_t s) {
+  const size_t smem = 2 * ((size_t)BN * kBK * 2) + 2 * 2 * ((size_t)kGM * kBK * 2);
+  auto k = nf_gemm_persist_kernel<BN, BMN>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const int64_t tiles = (g.M + kGM - 1) / kGM;
+  const int64_t grid = std::min<int64_t>(tiles, 2 * (int64_t)nat::device_sm_count());
+  k<<<(unsigned)grid, kGT, smem, s>>>(g, tiles);
+  return cudaGetLastError();
+}
+
 template <int BN, bool AMN, bool BMN>
 cudaError_t launch_gemm_t(const GemmArgs& g, int splits, cudaStream_t s) {
-  const size_t smem = 2 * ((size_t)kGM * kBK * 2 + (size_t)BN * kBK * 2);
+  const size_t smem = (size_t)gemm_stages<BN>() * ((size_t)kGM * kBK * 2 + (size_t)BN * kBK * 2);
   auto k = nf_gemm_kernel<BN, AMN, BMN>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -344,7 +505,19 @@ cudaError_t launch_gemm(const GemmArgs& g, bool a_mn, bool b_mn, int splits, cud
   const bool timed = nat::ktimer_on();  // diagnostics: flops = 2 M N K of the product
   if (timed) nat::ktimer_begin(nat::kTimerNfGemm, s);
   cudaError_t e;
-  if (!a_mn && !b_mn) e = launch_gemm_n<false, false>(g, splits, s);
+  static const bool persist_env = [] {  // NAT_NF_PERSIST=0: the one-tile-per-CTA kernel (A/B)
+    const char* v = std::getenv("NAT_NF_PERSIST");
+    return !(v && v[0] == '0');
+  }();
+  if (persist_env && !a_mn && splits == 1 && g.K <= 2 * kBK && g.k_per_cta >= g.K) {
+    switch (g.N) {
+      case 16: e = b_mn ? launch_persist_t<16, true>(g, s) : launch_persist_t<16, false>(g, s); break;
+      case 32: e = b_mn ? launch_persist_t<32, true>(g, s) : launch_persist_t<32, false>(g, s); break;
+      case 64: e = b_mn ? launch_persist_t<64, true>(g, s) : launch_persist_t<64, false>(g, s); break;
+      case 128: e = b_mn ? launch_persist_t<128, true>(g, s) : launch_persist_t<128, false>(g, s); break;
+      default: e = cudaErrorInvalidValue;
+    }
+  } else if (!a_mn && !b_mn) e = launch_gemm_n<false, false>(g, splits, s);
   else if (!a_mn && b_mn) e = launch_gemm_n<false, true>(g, splits, s);
   else if (a_mn && !b_mn) e = launch_gemm_n<true, false>(g, splits, s);
   else e = launch_gemm_n<true, true>(g, splits, s);
@@ -496,11 +669,40 @@ __global__ void __launch_bounds__(256) nf_reduce_wide_kernel(int64_t nparts, int
   }
 }
 
-__global__ void nf_loss_finish_kernel(int64_t nparts, const double* __restrict__ lpart, int64_t count,
-                                      float* __restrict__ loss) {
+// First level of a tall reduction (many parts, few columns): block (x, y) sums the parts
+// [y per, (y + 1) per) of columns x*32 .. x*32 + 31 (8 groups strided over the parts, then
+// the groups in order) into tmp[y][j]; nf_reduce_wide_kernel then sums the gridDim.y rows.
+__global__ void __launch_bounds__(256) nf_reduce_tall_kernel(int64_t nparts, int64_t total, int64_t per,
+                                                             const float* __restrict__ part, float* __restrict__ tmp) {
+  __shared__ float sm[8][33];
+  const int lane = threadIdx.x & 31, grp = threadIdx.x >> 5;
+  const int64_t j = blockIdx.x * 32 + lane;
+  const int64_t p0 = blockIdx.y * per, p1 = min(nparts, p0 + per);
+  float t = 0.f;
+  if (j < total)
+    for (int64_t p = p0 + grp; p < p1; p += 8) t += part[p * total + j];
+  sm[grp][lane] = t;
+  __syncthreads();
+  if (grp == 0 && j < total) {
+    float u = sm[0][lane];
+    for (int g = 1; g < 8; ++g) u += sm[g][lane];
+    tmp[blockIdx.y * total + j] = u;
+  }
+}
+
+// one block: thread t sums parts t, t + 256, ... in order, then a fixed tree
+__global__ void __launch_bounds__(256) nf_loss_finish_kernel(int64_t nparts, const double* __restrict__ lpart,
+                                                             int64_t count, float* __restrict__ loss) {
+  __shared__ double sm[256];
   double t = 0.0;
-  for (int64_t p = 0; p < nparts; ++p) t += lpart[p];
-  *loss = (float)(t / (double)count);
+  for (int64_t p = threadIdx.x; p < nparts; p += 256) t += lpart[p];
+  sm[threadIdx.x] = t;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) sm[threadIdx.x] += sm[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *loss = (float)(sm[0] / (double)count);
 }
 
 // dGrid[level][row] += w_corner * dX[b][level*4 + f]   (atomics: order-free sums).
@@ -589,12 +791,23 @@ struct NfWs {
   bf16* Wb;       // [5][128][128] bf16 weight slots
   float* wpart;   // [splits][128][128]
   float* cpart;   // [tiles][128]
+  float* rtmp;    // [kTallRows][128] first level of the tall column-sum reductions
   double* lpart;  // loss partials
   float* bpart;   // [loss blocks][16]
   int64_t splits, tiles, lblocks;
 };
 
 constexpr int64_t kSplitRows = 1024;  // batch rows per split-K CTA of the weight gradients
+constexpr int kTallRows = 64;         // first-level rows of the tall column-sum reductions
+
+// column sums of part[nparts][cols] (cols <= 128) -> out (fixed order, two levels)
+void reduce_tall(int64_t nparts, int64_t cols, const float* part, float* out, int64_t out_cols, float* tmp,
+                 cudaStream_t s) {
+  const int64_t G = std::min<int64_t>(kTallRows, (nparts + 31) / 32);
+  const int64_t per = (nparts + G - 1) / G;
+  nf_reduce_tall_kernel<<<dim3((unsigned)((cols + 31) / 32), (unsigned)G), 256, 0, s>>>(nparts, cols, per, part, tmp);
+  nf_reduce_wide_kernel<<<(unsigned)((cols + 31) / 32), 256, 0, s>>>(G, 1, cols, tmp, out, 1, out_cols, false);
+}
 
 size_t nf_carve(nat::Carver& c, NfWs* w, int64_t n, int64_t n_params) {
   NfWs t{};
@@ -612,6 +825,7 @@ size_t nf_carve(nat::Carver& c, NfWs* w, int64_t n, int64_t n_params) {
   t.lblocks = (n + kLossT - 1) / kLossT;
   t.wpart = c.take<float>((size_t)t.splits * kHidden * kHidden);
   t.cpart = c.take<float>((size_t)t.tiles * kHidden);
+  t.rtmp = c.take<float>((size_t)kTallRows * kHidden);
   t.lpart = c.take<double>((size_t)t.lblocks);
   t.bpart = c.take<float>((size_t)t.lblocks * kOutPad);
   if (w) *w = t;
@@ -644,6 +858,7 @@ nat_status forward_impl(const Layout& L, int64_t n, const float* params, NfWs& w
     g.K = L.in[q];
     g.k_per_cta = L.in[q];
     g.bias = params + L.b[q];
+    g.n_bias = L.out[q];
     if (q < kNHidden) {
       g.N = kHidden;
       g.epi = kEpiBiasReluBf16;
@@ -731,11 +946,10 @@ extern "C" nat_status nat_nf_train_step(const nat_nf_config* cfg, float* params,
   if (st != NAT_OK) return st;
   // loss and dY (MSE, l.124)
   nf_loss_kernel<<<(unsigned)w.lblocks, kLossT, 0, s>>>(n, cfg->n_out, w.Y, targets, w.dY, w.lpart, w.bpart);
-  nf_loss_finish_kernel<<<1, 1, 0, s>>>(w.lblocks, w.lpart, n * cfg->n_out, loss);
+  nf_loss_finish_kernel<<<1, 256, 0, s>>>(w.lblocks, w.lpart, n * cfg->n_out, loss);
   NAT_CUDA_TRY(cudaMemsetAsync(w.grad, 0, sizeof(float) * L.total, s));
   // output-layer bias gradient: column sums of dY
-  nf_reduce_wide_kernel<<<1, 256, 0, s>>>(w.lblocks, 1, kOutPad, w.bpart, w.grad + L.b[kNHidden], 1,
-                                          L.out[kNHidden], false);
+  reduce_tall(w.lblocks, kOutPad, w.bpart, w.grad + L.b[kNHidden], L.out[kNHidden], w.rtmp, s);
   // backward through the layers: d = gradient with respect to layer q's output
   const bf16* d = w.dY;
   int dcols = kOutPad;
@@ -789,8 +1003,7 @@ extern "C" nat_status nat_nf_train_step(const nat_nf_config* cfg, float* params,
       gd.colpart = w.cpart;
       NF_LAUNCH(launch_gemm(gd, false, true, 1, s));
       // bias gradient of layer q - 1: column sums of the masked gradient, tile order
-      nf_reduce_wide_kernel<<<kHidden / 32, 256, 0, s>>>(w.tiles, 1, kHidden, w.cpart, w.grad + L.b[q - 1], 1,
-                                                          kHidden, false);
+      reduce_tall(w.tiles, kHidden, w.cpart, w.grad + L.b[q - 1], kHidden, w.rtmp, s);
       NAT_LAUNCH_CHECK();
       d = w.dH[q & 1];
       dcols = in;
