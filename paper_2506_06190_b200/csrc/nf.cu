@@ -713,7 +713,7 @@ __host__ __device__ constexpr int64_t smem_grid_rows() { return level_rows(0) + 
 
 __global__ void __launch_bounds__(256) nf_grid_backward_kernel(int64_t n, int n_v, const float* __restrict__ in,
                                                                const float* __restrict__ dX, Layout L,
-                                                               float* __restrict__ grad) {
+                                                               float* __restrict__ grad, int smem_levels) {
   extern __shared__ float sg[];  // [smem_grid_rows][4]
   for (int64_t i = threadIdx.x; i < smem_grid_rows() * kFeat; i += blockDim.x) sg[i] = 0.f;
   __syncthreads();
@@ -732,17 +732,22 @@ __global__ void __launch_bounds__(256) nf_grid_backward_kernel(int64_t n, int n_
         fr[d] = p - fl;
       }
       const float4 g = *reinterpret_cast<const float4*>(dX + b * kInPad + l * kFeat);
-      float* G = l < kSmemLevels ? sg + (l == 0 ? 0 : level_rows(0) * kFeat) : grad + L.grid[l];
+      const bool in_smem = l < smem_levels;
+      float* G = in_smem ? sg + (l == 0 ? 0 : level_rows(0) * kFeat) : grad + L.grid[l];
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
         const int dx = c & 1, dy = (c >> 1) & 1, dz = (c >> 2) & 1;
         const float wx = dx ? fr[0] : 1.f - fr[0], wy = dy ? fr[1] : 1.f - fr[1], wz = dz ? fr[2] : 1.f - fr[2];
         const float w = (wx * wy) * wz;
         float* r = G + vertex_row(l, i0[0] + dx, i0[1] + dy, i0[2] + dz) * kFeat;
-        atomicAdd(r + 0, w * g.x);
-        atomicAdd(r + 1, w * g.y);
-        atomicAdd(r + 2, w * g.z);
-        atomicAdd(r + 3, w * g.w);
+        if (in_smem) {
+          atomicAdd(r + 0, w * g.x);
+          atomicAdd(r + 1, w * g.y);
+          atomicAdd(r + 2, w * g.z);
+          atomicAdd(r + 3, w * g.w);
+        } else {  // one 16-byte vector reduction (red.global.add.v4.f32) per corner
+          atomicAdd(reinterpret_cast<float4*>(r), make_float4(w * g.x, w * g.y, w * g.z, w * g.w));
+        }
       }
     }
   }
@@ -1019,7 +1024,11 @@ extern "C" nat_status nat_nf_train_step(const nat_nf_config* cfg, float* params,
     const size_t gsm = sizeof(float) * smem_grid_rows() * kFeat;
     NAT_CUDA_TRY(cudaFuncSetAttribute(nf_grid_backward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsm));
     const int64_t ctas = std::min<int64_t>(2 * (int64_t)nat::device_sm_count(), (n + 255) / 256);
-    nf_grid_backward_kernel<<<(unsigned)ctas, 256, gsm, s>>>(n, cfg->n_v, inputs, w.dX, L, w.grad);
+    static const int smem_levels = [] {  // NAT_NF_SMEM_LEVELS: coarse levels accumulated in shared memory
+      const char* v = std::getenv("NAT_NF_SMEM_LEVELS");
+      return v ? std::max(0, std::min(kSmemLevels, std::atoi(v))) : 1;  // level 0 only (A/B: 1.071 vs 1.080 ms)
+    }();
+    nf_grid_backward_kernel<<<(unsigned)ctas, 256, gsm, s>>>(n, cfg->n_v, inputs, w.dX, L, w.grad, smem_levels);
   }
   NAT_LAUNCH_CHECK();
   if (grad_out) NAT_CUDA_TRY(cudaMemcpyAsync(grad_out, w.grad, sizeof(float) * L.total, cudaMemcpyDeviceToDevice, s));
