@@ -33,6 +33,8 @@ inside the timed region.  Secondary lines (C2 dense BEM + BEM-MC, C3 modal MC) a
 import argparse
 import json
 import math
+import concurrent.futures
+import gc
 import os
 import queue
 import statistics
@@ -79,7 +81,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="nat", choices=["nat", "reference"])
-    ap.add_argument("--workers", type=int, default=int(os.environ.get("NAT_BENCH_WORKERS", "4")))
+    ap.add_argument("--workers", type=int, default=int(os.environ.get("NAT_BENCH_WORKERS", "6")))
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-profile-count", action="store_true")
@@ -165,19 +167,28 @@ def load_c4_host(geo_ids):
 
 
 class Worker:
-    """One host thread's CUDA stream, workspaces and output buffers."""
+    """One host thread's CUDA streams, workspaces and output buffers.  The MC solve runs on a
+    high-priority stream and the radiation on a low-priority one: the solve is a chain of
+    ~120-170 dependent small launches whose latency sets the geometry's time, the radiation
+    is a bulk MUFU-bound pass that can fill whatever the solves leave idle, and geometry
+    q + 1's solve overlaps geometry q's radiation (per-geometry buffers double-buffered)."""
 
     def __init__(self, nat, torch, n_vert, n_tri, e2e_out):
         dev = torch.device("cuda")
-        self.stream = torch.cuda.Stream()
+        self.stream = torch.cuda.Stream(priority=-5)   # clamped to the device's highest priority
+        self.rad_stream = torch.cuda.Stream(priority=0)
         self.copy_stream = torch.cuda.Stream()
         self.mc_plan = nat.McPlan(M_C4, N_K, "fp32", 200, dev)
         self.rad_plan = nat.RadiatePlan(M_C4, N_K, P_LIS, "fp32", dev)
-        self.smp = torch.empty(6, M_C4, dtype=torch.float64, device=dev)
-        self.stri = torch.empty(M_C4, dtype=torch.int32, device=dev)
-        self.p = torch.empty(N_K, M_C4, dtype=torch.complex128, device=dev)
-        self.gs = torch.empty(N_K, M_C4, dtype=torch.complex128, device=dev)
-        self.lis = torch.empty(3, P_LIS, dtype=torch.float64, device=dev)
+        # per-geometry buffers read by the radiation: two slots
+        self.smp = [torch.empty(6, M_C4, dtype=torch.float64, device=dev) for _ in range(2)]
+        self.stri = [torch.empty(M_C4, dtype=torch.int32, device=dev) for _ in range(2)]
+        self.p = [torch.empty(N_K, M_C4, dtype=torch.complex128, device=dev) for _ in range(2)]
+        self.gs = [torch.empty(N_K, M_C4, dtype=torch.complex128, device=dev) for _ in range(2)]
+        self.lis = [torch.empty(3, P_LIS, dtype=torch.float64, device=dev) for _ in range(2)]
+        self.solved = [torch.cuda.Event() for _ in range(2)]
+        self.radiated = [torch.cuda.Event() for _ in range(2)]
+        self.gslot = 0
         # double-buffered field: the D2H of geometry q overlaps the radiation of q + 1
         self.out = [torch.empty(N_K, P_LIS, dtype=torch.complex128, device=dev) for _ in range(2)]
         self.copied = [torch.cuda.Event() for _ in range(2)]
@@ -205,6 +216,9 @@ class Sweep:
             if e2e:
                 self.pinned[gi] = tuple(torch.from_numpy(h[k]).pin_memory() for k in ("v", "t", "g"))
         self.workers = [Worker(nat, torch, self.n_vert, self.n_tri, e2e) for _ in range(n_workers)]
+        self.verbose = bool(os.environ.get("NAT_BENCH_VERBOSE"))
+        self.cost = {}   # host seconds per geometry in the last pass (NAT_BENCH_VERBOSE)
+        self.pool, self.pool_size = None, 0
         self.lock = threading.Lock()
 
     def _geometry(self, w, gi, host_io, rec):
@@ -218,21 +232,26 @@ class Sweep:
             mesh, g = w.mesh, w.g
         else:
             mesh, g = self.dmesh[gi], self.dg[gi]
+        k = w.gslot
+        w.stream.wait_event(w.radiated[k])   # slot k's previous radiation has read its buffers
         geo = nat.nat_mesh_prepare(mesh)                                                       # a1
-        nat.nat_listener_grid(geo.center, geo.bound_radius, *GRID, out=w.lis)                  # a12
+        nat.nat_listener_grid(geo.center, geo.bound_radius, *GRID, out=w.lis[k])               # a12
         smp, stri, p, infos = nat.nat_mc_surface_pressure(mesh, geo, h["ks"], g, M_C4, seed=20250606, stream_id=gi,
                                                           prec="fp32", tol=1e-6, plan=w.mc_plan,
-                                                          out=(w.smp, w.stri, w.p))            # a8-a10
-        nat.nat_mc_gather_neumann(g, stri, out=w.gs)
-        src = nat.nat_mc_sources(smp, geo.total_area, p, w.gs, center=geo.center)
+                                                          out=(w.smp[k], w.stri[k], w.p[k]))   # a8-a10
+        nat.nat_mc_gather_neumann(g, stri, out=w.gs[k])
+        src = nat.nat_mc_sources(smp, geo.total_area, p, w.gs[k], center=geo.center)
+        w.solved[k].record(w.stream)
         out = w.out[w.slot]
-        if host_io:
-            torch.cuda.current_stream().wait_event(w.copied[w.slot])   # the slot's previous D2H is done
-        nat.nat_radiate_field(src, h["ks"], w.lis, "fp32", out=out, plan=w.rad_plan)           # a11
+        with torch.cuda.stream(w.rad_stream):
+            w.rad_stream.wait_event(w.solved[k])
+            if host_io:
+                w.rad_stream.wait_event(w.copied[w.slot])   # the slot's previous D2H is done
+            nat.nat_radiate_field(src, h["ks"], w.lis[k], "fp32", out=out, plan=w.rad_plan)   # a11
+            w.radiated[k].record(w.rad_stream)
+        w.gslot ^= 1
         if host_io:   # field -> pinned host on the copy stream
-            done = torch.cuda.Event()
-            done.record()
-            w.copy_stream.wait_event(done)
+            w.copy_stream.wait_event(w.radiated[k])
             with torch.cuda.stream(w.copy_stream):
                 w.host_out.copy_(out, non_blocking=True)
                 w.copied[w.slot].record()
@@ -265,31 +284,50 @@ class Sweep:
         ready.record(cur)
         err = []
 
+        t_run = time.perf_counter()
+        spans = {}
+
         def loop(w):
+            t_start = time.perf_counter() - t_run
+            n_done = 0
             try:
                 with torch.cuda.stream(w.stream):
                     w.stream.wait_event(ready)
+                    w.rad_stream.wait_event(ready)
                     while True:
                         try:
                             gi = q.get_nowait()
                         except queue.Empty:
                             return
+                        t0 = time.perf_counter()
                         self._geometry(w, gi, host_io, rec)
+                        dt = time.perf_counter() - t0
+                        n_done += 1
+                        with self.lock:
+                            self.cost[gi] = dt
+                            if self.verbose:
+                                rec.setdefault("host_s", []).append((round(dt, 3), gi))
+                                spans[id(w)] = (round(t_start, 3), round(time.perf_counter() - t_run, 3), n_done)
             except BaseException as ex:   # re-raised on the main thread
                 err.append(ex)
 
         if len(ws) == 1:
             loop(ws[0])
         else:
-            ths = [threading.Thread(target=loop, args=(w,)) for w in ws]
-            for t in ths:
-                t.start()
-            for t in ths:
-                t.join()
+            # persistent threads: libnat keeps per-thread pinned rings and events (created on a
+            # thread's first solve, released when it exits), so threads must outlive the steps
+            if self.pool is None or self.pool_size < len(ws):
+                self.pool = concurrent.futures.ThreadPoolExecutor(max_workers=len(ws))
+                self.pool_size = len(ws)
+            for f in [self.pool.submit(loop, w) for w in ws]:
+                f.result()
         if err:
             raise err[0]
+        if self.verbose:
+            print(f"[bench] worker spans (start, end, geometries): {sorted(spans.values())}", file=sys.stderr)
         for w in ws:
             cur.wait_stream(w.stream)
+            cur.wait_stream(w.rad_stream)
             cur.wait_stream(w.copy_stream)
         return rec
 
@@ -459,6 +497,7 @@ def main():
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     from paper_2506_06190_b200 import nat
+    nat.sweep_tuning()
     nat.lib()
     if world > 1:
         dist.init_process_group("nccl", init_method="env://", device_id=torch.device("cuda", local))
@@ -486,19 +525,29 @@ def main():
             flush.fill_(1)   # L2 flush between timed steps (outside the step events)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
+            t_host = time.perf_counter()
             rec = sweep.run(host_io=host_io)
             e1.record()
+            if sweep.verbose:
+                hs = sorted(rec.pop("host_s", []), reverse=True)
+                print(f"[bench] step host {time.perf_counter() - t_host:.3f} s, slowest geometries {hs[:4]}, "
+                      f"median {hs[len(hs) // 2] if hs else None}", file=sys.stderr)
             ev.append((e0, e1))
             tot = merge(tot, rec)
         barrier()
+        if os.environ.get("NAT_BENCH_VERBOSE"):
+            print("[bench] step ms:", [round(a.elapsed_time(b), 1) for a, b in ev], file=sys.stderr)
         return sum(a.elapsed_time(b) for a, b in ev), tot
 
     for _ in range(max(3, args.warmup)):
         sweep.run()
     barrier()
     cs = ClockSampler(local)
+    gc.collect()
+    gc.disable()   # no collector pauses on the worker threads inside the timed steps
     with cs:
         ms, tot = timed(args.steps)
+    gc.enable()
     clk = cs.summary()
     ms_max, pairs_all = allreduce_max_sum(ms, float(step_pairs(tot)))
     _, lis_all = allreduce_max_sum(0.0, float(tot["lis_pt_modes"]))
@@ -507,7 +556,10 @@ def main():
     e2e = None
     if not args.no_e2e:
         sweep.run(host_io=True)   # warm the pinned paths
+        gc.collect()
+        gc.disable()
         ms_e, tot_e = timed(args.steps, host_io=True)
+        gc.enable()
         ms_e_max, pe = allreduce_max_sum(ms_e, float(step_pairs(tot_e)))
         _, h2d = allreduce_max_sum(0.0, float(tot_e["h2d"]))
         _, d2h = allreduce_max_sum(0.0, float(tot_e["d2h"]))

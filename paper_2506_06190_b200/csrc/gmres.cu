@@ -670,7 +670,7 @@ __device__ __forceinline__ TB zero_tb() {
 }
 
 template <typename TB, int RT, int NTH, int CL>
-__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NTH, 1)
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NTH, NTH <= 256 ? 2 : 1)
     arnoldi_fused_v2_kernel(const TB* __restrict__ Vb, size_t vstride, int64_t ldv, int64_t n, int64_t rpc,
                             const double2* __restrict__ Wj, double2* Vnext, TB* Vbnext,
                             uint64_t active, GivensArgs ga) {
@@ -1030,7 +1030,12 @@ nat_status gmres_batched(int nsys, int64_t n, int64_t ldv, const double2* b, dou
     const char* e = std::getenv("NAT_FUSED_NARROW");
     return !(e && e[0] == '0');
   }();
-  const int fused_kg = (fused_rt <= 2 && !fused_narrow) ? 3 : 2;  // update groups (NTH / 256)
+  // NAT_FUSED_NTH=256: one update group (the fp32-basis kernel), half the registers per CTA
+  static const bool fused_256 = [] {
+    const char* e = std::getenv("NAT_FUSED_NTH");
+    return e && std::atoi(e) == 256;
+  }();
+  const int fused_kg = (basis32 && fused_256 && fused_cl == 4) ? 1 : (fused_rt <= 2 && !fused_narrow) ? 3 : 2;
   const int fused_nth = fused_kg * kT;
   const size_t fsmem = std::max(fused_cap, sizeof(double2) * ((size_t)rpc * fused_kg + 4 * (size_t)mp1));
   using FusedFn = void (*)(const double2*, size_t, int64_t, int64_t, int64_t, const double2*, double2*, uint64_t,
@@ -1057,7 +1062,10 @@ nat_status gmres_batched(int nsys, int64_t n, int64_t ldv, const double2* b, dou
                             uint64_t, GivensArgs);
   FusedV2d v2d = nullptr;
   FusedV2f v2f = nullptr;
-  if (fused && fused_cl == 4 && fused_kg == 2) {
+  if (fused && fused_cl == 4 && fused_kg == 1 && b32) {
+    v2f = fused_rt == 1 ? arnoldi_fused_v2_kernel<float2, 1, 256, 4> : fused_rt == 2 ? arnoldi_fused_v2_kernel<float2, 2, 256, 4>
+        : fused_rt == 4 ? arnoldi_fused_v2_kernel<float2, 4, 256, 4> : arnoldi_fused_v2_kernel<float2, 8, 256, 4>;
+  } else if (fused && fused_cl == 4 && fused_kg == 2) {
     if (b32)
       v2f = fused_rt == 1 ? arnoldi_fused_v2_kernel<float2, 1, 512, 4> : fused_rt == 2 ? arnoldi_fused_v2_kernel<float2, 2, 512, 4>
           : fused_rt == 4 ? arnoldi_fused_v2_kernel<float2, 4, 512, 4> : arnoldi_fused_v2_kernel<float2, 8, 512, 4>;

@@ -5,7 +5,7 @@ through mesh preparation, the listener shell grid, BEM-MC with 64 wavenu
 the 64 fields to the listeners — the dataset step of P:166 — with one result file per
 geometry and a manifest written last.
 
-    python -m paper_2506_06190_b200.sweep --out DIR [--geometries 64] [--grid 64] [--workers 4]
+    python -m paper_2506_06190_b200.sweep --out DIR [--geometries 64] [--grid 64] [--workers 6]
     torchrun --nproc-per-node N -m paper_2506_06190_b200.sweep --out DIR     # geometries i mod N
 
 Files in DIR:
@@ -108,9 +108,10 @@ def run_geometry(nat, torch, gi, grid, bufs):
     return out, rec
 
 
-def run(out_dir, n_geo=64, grid=64, workers=4, rank=0, world=1, log=print):
+def run(out_dir, n_geo=64, grid=64, workers=6, rank=0, world=1, log=print):
     import torch
     from paper_2506_06190_b200 import nat
+    nat.sweep_tuning()
     nat.lib()
     os.makedirs(out_dir, exist_ok=True)
     mine = [gi for gi in range(n_geo) if gi % world == rank]
@@ -157,7 +158,7 @@ def main():
     ap.add_argument("--out", required=True)
     ap.add_argument("--geometries", type=int, default=64)
     ap.add_argument("--grid", type=int, default=64)
-    ap.add_argument("--workers", type=int, default=4)
+    ap.add_argument("--workers", type=int, default=6)
     a = ap.parse_args()
     rank, world = int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1"))
     import torch
