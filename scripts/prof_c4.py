@@ -10,6 +10,8 @@ sys.path.insert(0, ".")
 import nat_inputs as I
 from paper_2506_06190_b200 import nat
 
+nat.sweep_tuning()   # the bench's configuration
+
 gi = int(sys.argv[1]) if len(sys.argv) > 1 else 0
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 2
 m, g8, D = I.c4_geometry(gi)
