@@ -446,12 +446,17 @@ def run_nf(nat, torch, steps, batch=262144, peaks=None):
     return {"workload": f"NEXT-4 NAT neural field training step (hash grid 4 x 8..64, PE(6), 4 x 128 MLP, MSE, "
                         f"Adam), batch {batch} samples, 3 condition variables, 8 outputs, synthetic targets",
             "ms_per_step": ms, "samples_per_s": batch / (ms * 1e-3), "loss": float(loss.item()),
-            "gemm": {"bound": "tensor", "achieved": flops / sec / 1e12 if sec > 0 else None, "peak": peak,
-                     "unit": "TFLOP/s", "frac": (flops / sec / 1e12 / peak) if sec > 0 else None,
-                     "launches_per_step": nl, "flops_per_step": flops, "gemm_ms_per_step": 1e3 * sec,
-                     "peak_note": "MEASURED_PEAKS.json bf16_tflops (cuBLAS burst)",
-                     "hbm_view": {"bound": "hbm", "bytes_per_step": gemm_bytes,
-                                  "achieved": gemm_bytes / sec / 1e9 if sec > 0 else None, "peak": hbm,
-                                  "unit": "GB/s", "frac": (gemm_bytes / sec / 1e9 / hbm) if sec > 0 else None,
-                                  "note": "K <= 128: each product moves ~2 bytes per flop x 1/64 .. 1/128; the "
-                                          "activations' HBM traffic, not the tensor pipe, bounds these layers"}}}
+            "gemm": {"bound": "hbm", "bytes_per_step": gemm_bytes,
+                     "achieved": gemm_bytes / sec / 1e9 if sec > 0 else None, "peak": hbm, "unit": "GB/s",
+                     "frac": (gemm_bytes / sec / 1e9 / hbm) if sec > 0 else None,
+                     "launches_per_step": nl, "gemm_ms_per_step": 1e3 * sec,
+                     "arithmetic_intensity_flop_per_byte": flops / gemm_bytes,
+                     "ridge_flop_per_byte": peak * 1e12 / (hbm * 1e9),
+                     "peak_note": "MEASURED_PEAKS.json hbm_gbs; K <= 128 puts every layer product below the "
+                                  "tensor/HBM ridge point, so the activations' traffic (read once, written once) "
+                                  "is the binding roofline",
+                     "tensor_view": {"bound": "tensor", "achieved": flops / sec / 1e12 if sec > 0 else None,
+                                     "peak": peak, "unit": "TFLOP/s",
+                                     "frac": (flops / sec / 1e12 / peak) if sec > 0 else None,
+                                     "flops_per_step": flops,
+                                     "peak_note": "MEASURED_PEAKS.json bf16_tflops (cuBLAS burst)"}}}

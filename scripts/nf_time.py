@@ -14,5 +14,6 @@ pk = json.load(open("MEASURED_PEAKS.json")) if os.path.exists("MEASURED_PEAKS.js
 for _ in range(2):
     r = S.run_nf(nat, torch, 10, peaks=pk)
     g = r["gemm"]
-    print(f"step {r['ms_per_step']:.3f} ms, gemm {g['gemm_ms_per_step']:.3f} ms, {g['achieved']:.1f} TFLOP/s "
-          f"({g['frac']:.3f}), hbm view {g['hbm_view']['frac']:.3f}, loss {r['loss']:.4f}", flush=True)
+    print(f"step {r['ms_per_step']:.3f} ms, gemm {g['gemm_ms_per_step']:.3f} ms, {g['achieved']:.0f} GB/s "
+          f"({g['frac']:.3f} of HBM), tensor view {g['tensor_view']['achieved']:.1f} TFLOP/s, loss {r['loss']:.4f}",
+          flush=True)
