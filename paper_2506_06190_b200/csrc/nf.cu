@@ -191,6 +191,13 @@ __device__ __forceinline__ void gemm_epilogue(const GemmArgs& g, uint32_t tmem, 
   const bool epi_warp = BN >= 64 || ch == 0;
 #pragma unroll 1
   for (int n0 = ch * kHalf; epi_warp && n0 < (ch + 1) * kHalf; n0 += 32) {
+    constexpr int WH = BN < 32 ? BN : 32;
+    uint4 hv[WH / 8];  // the ReLU mask's row slice, loaded ahead of the TMEM read (latency overlap)
+    if (g.epi == kEpiMaskBf16) {
+#pragma unroll
+      for (int q = 0; q < WH / 8; ++q)
+        hv[q] = row_ok ? *reinterpret_cast<const uint4*>(g.H + m * g.ldh + n0 + 8 * q) : make_uint4(0, 0, 0, 0);
+    }
     uint32_t v[32];
     const uint32_t taddr = tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)n0;
     if constexpr (BN >= 32) {
@@ -224,8 +231,7 @@ __device__ __forceinline__ void gemm_epilogue(const GemmArgs& g, uint32_t tmem, 
       } else {
 #pragma unroll
         for (int q = 0; q < W; q += 8) {
-          const uint4 hv = row_ok ? *reinterpret_cast<const uint4*>(g.H + m * g.ldh + n0 + q) : make_uint4(0, 0, 0, 0);
-          const bf16* hb = reinterpret_cast<const bf16*>(&hv);
+          const bf16* hb = reinterpret_cast<const bf16*>(&hv[q / 8]);
 #pragma unroll
           for (int e = 0; e < 8; ++e) f[q + e] = (row_ok && __bfloat162float(hb[e]) > 0.f) ? f[q + e] : 0.f;
         }
