@@ -324,6 +324,14 @@ nat_status nat_mc_check_coincident(int64_t M, const double* samples, int64_t* pa
                                    void* ws, size_t ws_bytes, nat_stream_t stream); /* (sync) */
 
 size_t nat_mc_workspace(nat_prec prec, int64_t M, int n_sys, int max_iter);
+/* Solve groups of nat_mc_surface_pressure (process-wide; default NAT_MC_GROUPS or 1): the
+ * systems of each batch of <= 64 are split into `groups` contiguous groups whose GMRES
+ * iterations run concurrently on their own streams from persistent library threads, so one
+ * group's Krylov steps overlap another's operator application.  Each system's iteration is
+ * the same arithmetic in any group (results agree to the launch shapes' rounding; the tests
+ * compare group counts 1, 2, 4).  nat_mc_workspace covers every group count.  groups in
+ * [1, 4], else NAT_ERR_INVALID_ARG. */
+nat_status nat_mc_set_groups(int groups);
 nat_status nat_mc_surface_pressure(const nat_mesh* mesh, const nat_geom* geom, int n_sys,
                                    const double* k /* [host] */, const void* g_tri, const nat_mc_opts* opts,
                                    nat_prec prec, double tol, int max_iter, double* samples_out,

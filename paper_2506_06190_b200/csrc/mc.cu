@@ -10,7 +10,16 @@
 // (TMA-staged source tiles, self pair excluded exactly).
 #include <chrono>
 #include <algorithm>
+#include <atomic>
 #include <cmath>
+#include <condition_variable>
+#include <cstdlib>
+#include <functional>
+#include <future>
+#include <map>
+#include <mutex>
+#include <queue>
+#include <thread>
 #include <vector>
 
 #include "krylov.cuh"
@@ -639,17 +648,99 @@ extern "C" nat_status nat_mc_apply_rows(nat_prec prec, int64_t M, const double* 
 }
 
 namespace {
+constexpr int kMaxGroups = 4;
+struct McGroupWs {   // one solve group: its Krylov state, operator workspace and compaction buffers
+  nat::KrylovWs kw;
+  void* rad;
+  size_t rad_bytes;
+  double2* tin;   // compacted operator input / output of the systems still iterating
+  double2* tout;
+};
 struct McWs {
   unsigned long long* best;
   double2* gs;
   double2* b;
-  nat::KrylovWs kw;
-  void* rad;
-  size_t rad_bytes;
   NearPairs np;
-  double2* tin;   // compacted operator input / output of the systems still iterating
-  double2* tout;
+  McGroupWs grp[kMaxGroups];
 };
+
+// Solve groups (NAT_MC_GROUPS or nat_mc_set_groups; default 1): the systems of a batch are
+// split into G contiguous groups whose GMRES iterations run concurrently on G streams (one
+// host thread each), so one group's latency-bound Krylov kernels overlap another group's
+// operator application inside a single call.
+std::atomic<int> g_mc_groups{0};
+int mc_groups() {
+  int v = g_mc_groups.load();
+  if (v <= 0) {
+    const char* e = std::getenv("NAT_MC_GROUPS");
+    v = e ? std::max(1, std::min(kMaxGroups, std::atoi(e))) : 1;
+    g_mc_groups.store(v);
+  }
+  return v;
+}
+
+// Persistent helper threads for the groups: libnat keeps per-thread pinned rings and events
+// (gmres.cu HostSync), so the threads that run solves must outlive the calls.
+class GroupPool {
+ public:
+  static GroupPool& get() {
+    static GroupPool* p = new GroupPool();  // never destroyed: detached workers
+    return *p;
+  }
+  std::future<nat_status> submit(std::function<nat_status()> f) {
+    auto task = std::make_shared<std::packaged_task<nat_status()>>(std::move(f));
+    std::future<nat_status> fut = task->get_future();
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      q_.push([task] { (*task)(); });
+      while ((int)n_threads_ < (int)q_.size() + busy_ && n_threads_ < kMaxGroups) {
+        std::thread([this] { loop(); }).detach();
+        ++n_threads_;
+      }
+    }
+    cv_.notify_one();
+    return fut;
+  }
+
+ private:
+  void loop() {
+    for (;;) {
+      std::function<void()> job;
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [this] { return !q_.empty(); });
+        job = std::move(q_.front());
+        q_.pop();
+        ++busy_;
+      }
+      job();
+      std::lock_guard<std::mutex> lk(mu_);
+      --busy_;
+    }
+  }
+  std::mutex mu_;
+  std::condition_variable cv_;
+  std::queue<std::function<void()>> q_;
+  int n_threads_ = 0, busy_ = 0;
+};
+
+// per-thread, per-device stream and event of a solve group
+struct GroupStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t ev = nullptr;
+};
+GroupStream* group_stream() {
+  thread_local std::map<int, GroupStream> per_dev;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  GroupStream& g = per_dev[dev];
+  if (!g.s) {
+    if (cudaStreamCreateWithFlags(&g.s, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&g.ev, cudaEventDisableTiming) != cudaSuccess)
+      return nullptr;
+  }
+  return &g;
+}
 
 struct RowIdx {
   int idx[64];
@@ -682,18 +773,29 @@ __global__ void coincident_near_kernel(int64_t M, const double* __restrict__ smp
   }
 }
 
-size_t mc_carve(nat::Carver& c, McWs* w, nat_prec prec, int64_t M, int n_sys, int max_iter) {
+int group_size(int nb, int groups) { return (nb + groups - 1) / groups; }
+
+size_t mc_carve(nat::Carver& c, McWs* w, nat_prec prec, int64_t M, int n_sys, int max_iter, int groups) {
   const int nb = n_sys < 64 ? n_sys : 64;
-  McWs t;
+  const int G = std::max(1, std::min(groups, nb));
+  const int nbg = group_size(nb, G);
+  McWs t{};
   t.best = c.take<unsigned long long>(1);
   t.gs = c.take<double2>((size_t)nb * M);
   t.b = c.take<double2>((size_t)nb * M);
-  nat::krylov_workspace(nb, M, M, max_iter, c, &t.kw);
-  t.rad_bytes = nat::radiate_ws_bytes_upto(prec, M, nb, M);  // the operator shrinks to the active systems
-  t.rad = c.take<char>(t.rad_bytes);
   carve_near(c, &t.np, M);
-  t.tin = c.take<double2>((size_t)nb * M);
-  t.tout = c.take<double2>((size_t)nb * M);
+  for (int g = 0; g < G; ++g) {
+    McGroupWs& q = t.grp[g];
+    nat::krylov_workspace(nbg, M, M, max_iter, c, &q.kw);
+    q.rad_bytes = nat::radiate_ws_bytes_upto(prec, M, nb, M);  // RHS (all nb systems) and the group's operator
+    q.rad = g == 0 ? c.take<char>(q.rad_bytes) : nullptr;
+    if (g > 0) {
+      q.rad_bytes = nat::radiate_ws_bytes_upto(prec, M, nbg, M);
+      q.rad = c.take<char>(q.rad_bytes);
+    }
+    q.tin = c.take<double2>((size_t)nbg * M);
+    q.tout = c.take<double2>((size_t)nbg * M);
+  }
   if (w) *w = t;
   return c.bytes();
 }
@@ -701,8 +803,18 @@ size_t mc_carve(nat::Carver& c, McWs* w, nat_prec prec, int64_t M, int n_sys, in
 
 extern "C" size_t nat_mc_workspace(nat_prec prec, int64_t M, int n_sys, int max_iter) {
   if (max_iter <= 0) max_iter = 200;
-  nat::Carver c(nullptr);
-  return mc_carve(c, nullptr, prec, M, n_sys, max_iter);
+  size_t b = 0;
+  for (int g = 1; g <= kMaxGroups; ++g) {  // any group count the process may select
+    nat::Carver c(nullptr);
+    b = std::max(b, mc_carve(c, nullptr, prec, M, n_sys, max_iter, g));
+  }
+  return b;
+}
+
+extern "C" nat_status nat_mc_set_groups(int groups) {
+  NAT_REQUIRE(groups >= 1 && groups <= kMaxGroups, "groups = %d must be in [1, %d]", groups, kMaxGroups);
+  g_mc_groups.store(groups);
+  return NAT_OK;
 }
 
 extern "C" nat_status nat_mc_surface_pressure(const nat_mesh* mesh, const nat_geom* geom, int n_sys,
@@ -729,7 +841,8 @@ extern "C" nat_status nat_mc_surface_pressure(const nat_mesh* mesh, const nat_ge
   NAT_REQUIRE_DEV(ws);
   nat::Carver c(ws);
   McWs w;
-  size_t need = mc_carve(c, &w, prec, M, n_sys, max_iter);
+  const int groups = mc_groups();
+  size_t need = mc_carve(c, &w, prec, M, n_sys, max_iter, groups);
   if (ws_bytes < need) return nat::fail(NAT_ERR_WORKSPACE, "workspace %zu < %zu", ws_bytes, need);
   cudaStream_t s = (cudaStream_t)stream;
   // a8: samples (or the caller's set, e.g. a host Poisson-disk set, enters unchanged)
@@ -777,47 +890,103 @@ extern "C" nat_status nat_mc_surface_pressure(const nat_mesh* mesh, const nat_ge
     gather_g_kernel<<<dim3((unsigned)((M + 255) / 256), nb), 256, 0, s>>>(
         nb, M, mesh->n_tri, (const double2*)g_tri + (size_t)s0 * mesh->n_tri, sample_tri_out, w.gs);
     NAT_LAUNCH_CHECK();
-    st = mc_rhs_impl(prec, M, samples_out, nb, k + s0, w.gs, wgt, eps, w.b, w.rad, w.rad_bytes, cen, w.np, s);
+    st = mc_rhs_impl(prec, M, samples_out, nb, k + s0, w.gs, wgt, eps, w.b, w.grp[0].rad, w.grp[0].rad_bytes, cen,
+                     w.np, s);
     if (st != NAT_OK) return deferred(st);
-    const uint64_t all = nb == 64 ? ~0ull : ((1ull << nb) - 1);
-    auto op = [&](const double2* in, double2* out, uint64_t active, const unsigned long long* dmask,
-                  cudaStream_t ss) -> nat_status {
-      if ((active & all) == all)
-        return mc_apply_impl(prec, M, samples_out, nb, k + s0, in, wgt, out, w.rad, w.rad_bytes, cen, w.np, ss,
-                             dmask);
-      // only the systems still iterating: gather them, apply, scatter back
-      RowIdx ix{};
-      double kc[64];
-      int na = 0;
-      for (int q = 0; q < nb; ++q)
-        if ((active >> q) & 1ull) {
-          ix.idx[na] = q;
-          kc[na++] = k[s0 + q];
-        }
-      if (na == 0) return NAT_OK;
-      const dim3 g2((unsigned)((M + 255) / 256), na);
-      copy_rows_kernel<<<g2, 256, 0, ss>>>(ix, M, in, w.tin, true);
-      nat_status r = mc_apply_impl(prec, M, samples_out, na, kc, w.tin, wgt, w.tout, w.rad, w.rad_bytes, cen,
-                                   w.np, ss, dmask);
-      if (r != NAT_OK) return r;
-      copy_rows_kernel<<<g2, 256, 0, ss>>>(ix, M, w.tout, out, false);
-      NAT_LAUNCH_CHECK();
-      return NAT_OK;
+    const int G = std::max(1, std::min(groups, nb));
+    const int nbg = group_size(nb, G);
+    // group g: systems [g0, g0 + n) of the batch, its own Krylov state and operator workspace
+    auto solve_group = [&, s0](int g, cudaStream_t gs_, std::vector<nat::KrylovResult>& res, double& t_op) -> nat_status {
+      const int g0 = g * nbg, n = std::min(nbg, nb - g0);
+      McGroupWs& q = w.grp[g];
+      const double* kg = k + s0 + g0;
+      const uint64_t all = n == 64 ? ~0ull : ((1ull << n) - 1);
+      auto op = [&, n, kg, all](const double2* in, double2* out, uint64_t active, const unsigned long long* dmask,
+                                cudaStream_t ss) -> nat_status {
+        if ((active & all) == all)
+          return mc_apply_impl(prec, M, samples_out, n, kg, in, wgt, out, q.rad, q.rad_bytes, cen, w.np, ss, dmask);
+        // only the systems still iterating: gather them, apply, scatter back
+        RowIdx ix{};
+        double kc[64];
+        int na = 0;
+        for (int r = 0; r < n; ++r)
+          if ((active >> r) & 1ull) {
+            ix.idx[na] = r;
+            kc[na++] = kg[r];
+          }
+        if (na == 0) return NAT_OK;
+        const dim3 g2((unsigned)((M + 255) / 256), na);
+        copy_rows_kernel<<<g2, 256, 0, ss>>>(ix, M, in, q.tin, true);
+        nat_status r = mc_apply_impl(prec, M, samples_out, na, kc, q.tin, wgt, q.tout, q.rad, q.rad_bytes, cen, w.np,
+                                     ss, dmask);
+        if (r != NAT_OK) return r;
+        copy_rows_kernel<<<g2, 256, 0, ss>>>(ix, M, q.tout, out, false);
+        NAT_LAUNCH_CHECK();
+        return NAT_OK;
+      };
+      return nat::gmres_batched(n, M, M, w.b + (size_t)g0 * M, (double2*)p_out + (size_t)(s0 + g0) * M, op, tol,
+                                max_iter, q.kw, res, gs_, info ? &t_op : nullptr, basis32(prec));
     };
-    std::vector<nat::KrylovResult> res;
-    double t_op = 0;
-    st = nat::gmres_batched(nb, M, M, w.b, (double2*)p_out + (size_t)s0 * M, op, tol, max_iter, w.kw, res, s,
-                            info ? &t_op : nullptr, basis32(prec));
-    if (st != NAT_OK) return deferred(st);
-    for (int q = 0; q < nb; ++q) all_conv = all_conv && res[q].converged;
-    if (info)
-      for (int q = 0; q < nb; ++q) {
-        info[s0 + q].iters = res[q].iters;
-        info[s0 + q].converged = res[q].converged;
-        info[s0 + q].rel_residual = res[q].rel_residual;
-        info[s0 + q].t_matvec_s = t_op;
-        info[s0 + q].t_comm_s = 0;
+    std::vector<std::vector<nat::KrylovResult>> res(G);
+    std::vector<double> t_op(G, 0.0);
+    if (G == 1) {
+      st = solve_group(0, s, res[0], t_op[0]);
+      if (st != NAT_OK) return deferred(st);
+    } else {
+      // fork: every group stream waits for the right-hand side; join: s waits for every group
+      GroupStream* mine = group_stream();
+      if (!mine) return nat::fail(NAT_ERR_CUDA, "group stream: %s", cudaGetErrorString(cudaGetLastError()));
+      NAT_CUDA_TRY(cudaEventRecord(mine->ev, s));
+      cudaEvent_t fork = mine->ev;
+      int dev = 0;
+      NAT_CUDA_TRY(cudaGetDevice(&dev));
+      std::vector<cudaEvent_t> joins(G, nullptr);
+      auto run = [&, fork, dev](int g) -> nat_status {
+        if (cudaSetDevice(dev) != cudaSuccess) return nat::fail(NAT_ERR_CUDA, "cudaSetDevice");
+        GroupStream* gsx = group_stream();
+        if (!gsx) return nat::fail(NAT_ERR_CUDA, "group stream");
+        if (cudaStreamWaitEvent(gsx->s, fork, 0) != cudaSuccess) return nat::fail(NAT_ERR_CUDA, "stream wait");
+        nat_status r = solve_group(g, gsx->s, res[g], t_op[g]);
+        if (cudaEventRecord(gsx->ev, gsx->s) != cudaSuccess) return nat::fail(NAT_ERR_CUDA, "event record");
+        joins[g] = gsx->ev;
+        return r;
+      };
+      std::vector<std::future<nat_status>> fut;
+      for (int g = 1; g < G; ++g) fut.push_back(GroupPool::get().submit([run, g] { return run(g); }));
+      // group 0 on this thread, on a stream of its own (the fork event above stays on s)
+      GroupStream* g0s = group_stream();
+      nat_status st0 = NAT_OK;
+      if (cudaStreamWaitEvent(g0s->s, fork, 0) != cudaSuccess) st0 = nat::fail(NAT_ERR_CUDA, "stream wait");
+      if (st0 == NAT_OK) st0 = solve_group(0, g0s->s, res[0], t_op[0]);
+      cudaEvent_t j0 = nullptr;
+      if (cudaEventCreateWithFlags(&j0, cudaEventDisableTiming) == cudaSuccess) {
+        cudaEventRecord(j0, g0s->s);
+        cudaStreamWaitEvent(s, j0, 0);
+        cudaEventDestroy(j0);
+      } else {
+        cudaStreamSynchronize(g0s->s);
       }
+      nat_status stg = st0;
+      for (int g = 1; g < G; ++g) {
+        nat_status r = fut[g - 1].get();
+        if (joins[g]) NAT_CUDA_TRY(cudaStreamWaitEvent(s, joins[g], 0));
+        if (stg == NAT_OK && r != NAT_OK) stg = r;
+      }
+      if (stg != NAT_OK) return deferred(stg);
+    }
+    for (int g = 0; g < G; ++g) {
+      const int g0 = g * nbg, n = std::min(nbg, nb - g0);
+      for (int q = 0; q < n; ++q) {
+        all_conv = all_conv && res[g][q].converged;
+        if (info) {
+          info[s0 + g0 + q].iters = res[g][q].iters;
+          info[s0 + g0 + q].converged = res[g][q].converged;
+          info[s0 + g0 + q].rel_residual = res[g][q].rel_residual;
+          info[s0 + g0 + q].t_matvec_s = t_op[g];
+          info[s0 + g0 + q].t_comm_s = 0;
+        }
+      }
+    }
   }
   st = deferred(NAT_OK);
   if (st != NAT_OK) return st;

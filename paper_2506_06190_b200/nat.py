@@ -115,6 +115,7 @@ _SIGS = {
     "nat_bem_solve_workspace": (_SZ, [C.c_int, _I64, _I64, C.c_int]),
     "nat_bem_solve": (C.c_int, [_P, C.c_int, _I64, _I64, _I64, _P, _I64, _P, _P, _D, C.c_int,
                                 _P, _SZ, C.POINTER(_SolveInfo), _P]),
+    "nat_mc_set_groups": (C.c_int, [C.c_int]),
     "nat_mc_sample": (C.c_int, [C.POINTER(_Mesh), C.POINTER(_Geom), _I64, C.c_uint64,
                                 C.c_uint64, _P, _P, _P]),
     "nat_mc_op_workspace": (_SZ, [C.c_int, _I64, C.c_int]),
@@ -187,6 +188,7 @@ SWEEP_WORKERS = 6
 def sweep_tuning():
     os.environ.setdefault("NAT_FUSED_NTH", "256")
     os.environ.setdefault("NAT_FUSED_SMEM_KB", "0")
+    os.environ.setdefault("NAT_MC_GROUPS", "1")   # the workers already overlap whole geometries
 
 
 def exported_symbols():
@@ -834,6 +836,11 @@ def nat_bem_mf_solve(op: BemMf, b_local: torch.Tensor, comm: Optional["Comm"] = 
 # diagnostics: per-kernel CUDA-event timer (nat_kernel_timer_*)
 # ------------------------------------------------------------------------------------
 KTIMER_MC_OP, KTIMER_MC_RHS, KTIMER_RADIATE, KTIMER_FAR, KTIMER_NF_GEMM = 0, 1, 2, 3, 4
+
+
+def nat_mc_set_groups(groups: int):
+    """Process-wide solve groups of nat_mc_surface_pressure (include/nat.h)."""
+    _check(lib().nat_mc_set_groups(int(groups)))
 
 
 def nat_kernel_timer_enable(on: bool = True):

@@ -238,3 +238,29 @@ def test_surface_pressure_caller_eps(prec):
         assert info[s]["converged"] == 1
         assert rel_l2(to_np(p)[s], p_ref[s]) <= TOL[prec]
         assert rel_l2(p_def[s], p_ref[s]) > 100 * TOL[prec]   # the radius changes the solution
+
+
+def test_solve_groups_agree():
+    """nat_mc_set_groups: the batch split into 1, 2 or 4 concurrently iterating groups
+    gives the same solution (same arithmetic per system; launch shapes may change the
+    rounding) and the same iteration counts within one."""
+    nat = _nat()
+    m = I.bowl(32, 8, 2)
+    geo, mesh, gg = _case(m)
+    M, seed = 700, 3
+    ks = list(np.linspace(0.5, 6.0, 7))
+    g_tri = torch.from_numpy(I.neumann_harmonics(m, 7)).cuda()
+    out = {}
+    try:
+        for G in (1, 2, 4):
+            nat.nat_mc_set_groups(G)
+            _, _, p, info = nat.nat_mc_surface_pressure(mesh, gg, ks, g_tri, M, seed, prec="fp32", tol=1e-6)
+            out[G] = (to_np(p), [i["iters"] for i in info], [i["converged"] for i in info])
+    finally:
+        nat.nat_mc_set_groups(1)
+    for G in (2, 4):
+        assert rel_l2(out[G][0], out[1][0]) <= 1e-6
+        assert all(abs(a - b) <= 1 for a, b in zip(out[G][1], out[1][1]))
+        assert all(out[G][2])
+    with pytest.raises(nat.NatError):
+        nat.nat_mc_set_groups(5)
