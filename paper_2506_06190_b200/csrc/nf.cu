@@ -856,8 +856,209 @@ nat_status check_cfg(const nat_nf_config* cfg) {
     if (_e != cudaSuccess) return nat::fail(NAT_ERR_CUDA, "%s: %s", #expr, cudaGetErrorString(_e)); \
   } while (0)
 
+// =====================================================================================
+// Fused forward: all five layer products of a 128-sample tile in one persistent CTA.  The
+// five bf16 weight matrices stay in shared memory (core-matrix K-major layout, 116 KB); a
+// tile's activations never leave the SM between layers: each epilogue (bias + ReLU + bf16)
+// writes its output both to global memory (H_q, kept for the backward pass) and into the
+// next layer's A operand in shared memory; the next tile's input rows load (cp.async) while
+// the current tile runs its chain.  One TMEM accumulator of 128 columns.
+// =====================================================================================
+struct FwdArgs {
+  const bf16* X;        // [n][64]
+  const bf16* Wb;       // [5][128][128] slots: W_q [out_pad][in]
+  const float* bias[kNLayers];
+  int n_bias[kNLayers];
+  bf16* H[kNHidden];    // [n][128]
+  float* Y;             // [n][16]
+  int n_out;
+  int64_t n;
+};
+constexpr uint32_t kFwdW0 = 128 * 64 * 2, kFwdWh = 128 * 128 * 2, kFwdW4 = 16 * 128 * 2;
+constexpr uint32_t kFwdX = kGM * 64 * 2, kFwdH = kGM * 128 * 2;
+constexpr uint32_t kFwdSmem = kFwdW0 + 3 * kFwdWh + kFwdW4 + 2 * kFwdX + 2 * kFwdH;
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]),
+        "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+        "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__global__ void __launch_bounds__(kGT, 1) nf_forward_fused_kernel(FwdArgs a, int64_t n_tiles) {
+  extern __shared__ __align__(1024) char fsm[];
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ uint32_t tmem_base;
+  __shared__ float bias_s[kNLayers][kHidden];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int wq = warp & 3, ch = warp >> 2;
+  char* sW0 = fsm;
+  char* sWh = sW0 + kFwdW0;                 // W1..W3
+  char* sW4 = sWh + 3 * kFwdWh;
+  char* sX[2] = {sW4 + kFwdW4, sW4 + kFwdW4 + kFwdX};
+  char* sH[2] = {sX[1] + kFwdX, sX[1] + kFwdX + kFwdH};
+  const int64_t my_n = n_tiles > blockIdx.x ? (n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  auto stage_x = [&](int64_t i) {
+    const int64_t m0 = (blockIdx.x + i * gridDim.x) * (int64_t)kGM;
+    stage_operand<kGM, false>(a.X, kInPad, a.n, kInPad, m0, 0, sX[i & 1]);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  if (tid == 0) {
+    nat::mbar_init(&bar, 1);
+    nat::fence_mbar_init();
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(nat::smem_u32(&tmem_base)),
+                 "r"(128));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (my_n > 0) {  // weights (group 0 with tile 0's rows)
+    stage_operand<128, false>(a.Wb, kInPad, 128, kInPad, 0, 0, sW0);
+    for (int q = 1; q <= 3; ++q)
+      for (int c = 0; c < 2; ++c)
+        stage_operand<128, false>(a.Wb + (size_t)q * kHidden * kHidden, kHidden, 128, kHidden, 0, c * kBK,
+                                  sWh + (size_t)(q - 1) * kFwdWh + c * (kFwdWh / 2));
+    for (int c = 0; c < 2; ++c)
+      stage_operand<16, false>(a.Wb + (size_t)kNHidden * kHidden * kHidden, kHidden, 16, kHidden, 0, c * kBK,
+                               sW4 + c * (kFwdW4 / 2));
+    stage_x(0);
+  }
+  for (int q = 0; q < kNLayers; ++q)
+    for (int c = tid; c < kHidden; c += kGT) bias_s[q][c] = c < a.n_bias[q] ? a.bias[q][c] : 0.f;
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = tmem_base;
+  uint32_t phase = 0;
+  // one layer product: acc = A [128 x K] * W^T, K in chunks of 64 (A and W K-major core layout)
+  auto mma = [&](const char* A, uint32_t a_chunk, const char* W, uint32_t w_chunk, int nchunk, int N) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (tid == 0) {
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const uint32_t a0 = nat::smem_u32(A), w0 = nat::smem_u32(W);
+      const uint32_t idesc = N == 128 ? idesc_bf16(kGM, 128, false, false) : idesc_bf16(kGM, 16, false, false);
+      for (int c = 0; c < nchunk; ++c)
+#pragma unroll
+        for (int kk = 0; kk < kBK / 16; ++kk)
+          mma_bf16(tmem, sdesc(a0 + c * a_chunk + kk * 256, 128, (kBK / 8) * 128),
+                   sdesc(w0 + c * w_chunk + kk * 256, 128, (kBK / 8) * 128), idesc, (c > 0 || kk > 0) ? 1u : 0u);
+      mma_commit(&bar);
+    }
+    nat::mbar_wait(&bar, phase);
+    phase ^= 1u;
+    asm volatile("tcgen05.fence::after_thread_sync;");
+  };
+  for (int64_t i = 0; i < my_n; ++i) {
+    const int64_t m0 = (blockIdx.x + i * gridDim.x) * (int64_t)kGM;
+    if (i + 1 < my_n) {
+      stage_x(i + 1);  // the other buffer: tile i-1's first product read it long ago
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    const int64_t m = m0 + wq * 32 + lane;
+    const bool row_ok = m < a.n;
+    for (int q = 0; q < kNLayers; ++q) {
+      if (q == 0) mma(sX[i & 1], kFwdX, sW0, kFwdW0, 1, 128);
+      else if (q < kNHidden) mma(sH[(q - 1) & 1], kFwdH / 2, sWh + (size_t)(q - 1) * kFwdWh, kFwdWh / 2, 2, 128);
+      else mma(sH[(q - 1) & 1], kFwdH / 2, sW4, kFwdW4 / 2, 2, 16);
+      if (q < kNHidden) {
+        // warp (wq, ch): rows 32 wq + lane, columns [64 ch, 64 ch + 64)
+        char* dst = sH[q & 1];
+#pragma unroll 1
+        for (int n0 = ch * 64; n0 < ch * 64 + 64; n0 += 32) {
+          uint32_t v[32];
+          tmem_ld32(tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)n0, v);
+          float f[32];
+#pragma unroll
+          for (int e = 0; e < 32; ++e) f[e] = fmaxf(__uint_as_float(v[e]) + bias_s[q][n0 + e], 0.f);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            uint4 o;
+            __nv_bfloat162* ob = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) ob[e] = __floats2bfloat162_rn(f[8 * u + 2 * e], f[8 * u + 2 * e + 1]);
+            if (row_ok) *reinterpret_cast<uint4*>(a.H[q] + m * kHidden + n0 + 8 * u) = o;
+            // next layer's A operand: row r = 32 wq + lane, K unit kc = (n0 + 8u) / 8 (chunk of 64)
+            const int r = wq * 32 + lane, kunit = (n0 + 8 * u) / 8;
+            const int chunk = kunit / 8, kc = kunit % 8;
+            *reinterpret_cast<uint4*>(dst + (size_t)chunk * (kFwdH / 2) + ((r / 8) * 8 + kc) * 128 + (r % 8) * 16) =
+                row_ok ? o : make_uint4(0, 0, 0, 0);
+          }
+        }
+      } else if (ch == 0) {  // output layer: 16 columns, fp32
+        uint32_t v[16];
+        tmem_ld16(tmem + ((uint32_t)(wq * 32) << 16), v);
+        if (row_ok) {
+          float* y = a.Y + m * kOutPad;
+#pragma unroll
+          for (int e = 0; e < 16; e += 4)
+            *reinterpret_cast<float4*>(y + e) =
+                make_float4(__uint_as_float(v[e]) + bias_s[q][e], __uint_as_float(v[e + 1]) + bias_s[q][e + 1],
+                            __uint_as_float(v[e + 2]) + bias_s[q][e + 2], __uint_as_float(v[e + 3]) + bias_s[q][e + 3]);
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(128));
+}
+
+cudaError_t launch_forward_fused(const FwdArgs& fa, cudaStream_t s) {
+  auto k = nf_forward_fused_kernel;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFwdSmem);
+  if (e != cudaSuccess) return e;
+  const int64_t tiles = (fa.n + kGM - 1) / kGM;
+  const int64_t grid = std::min<int64_t>(tiles, (int64_t)nat::device_sm_count());
+  const bool timed = nat::ktimer_on();
+  if (timed) nat::ktimer_begin(nat::kTimerNfGemm, s);
+  k<<<(unsigned)grid, kGT, kFwdSmem, s>>>(fa, tiles);
+  e = cudaGetLastError();
+  if (timed) {  // flops of the five products
+    const double n = (double)fa.n;
+    nat::ktimer_end(nat::kTimerNfGemm, s,
+                    2.0 * n * (kHidden * (double)kInPad + 3.0 * kHidden * kHidden + (double)kOutPad * kHidden), nullptr);
+  }
+  return e;
+}
+
 // forward through the 5 layers (weights already cast); H[q] stored for the backward pass
 nat_status forward_impl(const Layout& L, int64_t n, const float* params, NfWs& w, cudaStream_t s) {
+  static const bool fused = [] {  // NAT_NF_FUSED=0: the five layer products as separate launches (A/B)
+    const char* e = std::getenv("NAT_NF_FUSED");
+    return !(e && e[0] == '0');
+  }();
+  if (fused) {
+    FwdArgs fa{};
+    fa.X = w.X;
+    fa.Wb = w.Wb;
+    for (int q = 0; q < kNLayers; ++q) {
+      fa.bias[q] = params + L.b[q];
+      fa.n_bias[q] = L.out[q];
+    }
+    for (int q = 0; q < kNHidden; ++q) fa.H[q] = w.H[q];
+    fa.Y = w.Y;
+    fa.n_out = L.out[kNHidden];
+    fa.n = n;
+    NF_LAUNCH(launch_forward_fused(fa, s));
+    return NAT_OK;
+  }
   const bf16* act = w.X;
   for (int q = 0; q < kNLayers; ++q) {
     GemmArgs g{};
