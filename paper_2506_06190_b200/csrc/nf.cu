@@ -876,7 +876,7 @@ struct FwdArgs {
 };
 constexpr uint32_t kFwdW0 = 128 * 64 * 2, kFwdWh = 128 * 128 * 2, kFwdW4 = 16 * 128 * 2;
 constexpr uint32_t kFwdX = kGM * 64 * 2, kFwdH = kGM * 128 * 2;
-constexpr uint32_t kFwdSmem = kFwdW0 + 3 * kFwdWh + kFwdW4 + 2 * kFwdX + 2 * kFwdH;
+constexpr uint32_t kFwdSmem = kFwdW0 + 3 * kFwdWh + kFwdW4 + 2 * kFwdX + 2 * kFwdH;  // two warpgroups' buffers
 
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
   asm volatile(
@@ -898,34 +898,53 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// Two warpgroups, two tiles in flight: warpgroup g (warps 4g .. 4g + 3, one per TMEM lane
+// quarter) runs the layer chain of every other tile of the CTA with its own TMEM
+// accumulator (columns 128 g ..), its own input and activation buffers, its own mbarrier and
+// named barrier, so one group's epilogue overlaps the other group's tensor-core products.
+// A layer's epilogue overwrites the group's activation buffer in place: the product that
+// read it has completed (mbarrier) before the epilogue starts.
+__device__ __forceinline__ void wg_sync(int g) {
+  asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(128) : "memory");
+}
+
 __global__ void __launch_bounds__(kGT, 1) nf_forward_fused_kernel(FwdArgs a, int64_t n_tiles) {
   extern __shared__ __align__(1024) char fsm[];
-  __shared__ __align__(8) uint64_t bar;
+  __shared__ __align__(8) uint64_t bars[2];
   __shared__ uint32_t tmem_base;
   __shared__ float bias_s[kNLayers][kHidden];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int wq = warp & 3, ch = warp >> 2;
+  const int wg = warp >> 2, wq = warp & 3, gt = tid & 127;  // warpgroup, TMEM lane quarter, thread in group
   char* sW0 = fsm;
   char* sWh = sW0 + kFwdW0;                 // W1..W3
   char* sW4 = sWh + 3 * kFwdWh;
-  char* sX[2] = {sW4 + kFwdW4, sW4 + kFwdW4 + kFwdX};
-  char* sH[2] = {sX[1] + kFwdX, sX[1] + kFwdX + kFwdH};
+  char* sX = sW4 + kFwdW4 + (size_t)wg * kFwdX;
+  char* sH = sW4 + kFwdW4 + 2 * kFwdX + (size_t)wg * kFwdH;
   const int64_t my_n = n_tiles > blockIdx.x ? (n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  auto stage_x = [&](int64_t i) {
-    const int64_t m0 = (blockIdx.x + i * gridDim.x) * (int64_t)kGM;
-    stage_operand<kGM, false>(a.X, kInPad, a.n, kInPad, m0, 0, sX[i & 1]);
+  // this group's tiles: i = wg, wg + 2, ... of the CTA's
+  auto tile_row0 = [&](int64_t i) { return (blockIdx.x + i * gridDim.x) * (int64_t)kGM; };
+  auto stage_x = [&](int64_t i) {  // 128 threads of the group stage the tile's input rows
+    const int64_t m0 = tile_row0(i);
+    constexpr int kUnits = kGM * (kBK / 8);
+#pragma unroll 4
+    for (int u = gt; u < kUnits; u += 128) {
+      const int r = u / (kBK / 8), kc = u % (kBK / 8);
+      const int64_t gr = m0 + r;
+      cp16(sX + ((r / 8) * (kBK / 8) + kc) * 128 + (r % 8) * 16, a.X + gr * kInPad + kc * 8, gr < a.n);
+    }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
   if (tid == 0) {
-    nat::mbar_init(&bar, 1);
+    nat::mbar_init(&bars[0], 1);
+    nat::mbar_init(&bars[1], 1);
     nat::fence_mbar_init();
   }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(nat::smem_u32(&tmem_base)),
-                 "r"(128));
+                 "r"(256));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  if (my_n > 0) {  // weights (group 0 with tile 0's rows)
+  if (my_n > 0) {  // weights, then each group's first tile
     stage_operand<128, false>(a.Wb, kInPad, 128, kInPad, 0, 0, sW0);
     for (int q = 1; q <= 3; ++q)
       for (int c = 0; c < 2; ++c)
@@ -934,21 +953,24 @@ __global__ void __launch_bounds__(kGT, 1) nf_forward_fused_kernel(FwdArgs a, int
     for (int c = 0; c < 2; ++c)
       stage_operand<16, false>(a.Wb + (size_t)kNHidden * kHidden * kHidden, kHidden, 16, kHidden, 0, c * kBK,
                                sW4 + c * (kFwdW4 / 2));
-    stage_x(0);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    if (wg < my_n) stage_x(wg);
   }
   for (int q = 0; q < kNLayers; ++q)
     for (int c = tid; c < kHidden; c += kGT) bias_s[q][c] = c < a.n_bias[q] ? a.bias[q][c] : 0.f;
+  asm volatile("cp.async.wait_all;" ::: "memory");
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
-  const uint32_t tmem = tmem_base;
+  const uint32_t tmem = tmem_base + (uint32_t)wg * 128;
+  uint64_t* bar = &bars[wg];
   uint32_t phase = 0;
-  // one layer product: acc = A [128 x K] * W^T, K in chunks of 64 (A and W K-major core layout)
+  // one layer product of this group: acc = A [128 x K] * W^T (K-major core layout, chunks of 64)
   auto mma = [&](const char* A, uint32_t a_chunk, const char* W, uint32_t w_chunk, int nchunk, int N) {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;");
-    __syncthreads();
-    if (tid == 0) {
+    wg_sync(wg);
+    if (gt == 0) {
       asm volatile("tcgen05.fence::after_thread_sync;");
       const uint32_t a0 = nat::smem_u32(A), w0 = nat::smem_u32(W);
       const uint32_t idesc = N == 128 ? idesc_bf16(kGM, 128, false, false) : idesc_bf16(kGM, 16, false, false);
@@ -957,31 +979,24 @@ __global__ void __launch_bounds__(kGT, 1) nf_forward_fused_kernel(FwdArgs a, int
         for (int kk = 0; kk < kBK / 16; ++kk)
           mma_bf16(tmem, sdesc(a0 + c * a_chunk + kk * 256, 128, (kBK / 8) * 128),
                    sdesc(w0 + c * w_chunk + kk * 256, 128, (kBK / 8) * 128), idesc, (c > 0 || kk > 0) ? 1u : 0u);
-      mma_commit(&bar);
+      mma_commit(bar);
     }
-    nat::mbar_wait(&bar, phase);
+    nat::mbar_wait(bar, phase);
     phase ^= 1u;
     asm volatile("tcgen05.fence::after_thread_sync;");
   };
-  for (int64_t i = 0; i < my_n; ++i) {
-    const int64_t m0 = (blockIdx.x + i * gridDim.x) * (int64_t)kGM;
-    if (i + 1 < my_n) {
-      stage_x(i + 1);  // the other buffer: tile i-1's first product read it long ago
-      asm volatile("cp.async.wait_group 1;" ::: "memory");
-    } else {
-      asm volatile("cp.async.wait_group 0;" ::: "memory");
-    }
-    const int64_t m = m0 + wq * 32 + lane;
+  for (int64_t i = wg; i < my_n; i += 2) {
+    const int64_t m = tile_row0(i) + wq * 32 + lane;
     const bool row_ok = m < a.n;
+    asm volatile("cp.async.wait_all;" ::: "memory");  // this tile's input rows
     for (int q = 0; q < kNLayers; ++q) {
-      if (q == 0) mma(sX[i & 1], kFwdX, sW0, kFwdW0, 1, 128);
-      else if (q < kNHidden) mma(sH[(q - 1) & 1], kFwdH / 2, sWh + (size_t)(q - 1) * kFwdWh, kFwdWh / 2, 2, 128);
-      else mma(sH[(q - 1) & 1], kFwdH / 2, sW4, kFwdW4 / 2, 2, 16);
-      if (q < kNHidden) {
-        // warp (wq, ch): rows 32 wq + lane, columns [64 ch, 64 ch + 64)
-        char* dst = sH[q & 1];
+      if (q == 0) mma(sX, kFwdX, sW0, kFwdW0, 1, 128);
+      else if (q < kNHidden) mma(sH, kFwdH / 2, sWh + (size_t)(q - 1) * kFwdWh, kFwdWh / 2, 2, 128);
+      else mma(sH, kFwdH / 2, sW4, kFwdW4 / 2, 2, 16);
+      if (q == 0 && i + 2 < my_n) stage_x(i + 2);  // the input buffer is free once product 0 is done
+      if (q < kNHidden) {  // warp wq: rows 32 wq + lane, all 128 columns
 #pragma unroll 1
-        for (int n0 = ch * 64; n0 < ch * 64 + 64; n0 += 32) {
+        for (int n0 = 0; n0 < kHidden; n0 += 32) {
           uint32_t v[32];
           tmem_ld32(tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)n0, v);
           float f[32];
@@ -994,14 +1009,13 @@ __global__ void __launch_bounds__(kGT, 1) nf_forward_fused_kernel(FwdArgs a, int
 #pragma unroll
             for (int e = 0; e < 4; ++e) ob[e] = __floats2bfloat162_rn(f[8 * u + 2 * e], f[8 * u + 2 * e + 1]);
             if (row_ok) *reinterpret_cast<uint4*>(a.H[q] + m * kHidden + n0 + 8 * u) = o;
-            // next layer's A operand: row r = 32 wq + lane, K unit kc = (n0 + 8u) / 8 (chunk of 64)
+            // next product's A operand, in place: row r = 32 wq + lane, K unit (n0 + 8u) / 8
             const int r = wq * 32 + lane, kunit = (n0 + 8 * u) / 8;
-            const int chunk = kunit / 8, kc = kunit % 8;
-            *reinterpret_cast<uint4*>(dst + (size_t)chunk * (kFwdH / 2) + ((r / 8) * 8 + kc) * 128 + (r % 8) * 16) =
-                row_ok ? o : make_uint4(0, 0, 0, 0);
+            *reinterpret_cast<uint4*>(sH + (size_t)(kunit / 8) * (kFwdH / 2) + ((r / 8) * 8 + kunit % 8) * 128 +
+                                      (r % 8) * 16) = row_ok ? o : make_uint4(0, 0, 0, 0);
           }
         }
-      } else if (ch == 0) {  // output layer: 16 columns, fp32
+      } else {  // output layer: 16 columns, fp32
         uint32_t v[16];
         tmem_ld16(tmem + ((uint32_t)(wq * 32) << 16), v);
         if (row_ok) {
@@ -1017,7 +1031,7 @@ __global__ void __launch_bounds__(kGT, 1) nf_forward_fused_kernel(FwdArgs a, int
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(128));
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(256));
 }
 
 cudaError_t launch_forward_fused(const FwdArgs& fa, cudaStream_t s) {
