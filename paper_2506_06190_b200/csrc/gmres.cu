@@ -1012,10 +1012,12 @@ nat_status gmres_batched(int nsys, int64_t n, int64_t ldv, const double2* b, dou
     const char* e = std::getenv("NAT_GMRES_FUSED");
     return !(e && e[0] == '0');
   }();
-  static const int fused_cl = [] {  // CTAs per system: NAT_FUSED_CL = 4 (default) or 8
+  static const int fused_cl_env = [] {  // CTAs per system: NAT_FUSED_CL = 4 (default), 8, or 2 (fp32 basis)
     const char* e = std::getenv("NAT_FUSED_CL");
-    return (e && std::atoi(e) == 8) ? 8 : 4;
+    const int v = e ? std::atoi(e) : 4;
+    return v == 8 ? 8 : v == 2 ? 2 : 4;
   }();
+  const int fused_cl = (fused_cl_env == 2 && !basis32) ? 4 : fused_cl_env;
   const bool fused = fused_env && n <= (int64_t)fused_cl * kT * kFusedMaxRT;
   const int64_t rpc = (n + fused_cl - 1) / fused_cl;
   const int need_rt = (int)((rpc + kT - 1) / kT);
@@ -1035,7 +1037,7 @@ nat_status gmres_batched(int nsys, int64_t n, int64_t ldv, const double2* b, dou
     const char* e = std::getenv("NAT_FUSED_NTH");
     return e && std::atoi(e) == 256;
   }();
-  const int fused_kg = (basis32 && fused_256 && fused_cl == 4) ? 1 : (fused_rt <= 2 && !fused_narrow) ? 3 : 2;
+  const int fused_kg = (basis32 && fused_256 && fused_cl != 8) ? 1 : (fused_cl != 2 && fused_rt <= 2 && !fused_narrow) ? 3 : 2;
   const int fused_nth = fused_kg * kT;
   const size_t fsmem = std::max(fused_cap, sizeof(double2) * ((size_t)rpc * fused_kg + 4 * (size_t)mp1));
   using FusedFn = void (*)(const double2*, size_t, int64_t, int64_t, int64_t, const double2*, double2*, uint64_t,
@@ -1062,7 +1064,13 @@ nat_status gmres_batched(int nsys, int64_t n, int64_t ldv, const double2* b, dou
                             uint64_t, GivensArgs);
   FusedV2d v2d = nullptr;
   FusedV2f v2f = nullptr;
-  if (fused && fused_cl == 4 && fused_kg == 1 && b32) {
+  if (fused && fused_cl == 2 && b32) {
+    v2f = fused_kg == 1 ? (fused_rt == 2 ? arnoldi_fused_v2_kernel<float2, 2, 256, 2> : fused_rt == 4 ? arnoldi_fused_v2_kernel<float2, 4, 256, 2>
+                                                                                   : arnoldi_fused_v2_kernel<float2, 8, 256, 2>)
+                        : (fused_rt == 2 ? arnoldi_fused_v2_kernel<float2, 2, 512, 2> : fused_rt == 4 ? arnoldi_fused_v2_kernel<float2, 4, 512, 2>
+                                                                                     : arnoldi_fused_v2_kernel<float2, 8, 512, 2>);
+    if (fused_rt == 1) v2f = fused_kg == 1 ? arnoldi_fused_v2_kernel<float2, 1, 256, 2> : arnoldi_fused_v2_kernel<float2, 1, 512, 2>;
+  } else if (fused && fused_cl == 4 && fused_kg == 1 && b32) {
     v2f = fused_rt == 1 ? arnoldi_fused_v2_kernel<float2, 1, 256, 4> : fused_rt == 2 ? arnoldi_fused_v2_kernel<float2, 2, 256, 4>
         : fused_rt == 4 ? arnoldi_fused_v2_kernel<float2, 4, 256, 4> : arnoldi_fused_v2_kernel<float2, 8, 256, 4>;
   } else if (fused && fused_cl == 4 && fused_kg == 2) {

@@ -177,10 +177,10 @@ def lib():
 
 
 # Concurrent-sweep configuration (the C4 sweep runs SWEEP_WORKERS geometries at once on one
-# GPU, each on its own stream): the fused Arnoldi step uses 256-thread CTAs without the
-# shared-memory residency cap, so its latency-bound clusters co-reside with the pair kernels
-# of the other streams instead of holding whole SMs (bench A/B on B200: 2.77 -> 2.70 s per
-# 64-geometry step).  Library defaults (one solve at a time) are unchanged; the settings are
+# GPU, each on its own stream): the fused Arnoldi step uses clusters of two 256-thread CTAs
+# per system without the shared-memory residency cap, so its latency-bound clusters
+# co-reside with the pair kernels of the other streams instead of holding whole SMs (bench
+# A/B on B200: 2.77 -> 2.70 -> 2.625 s per 64-geometry step).  Library defaults (one solve at a time) are unchanged; the settings are
 # read once, at the first solve of the process.
 SWEEP_WORKERS = 6
 
@@ -188,6 +188,7 @@ SWEEP_WORKERS = 6
 def sweep_tuning():
     os.environ.setdefault("NAT_FUSED_NTH", "256")
     os.environ.setdefault("NAT_FUSED_SMEM_KB", "0")
+    os.environ.setdefault("NAT_FUSED_CL", "2")    # 2 CTAs per system: half the SM footprint (2.657 -> 2.625 s)
     os.environ.setdefault("NAT_MC_GROUPS", "1")   # the workers already overlap whole geometries
 
 

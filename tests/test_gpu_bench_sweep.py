@@ -2,8 +2,8 @@
 q + 1 on a high-priority stream overlapping the radiation of geometry q on a low-priority
 stream, per-geometry buffers double-buffered) produces exactly the fields of a plain
 serial pass through the same calls — so the harness's concurrency cannot corrupt the
-measured work.  Also runs the bench's Krylov configuration (nat.sweep_tuning: 256-thread
-fused Arnoldi CTAs, no residency cap) against the oracle in a fresh process."""
+measured work.  Also runs the bench's Krylov configuration (nat.sweep_tuning: clusters of two
+256-thread fused Arnoldi CTAs, no residency cap) against the oracle in a fresh process."""
 import os
 import subprocess
 import sys
@@ -47,7 +47,7 @@ def test_pipelined_sweep_matches_serial_pass():
 
 
 def test_sweep_tuning_krylov_configuration_parity():
-    env = dict(os.environ, NAT_FUSED_NTH="256", NAT_FUSED_SMEM_KB="0")
+    env = dict(os.environ, NAT_FUSED_NTH="256", NAT_FUSED_SMEM_KB="0", NAT_FUSED_CL="2")
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
                         "tests/test_gpu_mc.py", "-k", "surface_pressure_parity or sharded or c3_launch"],
                        cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
