@@ -176,7 +176,8 @@ class Worker:
 
     def __init__(self, nat, torch, n_vert, n_tri, e2e_out):
         dev = torch.device("cuda")
-        self.stream = torch.cuda.Stream(priority=-5)   # clamped to the device's highest priority
+        prio = os.environ.get("NAT_BENCH_PRIO", "1") != "0"   # A/B: equal priorities
+        self.stream = torch.cuda.Stream(priority=-5 if prio else 0)   # clamped to the device's highest priority
         self.rad_stream = torch.cuda.Stream(priority=0)
         self.copy_stream = torch.cuda.Stream()
         self.mc_plan = nat.McPlan(M_C4, N_K, "fp32", 200, dev)
