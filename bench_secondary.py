@@ -365,6 +365,7 @@ def run_c2(nat, torch, rank, world, comm, steps, barrier, allreduce_max_sum):
 
 def run_c3(nat, torch, rank, world, steps, barrier, allreduce_max_sum):
     import nat_inputs as I
+    nat.single_call_tuning()   # one large solve at a time: the wide fused step, two solve groups
     m = I.bowl()
     mesh = nat.Mesh.from_numpy(m.v, m.t)
     ks_all = list(I.c3_wavenumbers())

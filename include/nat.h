@@ -332,6 +332,14 @@ size_t nat_mc_workspace(nat_prec prec, int64_t M, int n_sys, int max_iter);
  * compare group counts 1, 2, 4).  nat_mc_workspace covers every group count.  groups in
  * [1, 4], else NAT_ERR_INVALID_ARG. */
 nat_status nat_mc_set_groups(int groups);
+/* Shape of the fused Arnoldi step of the batched GMRES (a7; process-wide, applies to the
+ * solves that start afterwards): cluster_ctas CTAs per system (2, 4, 8; 2 only with the
+ * fp32 basis, else 4), threads per CTA (256 — fp32 basis only —, 512, 768) and the
+ * shared-memory residency cap in KB (0 = none; default 120 = one CTA per SM).  Defaults:
+ * NAT_FUSED_CL / NAT_FUSED_NTH / NAT_FUSED_SMEM_KB, else (4, 512, 120).  The narrow shapes
+ * let the step's clusters co-reside with other streams' kernels (the C4 sweep); the wide
+ * default is fastest for one solve alone.  Invalid values: NAT_ERR_INVALID_ARG.        */
+nat_status nat_krylov_config(int cluster_ctas, int threads, int smem_cap_kb);
 nat_status nat_mc_surface_pressure(const nat_mesh* mesh, const nat_geom* geom, int n_sys,
                                    const double* k /* [host] */, const void* g_tri, const nat_mc_opts* opts,
                                    nat_prec prec, double tol, int max_iter, double* samples_out,

@@ -7,6 +7,7 @@
 // identical on every rank and for every GPU count.  The Givens update, the convergence
 // test and the back-substitution run on the device (one thread per system), so the host
 // never stalls the GPU between iterations (krylov.cuh).
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -460,6 +461,31 @@ __global__ void combine_kernel(const double2* __restrict__ V, const double2* __r
 // ------------------------------------------------------------------------------------
 constexpr int kFusedMaxRT = 8;                 // rows per thread (n <= CL x 256 x 8)
 constexpr int kFusedSmem = 120 * 1024;         // residency cap (1 CTA / SM)
+
+// Shape of the fused Arnoldi step, process-wide: nat_krylov_config() sets it at run time;
+// until then the NAT_FUSED_CL / NAT_FUSED_NTH / NAT_FUSED_SMEM_KB / NAT_FUSED_NARROW
+// environment variables (A/B runs) or the defaults (4 CTAs, 512 threads, 120 KB) apply.
+struct KrylovConfig {
+  int cl, nth, smem_kb;
+};
+std::atomic<int> g_kcfg_cl{0}, g_kcfg_nth{0}, g_kcfg_smem{-1};
+KrylovConfig krylov_config() {
+  if (g_kcfg_cl.load() == 0) {
+    const char* e = std::getenv("NAT_FUSED_CL");
+    const int cl = e ? std::atoi(e) : 4;
+    const char* t = std::getenv("NAT_FUSED_NTH");
+    const char* nw = std::getenv("NAT_FUSED_NARROW");
+    const int nth = (t && std::atoi(t) == 256) ? 256 : (nw && nw[0] == '0') ? 768 : 512;
+    const char* sm = std::getenv("NAT_FUSED_SMEM_KB");
+    int expected = -1;
+    g_kcfg_smem.compare_exchange_strong(expected, sm ? std::max(0, std::atoi(sm)) : kFusedSmem / 1024);
+    int z = 0;
+    g_kcfg_nth.compare_exchange_strong(z, nth);
+    z = 0;
+    g_kcfg_cl.compare_exchange_strong(z, cl == 8 ? 8 : cl == 2 ? 2 : 4);
+  }
+  return KrylovConfig{g_kcfg_cl.load(), g_kcfg_nth.load(), g_kcfg_smem.load()};
+}
 
 // Threads: NTH = KG x 256.  Dots: NTH / 32 warps, each two basis vectors at a time (16
 // loads of 16 B in flight per lane).  Update: group g (256 threads, RT rows each) sums the
@@ -1012,39 +1038,29 @@ nat_status gmres_batched(int nsys, int64_t n, int64_t ldv, const double2* b, dou
     const char* e = std::getenv("NAT_GMRES_FUSED");
     return !(e && e[0] == '0');
   }();
-  static const int fused_cl_env = [] {  // CTAs per system: NAT_FUSED_CL = 4 (default), 8, or 2 (fp32 basis)
-    const char* e = std::getenv("NAT_FUSED_CL");
-    const int v = e ? std::atoi(e) : 4;
-    return v == 8 ? 8 : v == 2 ? 2 : 4;
-  }();
-  const int fused_cl = (fused_cl_env == 2 && !basis32) ? 4 : fused_cl_env;
-  const bool fused = fused_env && n <= (int64_t)fused_cl * kT * kFusedMaxRT;
+  // fused-step shape (nat_krylov_config, else NAT_FUSED_CL / NAT_FUSED_NTH / NAT_FUSED_SMEM_KB):
+  // CTAs per system 4 (default), 8, or 2 (fp32 basis); 512 threads (2 update groups, leaving
+  // registers for pair-kernel CTAs of other streams) or 256 (fp32 basis); the shared-memory
+  // residency cap (default 120 KB: one CTA per SM keeps the clusters' basis slices in L2)
+  const KrylovConfig kc = krylov_config();
+  const int fused_cl = (kc.cl == 2 && !basis32) ? 4 : kc.cl;
   const int64_t rpc = (n + fused_cl - 1) / fused_cl;
+  const bool fused = fused_env && n <= (int64_t)fused_cl * kT * kFusedMaxRT;
   const int need_rt = (int)((rpc + kT - 1) / kT);
   const int fused_rt = need_rt <= 1 ? 1 : need_rt <= 2 ? 2 : need_rt <= 4 ? 4 : 8;
-  static const size_t fused_cap = [] {  // NAT_FUSED_SMEM_KB: residency cap (tuning A/B only)
-    const char* e = std::getenv("NAT_FUSED_SMEM_KB");
-    return e ? (size_t)std::atoi(e) * 1024 : (size_t)kFusedSmem;
-  }();
-  // 512 threads (2 update groups): leaves registers for pair-kernel CTAs of other streams on
-  // the same SM (C4 step -4 % with 4 worker streams); NAT_FUSED_NARROW=0: 768 threads for RT <= 2
-  static const bool fused_narrow = [] {
-    const char* e = std::getenv("NAT_FUSED_NARROW");
-    return !(e && e[0] == '0');
-  }();
-  // NAT_FUSED_NTH=256: one update group (the fp32-basis kernel), half the registers per CTA
-  static const bool fused_256 = [] {
-    const char* e = std::getenv("NAT_FUSED_NTH");
-    return e && std::atoi(e) == 256;
-  }();
+  const size_t fused_cap = (size_t)kc.smem_kb * 1024;
+  const bool fused_narrow = kc.nth != 768;
+  const bool fused_256 = kc.nth == 256;
   const int fused_kg = (basis32 && fused_256 && fused_cl != 8) ? 1 : (fused_cl != 2 && fused_rt <= 2 && !fused_narrow) ? 3 : 2;
   const int fused_nth = fused_kg * kT;
   const size_t fsmem = std::max(fused_cap, sizeof(double2) * ((size_t)rpc * fused_kg + 4 * (size_t)mp1));
   using FusedFn = void (*)(const double2*, size_t, int64_t, int64_t, int64_t, const double2*, double2*, uint64_t,
                            GivensArgs);
   FusedFn fused_fn = nullptr;
-  if (fused_cl == 8)
-    fused_fn = fused_rt == 1 ? arnoldi_fused_kernel<1, 768, 8> : fused_rt == 2 ? arnoldi_fused_kernel<2, 768, 8>
+  if (fused_cl == 8 && fused_kg == 3)
+    fused_fn = fused_rt == 1 ? arnoldi_fused_kernel<1, 768, 8> : arnoldi_fused_kernel<2, 768, 8>;
+  else if (fused_cl == 8)  // the kernel's thread count must match the launch (fused_nth)
+    fused_fn = fused_rt == 1 ? arnoldi_fused_kernel<1, 512, 8> : fused_rt == 2 ? arnoldi_fused_kernel<2, 512, 8>
              : fused_rt == 4 ? arnoldi_fused_kernel<4, 512, 8> : arnoldi_fused_kernel<8, 512, 8>;
   else if (fused_kg == 3)
     fused_fn = fused_rt == 1 ? arnoldi_fused_kernel<1, 768, 4> : fused_rt == 2 ? arnoldi_fused_kernel<2, 768, 4>
@@ -1428,4 +1444,16 @@ extern "C" nat_status nat_bem_mf_solve(nat_comm* comm, const nat_bem_mf* op, con
     info->t_total_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
   }
   return res[0].converged ? NAT_OK : NAT_WARN_NOT_CONVERGED;
+}
+
+extern "C" nat_status nat_krylov_config(int cluster_ctas, int threads, int smem_cap_kb) {
+  NAT_REQUIRE(cluster_ctas == 2 || cluster_ctas == 4 || cluster_ctas == 8, "cluster_ctas = %d must be 2, 4 or 8",
+              cluster_ctas);
+  NAT_REQUIRE(threads == 256 || threads == 512 || threads == 768, "threads = %d must be 256, 512 or 768", threads);
+  NAT_REQUIRE(smem_cap_kb >= 0 && smem_cap_kb <= 200, "smem_cap_kb = %d must be in [0, 200]", smem_cap_kb);
+  nat::krylov_config();  // settle the environment defaults first
+  nat::g_kcfg_cl.store(cluster_ctas);
+  nat::g_kcfg_nth.store(threads);
+  nat::g_kcfg_smem.store(smem_cap_kb);
+  return NAT_OK;
 }

@@ -116,6 +116,7 @@ _SIGS = {
     "nat_bem_solve": (C.c_int, [_P, C.c_int, _I64, _I64, _I64, _P, _I64, _P, _P, _D, C.c_int,
                                 _P, _SZ, C.POINTER(_SolveInfo), _P]),
     "nat_mc_set_groups": (C.c_int, [C.c_int]),
+    "nat_krylov_config": (C.c_int, [C.c_int, C.c_int, C.c_int]),
     "nat_mc_sample": (C.c_int, [C.POINTER(_Mesh), C.POINTER(_Geom), _I64, C.c_uint64,
                                 C.c_uint64, _P, _P, _P]),
     "nat_mc_op_workspace": (_SZ, [C.c_int, _I64, C.c_int]),
@@ -186,10 +187,15 @@ SWEEP_WORKERS = 6
 
 
 def sweep_tuning():
-    os.environ.setdefault("NAT_FUSED_NTH", "256")
-    os.environ.setdefault("NAT_FUSED_SMEM_KB", "0")
-    os.environ.setdefault("NAT_FUSED_CL", "2")    # 2 CTAs per system: half the SM footprint (2.657 -> 2.625 s)
-    os.environ.setdefault("NAT_MC_GROUPS", "1")   # the workers already overlap whole geometries
+    """The C4 sweep's configuration (many geometries in flight on one GPU)."""
+    nat_krylov_config(2, 256, 0)   # 2 x 256-thread CTAs per system, no cap (2.657 -> 2.625 s per step)
+    nat_mc_set_groups(1)           # the workers already overlap whole geometries
+
+
+def single_call_tuning():
+    """The library defaults for one large solve at a time (C3): wide fused step, two groups."""
+    nat_krylov_config(4, 512, 120)
+    nat_mc_set_groups(2)
 
 
 def exported_symbols():
@@ -837,6 +843,11 @@ def nat_bem_mf_solve(op: BemMf, b_local: torch.Tensor, comm: Optional["Comm"] = 
 # diagnostics: per-kernel CUDA-event timer (nat_kernel_timer_*)
 # ------------------------------------------------------------------------------------
 KTIMER_MC_OP, KTIMER_MC_RHS, KTIMER_RADIATE, KTIMER_FAR, KTIMER_NF_GEMM = 0, 1, 2, 3, 4
+
+
+def nat_krylov_config(cluster_ctas: int, threads: int, smem_cap_kb: int):
+    """Process-wide shape of the fused Arnoldi step (include/nat.h)."""
+    _check(lib().nat_krylov_config(int(cluster_ctas), int(threads), int(smem_cap_kb)))
 
 
 def nat_mc_set_groups(groups: int):

@@ -264,3 +264,30 @@ def test_solve_groups_agree():
         assert all(out[G][2])
     with pytest.raises(nat.NatError):
         nat.nat_mc_set_groups(5)
+
+
+def test_krylov_config_shapes_agree():
+    """nat_krylov_config: the fused Arnoldi step with 2 / 4 / 8 CTAs per system and 256 /
+    512 threads gives the same solution (summation order only) and iteration counts within
+    one; invalid shapes are rejected."""
+    nat = _nat()
+    m = I.bowl(32, 8, 2)
+    geo, mesh, gg = _case(m)
+    M, seed = 700, 3
+    ks = list(np.linspace(0.5, 6.0, 5))
+    g_tri = torch.from_numpy(I.neumann_harmonics(m, 5)).cuda()
+    out = {}
+    try:
+        for cfg in ((4, 512, 120), (2, 256, 0), (2, 512, 0), (4, 256, 0), (8, 512, 120)):
+            nat.nat_krylov_config(*cfg)
+            _, _, p, info = nat.nat_mc_surface_pressure(mesh, gg, ks, g_tri, M, seed, prec="fp32", tol=1e-6)
+            out[cfg] = (to_np(p), [i["iters"] for i in info])
+    finally:
+        nat.nat_krylov_config(4, 512, 120)
+    ref = out[(4, 512, 120)]
+    for cfg, (p, it) in out.items():
+        assert rel_l2(p, ref[0]) <= 1e-6, cfg
+        assert all(abs(a - b) <= 1 for a, b in zip(it, ref[1])), cfg
+    for bad in ((3, 512, 120), (4, 128, 120), (4, 512, -1)):
+        with pytest.raises(nat.NatError):
+            nat.nat_krylov_config(*bad)
