@@ -651,7 +651,13 @@ __global__ void __launch_bounds__(kThreads, kFarMinBlocks) far_kernel_x2(FarArgs
 // (d, r^2, rsqrt, r, d.n, the weights): per pair-evaluation x wavenumber 1/NK of the shared
 // work + kr, sincos and the V/K accumulation.  CTA = kTIM rows x 256 * kCC columns (the
 // column blocking of the one-wavenumber kernel, so the partial-sum layout is the same).
-constexpr int kTIM = 8;
+#ifndef NAT_FAR_TIM
+#define NAT_FAR_TIM 8
+#endif
+#ifndef NAT_FAR_MINB
+#define NAT_FAR_MINB 2
+#endif
+constexpr int kTIM = NAT_FAR_TIM;  // rows per CTA (compile-time variants: scripts/build_variants.sh)
 constexpr int kMaxK = 4;
 struct FarMultiArgs {
   FarArgs<float> b;          // n, row_begin, rows, lda, cols, cen, centre, g (one RHS), rhs0 = 0
@@ -661,7 +667,7 @@ struct FarMultiArgs {
 };
 
 template <int NQ, int NK>
-__global__ void __launch_bounds__(kThreads, 2) far_kernel_multi(FarMultiArgs m) {
+__global__ void __launch_bounds__(kThreads, NAT_FAR_MINB) far_kernel_multi(FarMultiArgs m) {
   constexpr int TP = kTIM / 2;
   const FarArgs<float>& a = m.b;
   __shared__ __align__(16) f2r s_c[3][TP];
