@@ -808,7 +808,15 @@ struct NfWs {
   int64_t splits, tiles, lblocks;
 };
 
-constexpr int64_t kSplitRows = 1024;  // batch rows per split-K CTA of the weight gradients
+// batch rows per split-K CTA of the weight gradients (NAT_NF_SPLIT_ROWS for A/B; default 1024)
+int64_t split_rows() {
+  static const int64_t v = [] {
+    const char* e = std::getenv("NAT_NF_SPLIT_ROWS");
+    const int64_t r = e ? std::atoll(e) : 1024;
+    return r >= 128 && r % 64 == 0 ? r : (int64_t)1024;
+  }();
+  return v;
+}
 constexpr int kTallRows = 64;         // first-level rows of the tall column-sum reductions
 
 // column sums of part[nparts][cols] (cols <= 128) -> out (fixed order, two levels)
@@ -831,7 +839,7 @@ size_t nf_carve(nat::Carver& c, NfWs* w, int64_t n, int64_t n_params) {
   t.dX = c.take<float>((size_t)n * kInPad);
   t.grad = c.take<float>((size_t)n_params);
   t.Wb = c.take<bf16>((size_t)kNLayers * kHidden * kHidden);
-  t.splits = (n + kSplitRows - 1) / kSplitRows;
+  t.splits = (n + split_rows() - 1) / split_rows();
   t.tiles = (n + kGM - 1) / kGM;
   t.lblocks = (n + kLossT - 1) / kLossT;
   t.wpart = c.take<float>((size_t)t.splits * kHidden * kHidden);
@@ -1185,7 +1193,7 @@ extern "C" nat_status nat_nf_train_step(const nat_nf_config* cfg, float* params,
     // dW_q = d^T h_in  (split-K over the batch): M = out (or in for the 16-wide last layer)
     GemmArgs gw{};
     gw.K = n;
-    gw.k_per_cta = kSplitRows;
+    gw.k_per_cta = split_rows();
     gw.epi = kEpiPartial;
     gw.C = w.wpart;
     if (q == kNHidden) {  // C[in][out_pad] = h_in^T d: A = h_in (MN-major), B = dY (MN-major)
