@@ -324,7 +324,7 @@ nat_status nat_mc_check_coincident(int64_t M, const double* samples, int64_t* pa
                                    void* ws, size_t ws_bytes, nat_stream_t stream); /* (sync) */
 
 size_t nat_mc_workspace(nat_prec prec, int64_t M, int n_sys, int max_iter);
-/* Solve groups of nat_mc_surface_pressure (process-wide; default NAT_MC_GROUPS or 1): the
+/* Solve groups of nat_mc_surface_pressure (process-wide; default NAT_MC_GROUPS or 2): the
  * systems of each batch of <= 64 are split into `groups` contiguous groups whose GMRES
  * iterations run concurrently on their own streams from persistent library threads, so one
  * group's Krylov steps overlap another's operator application.  Each system's iteration is

@@ -664,7 +664,7 @@ struct McWs {
   McGroupWs grp[kMaxGroups];
 };
 
-// Solve groups (NAT_MC_GROUPS or nat_mc_set_groups; default 1): the systems of a batch are
+// Solve groups (NAT_MC_GROUPS or nat_mc_set_groups; default 2): the systems of a batch are
 // split into G contiguous groups whose GMRES iterations run concurrently on G streams (one
 // host thread each), so one group's latency-bound Krylov kernels overlap another group's
 // operator application inside a single call.
@@ -673,7 +673,7 @@ int mc_groups() {
   int v = g_mc_groups.load();
   if (v <= 0) {
     const char* e = std::getenv("NAT_MC_GROUPS");
-    v = e ? std::max(1, std::min(kMaxGroups, std::atoi(e))) : 1;
+    v = e ? std::max(1, std::min(kMaxGroups, std::atoi(e))) : 2;
     g_mc_groups.store(v);
   }
   return v;

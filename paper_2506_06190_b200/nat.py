@@ -193,7 +193,7 @@ def sweep_tuning():
 
 
 def single_call_tuning():
-    """The library defaults for one large solve at a time (C3): wide fused step, two groups."""
+    """The library defaults, for one large solve at a time (C3): wide fused step, two groups."""
     nat_krylov_config(4, 512, 120)
     nat_mc_set_groups(2)
 
