@@ -465,6 +465,50 @@ def count_launches(sweep, torch, geo_ids):
         return None
 
 
+def mc_call_roofline(nat, torch, sweep, gi):
+    """The BEM-MC estimator as ONE call (nat_mc_surface_pressure of geometry gi alone on the
+    device, the library's single-call configuration): its binding roofline time (operator
+    and right-hand-side pair-evaluations at R(n), from the kernel timer's per-launch buckets)
+    over the call's device time (CUDA events, timer off).  In the sweep the same call overlaps
+    other geometries; this is the latency view the verdict asked for."""
+    h = sweep.host[gi]
+    mesh, g = sweep.dmesh[gi], sweep.dg[gi]
+    geo = nat.nat_mesh_prepare(mesh)
+    plan = nat.McPlan(M_C4, N_K, "fp32", 200, "cuda")
+    nat.single_call_tuning()
+    try:
+        def call():
+            return nat.nat_mc_surface_pressure(mesh, geo, h["ks"], g, M_C4, seed=20250606, stream_id=gi, prec="fp32",
+                                               tol=1e-6, plan=plan)
+        call()
+        torch.cuda.synchronize()
+        nat.nat_kernel_timer_enable(True)
+        call()
+        torch.cuda.synchronize()
+        t_roof = 0.0
+        for cat, kind in ((nat.KTIMER_MC_OP, 1), (nat.KTIMER_MC_RHS, 2)):
+            for n in range(1, 65):
+                _, pairs, nl = nat.nat_kernel_timer_read(cat, n)
+                if nl:
+                    t_roof += pairs * sm_clk_per_pair(kind, n) / (SM_COUNT * MAX_MHZ * 1e6)
+        nat.nat_kernel_timer_enable(False)
+        ms = []
+        for _ in range(3):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            _, _, _, infos = call()
+            e1.record()
+            torch.cuda.synchronize()
+            ms.append(e0.elapsed_time(e1))
+    finally:
+        nat.sweep_tuning()
+    t = min(ms) * 1e-3
+    return {"geometry": gi, "ms_per_call": 1e3 * t, "roofline_ms": 1e3 * t_roof, "frac": t_roof / t,
+            "iterations_max": max(i["iters"] for i in infos), "solve_groups": 2,
+            "note": "binding roofline of the call's pair work (operator + RHS at R(n)) / call time; the "
+                    "rest is the 84-200-step Krylov chain (fused CGS2 step, epilogue, Givens)"}
+
+
 def kernel_rooflines(nat, clk_mhz, traffic):
     """Per-category rooflines of the main pair kernels from the kernel timer's per-launch
     buckets (launches grouped by wavenumbers per pair): roofline time = pairs x binding
@@ -608,6 +652,7 @@ def main():
         roofline["share_of_serialised_step"] = roofline["seconds"] / (e0.elapsed_time(e1) * 1e-3)
         roofline["dominant"] = dom
 
+    mc_call = mc_call_roofline(nat, torch, sweep, sweep.geo_ids[0])
     n_launch = None if args.no_profile_count else count_launches(sweep, torch, sweep.geo_ids[:1])
 
     cpu = None
@@ -636,7 +681,7 @@ def main():
                            "max_true_rel_residual": tot["max_rel_residual"],
                            "note": "tol 1e-6, 200 iterations (P:372); a system at the cap returns its best iterate, "
                                    "flagged, with its true residual (S:276)"},
-        "roofline": roofline, "rooflines": roofs,
+        "roofline": roofline, "rooflines": roofs, "mc_call": mc_call,
         "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": (n_launch * len(sweep.geo_ids) * K) if n_launch else None,
         "gpu_launches_note": "libnat kernels of one geometry counted with torch.profiler (CUPTI) x geometries x steps",
