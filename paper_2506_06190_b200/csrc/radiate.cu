@@ -65,6 +65,7 @@ struct RadParams {
   int n_modes;
   float self_r2;        // SELF mode threshold (see radiate.cuh)
   const unsigned long long* skip;  // see RadInput::skip
+  int sub;              // fp32: CTAs per source tile (split s takes sources [s % sub] of tile s / sub)
 };
 
 // ------------------------------------------------------------------------------------
@@ -283,8 +284,11 @@ __global__ void __launch_bounds__(NT) radiate_f32x2_kernel(RadParams prm) {
       for (int m = 0; m < MB; ++m) ar[p][m] = ai[p][m] = br[p][m] = bi[p][m] = 0ull;
   };
 
-  const int t0 = split * prm.chunk_tiles;
+  // a split is chunk_tiles source tiles, or (sub > 1, one tile per split) a 1/sub part of one
+  const int sub = prm.sub;
+  const int t0 = (split / sub) * prm.chunk_tiles;
   const int t1 = min(t0 + prm.chunk_tiles, prm.n_tiles);
+  const int s_lo = (split % sub) * (kTile / sub), s_hi = s_lo + kTile / sub;
   const float* src = static_cast<const float*>(prm.rec) + (size_t)mch * prm.n_src_pad * NF;
   constexpr uint32_t kBytes = kTileFloats * sizeof(float);
 
@@ -310,7 +314,7 @@ __global__ void __launch_bounds__(NT) radiate_f32x2_kernel(RadParams prm) {
     // shared-memory loads of later sources overlap the arithmetic (ncu r01: LDS-wait)
     constexpr int kUnroll = (RP * MB <= 1) ? 4 : 2;
 #pragma unroll kUnroll
-    for (int s = 0; s < kTile; ++s) {
+    for (int s = s_lo; s < s_hi; ++s) {
       // one scalar per record field (LDS.128 broadcast), used as the .F32 operand of the
       // packed instructions (both targets of the pair share it)
       float fs[NF];
@@ -531,7 +535,7 @@ __global__ void mc_sources_kernel(int64_t M, const double* __restrict__ smp, dou
 // ------------------------------------------------------------------------------------
 struct Plan {
   int kind;  // record / kernel kind (fp32 only; see rec_geo)
-  int MB, R, NF, n_mchunk, tile, n_tiles, chunk_tiles, n_split;
+  int MB, R, NF, n_mchunk, tile, n_tiles, chunk_tiles, n_split, sub = 1;
   int64_t n_src_pad, tgt_tiles;
   size_t rec_elems, smem;
   bool fp64;
@@ -709,10 +713,21 @@ Plan make_plan(nat_prec prec, int64_t n_src, int n_modes, int64_t n_lis, int kin
     }
   }
   pl.n_split = (pl.n_tiles + pl.chunk_tiles - 1) / pl.chunk_tiles;
+  // MC operators whose grid leaves SMs idle (the compacted tail of a solve: few wavenumbers,
+  // one tile per CTA already): 2 or 4 CTAs per source tile (NAT_RAD_SUB=0 disables; A/B)
+  static const bool sub_on = [] {
+    const char* e = std::getenv("NAT_RAD_SUB");
+    return !(e && e[0] == '0');
+  }();
+  if (sub_on && !pl.fp64 && pl.kind != 0 && pl.chunk_tiles == 1) {
+    const int64_t ctas = pl.tgt_tiles * pl.n_mchunk * pl.n_split;
+    pl.sub = ctas >= 2 * (int64_t)n_sm ? 1 : ctas * 2 >= 2 * (int64_t)n_sm ? 2 : 4;
+    pl.n_split *= pl.sub;
+  }
   static const bool dbg = std::getenv("NAT_DEBUG_PLAN") != nullptr;
   if (dbg)
-    std::fprintf(stderr, "[plan] kind %d modes %d src %lld lis %lld: R %d NT %d MB %d chunk %d split %d tgt %lld occ %d smem %zu\n",
-                 pl.kind, n_modes, (long long)n_src, (long long)n_lis, pl.R, pl.NT, pl.MB, pl.chunk_tiles, pl.n_split,
+    std::fprintf(stderr, "[plan] kind %d modes %d src %lld lis %lld: R %d NT %d MB %d chunk %d split %d (sub %d) tgt %lld occ %d smem %zu\n",
+                 pl.kind, n_modes, (long long)n_src, (long long)n_lis, pl.R, pl.NT, pl.MB, pl.chunk_tiles, pl.n_split, pl.sub,
                  (long long)pl.tgt_tiles, occupancy(pl.fp64, pl.kind, pl.R, pl.MB, pl.NT, pl.smem), pl.smem);
   pl.rec_elems = (size_t)pl.n_mchunk * pl.n_src_pad * pl.NF;
   return pl;
@@ -828,6 +843,7 @@ nat_status radiate_internal(const RadInput& in, nat_prec prec, const double* k, 
     prm.n_modes = nm;
     prm.self_r2 = in.self_r2;
     prm.skip = in.skip;
+    prm.sub = pl.fp64 ? 1 : pl.sub;
     cudaError_t e = cudaSuccess;
     const int tcat = kind == 0 ? kTimerRadiate : kind == 1 ? kTimerMcOp : kTimerMcRhs;
     const bool timed = ktimer_on();
