@@ -312,7 +312,10 @@ __global__ void __launch_bounds__(NT) radiate_f32x2_kernel(RadParams prm) {
 
     // short bodies (one target pair, one wavenumber) need a deeper unroll so the
     // shared-memory loads of later sources overlap the arithmetic (ncu r01: LDS-wait)
-    constexpr int kUnroll = (RP * MB <= 1) ? 4 : 2;
+#ifndef NAT_RAD_UNROLL
+#define NAT_RAD_UNROLL 2
+#endif
+    constexpr int kUnroll = (RP * MB <= 1) ? 4 : NAT_RAD_UNROLL;
 #pragma unroll kUnroll
     for (int s = s_lo; s < s_hi; ++s) {
       // one scalar per record field (LDS.128 broadcast), used as the .F32 operand of the
