@@ -573,6 +573,11 @@ int occ_of(size_t smem) {
 
 template <int R, int KIND, int NT>
 int occ_mb(int MB, size_t smem) {
+  if constexpr (KIND == 1) {  // the MC operator also has balanced chunks of 5-7 wavenumbers
+    if (MB == 5) return occ_of<R, 5, KIND, NT>(smem);
+    if (MB == 6) return occ_of<R, 6, KIND, NT>(smem);
+    if (MB == 7) return occ_of<R, 7, KIND, NT>(smem);
+  }
   return MB == 1 ? occ_of<R, 1, KIND, NT>(smem) : MB == 2 ? occ_of<R, 2, KIND, NT>(smem)
        : MB == 3 ? occ_of<R, 3, KIND, NT>(smem) : MB == 4 ? occ_of<R, 4, KIND, NT>(smem)
        : occ_of<R, 8, KIND, NT>(smem);
@@ -615,6 +620,18 @@ Plan make_plan(nat_prec prec, int64_t n_src, int n_modes, int64_t n_lis, int kin
     pl.tile = kTile64;
   } else {
     pl.MB = pick_mb(n_modes);
+    // MC operator (the compacted tail launches any n): the same chunk count with balanced
+    // chunks, ceil(n / ceil(n / 8)) wavenumbers each, so the last chunk carries no padding
+    // (n = 41: 6 x 7 slots instead of 6 x 8); NAT_MB_BALANCE=0 disables (A/B)
+    static const bool balance = [] {
+      const char* e = std::getenv("NAT_MB_BALANCE");
+      return !(e && e[0] == '0');
+    }();
+    if (balance && kind == 1 && pl.MB == 8) {
+      const int chunks = (n_modes + 7) / 8;
+      pl.MB = (n_modes + chunks - 1) / chunks;
+      if (pl.MB < 5) pl.MB = 8;  // (never: n >= 8 gives 5..8)
+    }
     pl.R = 4;
     pl.NF = rec_nf(pl.kind, pl.MB);  // records of the FP32x2 kernel (scalars, broadcast operands)
     pl.tile = kTile;
@@ -759,8 +776,12 @@ cudaError_t launch_f32_r(const Plan& pl, const RadParams& prm, cudaStream_t s) {
     case 2: return launch_f32<R, 2, KIND, NT>(pl, prm, s);
     case 3: return launch_f32<R, 3, KIND, NT>(pl, prm, s);
     case 4: return launch_f32<R, 4, KIND, NT>(pl, prm, s);
-    default: return launch_f32<R, 8, KIND, NT>(pl, prm, s);
+    case 5: if constexpr (KIND == 1) return launch_f32<R, 5, KIND, NT>(pl, prm, s); else break;
+    case 6: if constexpr (KIND == 1) return launch_f32<R, 6, KIND, NT>(pl, prm, s); else break;
+    case 7: if constexpr (KIND == 1) return launch_f32<R, 7, KIND, NT>(pl, prm, s); else break;
+    default: break;
   }
+  return launch_f32<R, 8, KIND, NT>(pl, prm, s);
 }
 
 template <int KIND>
