@@ -5,7 +5,7 @@ SMI=$!
 NAT_BENCH_VERBOSE=1 timeout 1500 python bench.py --steps 5 --warmup 3 > gpurun_out/r02_bench.json 2> gpurun_out/r02_bench.err; echo "bench rc=$?"
 kill $SMI
 rm -f gpurun_out/r02_tail_rows.md
-for spec in "radiate_f32x2_kernel<.int.2, .int.4, .int.1:0" "radiate_f32x2_kernel<.int.2, .int.2, .int.1:0" "radiate_f32x2_kernel<.int.2, .int.1, .int.1:0"; do
+for spec in "radiate_f32x2_kernel<.int.2, .int.4, .int.1:0" "radiate_f32x2_kernel<.int.2, .int.1, .int.1:0"; do
   k="${spec%%:*}"; sk="${spec##*:}"
   timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:$k" -s $sk -c 1 -o /tmp/r02_tail python scripts/prof_c4.py 0 1 > /dev/null 2>&1; echo "ncu $k rc=$?"
   python scripts/ncu_rows.py /tmp/r02_tail.ncu-rep "C4 MC operator tail launch" >> gpurun_out/r02_tail_rows.md
